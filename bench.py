@@ -1,0 +1,368 @@
+"""Benchmark of the particle-PHD filter hot path (BASELINE.json metric:
+"particle-measurement update pairs/sec and filter step ms at 1/2/4/8 B200").
+
+Workload (N=1 and every N): config 5 "exchange stress" -- 2^24 particles
+(16,711,680 survivors + 65,536 births), 4096 measurements per step, position
+sensor; strong scaling over 1/2/4/8 GPUs.  One "step" = the
+whole hot path (predict + births, two-pass update with its all-reduces, STPHD
+extraction on rank 0, systematic resampling + exchange) via phd_step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  value = sum over timed steps of N*M pairs /
+device time (CUDA events on the filter stream, barrier + synchronize on both
+sides, max over ranks).  The particle state (335 MB) exceeds the 126 MB L2,
+so no explicit flush is needed between steps.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Per-pair algorithmic work of the two-pass update:
+# position: pass 1 = 6 FP32 + 1 EX2, pass 2 = 11 FP32 + 1 EX2; range-bearing +1 FP32 per pass.
+ALGO = {0: {"pass1": (6, 1), "pass2": (11, 1)}, 1: {"pass1": (7, 1), "pass2": (12, 1)}}
+FP32_PER_CLK_SM = 128.0   # measured: profiles/r01_pipes_microbench.jsonl (FFMA / FFMA2 lanes)
+EX2_PER_CLK_SM = 16.0     # measured: MUFU.EX2
+SM_MAX_MHZ = 1965.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=65536, help="particles in the oracle's bounded sample")
+    return ap.parse_args()
+
+
+def roofline_pairs_per_s(meas, which, n_sm, mhz):
+    fp, ex = ALGO[1 if meas == 1 else 0][which] if which != "update" else (
+        sum(ALGO[1 if meas == 1 else 0][p][0] for p in ("pass1", "pass2")),
+        sum(ALGO[1 if meas == 1 else 0][p][1] for p in ("pass1", "pass2")))
+    per_clk = min(FP32_PER_CLK_SM / fp, EX2_PER_CLK_SM / ex)
+    return per_clk * n_sm * mhz * 1e6
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, devices):
+        self.devices = devices
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", ",".join(str(d) for d in self.devices)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if r[5 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def scenario_for(name, steps):
+    import scenario
+    from dataclasses import replace
+    cfg = scenario.get(name)
+    if cfg.scenario.steps < steps:
+        cfg = replace(cfg, scenario=replace(cfg.scenario, steps=steps))
+    return cfg
+
+
+def cpu_oracle_sample(cfg, Z, soa, w, n_sample, k=1):
+    """The oracle, as it stands, on a bounded sample: one full serial step
+    (predict, births, normalisers, update, extraction, resampling) of the
+    first n_sample particles against the full measurement set Z_k."""
+    import numpy as np
+    import oracle
+    m = cfg.model
+    n = min(n_sample, soa.shape[1])
+    sub = np.ascontiguousarray(soa[:, :n])
+    ws = np.ascontiguousarray(w[:n])
+    J = max(1, int(round(m.births_per_step * n / max(1, soa.shape[1]))))
+    from dataclasses import replace
+    ms = replace(m, births_per_step=J)
+    z = Z[k - 1]
+    t0 = time.perf_counter()
+    r = oracle.step(ms, k, sub, ws, z, None, n, J)
+    dt = time.perf_counter() - t0
+    pairs = (n + J) * len(z)
+    return {"pairs": pairs, "seconds": dt, "n": n + J, "M": len(z)}
+
+
+def run_reference(args):
+    import numpy as np
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    steps = args.warmup + args.steps
+    cfg = scenario_for(args.config, steps)
+    import scenario
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    n_s = 16384
+    times, pairs = [], []
+    for s in range(steps):
+        r = cpu_oracle_sample(cfg, Z, soa, w, n_s, k=s + 1)
+        if s >= args.warmup:
+            times.append(r["seconds"])
+            pairs.append(r["pairs"])
+    T = sum(times)
+    val = sum(pairs) / T
+    sample = ("one full serial step (predict, births, normalisers, update, extraction, resampling) of the "
+              "first %d particles (+ proportional births) against all M=%d measurements of Z_k, per step" %
+              (n_s, len(Z[0])))
+    out = {"impl": "reference", "metric": "particle-measurement update pairs/sec and filter step ms",
+           "value": val, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * T / len(times), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg.name, "N": int(soa.shape[1] + cfg.model.births_per_step),
+                      "M": len(Z[0]), "sample_particles": n_s},
+           "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1503_03769_b200 as phd
+    import scenario
+    phd.load(build_if_missing=(rank == 0 and world == 1))
+
+    steps = args.warmup + args.steps
+    cfg = scenario_for(args.config, 2 * steps + 1)
+    m = cfg.model
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    n0 = soa.shape[1]
+    J = m.births_per_step
+    lo, hi = phd.rank_block(n0 + J, world, rank)
+    a, b = min(lo, n0), min(hi, n0)
+    nid = None
+    if world > 1:
+        obj = [phd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    stream = torch.cuda.current_stream(dev)
+    ws_bytes = phd.workspace_size(m, world)
+    workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)  # device memory from torch
+    f = phd.Filter(m, rank=rank, world=world, nccl_id=nid, device=local, stream=stream.cuda_stream,
+                   workspace=workspace)
+
+    def reset():
+        f.set_particles(np.ascontiguousarray(soa[:, a:b]), np.ascontiguousarray(w[a:b]), n0)
+
+    # device-resident measurement sets (value) and pinned host copies (e2e)
+    Zd = [torch.from_numpy(z).to(dev) for z in Z]
+    Zh = [torch.from_numpy(z).pin_memory() for z in Z]
+
+    def run_steps(kfirst, count, zs, timed):
+        pairs = 0
+        N_glob = n0 + J
+        for i in range(count):
+            k = kfirst + i
+            z = zs[k - 1]
+            M = int(z.shape[0])
+            f.step_raw(k, z.data_ptr(), M)
+            s = f._sum
+            pairs += int(s.N) * M
+        return pairs
+
+    def timed_region(zs, kfirst):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        l0 = f.launch_count()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t0 = time.perf_counter()
+        pairs = run_steps(kfirst, args.steps, zs, True)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        launches = f.launch_count() - l0
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return pairs, ms, launches, wall
+
+    # ---- device-resident run (value) ----
+    reset()
+    run_steps(1, args.warmup, Zd, False)
+    f.set_timing(True)
+    clocks = ClockSampler([local]) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    # per-kernel events: collect per-step pass timings
+    pass_ms = {"pass1": [], "pass2": [], "update": [], "predict": [], "resample": [], "exchange": []}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = f.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    pairs = 0
+    for i in range(args.steps):
+        k = args.warmup + 1 + i
+        z = Zd[k - 1]
+        f.step_raw(k, z.data_ptr(), int(z.shape[0]))
+        pairs += int(f._sum.N) * int(z.shape[0])
+        t = f.timing()
+        for key in pass_ms:
+            pass_ms[key].append(t[key])
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = f.launch_count() - l0
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    clk = clocks.stop() if clocks else None
+    f.set_timing(False)
+    N_glob = n0 + J
+    M = int(Z[0].shape[0])
+
+    # ---- e2e: host measurement buffers, copies inside the timed region ----
+    reset()
+    run_steps(1, args.warmup, Zh, False)
+    pairs_e, ms_e, _, _ = timed_region(Zh, args.warmup + 1)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    value = pairs / (ms * 1e-3)
+    value_e = pairs_e / (ms_e * 1e-3)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = (clk or {}).get("sm_mhz") or SM_MAX_MHZ
+    p2 = statistics.mean(pass_ms["pass2"])
+    p1 = statistics.mean(pass_ms["pass1"])
+    local_pairs = (hi - lo) * M
+    ach2 = local_pairs / (p2 * 1e-3)
+    peak2 = roofline_pairs_per_s(m.meas, "pass2", n_sm, SM_MAX_MHZ)
+    ach_upd = local_pairs / ((p1 + p2) * 1e-3)
+    peak_upd = roofline_pairs_per_s(m.meas, "update", n_sm, SM_MAX_MHZ)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("k_pass2")
+        except Exception:
+            traffic = None
+    cpu = None
+    if not args.no_cpu_baseline:
+        r = cpu_oracle_sample(cfg, Z, soa, w, args.cpu_sample, k=1)
+        cpu = {"value": r["pairs"] / r["seconds"], "unit": "pairs/s", "cores": 1, "kind": "oracle",
+               "sample": "one full serial fp64 step (predict, births, normalisers, update, extraction, resampling) "
+                         "of the first %d particles (+%d proportional births) against all M=%d measurements of "
+                         "Z_1; %.1f s" % (args.cpu_sample, r["n"] - args.cpu_sample, r["M"], r["seconds"])}
+    out = {
+        "metric": "particle-measurement update pairs/sec and filter step ms",
+        "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "N": N_glob, "M": M, "survivors": n0, "births": J,
+                   "meas_model": "position" if m.meas == 0 else "range_bearing", "parallelism": "dp%d" % world,
+                   "l2": "inputs larger than L2 (particle state %d MB > 126 MB)" % (N_glob * 20 // 2**20)},
+        "update_pairs_per_s": local_pairs * world / ((statistics.mean(pass_ms["update"])) * 1e-3),
+        "kernel_ms": {k: statistics.mean(v) for k, v in pass_ms.items()},
+        "roofline": {"bound": "alu", "kernel": "k_pass<pos,2> (update pass 2)", "achieved": ach2 / 1e9,
+                     "peak": peak2 / 1e9, "unit": "Gpair/s", "frac": ach2 / peak2, "traffic": traffic,
+                     "peak_basis": "min(128 FP32 lanes/11, 16 EX2/1) per SM-clk x %d SMs x %.0f MHz (max clock); "
+                                   "pipe rates measured (profiles/r01_pipes_microbench.jsonl)" % (n_sm, SM_MAX_MHZ),
+                     "frac_at_observed_clock": ach2 / roofline_pairs_per_s(m.meas, "pass2", n_sm, mhz)},
+        "update_roofline": {"achieved": ach_upd / 1e9, "peak": peak_upd / 1e9, "unit": "Gpair/s",
+                            "frac": ach_upd / peak_upd, "basis": "17 FP32 + 2 EX2 per pair (both passes)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": value_e, "unit": "pairs/s", "h2d_bytes_per_step": M * 8,
+                "d2h_bytes_per_step": int(f._sum.n_est) * 24 + 8 * (2 * world + 10)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(out), flush=True)
+    f.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

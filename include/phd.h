@@ -1,0 +1,215 @@
+/* include/phd.h -- C ABI of the B200-native particle PHD filter hot path.
+ *
+ * Implements one step of the particle PHD filter of arXiv 1503.03769
+ * ("Distributed Computation Particle PHD filter"; /root/reference/PAPER.md),
+ * sharded over P processes (one per GPU) exactly as the paper partitions
+ * particles over processing elements: every rank holds a
+ * contiguous block of the global particle array and the full measurement set.
+ *
+ * Step order (Algorithm 1):
+ *   phd_predict            Eq 5 survivors (CV model PAPER.md:370-388) + Eq 6 births
+ *   phd_update             Eq 7/11 normaliser C(z) (all-reduced), Eq 8/12-16 weights
+ *                          and STPHD accumulators (all-reduced)
+ *   phd_extract            PAPER.md:313-324 LT = round(W), top-LT labels, zeta = S/dW
+ *                          (rank 0 = the central unit)
+ *   phd_resample_exchange  PAPER.md:177-180, 339-352 systematic resampling, exact
+ *                          over the global array, then the particle exchange that
+ *                          rebalances the shards
+ * or the fused phd_step.  Readings of garbled/silent passages: DESIGN.md §2.
+ *
+ * Conventions
+ *  - Every call returns phd_status; nothing throws across the ABI.  On error
+ *    phd_last_error(ctx) holds a one-line message.
+ *  - Ownership: the ctx owns its device memory (allocated once in phd_create,
+ *    or carved from a caller workspace of phd_workspace_size() bytes that the
+ *    caller keeps alive until phd_destroy).  No allocation happens in a step.
+ *    Host arrays passed in are borrowed for the duration of the call; outputs
+ *    are caller-allocated.  Pointers to measurement / particle arrays may be
+ *    host or device pointers (copied with cudaMemcpyDefault).
+ *  - Streams: all device work is ordered on the ctx stream (the caller's
+ *    cudaStream_t passed to phd_create, or the ctx's own).  Calls that return
+ *    host data synchronise that stream.  A ctx is not thread-safe.
+ *  - Collectives: with world > 1 every call except the getters is collective:
+ *    every rank makes the same calls in the same order with the same
+ *    non-pointer arguments and the same measurement set.
+ *  - Labels are 0-based measurement indices into the array passed to
+ *    phd_update (the paper and SPEC use 1..M_k).
+ *  - State layout: particle state is SoA fp32 in the paper's component order
+ *    (x, vx, y, vy); host arrays "soa4" are [4][n] row-major.
+ */
+#ifndef PHD_H
+#define PHD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHD_ABI_VERSION 1
+
+typedef struct phd_ctx phd_ctx;
+
+typedef enum {
+  PHD_OK = 0,
+  PHD_EINVAL = 1,     /* invalid argument or parameter (message says which) */
+  PHD_ESTATE = 2,     /* call out of order (predict -> update -> [extract] -> resample) */
+  PHD_ECAPACITY = 3,  /* particle count exceeds capacity (fixed mode) */
+  PHD_EMODEL = 4,     /* non-finite C, D or W detected */
+  PHD_ENOMEM = 5,     /* device allocation failed / workspace too small */
+  PHD_ECUDA = 6,      /* CUDA runtime error (message has the CUDA string) */
+  PHD_ENCCL = 7,      /* NCCL error or NCCL unavailable for world > 1 */
+  PHD_ENODEV = 8      /* no CUDA device */
+} phd_status;
+
+typedef enum { PHD_MEAS_POSITION = 0, PHD_MEAS_RANGE_BEARING = 1 } phd_meas_model;
+typedef enum { PHD_COUNT_ADAPTIVE = 0, PHD_COUNT_FIXED = 1 } phd_count_mode;
+typedef enum { PHD_STAGE_RESAMPLED = 0, PHD_STAGE_PREDICTED = 1 } phd_stage;
+
+/* Model and sizing parameters (§4 simulation model; values per
+ * BASELINE.json configs).  All doubles; the kernels derive fp32 constants. */
+typedef struct {
+  int32_t abi_version;        /* must be PHD_ABI_VERSION */
+  int32_t meas;               /* phd_meas_model */
+  double T;                   /* CV sampling period, > 0 */
+  double sigma_a;             /* std of the CV process noise w_k, both axes, >= 0 */
+  double p_s;                 /* survival probability e_{k|k-1} in [0,1] (Eq 5) */
+  double p_d;                 /* detection probability P_D in [0,1] (Eq 4, 8) */
+  double sigma_z[2];          /* (sigma_x, sigma_y) or (sigma_r, sigma_theta), > 0 */
+  double sensor_xy[2];        /* range-bearing sensor position */
+  double region[4];           /* measurement region: position (xmin,xmax,ymin,ymax);
+                                 range-bearing (rmin,rmax,thmin,thmax); kappa = lambda/V */
+  double clutter_rate;        /* lambda >= 0 */
+  double birth_mass;          /* gamma >= 0: total birth mass per step (Eq 6) */
+  double birth_sigma_v;       /* birth velocity std >= 0 */
+  int64_t births_per_step;    /* J >= 0; J = 0 requires gamma = 0 */
+  int64_t particles_per_target; /* R >= 1 (adaptive mode: N_out = max(LT,1) R) */
+  int64_t fixed_count;        /* N_out in fixed mode */
+  int32_t count_mode;         /* phd_count_mode */
+  int32_t max_meas;           /* max M per step, 1..65536 */
+  int64_t capacity;           /* max global N = N_out + J */
+  uint64_t seed;              /* Philox4x32-10 key {lo32, hi32} */
+} phd_params;
+
+/* One labelled estimate: label = measurement index, state =
+ * zeta = S/dW (x, vx, y, vy), mass = dW (Eq 16). */
+typedef struct {
+  int32_t label;
+  float state[4];
+  float mass;
+} phd_estimate;
+
+typedef struct {
+  double W;               /* sum of updated weights over all ranks (N_k) */
+  double W_pred;          /* sum of predicted weights */
+  double undetected_mass; /* dW^0 = (1 - p_D) W_pred (Eq 17) */
+  int64_t LT;             /* round half away from zero of W */
+  int64_t N;              /* global particle count of this update */
+  int64_t N_out;          /* offspring count of the next resample (filled by extract) */
+  int32_t M;              /* measurements of this update */
+  int32_t n_est;          /* estimates written */
+  int32_t lt_clamped;     /* LT exceeded the eligible labels (dW > 0) */
+  int32_t count_clamped;  /* adaptive N_out clamped to capacity */
+  int32_t zero_mass;      /* W == 0: offspring spread uniformly with weight 0 */
+  int32_t near_half;      /* |W - (n + 1/2)| < 1e-4 max(1,W): LT may differ from fp64 */
+} phd_summary;
+
+/* ---- version / errors ---------------------------------------------------- */
+int32_t phd_abi_version(void);
+const char* phd_status_str(phd_status s);
+/* Last error message of ctx (never NULL; "" when none). */
+const char* phd_last_error(const phd_ctx* ctx);
+
+/* ---- lifecycle ----------------------------------------------------------- */
+/* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it). */
+phd_status phd_nccl_unique_id(uint8_t out[128]);
+/* Device bytes phd_create needs for these params at this world size. */
+phd_status phd_workspace_size(const phd_params* p, int32_t world, size_t* bytes);
+/* Create a context on `device` for rank `rank` of `world`.
+ * nccl_id: 128-byte id from phd_nccl_unique_id (ignored when world == 1).
+ * stream: a cudaStream_t to order work on, or NULL for an own stream.
+ * workspace: device pointer of >= phd_workspace_size bytes, or NULL to allocate.
+ * Errors: PHD_EINVAL (bad params: sigma <= 0, p outside [0,1], J = 0 with gamma > 0,
+ * fixed N_out + J > capacity, max_meas out of range, rank/world), PHD_ENODEV,
+ * PHD_ENOMEM, PHD_ENCCL. */
+phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const uint8_t* nccl_id,
+                      int32_t device, void* stream, void* workspace, phd_ctx** out);
+void phd_destroy(phd_ctx* ctx);
+
+/* ---- population injection / inspection (parity, checkpoint) ---------------
+ * The global particle array at a step is [survivors 0..N_out-1, births
+ * N_out..N_out+J-1]; rank r owns the block [floor(r N/W), floor((r+1) N/W)).
+ * stage = PHD_STAGE_RESAMPLED: soa4/w are this rank's survivors (the part of its
+ *   block below n_global), n_global = global survivor count N_out; the next
+ *   call must be phd_predict.  w == NULL: every weight = mass / n_global.
+ * stage = PHD_STAGE_PREDICTED: soa4/w are this rank's whole block of a
+ *   predicted array of n_global particles; the next call must be phd_update.
+ * Errors: PHD_EINVAL (n_local does not match the block), PHD_ECAPACITY. */
+phd_status phd_set_particles(phd_ctx* ctx, const float* soa4, const float* w, int64_t n_local,
+                             int64_t n_global, double mass, int32_t stage);
+/* Copy this rank's particles (SoA [4][n] and weights) to host; synchronous.
+ * n_local receives the count, global_offset the global index of element 0. */
+phd_status phd_get_particles(phd_ctx* ctx, float* soa4, float* w, int64_t cap, int64_t* n_local,
+                             int64_t* global_offset);
+
+/* ---- the step ------------------------------------------------------------- */
+/* Eq 5 + Eq 6 at step k >= 1.  z_prev [M_prev][2] is Z_{k-1} for the births
+ * (measurement-driven, S10); NULL = the Z retained by the last
+ * phd_update (none yet: births uniform over the region). */
+phd_status phd_predict(phd_ctx* ctx, int32_t k, const float* z_prev, int32_t M_prev);
+/* Update with Z_k: z [M][2] fp32 (position: (x,y); range-bearing: (r, theta) with
+ * theta in [-pi, pi]).  0 <= M <= max_meas. */
+phd_status phd_update(phd_ctx* ctx, const float* z, int32_t M);
+/* Estimates of the last update (rank 0 fills out[], every rank fills s).
+ * Writes min(LT, #eligible, cap) estimates sorted by (mass desc, label asc). */
+phd_status phd_extract(phd_ctx* ctx, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s);
+/* Systematic resampling of the updated global array into N_out offspring
+ * (adaptive: max(LT,1) R clamped to capacity - J; fixed: fixed_count), then
+ * the exchange that leaves every rank its block of the next step's array. */
+phd_status phd_resample_exchange(phd_ctx* ctx, int32_t k);
+/* predict(k, NULL) + update(z, M) + extract + resample_exchange(k). */
+phd_status phd_step(phd_ctx* ctx, int32_t k, const float* z, int32_t M, phd_estimate* out,
+                    int32_t cap, int32_t* n_out, phd_summary* s);
+
+/* ---- introspection (synchronous; for parity tests and debugging) ---------- */
+/* Global C[M] (Eq 7) of the last update, label order. */
+phd_status phd_get_normalizers(phd_ctx* ctx, double* C, int32_t cap);
+/* Global STPHD accumulators [M][5] = (dW, Sx, Svx, Sy, Svy) (Eqs 16, 18), label order. */
+phd_status phd_get_accumulators(phd_ctx* ctx, double* acc, int32_t cap);
+/* Ancestors (global index into the updated array) of this rank's produced
+ * offspring of the last resample, in global offspring order; n = count,
+ * first = global offspring index of anc[0]. */
+phd_status phd_get_ancestors(phd_ctx* ctx, int32_t* anc, int64_t cap, int64_t* n, int64_t* first);
+/* W, U, N_out and the per-rank masses W_r[world] of the last resample. */
+phd_status phd_get_resample_meta(phd_ctx* ctx, double* W, double* U, int64_t* N_out, double* W_r);
+/* Kernel launches issued by this ctx since creation (all streams). */
+int64_t phd_launch_count(const phd_ctx* ctx);
+/* Device time (ms) of the last update's pass-1 and pass-2 kernels, measured
+ * with CUDA events on the ctx stream when timing is enabled. */
+phd_status phd_set_timing(phd_ctx* ctx, int32_t enable);
+phd_status phd_get_timing(phd_ctx* ctx, float* ms /* [8]: predict, pass1, pass2, update_total,
+                                                      extract, resample, exchange, step */);
+
+/* ---- host-only helpers (no device needed; used by the CPU tests) ---------- */
+/* Library's own Philox4x32-10 (host build of the device generator). */
+void phd_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* Block [lo, hi) of n items owned by rank (floor(r n / world) bounds). */
+phd_status phd_rank_block(int64_t n, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
+/* Resampling bounds: W = sum W_r (rank order), O_r = exclusive prefix,
+ * bounds[r] = n(O_r) = clamp(ceil(O_r n_out / W - U), 0, n_out), bounds[world] = n_out.
+ * Rank r produces the offspring [bounds[r], bounds[r+1]). */
+phd_status phd_resample_bounds(int32_t world, const double* W_r, int64_t n_out, double U,
+                               int64_t* bounds, double* W);
+/* Exchange plan for `rank`: offspring produced on rank s are [bounds[s], bounds[s+1]);
+ * the next step's survivors [0, n_out) are owned per phd_rank_block(n_out + J).
+ * send_* / recv_* [world]: element counts and offsets (into the rank's produced
+ * range for sends, into its local block for receives). */
+phd_status phd_plan_exchange(int32_t world, int32_t rank, const int64_t* bounds, int64_t n_out,
+                             int64_t J, int64_t* send_count, int64_t* send_off, int64_t* recv_count,
+                             int64_t* recv_off);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHD_H */

@@ -1,0 +1,262 @@
+// Systematic resampling (Algorithm 1; Step 5 line
+// 339), exact over the global particle array and executed rank-locally
+// (DESIGN.md §4): rank r scans its own updated weights in fp64 starting at
+// O_r = sum_{s<r} W_s; particle i receives the offspring
+//   [n(B_{i-1}), n(B_i)),  n(B) = clamp(ceil(B n_out / W - U), 0, n_out),
+// pinned so that the ranks' ranges tile [0, n_out) exactly.  Offspring are
+// produced in global order by a mark + max-scan + gather pass (HBM-bound).
+#include "phd_internal.h"
+
+namespace phd {
+
+__device__ __forceinline__ int64_t n_of(double B, double scale, double U, int64_t lo, int64_t hi) {
+  double t = __dsub_rn(__dmul_rn(B, scale), U);
+  double c = ceil(t);
+  int64_t n = c <= (double)lo ? lo : (c >= (double)hi ? hi : (int64_t)c);
+  return n;
+}
+
+// Exclusive fp64 scan of the per-block masses (one CTA; fixed order).
+__global__ void __launch_bounds__(1024) k_scan_blocks(const double* __restrict__ blk, int nb, double* off) {
+  __shared__ double s[1024];
+  const int tid = threadIdx.x;
+  const int chunk = (nb + 1023) / 1024;
+  const int b0 = tid * chunk, b1 = min(b0 + chunk, nb);
+  double loc = 0.0;
+  for (int b = b0; b < b1; ++b) loc += blk[b];
+  s[tid] = loc;
+  __syncthreads();
+  // Hillis-Steele inclusive scan over thread sums
+  for (int o = 1; o < 1024; o <<= 1) {
+    double v = tid >= o ? s[tid - o] : 0.0;
+    __syncthreads();
+    s[tid] += v;
+    __syncthreads();
+  }
+  double run = tid > 0 ? s[tid - 1] : 0.0;
+  for (int b = b0; b < b1; ++b) {
+    off[b] = run;
+    run += blk[b];
+  }
+  if (tid == 1023) off[nb] = s[1023];
+}
+
+cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s) {
+  k_scan_blocks<<<1, 1024, 0, s>>>(blk, nb, blk_off);
+  return cudaGetLastError();
+}
+
+// Per block of kBlockW particles: local fp64 inclusive prefix, offspring ranges,
+// and a mark at the first offspring of every particle with a non-empty range.
+__global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
+  __shared__ double wsum[8];
+  __shared__ int64_t his[kBlockW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b = blockIdx.x;
+  const int64_t base = b * kBlockW;
+  const int64_t nb = (a.n_local + kBlockW - 1) / kBlockW;
+  double w4[4];
+  double tsum = 0.0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    int64_t i = base + 4 * tid + m;
+    w4[m] = i < a.n_local ? (double)a.w[i] : 0.0;
+    tsum += w4[m];
+  }
+  // block exclusive scan of thread sums: warp shuffle + smem over warps
+  double incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  double wpre = 0.0;
+  for (int k = 0; k < warp; ++k) wpre += wsum[k];
+  double excl = wpre + (incl - tsum);
+  // block bounds
+  const double Eb = a.O_r + a.blk_off[b];
+  const int64_t nEb = (b == 0) ? a.lo : n_of(Eb, a.scale, a.U, a.lo, a.hi);
+  const int64_t nEb1 = (b == nb - 1) ? a.hi : n_of(a.O_r + a.blk_off[b + 1], a.scale, a.U, a.lo, a.hi);
+  // raw upper bounds, clamped into [n(E_b), n(E_{b+1})]; the block's last particle
+  // (and the rank's last) is pinned to n(E_{b+1}); a block-wide running max makes
+  // the bounds non-decreasing so the ranges [his[k-1], his[k]) tile the block's
+  // offspring exactly (rounding of the fp64 partial sums cannot create gaps or
+  // overlaps).
+  __shared__ long long wmax[8];
+  double L = excl;
+  long long run = nEb;
+  long long h[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    int k = 4 * tid + m;
+    int64_t i = base + k;
+    L += w4[m];
+    long long hi;
+    if (i >= a.n_local - 1 || k == kBlockW - 1) hi = nEb1;
+    else hi = n_of(Eb + L, a.scale, a.U, nEb, nEb1);
+    run = run > hi ? run : hi;
+    h[m] = run;
+  }
+  long long incl_m = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long v = __shfl_up_sync(0xffffffffu, incl_m, o);
+    if (lane >= o) incl_m = incl_m > v ? incl_m : v;
+  }
+  if (lane == 31) wmax[warp] = incl_m;
+  __syncthreads();
+  long long carry = nEb;
+  for (int k = 0; k < warp; ++k) carry = carry > wmax[k] ? carry : wmax[k];
+  long long prev = __shfl_up_sync(0xffffffffu, incl_m, 1);
+  if (lane > 0) carry = carry > prev ? carry : prev;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) his[4 * tid + m] = h[m] > carry ? h[m] : carry;
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    int k = 4 * tid + m;
+    int64_t i = base + k;
+    if (i >= a.n_local) break;
+    int64_t lo = k == 0 ? nEb : his[k - 1];
+    int64_t hi = his[k];
+    if (hi > lo) a.marks[lo - a.lo] = (int32_t)(a.g0 + i);
+  }
+}
+
+cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s) {
+  if (a.n_local <= 0) return cudaSuccess;
+  unsigned nb = (unsigned)((a.n_local + kBlockW - 1) / kBlockW);
+  k_resample_mark<<<nb, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ int warp_max_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = max(v, u);
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_block_max(const int32_t* __restrict__ marks, int64_t n, int32_t* bmax) {
+  __shared__ int wm[8];
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * kBlockOff;
+  int m = -1;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int64_t j = base + 4 * tid + r;
+    if (j < n) m = max(m, marks[j]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((tid & 31) == 0) wm[tid >> 5] = m;
+  __syncthreads();
+  if (tid == 0) {
+    int r = -1;
+    for (int k = 0; k < 8; ++k) r = max(r, wm[k]);
+    bmax[blockIdx.x] = r;
+  }
+}
+
+cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_block_max<<<(unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s>>>(marks, n, bmax);
+  return cudaGetLastError();
+}
+
+// In place: bmax[b] <- max(bmax[0..b-1]) (exclusive; -1 for b = 0).
+__global__ void __launch_bounds__(1024) k_scan_max(int32_t* bmax, int nb) {
+  __shared__ int s[1024];
+  const int tid = threadIdx.x;
+  const int chunk = (nb + 1023) / 1024;
+  const int b0 = tid * chunk, b1 = min(b0 + chunk, nb);
+  int loc = -1;
+  for (int b = b0; b < b1; ++b) loc = max(loc, bmax[b]);
+  s[tid] = loc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    int v = tid >= o ? s[tid - o] : -1;
+    __syncthreads();
+    s[tid] = max(s[tid], v);
+    __syncthreads();
+  }
+  int run = tid > 0 ? s[tid - 1] : -1;
+  for (int b = b0; b < b1; ++b) {
+    int v = bmax[b];
+    bmax[b] = run;
+    run = max(run, v);
+  }
+}
+
+cudaError_t launch_scan_max(int32_t* bmax, int nb, cudaStream_t s) {
+  if (nb <= 0) return cudaSuccess;
+  k_scan_max<<<1, 1024, 0, s>>>(bmax, nb);
+  return cudaGetLastError();
+}
+
+// Offspring j (local produced index): ancestor = running max of the marks;
+// copy the ancestor's state, set the offspring weight W / n_out.
+__global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ marks, const int32_t* __restrict__ bex,
+                                                int64_t n, int64_t g0, const float* __restrict__ x,
+                                                const float* __restrict__ vx, const float* __restrict__ y,
+                                                const float* __restrict__ vy, float w_off, float* ox, float* ovx,
+                                                float* oy, float* ovy, float* ow, int32_t* anc, int zero_mass,
+                                                int64_t first, int64_t n_upd, int64_t n_out) {
+  __shared__ int wm[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kBlockOff;
+  int a4[4];
+  if (zero_mass) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int64_t j = base + 4 * tid + r;
+      a4[r] = (int)(((first + j) * n_upd) / n_out);
+    }
+  } else {
+    int m = -1;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int64_t j = base + 4 * tid + r;
+      a4[r] = j < n ? marks[j] : -1;
+      m = max(m, a4[r]);
+      a4[r] = m;  // thread-local inclusive running max
+    }
+    int incl = warp_max_scan(m, lane);
+    if (lane == 31) wm[warp] = incl;
+    __syncthreads();
+    int carry = bex[blockIdx.x];
+    for (int k = 0; k < warp; ++k) carry = max(carry, wm[k]);
+    int prev = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane > 0) carry = max(carry, prev);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a4[r] = max(a4[r], carry);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int64_t j = base + 4 * tid + r;
+    if (j >= n) break;
+    int64_t l = (int64_t)a4[r] - g0;
+    ox[j] = x[l];
+    ovx[j] = vx[l];
+    oy[j] = y[l];
+    ovy[j] = vy[l];
+    ow[j] = w_off;
+    anc[j] = a4[r];
+  }
+}
+
+cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_t n, int64_t g0, const float* x,
+                          const float* vx, const float* y, const float* vy, float w_off, float* ox, float* ovx,
+                          float* oy, float* ovy, float* ow, int32_t* anc, int zero_mass, int64_t first,
+                          int64_t n_global_upd, int64_t n_out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_gather<<<(unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s>>>(
+      marks, bmax_excl, n, g0, x, vx, y, vy, w_off, ox, ovx, oy, ovy, ow, anc, zero_mass, first, n_global_upd, n_out);
+  return cudaGetLastError();
+}
+
+}  // namespace phd

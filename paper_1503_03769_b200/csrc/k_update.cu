@@ -1,0 +1,573 @@
+// The fused two-pass particle x measurement update (§2.2 step 2,
+// Eqs 7-8; §3 Eqs 10-16).  Never materialises the N x M likelihood matrix.
+//
+// Tiling: measurement-stationary.  A CTA owns wz x 128
+// measurement slots (each lane 4 slots = two f32x2 pairs held in registers);
+// particles stream through shared memory in tiles of 64 and are broadcast to
+// every lane.  Per (particle, slot) pair the lane evaluates the likelihood with
+// packed FFMA2/FADD2/FMUL2 and one MUFU.EX2:
+//   pass 1:  e = 2^(-alpha q),  C'_s += e * (p_D c w_i)                 (Eq 7)
+//   pass 2:  u = e * (p_D c w_i);  dW'_s += u;  S'_s += u * (x_i - z_s);
+//            Pe_i += e * d_s,  d_s = 1/(kappa + C_s)                     (Eqs 8, 12-16)
+// Per-slot sums accumulate in fp32 over one tile (64 particles), then in an
+// fp32 mid level over 16 tiles, then in fp64 (DESIGN.md §5 "accumulation
+// precision").  Per-particle sums Pe_i are reduced across lanes with a
+// transposed butterfly and across warps through shared memory, giving one
+// fp32 partial per (particle, z-block).  Cross-CTA sums are fp64 in fixed order.
+#include "phd_internal.h"
+
+namespace phd {
+
+__device__ __forceinline__ float ex2a(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 ex2v(float2 a) { return make_float2(ex2a(a.x), ex2a(a.y)); }
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// Shared-memory particle record widths (floats, multiple of 4).
+template <int MODEL, int PASS>
+struct RecLayout {
+  static constexpr bool RB = MODEL == kRangeBearing;
+  static constexpr int WIDTH = RB ? (PASS == 1 ? 20 : 28) : (PASS == 1 ? 8 : 12);
+  static constexpr int WC = RB ? 16 : (PASS == 1 ? 4 : 8);
+  static constexpr int XY = RB ? 20 : 0;
+  static constexpr int V = RB ? 24 : 4;
+  static constexpr int NV = RB ? (PASS == 1 ? 9 : 13) : (PASS == 1 ? 3 : 5);  // floats fetched per particle
+};
+
+template <int MODEL, int PASS>
+struct TileLoader {
+  using L = RecLayout<MODEL, PASS>;
+  // one particle per loader thread: the CTA has >= kTileP threads (wz >= 2)
+  float v[1][L::NV];
+
+  __device__ __forceinline__ void fetch(const PassArgs& a, int64_t tile_base, int tid, int nthr) {
+    {
+      const int r = 0;
+      int p = tid;
+      if (p >= kTileP) return;
+      int64_t i = tile_base + p;
+      bool ok = i < a.n;
+      if (L::RB) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[r][c] = ok ? __ldg(a.rb + c * a.rb_stride + i) : 1e30f;
+        v[r][8] = ok ? __ldg(a.w + i) : 0.0f;
+        if (PASS == 2) {
+          v[r][9] = ok ? __ldg(a.x + i) : 0.0f;
+          v[r][10] = ok ? __ldg(a.y + i) : 0.0f;
+          v[r][11] = ok ? __ldg(a.vx + i) : 0.0f;
+          v[r][12] = ok ? __ldg(a.vy + i) : 0.0f;
+        }
+      } else {
+        v[r][0] = ok ? __ldg(a.x + i) : 0.0f;
+        v[r][1] = ok ? __ldg(a.y + i) : 0.0f;
+        v[r][2] = ok ? __ldg(a.w + i) : 0.0f;
+        if (PASS == 2) {
+          v[r][3] = ok ? __ldg(a.vx + i) : 0.0f;
+          v[r][4] = ok ? __ldg(a.vy + i) : 0.0f;
+        }
+      }
+    }
+  }
+
+  __device__ __forceinline__ void store(float* rec, float wscale, int tid, int nthr) {
+    {
+      const int r = 0;
+      int p = tid;
+      if (p >= kTileP) return;
+      float* d = rec + p * L::WIDTH;
+      if (L::RB) {
+        reinterpret_cast<float4*>(d)[0] = make_float4(v[r][0], v[r][0], v[r][1], v[r][1]);
+        reinterpret_cast<float4*>(d)[1] = make_float4(v[r][2], v[r][2], v[r][3], v[r][3]);
+        reinterpret_cast<float4*>(d)[2] = make_float4(v[r][4], v[r][4], v[r][5], v[r][5]);
+        reinterpret_cast<float4*>(d)[3] = make_float4(v[r][6], v[r][6], v[r][7], v[r][7]);
+        float wc = v[r][8] * wscale;
+        reinterpret_cast<float4*>(d)[4] = make_float4(wc, wc, 0.0f, 0.0f);
+        if (PASS == 2) {
+          reinterpret_cast<float4*>(d)[5] = make_float4(v[r][9], v[r][9], v[r][10], v[r][10]);
+          reinterpret_cast<float4*>(d)[6] = make_float4(v[r][11], v[r][11], v[r][12], v[r][12]);
+        }
+      } else {
+        reinterpret_cast<float4*>(d)[0] = make_float4(v[r][0], v[r][0], v[r][1], v[r][1]);
+        float wc = v[r][2] * wscale;
+        if (PASS == 2) {
+          reinterpret_cast<float4*>(d)[1] = make_float4(v[r][3], v[r][3], v[r][4], v[r][4]);
+          reinterpret_cast<float4*>(d)[2] = make_float4(wc, wc, 0.0f, 0.0f);
+        } else {
+          reinterpret_cast<float4*>(d)[1] = make_float4(wc, wc, 0.0f, 0.0f);
+        }
+      }
+    }
+  }
+};
+
+// Per-lane measurement constants for its two slot pairs.
+template <int MODEL, int PASS>
+struct LaneZ {
+  float2 n0[2], n1[2];  // -z components
+  float2 d[2];          // 1/(kappa + C)   (pass 2)
+  float2 c0[2], c1[2];  // -(Cartesian centre) (range-bearing, pass 2)
+  int roff[2];          // bearing-representation offset in the record (range-bearing)
+
+  __device__ __forceinline__ void load(const PassArgs& a, int slot0) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      int s = slot0 + 2 * j;
+      n0[j] = f2(a.sc.s0[s], a.sc.s0[s + 1]);
+      n1[j] = f2(a.sc.s1[s], a.sc.s1[s + 1]);
+      if (PASS == 2) d[j] = f2(a.sc.d[s], a.sc.d[s + 1]);
+      if (MODEL == kRangeBearing) {
+        roff[j] = 4 + 4 * a.sc.rep[s];
+        if (PASS == 2) {
+          c0[j] = f2(a.sc.s2[s], a.sc.s2[s + 1]);
+          c1[j] = f2(a.sc.s3[s], a.sc.s3[s + 1]);
+        }
+      }
+    }
+  }
+};
+
+// Quadratic form in log2 units: a = -(alpha0 d0^2 + alpha1 d1^2).
+template <int MODEL>
+__device__ __forceinline__ float2 expo(float2 d0, float2 d1, float2 na0, float2 na1) {
+  if (MODEL == kPosIso) {
+    float2 q = __fmul2_rn(d0, d0);
+    q = __ffma2_rn(d1, d1, q);
+    return __fmul2_rn(q, na0);
+  } else {
+    float2 q = __fmul2_rn(__fmul2_rn(d0, d0), na0);
+    return __ffma2_rn(__fmul2_rn(d1, d1), na1, q);
+  }
+}
+
+// Residuals (d0, d1) of the lane's slot pair j against the broadcast particle.
+template <int MODEL, int PASS>
+__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS>& z, int j, float2& d0,
+                                         float2& d1) {
+  if (MODEL == kRangeBearing) {
+    float4 R = *reinterpret_cast<const float4*>(rec);
+    float4 T = *reinterpret_cast<const float4*>(rec + z.roff[j]);
+    d0 = __fadd2_rn(__fadd2_rn(f2(R.x, R.y), z.n0[j]), f2(R.z, R.w));  // (r_hi - z_r) + r_lo
+    d1 = __fadd2_rn(__fadd2_rn(f2(T.x, T.y), z.n1[j]), f2(T.z, T.w));  // (th_hi - z_th) + th_lo
+  } else {
+    float4 P = *reinterpret_cast<const float4*>(rec);
+    d0 = __fadd2_rn(f2(P.x, P.y), z.n0[j]);  // x - z_x
+    d1 = __fadd2_rn(f2(P.z, P.w), z.n1[j]);  // y - z_y
+  }
+}
+
+// Sum of v[0..7] over the 32 lanes of a warp; lane l ends with the total of
+// particle l >> 2 (transposed butterfly: 9 SHFL + 9 FADD for 8 values).
+__device__ __forceinline__ float transpose_reduce8(float (&v)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float keep = b4 ? v[i + 4] : v[i];
+    float send = b4 ? v[i] : v[i + 4];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    float keep = b3 ? v[i + 2] : v[i];
+    float send = b3 ? v[i] : v[i + 2];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    float keep = b2 ? v[1] : v[0];
+    float send = b2 ? v[0] : v[1];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
+template <int MODEL, int PASS>
+__global__ void __launch_bounds__(256, 2) k_pass(const PassArgs a) {
+  using L = RecLayout<MODEL, PASS>;
+  constexpr int NQ = PASS == 1 ? 1 : 5;
+  extern __shared__ __align__(16) float smem[];
+  const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, wz = nthr >> 5;
+  float* recs = smem;                                   // [2][kTileP][WIDTH]
+  float* psum = recs + 2 * kTileP * L::WIDTH;            // [2][wz][kTileP] (pass 2)
+
+  const int zb = blockIdx.y;
+  const int slot0 = (zb * wz + warp) * kZPerWarp + lane * kZPerLane;
+  LaneZ<MODEL, PASS> z;
+  z.load(a, slot0);
+  const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
+
+  float2 in[NQ][2], mid[NQ][2];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) in[q][j] = mid[q][j] = f2(0.0f, 0.0f);
+  // fp64 outer accumulators live in shared memory, [NQ*4][nthr] (conflict-free)
+  double* out64 = reinterpret_cast<double*>(psum + (PASS == 2 ? 2 * wz * kTileP : 0));
+#pragma unroll
+  for (int q = 0; q < NQ * 4; ++q) out64[q * nthr + tid] = 0.0;
+
+  const int64_t ntiles = (a.n + kTileP - 1) / kTileP;
+  const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
+  const int64_t t_end = min(t_begin + a.tiles_per_cta, ntiles);
+
+  TileLoader<MODEL, PASS> ld;
+  if (t_begin < t_end) {
+    ld.fetch(a, t_begin * kTileP, tid, nthr);
+    ld.store(recs, a.wscale, tid, nthr);
+  }
+  __syncthreads();
+
+  for (int64_t t = t_begin; t < t_end; ++t) {
+    const int buf = (int)((t - t_begin) & 1);
+    const bool more = t + 1 < t_end;
+    if (more) ld.fetch(a, (t + 1) * kTileP, tid, nthr);
+    const float* rb = recs + buf * kTileP * L::WIDTH;
+
+#pragma unroll 1
+    for (int p0 = 0; p0 < kTileP; p0 += 8) {
+      float pe[8];
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp) {
+        const float* rec = rb + (p0 + pp) * L::WIDTH;
+        const float2 wc = *reinterpret_cast<const float2*>(rec + L::WC);
+        float2 pacc = f2(0.0f, 0.0f);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          float2 d0, d1;
+          residual<MODEL, PASS>(rec, z, j, d0, d1);
+          const float2 e = ex2v(expo<MODEL>(d0, d1, na0, na1));
+          if (PASS == 1) {
+            in[0][j] = __ffma2_rn(e, wc, in[0][j]);
+          } else {
+            const float2 u = __fmul2_rn(e, wc);
+            pacc = __ffma2_rn(e, z.d[j], pacc);
+            if (MODEL == kRangeBearing) {
+              const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
+              d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
+              d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
+            }
+            const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+            in[0][j] = __fadd2_rn(in[0][j], u);
+            in[1][j] = __ffma2_rn(u, d0, in[1][j]);
+            in[2][j] = __ffma2_rn(u, f2(V.x, V.y), in[2][j]);
+            in[3][j] = __ffma2_rn(u, d1, in[3][j]);
+            in[4][j] = __ffma2_rn(u, f2(V.z, V.w), in[4][j]);
+          }
+        }
+        pe[pp] = pacc.x + pacc.y;
+      }
+      if (PASS == 2) {
+        float s = transpose_reduce8(pe, lane);
+        if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = s;
+      }
+    }
+
+    if (more) ld.store(recs + (buf ^ 1) * kTileP * L::WIDTH, a.wscale, tid, nthr);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        mid[q][j] = __fadd2_rn(mid[q][j], in[q][j]);
+        in[q][j] = f2(0.0f, 0.0f);
+      }
+    __syncthreads();
+
+    if (PASS == 2) {
+      // per-particle partial over this CTA's slots: fixed-order sum over warps
+      for (int p = tid; p < kTileP; p += nthr) {
+        int64_t i = t * kTileP + p;
+        if (i < a.n) {
+          float s = 0.0f;
+          for (int w2 = 0; w2 < wz; ++w2) s += psum[(buf * wz + w2) * kTileP + p];
+          a.P[(int64_t)zb * a.P_stride + i] = s;
+        }
+      }
+    }
+    if (((t - t_begin + 1) % kFlushTiles) == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          out64[(4 * q + 2 * j) * nthr + tid] += (double)mid[q][j].x;
+          out64[(4 * q + 2 * j + 1) * nthr + tid] += (double)mid[q][j].y;
+          mid[q][j] = f2(0.0f, 0.0f);
+        }
+    }
+  }
+  const int64_t base = (int64_t)blockIdx.x * NQ * a.slots_pad;
+  double* dst = PASS == 1 ? a.Cpart : a.Apart;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      dst[base + (int64_t)q * a.slots_pad + slot0 + 2 * j] = out64[(4 * q + 2 * j) * nthr + tid] + (double)mid[q][j].x;
+      dst[base + (int64_t)q * a.slots_pad + slot0 + 2 * j + 1] =
+          out64[(4 * q + 2 * j + 1) * nthr + tid] + (double)mid[q][j].y;
+    }
+}
+
+template <int MODEL, int PASS>
+static size_t pass_smem(int wz) {
+  using L = RecLayout<MODEL, PASS>;
+  size_t b = sizeof(float) * 2 * kTileP * L::WIDTH;
+  if (PASS == 2) b += sizeof(float) * 2 * wz * kTileP;
+  b += sizeof(double) * (PASS == 1 ? 4 : 20) * wz * 32;
+  return b;
+}
+
+template <int MODEL, int PASS>
+static cudaError_t launch_one(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pass<MODEL, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pass_smem<MODEL, PASS>(kMaxWarpsZ));
+    attr = true;
+  }
+  dim3 grid((unsigned)gp, (unsigned)zb);
+  k_pass<MODEL, PASS><<<grid, wz * 32, pass_smem<MODEL, PASS>(wz), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+  if (gp <= 0 || zb <= 0) return cudaSuccess;
+  if (model == kPosIso) return pass == 1 ? launch_one<kPosIso, 1>(a, gp, zb, wz, s) : launch_one<kPosIso, 2>(a, gp, zb, wz, s);
+  if (model == kPosAniso) return pass == 1 ? launch_one<kPosAniso, 1>(a, gp, zb, wz, s) : launch_one<kPosAniso, 2>(a, gp, zb, wz, s);
+  return pass == 1 ? launch_one<kRangeBearing, 1>(a, gp, zb, wz, s) : launch_one<kRangeBearing, 2>(a, gp, zb, wz, s);
+}
+
+template <int MODEL, int PASS>
+static int occ_one(int wz) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pass<MODEL, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pass_smem<MODEL, PASS>(kMaxWarpsZ));
+    attr = true;
+  }
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<MODEL, PASS>, wz * 32, pass_smem<MODEL, PASS>(wz));
+  return n;
+}
+
+int pass_occupancy(int model, int pass, int wz) {
+  if (model == kPosIso) return pass == 1 ? occ_one<kPosIso, 1>(wz) : occ_one<kPosIso, 2>(wz);
+  if (model == kPosAniso) return pass == 1 ? occ_one<kPosAniso, 1>(wz) : occ_one<kPosAniso, 2>(wz);
+  return pass == 1 ? occ_one<kRangeBearing, 1>(wz) : occ_one<kRangeBearing, 2>(wz);
+}
+
+// ---------------------------------------------------------------------------
+// Measurement-slot preparation.  Slots hold labels (or -1 = padding); padding
+// slots get a sentinel that makes every likelihood term exactly 0.
+__global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* __restrict__ slot_label, int n,
+                        float sx, float sy, SlotConsts sc) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int lab = slot_label[s];
+  float s0 = -1e30f, s1 = -1e30f, s2 = 0.0f, s3 = 0.0f;
+  int rep = 0;
+  if (lab >= 0) {
+    float z0 = z[2 * lab], z1 = z[2 * lab + 1];
+    s0 = -z0;
+    s1 = -z1;
+    if (model == kRangeBearing) {
+      const float half_pi = 1.57079632679489662f;
+      rep = (z1 > half_pi) ? 1 : ((z1 < -half_pi) ? 2 : 0);
+      float sn, cs;
+      sincosf(z1, &sn, &cs);
+      s2 = -(sx + z0 * cs);
+      s3 = -(sy + z0 * sn);
+    }
+  }
+  sc.s0[s] = s0;
+  sc.s1[s] = s1;
+  if (sc.s2) {
+    sc.s2[s] = s2;
+    sc.s3[s] = s3;
+  }
+  if (sc.rep) sc.rep[s] = rep;
+  sc.d[s] = 0.0f;
+}
+
+cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad, float sensor_x,
+                         float sensor_y, SlotConsts sc, cudaStream_t s) {
+  if (n_slots_pad <= 0) return cudaSuccess;
+  k_zprep<<<(n_slots_pad + 255) / 256, 256, 0, s>>>(model, z_lab, slot_label, n_slots_pad, sensor_x, sensor_y, sc);
+  return cudaGetLastError();
+}
+
+// C[label] = sum over particle-CTAs (fixed order) of the pass-1 partials (fp64).
+__global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_pad, int n_slots,
+                           const int32_t* __restrict__ slot_label, double* C_lab) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_slots) return;
+  int lab = slot_label[s];
+  if (lab < 0) return;
+  double c = 0.0;
+  for (int b = 0; b < gp; ++b) c += Cpart[(int64_t)b * slots_pad + s];
+  C_lab[lab] = c;
+}
+
+cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
+                            double* C_lab, cudaStream_t s) {
+  if (n_slots <= 0) return cudaSuccess;
+  k_reduce_C<<<(n_slots + 127) / 128, 128, 0, s>>>(Cpart, gp, slots_pad, n_slots, slot_label, C_lab);
+  return cudaGetLastError();
+}
+
+// D = kappa + C (fp64, label order); per-slot d = 1/D as fp32 (0 when D == 0).
+__global__ void k_zconst(const double* __restrict__ C_lab, int M, double kappa,
+                         const int32_t* __restrict__ slot_label, int n, float* d_slot, double* D_lab, int* bad) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < M) {
+    double D = kappa + C_lab[s];
+    D_lab[s] = D;
+    if (!isfinite(D)) atomicAdd(bad, 1);
+  }
+  if (s < n) {
+    int lab = slot_label[s];
+    float d = 0.0f;
+    if (lab >= 0) {
+      double D = kappa + C_lab[lab];
+      d = D > 0.0 ? (float)(1.0 / D) : 0.0f;
+    }
+    d_slot[s] = d;
+  }
+}
+
+cudaError_t launch_zconst(const double* C_lab, int M, double kappa, const int32_t* slot_label, int n_slots_pad,
+                          float* d_slot, double* D_lab, int* bad, cudaStream_t s) {
+  int n = n_slots_pad > M ? n_slots_pad : M;
+  if (n <= 0) return cudaSuccess;
+  k_zconst<<<(n + 255) / 256, 256, 0, s>>>(C_lab, M, kappa, slot_label, n_slots_pad, d_slot, D_lab, bad);
+  return cudaGetLastError();
+}
+
+// w'_i = w_i [ (1 - p_D) + p_D c sum_zb P[zb][i] ]  (Eq 8 / Eq 15); fp64 block sums
+// of w' and of the predicted w (blocks of kBlockW particles, fixed tree order).
+__global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, const float* __restrict__ P,
+                                                  int64_t P_stride, int zb, int64_t n, float nu, float wscale,
+                                                  float* w_out, double* blk_w, double* blk_wp) {
+  __shared__ double sw[8], swp[8];
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * kBlockW;
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int r = 0; r < kBlockW / 256; ++r) {
+    int64_t i = base + r * 256 + tid;
+    if (i < n) {
+      float wi = w[i];
+      float s = 0.0f;
+      for (int k = 0; k < zb; ++k) s += P[(int64_t)k * P_stride + i];
+      float wn = wi * nu + (wi * wscale) * s;
+      w_out[i] = wn;
+      a += (double)wn;
+      b += (double)wi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((tid & 31) == 0) {
+    sw[tid >> 5] = a;
+    swp[tid >> 5] = b;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      x += sw[k];
+      y += swp[k];
+    }
+    blk_w[blockIdx.x] = x;
+    blk_wp[blockIdx.x] = y;
+  }
+}
+
+cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, int zb, int64_t n, float nu,
+                             float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  unsigned nb = (unsigned)((n + kBlockW - 1) / kBlockW);
+  k_finalize<<<nb, 256, 0, s>>>(w, P, P_stride, zb, n, nu, wscale, w_out, blk_w, blk_wp);
+  return cudaGetLastError();
+}
+
+// STPHD accumulators in label order (Eqs 16, 18):
+//   dW = A0 / D,  Sx = A1 / D + cx dW,  Svx = A2 / D,  Sy = A3 / D + cy dW,  Svy = A4 / D
+// with (cx, cy) the centre the kernel subtracted (the measurement itself for
+// the position sensor).  The last CTA reduces the per-block masses into this
+// rank's W_r and W_pred_r and writes them into the all-reduce buffer.
+__global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots_pad, int n_slots,
+                             const int32_t* __restrict__ slot_label, const double* __restrict__ D_lab,
+                             const float* __restrict__ s0, const float* __restrict__ s1,
+                             const float* __restrict__ s2, const float* __restrict__ s3, int model,
+                             const double* __restrict__ blk_w, const double* __restrict__ blk_wp, int nb,
+                             double* acc_lab, double* rank_slots, int rank, int world) {
+  if (blockIdx.x == gridDim.x - 1) {
+    __shared__ double sa[256], sb[256];
+    double a = 0.0, b = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      a += blk_w[k];
+      b += blk_wp[k];
+    }
+    sa[threadIdx.x] = a;
+    sb[threadIdx.x] = b;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) {
+        sa[threadIdx.x] += sa[threadIdx.x + o];
+        sb[threadIdx.x] += sb[threadIdx.x + o];
+      }
+      __syncthreads();
+    }
+    for (int r = threadIdx.x; r < 2 * world; r += blockDim.x) rank_slots[r] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      rank_slots[rank] = sa[0];
+      rank_slots[world + rank] = sb[0];
+    }
+    return;
+  }
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_slots) return;
+  int lab = slot_label[s];
+  if (lab < 0) return;
+  double A[5] = {0, 0, 0, 0, 0};
+  for (int b = 0; b < gp; ++b) {
+    const double* p = Apart + (int64_t)b * 5 * slots_pad + s;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) A[q] += p[(int64_t)q * slots_pad];
+  }
+  double D = D_lab[lab];
+  double inv = D > 0.0 ? 1.0 / D : 0.0;
+  double cx, cy;
+  if (model == kRangeBearing) {
+    cx = -(double)s2[s];
+    cy = -(double)s3[s];
+  } else {
+    cx = -(double)s0[s];
+    cy = -(double)s1[s];
+  }
+  double dW = A[0] * inv;
+  double* o = acc_lab + 5 * (int64_t)lab;
+  o[0] = dW;
+  o[1] = A[1] * inv + cx * dW;
+  o[2] = A[2] * inv;
+  o[3] = A[3] * inv + cy * dW;
+  o[4] = A[4] * inv;
+}
+
+cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
+                              const double* D_lab, const float* s0, const float* s1, const float* s2,
+                              const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
+                              double* acc_lab, double* rank_slots, int rank, int world, cudaStream_t s) {
+  int blocks = (n_slots + 255) / 256 + 1;
+  k_reduce_acc<<<blocks, 256, 0, s>>>(Apart, gp, slots_pad, n_slots, slot_label, D_lab, s0, s1, s2, s3, model,
+                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world);
+  return cudaGetLastError();
+}
+
+}  // namespace phd

@@ -1,0 +1,929 @@
+// C-ABI implementation (include/phd.h): context, device memory layout, step
+// orchestration on one CUDA stream, NCCL collectives for world > 1.
+//
+// Per step:
+//   predict   k_predict                                     (HBM)
+//   update    k_zprep -> k_pass<1> -> k_reduce_C -> [C1 all-reduce] -> k_zconst
+//             -> k_pass<2> -> k_finalize -> k_reduce_acc -> [C2 all-reduce]
+//             -> one 8*(2W+2) byte D2H (the step's only host sync)
+//   extract   k_extract on rank 0 (the central unit) + D2H of the estimates
+//   resample  k_scan_blocks -> k_resample_mark -> k_block_max -> k_scan_max -> k_gather
+//   exchange  world 1: buffer swap; world > 1: grouped ncclSend/ncclRecv (C3)
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "phd.h"
+#include "phd_internal.h"
+#include "philox.cuh"
+
+using namespace phd;
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+constexpr double kLog2e = 1.44269504088896340735992468100189214;
+enum Stage { kResampled = 0, kPredicted = 1, kUpdated = 2 };
+
+struct Layout {
+  int64_t cap_g = 0, cap_l = 0, cap_off = 0;
+  int slots_max = 0, zb_max = 0;
+  int64_t part_cap = 0;  // max gp * slots_pad
+  int64_t nbw_max = 0, nbo_max = 0;
+  size_t total = 0;
+  // byte offsets
+  size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_D,
+      o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_summ, o_bad;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+Layout make_layout(const phd_params* p, int world, int sms) {
+  Layout L;
+  L.cap_g = p->capacity;
+  L.cap_l = align_up((size_t)(ceil_div(p->capacity, world) + 1), kBlockW);
+  L.cap_off = align_up((size_t)p->capacity, kBlockOff);
+  L.slots_max = (int)align_up((size_t)p->max_meas + 2, 1024);
+  L.zb_max = std::max(1, L.slots_max / 1024);
+  L.part_cap = (int64_t)64 * sms * 128 + 8192;
+  L.nbw_max = ceil_div(L.cap_l, kBlockW) + 1;
+  L.nbo_max = ceil_div(L.cap_off, kBlockOff) + 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  for (int i = 0; i < 5; ++i) L.o_A[i] = take(sizeof(float) * L.cap_l);
+  for (int i = 0; i < 5; ++i) L.o_B[i] = take(sizeof(float) * std::max(L.cap_off, L.cap_l));
+  L.o_wn = take(sizeof(float) * L.cap_l);
+  L.o_rb = take(p->meas == PHD_MEAS_RANGE_BEARING ? sizeof(float) * 8 * L.cap_l : 256);
+  L.o_P = take(sizeof(float) * (size_t)L.zb_max * L.cap_l);
+  L.o_Cpart = take(sizeof(double) * L.part_cap);
+  L.o_Apart = take(sizeof(double) * 5 * L.part_cap);
+  L.o_zlab = take(sizeof(float) * 2 * (size_t)(p->max_meas + 1));
+  L.o_zprev = take(sizeof(float) * 2 * (size_t)(p->max_meas + 1));
+  L.o_slot = take(sizeof(int32_t) * L.slots_max);
+  for (int i = 0; i < 5; ++i) L.o_s[i] = take(sizeof(float) * L.slots_max);
+  L.o_rep = take(sizeof(int32_t) * L.slots_max);
+  L.o_C = take(sizeof(double) * (size_t)(p->max_meas + 1));
+  L.o_D = take(sizeof(double) * (size_t)(p->max_meas + 1));
+  L.o_acc = take(sizeof(double) * (5 * (size_t)p->max_meas + 2 * (size_t)world + 8));
+  L.o_blk_w = take(sizeof(double) * L.nbw_max);
+  L.o_blk_wp = take(sizeof(double) * L.nbw_max);
+  L.o_blk_off = take(sizeof(double) * (L.nbw_max + 1));
+  L.o_marks = take(sizeof(int32_t) * L.cap_off);
+  L.o_bmax = take(sizeof(int32_t) * L.nbo_max);
+  L.o_anc = take(sizeof(int32_t) * L.cap_off);
+  L.o_est = take(sizeof(phd_estimate) * (size_t)(p->max_meas + 1));
+  L.o_summ = take(sizeof(double) * 16);
+  L.o_bad = take(sizeof(int) * 4);
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+struct phd_ctx {
+  phd_params p{};
+  int rank = 0, world = 1, device = 0, sms = 148;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  char* ws = nullptr;
+  bool own_ws = false;
+  Layout L;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int model = kPosIso;
+  double kappa = 0.0;
+  float na0 = 0, na1 = 0, wscale = 0, nu = 0;
+  // device arrays
+  float* A[5];   // x, vx, y, vy, w
+  float* B[5];   // offspring
+  float* wn;
+  float* rb;
+  float* P;
+  double *Cpart, *Apart;
+  float *zlab, *zprev;
+  int32_t* slot_label;
+  float* s[5];   // s0, s1, s2, s3, d
+  int32_t* rep;
+  double *C, *D, *acc;
+  double *blk_w, *blk_wp, *blk_off;
+  int32_t *marks, *bmax, *anc;
+  phd_estimate* est;
+  double* summ;
+  int* bad;
+  // pinned host staging
+  double* h_meta = nullptr;  // [16 + 2 world + 2]
+  phd_estimate* h_est = nullptr;
+  float* h_z = nullptr;
+  int32_t* h_slot = nullptr;
+  // step state
+  int stage = kResampled;
+  bool populated = false;
+  int64_t n_out = 0;      // global survivors entering predict
+  int64_t N = 0;          // global particles of the predicted/updated array
+  int64_t n_local = 0, g0 = 0;
+  int64_t n_surv_local = 0;
+  int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zb = 0, gp = 0, M_z = -1;
+  int m_prev_ext = -1;   // >= 0: zprev holds an explicit Z_{k-1} of this size
+  double W = 0, W_pred = 0;
+  int64_t LT = 0;
+  std::vector<double> Wr, Wpr;
+  int bad_flag = 0;
+  int near_half = 0;
+  // resample
+  double U_last = 0, W_last = 0;
+  int64_t N_out_last = 0, prod_first = 0, prod_n = 0;
+  int count_clamped = 0, zero_mass = 0;
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[16] = {};
+  float t_ms[8] = {};
+};
+
+// ---------------------------------------------------------------------------
+namespace {
+
+phd_status fail(phd_ctx* c, phd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CU(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(c, PHD_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                       \
+  } while (0)
+#define KL(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    ++c->launches;                                                                                \
+    if (e_ != cudaSuccess) return fail(c, PHD_ECUDA, "launch %s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define NC(call)                                                                                  \
+  do {                                                                                            \
+    ncclResult_t r_ = (call);                                                                     \
+    if (r_ != ncclSuccess) return fail(c, PHD_ENCCL, "%s: %s", #call, ncclGetErrorString(r_));    \
+  } while (0)
+
+void block_of(int64_t n, int world, int rank, int64_t* lo, int64_t* hi) {
+  *lo = (int64_t)((__int128)n * rank / world);
+  *hi = (int64_t)((__int128)n * (rank + 1) / world);
+}
+
+int64_t n_of_host(double B, double scale, double U, int64_t n_out) {
+  volatile double t = B * scale;  // no contraction: same IEEE ops as the device __dmul_rn/__dsub_rn
+  volatile double t2 = t - U;
+  double c = std::ceil((double)t2);
+  if (c <= 0.0) return 0;
+  if (c >= (double)n_out) return n_out;
+  return (int64_t)c;
+}
+
+phd_status validate(const phd_params* p, int world, phd_ctx* c) {
+  if (!p) return fail(c, PHD_EINVAL, "params is NULL");
+  if (p->abi_version != PHD_ABI_VERSION) return fail(c, PHD_EINVAL, "abi_version %d != %d", p->abi_version, PHD_ABI_VERSION);
+  if (p->meas != PHD_MEAS_POSITION && p->meas != PHD_MEAS_RANGE_BEARING) return fail(c, PHD_EINVAL, "meas model %d", p->meas);
+  if (!(p->T > 0)) return fail(c, PHD_EINVAL, "T must be > 0");
+  if (!(p->sigma_a >= 0)) return fail(c, PHD_EINVAL, "sigma_a must be >= 0");
+  if (!(p->p_s >= 0 && p->p_s <= 1)) return fail(c, PHD_EINVAL, "p_s outside [0,1]");
+  if (!(p->p_d >= 0 && p->p_d <= 1)) return fail(c, PHD_EINVAL, "p_d outside [0,1]");
+  if (!(p->sigma_z[0] > 0 && p->sigma_z[1] > 0)) return fail(c, PHD_EINVAL, "sigma_z must be > 0");
+  if (!(p->region[1] > p->region[0] && p->region[3] > p->region[2])) return fail(c, PHD_EINVAL, "empty region");
+  if (!(p->clutter_rate >= 0)) return fail(c, PHD_EINVAL, "clutter_rate must be >= 0");
+  if (!(p->birth_mass >= 0 && p->birth_sigma_v >= 0)) return fail(c, PHD_EINVAL, "birth params must be >= 0");
+  if (p->births_per_step < 0) return fail(c, PHD_EINVAL, "births_per_step < 0");
+  if (p->births_per_step == 0 && p->birth_mass > 0) return fail(c, PHD_EINVAL, "J = 0 with gamma > 0 (SPEC.md:161)");
+  if (p->max_meas < 1 || p->max_meas > 8192) return fail(c, PHD_EINVAL, "max_meas must be in [1, 8192]");
+  if (p->capacity < 1 || p->capacity > ((int64_t)1 << 31) - 1) return fail(c, PHD_EINVAL, "capacity must be in [1, 2^31)");
+  if (p->count_mode == PHD_COUNT_FIXED) {
+    if (p->fixed_count < 1) return fail(c, PHD_EINVAL, "fixed_count must be >= 1");
+    if (p->fixed_count + p->births_per_step > p->capacity) return fail(c, PHD_EINVAL, "fixed N_out + J > capacity");
+  } else if (p->count_mode == PHD_COUNT_ADAPTIVE) {
+    if (p->particles_per_target < 1) return fail(c, PHD_EINVAL, "particles_per_target must be >= 1");
+    if (p->particles_per_target + p->births_per_step > p->capacity) return fail(c, PHD_EINVAL, "R + J > capacity");
+  } else {
+    return fail(c, PHD_EINVAL, "count_mode %d", p->count_mode);
+  }
+  if (world < 1) return fail(c, PHD_EINVAL, "world < 1");
+  return PHD_OK;
+}
+
+template <class T>
+T* at(char* base, size_t off) {
+  return reinterpret_cast<T*>(base + off);
+}
+
+void timing_record(phd_ctx* c, int i) {
+  if (c->timing) cudaEventRecord(c->ev[i], c->st);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int32_t phd_abi_version(void) { return PHD_ABI_VERSION; }
+
+const char* phd_status_str(phd_status s) {
+  switch (s) {
+    case PHD_OK: return "ok";
+    case PHD_EINVAL: return "invalid argument";
+    case PHD_ESTATE: return "call out of order";
+    case PHD_ECAPACITY: return "capacity exceeded";
+    case PHD_EMODEL: return "non-finite model quantity";
+    case PHD_ENOMEM: return "out of device memory";
+    case PHD_ECUDA: return "CUDA error";
+    case PHD_ENCCL: return "NCCL error";
+    case PHD_ENODEV: return "no CUDA device";
+  }
+  return "unknown status";
+}
+
+const char* phd_last_error(const phd_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+void phd_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  U4 o = philox10(U4{ctr[0], ctr[1], ctr[2], ctr[3]}, key[0], key[1]);
+  out[0] = o.x;
+  out[1] = o.y;
+  out[2] = o.z;
+  out[3] = o.w;
+}
+
+phd_status phd_rank_block(int64_t n, int32_t world, int32_t rank, int64_t* lo, int64_t* hi) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi) return PHD_EINVAL;
+  block_of(n, world, rank, lo, hi);
+  return PHD_OK;
+}
+
+phd_status phd_resample_bounds(int32_t world, const double* W_r, int64_t n_out, double U, int64_t* bounds,
+                               double* W_out) {
+  if (world < 1 || !W_r || !bounds || n_out < 0) return PHD_EINVAL;
+  double W = 0.0;
+  for (int r = 0; r < world; ++r) W += W_r[r];
+  if (W_out) *W_out = W;
+  if (!(W > 0.0)) return PHD_EINVAL;
+  double scale = (double)n_out / W;
+  double O = 0.0;
+  for (int r = 0; r < world; ++r) {
+    bounds[r] = r == 0 ? 0 : n_of_host(O, scale, U, n_out);
+    O += W_r[r];
+  }
+  bounds[world] = n_out;
+  return PHD_OK;
+}
+
+phd_status phd_plan_exchange(int32_t world, int32_t rank, const int64_t* bounds, int64_t n_out, int64_t J,
+                             int64_t* send_count, int64_t* send_off, int64_t* recv_count, int64_t* recv_off) {
+  if (world < 1 || rank < 0 || rank >= world || !bounds) return PHD_EINVAL;
+  int64_t Nn = n_out + J;
+  for (int q = 0; q < world; ++q) {
+    int64_t lo, hi;
+    block_of(Nn, world, q, &lo, &hi);
+    int64_t a = std::min(lo, n_out), b = std::min(hi, n_out);
+    // what rank sends to q
+    int64_t s0 = std::max(bounds[rank], a), s1 = std::min(bounds[rank + 1], b);
+    send_count[q] = std::max<int64_t>(0, s1 - s0);
+    send_off[q] = send_count[q] ? s0 - bounds[rank] : 0;
+  }
+  int64_t mlo, mhi;
+  block_of(Nn, world, rank, &mlo, &mhi);
+  int64_t a = std::min(mlo, n_out), b = std::min(mhi, n_out);
+  for (int q = 0; q < world; ++q) {
+    int64_t r0 = std::max(bounds[q], a), r1 = std::min(bounds[q + 1], b);
+    recv_count[q] = std::max<int64_t>(0, r1 - r0);
+    recv_off[q] = recv_count[q] ? r0 - mlo : 0;
+  }
+  return PHD_OK;
+}
+
+phd_status phd_nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PHD_ENCCL;
+  static_assert(sizeof(id) == 128, "nccl id size");
+  memcpy(out, &id, 128);
+  return PHD_OK;
+}
+
+phd_status phd_workspace_size(const phd_params* p, int32_t world, size_t* bytes) {
+  phd_status s = validate(p, world, nullptr);
+  if (s != PHD_OK) return s;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  *bytes = make_layout(p, world, sms).total;
+  return PHD_OK;
+}
+
+phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const uint8_t* nccl_id, int32_t device,
+                      void* stream, void* workspace, phd_ctx** out) {
+  if (!out) return PHD_EINVAL;
+  *out = nullptr;
+  phd_ctx* c = new phd_ctx();
+  phd_status s = validate(p, world, c);
+  if (s == PHD_OK && (rank < 0 || rank >= world)) s = fail(c, PHD_EINVAL, "rank %d of world %d", rank, world);
+  if (s != PHD_OK) {
+    fprintf(stderr, "phd_create: %s\n", c->err.c_str());
+    delete c;
+    return s;
+  }
+  c->p = *p;
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    delete c;
+    return PHD_ENODEV;
+  }
+  auto bail = [&](phd_status st) {
+    fprintf(stderr, "phd_create: %s\n", c->err.c_str());
+    phd_destroy(c);
+    return st;
+  };
+#define CUB(call)                                                                              \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) return bail(fail(c, PHD_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); \
+  } while (0)
+  CUB(cudaSetDevice(device));
+  CUB(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+  if (stream) {
+    c->st = (cudaStream_t)stream;
+  } else {
+    CUB(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  c->L = make_layout(p, world, c->sms);
+  if (workspace) {
+    c->ws = (char*)workspace;
+  } else {
+    cudaError_t e = cudaMalloc(&c->ws, c->L.total);
+    if (e != cudaSuccess) return bail(fail(c, PHD_ENOMEM, "cudaMalloc(%zu): %s", c->L.total, cudaGetErrorString(e)));
+    c->own_ws = true;
+  }
+  const Layout& L = c->L;
+  for (int i = 0; i < 5; ++i) {
+    c->A[i] = at<float>(c->ws, L.o_A[i]);
+    c->B[i] = at<float>(c->ws, L.o_B[i]);
+    c->s[i] = at<float>(c->ws, L.o_s[i]);
+  }
+  c->wn = at<float>(c->ws, L.o_wn);
+  c->rb = p->meas == PHD_MEAS_RANGE_BEARING ? at<float>(c->ws, L.o_rb) : nullptr;
+  c->P = at<float>(c->ws, L.o_P);
+  c->Cpart = at<double>(c->ws, L.o_Cpart);
+  c->Apart = at<double>(c->ws, L.o_Apart);
+  c->zlab = at<float>(c->ws, L.o_zlab);
+  c->zprev = at<float>(c->ws, L.o_zprev);
+  c->slot_label = at<int32_t>(c->ws, L.o_slot);
+  c->rep = at<int32_t>(c->ws, L.o_rep);
+  c->C = at<double>(c->ws, L.o_C);
+  c->D = at<double>(c->ws, L.o_D);
+  c->acc = at<double>(c->ws, L.o_acc);
+  c->blk_w = at<double>(c->ws, L.o_blk_w);
+  c->blk_wp = at<double>(c->ws, L.o_blk_wp);
+  c->blk_off = at<double>(c->ws, L.o_blk_off);
+  c->marks = at<int32_t>(c->ws, L.o_marks);
+  c->bmax = at<int32_t>(c->ws, L.o_bmax);
+  c->anc = at<int32_t>(c->ws, L.o_anc);
+  c->est = at<phd_estimate>(c->ws, L.o_est);
+  c->summ = at<double>(c->ws, L.o_summ);
+  c->bad = at<int>(c->ws, L.o_bad);
+  CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (32 + 2 * world)));
+  CUB(cudaMallocHost(&c->h_est, sizeof(phd_estimate) * (p->max_meas + 1)));
+  CUB(cudaMallocHost(&c->h_z, sizeof(float) * 2 * (p->max_meas + 1)));
+  CUB(cudaMallocHost(&c->h_slot, sizeof(int32_t) * L.slots_max));
+  for (int i = 0; i < 16; ++i) CUB(cudaEventCreate(&c->ev[i]));
+  // derived model constants (fp32 for the pair kernels, fp64 for kappa)
+  double s0 = p->sigma_z[0], s1 = p->sigma_z[1];
+  bool rbm = p->meas == PHD_MEAS_RANGE_BEARING;
+  c->model = rbm ? kRangeBearing : (s0 == s1 ? kPosIso : kPosAniso);
+  c->na0 = (float)(-kLog2e / (2.0 * s0 * s0));
+  c->na1 = (float)(-kLog2e / (2.0 * s1 * s1));
+  c->wscale = (float)(p->p_d / (2.0 * kPi * s0 * s1));
+  c->nu = (float)(1.0 - p->p_d);
+  c->kappa = p->clutter_rate / ((p->region[1] - p->region[0]) * (p->region[3] - p->region[2]));
+  c->Wr.assign(world, 0.0);
+  c->Wpr.assign(world, 0.0);
+  if (world > 1) {
+    if (!nccl_id) return bail(fail(c, PHD_EINVAL, "nccl_id required for world > 1"));
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) return bail(fail(c, PHD_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+  }
+  CUB(cudaMemsetAsync(c->ws, 0, L.total, c->st));
+  CUB(cudaStreamSynchronize(c->st));
+#undef CUB
+  *out = c;
+  return PHD_OK;
+}
+
+void phd_destroy(phd_ctx* c) {
+  if (!c) return;
+  if (c->st) cudaStreamSynchronize(c->st);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (int i = 0; i < 16; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  if (c->own_ws && c->ws) cudaFree(c->ws);
+  if (c->h_meta) cudaFreeHost(c->h_meta);
+  if (c->h_est) cudaFreeHost(c->h_est);
+  if (c->h_z) cudaFreeHost(c->h_z);
+  if (c->h_slot) cudaFreeHost(c->h_slot);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+int64_t phd_launch_count(const phd_ctx* c) { return c ? c->launches : 0; }
+
+phd_status phd_set_timing(phd_ctx* c, int32_t enable) {
+  if (!c) return PHD_EINVAL;
+  c->timing = enable != 0;
+  return PHD_OK;
+}
+
+phd_status phd_get_timing(phd_ctx* c, float* ms) {
+  if (!c || !ms) return PHD_EINVAL;
+  CU(cudaStreamSynchronize(c->st));
+  for (int i = 0; i < 8; ++i) ms[i] = c->t_ms[i];
+  return PHD_OK;
+}
+
+// ---------------------------------------------------------------------------
+phd_status phd_set_particles(phd_ctx* c, const float* soa4, const float* w, int64_t n_local, int64_t n_global,
+                             double mass, int32_t stage) {
+  if (!c || !soa4) return PHD_EINVAL;
+  c->err.clear();
+  int64_t J = c->p.births_per_step;
+  int64_t Nblk = stage == PHD_STAGE_PREDICTED ? n_global : n_global + J;
+  if (n_global < 0 || Nblk > c->p.capacity) return fail(c, PHD_ECAPACITY, "n_global %lld exceeds capacity", (long long)n_global);
+  int64_t lo, hi;
+  block_of(Nblk, c->world, c->rank, &lo, &hi);
+  int64_t expect = stage == PHD_STAGE_PREDICTED ? hi - lo : std::max<int64_t>(0, std::min(hi, n_global) - std::min(lo, n_global));
+  if (n_local != expect)
+    return fail(c, PHD_EINVAL, "n_local %lld != %lld (rank block of %lld)", (long long)n_local, (long long)expect, (long long)Nblk);
+  for (int i = 0; i < 4; ++i)
+    CU(cudaMemcpyAsync(c->A[i], soa4 + (size_t)i * n_local, sizeof(float) * n_local, cudaMemcpyDefault, c->st));
+  if (w) {
+    CU(cudaMemcpyAsync(c->A[4], w, sizeof(float) * n_local, cudaMemcpyDefault, c->st));
+  } else {
+    KL(launch_fill(c->A[4], (float)(n_global > 0 ? mass / (double)n_global : 0.0), n_local, c->st));
+  }
+  if (stage == PHD_STAGE_PREDICTED) {
+    c->N = n_global;
+    c->n_out = n_global;
+    c->n_local = n_local;
+    c->g0 = lo;
+    if (c->rb) KL(launch_rb_repr(c->A[0], c->A[2], n_local, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], c->rb, c->L.cap_l, c->st));
+    c->stage = kPredicted;
+  } else {
+    c->n_out = n_global;
+    c->n_surv_local = n_local;
+    c->stage = kResampled;
+  }
+  c->populated = true;
+  CU(cudaStreamSynchronize(c->st));
+  return PHD_OK;
+}
+
+phd_status phd_get_particles(phd_ctx* c, float* soa4, float* w, int64_t cap, int64_t* n_local, int64_t* global_offset) {
+  if (!c) return PHD_EINVAL;
+  int64_t n, g0;
+  if (c->stage == kResampled) {
+    int64_t lo, hi;
+    block_of(c->n_out + c->p.births_per_step, c->world, c->rank, &lo, &hi);
+    n = c->n_surv_local;
+    g0 = lo;
+  } else {
+    n = c->n_local;
+    g0 = c->g0;
+  }
+  if (n_local) *n_local = n;
+  if (global_offset) *global_offset = g0;
+  if (cap < n) return fail(c, PHD_EINVAL, "cap %lld < %lld", (long long)cap, (long long)n);
+  if (soa4)
+    for (int i = 0; i < 4; ++i) CU(cudaMemcpyAsync(soa4 + (size_t)i * n, c->A[i], sizeof(float) * n, cudaMemcpyDeviceToHost, c->st));
+  if (w) CU(cudaMemcpyAsync(w, c->stage == kUpdated ? c->wn : c->A[4], sizeof(float) * n, cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  return PHD_OK;
+}
+
+phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_prev) {
+  if (!c) return PHD_EINVAL;
+  c->err.clear();
+  if (!c->populated || c->stage != kResampled) return fail(c, PHD_ESTATE, "phd_predict needs a resampled population");
+  if (k < 1) return fail(c, PHD_EINVAL, "k must be >= 1");
+  if (z_prev && (M_prev < 0 || M_prev > c->p.max_meas)) return fail(c, PHD_EINVAL, "M_prev %d out of range", M_prev);
+  timing_record(c, 0);
+  const float* zp = nullptr;
+  int mp = 0;
+  if (z_prev) {
+    if (M_prev > 0) CU(cudaMemcpyAsync(c->zprev, z_prev, sizeof(float) * 2 * M_prev, cudaMemcpyDefault, c->st));
+    zp = c->zprev;
+    mp = M_prev;
+  } else if (c->M_z >= 0) {
+    zp = c->zlab;  // Z retained by the last update
+    mp = c->M_z;
+  }
+  int64_t J = c->p.births_per_step;
+  c->N = c->n_out + J;
+  block_of(c->N, c->world, c->rank, &c->g0, &c->n_local);
+  c->n_local -= c->g0;
+  PredictArgs a{};
+  a.n_local = c->n_local;
+  a.g0 = c->g0;
+  a.n_out = c->n_out;
+  a.J = J;
+  a.k = k;
+  a.seed = c->p.seed;
+  a.T = (float)c->p.T;
+  a.sigma_a = (float)c->p.sigma_a;
+  a.p_s = (float)c->p.p_s;
+  a.w_uniform = -1.0f;
+  a.meas = c->p.meas;
+  a.sigma_z0 = (float)c->p.sigma_z[0];
+  a.sigma_z1 = (float)c->p.sigma_z[1];
+  a.sensor_x = (float)c->p.sensor_xy[0];
+  a.sensor_y = (float)c->p.sensor_xy[1];
+  for (int i = 0; i < 4; ++i) a.region[i] = (float)c->p.region[i];
+  a.birth_w = J > 0 ? (float)(c->p.birth_mass / (double)J) : 0.0f;
+  a.birth_sigma_v = (float)c->p.birth_sigma_v;
+  a.zprev = zp;
+  a.m_prev = mp;
+  a.x = c->A[0];
+  a.vx = c->A[1];
+  a.y = c->A[2];
+  a.vy = c->A[3];
+  a.w = c->A[4];
+  a.rb = c->rb;
+  a.rb_stride = c->L.cap_l;
+  KL(launch_predict(a, c->st));
+  timing_record(c, 1);
+  c->stage = kPredicted;
+  return PHD_OK;
+}
+
+static void build_slots(phd_ctx* c, int M) {
+  // slot -> label map; range-bearing: measurements grouped by bearing class so
+  // that every f32x2 slot pair uses one bearing representation
+  int n = 0;
+  if (c->model == kRangeBearing) {
+    const float hp = 1.57079632679489662f;
+    for (int cls = 0; cls < 3; ++cls) {
+      for (int l = 0; l < M; ++l) {
+        float t = c->h_z[2 * l + 1];
+        int r = t > hp ? 1 : (t < -hp ? 2 : 0);
+        if (r == cls) c->h_slot[n++] = l;
+      }
+      if (n & 1) c->h_slot[n++] = -1;
+    }
+  } else {
+    for (int l = 0; l < M; ++l) c->h_slot[n++] = l;
+  }
+  c->n_slots = n;
+  int wz = (int)std::min<int64_t>(kMaxWarpsZ, std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), kZPerWarp)));
+  int zb = (int)ceil_div(std::max(n, 1), (int64_t)wz * kZPerWarp);
+  c->wz = wz;
+  c->zb = M > 0 ? zb : 0;
+  c->slots_pad = zb * wz * kZPerWarp;
+  for (int s = n; s < c->slots_pad; ++s) c->h_slot[s] = -1;
+}
+
+phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
+  if (!c) return PHD_EINVAL;
+  c->err.clear();
+  if (c->stage != kPredicted) return fail(c, PHD_ESTATE, "phd_update needs a predicted population");
+  if (M < 0 || M > c->p.max_meas) return fail(c, PHD_EINVAL, "M = %d outside [0, max_meas = %d]", M, c->p.max_meas);
+  if (M > 0 && !z) return fail(c, PHD_EINVAL, "z is NULL");
+  timing_record(c, 2);
+  c->M = M;
+  if (M > 0) {
+    cudaPointerAttributes pa{};
+    bool dev = cudaPointerGetAttributes(&pa, z) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    if (dev) {
+      CU(cudaMemcpyAsync(c->h_z, z, sizeof(float) * 2 * M, cudaMemcpyDeviceToHost, c->st));
+      CU(cudaStreamSynchronize(c->st));
+    } else {
+      memcpy(c->h_z, z, sizeof(float) * 2 * M);
+    }
+    CU(cudaMemcpyAsync(c->zlab, c->h_z, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, c->st));
+  }
+  c->M_z = M;
+  build_slots(c, M);
+  const int64_t n = c->n_local;
+  const int64_t tiles = ceil_div(n, kTileP);
+  if (M > 0) {
+    CU(cudaMemcpyAsync(c->slot_label, c->h_slot, sizeof(int32_t) * c->slots_pad, cudaMemcpyHostToDevice, c->st));
+    SlotConsts sc{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
+    KL(launch_zprep(c->model, c->zlab, c->slot_label, c->slots_pad, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->st));
+  }
+  // particle-CTA count: one wave of resident CTAs over the z-blocks
+  int gp = 0;
+  if (M > 0 && n > 0) {
+    int occ = std::max(1, std::min(pass_occupancy(c->model, 1, c->wz), pass_occupancy(c->model, 2, c->wz)));
+    int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / c->zb);
+    int64_t cap_gp = std::max<int64_t>(1, c->L.part_cap / c->slots_pad);
+    gp = (int)std::min<int64_t>(std::min(want, cap_gp), tiles);
+    int64_t tpc = ceil_div(tiles, gp);
+    gp = (int)ceil_div(tiles, tpc);
+  }
+  c->gp = gp;
+  PassArgs pa{};
+  pa.n = n;
+  pa.tiles_per_cta = gp > 0 ? ceil_div(tiles, gp) : 0;
+  pa.x = c->A[0];
+  pa.vx = c->A[1];
+  pa.y = c->A[2];
+  pa.vy = c->A[3];
+  pa.w = c->A[4];
+  pa.rb = c->rb;
+  pa.rb_stride = c->L.cap_l;
+  pa.sc = SlotConsts{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
+  pa.slots_pad = c->slots_pad;
+  pa.na0 = c->na0;
+  pa.na1 = c->na1;
+  pa.wscale = c->wscale;
+  pa.Cpart = c->Cpart;
+  pa.Apart = c->Apart;
+  pa.P = c->P;
+  pa.P_stride = c->L.cap_l;
+  CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
+  timing_record(c, 3);
+  if (M > 0) {
+    if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->st));
+    timing_record(c, 4);
+    KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, c->n_slots, c->slot_label, c->C, c->st));
+    if (gp == 0) CU(cudaMemsetAsync(c->C, 0, sizeof(double) * M, c->st));
+    if (c->world > 1) NC(ncclAllReduce(c->C, c->C, (size_t)M, ncclDouble, ncclSum, c->comm, c->st));
+    KL(launch_zconst(c->C, M, c->kappa, c->slot_label, c->slots_pad, c->s[4], c->D, c->bad, c->st));
+    timing_record(c, 5);
+    if (gp > 0) KL(launch_pass(c->model, 2, pa, gp, c->zb, c->wz, c->st));
+    timing_record(c, 6);
+  } else {
+    timing_record(c, 4);
+    timing_record(c, 5);
+    timing_record(c, 6);
+  }
+  int nbw = (int)ceil_div(n, kBlockW);
+  if (n > 0)
+    KL(launch_finalize(c->A[4], c->P, c->L.cap_l, M > 0 && gp > 0 ? c->zb : 0, n, c->nu, c->wscale, c->wn, c->blk_w, c->blk_wp, c->st));
+  double* rank_slots = c->acc + 5 * (size_t)M;
+  KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->n_slots : 0, c->slot_label, c->D, c->s[0], c->s[1],
+                       c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank, c->world, c->st));
+  if (M > 0 && gp == 0) CU(cudaMemsetAsync(c->acc, 0, sizeof(double) * 5 * M, c->st));
+  if (c->world > 1)
+    NC(ncclAllReduce(c->acc, c->acc, (size_t)(5 * M + 2 * c->world), ncclDouble, ncclSum, c->comm, c->st));
+  CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 2 * c->world, cudaMemcpyDeviceToHost, c->st));
+  CU(cudaMemcpyAsync(c->h_meta + 2 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
+  timing_record(c, 7);
+  CU(cudaStreamSynchronize(c->st));
+  c->W = 0.0;
+  c->W_pred = 0.0;
+  for (int r = 0; r < c->world; ++r) {
+    c->Wr[r] = c->h_meta[r];
+    c->Wpr[r] = c->h_meta[c->world + r];
+    c->W += c->Wr[r];
+    c->W_pred += c->Wpr[r];
+  }
+  c->bad_flag = reinterpret_cast<int*>(c->h_meta + 2 * c->world)[0];
+  c->LT = (int64_t)std::floor(c->W + 0.5);
+  if (c->LT < 0) c->LT = 0;
+  double frac = c->W - std::floor(c->W);
+  c->near_half = std::fabs(frac - 0.5) < 1e-4 * std::max(1.0, c->W);
+  c->stage = kUpdated;
+  if (c->timing) {
+    cudaEventElapsedTime(&c->t_ms[0], c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&c->t_ms[1], c->ev[3], c->ev[4]);
+    cudaEventElapsedTime(&c->t_ms[2], c->ev[5], c->ev[6]);
+    cudaEventElapsedTime(&c->t_ms[3], c->ev[2], c->ev[7]);
+  }
+  if (c->bad_flag || !std::isfinite(c->W) || !std::isfinite(c->W_pred))
+    return fail(c, PHD_EMODEL, "non-finite C/D/W (bad=%d, W=%g)", c->bad_flag, c->W);
+  return PHD_OK;
+}
+
+static int64_t next_count(phd_ctx* c, int* clamped) {
+  *clamped = 0;
+  if (c->p.count_mode == PHD_COUNT_FIXED) return c->p.fixed_count;
+  int64_t want = std::max<int64_t>(c->LT, 1) * c->p.particles_per_target;
+  int64_t lim = c->p.capacity - c->p.births_per_step;
+  if (want > lim) {
+    *clamped = 1;
+    want = lim;
+  }
+  return want;
+}
+
+phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s) {
+  if (!c) return PHD_EINVAL;
+  c->err.clear();
+  if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_extract needs an updated population");
+  int nest = 0;
+  int lt_clamped = 0;
+  if (c->rank == 0) {
+    timing_record(c, 8);
+    int capd = std::max(0, std::min(cap, c->p.max_meas));
+    KL(launch_extract(c->acc, c->M, c->acc + 5 * (size_t)c->M, c->world, c->p.p_d, c->est, capd, c->summ, nullptr, c->st));
+    CU(cudaMemcpyAsync(c->h_meta + 2 * c->world + 4, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    const double* sm = c->h_meta + 2 * c->world + 4;
+    nest = (int)sm[5];
+    lt_clamped = (int)sm[6];
+    if (nest > 0 && out) {
+      CU(cudaMemcpyAsync(c->h_est, c->est, sizeof(phd_estimate) * nest, cudaMemcpyDeviceToHost, c->st));
+      CU(cudaStreamSynchronize(c->st));
+      memcpy(out, c->h_est, sizeof(phd_estimate) * nest);
+    }
+    timing_record(c, 9);
+    if (c->timing) cudaEventElapsedTime(&c->t_ms[4], c->ev[8], c->ev[9]);
+  }
+  if (n_out) *n_out = nest;
+  if (s) {
+    int clamped;
+    s->W = c->W;
+    s->W_pred = c->W_pred;
+    s->undetected_mass = (1.0 - c->p.p_d) * c->W_pred;
+    s->LT = c->LT;
+    s->N = c->N;
+    s->N_out = next_count(c, &clamped);
+    s->M = c->M;
+    s->n_est = nest;
+    s->lt_clamped = lt_clamped;
+    s->count_clamped = clamped;
+    s->zero_mass = !(c->W > 0.0);
+    s->near_half = c->near_half;
+  }
+  return PHD_OK;
+}
+
+phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
+  if (!c) return PHD_EINVAL;
+  c->err.clear();
+  if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_resample_exchange needs an updated population");
+  timing_record(c, 10);
+  int clamped = 0;
+  const int64_t n_out = next_count(c, &clamped);
+  c->count_clamped = clamped;
+  const int64_t J = c->p.births_per_step;
+  U4 o = philox_at(c->p.seed, 0, (uint32_t)k, 3u);
+  const double U = u52(o.x, o.y);
+  const double W = c->W;
+  c->zero_mass = !(W > 0.0);
+  std::vector<int64_t> bounds(c->world + 1);
+  if (!c->zero_mass) {
+    phd_resample_bounds(c->world, c->Wr.data(), n_out, U, bounds.data(), nullptr);
+  } else {
+    // W == 0: offspring j copies particle floor(j N / n_out), produced by its owner
+    for (int r = 0; r <= c->world; ++r) {
+      int64_t lo, hi;
+      block_of(c->N, c->world, std::min(r, c->world - 1), &lo, &hi);
+      int64_t g = r == c->world ? c->N : lo;
+      bounds[r] = (int64_t)(((__int128)g * n_out + c->N - 1) / c->N);
+    }
+    bounds[c->world] = n_out;
+  }
+  const int64_t lo = bounds[c->rank], hi = bounds[c->rank + 1];
+  const int64_t nprod = hi - lo;
+  double O_r = 0.0;
+  for (int r = 0; r < c->rank; ++r) O_r += c->Wr[r];
+  const float w_off = n_out > 0 ? (float)(W / (double)n_out) : 0.0f;
+  const int64_t n = c->n_local;
+  const int nbw = (int)ceil_div(n, kBlockW);
+  const int nbo = (int)ceil_div(nprod, kBlockOff);
+  if (!c->zero_mass && nprod > 0) {
+    CU(cudaMemsetAsync(c->marks, 0xFF, sizeof(int32_t) * nprod, c->st));
+    KL(launch_scan_blocks(c->blk_w, nbw, c->blk_off, c->st));
+    ResampleArgs ra{};
+    ra.n_local = n;
+    ra.g0 = c->g0;
+    ra.w = c->wn;
+    ra.blk_off = c->blk_off;
+    ra.O_r = O_r;
+    ra.scale = (double)n_out / W;
+    ra.U = U;
+    ra.lo = lo;
+    ra.hi = hi;
+    ra.marks = c->marks;
+    KL(launch_resample_mark(ra, c->st));
+    KL(launch_block_max(c->marks, nprod, c->bmax, c->st));
+    KL(launch_scan_max(c->bmax, nbo, c->st));
+  }
+  KL(launch_gather(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, c->B[0], c->B[1],
+                   c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->N, n_out, c->st));
+  timing_record(c, 11);
+  // exchange: the next step's survivors [0, n_out) are block-partitioned over N' = n_out + J
+  if (c->world == 1) {
+    for (int i = 0; i < 5; ++i) std::swap(c->A[i], c->B[i]);
+    c->n_surv_local = n_out;
+  } else {
+    std::vector<int64_t> sc(c->world), so(c->world), rc(c->world), ro(c->world);
+    phd_plan_exchange(c->world, c->rank, bounds.data(), n_out, J, sc.data(), so.data(), rc.data(), ro.data());
+    // local part first (device copy), then the grouped peer transfers (C3)
+    if (sc[c->rank] > 0)
+      for (int i = 0; i < 5; ++i)
+        CU(cudaMemcpyAsync(c->A[i] + ro[c->rank], c->B[i] + so[c->rank], sizeof(float) * sc[c->rank],
+                           cudaMemcpyDeviceToDevice, c->st));
+    NC(ncclGroupStart());
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) continue;
+      for (int i = 0; i < 5; ++i) {
+        if (sc[q] > 0) NC(ncclSend(c->B[i] + so[q], (size_t)sc[q], ncclFloat, q, c->comm, c->st));
+        if (rc[q] > 0) NC(ncclRecv(c->A[i] + ro[q], (size_t)rc[q], ncclFloat, q, c->comm, c->st));
+      }
+    }
+    NC(ncclGroupEnd());
+    int64_t blo, bhi;
+    block_of(n_out + J, c->world, c->rank, &blo, &bhi);
+    c->n_surv_local = std::max<int64_t>(0, std::min(bhi, n_out) - std::min(blo, n_out));
+  }
+  timing_record(c, 12);
+  if (c->timing) {
+    cudaEventSynchronize(c->ev[12]);
+    cudaEventElapsedTime(&c->t_ms[5], c->ev[10], c->ev[11]);
+    cudaEventElapsedTime(&c->t_ms[6], c->ev[11], c->ev[12]);
+  }
+  c->U_last = U;
+  c->W_last = W;
+  c->N_out_last = n_out;
+  c->prod_first = lo;
+  c->prod_n = nprod;
+  c->n_out = n_out;
+  c->stage = kResampled;
+  return PHD_OK;
+}
+
+phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estimate* out, int32_t cap, int32_t* n_out,
+                    phd_summary* s) {
+  if (!c) return PHD_EINVAL;
+  timing_record(c, 13);
+  phd_status st = phd_predict(c, k, nullptr, 0);
+  if (st != PHD_OK) return st;
+  st = phd_update(c, z, M);
+  if (st != PHD_OK) return st;
+  st = phd_extract(c, out, cap, n_out, s);
+  if (st != PHD_OK) return st;
+  st = phd_resample_exchange(c, k);
+  timing_record(c, 14);
+  if (c->timing) {
+    cudaEventSynchronize(c->ev[14]);
+    cudaEventElapsedTime(&c->t_ms[7], c->ev[13], c->ev[14]);
+  }
+  return st;
+}
+
+phd_status phd_get_normalizers(phd_ctx* c, double* C, int32_t cap) {
+  if (!c || !C) return PHD_EINVAL;
+  if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "no update yet");
+  if (cap < c->M) return fail(c, PHD_EINVAL, "cap < M");
+  if (c->M > 0) CU(cudaMemcpyAsync(C, c->C, sizeof(double) * c->M, cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  return PHD_OK;
+}
+
+phd_status phd_get_accumulators(phd_ctx* c, double* acc, int32_t cap) {
+  if (!c || !acc) return PHD_EINVAL;
+  if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "no update yet");
+  if (cap < c->M) return fail(c, PHD_EINVAL, "cap < M");
+  if (c->M > 0) CU(cudaMemcpyAsync(acc, c->acc, sizeof(double) * 5 * c->M, cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  return PHD_OK;
+}
+
+phd_status phd_get_ancestors(phd_ctx* c, int32_t* anc, int64_t cap, int64_t* n, int64_t* first) {
+  if (!c || !anc) return PHD_EINVAL;
+  if (n) *n = c->prod_n;
+  if (first) *first = c->prod_first;
+  if (cap < c->prod_n) return fail(c, PHD_EINVAL, "cap < produced");
+  if (c->prod_n > 0) CU(cudaMemcpyAsync(anc, c->anc, sizeof(int32_t) * c->prod_n, cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  return PHD_OK;
+}
+
+phd_status phd_get_resample_meta(phd_ctx* c, double* W, double* U, int64_t* N_out, double* W_r) {
+  if (!c) return PHD_EINVAL;
+  if (W) *W = c->W_last;
+  if (U) *U = c->U_last;
+  if (N_out) *N_out = c->N_out_last;
+  if (W_r)
+    for (int r = 0; r < c->world; ++r) W_r[r] = c->Wr[r];
+  return PHD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Internal interface between the C-ABI orchestration (phd_api.cpp) and the
+// CUDA kernels (k_*.cu).  Not installed; not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace phd {
+
+// ---- tiling constants ----------------------------------------
+constexpr int kZPerLane = 4;                    // measurements per lane (2 f32x2 pairs)
+constexpr int kZPerWarp = 32 * kZPerLane;       // 128 measurement slots per warp
+constexpr int kMaxWarpsZ = 8;                   // warps per CTA (each owns 128 slots)
+constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one particle per loader thread
+constexpr int kTileP = 64;                      // particles per smem tile
+constexpr int kFlushTiles = 16;                 // fp32 mid-level -> fp64 every 16 tiles
+constexpr int kBlockW = 1024;                   // particles per finalize / scan block
+constexpr int kBlockOff = 1024;                 // offspring per gather block
+
+enum Model : int { kPosIso = 0, kPosAniso = 1, kRangeBearing = 2 };
+
+// Per-slot measurement constants, slot-major arrays of length slots_pad.
+// position: s0 = -z_x, s1 = -z_y; range-bearing: s0 = -z_r, s1 = -z_theta,
+// s2/s3 = -(centre x / y) of z in Cartesian, rep = bearing representation.
+struct SlotConsts {
+  float* s0;
+  float* s1;
+  float* s2;
+  float* s3;
+  float* d;        // 1 / (kappa + C) (fp32, 0 when D == 0)
+  int32_t* rep;    // range-bearing: 0 (-pi,pi], 1 [0,2pi), 2 (-2pi,0]
+};
+
+struct PassArgs {
+  int64_t n;                 // local particles
+  int64_t tiles_per_cta;
+  const float* x;
+  const float* vx;
+  const float* y;
+  const float* vy;
+  const float* w;
+  const float* rb;           // range-bearing repr [8][rb_stride]
+  int64_t rb_stride;
+  SlotConsts sc;
+  int slots_pad;             // stride of slot-major partials
+  float na0, na1;            // -alpha_0, -alpha_1 (log2 units)
+  float wscale;              // p_D * c, c = 1 / (2 pi sigma_0 sigma_1)
+  double* Cpart;             // [gp][slots_pad]
+  double* Apart;             // [gp][5][slots_pad]
+  float* P;                  // [zb][P_stride]
+  int64_t P_stride;
+};
+
+struct PredictArgs {
+  int64_t n_local;           // slots of this rank's block
+  int64_t g0;                // global index of local slot 0
+  int64_t n_out;             // global survivors (slots g < n_out are survivors)
+  int64_t J;                 // births per step
+  int32_t k;
+  uint64_t seed;
+  float T, sigma_a, p_s;
+  float w_uniform;           // >= 0: survivors' weight before predict; < 0: read w
+  int meas;
+  float sigma_z0, sigma_z1, sensor_x, sensor_y;
+  float region[4];
+  float birth_w, birth_sigma_v;
+  const float* zprev;        // device [m_prev][2]
+  int32_t m_prev;
+  float *x, *vx, *y, *vy, *w;
+  float* rb;                 // range-bearing repr out (nullptr for position)
+  int64_t rb_stride;
+};
+
+struct ResampleArgs {
+  int64_t n_local;
+  int64_t g0;
+  const float* w;            // updated weights
+  const double* blk_off;     // exclusive prefix of block sums (nb + 1 entries)
+  double O_r;                // exclusive prefix of the per-rank masses
+  double scale;              // n_out / W
+  double U;
+  int64_t lo, hi;            // bounds[r], bounds[r+1]
+  int32_t* marks;            // [hi - lo]
+};
+
+// ---- launchers (return cudaGetLastError of the launch) -----------------------
+cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s);
+cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, float sy, float* rb,
+                           int64_t stride, cudaStream_t s);
+cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad,
+                         float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s);
+cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, cudaStream_t s);
+int pass_occupancy(int model, int pass, int wz);
+cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
+                            double* C_lab, cudaStream_t s);
+cudaError_t launch_zconst(const double* C_lab, int M, double kappa, const int32_t* slot_label, int n_slots_pad,
+                          float* d_slot, double* D_lab, int* bad, cudaStream_t s);
+cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, int zb, int64_t n, float nu,
+                            float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s);
+cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
+                              const double* D_lab, const float* s0, const float* s1, const float* s2,
+                              const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
+                              double* acc_lab, double* rank_slots, int rank, int world, cudaStream_t s);
+cudaError_t launch_extract(const double* acc_lab, int M, const double* rank_slots, int world, double p_d,
+                           void* est /*phd_estimate*/, int cap, double* summary /*[8]*/, int32_t* keys_tmp,
+                           cudaStream_t s);
+cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s);
+cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s);
+cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cudaStream_t s);
+cudaError_t launch_scan_max(int32_t* bmax, int nb, cudaStream_t s);
+cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_t n, int64_t g0,
+                          const float* x, const float* vx, const float* y, const float* vy, float w_off,
+                          float* ox, float* ovx, float* oy, float* ovy, float* ow, int32_t* anc,
+                          int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out, cudaStream_t s);
+cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s);
+
+}  // namespace phd

@@ -1,0 +1,385 @@
+"""GPU parity: the CUDA path through the C-ABI vs the fp64 oracle, stage by
+stage on identical injected inputs (-m gpu).
+
+Tolerances (DESIGN.md §6 derives them):
+  predicted survivor states  |d| <= 5e-7 |ref| + 2e-6 (T^2/2 sigma_a + T sigma_a) + 1e-6
+  births                     |d| <= 1e-6 (|ref| + r_scale) + 1e-5
+  C(z)                       |d| <= 1e-5 C + 1e-9 kappa                  (north_star)
+  updated weights            |d| <= 1e-4 w' + 1e-7 w                      (north_star)
+  estimates zeta             |d| <= 1e-3 per component, matched labels   (north_star)
+  dW                         |d| <= 2e-5 dW + 1e-9
+  ancestors                  bit-exact except thresholds within 1e-9 of a cumsum boundary (counted)
+"""
+import math
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import scenario
+from scenario.configs import Model, POSITION, RANGE_BEARING, COUNT_FIXED, COUNT_ADAPTIVE
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def phd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1503_03769_b200 as p
+    p.load()
+    return p
+
+
+POS = Model(meas=POSITION, sigma_z=(10.0, 10.0), p_d=0.98, p_s=0.99, clutter_rate=50.0,
+            region=(-1000.0, 1000.0, -1000.0, 1000.0), births_per_step=256, fixed_count=8000,
+            count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=2048, seed=7)
+RB = Model(meas=RANGE_BEARING, sigma_z=(10.0, 0.01), p_d=0.98, p_s=0.99, clutter_rate=50.0,
+           region=(0.0, 2000.0, -math.pi, math.pi), sensor_xy=(0.0, 0.0), births_per_step=256,
+           fixed_count=8000, count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=2048, seed=7)
+ANISO = replace(POS, sigma_z=(7.0, 13.0))
+MODELS = {"position": POS, "range_bearing": RB, "aniso": ANISO}
+
+
+def _meas(model, M, seed):
+    z = scenario.random_measurements(M, seed, meas=model.meas, region=model.region)
+    if model.meas == RANGE_BEARING and M >= 4:
+        # measurements on / next to the bearing seam and the class boundaries
+        z[0, 1] = np.float32(math.pi - 1e-4)
+        z[1, 1] = np.float32(-math.pi + 1e-4)
+        z[2, 1] = np.float32(math.pi / 2)
+        z[3, 1] = np.float32(-math.pi / 2 - 1e-6)
+        z[:4, 0] = np.float32(600.0)
+    return z
+
+
+def _cloud(model, n, z, seed):
+    soa, w = scenario.clustered_particles(n, z, seed, meas=model.meas, sensor=model.sensor_xy,
+                                          box=(-1000.0, 1000.0, -1000.0, 1000.0))
+    return soa, w
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
+def test_predict_parity(phd, orc, mname):
+    m = MODELS[mname]
+    n_out, J = 5000 + 37, m.births_per_step
+    soa, w = scenario.random_particles(n_out, 3)
+    zprev = _meas(m, 23, 5)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, n_out)
+    f.predict(3, zprev)
+    gs, gw, g0 = f.get_particles()
+    assert g0 == 0 and gs.shape[1] == n_out + J
+    os_, ow = orc.predict(m, 3, soa, w)
+    T, sa = m.T, m.sigma_a
+    tol = 5e-7 * np.abs(os_) + 2e-6 * (0.5 * T * T * sa + T * sa) * 6 + 1e-6
+    assert np.all(np.abs(gs[:, :n_out] - os_) <= tol), np.max(np.abs(gs[:, :n_out] - os_) / tol)
+    assert np.allclose(gw[:n_out], ow, rtol=2e-7, atol=0)
+    bs, bw = orc.births(m, 3, n_out, J, zprev.astype(np.float64))
+    rscale = 0.0 if m.meas == POSITION else float(np.max(zprev[:, 0]))
+    tolb = 1e-6 * (np.abs(bs) + rscale) + 1e-5
+    assert np.all(np.abs(gs[:, n_out:] - bs) <= tolb), np.max(np.abs(gs[:, n_out:] - bs) / tolb)
+    assert np.allclose(gw[n_out:], bw, rtol=1e-7)
+    f.close()
+
+
+def test_births_uniform_first_step(phd, orc):
+    m = POS
+    f = phd.Filter(m)
+    soa, w = scenario.random_particles(1000, 1)
+    f.set_particles(soa, w, 1000)
+    f.predict(1)  # no previous Z: uniform births over the region
+    gs, _, _ = f.get_particles()
+    bs, _ = orc.births(m, 1, 1000, m.births_per_step, None)
+    assert np.all(np.abs(gs[:, 1000:] - bs) <= 1e-6 * np.abs(bs) + 1e-5)
+    f.close()
+
+
+def _update_case(phd, orc, m, n, M, seed, z=None, soa=None, w=None):
+    z = _meas(m, M, seed) if z is None else z
+    if soa is None:
+        soa, w = _cloud(m, n, z, seed)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+    f.update(z)
+    C = f.normalizers(len(z))
+    acc = f.accumulators(len(z))
+    _, wn, _ = f.get_particles()
+    est, summ = f.extract()
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    return f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco
+
+
+def _check_update(orc, m, C, acc, wn, w, Co, wo, acco):
+    kap = orc.kappa(m)
+    assert np.all(np.abs(C - Co) <= 1e-5 * Co + 1e-9 * kap), np.max(np.abs(C - Co) / (1e-5 * Co + 1e-9 * kap))
+    tw = 1e-4 * wo + 1e-7 * w
+    assert np.all(np.abs(wn - wo) <= tw), np.max(np.abs(wn - wo) / tw)
+    assert np.all(np.abs(acc[:, 0] - acco[:, 0]) <= 2e-5 * acco[:, 0] + 1e-9)
+    big = acco[:, 0] > 1e-6
+    zeta_g = acc[big, 1:] / acc[big, :1]
+    zeta_o = acco[big, 1:] / acco[big, :1]
+    assert np.all(np.abs(zeta_g - zeta_o) <= 1e-3), np.max(np.abs(zeta_g - zeta_o))
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing", "aniso"])
+@pytest.mark.parametrize("n,M", [(64 * 37 + 19, 37), (64 * 150 + 5, 130), (20011, 600), (9000, 1100)])
+def test_update_parity(phd, orc, mname, n, M):
+    m = MODELS[mname]
+    f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, n, M, seed=n + M)
+    _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
+    # mass identity (north_star): sum w' = (1 - pD) W + sum_z C/(kappa + C)
+    kap = orc.kappa(m)
+    rhs = (1 - m.p_d) * math.fsum(w.astype(np.float64)) + math.fsum(C / (kap + C))
+    assert abs(summ["W"] - rhs) <= 2e-6 * rhs
+    f.close()
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
+def test_extract_parity(phd, orc, mname):
+    m = replace(MODELS[mname], clutter_rate=5.0)
+    f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 12000, 300, seed=3)
+    W = math.fsum(wo)
+    eo = orc.extract(m, acco, W, math.fsum(w.astype(np.float64)))
+    assert summ["LT"] == eo["LT"] or summ["near_half"]
+    # stage-wise: the oracle's selection on the GPU accumulators is identical
+    eg = orc.extract(m, acc, summ["W"], summ["W_pred"])
+    assert list(est["labels"]) == list(eg["labels"])
+    assert np.allclose(est["states"], eg["states"], rtol=1e-6, atol=1e-4)
+    # end-to-end vs the all-oracle path: same label set except near-ties (S8)
+    n = min(len(eo["labels"]), len(est["labels"]))
+    ties = 0
+    for a, b in zip(est["labels"][:n], eo["labels"][:n]):
+        if a != b:
+            ties += 1
+            assert abs(acco[a, 0] - acco[b, 0]) <= 1e-5 * acco[b, 0]
+    assert ties <= 2
+    for i, lab in enumerate(est["labels"]):
+        j = list(eo["labels"]).index(lab) if lab in eo["labels"] else None
+        if j is not None:
+            assert np.all(np.abs(est["states"][i] - eo["states"][j]) <= 1e-3)
+    f.close()
+
+
+def _near_ties(w, U, n_out, tol=1e-9):
+    B = np.cumsum(np.asarray(w, np.float64))
+    W = B[-1]
+    t = (np.arange(n_out) + U) * W / n_out
+    idx = np.searchsorted(B, t)
+    d = np.full(n_out, np.inf)
+    for off in (-1, 0):
+        k = np.clip(idx + off, 0, len(B) - 1)
+        d = np.minimum(d, np.abs(B[k] - t))
+    return d <= tol
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
+def test_resample_parity(phd, orc, mname):
+    m = MODELS[mname]
+    f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 20011, 400, seed=11)
+    k = 4
+    f.resample_exchange(k)
+    anc, first = f.ancestors()
+    meta = f.resample_meta()
+    assert first == 0 and meta["N_out"] == m.fixed_count and len(anc) == m.fixed_count
+    assert meta["U"] == orc.resample_U(m.seed, k)
+    ao, Wo = orc.resample(wn.astype(np.float64), meta["U"], meta["N_out"])
+    ties = _near_ties(wn, meta["U"], meta["N_out"])
+    mism = anc != ao
+    assert np.all(ties[mism]), int(np.sum(mism & ~ties))
+    assert np.all(np.diff(anc) >= 0)
+    # offspring states are the ancestors' predicted states; weights W / N_out
+    gs, gw, _ = f.get_particles()
+    assert np.array_equal(gs[:, :len(anc)], soa[:, anc])
+    assert np.allclose(gw[:len(anc)], np.float32(summ["W"] / meta["N_out"]))
+    f.close()
+
+
+def test_zero_mass_and_empty_measurements(phd, orc):
+    m = POS
+    soa, w = scenario.random_particles(3000, 2)
+    w[:] = 0
+    f = phd.Filter(m)
+    f.set_particles(soa, w, 3000, stage=phd.STAGE_PREDICTED)
+    f.update(np.zeros((0, 2), np.float32))
+    est, summ = f.extract()
+    assert summ["W"] == 0 and summ["zero_mass"] == 1 and len(est["labels"]) == 0
+    f.resample_exchange(2)
+    anc, _ = f.ancestors()
+    assert np.array_equal(anc, (np.arange(m.fixed_count) * 3000) // m.fixed_count)
+    f.close()
+
+
+def test_empty_measurements_weights(phd, orc):
+    m = POS
+    soa, w = scenario.random_particles(4097, 5)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, 4097, stage=phd.STAGE_PREDICTED)
+    f.update(np.zeros((0, 2), np.float32))
+    _, wn, _ = f.get_particles()
+    assert np.allclose(wn, (1 - m.p_d) * w, rtol=1e-6)
+    f.close()
+
+
+def test_far_measurement_and_pd_zero(phd, orc):
+    m0 = replace(POS, p_d=0.0)
+    z = np.array([[10.0, 20.0], [5000.0, 5000.0]], np.float32)
+    f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m0, 3000, 2, 1, z=z)
+    assert np.all(C == 0) and np.allclose(wn, w) and len(est["labels"]) == 0
+    f.close()
+    mk = replace(POS, clutter_rate=0.0)  # kappa = 0: far measurement has D = 0 -> term 0
+    soa, w = _cloud(mk, 3000, z[:1], 1)  # no particle near the far measurement
+    f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, mk, 3000, 2, 1, z=z, soa=soa, w=w)
+    assert C[1] == 0 and np.all(np.isfinite(wn)) and acc[1, 0] == 0
+    _check_update(orc, mk, C, acc, wn, w, Co, wo, acco)
+    f.close()
+
+
+def test_small_population_and_max_meas(phd, orc):
+    m = replace(POS, max_meas=2048)
+    for n in [1, 5, 63, 65]:
+        f, *r = _update_case(phd, orc, m, n, 9, seed=n)
+        z, soa, w, C, acc, wn, est, summ, Co, wo, acco = r
+        _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
+        f.close()
+    f, *r = _update_case(phd, orc, m, 700, 2048, seed=3)
+    z, soa, w, C, acc, wn, est, summ, Co, wo, acco = r
+    _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
+    f.close()
+
+
+def test_errors_and_state_machine(phd):
+    m = POS
+    f = phd.Filter(m)
+    with pytest.raises(phd.PhdError) as e:
+        f.update(np.zeros((3, 2), np.float32))
+    assert e.value.status == 2  # PHD_ESTATE before any population
+    soa, w = scenario.random_particles(100, 1)
+    f.set_particles(soa, w, 100)
+    with pytest.raises(phd.PhdError) as e:
+        f.resample_exchange(1)
+    assert e.value.status == 2
+    f.predict(1)
+    with pytest.raises(phd.PhdError) as e:
+        f.update(np.zeros((m.max_meas + 1, 2), np.float32))
+    assert e.value.status == 1
+    with pytest.raises(phd.PhdError) as e:
+        f.set_particles(soa[:, :10], w[:10], 100)  # n_local mismatch
+    assert e.value.status == 1
+    f.close()
+
+
+# ---------------------------------------------------------------------------
+# Full filter steps, stage-wise injection (configs 1 and 2 at their real sizes)
+@pytest.mark.parametrize("cname,steps", [("cfg1", 20), ("cfg2", 8)])
+def test_filter_steps_stagewise(phd, orc, cname, steps):
+    cfg = scenario.get(cname)
+    m = cfg.model
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1])
+    prev_soa, prev_w = soa, w
+    zprev = None
+    for k in range(1, steps + 1):
+        z = Z[k - 1]
+        f.predict(k)
+        ps, pw, _ = f.get_particles()
+        n_surv = prev_soa.shape[1]
+        os_, ow = orc.predict(m, k, prev_soa, prev_w)
+        assert np.all(np.abs(ps[:, :n_surv] - os_) <= 5e-7 * np.abs(os_) + 7e-5)
+        bs, _ = orc.births(m, k, n_surv, m.births_per_step, None if zprev is None else zprev.astype(np.float64))
+        rscale = 0.0 if m.meas == POSITION else 2000.0
+        assert np.all(np.abs(ps[:, n_surv:] - bs) <= 1e-6 * (np.abs(bs) + rscale) + 1e-5)
+        f.update(z)
+        C = f.normalizers(len(z))
+        acc = f.accumulators(len(z))
+        _, wn, _ = f.get_particles()
+        Co = orc.normalizers(m, ps, pw, z)
+        wo, acco = orc.update(m, ps, pw, z, Co)
+        _check_update(orc, m, C, acc, wn, pw, Co, wo, acco)
+        est, summ = f.extract()
+        eg = orc.extract(m, acc, summ["W"], summ["W_pred"])
+        assert list(est["labels"]) == list(eg["labels"])
+        f.resample_exchange(k)
+        anc, _ = f.ancestors()
+        meta = f.resample_meta()
+        ao, _ = orc.resample(wn.astype(np.float64), meta["U"], meta["N_out"])
+        assert meta["N_out"] == (m.fixed_count if m.count_mode == COUNT_FIXED else
+                                 min(max(summ["LT"], 1) * m.particles_per_target, m.capacity - m.births_per_step))
+        ties = _near_ties(wn, meta["U"], meta["N_out"])
+        assert np.all(ties[anc != ao])
+        prev_soa, prev_w, _ = f.get_particles()
+        assert np.array_equal(prev_soa, ps[:, anc])
+        zprev = z
+    f.close()
+
+
+def test_step_equals_staged_calls(phd):
+    cfg = scenario.get("cfg1")
+    m = cfg.model
+    Z = scenario.measurements(cfg)
+    soa, w = scenario.initial_population(cfg)
+    fa, fb = phd.Filter(m), phd.Filter(m)
+    fa.set_particles(soa, w, soa.shape[1])
+    fb.set_particles(soa, w, soa.shape[1])
+    for k in range(1, 6):
+        fa.step(k, Z[k - 1])
+        ea = fa._estimates()
+        fb.predict(k)
+        fb.update(Z[k - 1])
+        eb, _ = fb.extract()
+        fb.resample_exchange(k)
+        assert np.array_equal(ea["labels"], eb["labels"]) and np.array_equal(ea["states"], eb["states"])
+    sa, wa, _ = fa.get_particles()
+    sb, wb, _ = fb.get_particles()
+    assert np.array_equal(sa, sb) and np.array_equal(wa, wb)
+    fa.close()
+    fb.close()
+
+
+# ---------------------------------------------------------------------------
+# Full size (cfg 5, the bench launch configuration): sampled outputs + properties
+def test_full_size_cfg5_sampled(phd, orc):
+    cfg = scenario.get("cfg5")
+    m = cfg.model
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1])
+    f.predict(1)
+    ps, pw, _ = f.get_particles()
+    f.update(Z[0])
+    M = len(Z[0])
+    C = f.normalizers(M)
+    acc = f.accumulators(M)
+    _, wn, _ = f.get_particles()
+    est, summ = f.extract()
+    kap = orc.kappa(m)
+    N = ps.shape[1]
+    assert N == 1 << 24 and M == 4096
+    # sampled normalisers: the oracle sums all 2^24 particles for 3 measurements
+    rng = np.random.default_rng(0)
+    for p in rng.choice(M, 3, replace=False):
+        Co = orc.normalizers(m, ps, pw, Z[0][p:p + 1])[0]
+        assert abs(C[p] - Co) <= 1e-5 * Co + 1e-9 * kap
+    # sampled weights: w'_i from the oracle formula with the GPU's (all-particle) C
+    idx = np.concatenate([rng.choice(N, 64, replace=False), np.argsort(wn)[-64:]])
+    wo, _ = orc.update(m, ps[:, idx], pw[idx], Z[0], C)
+    assert np.all(np.abs(wn[idx] - wo) <= 1e-4 * wo + 1e-7 * pw[idx])
+    # mass identity at full size
+    rhs = (1 - m.p_d) * summ["W_pred"] + math.fsum(C / (kap + C))
+    assert abs(summ["W"] - rhs) <= 1e-5 * rhs
+    f.resample_exchange(1)
+    anc, _ = f.ancestors()
+    meta = f.resample_meta()
+    assert len(anc) == m.fixed_count and np.all(np.diff(anc) >= 0)
+    counts = np.bincount(anc, minlength=N)
+    share = meta["N_out"] * wn.astype(np.float64) / meta["W"]
+    assert np.all(counts >= np.floor(share) - 1) and np.all(counts <= np.ceil(share) + 1)
+    f.close()
