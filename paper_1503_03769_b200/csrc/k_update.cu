@@ -83,7 +83,7 @@ struct TileLoader {
         reinterpret_cast<float4*>(d)[1] = make_float4(v[r][2], v[r][2], v[r][3], v[r][3]);
         reinterpret_cast<float4*>(d)[2] = make_float4(v[r][4], v[r][4], v[r][5], v[r][5]);
         reinterpret_cast<float4*>(d)[3] = make_float4(v[r][6], v[r][6], v[r][7], v[r][7]);
-        float wc = v[r][8] * wscale;
+        float wc = PASS == 1 ? v[r][8] * wscale : log2f(v[r][8] * wscale);
         reinterpret_cast<float4*>(d)[4] = make_float4(wc, wc, 0.0f, 0.0f);
         if (PASS == 2) {
           reinterpret_cast<float4*>(d)[5] = make_float4(v[r][9], v[r][9], v[r][10], v[r][10]);
@@ -91,7 +91,7 @@ struct TileLoader {
         }
       } else {
         reinterpret_cast<float4*>(d)[0] = make_float4(v[r][0], v[r][0], v[r][1], v[r][1]);
-        float wc = v[r][2] * wscale;
+        float wc = PASS == 1 ? v[r][2] * wscale : log2f(v[r][2] * wscale);
         if (PASS == 2) {
           reinterpret_cast<float4*>(d)[1] = make_float4(v[r][3], v[r][3], v[r][4], v[r][4]);
           reinterpret_cast<float4*>(d)[2] = make_float4(wc, wc, 0.0f, 0.0f);
@@ -103,17 +103,17 @@ struct TileLoader {
   }
 };
 
-// Per-lane measurement constants for its two slot pairs.
-template <int MODEL, int PASS>
+// Per-lane measurement constants for its NP slot pairs.
+template <int MODEL, int PASS, int NP>
 struct LaneZ {
-  float2 n0[2], n1[2];  // -z components
-  float2 d[2];          // 1/(kappa + C)   (pass 2)
-  float2 c0[2], c1[2];  // -(Cartesian centre) (range-bearing, pass 2)
-  int roff[2];          // bearing-representation offset in the record (range-bearing)
+  float2 n0[NP], n1[NP];  // -z components
+  float2 d[NP];           // 1/(kappa + C)   (pass 2)
+  float2 c0[NP], c1[NP];  // -(Cartesian centre) (range-bearing, pass 2)
+  int roff[NP];           // bearing-representation offset in the record (range-bearing)
 
   __device__ __forceinline__ void load(const PassArgs& a, int slot0) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NP; ++j) {
       int s = slot0 + 2 * j;
       n0[j] = f2(a.sc.s0[s], a.sc.s0[s + 1]);
       n1[j] = f2(a.sc.s1[s], a.sc.s1[s + 1]);
@@ -129,22 +129,24 @@ struct LaneZ {
   }
 };
 
-// Quadratic form in log2 units: a = -(alpha0 d0^2 + alpha1 d1^2).
+// Pass-1 exponent: a = -(alpha0 d0^2 + alpha1 d1^2) (log2 units).
+// Pass-2 exponent: the same plus lw = log2(p_D c w_i) folded into the last FFMA,
+// so that 2^a is directly u = p_D g w (one FMUL per pair saved).
 template <int MODEL>
-__device__ __forceinline__ float2 expo(float2 d0, float2 d1, float2 na0, float2 na1) {
+__device__ __forceinline__ float2 expo(float2 d0, float2 d1, float2 na0, float2 na1, float2 base) {
   if (MODEL == kPosIso) {
     float2 q = __fmul2_rn(d0, d0);
     q = __ffma2_rn(d1, d1, q);
-    return __fmul2_rn(q, na0);
+    return __ffma2_rn(q, na0, base);
   } else {
-    float2 q = __fmul2_rn(__fmul2_rn(d0, d0), na0);
+    float2 q = __ffma2_rn(__fmul2_rn(d0, d0), na0, base);
     return __ffma2_rn(__fmul2_rn(d1, d1), na1, q);
   }
 }
 
 // Residuals (d0, d1) of the lane's slot pair j against the broadcast particle.
-template <int MODEL, int PASS>
-__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS>& z, int j, float2& d0,
+template <int MODEL, int PASS, int NP>
+__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS, NP>& z, int j, float2& d0,
                                          float2& d1) {
   if (MODEL == kRangeBearing) {
     float4 R = *reinterpret_cast<const float4*>(rec);
@@ -184,30 +186,32 @@ __device__ __forceinline__ float transpose_reduce8(float (&v)[8], int lane) {
   return v[0];
 }
 
-template <int MODEL, int PASS>
-__global__ void __launch_bounds__(256, 2) k_pass(const PassArgs a) {
+// ZL = measurement slots per lane (4 or 8); the CTA covers wz * 32 * ZL slots.
+template <int MODEL, int PASS, int ZL>
+__global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a) {
   using L = RecLayout<MODEL, PASS>;
-  constexpr int NQ = PASS == 1 ? 1 : 5;
+  constexpr int NQ = PASS == 1 ? 1 : 4;  // pass 2: S'x, Svx, S'y, Svy (dW = C/D from pass 1)
+  constexpr int NP = ZL / 2;
   extern __shared__ __align__(16) float smem[];
   const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, wz = nthr >> 5;
   float* recs = smem;                                   // [2][kTileP][WIDTH]
   float* psum = recs + 2 * kTileP * L::WIDTH;            // [2][wz][kTileP] (pass 2)
+  // fp64 accumulators per lane slot in shared memory, [NQ*ZL][nthr] (conflict-free)
+  double* out64 = reinterpret_cast<double*>(psum + (PASS == 2 ? 2 * wz * kTileP : 0));
 
   const int zb = blockIdx.y;
-  const int slot0 = (zb * wz + warp) * kZPerWarp + lane * kZPerLane;
-  LaneZ<MODEL, PASS> z;
+  const int slot0 = (zb * wz + warp) * (32 * ZL) + lane * ZL;
+  LaneZ<MODEL, PASS, NP> z;
   z.load(a, slot0);
   const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
 
-  float2 in[NQ][2], mid[NQ][2];
+  float2 in[NQ][NP];
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) in[q][j] = mid[q][j] = f2(0.0f, 0.0f);
-  // fp64 outer accumulators live in shared memory, [NQ*4][nthr] (conflict-free)
-  double* out64 = reinterpret_cast<double*>(psum + (PASS == 2 ? 2 * wz * kTileP : 0));
+    for (int j = 0; j < NP; ++j) in[q][j] = f2(0.0f, 0.0f);
 #pragma unroll
-  for (int q = 0; q < NQ * 4; ++q) out64[q * nthr + tid] = 0.0;
+  for (int q = 0; q < NQ * ZL; ++q) out64[q * nthr + tid] = 0.0;
 
   const int64_t ntiles = (a.n + kTileP - 1) / kTileP;
   const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
@@ -232,29 +236,29 @@ __global__ void __launch_bounds__(256, 2) k_pass(const PassArgs a) {
 #pragma unroll
       for (int pp = 0; pp < 8; ++pp) {
         const float* rec = rb + (p0 + pp) * L::WIDTH;
-        const float2 wc = *reinterpret_cast<const float2*>(rec + L::WC);
+        // pass 1: (p_D c w, .); pass 2: (log2(p_D c w), .)
+        const float2 wv = *reinterpret_cast<const float2*>(rec + L::WC);
         float2 pacc = f2(0.0f, 0.0f);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NP; ++j) {
           float2 d0, d1;
-          residual<MODEL, PASS>(rec, z, j, d0, d1);
-          const float2 e = ex2v(expo<MODEL>(d0, d1, na0, na1));
+          residual<MODEL, PASS, NP>(rec, z, j, d0, d1);
           if (PASS == 1) {
-            in[0][j] = __ffma2_rn(e, wc, in[0][j]);
+            const float2 e = ex2v(expo<MODEL>(d0, d1, na0, na1, f2(0.0f, 0.0f)));
+            in[0][j] = __ffma2_rn(e, wv, in[0][j]);
           } else {
-            const float2 u = __fmul2_rn(e, wc);
-            pacc = __ffma2_rn(e, z.d[j], pacc);
+            const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
+            pacc = __ffma2_rn(u, z.d[j], pacc);
             if (MODEL == kRangeBearing) {
               const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
               d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
               d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
             }
             const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
-            in[0][j] = __fadd2_rn(in[0][j], u);
-            in[1][j] = __ffma2_rn(u, d0, in[1][j]);
-            in[2][j] = __ffma2_rn(u, f2(V.x, V.y), in[2][j]);
-            in[3][j] = __ffma2_rn(u, d1, in[3][j]);
-            in[4][j] = __ffma2_rn(u, f2(V.z, V.w), in[4][j]);
+            in[0][j] = __ffma2_rn(u, d0, in[0][j]);
+            in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+            in[2][j] = __ffma2_rn(u, d1, in[2][j]);
+            in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
           }
         }
         pe[pp] = pacc.x + pacc.y;
@@ -266,11 +270,13 @@ __global__ void __launch_bounds__(256, 2) k_pass(const PassArgs a) {
     }
 
     if (more) ld.store(recs + (buf ^ 1) * kTileP * L::WIDTH, a.wscale, tid, nthr);
+    // tile sums (<= 64 particles in fp32) -> fp64
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        mid[q][j] = __fadd2_rn(mid[q][j], in[q][j]);
+      for (int j = 0; j < NP; ++j) {
+        out64[(q * ZL + 2 * j) * nthr + tid] += (double)in[q][j].x;
+        out64[(q * ZL + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
         in[q][j] = f2(0.0f, 0.0f);
       }
     __syncthreads();
@@ -286,75 +292,76 @@ __global__ void __launch_bounds__(256, 2) k_pass(const PassArgs a) {
         }
       }
     }
-    if (((t - t_begin + 1) % kFlushTiles) == 0) {
-#pragma unroll
-      for (int q = 0; q < NQ; ++q)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          out64[(4 * q + 2 * j) * nthr + tid] += (double)mid[q][j].x;
-          out64[(4 * q + 2 * j + 1) * nthr + tid] += (double)mid[q][j].y;
-          mid[q][j] = f2(0.0f, 0.0f);
-        }
-    }
   }
   const int64_t base = (int64_t)blockIdx.x * NQ * a.slots_pad;
   double* dst = PASS == 1 ? a.Cpart : a.Apart;
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      dst[base + (int64_t)q * a.slots_pad + slot0 + 2 * j] = out64[(4 * q + 2 * j) * nthr + tid] + (double)mid[q][j].x;
-      dst[base + (int64_t)q * a.slots_pad + slot0 + 2 * j + 1] =
-          out64[(4 * q + 2 * j + 1) * nthr + tid] + (double)mid[q][j].y;
-    }
+    for (int m = 0; m < ZL; ++m) dst[base + (int64_t)q * a.slots_pad + slot0 + m] = out64[(q * ZL + m) * nthr + tid];
 }
 
-template <int MODEL, int PASS>
+template <int MODEL, int PASS, int ZL>
 static size_t pass_smem(int wz) {
   using L = RecLayout<MODEL, PASS>;
   size_t b = sizeof(float) * 2 * kTileP * L::WIDTH;
   if (PASS == 2) b += sizeof(float) * 2 * wz * kTileP;
-  b += sizeof(double) * (PASS == 1 ? 4 : 20) * wz * 32;
+  b += sizeof(double) * (PASS == 1 ? 1 : 4) * ZL * wz * 32;
   return b;
 }
 
-template <int MODEL, int PASS>
-static cudaError_t launch_one(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+template <int MODEL, int PASS, int ZL>
+static void set_attr() {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_pass<MODEL, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)pass_smem<MODEL, PASS>(kMaxWarpsZ));
+    cudaFuncSetAttribute(k_pass<MODEL, PASS, ZL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pass_smem<MODEL, PASS, ZL>(kMaxWarpsZ));
     attr = true;
   }
+}
+
+template <int MODEL, int PASS, int ZL>
+static cudaError_t launch_one(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+  set_attr<MODEL, PASS, ZL>();
   dim3 grid((unsigned)gp, (unsigned)zb);
-  k_pass<MODEL, PASS><<<grid, wz * 32, pass_smem<MODEL, PASS>(wz), s>>>(a);
+  k_pass<MODEL, PASS, ZL><<<grid, wz * 32, pass_smem<MODEL, PASS, ZL>(wz), s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
-  if (gp <= 0 || zb <= 0) return cudaSuccess;
-  if (model == kPosIso) return pass == 1 ? launch_one<kPosIso, 1>(a, gp, zb, wz, s) : launch_one<kPosIso, 2>(a, gp, zb, wz, s);
-  if (model == kPosAniso) return pass == 1 ? launch_one<kPosAniso, 1>(a, gp, zb, wz, s) : launch_one<kPosAniso, 2>(a, gp, zb, wz, s);
-  return pass == 1 ? launch_one<kRangeBearing, 1>(a, gp, zb, wz, s) : launch_one<kRangeBearing, 2>(a, gp, zb, wz, s);
+template <int MODEL, int ZL>
+static cudaError_t launch_m(int pass, const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+  return pass == 1 ? launch_one<MODEL, 1, ZL>(a, gp, zb, wz, s) : launch_one<MODEL, 2, ZL>(a, gp, zb, wz, s);
 }
 
-template <int MODEL, int PASS>
+template <int ZL>
+static cudaError_t launch_z(int model, int pass, const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+  if (model == kPosIso) return launch_m<kPosIso, ZL>(pass, a, gp, zb, wz, s);
+  if (model == kPosAniso) return launch_m<kPosAniso, ZL>(pass, a, gp, zb, wz, s);
+  return launch_m<kRangeBearing, ZL>(pass, a, gp, zb, wz, s);
+}
+
+cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s) {
+  if (gp <= 0 || zb <= 0) return cudaSuccess;
+  return zl == 8 ? launch_z<8>(model, pass, a, gp, zb, wz, s) : launch_z<4>(model, pass, a, gp, zb, wz, s);
+}
+
+template <int MODEL, int PASS, int ZL>
 static int occ_one(int wz) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_pass<MODEL, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)pass_smem<MODEL, PASS>(kMaxWarpsZ));
-    attr = true;
-  }
+  set_attr<MODEL, PASS, ZL>();
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<MODEL, PASS>, wz * 32, pass_smem<MODEL, PASS>(wz));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<MODEL, PASS, ZL>, wz * 32, pass_smem<MODEL, PASS, ZL>(wz));
   return n;
 }
 
-int pass_occupancy(int model, int pass, int wz) {
-  if (model == kPosIso) return pass == 1 ? occ_one<kPosIso, 1>(wz) : occ_one<kPosIso, 2>(wz);
-  if (model == kPosAniso) return pass == 1 ? occ_one<kPosAniso, 1>(wz) : occ_one<kPosAniso, 2>(wz);
-  return pass == 1 ? occ_one<kRangeBearing, 1>(wz) : occ_one<kRangeBearing, 2>(wz);
+template <int ZL>
+static int occ_z(int model, int pass, int wz) {
+  if (model == kPosIso) return pass == 1 ? occ_one<kPosIso, 1, ZL>(wz) : occ_one<kPosIso, 2, ZL>(wz);
+  if (model == kPosAniso) return pass == 1 ? occ_one<kPosAniso, 1, ZL>(wz) : occ_one<kPosAniso, 2, ZL>(wz);
+  return pass == 1 ? occ_one<kRangeBearing, 1, ZL>(wz) : occ_one<kRangeBearing, 2, ZL>(wz);
+}
+
+int pass_occupancy(int model, int pass, int wz, int zl) {
+  return zl == 8 ? occ_z<8>(model, pass, wz) : occ_z<4>(model, pass, wz);
 }
 
 // ---------------------------------------------------------------------------
@@ -460,7 +467,7 @@ __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, c
       float wi = w[i];
       float s = 0.0f;
       for (int k = 0; k < zb; ++k) s += P[(int64_t)k * P_stride + i];
-      float wn = wi * nu + (wi * wscale) * s;
+      float wn = wi * nu + s;  // P carries p_D c w (pass 2 folds log2 w into the exponent)
       w_out[i] = wn;
       a += (double)wn;
       b += (double)wi;
@@ -496,16 +503,18 @@ cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, in
 }
 
 // STPHD accumulators in label order (Eqs 16, 18):
-//   dW = A0 / D,  Sx = A1 / D + cx dW,  Svx = A2 / D,  Sy = A3 / D + cy dW,  Svy = A4 / D
+//   dW = C / D  (Eq 16 summed over i is exactly C_p/(kappa + C_p), the north_star identity),
+//   Sx = A0 / D + cx dW,  Svx = A1 / D,  Sy = A2 / D + cy dW,  Svy = A3 / D
 // with (cx, cy) the centre the kernel subtracted (the measurement itself for
 // the position sensor).  The last CTA reduces the per-block masses into this
 // rank's W_r and W_pred_r and writes them into the all-reduce buffer.
 __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots_pad, int n_slots,
-                             const int32_t* __restrict__ slot_label, const double* __restrict__ D_lab,
-                             const float* __restrict__ s0, const float* __restrict__ s1,
-                             const float* __restrict__ s2, const float* __restrict__ s3, int model,
-                             const double* __restrict__ blk_w, const double* __restrict__ blk_wp, int nb,
-                             double* acc_lab, double* rank_slots, int rank, int world) {
+                             const int32_t* __restrict__ slot_label, const double* __restrict__ C_lab,
+                             const double* __restrict__ D_lab, const float* __restrict__ s0,
+                             const float* __restrict__ s1, const float* __restrict__ s2,
+                             const float* __restrict__ s3, int model, const double* __restrict__ blk_w,
+                             const double* __restrict__ blk_wp, int nb, double* acc_lab, double* rank_slots,
+                             int rank, int world) {
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double sa[256], sb[256];
     double a = 0.0, b = 0.0;
@@ -535,11 +544,11 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
   if (s >= n_slots) return;
   int lab = slot_label[s];
   if (lab < 0) return;
-  double A[5] = {0, 0, 0, 0, 0};
+  double A[4] = {0, 0, 0, 0};
   for (int b = 0; b < gp; ++b) {
-    const double* p = Apart + (int64_t)b * 5 * slots_pad + s;
+    const double* p = Apart + (int64_t)b * 4 * slots_pad + s;
 #pragma unroll
-    for (int q = 0; q < 5; ++q) A[q] += p[(int64_t)q * slots_pad];
+    for (int q = 0; q < 4; ++q) A[q] += p[(int64_t)q * slots_pad];
   }
   double D = D_lab[lab];
   double inv = D > 0.0 ? 1.0 / D : 0.0;
@@ -551,21 +560,21 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
     cx = -(double)s0[s];
     cy = -(double)s1[s];
   }
-  double dW = A[0] * inv;
+  double dW = C_lab[lab] * inv;
   double* o = acc_lab + 5 * (int64_t)lab;
   o[0] = dW;
-  o[1] = A[1] * inv + cx * dW;
-  o[2] = A[2] * inv;
-  o[3] = A[3] * inv + cy * dW;
-  o[4] = A[4] * inv;
+  o[1] = A[0] * inv + cx * dW;
+  o[2] = A[1] * inv;
+  o[3] = A[2] * inv + cy * dW;
+  o[4] = A[3] * inv;
 }
 
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
-                              const double* D_lab, const float* s0, const float* s1, const float* s2,
-                              const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
-                              double* acc_lab, double* rank_slots, int rank, int world, cudaStream_t s) {
+                              const double* C_lab, const double* D_lab, const float* s0, const float* s1,
+                              const float* s2, const float* s3, int model, const double* blk_w, const double* blk_wp,
+                              int nb, double* acc_lab, double* rank_slots, int rank, int world, cudaStream_t s) {
   int blocks = (n_slots + 255) / 256 + 1;
-  k_reduce_acc<<<blocks, 256, 0, s>>>(Apart, gp, slots_pad, n_slots, slot_label, D_lab, s0, s1, s2, s3, model,
+  k_reduce_acc<<<blocks, 256, 0, s>>>(Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
                                       blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world);
   return cudaGetLastError();
 }

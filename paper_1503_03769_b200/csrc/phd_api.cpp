@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -51,9 +52,9 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.cap_g = p->capacity;
   L.cap_l = align_up((size_t)(ceil_div(p->capacity, world) + 1), kBlockW);
   L.cap_off = align_up((size_t)p->capacity, kBlockOff);
-  L.slots_max = (int)align_up((size_t)p->max_meas + 2, 1024);
+  L.slots_max = (int)align_up((size_t)p->max_meas + 2, 2048);
   L.zb_max = std::max(1, L.slots_max / 1024);
-  L.part_cap = (int64_t)64 * sms * 128 + 8192;
+  L.part_cap = (int64_t)64 * sms * 256 + 8192;
   L.nbw_max = ceil_div(L.cap_l, kBlockW) + 1;
   L.nbo_max = ceil_div(L.cap_off, kBlockOff) + 1;
   size_t off = 0;
@@ -68,7 +69,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_rb = take(p->meas == PHD_MEAS_RANGE_BEARING ? sizeof(float) * 8 * L.cap_l : 256);
   L.o_P = take(sizeof(float) * (size_t)L.zb_max * L.cap_l);
   L.o_Cpart = take(sizeof(double) * L.part_cap);
-  L.o_Apart = take(sizeof(double) * 5 * L.part_cap);
+  L.o_Apart = take(sizeof(double) * 4 * L.part_cap);
   L.o_zlab = take(sizeof(float) * 2 * (size_t)(p->max_meas + 1));
   L.o_zprev = take(sizeof(float) * 2 * (size_t)(p->max_meas + 1));
   L.o_slot = take(sizeof(int32_t) * L.slots_max);
@@ -135,7 +136,7 @@ struct phd_ctx {
   int64_t N = 0;          // global particles of the predicted/updated array
   int64_t n_local = 0, g0 = 0;
   int64_t n_surv_local = 0;
-  int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zb = 0, gp = 0, M_z = -1;
+  int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zl = 4, zb = 0, gp = 0, M_z = -1;
   int m_prev_ext = -1;   // >= 0: zprev holds an explicit Z_{k-1} of this size
   double W = 0, W_pred = 0;
   int64_t LT = 0;
@@ -597,11 +598,34 @@ static void build_slots(phd_ctx* c, int M) {
     for (int l = 0; l < M; ++l) c->h_slot[n++] = l;
   }
   c->n_slots = n;
-  int wz = (int)std::min<int64_t>(kMaxWarpsZ, std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), kZPerWarp)));
-  int zb = (int)ceil_div(std::max(n, 1), (int64_t)wz * kZPerWarp);
-  c->wz = wz;
-  c->zb = M > 0 ? zb : 0;
-  c->slots_pad = zb * wz * kZPerWarp;
+  // slots per lane: 8 (halves the per-particle overheads) unless it pads much more than 4
+  int best_zl = 4, best_wz = 2, best_zb = 1;
+  int64_t best_pad = -1;
+  for (int zl : {8, 4}) {
+    int64_t per_warp = 32 * zl;
+    int wz = (int)std::min<int64_t>(kMaxWarpsZ, std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), per_warp)));
+    int zb = (int)ceil_div(std::max(n, 1), (int64_t)wz * per_warp);
+    int64_t pad = (int64_t)zb * wz * per_warp;
+    if (best_pad < 0 || pad < best_pad - std::max(n, 16) / 16) {
+      best_pad = pad;
+      best_zl = zl;
+      best_wz = wz;
+      best_zb = zb;
+    }
+  }
+  if (const char* fz = getenv("PHD_FORCE_ZL")) {  // tuning experiments only
+    int zl = atoi(fz);
+    if (zl == 4 || zl == 8) {
+      best_zl = zl;
+      best_wz = (int)std::min<int64_t>(kMaxWarpsZ, std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), 32 * zl)));
+      best_zb = (int)ceil_div(std::max(n, 1), (int64_t)best_wz * 32 * zl);
+      best_pad = (int64_t)best_zb * best_wz * 32 * zl;
+    }
+  }
+  c->zl = best_zl;
+  c->wz = best_wz;
+  c->zb = M > 0 ? best_zb : 0;
+  c->slots_pad = (int)best_pad;
   for (int s = n; s < c->slots_pad; ++s) c->h_slot[s] = -1;
 }
 
@@ -637,7 +661,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   // particle-CTA count: one wave of resident CTAs over the z-blocks
   int gp = 0;
   if (M > 0 && n > 0) {
-    int occ = std::max(1, std::min(pass_occupancy(c->model, 1, c->wz), pass_occupancy(c->model, 2, c->wz)));
+    int occ = std::max(1, std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl)));
     int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / c->zb);
     int64_t cap_gp = std::max<int64_t>(1, c->L.part_cap / c->slots_pad);
     gp = (int)std::min<int64_t>(std::min(want, cap_gp), tiles);
@@ -667,14 +691,14 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
   timing_record(c, 3);
   if (M > 0) {
-    if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->st));
+    if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 4);
     KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, c->n_slots, c->slot_label, c->C, c->st));
     if (gp == 0) CU(cudaMemsetAsync(c->C, 0, sizeof(double) * M, c->st));
     if (c->world > 1) NC(ncclAllReduce(c->C, c->C, (size_t)M, ncclDouble, ncclSum, c->comm, c->st));
     KL(launch_zconst(c->C, M, c->kappa, c->slot_label, c->slots_pad, c->s[4], c->D, c->bad, c->st));
     timing_record(c, 5);
-    if (gp > 0) KL(launch_pass(c->model, 2, pa, gp, c->zb, c->wz, c->st));
+    if (gp > 0) KL(launch_pass(c->model, 2, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 6);
   } else {
     timing_record(c, 4);
@@ -685,7 +709,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (n > 0)
     KL(launch_finalize(c->A[4], c->P, c->L.cap_l, M > 0 && gp > 0 ? c->zb : 0, n, c->nu, c->wscale, c->wn, c->blk_w, c->blk_wp, c->st));
   double* rank_slots = c->acc + 5 * (size_t)M;
-  KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->n_slots : 0, c->slot_label, c->D, c->s[0], c->s[1],
+  KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->n_slots : 0, c->slot_label, c->C, c->D, c->s[0], c->s[1],
                        c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank, c->world, c->st));
   if (M > 0 && gp == 0) CU(cudaMemsetAsync(c->acc, 0, sizeof(double) * 5 * M, c->st));
   if (c->world > 1)

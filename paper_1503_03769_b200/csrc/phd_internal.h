@@ -7,8 +7,7 @@
 namespace phd {
 
 // ---- tiling constants ----------------------------------------
-constexpr int kZPerLane = 4;                    // measurements per lane (2 f32x2 pairs)
-constexpr int kZPerWarp = 32 * kZPerLane;       // 128 measurement slots per warp
+// measurement slots per lane: 4 or 8 (kernel template), i.e. 128 or 256 per warp
 constexpr int kMaxWarpsZ = 8;                   // warps per CTA (each owns 128 slots)
 constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one particle per loader thread
 constexpr int kTileP = 64;                      // particles per smem tile
@@ -45,7 +44,7 @@ struct PassArgs {
   float na0, na1;            // -alpha_0, -alpha_1 (log2 units)
   float wscale;              // p_D * c, c = 1 / (2 pi sigma_0 sigma_1)
   double* Cpart;             // [gp][slots_pad]
-  double* Apart;             // [gp][5][slots_pad]
+  double* Apart;             // [gp][4][slots_pad]
   float* P;                  // [zb][P_stride]
   int64_t P_stride;
 };
@@ -88,8 +87,8 @@ cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, 
                            int64_t stride, cudaStream_t s);
 cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad,
                          float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s);
-cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, cudaStream_t s);
-int pass_occupancy(int model, int pass, int wz);
+cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
+int pass_occupancy(int model, int pass, int wz, int zl);
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
                             double* C_lab, cudaStream_t s);
 cudaError_t launch_zconst(const double* C_lab, int M, double kappa, const int32_t* slot_label, int n_slots_pad,
@@ -97,7 +96,7 @@ cudaError_t launch_zconst(const double* C_lab, int M, double kappa, const int32_
 cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, int zb, int64_t n, float nu,
                             float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s);
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
-                              const double* D_lab, const float* s0, const float* s1, const float* s2,
+                              const double* C_lab, const double* D_lab, const float* s0, const float* s1, const float* s2,
                               const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
                               double* acc_lab, double* rank_slots, int rank, int world, cudaStream_t s);
 cudaError_t launch_extract(const double* acc_lab, int M, const double* rank_slots, int world, double p_d,

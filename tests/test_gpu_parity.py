@@ -149,14 +149,17 @@ def test_extract_parity(phd, orc, mname):
     eg = orc.extract(m, acc, summ["W"], summ["W_pred"])
     assert list(est["labels"]) == list(eg["labels"])
     assert np.allclose(est["states"], eg["states"], rtol=1e-6, atol=1e-4)
-    # end-to-end vs the all-oracle path: same label set except near-ties (S8)
-    n = min(len(eo["labels"]), len(est["labels"]))
-    ties = 0
-    for a, b in zip(est["labels"][:n], eo["labels"][:n]):
+    # end-to-end vs the all-oracle path: the selected label sets agree except for
+    # near-ties of dW at the selection threshold (S8: within 1e-5 relative)
+    ga, oa = set(est["labels"].tolist()), set(eo["labels"].tolist())
+    if len(eo["labels"]):
+        thr = acco[eo["labels"][-1], 0]
+        for lab in ga ^ oa:
+            assert abs(acco[lab, 0] - thr) <= 1e-5 * thr, (lab, acco[lab, 0], thr)
+    # order: a swap of neighbours is allowed only between near-equal dW
+    for a, b in zip(est["labels"], eo["labels"]):
         if a != b:
-            ties += 1
             assert abs(acco[a, 0] - acco[b, 0]) <= 1e-5 * acco[b, 0]
-    assert ties <= 2
     for i, lab in enumerate(est["labels"]):
         j = list(eo["labels"]).index(lab) if lab in eo["labels"] else None
         if j is not None:

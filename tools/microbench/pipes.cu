@@ -127,6 +127,33 @@ __global__ void k_f2f_dadd(float* out, long long* cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+// mixed packed + scalar FP32: does the lite FMA pipe run scalar FFMA while the
+// heavy pipe runs FFMA2?  RATIO scalar chains per packed chain.
+template <int NS>
+__global__ void k_mix_ffma2_scalar(float* out, const float* ab, long long* cyc) {
+  float2 a = make_float2(ab[threadIdx.x & 31], ab[(threadIdx.x + 1) & 31]);
+  float2 b = make_float2(ab[32 + (threadIdx.x & 31)], ab[32 + ((threadIdx.x + 3) & 31)]);
+  float as = ab[(threadIdx.x + 5) & 31], bs = ab[32 + ((threadIdx.x + 7) & 31)];
+  float2 v[CH];
+  float w[CH * NS];
+  for (int c = 0; c < CH; ++c) v[c] = make_float2(threadIdx.x * 1e-3f + c, c * 0.5f);
+  for (int c = 0; c < CH * NS; ++c) w[c] = threadIdx.x * 2e-3f + c;
+  long long t0 = clock64();
+#pragma unroll 2
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = __ffma2_rn(v[c], a, b);
+#pragma unroll
+    for (int c = 0; c < CH * NS; ++c) w[c] = fmaf(w[c], as, bs);
+  }
+  long long t1 = clock64();
+  float s = 0; for (int c = 0; c < CH; ++c) s += v[c].x + v[c].y;
+  for (int c = 0; c < CH * NS; ++c) s += w[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   int dev = 0; cudaDeviceProp p; CHK(cudaGetDeviceProperties(&p, dev));
   int sms = p.multiProcessorCount;
@@ -141,12 +168,13 @@ int main() {
   float hab[64]; for (int i = 0; i < 64; ++i) hab[i] = 0.999f - i * 1e-5f;
   CHK(cudaMemcpy(ab, hab, sizeof(hab), cudaMemcpyHostToDevice));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char* names[] = {"ffma_imm", "ffma_3reg", "ffma2", "fadd2", "ex2", "mix_3ffma2_2ex2", "f2f_dadd"};
-  // thread-ops per thread-iteration (per chain step): lanes of fp32 work
-  double ops_per[] = {1, 1, 2, 2, 1, 2, 1};
+  const char* names[] = {"ffma_imm", "ffma_3reg", "ffma2", "fadd2", "ex2", "mix_3ffma2_2ex2", "f2f_dadd",
+                         "ffma2+1scalar", "ffma2+2scalar"};
+  // fp32 lane-ops per chain step
+  double ops_per[] = {1, 1, 2, 2, 1, 2, 1, 3, 4};
   for (int bi = 0; bi < 2; ++bi) {
     int blocks = blocks_list[bi];
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 0; k < 9; ++k) {
       for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(e0);
         switch (k) {
@@ -157,6 +185,8 @@ int main() {
           case 4: k_ex2<<<blocks, threads>>>(out, cyc); break;
           case 5: k_mix13<<<blocks, threads>>>(out, ab, cyc); break;
           case 6: k_f2f_dadd<<<blocks, threads>>>(out, cyc); break;
+          case 7: k_mix_ffma2_scalar<1><<<blocks, threads>>>(out, ab, cyc); break;
+          case 8: k_mix_ffma2_scalar<2><<<blocks, threads>>>(out, ab, cyc); break;
         }
         cudaEventRecord(e1); CHK(cudaEventSynchronize(e1)); CHK(cudaGetLastError());
         float ms; cudaEventElapsedTime(&ms, e0, e1);
