@@ -137,6 +137,19 @@ phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const ui
                       int32_t device, void* stream, void* workspace, phd_ctx** out);
 void phd_destroy(phd_ctx* ctx);
 
+/* In-process rank group: `world` contexts in ONE process (one host thread per
+ * rank, possibly all on one GPU) whose collectives are host barriers plus
+ * device-to-device copies instead of NCCL.  It runs exactly the multi-rank
+ * orchestration of phd_update / phd_resample_exchange and exists to test that
+ * path without W GPUs; ranks never wait on one another inside a kernel.  Every
+ * rank's calls must be issued concurrently (one thread per rank).
+ * world in [1, 16].  The group must outlive its contexts. */
+typedef struct phd_group phd_group;
+phd_status phd_group_create(int32_t world, phd_group** out);
+void phd_group_destroy(phd_group* g);
+phd_status phd_create_in_group(const phd_params* p, phd_group* g, int32_t rank, int32_t device, void* stream,
+                               void* workspace, phd_ctx** out);
+
 /* ---- population injection / inspection (parity, checkpoint) ---------------
  * The global particle array at a step is [survivors 0..N_out-1, births
  * N_out..N_out+J-1]; rank r owns the block [floor(r N/W), floor((r+1) N/W)).

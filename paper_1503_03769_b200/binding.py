@@ -54,7 +54,8 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_create", "phd_destroy", "phd_set_particles", "phd_get_particles", "phd_predict", "phd_update",
            "phd_extract", "phd_resample_exchange", "phd_step", "phd_get_normalizers", "phd_get_accumulators",
            "phd_get_ancestors", "phd_get_resample_meta", "phd_launch_count", "phd_set_timing", "phd_get_timing",
-           "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange"]
+           "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
+           "phd_group_create", "phd_group_destroy", "phd_create_in_group"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -89,6 +90,11 @@ def load(build_if_missing=True):
     L.phd_workspace_size.argtypes = [ctypes.POINTER(Params), ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
     L.phd_create.argtypes = [ctypes.POINTER(Params), ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p,
                              ctypes.c_int32, _P, _P, ctypes.POINTER(_P)]
+    L.phd_create_in_group.argtypes = [ctypes.POINTER(Params), _P, ctypes.c_int32, ctypes.c_int32, _P, _P,
+                                      ctypes.POINTER(_P)]
+    L.phd_group_create.argtypes = [ctypes.c_int32, ctypes.POINTER(_P)]
+    L.phd_group_destroy.argtypes = [_P]
+    L.phd_group_destroy.restype = None
     L.phd_destroy.argtypes = [_P]
     L.phd_destroy.restype = None
     L.phd_set_particles.argtypes = [_P, _P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int32]
@@ -211,18 +217,41 @@ def workspace_size(model, world=1):
     return n.value
 
 
+class LocalGroup:
+    """In-process rank group (phd_group): run `world` Filter contexts of one
+    process (one thread per rank) through the multi-rank path without NCCL."""
+
+    def __init__(self, world):
+        self.L = load()
+        h = _P()
+        st = self.L.phd_group_create(int(world), ctypes.byref(h))
+        if st != 0:
+            raise PhdError(st, "phd_group_create")
+        self.h, self.world = h, world
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.phd_group_destroy(self.h)
+            self.h = None
+
+
 class Filter:
     """One rank's filter context (phd_ctx)."""
 
-    def __init__(self, model, rank=0, world=1, nccl_id=None, device=0, stream=None, workspace=None):
+    def __init__(self, model, rank=0, world=1, nccl_id=None, device=0, stream=None, workspace=None, group=None):
         self.L = load()
         self.model = model
         self.params = params_from(model)
-        self.rank, self.world = rank, world
+        self.rank, self.world = rank, (group.world if group is not None else world)
         self._ws = workspace  # keep the caller's buffer alive
+        self._group = group
         h = _P()
-        st = self.L.phd_create(ctypes.byref(self.params), int(rank), int(world), nccl_id, int(device),
-                               stream, _ptr(workspace), ctypes.byref(h))
+        if group is not None:
+            st = self.L.phd_create_in_group(ctypes.byref(self.params), group.h, int(rank), int(device), stream,
+                                            _ptr(workspace), ctypes.byref(h))
+        else:
+            st = self.L.phd_create(ctypes.byref(self.params), int(rank), int(world), nccl_id, int(device),
+                                   stream, _ptr(workspace), ctypes.byref(h))
         if st != 0:
             raise PhdError(st, "phd_create failed (see stderr)")
         self.h = h

@@ -1,0 +1,162 @@
+// Collective transports (see comm.h).
+#include "comm.h"
+
+#include <nccl.h>
+
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+
+namespace phd {
+
+// ---------------------------------------------------------------------------
+class NcclComm : public Comm {
+ public:
+  NcclComm(ncclComm_t c, int world, int rank) : c_(c), world_(world), rank_(rank) {}
+  ~NcclComm() override {
+    if (c_) ncclCommDestroy(c_);
+  }
+  const char* name() const override { return "nccl"; }
+
+  std::string allreduce_f64(double* buf, size_t n, cudaStream_t s) override {
+    if (n == 0) return "";
+    ncclResult_t r = ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, c_, s);
+    return r == ncclSuccess ? "" : std::string("ncclAllReduce: ") + ncclGetErrorString(r);
+  }
+
+  std::string exchange(float* const* src, float* const* dst, int narr, const ExchangePlan& p,
+                       cudaStream_t s) override {
+    ncclResult_t r = ncclGroupStart();
+    for (int q = 0; q < world_ && r == ncclSuccess; ++q) {
+      if (q == rank_) continue;
+      for (int i = 0; i < narr && r == ncclSuccess; ++i) {
+        if (p.send_count[q] > 0)
+          r = ncclSend(src[i] + p.send_off[q], (size_t)p.send_count[q], ncclFloat, q, c_, s);
+        if (r == ncclSuccess && p.recv_count[q] > 0)
+          r = ncclRecv(dst[i] + p.recv_off[q], (size_t)p.recv_count[q], ncclFloat, q, c_, s);
+      }
+    }
+    ncclResult_t e = ncclGroupEnd();
+    if (r == ncclSuccess) r = e;
+    return r == ncclSuccess ? "" : std::string("nccl exchange: ") + ncclGetErrorString(r);
+  }
+
+ private:
+  ncclComm_t c_;
+  int world_, rank_;
+};
+
+Comm* make_nccl_comm(const uint8_t* id128, int world, int rank, std::string* err) {
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  ncclComm_t c = nullptr;
+  ncclResult_t r = ncclCommInitRank(&c, world, id, rank);
+  if (r != ncclSuccess) {
+    *err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+    return nullptr;
+  }
+  return new NcclComm(c, world, rank);
+}
+
+bool nccl_unique_id(uint8_t* out128) {
+  ncclUniqueId id;
+  static_assert(sizeof(id) == 128, "nccl id size");
+  if (ncclGetUniqueId(&id) != ncclSuccess) return false;
+  memcpy(out128, &id, 128);
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+struct LocalGroup {
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t generation = 0;
+  std::vector<double*> bufs;
+  std::vector<std::vector<float*>> srcs;
+  std::vector<ExchangePlan> plans;
+
+  explicit LocalGroup(int w) : world(w), bufs(w, nullptr), srcs(w), plans(w) {}
+
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    int64_t gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+LocalGroup* local_group_create(int world) { return world >= 1 ? new LocalGroup(world) : nullptr; }
+void local_group_destroy(LocalGroup* g) { delete g; }
+int local_group_world(const LocalGroup* g) { return g ? g->world : 0; }
+
+class LocalComm : public Comm {
+ public:
+  LocalComm(LocalGroup* g, int rank) : g_(g), rank_(rank) {}
+  ~LocalComm() override {
+    if (tmp_) cudaFree(tmp_);
+  }
+  const char* name() const override { return "local"; }
+
+  std::string allreduce_f64(double* buf, size_t n, cudaStream_t s) override {
+    if (n > tmp_n_) {
+      if (tmp_) cudaFree(tmp_);
+      if (cudaMalloc(&tmp_, n * sizeof(double)) != cudaSuccess) return "local allreduce: cudaMalloc failed";
+      tmp_n_ = n;
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cudaGetErrorString(e);
+    g_->bufs[rank_] = buf;
+    g_->barrier();
+    // every rank sums all ranks' buffers in rank order (identical bits on every rank)
+    if (n) {
+      e = launch_sum_ranks(g_->bufs.data(), g_->world, tmp_, n, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    g_->barrier();  // all reads of the peers' buffers are done
+    if (n && e == cudaSuccess) e = cudaMemcpyAsync(buf, tmp_, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? "" : std::string("local allreduce: ") + cudaGetErrorString(e);
+  }
+
+  std::string exchange(float* const* src, float* const* dst, int narr, const ExchangePlan& p,
+                       cudaStream_t s) override {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cudaGetErrorString(e);
+    g_->srcs[rank_].assign(src, src + narr);
+    g_->plans[rank_] = p;
+    g_->barrier();
+    for (int q = 0; q < g_->world && e == cudaSuccess; ++q) {
+      if (q == rank_ || p.recv_count[q] <= 0) continue;
+      int64_t off = g_->plans[q].send_off[rank_];
+      for (int i = 0; i < narr && e == cudaSuccess; ++i)
+        e = cudaMemcpyAsync(dst[i] + p.recv_off[q], g_->srcs[q][i] + off, sizeof(float) * p.recv_count[q],
+                            cudaMemcpyDeviceToDevice, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    g_->barrier();  // peers may reuse their source buffers only after every pull
+    return e == cudaSuccess ? "" : std::string("local exchange: ") + cudaGetErrorString(e);
+  }
+
+ private:
+  LocalGroup* g_;
+  int rank_;
+  double* tmp_ = nullptr;
+  size_t tmp_n_ = 0;
+};
+
+Comm* make_local_comm(LocalGroup* g, int rank, std::string* err) {
+  if (!g || rank < 0 || rank >= g->world) {
+    *err = "bad local group / rank";
+    return nullptr;
+  }
+  return new LocalComm(g, rank);
+}
+
+}  // namespace phd

@@ -1,0 +1,44 @@
+// Collective transport for the multi-rank step.
+//   NcclComm  : one process per GPU, NCCL over NVLink/NVSwitch (the product path).
+//   LocalComm : a group of rank contexts inside one process (one host thread per
+//               rank, host barriers, device-to-device copies).  Used to run the
+//               library's multi-rank orchestration on a single GPU in the tests;
+//               ranks never wait on one another inside a kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace phd {
+
+struct ExchangePlan {
+  std::vector<int64_t> send_count, send_off, recv_count, recv_off;
+};
+
+class Comm {
+ public:
+  virtual ~Comm() {}
+  virtual const char* name() const = 0;
+  // In-place fp64 sum over all ranks, ordered on stream s.  Returns "" or an error.
+  virtual std::string allreduce_f64(double* buf, size_t n, cudaStream_t s) = 0;
+  // Peer transfers of the plan (the rank's own segment is copied by the caller):
+  // narr float arrays; send src[i] + send_off[q] (send_count[q] items) to rank q,
+  // receive into dst[i] + recv_off[q] (recv_count[q] items) from rank q.
+  virtual std::string exchange(float* const* src, float* const* dst, int narr, const ExchangePlan& p,
+                               cudaStream_t s) = 0;
+};
+
+Comm* make_nccl_comm(const uint8_t* id128, int world, int rank, std::string* err);
+bool nccl_unique_id(uint8_t* out128);
+
+struct LocalGroup;
+LocalGroup* local_group_create(int world);
+void local_group_destroy(LocalGroup* g);
+int local_group_world(const LocalGroup* g);
+Comm* make_local_comm(LocalGroup* g, int rank, std::string* err);
+
+cudaError_t launch_sum_ranks(const double* const* srcs, int world, double* dst, size_t n, cudaStream_t s);
+
+}  // namespace phd

@@ -126,3 +126,32 @@ cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s) {
 }
 
 }  // namespace phd
+
+// ---------------------------------------------------------------------------
+// In-process rank-group all-reduce (LocalComm, test transport): dst = sum over
+// ranks in rank order of srcs[r] (all buffers device-visible).
+#include "comm.h"
+
+namespace phd {
+
+struct RankPtrs {
+  const double* p[16];
+};
+
+__global__ void k_sum_ranks(RankPtrs ptrs, int world, double* dst, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < world; ++r) s += ptrs.p[r][i];
+  dst[i] = s;
+}
+
+cudaError_t launch_sum_ranks(const double* const* srcs, int world, double* dst, size_t n, cudaStream_t s) {
+  if (world > 16) return cudaErrorInvalidValue;
+  RankPtrs rp{};
+  for (int r = 0; r < world; ++r) rp.p[r] = srcs[r];
+  k_sum_ranks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rp, world, dst, n);
+  return cudaGetLastError();
+}
+
+}  // namespace phd

@@ -560,7 +560,9 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
     cx = -(double)s0[s];
     cy = -(double)s1[s];
   }
-  double dW = C_lab[lab] * inv;
+  // C (hence dW) is already global: only rank 0 contributes the dW and centre
+  // terms, every rank its own centred partial sums (the C2 all-reduce adds them).
+  double dW = rank == 0 ? C_lab[lab] * inv : 0.0;
   double* o = acc_lab + 5 * (int64_t)lab;
   o[0] = dW;
   o[1] = A[0] * inv + cx * dW;

@@ -9,8 +9,6 @@
 //   extract   k_extract on rank 0 (the central unit) + D2H of the estimates
 //   resample  k_scan_blocks -> k_resample_mark -> k_block_max -> k_scan_max -> k_gather
 //   exchange  world 1: buffer swap; world > 1: grouped ncclSend/ncclRecv (C3)
-#include <nccl.h>
-
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -20,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "phd.h"
 #include "phd_internal.h"
 #include "philox.cuh"
@@ -101,7 +100,7 @@ struct phd_ctx {
   char* ws = nullptr;
   bool own_ws = false;
   Layout L;
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;
   std::string err;
   int64_t launches = 0;
   int model = kPosIso;
@@ -178,10 +177,10 @@ phd_status fail(phd_ctx* c, phd_status s, const char* fmt, ...) {
     ++c->launches;                                                                                \
     if (e_ != cudaSuccess) return fail(c, PHD_ECUDA, "launch %s: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
-#define NC(call)                                                                                  \
+#define COMM(call)                                                                                \
   do {                                                                                            \
-    ncclResult_t r_ = (call);                                                                     \
-    if (r_ != ncclSuccess) return fail(c, PHD_ENCCL, "%s: %s", #call, ncclGetErrorString(r_));    \
+    std::string e_ = (call);                                                                      \
+    if (!e_.empty()) return fail(c, PHD_ENCCL, "%s", e_.c_str());                                 \
   } while (0)
 
 void block_of(int64_t n, int world, int rank, int64_t* lo, int64_t* hi) {
@@ -315,12 +314,22 @@ phd_status phd_plan_exchange(int32_t world, int32_t rank, const int64_t* bounds,
   return PHD_OK;
 }
 
-phd_status phd_nccl_unique_id(uint8_t out[128]) {
-  ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return PHD_ENCCL;
-  static_assert(sizeof(id) == 128, "nccl id size");
-  memcpy(out, &id, 128);
+phd_status phd_nccl_unique_id(uint8_t out[128]) { return nccl_unique_id(out) ? PHD_OK : PHD_ENCCL; }
+
+struct phd_group {
+  LocalGroup* g;
+};
+
+phd_status phd_group_create(int32_t world, phd_group** out) {
+  if (!out || world < 1 || world > 16) return PHD_EINVAL;
+  *out = new phd_group{local_group_create(world)};
   return PHD_OK;
+}
+
+void phd_group_destroy(phd_group* g) {
+  if (!g) return;
+  local_group_destroy(g->g);
+  delete g;
 }
 
 phd_status phd_workspace_size(const phd_params* p, int32_t world, size_t* bytes) {
@@ -332,8 +341,8 @@ phd_status phd_workspace_size(const phd_params* p, int32_t world, size_t* bytes)
   return PHD_OK;
 }
 
-phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const uint8_t* nccl_id, int32_t device,
-                      void* stream, void* workspace, phd_ctx** out) {
+static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, const uint8_t* nccl_id,
+                              phd_group* group, int32_t device, void* stream, void* workspace, phd_ctx** out) {
   if (!out) return PHD_EINVAL;
   *out = nullptr;
   phd_ctx* c = new phd_ctx();
@@ -423,11 +432,14 @@ phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const ui
   c->Wr.assign(world, 0.0);
   c->Wpr.assign(world, 0.0);
   if (world > 1) {
-    if (!nccl_id) return bail(fail(c, PHD_EINVAL, "nccl_id required for world > 1"));
-    ncclUniqueId id;
-    memcpy(&id, nccl_id, sizeof id);
-    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
-    if (r != ncclSuccess) return bail(fail(c, PHD_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    std::string e;
+    if (group) {
+      c->comm = make_local_comm(group->g, rank, &e);
+    } else {
+      if (!nccl_id) return bail(fail(c, PHD_EINVAL, "nccl_id required for world > 1"));
+      c->comm = make_nccl_comm(nccl_id, world, rank, &e);
+    }
+    if (!c->comm) return bail(fail(c, PHD_ENCCL, "%s", e.c_str()));
   }
   CUB(cudaMemsetAsync(c->ws, 0, L.total, c->st));
   CUB(cudaStreamSynchronize(c->st));
@@ -436,10 +448,21 @@ phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const ui
   return PHD_OK;
 }
 
+phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const uint8_t* nccl_id, int32_t device,
+                      void* stream, void* workspace, phd_ctx** out) {
+  return create_impl(p, rank, world, nccl_id, nullptr, device, stream, workspace, out);
+}
+
+phd_status phd_create_in_group(const phd_params* p, phd_group* g, int32_t rank, int32_t device, void* stream,
+                               void* workspace, phd_ctx** out) {
+  if (!g) return PHD_EINVAL;
+  return create_impl(p, rank, local_group_world(g->g), nullptr, g, device, stream, workspace, out);
+}
+
 void phd_destroy(phd_ctx* c) {
   if (!c) return;
   if (c->st) cudaStreamSynchronize(c->st);
-  if (c->comm) ncclCommDestroy(c->comm);
+  delete c->comm;
   for (int i = 0; i < 16; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   if (c->own_ws && c->ws) cudaFree(c->ws);
@@ -461,6 +484,7 @@ phd_status phd_set_timing(phd_ctx* c, int32_t enable) {
 
 phd_status phd_get_timing(phd_ctx* c, float* ms) {
   if (!c || !ms) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   CU(cudaStreamSynchronize(c->st));
   for (int i = 0; i < 8; ++i) ms[i] = c->t_ms[i];
   return PHD_OK;
@@ -470,6 +494,7 @@ phd_status phd_get_timing(phd_ctx* c, float* ms) {
 phd_status phd_set_particles(phd_ctx* c, const float* soa4, const float* w, int64_t n_local, int64_t n_global,
                              double mass, int32_t stage) {
   if (!c || !soa4) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   c->err.clear();
   int64_t J = c->p.births_per_step;
   int64_t Nblk = stage == PHD_STAGE_PREDICTED ? n_global : n_global + J;
@@ -505,6 +530,7 @@ phd_status phd_set_particles(phd_ctx* c, const float* soa4, const float* w, int6
 
 phd_status phd_get_particles(phd_ctx* c, float* soa4, float* w, int64_t cap, int64_t* n_local, int64_t* global_offset) {
   if (!c) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   int64_t n, g0;
   if (c->stage == kResampled) {
     int64_t lo, hi;
@@ -527,6 +553,7 @@ phd_status phd_get_particles(phd_ctx* c, float* soa4, float* w, int64_t cap, int
 
 phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_prev) {
   if (!c) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   c->err.clear();
   if (!c->populated || c->stage != kResampled) return fail(c, PHD_ESTATE, "phd_predict needs a resampled population");
   if (k < 1) return fail(c, PHD_EINVAL, "k must be >= 1");
@@ -631,6 +658,7 @@ static void build_slots(phd_ctx* c, int M) {
 
 phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (!c) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   c->err.clear();
   if (c->stage != kPredicted) return fail(c, PHD_ESTATE, "phd_update needs a predicted population");
   if (M < 0 || M > c->p.max_meas) return fail(c, PHD_EINVAL, "M = %d outside [0, max_meas = %d]", M, c->p.max_meas);
@@ -695,7 +723,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     timing_record(c, 4);
     KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, c->n_slots, c->slot_label, c->C, c->st));
     if (gp == 0) CU(cudaMemsetAsync(c->C, 0, sizeof(double) * M, c->st));
-    if (c->world > 1) NC(ncclAllReduce(c->C, c->C, (size_t)M, ncclDouble, ncclSum, c->comm, c->st));
+    if (c->world > 1) COMM(c->comm->allreduce_f64(c->C, (size_t)M, c->st));
     KL(launch_zconst(c->C, M, c->kappa, c->slot_label, c->slots_pad, c->s[4], c->D, c->bad, c->st));
     timing_record(c, 5);
     if (gp > 0) KL(launch_pass(c->model, 2, pa, gp, c->zb, c->wz, c->zl, c->st));
@@ -713,7 +741,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
                        c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank, c->world, c->st));
   if (M > 0 && gp == 0) CU(cudaMemsetAsync(c->acc, 0, sizeof(double) * 5 * M, c->st));
   if (c->world > 1)
-    NC(ncclAllReduce(c->acc, c->acc, (size_t)(5 * M + 2 * c->world), ncclDouble, ncclSum, c->comm, c->st));
+    COMM(c->comm->allreduce_f64(c->acc, (size_t)(5 * M + 2 * c->world), c->st));
   CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 2 * c->world, cudaMemcpyDeviceToHost, c->st));
   CU(cudaMemcpyAsync(c->h_meta + 2 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
   timing_record(c, 7);
@@ -757,6 +785,7 @@ static int64_t next_count(phd_ctx* c, int* clamped) {
 
 phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s) {
   if (!c) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   c->err.clear();
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_extract needs an updated population");
   int nest = 0;
@@ -799,6 +828,7 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
 
 phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   if (!c) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   c->err.clear();
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_resample_exchange needs an updated population");
   timing_record(c, 10);
@@ -864,15 +894,8 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
       for (int i = 0; i < 5; ++i)
         CU(cudaMemcpyAsync(c->A[i] + ro[c->rank], c->B[i] + so[c->rank], sizeof(float) * sc[c->rank],
                            cudaMemcpyDeviceToDevice, c->st));
-    NC(ncclGroupStart());
-    for (int q = 0; q < c->world; ++q) {
-      if (q == c->rank) continue;
-      for (int i = 0; i < 5; ++i) {
-        if (sc[q] > 0) NC(ncclSend(c->B[i] + so[q], (size_t)sc[q], ncclFloat, q, c->comm, c->st));
-        if (rc[q] > 0) NC(ncclRecv(c->A[i] + ro[q], (size_t)rc[q], ncclFloat, q, c->comm, c->st));
-      }
-    }
-    NC(ncclGroupEnd());
+    ExchangePlan plan{sc, so, rc, ro};
+    COMM(c->comm->exchange(c->B, c->A, 5, plan, c->st));
     int64_t blo, bhi;
     block_of(n_out + J, c->world, c->rank, &blo, &bhi);
     c->n_surv_local = std::max<int64_t>(0, std::min(bhi, n_out) - std::min(blo, n_out));
@@ -914,6 +937,7 @@ phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estima
 
 phd_status phd_get_normalizers(phd_ctx* c, double* C, int32_t cap) {
   if (!c || !C) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "no update yet");
   if (cap < c->M) return fail(c, PHD_EINVAL, "cap < M");
   if (c->M > 0) CU(cudaMemcpyAsync(C, c->C, sizeof(double) * c->M, cudaMemcpyDeviceToHost, c->st));
@@ -923,6 +947,7 @@ phd_status phd_get_normalizers(phd_ctx* c, double* C, int32_t cap) {
 
 phd_status phd_get_accumulators(phd_ctx* c, double* acc, int32_t cap) {
   if (!c || !acc) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "no update yet");
   if (cap < c->M) return fail(c, PHD_EINVAL, "cap < M");
   if (c->M > 0) CU(cudaMemcpyAsync(acc, c->acc, sizeof(double) * 5 * c->M, cudaMemcpyDeviceToHost, c->st));
@@ -932,6 +957,7 @@ phd_status phd_get_accumulators(phd_ctx* c, double* acc, int32_t cap) {
 
 phd_status phd_get_ancestors(phd_ctx* c, int32_t* anc, int64_t cap, int64_t* n, int64_t* first) {
   if (!c || !anc) return PHD_EINVAL;
+  cudaSetDevice(c->device);
   if (n) *n = c->prod_n;
   if (first) *first = c->prod_first;
   if (cap < c->prod_n) return fail(c, PHD_EINVAL, "cap < produced");
