@@ -60,8 +60,6 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
       __syncthreads();
     }
   }
-  __shared__ double sW, sWp;
-  __shared__ long long sLT;
   __shared__ int snsel;
   if (tid == 0) {
     double W = 0.0, Wp = 0.0;
@@ -73,9 +71,6 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
     if (LT < 0) LT = 0;
     long long nsel = LT < n_elig ? LT : n_elig;
     if (nsel > cap) nsel = cap;
-    sW = W;
-    sWp = Wp;
-    sLT = LT;
     snsel = (int)nsel;
     double frac = W - floor(W);
     summary[0] = W;

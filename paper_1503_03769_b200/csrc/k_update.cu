@@ -365,6 +365,206 @@ int pass_occupancy(int model, int pass, int wz, int zl) {
 }
 
 // ---------------------------------------------------------------------------
+// Group-pipelined update: one particle sweep evaluates pass 1
+// (C) for measurement group j and pass 2 (weights, STPHD sums) for group j-1,
+// whose C is already reduced.  Pass 1 is EX2-bound and pass 2 FMA-bound; with
+// both in the same instruction stream the two pipes overlap.  H1 / H2 select
+// the halves (the first sweep has only pass 1, the last only pass 2).  4 slots
+// per lane per pass; both passes fold log2(p_D c w_i) into the exponent, so the
+// pass-1 and pass-2 terms u = p_D g w are bitwise identical.
+struct FusedArgs {
+  PassArgs a;
+  int s1_base;   // first slot of the pass-1 group
+  int s2_base;   // first slot of the pass-2 group
+  int p_plane;   // P plane of the pass-2 group's first CTA z-block
+};
+
+template <int MODEL, bool H1, bool H2>
+__global__ void __launch_bounds__(256, 2) k_fused(const FusedArgs fa) {
+  using L = RecLayout<MODEL, 2>;
+  constexpr int NP = 2;  // slot pairs per lane per pass
+  const PassArgs& a = fa.a;
+  extern __shared__ __align__(16) float smem[];
+  const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, wz = nthr >> 5;
+  float* recs = smem;                                  // [2][kTileP][WIDTH]
+  float* psum = recs + 2 * kTileP * L::WIDTH;          // [2][wz][kTileP]
+  double* out64 = reinterpret_cast<double*>(psum + 2 * wz * kTileP);  // [4 + 16][nthr]
+
+  const int zb = blockIdx.y;
+  const int off = (zb * wz + warp) * 128 + lane * 4;
+  const int slot1 = fa.s1_base + off, slot2 = fa.s2_base + off;
+  LaneZ<MODEL, 1, NP> z1;
+  LaneZ<MODEL, 2, NP> z2;
+  if (H1) z1.load(a, slot1);
+  if (H2) z2.load(a, slot2);
+  const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
+
+  float2 c1[NP], in[4][NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    c1[j] = f2(0.0f, 0.0f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) in[q][j] = f2(0.0f, 0.0f);
+  }
+#pragma unroll
+  for (int q = 0; q < 20; ++q) out64[q * nthr + tid] = 0.0;
+
+  const int64_t ntiles = (a.n + kTileP - 1) / kTileP;
+  const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
+  const int64_t t_end = min(t_begin + a.tiles_per_cta, ntiles);
+
+  TileLoader<MODEL, 2> ld;
+  if (t_begin < t_end) {
+    ld.fetch(a, t_begin * kTileP, tid, nthr);
+    ld.store(recs, a.wscale, tid, nthr);
+  }
+  __syncthreads();
+
+  for (int64_t t = t_begin; t < t_end; ++t) {
+    const int buf = (int)((t - t_begin) & 1);
+    const bool more = t + 1 < t_end;
+    if (more) ld.fetch(a, (t + 1) * kTileP, tid, nthr);
+    const float* rb = recs + buf * kTileP * L::WIDTH;
+
+#pragma unroll 1
+    for (int p0 = 0; p0 < kTileP; p0 += 8) {
+      float pe[8];
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp) {
+        const float* rec = rb + (p0 + pp) * L::WIDTH;
+        const float2 lw = *reinterpret_cast<const float2*>(rec + L::WC);
+        if (H1) {
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            float2 d0, d1;
+            residual<MODEL, 1, NP>(rec, z1, j, d0, d1);
+            c1[j] = __fadd2_rn(c1[j], ex2v(expo<MODEL>(d0, d1, na0, na1, lw)));
+          }
+        }
+        if (H2) {
+          float2 pacc = f2(0.0f, 0.0f);
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            float2 d0, d1;
+            residual<MODEL, 2, NP>(rec, z2, j, d0, d1);
+            const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, lw));  // u = p_D g w
+            pacc = __ffma2_rn(u, z2.d[j], pacc);
+            if (MODEL == kRangeBearing) {
+              const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
+              d0 = __fadd2_rn(f2(XY.x, XY.y), z2.c0[j]);
+              d1 = __fadd2_rn(f2(XY.z, XY.w), z2.c1[j]);
+            }
+            const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+            in[0][j] = __ffma2_rn(u, d0, in[0][j]);
+            in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+            in[2][j] = __ffma2_rn(u, d1, in[2][j]);
+            in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+          }
+          pe[pp] = pacc.x + pacc.y;
+        }
+      }
+      if (H2) {
+        float sres = transpose_reduce8(pe, lane);
+        if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = sres;
+      }
+    }
+
+    if (more) ld.store(recs + (buf ^ 1) * kTileP * L::WIDTH, a.wscale, tid, nthr);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      if (H1) {
+        out64[(2 * j) * nthr + tid] += (double)c1[j].x;
+        out64[(2 * j + 1) * nthr + tid] += (double)c1[j].y;
+        c1[j] = f2(0.0f, 0.0f);
+      }
+      if (H2) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          out64[(4 + q * 4 + 2 * j) * nthr + tid] += (double)in[q][j].x;
+          out64[(4 + q * 4 + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
+          in[q][j] = f2(0.0f, 0.0f);
+        }
+      }
+    }
+    __syncthreads();
+
+    if (H2) {
+      for (int p = tid; p < kTileP; p += nthr) {
+        int64_t i = t * kTileP + p;
+        if (i < a.n) {
+          float sres = 0.0f;
+          for (int w2 = 0; w2 < wz; ++w2) sres += psum[(buf * wz + w2) * kTileP + p];
+          a.P[(int64_t)(fa.p_plane + zb) * a.P_stride + i] = sres;
+        }
+      }
+    }
+  }
+  if (H1) {
+    const int64_t base = (int64_t)blockIdx.x * a.slots_pad;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a.Cpart[base + slot1 + m] = out64[m * nthr + tid];
+  }
+  if (H2) {
+    const int64_t base = (int64_t)blockIdx.x * 4 * a.slots_pad;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        a.Apart[base + (int64_t)q * a.slots_pad + slot2 + m] = out64[(4 + q * 4 + m) * nthr + tid];
+  }
+}
+
+template <int MODEL>
+static size_t fused_smem(int wz) {
+  using L = RecLayout<MODEL, 2>;
+  return sizeof(float) * 2 * kTileP * L::WIDTH + sizeof(float) * 2 * wz * kTileP + sizeof(double) * 20 * wz * 32;
+}
+
+template <int MODEL, bool H1, bool H2>
+static cudaError_t launch_fused_t(const FusedArgs& fa, int gp, int zbg, int wz, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fused<MODEL, H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fused_smem<MODEL>(kMaxWarpsZ));
+    attr = true;
+  }
+  k_fused<MODEL, H1, H2><<<dim3((unsigned)gp, (unsigned)zbg), wz * 32, fused_smem<MODEL>(wz), s>>>(fa);
+  return cudaGetLastError();
+}
+
+template <int MODEL>
+static cudaError_t launch_fused_m(bool h1, bool h2, const FusedArgs& fa, int gp, int zbg, int wz, cudaStream_t s) {
+  if (h1 && h2) return launch_fused_t<MODEL, true, true>(fa, gp, zbg, wz, s);
+  if (h1) return launch_fused_t<MODEL, true, false>(fa, gp, zbg, wz, s);
+  return launch_fused_t<MODEL, false, true>(fa, gp, zbg, wz, s);
+}
+
+cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,
+                         int zbg, int wz, cudaStream_t s) {
+  if (gp <= 0 || zbg <= 0 || (!h1 && !h2)) return cudaSuccess;
+  FusedArgs fa{a, s1_base, s2_base, p_plane};
+  if (model == kPosIso) return launch_fused_m<kPosIso>(h1, h2, fa, gp, zbg, wz, s);
+  if (model == kPosAniso) return launch_fused_m<kPosAniso>(h1, h2, fa, gp, zbg, wz, s);
+  return launch_fused_m<kRangeBearing>(h1, h2, fa, gp, zbg, wz, s);
+}
+
+template <int MODEL>
+static int fused_occ_m(int wz) {
+  int n = 0, m;
+  cudaFuncSetAttribute(k_fused<MODEL, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fused_smem<MODEL>(kMaxWarpsZ));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<MODEL, true, true>, wz * 32, fused_smem<MODEL>(wz));
+  m = n;
+  return m;
+}
+
+int fused_occupancy(int model, int wz) {
+  if (model == kPosIso) return fused_occ_m<kPosIso>(wz);
+  if (model == kPosAniso) return fused_occ_m<kPosAniso>(wz);
+  return fused_occ_m<kRangeBearing>(wz);
+}
+
+// ---------------------------------------------------------------------------
 // Measurement-slot preparation.  Slots hold labels (or -1 = padding); padding
 // slots get a sentinel that makes every likelihood term exactly 0.
 __global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* __restrict__ slot_label, int n,
@@ -404,50 +604,48 @@ cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_labe
   return cudaGetLastError();
 }
 
-// C[label] = sum over particle-CTAs (fixed order) of the pass-1 partials (fp64).
-__global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_pad, int n_slots,
-                           const int32_t* __restrict__ slot_label, double* C_lab) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n_slots) return;
-  int lab = slot_label[s];
-  if (lab < 0) return;
+// C_slot[s] = sum over particle-CTAs (fixed order) of the pass-1 partials (fp64),
+// for the slot range [s0, s1) (one measurement group).
+__global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_pad, int s0, int s1,
+                           double* C_slot) {
+  int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s1) return;
   double c = 0.0;
   for (int b = 0; b < gp; ++b) c += Cpart[(int64_t)b * slots_pad + s];
-  C_lab[lab] = c;
+  C_slot[s] = c;
 }
 
-cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
-                            double* C_lab, cudaStream_t s) {
-  if (n_slots <= 0) return cudaSuccess;
-  k_reduce_C<<<(n_slots + 127) / 128, 128, 0, s>>>(Cpart, gp, slots_pad, n_slots, slot_label, C_lab);
+cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
+                            cudaStream_t s) {
+  if (s1 <= s0) return cudaSuccess;
+  k_reduce_C<<<(s1 - s0 + 127) / 128, 128, 0, s>>>(Cpart, gp, slots_pad, s0, s1, C_slot);
   return cudaGetLastError();
 }
 
-// D = kappa + C (fp64, label order); per-slot d = 1/D as fp32 (0 when D == 0).
-__global__ void k_zconst(const double* __restrict__ C_lab, int M, double kappa,
-                         const int32_t* __restrict__ slot_label, int n, float* d_slot, double* D_lab, int* bad) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < M) {
-    double D = kappa + C_lab[s];
-    D_lab[s] = D;
+// For slots [s0, s1) of one group, with C_slot global (after the C1 all-reduce):
+// D = kappa + C, per-slot d = 1/D as fp32 (0 when D == 0 or padding), and the
+// label-order copies C_lab, D_lab used by the STPHD reduction and the getters.
+__global__ void k_zconst(const double* __restrict__ C_slot, const int32_t* __restrict__ slot_label, int s0, int s1,
+                         double kappa, float* d_slot, double* C_lab, double* D_lab, int* bad) {
+  int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s1) return;
+  int lab = slot_label[s];
+  float d = 0.0f;
+  if (lab >= 0) {
+    double C = C_slot[s];
+    double D = kappa + C;
+    C_lab[lab] = C;
+    D_lab[lab] = D;
     if (!isfinite(D)) atomicAdd(bad, 1);
+    d = D > 0.0 ? (float)(1.0 / D) : 0.0f;
   }
-  if (s < n) {
-    int lab = slot_label[s];
-    float d = 0.0f;
-    if (lab >= 0) {
-      double D = kappa + C_lab[lab];
-      d = D > 0.0 ? (float)(1.0 / D) : 0.0f;
-    }
-    d_slot[s] = d;
-  }
+  d_slot[s] = d;
 }
 
-cudaError_t launch_zconst(const double* C_lab, int M, double kappa, const int32_t* slot_label, int n_slots_pad,
-                          float* d_slot, double* D_lab, int* bad, cudaStream_t s) {
-  int n = n_slots_pad > M ? n_slots_pad : M;
-  if (n <= 0) return cudaSuccess;
-  k_zconst<<<(n + 255) / 256, 256, 0, s>>>(C_lab, M, kappa, slot_label, n_slots_pad, d_slot, D_lab, bad);
+cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
+                          float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s) {
+  if (s1 <= s0) return cudaSuccess;
+  k_zconst<<<(s1 - s0 + 255) / 256, 256, 0, s>>>(C_slot, slot_label, s0, s1, kappa, d_slot, C_lab, D_lab, bad);
   return cudaGetLastError();
 }
 

@@ -38,7 +38,7 @@ struct Layout {
   int64_t nbw_max = 0, nbo_max = 0;
   size_t total = 0;
   // byte offsets
-  size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_D,
+  size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_D,
       o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_summ, o_bad;
 };
 
@@ -52,7 +52,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.cap_l = align_up((size_t)(ceil_div(p->capacity, world) + 1), kBlockW);
   L.cap_off = align_up((size_t)p->capacity, kBlockOff);
   L.slots_max = (int)align_up((size_t)p->max_meas + 2, 2048);
-  L.zb_max = std::max(1, L.slots_max / 1024);
+  L.zb_max = std::max(1, L.slots_max / std::min(1024, kFuseGroup));  // P planes: one per CTA z-block / group
   L.part_cap = (int64_t)64 * sms * 256 + 8192;
   L.nbw_max = ceil_div(L.cap_l, kBlockW) + 1;
   L.nbo_max = ceil_div(L.cap_off, kBlockOff) + 1;
@@ -75,6 +75,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   for (int i = 0; i < 5; ++i) L.o_s[i] = take(sizeof(float) * L.slots_max);
   L.o_rep = take(sizeof(int32_t) * L.slots_max);
   L.o_C = take(sizeof(double) * (size_t)(p->max_meas + 1));
+  L.o_Cslot = take(sizeof(double) * (size_t)L.slots_max);
   L.o_D = take(sizeof(double) * (size_t)(p->max_meas + 1));
   L.o_acc = take(sizeof(double) * (5 * (size_t)p->max_meas + 2 * (size_t)world + 8));
   L.o_blk_w = take(sizeof(double) * L.nbw_max);
@@ -136,6 +137,8 @@ struct phd_ctx {
   int64_t n_local = 0, g0 = 0;
   int64_t n_surv_local = 0;
   int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zl = 4, zb = 0, gp = 0, M_z = -1;
+  bool fused = false;    // group-pipelined update (pass 1 of group j with pass 2 of group j-1)
+  double* C_slot = nullptr;
   int m_prev_ext = -1;   // >= 0: zprev holds an explicit Z_{k-1} of this size
   double W = 0, W_pred = 0;
   int64_t LT = 0;
@@ -404,6 +407,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->slot_label = at<int32_t>(c->ws, L.o_slot);
   c->rep = at<int32_t>(c->ws, L.o_rep);
   c->C = at<double>(c->ws, L.o_C);
+  c->C_slot = at<double>(c->ws, L.o_Cslot);
   c->D = at<double>(c->ws, L.o_D);
   c->acc = at<double>(c->ws, L.o_acc);
   c->blk_w = at<double>(c->ws, L.o_blk_w);
@@ -625,6 +629,18 @@ static void build_slots(phd_ctx* c, int M) {
     for (int l = 0; l < M; ++l) c->h_slot[n++] = l;
   }
   c->n_slots = n;
+  // group-pipelined update for large M: 4 slots/lane/pass, 4 warps,
+  // groups of 512 slots; otherwise the two-sweep path with 8 (or 4) slots per lane
+  // Opt-in (PHD_FUSE=1): measured neutral on B200 (49.6 vs 49.0 ms at cfg 5) because
+  // both passes are register-file-read bound, not pipe bound.
+  const char* fz = getenv("PHD_FUSE");
+  c->fused = n >= kFuseMinSlots && fz && fz[0] == '1';
+  if (c->fused) {
+    c->zl = 4;
+    c->wz = kFuseWarps;
+    c->zb = M > 0 ? (int)ceil_div(n, kFuseGroup) : 0;
+    c->slots_pad = (int)ceil_div(std::max(n, 1), kFuseGroup) * kFuseGroup;
+  } else {
   // slots per lane: 8 (halves the per-particle overheads) unless it pads much more than 4
   int best_zl = 4, best_wz = 2, best_zb = 1;
   int64_t best_pad = -1;
@@ -653,6 +669,7 @@ static void build_slots(phd_ctx* c, int M) {
   c->wz = best_wz;
   c->zb = M > 0 ? best_zb : 0;
   c->slots_pad = (int)best_pad;
+  }
   for (int s = n; s < c->slots_pad; ++s) c->h_slot[s] = -1;
 }
 
@@ -686,11 +703,14 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     SlotConsts sc{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
     KL(launch_zprep(c->model, c->zlab, c->slot_label, c->slots_pad, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->st));
   }
-  // particle-CTA count: one wave of resident CTAs over the z-blocks
+  // particle-CTA count: one wave of resident CTAs over the z-blocks of one sweep
   int gp = 0;
+  const int zb_sweep = c->fused ? 1 : c->zb;
   if (M > 0 && n > 0) {
-    int occ = std::max(1, std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl)));
-    int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / c->zb);
+    int occ = c->fused ? fused_occupancy(c->model, c->wz)
+                       : std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl));
+    occ = std::max(1, occ);
+    int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / zb_sweep);
     int64_t cap_gp = std::max<int64_t>(1, c->L.part_cap / c->slots_pad);
     gp = (int)std::min<int64_t>(std::min(want, cap_gp), tiles);
     int64_t tpc = ceil_div(tiles, gp);
@@ -717,14 +737,34 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   pa.P = c->P;
   pa.P_stride = c->L.cap_l;
   CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
+  // C of slots [s0, s1): fixed-order reduction, C1 all-reduce, per-slot constants
+  auto normalise = [&](int s0, int s1) -> phd_status {
+    KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, s0, s1, c->C_slot, c->st));
+    if (c->world > 1) COMM(c->comm->allreduce_f64(c->C_slot + s0, (size_t)(s1 - s0), c->st));
+    KL(launch_zconst(c->C_slot, c->slot_label, s0, s1, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+    return PHD_OK;
+  };
   timing_record(c, 3);
-  if (M > 0) {
+  if (M > 0 && c->fused) {
+    // group-pipelined sweeps: sweep j = pass 1 of group j + pass 2 of group j-1
+    const int Q = c->zb;
+    for (int j = 0; j <= Q; ++j) {
+      const bool h1 = j < Q, h2 = j >= 1;
+      if (gp > 0)
+        KL(launch_fused(c->model, h1, h2, pa, j * kFuseGroup, (j - 1) * kFuseGroup, j - 1, gp, 1, c->wz, c->st));
+      if (j == 0) timing_record(c, 4);
+      if (h1) {
+        phd_status st = normalise(j * kFuseGroup, (j + 1) * kFuseGroup);
+        if (st != PHD_OK) return st;
+      }
+      if (j == 0) timing_record(c, 5);
+    }
+    timing_record(c, 6);
+  } else if (M > 0) {
     if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 4);
-    KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, c->n_slots, c->slot_label, c->C, c->st));
-    if (gp == 0) CU(cudaMemsetAsync(c->C, 0, sizeof(double) * M, c->st));
-    if (c->world > 1) COMM(c->comm->allreduce_f64(c->C, (size_t)M, c->st));
-    KL(launch_zconst(c->C, M, c->kappa, c->slot_label, c->slots_pad, c->s[4], c->D, c->bad, c->st));
+    phd_status st = normalise(0, c->slots_pad);
+    if (st != PHD_OK) return st;
     timing_record(c, 5);
     if (gp > 0) KL(launch_pass(c->model, 2, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 6);
@@ -739,7 +779,6 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   double* rank_slots = c->acc + 5 * (size_t)M;
   KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->n_slots : 0, c->slot_label, c->C, c->D, c->s[0], c->s[1],
                        c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank, c->world, c->st));
-  if (M > 0 && gp == 0) CU(cudaMemsetAsync(c->acc, 0, sizeof(double) * 5 * M, c->st));
   if (c->world > 1)
     COMM(c->comm->allreduce_f64(c->acc, (size_t)(5 * M + 2 * c->world), c->st));
   CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 2 * c->world, cudaMemcpyDeviceToHost, c->st));

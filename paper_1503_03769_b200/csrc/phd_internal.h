@@ -10,6 +10,9 @@ namespace phd {
 // measurement slots per lane: 4 or 8 (kernel template), i.e. 128 or 256 per warp
 constexpr int kMaxWarpsZ = 8;                   // warps per CTA (each owns 128 slots)
 constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one particle per loader thread
+constexpr int kFuseGroup = 512;                 // slots per measurement group (group-pipelined update)
+constexpr int kFuseWarps = 4;                   // warps per CTA in the group-pipelined update (4 x 128 = 512)
+constexpr int kFuseMinSlots = 2048;             // use the group-pipelined update from 4 groups up
 constexpr int kTileP = 64;                      // particles per smem tile
 constexpr int kFlushTiles = 16;                 // fp32 mid-level -> fp64 every 16 tiles
 constexpr int kBlockW = 1024;                   // particles per finalize / scan block
@@ -89,10 +92,13 @@ cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_labe
                          float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s);
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
 int pass_occupancy(int model, int pass, int wz, int zl);
-cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
-                            double* C_lab, cudaStream_t s);
-cudaError_t launch_zconst(const double* C_lab, int M, double kappa, const int32_t* slot_label, int n_slots_pad,
-                          float* d_slot, double* D_lab, int* bad, cudaStream_t s);
+cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,
+                         int zbg, int wz, cudaStream_t s);
+int fused_occupancy(int model, int wz);
+cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
+                            cudaStream_t s);
+cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
+                          float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s);
 cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, int zb, int64_t n, float nu,
                             float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s);
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,

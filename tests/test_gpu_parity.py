@@ -34,10 +34,10 @@ def phd():
 
 POS = Model(meas=POSITION, sigma_z=(10.0, 10.0), p_d=0.98, p_s=0.99, clutter_rate=50.0,
             region=(-1000.0, 1000.0, -1000.0, 1000.0), births_per_step=256, fixed_count=8000,
-            count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=2048, seed=7)
+            count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=4096, seed=7)
 RB = Model(meas=RANGE_BEARING, sigma_z=(10.0, 0.01), p_d=0.98, p_s=0.99, clutter_rate=50.0,
            region=(0.0, 2000.0, -math.pi, math.pi), sensor_xy=(0.0, 0.0), births_per_step=256,
-           fixed_count=8000, count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=2048, seed=7)
+           fixed_count=8000, count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=4096, seed=7)
 ANISO = replace(POS, sigma_z=(7.0, 13.0))
 MODELS = {"position": POS, "range_bearing": RB, "aniso": ANISO}
 
@@ -126,7 +126,8 @@ def _check_update(orc, m, C, acc, wn, w, Co, wo, acco):
 
 
 @pytest.mark.parametrize("mname", ["position", "range_bearing", "aniso"])
-@pytest.mark.parametrize("n,M", [(64 * 37 + 19, 37), (64 * 150 + 5, 130), (20011, 600), (9000, 1100)])
+@pytest.mark.parametrize("n,M", [(64 * 37 + 19, 37), (64 * 150 + 5, 130), (20011, 600), (9000, 1100),
+                                 (7001, 2500)])
 def test_update_parity(phd, orc, mname, n, M):
     m = MODELS[mname]
     f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, n, M, seed=n + M)
@@ -386,3 +387,12 @@ def test_full_size_cfg5_sampled(phd, orc):
     share = meta["N_out"] * wn.astype(np.float64) / meta["W"]
     assert np.all(counts >= np.floor(share) - 1) and np.all(counts <= np.ceil(share) + 1)
     f.close()
+
+
+def test_group_pipelined_update_parity(phd, orc, monkeypatch):
+    """The opt-in group-pipelined update (PHD_FUSE=1) on both sensor models."""
+    monkeypatch.setenv("PHD_FUSE", "1")
+    for m in (POS, RB):
+        f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 9001, 2600, seed=5)
+        _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
+        f.close()
