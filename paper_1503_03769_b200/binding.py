@@ -75,8 +75,8 @@ def load(build_if_missing=True):
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if build_if_missing:
+    path = os.environ.get("PHD_LIB") or _build.LIB  # PHD_LIB: an alternate build (tuning experiments)
+    if build_if_missing and path == _build.LIB:
         _build.build()
     if not os.path.exists(path):
         raise OSError("libphd.so not built (%s); run __graft_entry__.build()" % path)

@@ -42,15 +42,18 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, out=None, extra=()):
+    """Compile every csrc/ source for sm_100a and link libphd.so (or `out` with
+    extra nvcc flags, for tuning experiments)."""
+    if out is None and not force and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(PKG, "build")
+    lib = out or LIB
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    objdir = os.path.join(PKG, "build", "default" if out is None else os.path.basename(lib))
     os.makedirs(objdir, exist_ok=True)
     inc, libd = nccl_dirs()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + inc]
+              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + inc] + list(extra)
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
@@ -68,14 +71,14 @@ def build(force=False, verbose=False):
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-L" + libd, "-l:libnccl.so.2",
                                                            "-Xlinker", "-rpath=" + libd]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed: %s\n%s" % (" ".join(cmd), r.stdout))
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -16,7 +16,18 @@
 // fp32 partial per (particle, z-block).  Cross-CTA sums are fp64 in fixed order.
 #include "phd_internal.h"
 
+#ifndef PHD_PP_UNROLL1
+#define PHD_PP_UNROLL1 8
+#endif
+#ifndef PHD_PP_UNROLL2
+#define PHD_PP_UNROLL2 4
+#endif
+
 namespace phd {
+
+// particles unrolled per lane in the pair loop (pass 1 / pass 2; measured on B200)
+constexpr int kPPUnroll1 = PHD_PP_UNROLL1;
+constexpr int kPPUnroll2 = PHD_PP_UNROLL2;
 
 __device__ __forceinline__ float ex2a(float x) {
   float y;
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
 #pragma unroll 1
     for (int p0 = 0; p0 < kTileP; p0 += 8) {
       float pe[8];
-#pragma unroll
+#pragma unroll(PASS == 1 ? kPPUnroll1 : kPPUnroll2)
       for (int pp = 0; pp < 8; ++pp) {
         const float* rec = rb + (p0 + pp) * L::WIDTH;
         // pass 1: (p_D c w, .); pass 2: (log2(p_D c w), .)
