@@ -347,9 +347,11 @@ def test_step_equals_staged_calls(phd):
 
 
 # ---------------------------------------------------------------------------
-# Full size (cfg 5, the bench launch configuration): sampled outputs + properties
-def test_full_size_cfg5_sampled(phd, orc):
-    cfg = scenario.get("cfg5")
+# Full size (configs 3-5 at their BASELINE sizes; cfg 5 is the bench launch
+# configuration): sampled outputs the oracle computes one by one + properties
+@pytest.mark.parametrize("cname", ["cfg3", "cfg4", "cfg5"])
+def test_full_size_sampled(phd, orc, cname):
+    cfg = scenario.get(cname)
     m = cfg.model
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
@@ -366,8 +368,8 @@ def test_full_size_cfg5_sampled(phd, orc):
     est, summ = f.extract()
     kap = orc.kappa(m)
     N = ps.shape[1]
-    assert N == 1 << 24 and M == 4096
-    # sampled normalisers: the oracle sums all 2^24 particles for 3 measurements
+    assert N == m.fixed_count + m.births_per_step
+    # sampled normalisers: the oracle sums all N particles for 3 measurements
     rng = np.random.default_rng(0)
     for p in rng.choice(M, 3, replace=False):
         Co = orc.normalizers(m, ps, pw, Z[0][p:p + 1])[0]
@@ -379,6 +381,12 @@ def test_full_size_cfg5_sampled(phd, orc):
     # mass identity at full size
     rhs = (1 - m.p_d) * summ["W_pred"] + math.fsum(C / (kap + C))
     assert abs(summ["W"] - rhs) <= 1e-5 * rhs
+    # estimates: zeta of the top labels against the oracle's weighted mean of all N particles
+    for i in range(min(2, len(est["labels"]))):
+        lab = int(est["labels"][i])
+        _, ao = orc.update(m, ps, pw, Z[0][lab:lab + 1], C[lab:lab + 1])
+        zeta = ao[0, 1:] / ao[0, 0]
+        assert np.all(np.abs(est["states"][i] - zeta) <= 1e-3)
     f.resample_exchange(1)
     anc, _ = f.ancestors()
     meta = f.resample_meta()
