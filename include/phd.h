@@ -66,6 +66,15 @@ typedef enum {
 typedef enum { PHD_MEAS_POSITION = 0, PHD_MEAS_RANGE_BEARING = 1 } phd_meas_model;
 typedef enum { PHD_COUNT_ADAPTIVE = 0, PHD_COUNT_FIXED = 1 } phd_count_mode;
 typedef enum { PHD_STAGE_RESAMPLED = 0, PHD_STAGE_PREDICTED = 1 } phd_stage;
+/* PHD_MODE_EXACT: global C (all-reduced), exact global systematic resampling with
+ *   an order-preserving rebalance -- the single-device particle PHD filter,
+ *   P-invariant (north_star hot path).
+ * PHD_MODE_DCP: the paper's DCPFPHD (§3, Algorithm 1, Steps 1-6): every
+ *   rank is a group with its own population, local C (Eq 11), local estimates
+ *   fused at rank 0 by the label vote of Step 4, local resampling to
+ *   max(LT_j,1) R (Algorithm 1) and the ring exchange of L particles of
+ *   Step 6.  With world = 1 both modes are identical. */
+typedef enum { PHD_MODE_EXACT = 0, PHD_MODE_DCP = 1 } phd_mode;
 
 /* Model and sizing parameters (§4 simulation model; values per
  * BASELINE.json configs).  All doubles; the kernels derive fp32 constants. */
@@ -90,6 +99,10 @@ typedef struct {
   int32_t max_meas;           /* max M per step, 1..65536 */
   int64_t capacity;           /* max global N = N_out + J */
   uint64_t seed;              /* Philox4x32-10 key {lo32, hi32} */
+  int32_t mode;               /* phd_mode */
+  int32_t reserved0;          /* must be 0 */
+  int64_t exchange_count;     /* DCP ring exchange L per step (0: floor(min_j N_j / 10));
+                                 clamped to floor(min_j N_j / 2) */
 } phd_params;
 
 /* One labelled estimate: label = measurement index, state =
@@ -156,6 +169,7 @@ phd_status phd_create_in_group(const phd_params* p, phd_group* g, int32_t rank, 
  * stage = PHD_STAGE_RESAMPLED: soa4/w are this rank's survivors (the part of its
  *   block below n_global), n_global = global survivor count N_out; the next
  *   call must be phd_predict.  w == NULL: every weight = mass / n_global.
+ *   DCP mode: every rank holds its own group; n_global is ignored (= n_local).
  * stage = PHD_STAGE_PREDICTED: soa4/w are this rank's whole block of a
  *   predicted array of n_global particles; the next call must be phd_update.
  * Errors: PHD_EINVAL (n_local does not match the block), PHD_ECAPACITY. */
@@ -190,6 +204,9 @@ phd_status phd_step(phd_ctx* ctx, int32_t k, const float* z, int32_t M, phd_esti
 phd_status phd_get_normalizers(phd_ctx* ctx, double* C, int32_t cap);
 /* Global STPHD accumulators [M][5] = (dW, Sx, Svx, Sy, Svy) (Eqs 16, 18), label order. */
 phd_status phd_get_accumulators(phd_ctx* ctx, double* acc, int32_t cap);
+/* DCP mode: this rank's local (pre-fusion) estimates of the last extract,
+ * sorted by (mass desc, label asc); n receives the count. */
+phd_status phd_get_local_estimates(phd_ctx* ctx, phd_estimate* out, int32_t cap, int32_t* n);
 /* Ancestors (global index into the updated array) of this rank's produced
  * offspring of the last resample, in global offspring order; n = count,
  * first = global offspring index of anc[0]. */

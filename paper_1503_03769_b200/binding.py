@@ -33,7 +33,8 @@ class Params(ctypes.Structure):
                 ("birth_mass", ctypes.c_double), ("birth_sigma_v", ctypes.c_double),
                 ("births_per_step", ctypes.c_int64), ("particles_per_target", ctypes.c_int64),
                 ("fixed_count", ctypes.c_int64), ("count_mode", ctypes.c_int32), ("max_meas", ctypes.c_int32),
-                ("capacity", ctypes.c_int64), ("seed", ctypes.c_uint64)]
+                ("capacity", ctypes.c_int64), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("exchange_count", ctypes.c_int64)]
 
 
 class Estimate(ctypes.Structure):
@@ -55,7 +56,7 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_extract", "phd_resample_exchange", "phd_step", "phd_get_normalizers", "phd_get_accumulators",
            "phd_get_ancestors", "phd_get_resample_meta", "phd_launch_count", "phd_set_timing", "phd_get_timing",
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
-           "phd_group_create", "phd_group_destroy", "phd_create_in_group"]
+           "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -108,6 +109,7 @@ def load(build_if_missing=True):
     L.phd_get_normalizers.argtypes = [_P, _D, ctypes.c_int32]
     L.phd_get_accumulators.argtypes = [_P, _D, ctypes.c_int32]
     L.phd_get_ancestors.argtypes = [_P, _I32, ctypes.c_int64, _I64, _I64]
+    L.phd_get_local_estimates.argtypes = [_P, ctypes.POINTER(Estimate), ctypes.c_int32, _I32]
     L.phd_get_resample_meta.argtypes = [_P, _D, _D, _I64, _D]
     L.phd_launch_count.argtypes = [_P]
     L.phd_launch_count.restype = ctypes.c_int64
@@ -143,6 +145,9 @@ def params_from(model):
     p.max_meas = int(model.max_meas)
     p.capacity = int(model.capacity)
     p.seed = int(model.seed)
+    p.mode = int(getattr(model, "mode", 0))
+    p.reserved0 = 0
+    p.exchange_count = int(getattr(model, "exchange_count", 0))
     return p
 
 
@@ -355,6 +360,16 @@ class Filter:
         self._check(self.L.phd_get_ancestors(self.h, a.ctypes.data_as(_I32), len(a), ctypes.byref(n),
                                              ctypes.byref(first)), "phd_get_ancestors")
         return a[:n.value], first.value
+
+    def local_estimates(self):
+        """DCP mode: this rank's pre-fusion estimates of the last extract."""
+        n = ctypes.c_int32()
+        buf = (Estimate * max(1, self.cap))()
+        self._check(self.L.phd_get_local_estimates(self.h, buf, self.cap, ctypes.byref(n)), "phd_get_local_estimates")
+        k = n.value
+        return {"labels": np.array([buf[i].label for i in range(k)], dtype=np.int32),
+                "states": np.array([list(buf[i].state) for i in range(k)], dtype=np.float32).reshape(k, 4),
+                "mass": np.array([buf[i].mass for i in range(k)], dtype=np.float32)}
 
     def resample_meta(self):
         W, U = ctypes.c_double(), ctypes.c_double()

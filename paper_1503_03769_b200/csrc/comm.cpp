@@ -41,6 +41,11 @@ class NcclComm : public Comm {
     return r == ncclSuccess ? "" : std::string("nccl exchange: ") + ncclGetErrorString(r);
   }
 
+  std::string allgather_bytes(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    ncclResult_t r = ncclAllGather(send, recv, bytes, ncclChar, c_, s);
+    return r == ncclSuccess ? "" : std::string("ncclAllGather: ") + ncclGetErrorString(r);
+  }
+
  private:
   ncclComm_t c_;
   int world_, rank_;
@@ -76,8 +81,9 @@ struct LocalGroup {
   std::vector<double*> bufs;
   std::vector<std::vector<float*>> srcs;
   std::vector<ExchangePlan> plans;
+  std::vector<const void*> gsrc;
 
-  explicit LocalGroup(int w) : world(w), bufs(w, nullptr), srcs(w), plans(w) {}
+  explicit LocalGroup(int w) : world(w), bufs(w, nullptr), srcs(w), plans(w), gsrc(w, nullptr) {}
 
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
@@ -142,6 +148,18 @@ class LocalComm : public Comm {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     g_->barrier();  // peers may reuse their source buffers only after every pull
     return e == cudaSuccess ? "" : std::string("local exchange: ") + cudaGetErrorString(e);
+  }
+
+  std::string allgather_bytes(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cudaGetErrorString(e);
+    g_->gsrc[rank_] = send;
+    g_->barrier();
+    for (int r = 0; r < g_->world && e == cudaSuccess; ++r)
+      e = cudaMemcpyAsync((char*)recv + r * bytes, g_->gsrc[r], bytes, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    g_->barrier();
+    return e == cudaSuccess ? "" : std::string("local allgather: ") + cudaGetErrorString(e);
   }
 
  private:

@@ -28,6 +28,8 @@ class Comm {
   // receive into dst[i] + recv_off[q] (recv_count[q] items) from rank q.
   virtual std::string exchange(float* const* src, float* const* dst, int narr, const ExchangePlan& p,
                                cudaStream_t s) = 0;
+  // recv[r * bytes .. ) = rank r's send[0 .. bytes) for every rank r (device buffers).
+  virtual std::string allgather_bytes(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
 };
 
 Comm* make_nccl_comm(const uint8_t* id128, int world, int rank, std::string* err);

@@ -18,8 +18,9 @@ __device__ __forceinline__ bool before(double wa, int la, double wb, int lb) {
 }
 
 __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc, int M, int n2,
-                                                  const double* __restrict__ rank_slots, int world, double p_d,
-                                                  EstOut* est, int cap, double* summary) {
+                                                  const double* __restrict__ Wv, const double* __restrict__ Wpv,
+                                                  int count, double p_d, EstOut* est, int cap, double* summary,
+                                                  int32_t* count_out) {
   extern __shared__ __align__(16) unsigned char sm[];
   double* kw = reinterpret_cast<double*>(sm);
   int* kl = reinterpret_cast<int*>(kw + n2);
@@ -63,9 +64,9 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
   __shared__ int snsel;
   if (tid == 0) {
     double W = 0.0, Wp = 0.0;
-    for (int r = 0; r < world; ++r) {
-      W += rank_slots[r];
-      Wp += rank_slots[world + r];
+    for (int r = 0; r < count; ++r) {
+      W += Wv[r];
+      Wp += Wpv[r];
     }
     long long LT = (long long)floor(W + 0.5);
     if (LT < 0) LT = 0;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
     summary[5] = (double)nsel;
     summary[6] = LT > n_elig ? 1.0 : 0.0;
     summary[7] = fabs(frac - 0.5) < 1e-4 * fmax(1.0, W) ? 1.0 : 0.0;
+    if (count_out) *count_out = (int32_t)nsel;
   }
   __syncthreads();
   for (int s = tid; s < snsel; s += nthr) {
@@ -95,9 +97,8 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
   }
 }
 
-cudaError_t launch_extract(const double* acc_lab, int M, const double* rank_slots, int world, double p_d, void* est,
-                           int cap, double* summary, int32_t* keys_tmp, cudaStream_t s) {
-  (void)keys_tmp;
+cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
+                           void* est, int cap, double* summary, int32_t* count_out, cudaStream_t s) {
   int n2 = 1;
   while (n2 < M) n2 <<= 1;
   size_t smem = (size_t)n2 * (sizeof(double) + sizeof(int));
@@ -106,8 +107,8 @@ cudaError_t launch_extract(const double* acc_lab, int M, const double* rank_slot
     cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 12);
     attr_set = true;
   }
-  k_extract<<<1, 1024, smem, s>>>(acc_lab, M, n2, rank_slots, world, p_d, reinterpret_cast<EstOut*>(est), cap,
-                                  summary);
+  k_extract<<<1, 1024, smem, s>>>(acc_lab, M, n2, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
+                                  count_out);
   return cudaGetLastError();
 }
 

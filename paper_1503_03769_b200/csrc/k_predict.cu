@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
   float x, vx, y, vy, w;
   if (g < a.n_out) {
     // Eq 5: x~ ~ f(.|x) (q = transition prior), w~ = e_{k|k-1} w.
-    U4 o = philox_at(a.seed, (uint64_t)g, (uint32_t)a.k, 1u);
+    U4 o = philox_at(a.seed, a.ctr_base + (uint64_t)g, (uint32_t)a.k, 1u);
     float u1 = u01(o.x), u2 = u01(o.y);
     float rad = sqrtf(-2.0f * logf(u1));
     float sn, cs;
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
   } else {
     // Eq 6: birth b ~ p_k(.|Z_{k-1}) with weight gamma / J_k.
     int64_t b = g - a.n_out;
-    U4 o = philox_at(a.seed, (uint64_t)g, (uint32_t)a.k, 2u);
+    U4 o = philox_at(a.seed, a.ctr_base + (uint64_t)g, (uint32_t)a.k, 2u);
     float u0 = u01(o.x), u1 = u01(o.y), u2 = u01(o.z), u3 = u01(o.w);
     float r01 = sqrtf(-2.0f * logf(u0)), r23 = sqrtf(-2.0f * logf(u2));
     float s1, c1, s2, c2;
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
     float n1 = r01 * c1, n2 = r01 * s1, n3 = r23 * c2, n4 = r23 * s2;
     float p0, p1;
     if (a.m_prev > 0) {
-      int64_t m = b % a.m_prev;
+      int64_t m = (a.birth_offset + b) % a.m_prev;
       p0 = a.zprev[2 * m] + a.sigma_z0 * n1;
       p1 = a.zprev[2 * m + 1] + a.sigma_z1 * n2;
     } else {

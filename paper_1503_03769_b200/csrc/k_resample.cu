@@ -259,4 +259,53 @@ cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_
   return cudaGetLastError();
 }
 
+// DCP ring exchange: the L slots s_i = floor(((i + v) n) / L)
+// of this group (fp64, one rounding per operation, as in the oracle).
+struct Arr5 {
+  float* p[5];
+};
+
+__device__ __forceinline__ int64_t ring_slot(int64_t i, int64_t n, int64_t L, double v) {
+  double t = __ddiv_rn(__dmul_rn(__dadd_rn((double)i, v), (double)n), (double)L);
+  return (int64_t)floor(t);
+}
+
+__global__ void k_ring_pack(Arr5 src, Arr5 dst, int narr, int64_t L, int64_t n, double v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  int64_t sl = ring_slot(i, n, L, v);
+  for (int q = 0; q < narr; ++q) dst.p[q][i] = src.p[q][sl];
+}
+
+__global__ void k_ring_unpack(Arr5 src, Arr5 dst, int narr, int64_t L, int64_t n, double v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  int64_t sl = ring_slot(i, n, L, v);
+  for (int q = 0; q < narr; ++q) dst.p[q][sl] = src.p[q][i];
+}
+
+cudaError_t launch_ring_pack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
+                             cudaStream_t s) {
+  if (L <= 0) return cudaSuccess;
+  Arr5 a{}, b{};
+  for (int q = 0; q < narr; ++q) {
+    a.p[q] = src[q];
+    b.p[q] = dst[q];
+  }
+  k_ring_pack<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(a, b, narr, L, n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
+                               cudaStream_t s) {
+  if (L <= 0) return cudaSuccess;
+  Arr5 a{}, b{};
+  for (int q = 0; q < narr; ++q) {
+    a.p[q] = src[q];
+    b.p[q] = dst[q];
+  }
+  k_ring_unpack<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(a, b, narr, L, n, v);
+  return cudaGetLastError();
+}
+
 }  // namespace phd

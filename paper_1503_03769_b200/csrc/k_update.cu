@@ -723,7 +723,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
                              const float* __restrict__ s1, const float* __restrict__ s2,
                              const float* __restrict__ s3, int model, const double* __restrict__ blk_w,
                              const double* __restrict__ blk_wp, int nb, double* acc_lab, double* rank_slots,
-                             int rank, int world) {
+                             int rank, int world, int lead) {
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double sa[256], sb[256];
     double a = 0.0, b = 0.0;
@@ -741,7 +741,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
       }
       __syncthreads();
     }
-    for (int r = threadIdx.x; r < 2 * world; r += blockDim.x) rank_slots[r] = 0.0;
+    for (int r = threadIdx.x; r < 3 * world; r += blockDim.x) rank_slots[r] = 0.0;
     __syncthreads();
     if (threadIdx.x == 0) {
       rank_slots[rank] = sa[0];
@@ -771,7 +771,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
   }
   // C (hence dW) is already global: only rank 0 contributes the dW and centre
   // terms, every rank its own centred partial sums (the C2 all-reduce adds them).
-  double dW = rank == 0 ? C_lab[lab] * inv : 0.0;
+  double dW = lead ? C_lab[lab] * inv : 0.0;
   double* o = acc_lab + 5 * (int64_t)lab;
   o[0] = dW;
   o[1] = A[0] * inv + cx * dW;
@@ -783,10 +783,11 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1,
                               const float* s2, const float* s3, int model, const double* blk_w, const double* blk_wp,
-                              int nb, double* acc_lab, double* rank_slots, int rank, int world, cudaStream_t s) {
+                              int nb, double* acc_lab, double* rank_slots, int rank, int world, int lead,
+                              cudaStream_t s) {
   int blocks = (n_slots + 255) / 256 + 1;
   k_reduce_acc<<<blocks, 256, 0, s>>>(Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
-                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world);
+                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,7 @@
 //   resample  k_scan_blocks -> k_resample_mark -> k_block_max -> k_scan_max -> k_gather
 //   exchange  world 1: buffer swap; world > 1: grouped ncclSend/ncclRecv (C3)
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -39,7 +40,7 @@ struct Layout {
   size_t total = 0;
   // byte offsets
   size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_D,
-      o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_summ, o_bad;
+      o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_gather, o_ring, o_summ, o_bad;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -77,14 +78,16 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_C = take(sizeof(double) * (size_t)(p->max_meas + 1));
   L.o_Cslot = take(sizeof(double) * (size_t)L.slots_max);
   L.o_D = take(sizeof(double) * (size_t)(p->max_meas + 1));
-  L.o_acc = take(sizeof(double) * (5 * (size_t)p->max_meas + 2 * (size_t)world + 8));
+  L.o_acc = take(sizeof(double) * (5 * (size_t)p->max_meas + 3 * (size_t)world + 8));
+  L.o_ring = take(sizeof(double) * ((size_t)world + 8));
   L.o_blk_w = take(sizeof(double) * L.nbw_max);
   L.o_blk_wp = take(sizeof(double) * L.nbw_max);
   L.o_blk_off = take(sizeof(double) * (L.nbw_max + 1));
   L.o_marks = take(sizeof(int32_t) * L.cap_off);
   L.o_bmax = take(sizeof(int32_t) * L.nbo_max);
   L.o_anc = take(sizeof(int32_t) * L.cap_off);
-  L.o_est = take(sizeof(phd_estimate) * (size_t)(p->max_meas + 1));
+  L.o_est = take(sizeof(phd_estimate) * (size_t)(p->max_meas + 1));  // [0] header (count), [1..] estimates
+  L.o_gather = take(p->mode == PHD_MODE_DCP ? sizeof(phd_estimate) * (size_t)(p->max_meas + 1) * world : 256);
   L.o_summ = take(sizeof(double) * 16);
   L.o_bad = take(sizeof(int) * 4);
   L.total = off;
@@ -121,7 +124,12 @@ struct phd_ctx {
   double *C, *D, *acc;
   double *blk_w, *blk_wp, *blk_off;
   int32_t *marks, *bmax, *anc;
-  phd_estimate* est;
+  phd_estimate* est;      // gather block: est[0].label = count, est[1..] = estimates
+  phd_estimate* gather;   // DCP: every rank's gather block
+  phd_estimate* h_gather = nullptr;
+  double* ring = nullptr;   // DCP: per-rank offspring counts (one-hot all-reduce)
+  std::vector<phd_estimate> local_est;
+  bool dcp = false;
   double* summ;
   int* bad;
   // pinned host staging
@@ -142,6 +150,7 @@ struct phd_ctx {
   int m_prev_ext = -1;   // >= 0: zprev holds an explicit Z_{k-1} of this size
   double W = 0, W_pred = 0;
   int64_t LT = 0;
+  int64_t N_all = 0;      // particles updated over all ranks
   std::vector<double> Wr, Wpr;
   int bad_flag = 0;
   int near_half = 0;
@@ -149,6 +158,7 @@ struct phd_ctx {
   double U_last = 0, W_last = 0;
   int64_t N_out_last = 0, prod_first = 0, prod_n = 0;
   int count_clamped = 0, zero_mass = 0;
+  int64_t ring_L = 0;
   // timing
   bool timing = false;
   cudaEvent_t ev[16] = {};
@@ -225,6 +235,9 @@ phd_status validate(const phd_params* p, int world, phd_ctx* c) {
   } else {
     return fail(c, PHD_EINVAL, "count_mode %d", p->count_mode);
   }
+  if (p->mode != PHD_MODE_EXACT && p->mode != PHD_MODE_DCP) return fail(c, PHD_EINVAL, "mode %d", p->mode);
+  if (p->reserved0 != 0) return fail(c, PHD_EINVAL, "reserved0 must be 0");
+  if (p->exchange_count < 0) return fail(c, PHD_EINVAL, "exchange_count < 0");
   if (world < 1) return fail(c, PHD_EINVAL, "world < 1");
   return PHD_OK;
 }
@@ -237,6 +250,13 @@ T* at(char* base, size_t off) {
 void timing_record(phd_ctx* c, int i) {
   if (c->timing) cudaEventRecord(c->ev[i], c->st);
 }
+
+// DCP: the births of group `rank` are the block [jlo, jhi) of the J births (Step 1).
+void group_births(const phd_ctx* c, int64_t* jlo, int64_t* jhi) {
+  block_of(c->p.births_per_step, c->world, c->rank, jlo, jhi);
+}
+
+uint64_t dcp_space(const phd_ctx* c) { return ((uint64_t)0x40000000u << 32) | (uint64_t)c->rank; }
 
 }  // namespace
 
@@ -417,10 +437,14 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->bmax = at<int32_t>(c->ws, L.o_bmax);
   c->anc = at<int32_t>(c->ws, L.o_anc);
   c->est = at<phd_estimate>(c->ws, L.o_est);
+  c->gather = at<phd_estimate>(c->ws, L.o_gather);
+  c->ring = at<double>(c->ws, L.o_ring);
+  c->dcp = p->mode == PHD_MODE_DCP;
   c->summ = at<double>(c->ws, L.o_summ);
   c->bad = at<int>(c->ws, L.o_bad);
-  CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (32 + 2 * world)));
+  CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (40 + 4 * world)));
   CUB(cudaMallocHost(&c->h_est, sizeof(phd_estimate) * (p->max_meas + 1)));
+  if (c->dcp) CUB(cudaMallocHost(&c->h_gather, sizeof(phd_estimate) * (p->max_meas + 1) * world));
   CUB(cudaMallocHost(&c->h_z, sizeof(float) * 2 * (p->max_meas + 1)));
   CUB(cudaMallocHost(&c->h_slot, sizeof(int32_t) * L.slots_max));
   for (int i = 0; i < 16; ++i) CUB(cudaEventCreate(&c->ev[i]));
@@ -472,6 +496,7 @@ void phd_destroy(phd_ctx* c) {
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->h_meta) cudaFreeHost(c->h_meta);
   if (c->h_est) cudaFreeHost(c->h_est);
+  if (c->h_gather) cudaFreeHost(c->h_gather);
   if (c->h_z) cudaFreeHost(c->h_z);
   if (c->h_slot) cudaFreeHost(c->h_slot);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
@@ -501,13 +526,23 @@ phd_status phd_set_particles(phd_ctx* c, const float* soa4, const float* w, int6
   cudaSetDevice(c->device);
   c->err.clear();
   int64_t J = c->p.births_per_step;
-  int64_t Nblk = stage == PHD_STAGE_PREDICTED ? n_global : n_global + J;
-  if (n_global < 0 || Nblk > c->p.capacity) return fail(c, PHD_ECAPACITY, "n_global %lld exceeds capacity", (long long)n_global);
-  int64_t lo, hi;
-  block_of(Nblk, c->world, c->rank, &lo, &hi);
-  int64_t expect = stage == PHD_STAGE_PREDICTED ? hi - lo : std::max<int64_t>(0, std::min(hi, n_global) - std::min(lo, n_global));
-  if (n_local != expect)
-    return fail(c, PHD_EINVAL, "n_local %lld != %lld (rank block of %lld)", (long long)n_local, (long long)expect, (long long)Nblk);
+  int64_t lo = 0, hi = 0;
+  if (c->dcp) {
+    // every rank is a group with its own population (n_global ignored)
+    int64_t jlo, jhi;
+    group_births(c, &jlo, &jhi);
+    n_global = n_local;
+    int64_t need = stage == PHD_STAGE_PREDICTED ? n_local : n_local + (jhi - jlo);
+    if (n_local < 0 || need > c->L.cap_l - 1) return fail(c, PHD_ECAPACITY, "group size %lld exceeds capacity", (long long)need);
+    hi = n_local;
+  } else {
+    int64_t Nblk = stage == PHD_STAGE_PREDICTED ? n_global : n_global + J;
+    if (n_global < 0 || Nblk > c->p.capacity) return fail(c, PHD_ECAPACITY, "n_global %lld exceeds capacity", (long long)n_global);
+    block_of(Nblk, c->world, c->rank, &lo, &hi);
+    int64_t expect = stage == PHD_STAGE_PREDICTED ? hi - lo : std::max<int64_t>(0, std::min(hi, n_global) - std::min(lo, n_global));
+    if (n_local != expect)
+      return fail(c, PHD_EINVAL, "n_local %lld != %lld (rank block of %lld)", (long long)n_local, (long long)expect, (long long)Nblk);
+  }
   for (int i = 0; i < 4; ++i)
     CU(cudaMemcpyAsync(c->A[i], soa4 + (size_t)i * n_local, sizeof(float) * n_local, cudaMemcpyDefault, c->st));
   if (w) {
@@ -537,8 +572,8 @@ phd_status phd_get_particles(phd_ctx* c, float* soa4, float* w, int64_t cap, int
   cudaSetDevice(c->device);
   int64_t n, g0;
   if (c->stage == kResampled) {
-    int64_t lo, hi;
-    block_of(c->n_out + c->p.births_per_step, c->world, c->rank, &lo, &hi);
+    int64_t lo = 0, hi;
+    if (!c->dcp) block_of(c->n_out + c->p.births_per_step, c->world, c->rank, &lo, &hi);
     n = c->n_surv_local;
     g0 = lo;
   } else {
@@ -574,14 +609,29 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
     mp = c->M_z;
   }
   int64_t J = c->p.births_per_step;
-  c->N = c->n_out + J;
-  block_of(c->N, c->world, c->rank, &c->g0, &c->n_local);
-  c->n_local -= c->g0;
   PredictArgs a{};
+  if (c->dcp) {
+    // group-local array [survivors, births of this group]; own Philox counter space
+    int64_t jlo, jhi;
+    group_births(c, &jlo, &jhi);
+    c->N = c->n_out + (jhi - jlo);
+    c->g0 = 0;
+    c->n_local = c->N;
+    if (c->N > c->L.cap_l - 1) return fail(c, PHD_ECAPACITY, "group size %lld exceeds capacity", (long long)c->N);
+    a.ctr_base = c->world > 1 ? ((uint64_t)(0x40000000u + (uint32_t)c->rank)) << 32 : 0;  // c3 = 0x40000000 + j
+    a.birth_offset = jlo;
+    a.J = jhi - jlo;
+  } else {
+    c->N = c->n_out + J;
+    block_of(c->N, c->world, c->rank, &c->g0, &c->n_local);
+    c->n_local -= c->g0;
+    a.ctr_base = 0;
+    a.birth_offset = 0;
+    a.J = J;
+  }
   a.n_local = c->n_local;
   a.g0 = c->g0;
   a.n_out = c->n_out;
-  a.J = J;
   a.k = k;
   a.seed = c->p.seed;
   a.T = (float)c->p.T;
@@ -740,7 +790,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   // C of slots [s0, s1): fixed-order reduction, C1 all-reduce, per-slot constants
   auto normalise = [&](int s0, int s1) -> phd_status {
     KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, s0, s1, c->C_slot, c->st));
-    if (c->world > 1) COMM(c->comm->allreduce_f64(c->C_slot + s0, (size_t)(s1 - s0), c->st));
+    if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot + s0, (size_t)(s1 - s0), c->st));
     KL(launch_zconst(c->C_slot, c->slot_label, s0, s1, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
     return PHD_OK;
   };
@@ -778,22 +828,33 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     KL(launch_finalize(c->A[4], c->P, c->L.cap_l, M > 0 && gp > 0 ? c->zb : 0, n, c->nu, c->wscale, c->wn, c->blk_w, c->blk_wp, c->st));
   double* rank_slots = c->acc + 5 * (size_t)M;
   KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->n_slots : 0, c->slot_label, c->C, c->D, c->s[0], c->s[1],
-                       c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank, c->world, c->st));
-  if (c->world > 1)
-    COMM(c->comm->allreduce_f64(c->acc, (size_t)(5 * M + 2 * c->world), c->st));
-  CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 2 * c->world, cudaMemcpyDeviceToHost, c->st));
-  CU(cudaMemcpyAsync(c->h_meta + 2 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
+                       c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank, c->world,
+                       c->dcp || c->rank == 0 ? 1 : 0, c->st));
+  // rank slots [W_r | W_pred_r | N_r] (3 per rank); N_r written from the host
+  c->h_meta[3 * c->world + 16] = (double)n;
+  CU(cudaMemcpyAsync(rank_slots + 2 * c->world + c->rank, c->h_meta + 3 * c->world + 16, sizeof(double),
+                     cudaMemcpyHostToDevice, c->st));
+  if (c->world > 1) {
+    if (c->dcp)  // groups keep their own accumulators; only the per-group masses are shared
+      COMM(c->comm->allreduce_f64(rank_slots, (size_t)(3 * c->world), c->st));
+    else
+      COMM(c->comm->allreduce_f64(c->acc, (size_t)(5 * M + 3 * c->world), c->st));
+  }
+  CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 3 * c->world, cudaMemcpyDeviceToHost, c->st));
+  CU(cudaMemcpyAsync(c->h_meta + 3 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
   timing_record(c, 7);
   CU(cudaStreamSynchronize(c->st));
   c->W = 0.0;
   c->W_pred = 0.0;
+  c->N_all = 0;
   for (int r = 0; r < c->world; ++r) {
     c->Wr[r] = c->h_meta[r];
     c->Wpr[r] = c->h_meta[c->world + r];
     c->W += c->Wr[r];
     c->W_pred += c->Wpr[r];
+    c->N_all += (int64_t)c->h_meta[2 * c->world + r];
   }
-  c->bad_flag = reinterpret_cast<int*>(c->h_meta + 2 * c->world)[0];
+  c->bad_flag = reinterpret_cast<int*>(c->h_meta + 3 * c->world)[0];
   c->LT = (int64_t)std::floor(c->W + 0.5);
   if (c->LT < 0) c->LT = 0;
   double frac = c->W - std::floor(c->W);
@@ -822,6 +883,57 @@ static int64_t next_count(phd_ctx* c, int* clamped) {
   return want;
 }
 
+static int64_t next_count_dcp(phd_ctx* c, int* clamped) {
+  // Algorithm 1: the group resamples into N_k(j) R_k = max(LT_j, 1) R particles
+  // (fixed-count configs: the group's block of N_out)
+  *clamped = 0;
+  if (c->p.count_mode == PHD_COUNT_FIXED) {
+    int64_t lo, hi;
+    block_of(c->p.fixed_count, c->world, c->rank, &lo, &hi);
+    return hi - lo;
+  }
+  int64_t jlo, jhi;
+  group_births(c, &jlo, &jhi);
+  int64_t LT = (int64_t)std::floor(c->Wr[c->rank] + 0.5);
+  int64_t want = std::max<int64_t>(LT, 1) * c->p.particles_per_target;
+  int64_t lim = c->L.cap_l - 1 - (jhi - jlo);
+  if (want > lim) {
+    *clamped = 1;
+    want = lim;
+  }
+  return want;
+}
+
+// Step 4: keep a label reported by more than half of the groups,
+// state = mean of the supporters' states (fp64), mass = mean of their dW.  Labels ascending.
+static int fuse_estimates(phd_ctx* c, phd_estimate* out, int cap) {
+  const int cap1 = c->p.max_meas + 1;
+  std::vector<int> cnt(c->p.max_meas, 0);
+  std::vector<double> acc((size_t)c->p.max_meas * 5, 0.0);
+  for (int r = 0; r < c->world; ++r) {
+    const phd_estimate* blk = c->h_gather + (size_t)r * cap1;
+    int n = blk[0].label;
+    for (int i = 0; i < n; ++i) {
+      const phd_estimate& e = blk[1 + i];
+      if (e.label < 0 || e.label >= c->p.max_meas) continue;
+      cnt[e.label] += 1;
+      for (int q = 0; q < 4; ++q) acc[5 * (size_t)e.label + q] += (double)e.state[q];
+      acc[5 * (size_t)e.label + 4] += (double)e.mass;
+    }
+  }
+  int k = 0;
+  for (int l = 0; l < c->p.max_meas && k < cap; ++l) {
+    if (2 * cnt[l] <= c->world) continue;
+    phd_estimate e;
+    e.label = l;
+    for (int q = 0; q < 4; ++q) e.state[q] = (float)(acc[5 * (size_t)l + q] / cnt[l]);
+    e.mass = (float)(acc[5 * (size_t)l + 4] / cnt[l]);
+    if (out) out[k] = e;
+    ++k;
+  }
+  return k;
+}
+
 phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s) {
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
@@ -829,17 +941,47 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_extract needs an updated population");
   int nest = 0;
   int lt_clamped = 0;
-  if (c->rank == 0) {
+  double* rank_slots = c->acc + 5 * (size_t)c->M;
+  double* smh = c->h_meta + 3 * c->world + 4;
+  if (c->dcp) {
+    // every group extracts locally (Step 3); the CU (rank 0) fuses (Step 4)
+    timing_record(c, 8);
+    const int capd = c->p.max_meas;
+    KL(launch_extract(c->acc, c->M, rank_slots + c->rank, rank_slots + c->world + c->rank, 1, c->p.p_d, c->est + 1,
+                      capd, c->summ, &c->est[0].label, c->st));
+    CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
+    if (c->world > 1)
+      COMM(c->comm->allgather_bytes(c->est, c->gather, sizeof(phd_estimate) * (size_t)(c->p.max_meas + 1), c->st));
+    CU(cudaStreamSynchronize(c->st));
+    const int nloc = (int)smh[5];
+    lt_clamped = (int)smh[6];
+    c->local_est.resize(nloc);
+    if (nloc > 0)
+      CU(cudaMemcpyAsync(c->local_est.data(), c->est + 1, sizeof(phd_estimate) * nloc, cudaMemcpyDeviceToHost, c->st));
+    if (c->rank == 0) {
+      if (c->world > 1) {
+        CU(cudaMemcpyAsync(c->h_gather, c->gather, sizeof(phd_estimate) * (size_t)(c->p.max_meas + 1) * c->world,
+                           cudaMemcpyDeviceToHost, c->st));
+      } else {
+        CU(cudaMemcpyAsync(c->h_gather, c->est, sizeof(phd_estimate) * (size_t)(c->p.max_meas + 1),
+                           cudaMemcpyDeviceToHost, c->st));
+      }
+    }
+    CU(cudaStreamSynchronize(c->st));
+    if (c->rank == 0) nest = fuse_estimates(c, out, std::max(0, cap));
+    timing_record(c, 9);
+    if (c->timing) cudaEventElapsedTime(&c->t_ms[4], c->ev[8], c->ev[9]);
+  } else if (c->rank == 0) {
     timing_record(c, 8);
     int capd = std::max(0, std::min(cap, c->p.max_meas));
-    KL(launch_extract(c->acc, c->M, c->acc + 5 * (size_t)c->M, c->world, c->p.p_d, c->est, capd, c->summ, nullptr, c->st));
-    CU(cudaMemcpyAsync(c->h_meta + 2 * c->world + 4, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
+    KL(launch_extract(c->acc, c->M, rank_slots, rank_slots + c->world, c->world, c->p.p_d, c->est + 1, capd, c->summ,
+                      &c->est[0].label, c->st));
+    CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
-    const double* sm = c->h_meta + 2 * c->world + 4;
-    nest = (int)sm[5];
-    lt_clamped = (int)sm[6];
+    nest = (int)smh[5];
+    lt_clamped = (int)smh[6];
     if (nest > 0 && out) {
-      CU(cudaMemcpyAsync(c->h_est, c->est, sizeof(phd_estimate) * nest, cudaMemcpyDeviceToHost, c->st));
+      CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * nest, cudaMemcpyDeviceToHost, c->st));
       CU(cudaStreamSynchronize(c->st));
       memcpy(out, c->h_est, sizeof(phd_estimate) * nest);
     }
@@ -853,8 +995,8 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     s->W_pred = c->W_pred;
     s->undetected_mass = (1.0 - c->p.p_d) * c->W_pred;
     s->LT = c->LT;
-    s->N = c->N;
-    s->N_out = next_count(c, &clamped);
+    s->N = c->dcp ? c->N_all : c->N;
+    s->N_out = c->dcp ? next_count_dcp(c, &clamped) : next_count(c, &clamped);
     s->M = c->M;
     s->n_est = nest;
     s->lt_clamped = lt_clamped;
@@ -865,6 +1007,14 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
   return PHD_OK;
 }
 
+phd_status phd_get_local_estimates(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n) {
+  if (!c) return PHD_EINVAL;
+  int k = (int)std::min<size_t>(c->local_est.size(), (size_t)std::max(0, cap));
+  if (n) *n = (int32_t)c->local_est.size();
+  if (out && k > 0) memcpy(out, c->local_est.data(), sizeof(phd_estimate) * k);
+  return PHD_OK;
+}
+
 phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
@@ -872,30 +1022,40 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_resample_exchange needs an updated population");
   timing_record(c, 10);
   int clamped = 0;
-  const int64_t n_out = next_count(c, &clamped);
+  const int64_t n_out = c->dcp ? next_count_dcp(c, &clamped) : next_count(c, &clamped);
   c->count_clamped = clamped;
   const int64_t J = c->p.births_per_step;
-  U4 o = philox_at(c->p.seed, 0, (uint32_t)k, 3u);
+  // systematic-resampling offset: one U shared by all ranks (exact mode); one per group (DCP, K > 1)
+  U4 o = (c->dcp && c->world > 1) ? philox_at(c->p.seed, dcp_space(c), (uint32_t)k, 3u)
+                                  : philox_at(c->p.seed, 0, (uint32_t)k, 3u);
   const double U = u52(o.x, o.y);
-  const double W = c->W;
+  const double W = c->dcp ? c->Wr[c->rank] : c->W;
   c->zero_mass = !(W > 0.0);
   std::vector<int64_t> bounds(c->world + 1);
-  if (!c->zero_mass) {
-    phd_resample_bounds(c->world, c->Wr.data(), n_out, U, bounds.data(), nullptr);
-  } else {
-    // W == 0: offspring j copies particle floor(j N / n_out), produced by its owner
-    for (int r = 0; r <= c->world; ++r) {
-      int64_t lo, hi;
-      block_of(c->N, c->world, std::min(r, c->world - 1), &lo, &hi);
-      int64_t g = r == c->world ? c->N : lo;
-      bounds[r] = (int64_t)(((__int128)g * n_out + c->N - 1) / c->N);
-    }
-    bounds[c->world] = n_out;
-  }
-  const int64_t lo = bounds[c->rank], hi = bounds[c->rank + 1];
-  const int64_t nprod = hi - lo;
   double O_r = 0.0;
-  for (int r = 0; r < c->rank; ++r) O_r += c->Wr[r];
+  int64_t lo, hi;
+  if (c->dcp) {
+    // local resampling of the group (Step 5)
+    lo = 0;
+    hi = n_out;
+  } else {
+    if (!c->zero_mass) {
+      phd_resample_bounds(c->world, c->Wr.data(), n_out, U, bounds.data(), nullptr);
+    } else {
+      // W == 0: offspring j copies particle floor(j N / n_out), produced by its owner
+      for (int r = 0; r <= c->world; ++r) {
+        int64_t blo, bhi;
+        block_of(c->N, c->world, std::min(r, c->world - 1), &blo, &bhi);
+        int64_t g = r == c->world ? c->N : blo;
+        bounds[r] = (int64_t)(((__int128)g * n_out + c->N - 1) / c->N);
+      }
+      bounds[c->world] = n_out;
+    }
+    lo = bounds[c->rank];
+    hi = bounds[c->rank + 1];
+    for (int r = 0; r < c->rank; ++r) O_r += c->Wr[r];
+  }
+  const int64_t nprod = hi - lo;
   const float w_off = n_out > 0 ? (float)(W / (double)n_out) : 0.0f;
   const int64_t n = c->n_local;
   const int nbw = (int)ceil_div(n, kBlockW);
@@ -919,10 +1079,49 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     KL(launch_scan_max(c->bmax, nbo, c->st));
   }
   KL(launch_gather(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, c->B[0], c->B[1],
-                   c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->N, n_out, c->st));
+                   c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->dcp ? c->n_local : c->N, n_out, c->st));
   timing_record(c, 11);
   // exchange: the next step's survivors [0, n_out) are block-partitioned over N' = n_out + J
-  if (c->world == 1) {
+  if (c->dcp) {
+    for (int i = 0; i < 5; ++i) std::swap(c->A[i], c->B[i]);
+    c->n_surv_local = n_out;
+    if (c->world > 1) {
+      // Step 6 ring exchange: L particles to rank+1, refill the same
+      // slots from rank-1 (swap semantics); L is common to all groups
+      for (int r = 0; r < c->world; ++r) c->h_meta[3 * c->world + 20 + r] = r == c->rank ? (double)n_out : 0.0;
+      CU(cudaMemcpyAsync(c->ring, c->h_meta + 3 * c->world + 20, sizeof(double) * c->world, cudaMemcpyHostToDevice,
+                         c->st));
+      COMM(c->comm->allreduce_f64(c->ring, (size_t)c->world, c->st));
+      CU(cudaMemcpyAsync(c->h_meta + 3 * c->world + 20, c->ring, sizeof(double) * c->world, cudaMemcpyDeviceToHost,
+                         c->st));
+      CU(cudaStreamSynchronize(c->st));
+      int64_t n_min = INT64_MAX;
+      for (int r = 0; r < c->world; ++r) n_min = std::min<int64_t>(n_min, (int64_t)c->h_meta[3 * c->world + 20 + r]);
+      int64_t L = c->p.exchange_count > 0 ? c->p.exchange_count : n_min / 10;
+      L = std::min<int64_t>(L, n_min / 2);
+      c->ring_L = L;
+      if (L > 0) {
+        U4 v4 = philox_at(c->p.seed, dcp_space(c), (uint32_t)k, 4u);
+        const double v = u52(v4.x, v4.y);
+        float* sendb[5];
+        float* recvb[5];
+        for (int i = 0; i < 5; ++i) {
+          sendb[i] = c->B[i];
+          recvb[i] = c->B[i] + L;
+        }
+        KL(launch_ring_pack(c->A, sendb, 5, L, n_out, v, c->st));
+        ExchangePlan plan;
+        plan.send_count.assign(c->world, 0);
+        plan.send_off.assign(c->world, 0);
+        plan.recv_count.assign(c->world, 0);
+        plan.recv_off.assign(c->world, 0);
+        plan.send_count[(c->rank + 1) % c->world] = L;
+        plan.recv_count[(c->rank + c->world - 1) % c->world] = L;
+        COMM(c->comm->exchange(sendb, recvb, 5, plan, c->st));
+        KL(launch_ring_unpack(recvb, c->A, 5, L, n_out, v, c->st));
+      }
+    }
+  } else if (c->world == 1) {
     for (int i = 0; i < 5; ++i) std::swap(c->A[i], c->B[i]);
     c->n_surv_local = n_out;
   } else {

@@ -59,6 +59,8 @@ struct PredictArgs {
   int64_t J;                 // births per step
   int32_t k;
   uint64_t seed;
+  uint64_t ctr_base;         // Philox counter of local slot i is ctr_base + g0 + i (DCP groups: own space)
+  int64_t birth_offset;      // global index of this rank's first birth (measurement choice b mod M)
   float T, sigma_a, p_s;
   float w_uniform;           // >= 0: survivors' weight before predict; < 0: read w
   int meas;
@@ -104,10 +106,16 @@ cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, in
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1, const float* s2,
                               const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
-                              double* acc_lab, double* rank_slots, int rank, int world, cudaStream_t s);
-cudaError_t launch_extract(const double* acc_lab, int M, const double* rank_slots, int world, double p_d,
-                           void* est /*phd_estimate*/, int cap, double* summary /*[8]*/, int32_t* keys_tmp,
+                              double* acc_lab, double* rank_slots, int rank, int world, int lead, cudaStream_t s);
+// W = sum_{r < count} W[r], W_pred = sum Wp[r]; writes the estimates to est[0..)
+// and their count to *count_out (the header entry of the gather block).
+cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
+                           void* est /*phd_estimate*/, int cap, double* summary /*[8]*/, int32_t* count_out,
                            cudaStream_t s);
+cudaError_t launch_ring_pack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
+                             cudaStream_t s);
+cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
+                               cudaStream_t s);
 cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s);
 cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s);
 cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cudaStream_t s);

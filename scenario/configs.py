@@ -10,6 +10,8 @@ import math
 
 POSITION = 0
 RANGE_BEARING = 1
+MODE_EXACT = 0
+MODE_DCP = 1
 COUNT_ADAPTIVE = 0
 COUNT_FIXED = 1
 
@@ -35,6 +37,8 @@ class Model:
     capacity: int = 1 << 16        # max N (global) = max N_out + J
     max_meas: int = 1024
     seed: int = 1
+    mode: int = 0                  # 0 exact (global C, exact resampling), 1 DCP (paper-literal groups)
+    exchange_count: int = 0        # DCP ring exchange L (0: min_j N_j / 10)
 
 
 @dataclass(frozen=True)

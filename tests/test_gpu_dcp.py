@@ -1,0 +1,175 @@
+"""Paper-literal DCPFPHD mode (PHD_MODE_DCP; §3) vs the K-group oracle
+(oracle/dcp.py), stage by stage on the GPU's own previous-step groups (-m gpu).
+
+K groups = K rank contexts of one process (in-process rank group, one thread
+per rank).  Checked per group and step: predicted survivors and births, the
+group-local normaliser C_j (rel 1e-5), weights (rel 1e-4), local estimates
+(labels exact on the GPU accumulators), the CU's fused estimates (Step 4),
+resampled ancestors (bit-exact except counted near-ties) and the ring exchange
+(exact copies into the oracle's slots)."""
+import math
+import threading
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import scenario
+from scenario.configs import COUNT_ADAPTIVE, COUNT_FIXED, MODE_DCP, POSITION
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def phd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1503_03769_b200 as p
+    p.load()
+    return p
+
+
+def _near_ties(w, U, n_out, tol=1e-9):
+    B = np.cumsum(np.asarray(w, np.float64))
+    t = (np.arange(n_out) + U) * B[-1] / n_out
+    idx = np.searchsorted(B, t)
+    d = np.full(n_out, np.inf)
+    for off in (-1, 0):
+        k = np.clip(idx + off, 0, len(B) - 1)
+        d = np.minimum(d, np.abs(B[k] - t))
+    return d <= tol
+
+
+def _run_parallel(fns):
+    errs = []
+
+    def wrap(f):
+        try:
+            f()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+    th = [threading.Thread(target=wrap, args=(f,)) for f in fns]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not errs, errs
+
+
+@pytest.mark.parametrize("K,cname", [(1, "cfg1"), (2, "cfg1"), (3, "cfg1"), (4, "cfg3"), (2, "cfg2")])
+def test_dcp_stagewise(phd, orc, K, cname):
+    from oracle import dcp
+    cfg = scenario.get(cname)
+    m = replace(cfg.model, mode=MODE_DCP)
+    if cname == "cfg3":
+        m = replace(m, fixed_count=24000, births_per_step=2000, capacity=40000, max_meas=1024)
+        cfg = replace(cfg, model=m, scenario=replace(cfg.scenario, n_targets=30, steps=3))
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    n0 = soa.shape[1]
+    groups = [(np.ascontiguousarray(soa[:, (n0 * j) // K:(n0 * (j + 1)) // K]),
+               np.ascontiguousarray(w[(n0 * j) // K:(n0 * (j + 1)) // K])) for j in range(K)]
+    grp = phd.LocalGroup(K) if K > 1 else None
+    fs = [phd.Filter(m, rank=j, group=grp) for j in range(K)]
+    for j, f in enumerate(fs):
+        f.set_particles(groups[j][0], groups[j][1], groups[j][0].shape[1])
+    if m.count_mode == COUNT_FIXED:
+        rule = lambda j, LT: (m.fixed_count * (j + 1)) // K - (m.fixed_count * j) // K
+    else:
+        rule = lambda j, LT: max(LT, 1) * m.particles_per_target
+    zprev = None
+    kap = orc.kappa(m)
+    for k in range(1, 4):
+        z = Z[k - 1]
+        rec = [dict() for _ in range(K)]
+
+        def stage(j):
+            f, r = fs[j], rec[j]
+            f.predict(k)
+            r["pred"], r["w_pred"], _ = f.get_particles()
+            f.update(z)
+            r["C"] = f.normalizers(len(z))
+            r["acc"] = f.accumulators(len(z))
+            _, r["wn"], _ = f.get_particles()
+            r["fused"], r["summ"] = f.extract()
+            r["local"] = f.local_estimates()
+            f.resample_exchange(k)
+            r["anc"], _ = f.ancestors()
+            r["meta"] = f.resample_meta()
+            r["next"], r["w_next"], _ = f.get_particles()
+        _run_parallel([lambda j=j: stage(j) for j in range(K)])
+
+        d = dcp.dcp_step(m, k, [(g[0].astype(np.float64), g[1].astype(np.float64)) for g in groups], z,
+                         None if zprev is None else zprev.astype(np.float64), rule)
+        pre_ring = []
+        for j in range(K):
+            r, o = rec[j], d["groups"][j]
+            nsv = groups[j][0].shape[1]
+            # Step 1: survivors and this group's births
+            assert r["pred"].shape == o["pred"].shape
+            ds = np.abs(r["pred"][:, :nsv] - o["pred"][:, :nsv])
+            assert np.all(ds <= 5e-7 * np.abs(o["pred"][:, :nsv]) + 7e-5)
+            rscale = 0.0 if m.meas == POSITION else 2000.0
+            db = np.abs(r["pred"][:, nsv:] - o["pred"][:, nsv:])
+            assert np.all(db <= 1e-6 * (np.abs(o["pred"][:, nsv:]) + rscale) + 1e-5)
+            # Step 2 on the GPU's predicted group (stage-wise): local C_j and weights
+            Co = orc.normalizers(m, r["pred"], r["w_pred"], z)
+            wo, acco = orc.update(m, r["pred"], r["w_pred"], z, Co)
+            assert np.all(np.abs(r["C"] - Co) <= 1e-5 * Co + 1e-9 * kap)
+            assert np.all(np.abs(r["wn"] - wo) <= 1e-4 * wo + 1e-7 * r["w_pred"])
+            # Step 3: local estimates = oracle selection on the GPU accumulators
+            Wj = r["meta"]["W_r"][j]
+            eo = orc.extract(m, r["acc"], Wj, math.fsum(r["w_pred"].astype(np.float64)))
+            assert list(r["local"]["labels"]) == list(eo["labels"])
+            # Step 5: resampling of the group's own weights
+            ao, _ = orc.resample(r["wn"].astype(np.float64), r["meta"]["U"], r["meta"]["N_out"])
+            assert r["meta"]["U"] == d["resampled"][j][3]
+            assert r["meta"]["N_out"] == rule(j, orc.round_half_away(Wj))
+            ties = _near_ties(r["wn"], r["meta"]["U"], r["meta"]["N_out"])
+            assert np.all(ties[r["anc"] != ao])
+            pre_ring.append((r["pred"][:, r["anc"]], np.full(len(r["anc"]), np.float32(Wj / len(r["anc"])))))
+        # Step 4 (CU, rank 0): fusion of the GPU's local estimates
+        fl, fs_states, _ = dcp.fuse([(rec[j]["local"]["labels"], rec[j]["local"]["states"]) for j in range(K)], K)
+        assert list(rec[0]["fused"]["labels"]) == list(fl)
+        assert np.allclose(rec[0]["fused"]["states"], fs_states, rtol=1e-6, atol=1e-4)
+        # Step 6: ring exchange applied to the GPU's pre-ring groups
+        n_min = min(len(rec[j]["anc"]) for j in range(K))
+        L = min(n_min // 10, n_min // 2) if K > 1 else 0
+        slots = [dcp.ring_slots(m.seed, k, j, len(rec[j]["anc"]), L, K) if L else [] for j in range(K)]
+        for j in range(K):
+            exp_s, exp_w = pre_ring[j][0].copy(), pre_ring[j][1].copy()
+            src = (j - 1) % K
+            for i in range(L):
+                exp_s[:, slots[j][i]] = pre_ring[src][0][:, slots[src][i]]
+                exp_w[slots[j][i]] = pre_ring[src][1][slots[src][i]]
+            assert np.array_equal(rec[j]["next"], exp_s)
+            assert np.allclose(rec[j]["w_next"], exp_w, rtol=1e-7)
+        groups = [(rec[j]["next"], rec[j]["w_next"]) for j in range(K)]
+        zprev = z
+    for f in fs:
+        f.close()
+    if grp is not None:
+        grp.close()
+
+
+def test_dcp_single_group_equals_exact(phd):
+    """With one group the paper's DCPFPHD is the serial filter: DCP and exact modes agree."""
+    cfg = scenario.get("cfg1")
+    Z = scenario.measurements(cfg)
+    soa, w = scenario.initial_population(cfg)
+    fa = phd.Filter(cfg.model)
+    fb = phd.Filter(replace(cfg.model, mode=MODE_DCP))
+    fa.set_particles(soa, w, soa.shape[1])
+    fb.set_particles(soa, w, soa.shape[1])
+    for k in range(1, 6):
+        fa.step(k, Z[k - 1])
+        fb.step(k, Z[k - 1])
+        ea, eb = fa._estimates(), fb._estimates()
+        order = np.argsort(ea["labels"])
+        assert np.array_equal(ea["labels"][order], eb["labels"])
+        assert np.array_equal(ea["states"][order], eb["states"])
+    sa, wa, _ = fa.get_particles()
+    sb, wb, _ = fb.get_particles()
+    assert np.array_equal(sa, sb) and np.array_equal(wa, wb)
+    fa.close()
+    fb.close()
