@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="exact", choices=["exact", "dcp"],
+                    help="exact: global C + exact resampling (north_star hot path); dcp: the paper's DCPFPHD groups")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=65536, help="particles in the oracle's bounded sample")
     return ap.parse_args()
@@ -189,14 +191,20 @@ def run_ours(args):
 
     steps = args.warmup + args.steps
     cfg = scenario_for(args.config, 2 * steps + 1)
+    from dataclasses import replace as _replace
+    cfg = _replace(cfg, model=_replace(cfg.model, mode=1 if args.mode == "dcp" else 0))
     m = cfg.model
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
     soa, w = scenario.initial_population(cfg, truth)
     n0 = soa.shape[1]
     J = m.births_per_step
-    lo, hi = phd.rank_block(n0 + J, world, rank)
-    a, b = min(lo, n0), min(hi, n0)
+    if args.mode == "dcp":   # every rank is one DCPFPHD group holding its block of the population
+        lo, hi = phd.rank_block(n0, world, rank)
+        a, b = lo, hi
+    else:
+        lo, hi = phd.rank_block(n0 + J, world, rank)
+        a, b = min(lo, n0), min(hi, n0)
     nid = None
     if world > 1:
         obj = [phd.nccl_unique_id() if rank == 0 else None]
@@ -332,6 +340,7 @@ def run_ours(args):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "N": N_glob, "M": M, "survivors": n0, "births": J,
                    "meas_model": "position" if m.meas == 0 else "range_bearing", "parallelism": "dp%d" % world,
+                   "mode": args.mode,
                    "l2": "inputs larger than L2 (particle state %d MB > 126 MB)" % (N_glob * 20 // 2**20)},
         "update_pairs_per_s": local_pairs * world / ((statistics.mean(pass_ms["update"])) * 1e-3),
         "kernel_ms": {k: statistics.mean(v) for k, v in pass_ms.items()},
