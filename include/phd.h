@@ -103,6 +103,11 @@ typedef struct {
   int32_t reserved0;          /* must be 0 */
   int64_t exchange_count;     /* DCP ring exchange L per step (0: floor(min_j N_j / 10));
                                  clamped to floor(min_j N_j / 2) */
+  int32_t birth_model;        /* 0: births around Z_{k-1} (uniform when none), S10;
+                                 1: N(birth_mean, diag(birth_std^2)) */
+  int32_t reserved1;          /* must be 0 */
+  double birth_mean[4];       /* x-bar (x, vx, y, vy) of birth_model 1 */
+  double birth_std[4];        /* sqrt(diag Q) of birth_model 1, >= 0 */
 } phd_params;
 
 /* One labelled estimate: label = measurement index, state =

@@ -33,7 +33,8 @@ class _Model(ctypes.Structure):
                 ("sigma_z", ctypes.c_double * 2), ("sensor", ctypes.c_double * 2),
                 ("region", ctypes.c_double * 4), ("clutter_rate", ctypes.c_double),
                 ("birth_mass", ctypes.c_double), ("birth_sigma_v", ctypes.c_double),
-                ("seed", ctypes.c_uint64)]
+                ("seed", ctypes.c_uint64), ("birth_model", ctypes.c_int32), ("pad2_", ctypes.c_int32),
+                ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4)]
 
 
 _lib = None
@@ -89,6 +90,10 @@ def model(m):
     om.birth_mass = float(m.birth_mass)
     om.birth_sigma_v = float(m.birth_sigma_v)
     om.seed = int(m.seed)
+    om.birth_model = int(getattr(m, "birth_model", 0))
+    for i in range(4):
+        om.birth_mean[i] = float(getattr(m, "birth_mean", (0.0, 0.0, 0.0, 0.0))[i])
+        om.birth_std[i] = float(getattr(m, "birth_std", (0.0, 0.0, 0.0, 0.0))[i])
     return om
 
 

@@ -145,6 +145,15 @@ void orc_births(const orc_model* m, int32_t k, int64_t n_out, int64_t J, int64_t
     double n1, n2, n3, n4;
     orc_box_muller(u0, u1, &n1, &n2);
     orc_box_muller(u2, u3, &n3, &n4);
+    if (m->birth_model == 1) {
+      /* births from the normal density N(x-bar, Q), Q diagonal */
+      x[i] = m->birth_mean[0] + m->birth_std[0] * n1;
+      vx[i] = m->birth_mean[1] + m->birth_std[1] * n2;
+      y[i] = m->birth_mean[2] + m->birth_std[2] * n3;
+      vy[i] = m->birth_mean[3] + m->birth_std[3] * n4;
+      w[i] = m->birth_mass / (double)J;
+      continue;
+    }
     double a, c;
     if (m_prev > 0) {
       const double* z = zprev + 2 * (b % m_prev);

@@ -32,6 +32,10 @@ typedef struct {
   double birth_mass;     /* gamma: total birth mass per step */
   double birth_sigma_v;  /* birth velocity std */
   uint64_t seed;         /* Philox key {lo32, hi32} */
+  int32_t birth_model;   /* 0: around Z_{k-1} (S10); 1: N(birth_mean, diag(birth_std^2)) */
+  int32_t pad2_;
+  double birth_mean[4];  /* x-bar (x, vx, y, vy) */
+  double birth_std[4];   /* sqrt(diag Q) */
 } orc_model;
 
 /* Philox4x32-10 block cipher; ctr = {c0,c1,c2,c3}, key = {k0,k1}. */

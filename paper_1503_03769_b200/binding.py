@@ -34,7 +34,8 @@ class Params(ctypes.Structure):
                 ("births_per_step", ctypes.c_int64), ("particles_per_target", ctypes.c_int64),
                 ("fixed_count", ctypes.c_int64), ("count_mode", ctypes.c_int32), ("max_meas", ctypes.c_int32),
                 ("capacity", ctypes.c_int64), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("exchange_count", ctypes.c_int64)]
+                ("reserved0", ctypes.c_int32), ("exchange_count", ctypes.c_int64), ("birth_model", ctypes.c_int32),
+                ("reserved1", ctypes.c_int32), ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4)]
 
 
 class Estimate(ctypes.Structure):
@@ -148,6 +149,11 @@ def params_from(model):
     p.mode = int(getattr(model, "mode", 0))
     p.reserved0 = 0
     p.exchange_count = int(getattr(model, "exchange_count", 0))
+    p.birth_model = int(getattr(model, "birth_model", 0))
+    p.reserved1 = 0
+    for i in range(4):
+        p.birth_mean[i] = float(getattr(model, "birth_mean", (0.0, 0.0, 0.0, 0.0))[i])
+        p.birth_std[i] = float(getattr(model, "birth_std", (0.0, 0.0, 0.0, 0.0))[i])
     return p
 
 

@@ -65,6 +65,16 @@ __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
     sincospif(2.0f * u3, &s2, &c2);
     float n1 = r01 * c1, n2 = r01 * s1, n3 = r23 * c2, n4 = r23 * s2;
     float p0, p1;
+    if (a.birth_model == 1) {
+      // birth intensity N(x-bar, Q), Q diagonal
+      a.x[i] = a.birth_mean[0] + a.birth_std[0] * n1;
+      a.vx[i] = a.birth_mean[1] + a.birth_std[1] * n2;
+      a.y[i] = a.birth_mean[2] + a.birth_std[2] * n3;
+      a.vy[i] = a.birth_mean[3] + a.birth_std[3] * n4;
+      a.w[i] = a.birth_w;
+      if (a.rb) rb_repr(a.x[i], a.y[i], a.sensor_x, a.sensor_y, a.rb, a.rb_stride, i);
+      return;
+    }
     if (a.m_prev > 0) {
       int64_t m = (a.birth_offset + b) % a.m_prev;
       p0 = a.zprev[2 * m] + a.sigma_z0 * n1;

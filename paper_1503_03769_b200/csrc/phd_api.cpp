@@ -238,6 +238,10 @@ phd_status validate(const phd_params* p, int world, phd_ctx* c) {
   if (p->mode != PHD_MODE_EXACT && p->mode != PHD_MODE_DCP) return fail(c, PHD_EINVAL, "mode %d", p->mode);
   if (p->reserved0 != 0) return fail(c, PHD_EINVAL, "reserved0 must be 0");
   if (p->exchange_count < 0) return fail(c, PHD_EINVAL, "exchange_count < 0");
+  if (p->birth_model != 0 && p->birth_model != 1) return fail(c, PHD_EINVAL, "birth_model %d", p->birth_model);
+  if (p->reserved1 != 0) return fail(c, PHD_EINVAL, "reserved1 must be 0");
+  for (int i = 0; i < 4; ++i)
+    if (!(p->birth_std[i] >= 0)) return fail(c, PHD_EINVAL, "birth_std must be >= 0");
   if (world < 1) return fail(c, PHD_EINVAL, "world < 1");
   return PHD_OK;
 }
@@ -646,6 +650,11 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
   for (int i = 0; i < 4; ++i) a.region[i] = (float)c->p.region[i];
   a.birth_w = J > 0 ? (float)(c->p.birth_mass / (double)J) : 0.0f;
   a.birth_sigma_v = (float)c->p.birth_sigma_v;
+  a.birth_model = c->p.birth_model;
+  for (int i = 0; i < 4; ++i) {
+    a.birth_mean[i] = (float)c->p.birth_mean[i];
+    a.birth_std[i] = (float)c->p.birth_std[i];
+  }
   a.zprev = zp;
   a.m_prev = mp;
   a.x = c->A[0];

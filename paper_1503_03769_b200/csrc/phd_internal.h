@@ -67,6 +67,8 @@ struct PredictArgs {
   float sigma_z0, sigma_z1, sensor_x, sensor_y;
   float region[4];
   float birth_w, birth_sigma_v;
+  int birth_model;           // 0 around Z_{k-1}; 1 N(birth_mean, diag(birth_std^2))
+  float birth_mean[4], birth_std[4];
   const float* zprev;        // device [m_prev][2]
   int32_t m_prev;
   float *x, *vx, *y, *vy, *w;

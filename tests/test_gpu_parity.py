@@ -404,3 +404,18 @@ def test_group_pipelined_update_parity(phd, orc, monkeypatch):
         f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 9001, 2600, seed=5)
         _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
         f.close()
+
+
+def test_births_gaussian_model(phd, orc):
+    """NEXT-4: the paper's fixed Gaussian birth intensity N(x-bar, Q)."""
+    for base in (POS, RB):
+        m = replace(base, birth_model=1, births_per_step=3000)
+        soa, w = scenario.random_particles(1234, 6)
+        f = phd.Filter(m)
+        f.set_particles(soa, w, 1234)
+        f.predict(2, _meas(m, 10, 3))
+        gs, gw, _ = f.get_particles()
+        bs, bw = orc.births(m, 2, 1234, m.births_per_step, None)
+        assert np.all(np.abs(gs[:, 1234:] - bs) <= 1e-6 * np.abs(bs) + 1e-5)
+        assert np.allclose(gw[1234:], bw, rtol=1e-7)
+        f.close()

@@ -456,3 +456,19 @@ def test_golden_spec_examples(orc):
             assert abs(orc.likelihood(m, (5.0, math.atan2(4, 3)), (3.0, 4.0)) - ex["expect"]) < ex["tol"], ex["cite"]
         else:
             raise AssertionError(ex)
+
+
+def test_births_gaussian_model(orc):
+    """birth intensity N(x-bar, Q), x-bar = (0,3,0,-3), Q = diag(10,1,10,1)."""
+    m = Model(birth_model=1, birth_mass=0.2)
+    J = 40000
+    s, w = orc.births(m, 3, 500, J, np.array([[100.0, 100.0]]))  # Z_{k-1} is ignored by this model
+    assert np.allclose(w, 0.2 / J)
+    mean, std = s.mean(axis=1), s.std(axis=1)
+    assert np.all(np.abs(mean - np.array([0.0, 3.0, 0.0, -3.0])) < 5 * np.array(m.birth_std) / math.sqrt(J))
+    assert np.all(np.abs(std - np.array(m.birth_std)) < 0.02 * np.array(m.birth_std))
+    assert abs(np.corrcoef(s[0], s[2])[0, 1]) < 4 / math.sqrt(J)
+    # zero covariance -> exact copies of x-bar (SPEC.md:90)
+    m0 = Model(birth_model=1, birth_std=(0.0, 0.0, 0.0, 0.0))
+    s0, _ = orc.births(m0, 1, 0, 3, None)
+    assert np.array_equal(s0, np.tile(np.array([[0.0], [3.0], [0.0], [-3.0]]), (1, 3)))
