@@ -202,6 +202,7 @@ def run_ours(args):
     if args.mode == "dcp":   # every rank is one DCPFPHD group holding its block of the population
         lo, hi = phd.rank_block(n0, world, rank)
         a, b = lo, hi
+        w = w * np.float32(world)  # each group is a full-intensity filter
     else:
         lo, hi = phd.rank_block(n0 + J, world, rank)
         a, b = min(lo, n0), min(hi, n0)

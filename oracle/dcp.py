@@ -5,7 +5,10 @@ lines 260-359), NEXT-1 of SURVEY.md §8(f).
 K groups, run one after the other in a plain loop, each with its own particle
 population and the FULL measurement set:
   Step 1 (line 266): survivors predicted (Eq 5); the J births are divided
-         equally over the groups (group j gets the block [jJ/K, (j+1)J/K)).
+         equally over the groups (group j gets the block [jJ/K, (j+1)J/K)),
+         each weighted gamma / J_j (Eq 6 with the group's J_k): every group is a
+         separate particle PHD filter of the full intensity (line 221; omega_0 =
+         1/M per group, line 260), so callers give each group a full-mass population.
   Step 2 (lines 269-297): the group's own normaliser C_j(z) (Eq 11 sums over
          the group's particles only) and weights (Eqs 12-15).
   Step 3 (lines 299-324): local estimation: LT_j = round(W_j), top-LT_j labels
@@ -82,7 +85,9 @@ def dcp_step(m, k, groups, z, zprev, n_out_rule, L_param=0):
         n_j = soa.shape[1]
         ps, pw = predict(m, k, soa, w, g0=group_base(j, K))                   # Eq 5
         b0, b1 = block(J, K, j)
-        bs, bw = births(m, k, group_base(j, K) + n_j - b0, J, zprev, b0=b0, nb=b1 - b0)  # Eq 6, Step 1
+        # Eq 6 with the group's own J_k: each group is a separate PHD filter of the full
+        # intensity, so its births carry the full birth mass gamma
+        bs, bw = births(m, k, group_base(j, K) + n_j - b0, b1 - b0, zprev, b0=b0, nb=b1 - b0)
         xs = np.concatenate([ps, bs], axis=1)
         ws = np.concatenate([pw, bw])
         C = normalizers(m, xs, ws, z)                                          # Eq 11 (group-local)

@@ -6,9 +6,10 @@
 // particles stream through shared memory in tiles of 64 and are broadcast to
 // every lane.  Per (particle, slot) pair the lane evaluates the likelihood with
 // packed FFMA2/FADD2/FMUL2 and one MUFU.EX2:
-//   pass 1:  e = 2^(-alpha q),  C'_s += e * (p_D c w_i)                 (Eq 7)
-//   pass 2:  u = e * (p_D c w_i);  dW'_s += u;  S'_s += u * (x_i - z_s);
-//            Pe_i += e * d_s,  d_s = 1/(kappa + C_s)                     (Eqs 8, 12-16)
+//   both:    u = 2^(-alpha q + log2(p_D c w_i)) = p_D g(z_s|x_i) w_i (ex2.approx.ftz)
+//   pass 1:  C_s += u                                                      (Eq 7)
+//   pass 2:  P_i += u d_s, d_s = 1/(kappa + C_s);  S'_s += u (x_i - z_s), u vx_i, ...
+//            (Eqs 8, 12-16; dW_s = C_s/D_s)
 // Per-slot sums accumulate in fp32 over one tile (64 particles), then in an
 // fp32 mid level over 16 tiles, then in fp64 (DESIGN.md §5 "accumulation
 // precision").  Per-particle sums Pe_i are reduced across lanes with a
@@ -94,7 +95,7 @@ struct TileLoader {
         reinterpret_cast<float4*>(d)[1] = make_float4(v[r][2], v[r][2], v[r][3], v[r][3]);
         reinterpret_cast<float4*>(d)[2] = make_float4(v[r][4], v[r][4], v[r][5], v[r][5]);
         reinterpret_cast<float4*>(d)[3] = make_float4(v[r][6], v[r][6], v[r][7], v[r][7]);
-        float wc = PASS == 1 ? v[r][8] * wscale : log2f(v[r][8] * wscale);
+        float wc = log2f(v[r][8] * wscale);
         reinterpret_cast<float4*>(d)[4] = make_float4(wc, wc, 0.0f, 0.0f);
         if (PASS == 2) {
           reinterpret_cast<float4*>(d)[5] = make_float4(v[r][9], v[r][9], v[r][10], v[r][10]);
@@ -102,7 +103,7 @@ struct TileLoader {
         }
       } else {
         reinterpret_cast<float4*>(d)[0] = make_float4(v[r][0], v[r][0], v[r][1], v[r][1]);
-        float wc = PASS == 1 ? v[r][2] * wscale : log2f(v[r][2] * wscale);
+        float wc = log2f(v[r][2] * wscale);
         if (PASS == 2) {
           reinterpret_cast<float4*>(d)[1] = make_float4(v[r][3], v[r][3], v[r][4], v[r][4]);
           reinterpret_cast<float4*>(d)[2] = make_float4(wc, wc, 0.0f, 0.0f);
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
 #pragma unroll(PASS == 1 ? kPPUnroll1 : kPPUnroll2)
       for (int pp = 0; pp < 8; ++pp) {
         const float* rec = rb + (p0 + pp) * L::WIDTH;
-        // pass 1: (p_D c w, .); pass 2: (log2(p_D c w), .)
+        // (log2(p_D c w), .) for both passes
         const float2 wv = *reinterpret_cast<const float2*>(rec + L::WC);
         float2 pacc = f2(0.0f, 0.0f);
 #pragma unroll
@@ -255,8 +256,9 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
           float2 d0, d1;
           residual<MODEL, PASS, NP>(rec, z, j, d0, d1);
           if (PASS == 1) {
-            const float2 e = ex2v(expo<MODEL>(d0, d1, na0, na1, f2(0.0f, 0.0f)));
-            in[0][j] = __ffma2_rn(e, wv, in[0][j]);
+            // u = p_D g w = 2^(-alpha q + log2(p_D c w)), flushed to zero below 2^-126
+            // exactly as in pass 2 (the two passes see bitwise-identical terms)
+            in[0][j] = __fadd2_rn(in[0][j], ex2v(expo<MODEL>(d0, d1, na0, na1, wv)));
           } else {
             const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
             pacc = __ffma2_rn(u, z.d[j], pacc);
@@ -648,7 +650,7 @@ __global__ void k_zconst(const double* __restrict__ C_slot, const int32_t* __res
     C_lab[lab] = C;
     D_lab[lab] = D;
     if (!isfinite(D)) atomicAdd(bad, 1);
-    d = D > 0.0 ? (float)(1.0 / D) : 0.0f;
+    d = D > 0.0 ? (float)fmin(1.0 / D, 3.0e38) : 0.0f;
   }
   d_slot[s] = d;
 }

@@ -648,7 +648,8 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
   a.sensor_x = (float)c->p.sensor_xy[0];
   a.sensor_y = (float)c->p.sensor_xy[1];
   for (int i = 0; i < 4; ++i) a.region[i] = (float)c->p.region[i];
-  a.birth_w = J > 0 ? (float)(c->p.birth_mass / (double)J) : 0.0f;
+  // Eq 6 weight gamma / J_k; a DCP group is a full-intensity PHD filter with its own J_k births
+  a.birth_w = a.J > 0 ? (float)(c->p.birth_mass / (double)a.J) : 0.0f;
   a.birth_sigma_v = (float)c->p.birth_sigma_v;
   a.birth_model = c->p.birth_model;
   for (int i = 0; i < 4; ++i) {

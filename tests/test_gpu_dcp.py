@@ -173,3 +173,37 @@ def test_dcp_single_group_equals_exact(phd):
     assert np.array_equal(sa, sb) and np.array_equal(wa, wb)
     fa.close()
     fb.close()
+
+
+def test_tracking_sanity_exact_and_dcp(phd):
+    """Tracking quality on cfg 1 (no paper-derived target: a sanity bound):
+    both modes find the 3 targets (cardinality error <= 1 on most late scans, OSPA well
+    below the cut-off)."""
+    from paper_1503_03769_b200.metrics import ospa, positions
+    cfg = scenario.get("cfg1")
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    for K in (1, 2):
+        m = replace(cfg.model, mode=MODE_DCP if K > 1 else 0)
+        big = replace(cfg, model=replace(m, particles_per_target=m.particles_per_target * K))
+        soa, w = scenario.initial_population(big, truth)
+        w = w * np.float32(K)
+        n0 = soa.shape[1]
+        grp = phd.LocalGroup(K) if K > 1 else None
+        fs = [phd.Filter(m, rank=j, group=grp) for j in range(K)]
+        for j, f in enumerate(fs):
+            a, b = (n0 * j) // K, (n0 * (j + 1)) // K
+            f.set_particles(np.ascontiguousarray(soa[:, a:b]), np.ascontiguousarray(w[a:b]), b - a if K > 1 else n0)
+        os_, card = [], []
+        for k in range(1, 21):
+            _run_parallel([lambda f=f: f.step(k, Z[k - 1]) for f in fs])
+            est = fs[0]._estimates()
+            tru = truth.states[k][truth.alive[k]][:, [0, 2]]
+            os_.append(ospa(positions(est["states"]), tru))
+            card.append(abs(len(est["labels"]) - len(tru)))
+        assert np.mean(os_[10:]) < 40.0, os_
+        assert np.mean(np.array(card[10:]) <= 1) >= 0.8, card
+        for f in fs:
+            f.close()
+        if grp is not None:
+            grp.close()
