@@ -27,9 +27,12 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Per-pair algorithmic work of the two-pass update (SURVEY.md §8(d); DESIGN.md §7):
-# position: pass 1 = 6 FP32 + 1 EX2, pass 2 = 11 FP32 + 1 EX2; range-bearing +1 FP32 per pass.
-ALGO = {0: {"pass1": (6, 1), "pass2": (11, 1)}, 1: {"pass1": (7, 1), "pass2": (12, 1)}}
+# Per-pair algorithmic work of the two-pass update (DESIGN.md §5):
+#   pass 1: 6 FP32 + 1 EX2 (position; +1 FP32 range-bearing)
+#   pass 2: 6 FP32 + 1 EX2 for the weights (+1 range-bearing), plus 4 FP32 (+2 range-bearing
+#           centring) for the STPHD state sums of the pairs whose label is in the estimated
+#           index set I (fraction f = |I| / M); SURVEY.md §8(d) counted the state sums for
+#           every pair (11 FP32), reported as "frac_survey_count".
 FP32_PER_CLK_SM = 128.0   # measured: profiles/r01_pipes_microbench.jsonl (FFMA / FFMA2 lanes)
 EX2_PER_CLK_SM = 16.0     # measured: MUFU.EX2
 SM_MAX_MHZ = 1965.0
@@ -49,12 +52,27 @@ def parse():
     return ap.parse_args()
 
 
-def roofline_pairs_per_s(meas, which, n_sm, mhz):
-    fp, ex = ALGO[1 if meas == 1 else 0][which] if which != "update" else (
-        sum(ALGO[1 if meas == 1 else 0][p][0] for p in ("pass1", "pass2")),
-        sum(ALGO[1 if meas == 1 else 0][p][1] for p in ("pass1", "pass2")))
+def pass_ops(meas, which, f):
+    rb = 1 if meas == 1 else 0
+    if which == "pass1":
+        return 6 + rb, 1
+    if which == "pass2":
+        return 6 + rb + (4 + 2 * rb) * f, 1
+    if which == "pass2_survey":
+        return 11 + rb, 1
+    a, b = pass_ops(meas, "pass1", f), pass_ops(meas, "pass2", f)
+    return a[0] + b[0], a[1] + b[1]
+
+
+def roofline_pairs_per_s(meas, which, n_sm, mhz, f=1.0):
+    fp, ex = pass_ops(meas, which, f)
     per_clk = min(FP32_PER_CLK_SM / fp, EX2_PER_CLK_SM / ex)
     return per_clk * n_sm * mhz * 1e6
+
+
+def bound_of(meas, which, f):
+    fp, ex = pass_ops(meas, which, f)
+    return "alu:fp32" if fp / FP32_PER_CLK_SM >= ex / EX2_PER_CLK_SM else "alu:mufu.ex2"
 
 
 class ClockSampler:
@@ -316,10 +334,13 @@ def run_ours(args):
     p2 = statistics.mean(pass_ms["pass2"])
     p1 = statistics.mean(pass_ms["pass1"])
     local_pairs = (hi - lo) * M
+    n_sel = min(int(f._sum.LT), M)
+    frac_sel = (n_sel / M) if (M and m.stphd_all == 0) else 1.0
     ach2 = local_pairs / (p2 * 1e-3)
-    peak2 = roofline_pairs_per_s(m.meas, "pass2", n_sm, SM_MAX_MHZ)
+    peak2 = roofline_pairs_per_s(m.meas, "pass2", n_sm, SM_MAX_MHZ, frac_sel)
+    peak2_survey = roofline_pairs_per_s(m.meas, "pass2_survey", n_sm, SM_MAX_MHZ)
     ach_upd = local_pairs / ((p1 + p2) * 1e-3)
-    peak_upd = roofline_pairs_per_s(m.meas, "update", n_sm, SM_MAX_MHZ)
+    peak_upd = roofline_pairs_per_s(m.meas, "update", n_sm, SM_MAX_MHZ, frac_sel)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -345,13 +366,21 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (particle state %d MB > 126 MB)" % (N_glob * 20 // 2**20)},
         "update_pairs_per_s": local_pairs * world / ((statistics.mean(pass_ms["update"])) * 1e-3),
         "kernel_ms": {k: statistics.mean(v) for k, v in pass_ms.items()},
-        "roofline": {"bound": "alu", "kernel": "k_pass<pos,2> (update pass 2)", "achieved": ach2 / 1e9,
-                     "peak": peak2 / 1e9, "unit": "Gpair/s", "frac": ach2 / peak2, "traffic": traffic,
-                     "peak_basis": "min(128 FP32 lanes/11, 16 EX2/1) per SM-clk x %d SMs x %.0f MHz (max clock); "
-                                   "pipe rates measured (profiles/r01_pipes_microbench.jsonl)" % (n_sm, SM_MAX_MHZ),
-                     "frac_at_observed_clock": ach2 / roofline_pairs_per_s(m.meas, "pass2", n_sm, mhz)},
+        "roofline": {"bound": bound_of(m.meas, "pass2", frac_sel), "kernel": "k_pass<pass 2> (weights + STPHD sums)",
+                     "achieved": ach2 / 1e9, "peak": peak2 / 1e9, "unit": "Gpair/s", "frac": ach2 / peak2,
+                     "traffic": traffic,
+                     "peak_basis": "min(128 FP32 lanes / %.2f, 16 EX2 / 1) per SM-clk x %d SMs x %.0f MHz (max clock); "
+                                   "%.2f FP32 = 6 + 4 f, f = |I|/M = %.3f (state sums for the estimated index set); "
+                                   "pipe rates measured (profiles/r01_pipes_microbench.jsonl)"
+                                   % (pass_ops(m.meas, "pass2", frac_sel)[0], n_sm, SM_MAX_MHZ,
+                                      pass_ops(m.meas, "pass2", frac_sel)[0], frac_sel),
+                     "frac_at_observed_clock": ach2 / roofline_pairs_per_s(m.meas, "pass2", n_sm, mhz, frac_sel),
+                     "frac_survey_count": ach2 / peak2_survey},
         "update_roofline": {"achieved": ach_upd / 1e9, "peak": peak_upd / 1e9, "unit": "Gpair/s",
-                            "frac": ach_upd / peak_upd, "basis": "17 FP32 + 2 EX2 per pair (both passes)"},
+                            "frac": ach_upd / peak_upd, "bound": bound_of(m.meas, "update", frac_sel),
+                            "basis": "both passes: (12 + 4 f) FP32 + 2 EX2 per pair, f = %.3f" % frac_sel,
+                            "frac_vs_survey_17fp32_2ex2": ach_upd / roofline_pairs_per_s(m.meas, "update", n_sm,
+                                                                                         SM_MAX_MHZ, 1.25)},
         "cpu_baseline": cpu,
         "e2e": {"value": value_e, "unit": "pairs/s", "h2d_bytes_per_step": M * 8,
                 "d2h_bytes_per_step": int(f._sum.n_est) * 24 + 8 * (2 * world + 10)},

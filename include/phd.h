@@ -108,6 +108,11 @@ typedef struct {
   int32_t reserved1;          /* must be 0 */
   double birth_mean[4];       /* x-bar (x, vx, y, vy) of birth_model 1 */
   double birth_std[4];        /* sqrt(diag Q) of birth_model 1, >= 0 */
+  int32_t stphd_all;          /* 0: pass 2 accumulates the STPHD state sums S_l only for the
+                                 top-LT index set I, selected right after
+                                 pass 1 from dW = C/D and W = (1-pD) W_pred + sum dW; the
+                                 accumulators of other labels read 0.  1: for every measurement. */
+  int32_t reserved2;          /* must be 0 */
 } phd_params;
 
 /* One labelled estimate: label = measurement index, state =
@@ -207,7 +212,8 @@ phd_status phd_step(phd_ctx* ctx, int32_t k, const float* z, int32_t M, phd_esti
 /* ---- introspection (synchronous; for parity tests and debugging) ---------- */
 /* Global C[M] (Eq 7) of the last update, label order. */
 phd_status phd_get_normalizers(phd_ctx* ctx, double* C, int32_t cap);
-/* Global STPHD accumulators [M][5] = (dW, Sx, Svx, Sy, Svy) (Eqs 16, 18), label order. */
+/* Global STPHD accumulators [M][5] = (dW, Sx, Svx, Sy, Svy) (Eqs 16, 18), label order.
+ * With stphd_all = 0 the state sums of labels outside the estimated index set are 0. */
 phd_status phd_get_accumulators(phd_ctx* ctx, double* acc, int32_t cap);
 /* DCP mode: this rank's local (pre-fusion) estimates of the last extract,
  * sorted by (mass desc, label asc); n receives the count. */

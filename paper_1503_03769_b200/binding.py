@@ -35,7 +35,8 @@ class Params(ctypes.Structure):
                 ("fixed_count", ctypes.c_int64), ("count_mode", ctypes.c_int32), ("max_meas", ctypes.c_int32),
                 ("capacity", ctypes.c_int64), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32),
                 ("reserved0", ctypes.c_int32), ("exchange_count", ctypes.c_int64), ("birth_model", ctypes.c_int32),
-                ("reserved1", ctypes.c_int32), ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4)]
+                ("reserved1", ctypes.c_int32), ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4),
+                ("stphd_all", ctypes.c_int32), ("reserved2", ctypes.c_int32)]
 
 
 class Estimate(ctypes.Structure):
@@ -154,6 +155,8 @@ def params_from(model):
     for i in range(4):
         p.birth_mean[i] = float(getattr(model, "birth_mean", (0.0, 0.0, 0.0, 0.0))[i])
         p.birth_std[i] = float(getattr(model, "birth_std", (0.0, 0.0, 0.0, 0.0))[i])
+    p.stphd_all = int(getattr(model, "stphd_all", 0))
+    p.reserved2 = 0
     return p
 
 

@@ -20,7 +20,7 @@ __device__ __forceinline__ bool before(double wa, int la, double wb, int lb) {
 __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc, int M, int n2,
                                                   const double* __restrict__ Wv, const double* __restrict__ Wpv,
                                                   int count, double p_d, EstOut* est, int cap, double* summary,
-                                                  int32_t* count_out) {
+                                                  int32_t* count_out, const double* sel_info) {
   extern __shared__ __align__(16) unsigned char sm[];
   double* kw = reinterpret_cast<double*>(sm);
   int* kl = reinterpret_cast<int*>(kw + n2);
@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
       Wp += Wpv[r];
     }
     long long LT = (long long)floor(W + 0.5);
+    if (sel_info) LT = (long long)sel_info[1];  // the index set of k_select (mass identity W)
     if (LT < 0) LT = 0;
     long long nsel = LT < n_elig ? LT : n_elig;
     if (nsel > cap) nsel = cap;
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
 }
 
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
-                           void* est, int cap, double* summary, int32_t* count_out, cudaStream_t s) {
+                           void* est, int cap, double* summary, int32_t* count_out, const double* sel_info,
+                           cudaStream_t s) {
   int n2 = 1;
   while (n2 < M) n2 <<= 1;
   size_t smem = (size_t)n2 * (sizeof(double) + sizeof(int));
@@ -108,7 +110,7 @@ cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const 
     attr_set = true;
   }
   k_extract<<<1, 1024, smem, s>>>(acc_lab, M, n2, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
-                                  count_out);
+                                  count_out, sel_info);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,281 @@
+// STPHD label selection before pass 2.
+//
+// After pass 1 the normalisers C are global, so every quantity the extraction
+// needs is already known except the state sums:
+//   dW_l = C_l / (kappa + C_l)            (Eq 16 summed over particles, exactly)
+//   W    = (1 - p_D) W_pred + sum_l dW_l   (the mass identity of Eqs 8 / 15)
+//   LT   = round(W), index set I = the LT largest dW (dW desc, label asc).
+// Pass 2 then accumulates the weighted-state sums S_l (Eq 18) only for l in I
+// -- the labels whose states the paper estimates -- in a
+// slot layout that puts I first, so the choice is warp-uniform.
+#include "phd_internal.h"
+
+namespace phd {
+
+// fp64 block sums of w (kBlockW per block), then one CTA reduces them to *out.
+__global__ void __launch_bounds__(256) k_block_sum(const float* __restrict__ w, int64_t n, double* blk) {
+  __shared__ double sw[8];
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * kBlockW;
+  double a = 0.0;
+#pragma unroll
+  for (int r = 0; r < kBlockW / 256; ++r) {
+    int64_t i = base + r * 256 + tid;
+    if (i < n) a += (double)w[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((tid & 31) == 0) sw[tid >> 5] = a;
+  __syncthreads();
+  if (tid == 0) {
+    double x = 0.0;
+    for (int k = 0; k < 8; ++k) x += sw[k];
+    blk[blockIdx.x] = x;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sum_blocks(const double* __restrict__ blk, int nb, double* out) {
+  __shared__ double s[256];
+  double a = 0.0;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) a += blk[k];
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cudaStream_t s) {
+  int nb = (int)((n + kBlockW - 1) / kBlockW);
+  if (nb > 0) {
+    k_block_sum<<<nb, 256, 0, s>>>(w, n, blk);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_sum_blocks<<<1, 256, 0, s>>>(blk, nb, out);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ bool sel_before(double wa, int la, double wb, int lb) {
+  return wa > wb || (wa == wb && la < lb);
+}
+
+// One CTA.  sel_flag[l] = 1 for l in I; info = (W_id, LT, n_eligible, n_sel).
+__global__ void __launch_bounds__(1024) k_select(const double* __restrict__ C_lab, const double* __restrict__ D_lab,
+                                                 int M, int n2, const double* __restrict__ W_pred, double p_d,
+                                                 int32_t* sel_flag, double* info) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* kw = reinterpret_cast<double*>(sm);
+  int* kl = reinterpret_cast<int*>(kw + n2);
+  __shared__ double red[1024];
+  __shared__ int n_elig;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  if (tid == 0) n_elig = 0;
+  __syncthreads();
+  double part = 0.0;
+  int cnt = 0;
+  for (int i = tid; i < n2; i += nthr) {
+    double w = -1.0;
+    if (i < M) {
+      double D = D_lab[i];
+      double dW = C_lab[i] * (D > 0.0 ? 1.0 / D : 0.0);  // same arithmetic as k_reduce_acc
+      part += dW;
+      sel_flag[i] = 0;
+      if (dW > 0.0) {
+        w = dW;
+        ++cnt;
+      }
+    }
+    kw[i] = w;
+    kl[i] = i;
+  }
+  red[tid] = part;
+  if (cnt) atomicAdd(&n_elig, cnt);
+  __syncthreads();
+  for (int o = nthr / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n2; i += nthr) {
+        int p = i ^ j;
+        if (p > i) {
+          bool up = (i & k) == 0;
+          double wi = kw[i], wp = kw[p];
+          int li = kl[i], lp = kl[p];
+          bool swap = up ? sel_before(wp, lp, wi, li) : sel_before(wi, li, wp, lp);
+          if (swap) {
+            kw[i] = wp;
+            kw[p] = wi;
+            kl[i] = lp;
+            kl[p] = li;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __shared__ int snsel;
+  if (tid == 0) {
+    double W = (1.0 - p_d) * (*W_pred) + red[0];
+    long long LT = (long long)floor(W + 0.5);
+    if (LT < 0) LT = 0;
+    long long nsel = LT < n_elig ? LT : n_elig;
+    snsel = (int)nsel;
+    info[0] = W;
+    info[1] = (double)LT;
+    info[2] = (double)n_elig;
+    info[3] = (double)nsel;
+  }
+  __syncthreads();
+  for (int s = tid; s < snsel; s += nthr) sel_flag[kl[s]] = 1;
+}
+
+cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
+                          int32_t* sel_flag, double* info, cudaStream_t s) {
+  int n2 = 1;
+  while (n2 < M) n2 <<= 1;
+  size_t smem = (size_t)n2 * (sizeof(double) + sizeof(int));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 12);
+    attr = true;
+  }
+  k_select<<<1, 1024, smem, s>>>(C_lab, D_lab, M, n2, W_pred, p_d, sel_flag, info);
+  return cudaGetLastError();
+}
+
+// Pass-2 slot layout (one CTA).  Sequence = [selected labels | unselected labels],
+// each part grouped by bearing class (range-bearing) and padded to even counts so
+// that every f32x2 slot pair is class-homogeneous; labels ascending inside.  The
+// sequence fills first the "state-sum" slots -- the first 2 js slots of every lane,
+// js = ceil(#selected / (2 * lanes)) -- then the remaining slots, so that every
+// warp carries the same share of state-sum work.  *js_out = js.
+__device__ __forceinline__ int seq_slot(int p, int n_s, int lanes, int zl, int js) {
+  if (p < n_s) {
+    int l = p / (2 * js);
+    return l * zl + p % (2 * js);
+  }
+  int q = p - n_s, rest = zl - 2 * js;
+  int l = q / rest;
+  return l * zl + 2 * js + q % rest;
+}
+
+__global__ void __launch_bounds__(1024) k_slots2(const float* __restrict__ z, const int32_t* __restrict__ sel_flag,
+                                                 int M, int model, int zl, int slots_pad, int32_t* slot_label,
+                                                 int32_t* js_out) {
+  __shared__ int wsum[32];
+  __shared__ int base_s;
+  __shared__ int cat_start[7];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  const int per = (M + nthr - 1) / nthr;
+  const float hp = 1.57079632679489662f;
+  const int lanes = slots_pad / zl;
+  for (int s = tid; s < slots_pad; s += nthr) slot_label[s] = -1;
+  if (tid == 0) base_s = 0;
+  __syncthreads();
+  // pass A: category sizes (with pair padding) -> sequence offsets; pass B: placement
+  for (int phase = 0; phase < 2; ++phase) {
+    int js = 1, n_s = 0;
+    if (phase == 1) {
+      int n_sel = cat_start[3];
+      js = (n_sel + 2 * lanes - 1) / (2 * lanes);
+      js = max(js, 0);
+      js = min(js, zl / 2);
+      n_s = 2 * js * lanes;
+      if (tid == 0) *js_out = js;
+      if (tid == 0) base_s = 0;
+      __syncthreads();
+    }
+    for (int cat = 0; cat < 6; ++cat) {
+      const int want_sel = cat < 3 ? 1 : 0, want_cls = cat % 3;
+      if (phase == 0 && tid == 0) cat_start[cat] = base_s;
+      if (model != kRangeBearing && want_cls != 0) {
+        __syncthreads();
+        continue;
+      }
+      int c = 0;
+      for (int q = 0; q < per; ++q) {
+        int l = tid * per + q;
+        if (l >= M) break;
+        int cls = 0;
+        if (model == kRangeBearing) {
+          float t = z[2 * l + 1];
+          cls = t > hp ? 1 : (t < -hp ? 2 : 0);
+        }
+        if ((sel_flag[l] != 0) == (want_sel != 0) && cls == want_cls) ++c;
+      }
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        int v = lane < nthr / 32 ? wsum[lane] : 0;
+        int inc2 = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int u = __shfl_up_sync(0xffffffffu, inc2, o);
+          if (lane >= o) inc2 += u;
+        }
+        if (lane < nthr / 32) wsum[lane] = inc2 - v;
+      }
+      __syncthreads();
+      if (phase == 1) {
+        int pos = base_s + wsum[warp] + (incl - c);
+        for (int q = 0; q < per; ++q) {
+          int l = tid * per + q;
+          if (l >= M) break;
+          int cls = 0;
+          if (model == kRangeBearing) {
+            float t = z[2 * l + 1];
+            cls = t > hp ? 1 : (t < -hp ? 2 : 0);
+          }
+          if ((sel_flag[l] != 0) == (want_sel != 0) && cls == want_cls) slot_label[seq_slot(pos++, n_s, lanes, zl, js)] = l;
+        }
+      }
+      __syncthreads();
+      if (tid == nthr - 1) {
+        int total = base_s + wsum[warp] + incl;
+        if (model == kRangeBearing && (total & 1)) ++total;  // pair padding (slot stays -1)
+        base_s = total;
+      }
+      __syncthreads();
+    }
+    if (phase == 0 && tid == 0) cat_start[6] = base_s;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
+                          int32_t* slot_label, int32_t* js, cudaStream_t s) {
+  k_slots2<<<1, 1024, 0, s>>>(z, sel_flag, M, model, zl, slots_pad, slot_label, js);
+  return cudaGetLastError();
+}
+
+// Per-slot d = 1/D(label) for the pass-2 layout (0 for padding).
+__global__ void k_dslot(const int32_t* __restrict__ slot_label, const double* __restrict__ D_lab, int n, float* d) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int lab = slot_label[s];
+  float v = 0.0f;
+  if (lab >= 0) {
+    double D = D_lab[lab];
+    v = D > 0.0 ? (float)fmin(1.0 / D, 3.0e38) : 0.0f;
+  }
+  d[s] = v;
+}
+
+cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, float* d, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_dslot<<<(n + 255) / 256, 256, 0, s>>>(slot_label, D_lab, n, d);
+  return cudaGetLastError();
+}
+
+}  // namespace phd

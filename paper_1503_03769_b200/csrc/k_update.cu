@@ -17,6 +17,8 @@
 // fp32 partial per (particle, z-block).  Cross-CTA sums are fp64 in fixed order.
 #include "phd_internal.h"
 
+#include <type_traits>
+
 #ifndef PHD_PP_UNROLL1
 #define PHD_PP_UNROLL1 8
 #endif
@@ -213,6 +215,8 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
 
   const int zb = blockIdx.y;
   const int slot0 = (zb * wz + warp) * (32 * ZL) + lane * ZL;
+  // pass 2: state sums for the first js slot pairs of every lane (the index set I sits there)
+  const int js = PASS == 2 ? (a.js == nullptr ? NP : min(*a.js, NP)) : 0;
   LaneZ<MODEL, PASS, NP> z;
   z.load(a, slot0);
   const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
@@ -242,6 +246,10 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
     if (more) ld.fetch(a, (t + 1) * kTileP, tid, nthr);
     const float* rb = recs + buf * kTileP * L::WIDTH;
 
+    // pass 2: state sums only in the first JS slot pairs of each lane, where the
+    // index set I lives (uniform over the warp; one instance of the loop per JS)
+    auto sweep = [&](auto js_tag) {
+      constexpr int JS = decltype(js_tag)::value;
 #pragma unroll 1
     for (int p0 = 0; p0 < kTileP; p0 += 8) {
       float pe[8];
@@ -262,16 +270,18 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
           } else {
             const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
             pacc = __ffma2_rn(u, z.d[j], pacc);
-            if (MODEL == kRangeBearing) {
+            if (j < JS && MODEL == kRangeBearing) {
               const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
               d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
               d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
             }
-            const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
-            in[0][j] = __ffma2_rn(u, d0, in[0][j]);
-            in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
-            in[2][j] = __ffma2_rn(u, d1, in[2][j]);
-            in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+            if (j < JS) {
+              const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+              in[0][j] = __ffma2_rn(u, d0, in[0][j]);
+              in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+              in[2][j] = __ffma2_rn(u, d1, in[2][j]);
+              in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+            }
           }
         }
         pe[pp] = pacc.x + pacc.y;
@@ -281,6 +291,12 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
         if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = s;
       }
     }
+    };
+    if (PASS == 1 || js >= NP) sweep(std::integral_constant<int, NP>{});
+    else if (js == 0) sweep(std::integral_constant<int, 0>{});
+    else if (js == 1) sweep(std::integral_constant<int, 1>{});
+    else if (NP > 2 && js == 2) sweep(std::integral_constant<int, (NP > 2 ? 2 : 1)>{});
+    else sweep(std::integral_constant<int, (NP > 3 ? 3 : 1)>{});
 
     if (more) ld.store(recs + (buf ^ 1) * kTileP * L::WIDTH, a.wscale, tid, nthr);
     // tile sums (<= 64 particles in fp32) -> fp64
@@ -725,7 +741,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
                              const float* __restrict__ s1, const float* __restrict__ s2,
                              const float* __restrict__ s3, int model, const double* __restrict__ blk_w,
                              const double* __restrict__ blk_wp, int nb, double* acc_lab, double* rank_slots,
-                             int rank, int world, int lead) {
+                             int rank, int world, int lead, const int32_t* __restrict__ sel_flag) {
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double sa[256], sb[256];
     double a = 0.0, b = 0.0;
@@ -775,6 +791,11 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
   // terms, every rank its own centred partial sums (the C2 all-reduce adds them).
   double dW = lead ? C_lab[lab] * inv : 0.0;
   double* o = acc_lab + 5 * (int64_t)lab;
+  if (sel_flag && !sel_flag[lab]) {  // state sums not accumulated outside the index set I
+    o[0] = dW;
+    o[1] = o[2] = o[3] = o[4] = 0.0;
+    return;
+  }
   o[0] = dW;
   o[1] = A[0] * inv + cx * dW;
   o[2] = A[1] * inv;
@@ -786,10 +807,10 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1,
                               const float* s2, const float* s3, int model, const double* blk_w, const double* blk_wp,
                               int nb, double* acc_lab, double* rank_slots, int rank, int world, int lead,
-                              cudaStream_t s) {
+                              const int32_t* sel_flag, cudaStream_t s) {
   int blocks = (n_slots + 255) / 256 + 1;
   k_reduce_acc<<<blocks, 256, 0, s>>>(Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
-                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead);
+                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead, sel_flag);
   return cudaGetLastError();
 }
 

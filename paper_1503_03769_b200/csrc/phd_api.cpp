@@ -39,7 +39,7 @@ struct Layout {
   int64_t nbw_max = 0, nbo_max = 0;
   size_t total = 0;
   // byte offsets
-  size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_D,
+  size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_sel, o_selinfo, o_D,
       o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_gather, o_ring, o_summ, o_bad;
 };
 
@@ -76,7 +76,9 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   for (int i = 0; i < 5; ++i) L.o_s[i] = take(sizeof(float) * L.slots_max);
   L.o_rep = take(sizeof(int32_t) * L.slots_max);
   L.o_C = take(sizeof(double) * (size_t)(p->max_meas + 1));
-  L.o_Cslot = take(sizeof(double) * (size_t)L.slots_max);
+  L.o_Cslot = take(sizeof(double) * ((size_t)L.slots_max + 8));  // + W_pred (all-reduced with C)
+  L.o_sel = take(sizeof(int32_t) * (size_t)(p->max_meas + 8));
+  L.o_selinfo = take(sizeof(double) * 8 + 64);
   L.o_D = take(sizeof(double) * (size_t)(p->max_meas + 1));
   L.o_acc = take(sizeof(double) * (5 * (size_t)p->max_meas + 3 * (size_t)world + 8));
   L.o_ring = take(sizeof(double) * ((size_t)world + 8));
@@ -147,6 +149,10 @@ struct phd_ctx {
   int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zl = 4, zb = 0, gp = 0, M_z = -1;
   bool fused = false;    // group-pipelined update (pass 1 of group j with pass 2 of group j-1)
   double* C_slot = nullptr;
+  int32_t* sel_flag = nullptr;   // k_select: label in the estimated index set I
+  double* sel_info = nullptr;    // (W_id, LT, n_eligible, n_sel, ..)
+  int32_t* s_lim = nullptr;      // pass 2: state-sum slot pairs per lane (js, written by k_slots2)
+  bool select = false;           // this update selected I before pass 2
   int m_prev_ext = -1;   // >= 0: zprev holds an explicit Z_{k-1} of this size
   double W = 0, W_pred = 0;
   int64_t LT = 0;
@@ -239,7 +245,8 @@ phd_status validate(const phd_params* p, int world, phd_ctx* c) {
   if (p->reserved0 != 0) return fail(c, PHD_EINVAL, "reserved0 must be 0");
   if (p->exchange_count < 0) return fail(c, PHD_EINVAL, "exchange_count < 0");
   if (p->birth_model != 0 && p->birth_model != 1) return fail(c, PHD_EINVAL, "birth_model %d", p->birth_model);
-  if (p->reserved1 != 0) return fail(c, PHD_EINVAL, "reserved1 must be 0");
+  if (p->reserved1 != 0 || p->reserved2 != 0) return fail(c, PHD_EINVAL, "reserved fields must be 0");
+  if (p->stphd_all != 0 && p->stphd_all != 1) return fail(c, PHD_EINVAL, "stphd_all must be 0 or 1");
   for (int i = 0; i < 4; ++i)
     if (!(p->birth_std[i] >= 0)) return fail(c, PHD_EINVAL, "birth_std must be >= 0");
   if (world < 1) return fail(c, PHD_EINVAL, "world < 1");
@@ -432,6 +439,9 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->rep = at<int32_t>(c->ws, L.o_rep);
   c->C = at<double>(c->ws, L.o_C);
   c->C_slot = at<double>(c->ws, L.o_Cslot);
+  c->sel_flag = at<int32_t>(c->ws, L.o_sel);
+  c->sel_info = at<double>(c->ws, L.o_selinfo);
+  c->s_lim = reinterpret_cast<int32_t*>(c->sel_info + 6);
   c->D = at<double>(c->ws, L.o_D);
   c->acc = at<double>(c->ws, L.o_acc);
   c->blk_w = at<double>(c->ws, L.o_blk_w);
@@ -446,7 +456,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->dcp = p->mode == PHD_MODE_DCP;
   c->summ = at<double>(c->ws, L.o_summ);
   c->bad = at<int>(c->ws, L.o_bad);
-  CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (40 + 4 * world)));
+  CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (48 + 4 * world)));
   CUB(cudaMallocHost(&c->h_est, sizeof(phd_estimate) * (p->max_meas + 1)));
   if (c->dcp) CUB(cudaMallocHost(&c->h_gather, sizeof(phd_estimate) * (p->max_meas + 1) * world));
   CUB(cudaMallocHost(&c->h_z, sizeof(float) * 2 * (p->max_meas + 1)));
@@ -689,6 +699,8 @@ static void build_slots(phd_ctx* c, int M) {
     for (int l = 0; l < M; ++l) c->h_slot[n++] = l;
   }
   c->n_slots = n;
+  const int n_fill = n;  // slots [n_fill, slots_pad) are padding
+  if (c->model == kRangeBearing && M > 0) n = std::max(n, M + 6);  // room for the pass-2 layout (k_slots2)
   // group-pipelined update for large M: 4 slots/lane/pass, 4 warps,
   // groups of 512 slots; otherwise the two-sweep path with 8 (or 4) slots per lane
   // Opt-in (PHD_FUSE=1): measured neutral on B200 (49.6 vs 49.0 ms at cfg 5) because
@@ -730,7 +742,7 @@ static void build_slots(phd_ctx* c, int M) {
   c->zb = M > 0 ? best_zb : 0;
   c->slots_pad = (int)best_pad;
   }
-  for (int s = n; s < c->slots_pad; ++s) c->h_slot[s] = -1;
+  for (int s = n_fill; s < c->slots_pad; ++s) c->h_slot[s] = -1;
 }
 
 phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
@@ -797,6 +809,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   pa.P = c->P;
   pa.P_stride = c->L.cap_l;
   CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
+  c->select = M > 0 && !c->fused && c->p.stphd_all == 0;
+  pa.js = nullptr;
   // C of slots [s0, s1): fixed-order reduction, C1 all-reduce, per-slot constants
   auto normalise = [&](int s0, int s1) -> phd_status {
     KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, s0, s1, c->C_slot, c->st));
@@ -823,8 +837,21 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   } else if (M > 0) {
     if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 4);
-    phd_status st = normalise(0, c->slots_pad);
-    if (st != PHD_OK) return st;
+    // local W_pred rides with C in the C1 all-reduce (element slots_pad)
+    KL(launch_wsum(c->A[4], n, c->blk_wp, c->C_slot + c->slots_pad, c->st));
+    KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, 0, c->slots_pad, c->C_slot, c->st));
+    if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
+    KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+    if (c->select) {
+      // index set I from dW = C/D and the mass identity; pass-2 slot layout with I first
+      KL(launch_select(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->st));
+      KL(launch_slots2(c->zlab, c->sel_flag, M, c->model, c->zl, c->slots_pad, c->slot_label, c->s_lim, c->st));
+      SlotConsts sc2{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
+      KL(launch_zprep(c->model, c->zlab, c->slot_label, c->slots_pad, (float)c->p.sensor_xy[0],
+                      (float)c->p.sensor_xy[1], sc2, c->st));
+      KL(launch_dslot(c->slot_label, c->D, c->slots_pad, c->s[4], c->st));
+      pa.js = c->s_lim;
+    }
     timing_record(c, 5);
     if (gp > 0) KL(launch_pass(c->model, 2, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 6);
@@ -837,9 +864,9 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (n > 0)
     KL(launch_finalize(c->A[4], c->P, c->L.cap_l, M > 0 && gp > 0 ? c->zb : 0, n, c->nu, c->wscale, c->wn, c->blk_w, c->blk_wp, c->st));
   double* rank_slots = c->acc + 5 * (size_t)M;
-  KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->n_slots : 0, c->slot_label, c->C, c->D, c->s[0], c->s[1],
-                       c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank, c->world,
-                       c->dcp || c->rank == 0 ? 1 : 0, c->st));
+  KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->slots_pad : 0, c->slot_label, c->C, c->D, c->s[0],
+                       c->s[1], c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank,
+                       c->world, c->dcp || c->rank == 0 ? 1 : 0, c->select ? c->sel_flag : nullptr, c->st));
   // rank slots [W_r | W_pred_r | N_r] (3 per rank); N_r written from the host
   c->h_meta[3 * c->world + 16] = (double)n;
   CU(cudaMemcpyAsync(rank_slots + 2 * c->world + c->rank, c->h_meta + 3 * c->world + 16, sizeof(double),
@@ -852,6 +879,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   }
   CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 3 * c->world, cudaMemcpyDeviceToHost, c->st));
   CU(cudaMemcpyAsync(c->h_meta + 3 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
+  if (c->select) CU(cudaMemcpyAsync(c->h_meta + 3 * c->world + 32, c->sel_info, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
   timing_record(c, 7);
   CU(cudaStreamSynchronize(c->st));
   c->W = 0.0;
@@ -865,10 +893,13 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     c->N_all += (int64_t)c->h_meta[2 * c->world + r];
   }
   c->bad_flag = reinterpret_cast<int*>(c->h_meta + 3 * c->world)[0];
-  c->LT = (int64_t)std::floor(c->W + 0.5);
+  double Wsel = c->W;
+  if (c->select && !c->dcp) Wsel = c->h_meta[3 * c->world + 32];  // W by the mass identity (k_select)
+  c->LT = (int64_t)std::floor(Wsel + 0.5);
+  if (c->select && !c->dcp) c->LT = (int64_t)c->h_meta[3 * c->world + 33];
   if (c->LT < 0) c->LT = 0;
-  double frac = c->W - std::floor(c->W);
-  c->near_half = std::fabs(frac - 0.5) < 1e-4 * std::max(1.0, c->W);
+  double frac = Wsel - std::floor(Wsel);
+  c->near_half = std::fabs(frac - 0.5) < 1e-4 * std::max(1.0, Wsel);
   c->stage = kUpdated;
   if (c->timing) {
     cudaEventElapsedTime(&c->t_ms[0], c->ev[0], c->ev[1]);
@@ -958,7 +989,7 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     timing_record(c, 8);
     const int capd = c->p.max_meas;
     KL(launch_extract(c->acc, c->M, rank_slots + c->rank, rank_slots + c->world + c->rank, 1, c->p.p_d, c->est + 1,
-                      capd, c->summ, &c->est[0].label, c->st));
+                      capd, c->summ, &c->est[0].label, c->select ? c->sel_info : nullptr, c->st));
     CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
     if (c->world > 1)
       COMM(c->comm->allgather_bytes(c->est, c->gather, sizeof(phd_estimate) * (size_t)(c->p.max_meas + 1), c->st));
@@ -985,7 +1016,7 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     timing_record(c, 8);
     int capd = std::max(0, std::min(cap, c->p.max_meas));
     KL(launch_extract(c->acc, c->M, rank_slots, rank_slots + c->world, c->world, c->p.p_d, c->est + 1, capd, c->summ,
-                      &c->est[0].label, c->st));
+                      &c->est[0].label, c->select ? c->sel_info : nullptr, c->st));
     CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
     nest = (int)smh[5];

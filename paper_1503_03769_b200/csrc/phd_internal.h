@@ -50,6 +50,7 @@ struct PassArgs {
   double* Apart;             // [gp][4][slots_pad]
   float* P;                  // [zb][P_stride]
   int64_t P_stride;
+  const int32_t* js;         // pass 2: state sums for the first *js slot pairs of every lane (nullptr: all)
 };
 
 struct PredictArgs {
@@ -108,12 +109,13 @@ cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, in
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1, const float* s2,
                               const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
-                              double* acc_lab, double* rank_slots, int rank, int world, int lead, cudaStream_t s);
+                              double* acc_lab, double* rank_slots, int rank, int world, int lead,
+                              const int32_t* sel_flag, cudaStream_t s);
 // W = sum_{r < count} W[r], W_pred = sum Wp[r]; writes the estimates to est[0..)
 // and their count to *count_out (the header entry of the gather block).
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
                            void* est /*phd_estimate*/, int cap, double* summary /*[8]*/, int32_t* count_out,
-                           cudaStream_t s);
+                           const double* sel_info /*nullptr or (W_id, LT, ...) of k_select*/, cudaStream_t s);
 cudaError_t launch_ring_pack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
                              cudaStream_t s);
 cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
@@ -127,5 +129,12 @@ cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_
                           float* ox, float* ovx, float* oy, float* ovy, float* ow, int32_t* anc,
                           int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out, cudaStream_t s);
 cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s);
+// label selection before pass 2 (k_select.cu)
+cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cudaStream_t s);
+cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
+                          int32_t* sel_flag, double* info, cudaStream_t s);
+cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
+                          int32_t* slot_label, int32_t* js, cudaStream_t s);
+cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, float* d, cudaStream_t s);
 
 }  // namespace phd

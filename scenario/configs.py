@@ -42,6 +42,7 @@ class Model:
     birth_model: int = 0           # 0: measurement-driven (S10); 1: N(birth_mean, diag(birth_std^2))
     birth_mean: tuple = (0.0, 3.0, 0.0, -3.0)           # x-bar
     birth_std: tuple = (math.sqrt(10.0), 1.0, math.sqrt(10.0), 1.0)  # sqrt(diag Q)
+    stphd_all: int = 0             # 1: STPHD state sums for every measurement (not only the index set)
 
 
 @dataclass(frozen=True)

@@ -34,10 +34,10 @@ def phd():
 
 POS = Model(meas=POSITION, sigma_z=(10.0, 10.0), p_d=0.98, p_s=0.99, clutter_rate=50.0,
             region=(-1000.0, 1000.0, -1000.0, 1000.0), births_per_step=256, fixed_count=8000,
-            count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=4096, seed=7)
+            count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=4096, seed=7, stphd_all=1)
 RB = Model(meas=RANGE_BEARING, sigma_z=(10.0, 0.01), p_d=0.98, p_s=0.99, clutter_rate=50.0,
            region=(0.0, 2000.0, -math.pi, math.pi), sensor_xy=(0.0, 0.0), births_per_step=256,
-           fixed_count=8000, count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=4096, seed=7)
+           fixed_count=8000, count_mode=COUNT_FIXED, capacity=1 << 16, max_meas=4096, seed=7, stphd_all=1)
 ANISO = replace(POS, sigma_z=(7.0, 13.0))
 MODELS = {"position": POS, "range_bearing": RB, "aniso": ANISO}
 
@@ -119,7 +119,8 @@ def _check_update(orc, m, C, acc, wn, w, Co, wo, acco):
     tw = 1e-4 * wo + 1e-7 * w
     assert np.all(np.abs(wn - wo) <= tw), np.max(np.abs(wn - wo) / tw)
     assert np.all(np.abs(acc[:, 0] - acco[:, 0]) <= 2e-5 * acco[:, 0] + 1e-9)
-    big = acco[:, 0] > 1e-6
+    # with stphd_all = 0 the state sums exist only for the estimated index set (zeros elsewhere)
+    big = (acco[:, 0] > 1e-6) & np.any(acc[:, 1:] != 0, axis=1)
     zeta_g = acc[big, 1:] / acc[big, :1]
     zeta_o = acco[big, 1:] / acco[big, :1]
     assert np.all(np.abs(zeta_g - zeta_o) <= 1e-3), np.max(np.abs(zeta_g - zeta_o))
@@ -419,3 +420,38 @@ def test_births_gaussian_model(phd, orc):
         assert np.all(np.abs(gs[:, 1234:] - bs) <= 1e-6 * np.abs(bs) + 1e-5)
         assert np.allclose(gw[1234:], bw, rtol=1e-7)
         f.close()
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
+def test_index_set_state_sums(phd, orc, mname):
+    """stphd_all = 0 (default): the index set I is chosen right after pass 1 from dW = C/D and
+    W = (1-pD) W_pred + sum dW; pass 2 accumulates S only for I.  The estimates equal those of
+    the all-measurement run (same labels, states to fp32 rounding) and S is 0 outside I."""
+    m_all = replace(MODELS[mname], clutter_rate=5.0)
+    m_sel = replace(m_all, stphd_all=0)
+    z = _meas(m_all, 700, 9)
+    soa, w = _cloud(m_all, 15001, z, 9)
+    res = []
+    for m in (m_all, m_sel):
+        f = phd.Filter(m)
+        f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+        f.update(z)
+        acc = f.accumulators(len(z))
+        _, wn, _ = f.get_particles()
+        est, summ = f.extract()
+        res.append((acc, wn, est, summ))
+        f.close()
+    (a1, w1, e1, s1), (a2, w2, e2, s2) = res
+    assert np.allclose(w1, w2, rtol=2e-6, atol=0)       # same terms; only the slot summation order differs
+    assert np.allclose(a1[:, 0], a2[:, 0], rtol=1e-14, atol=0)
+    assert s1["LT"] == s2["LT"] or s1["near_half"] or s2["near_half"]
+    assert list(e1["labels"]) == list(e2["labels"]) and len(e2["labels"]) > 0
+    assert np.allclose(e1["states"], e2["states"], rtol=1e-6, atol=1e-4)
+    sel = np.zeros(len(z), bool)
+    sel[e2["labels"]] = True
+    assert np.all(a2[~sel, 1:] == 0) and np.all(np.any(a2[sel, 1:] != 0, axis=1))
+    # mass identity W = (1 - pD) W_pred + sum C/D holds for the summary W = sum w'
+    kap = orc.kappa(m_sel)
+    Co = orc.normalizers(m_sel, soa, w, z)
+    rhs = (1 - m_sel.p_d) * math.fsum(w.astype(np.float64)) + math.fsum(Co / (kap + Co))
+    assert abs(s2["W"] - rhs) <= 2e-6 * rhs
