@@ -154,3 +154,17 @@ def test_exchange_moves_mass_to_every_rank(phd):
     for f in fs:
         f.close()
     group.close()
+
+
+def test_rank_with_no_particles(phd):
+    """Tiny population over 4 ranks: some ranks hold no survivors (and no births) in a step;
+    the collectives still line up and the result equals the 1-rank run."""
+    from dataclasses import replace as rp
+    cfg = _cfg("cfg3")
+    m = rp(cfg.model, fixed_count=3, births_per_step=2, capacity=64, max_meas=4096)
+    cfg = rp(cfg, model=m)
+    ref = _run(phd, cfg, 1, 2)
+    got = _run(phd, cfg, 4, 2)
+    for k in range(2):
+        assert abs(ref["summ"][k]["W"] - got["summ"][k]["W"]) <= 1e-6 * max(1.0, ref["summ"][k]["W"])
+        assert np.array_equal(ref["anc"][k], got["anc"][k])

@@ -455,3 +455,59 @@ def test_index_set_state_sums(phd, orc, mname):
     Co = orc.normalizers(m_sel, soa, w, z)
     rhs = (1 - m_sel.p_d) * math.fsum(w.astype(np.float64)) + math.fsum(Co / (kap + Co))
     assert abs(s2["W"] - rhs) <= 2e-6 * rhs
+
+
+def test_edge_counts_and_flags(phd, orc):
+    """M = 1; M = max_meas = 8192 (largest sort / slot layout); LT above the eligible labels
+    (lt_clamped); adaptive N_out clamped to capacity - J (count_clamped)."""
+    m = replace(POS, max_meas=8192, stphd_all=0)
+    for M in (1, 8192):
+        z = _meas(m, M, 4)
+        soa, w = _cloud(m, 3001, z[:min(M, 50)], 4)
+        f = phd.Filter(m)
+        f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+        f.update(z)
+        C = f.normalizers(M)
+        _, wn, _ = f.get_particles()
+        Co = orc.normalizers(m, soa, w, z)
+        wo, _ = orc.update(m, soa, w, z, Co)
+        kap = orc.kappa(m)
+        assert np.all(np.abs(C - Co) <= 1e-5 * Co + 1e-9 * kap)
+        assert np.all(np.abs(wn - wo) <= 1e-4 * wo + 1e-7 * w)
+        est, summ = f.extract()
+        assert len(est["labels"]) == min(summ["LT"], int(np.sum(f.accumulators(M)[:, 0] > 0)))
+        f.close()
+    # LT > eligible: large mass, two measurements
+    z = np.array([[0.0, 0.0], [300.0, 300.0]], np.float32)
+    soa, w = _cloud(m, 2000, z, 1)
+    w = np.full(2000, 6.0 / 2000, np.float32)   # pD = 0.5: W = 0.5 * 6 + ~2 -> LT = 5 > 2 labels
+    f = phd.Filter(replace(m, p_d=0.5))
+    f.set_particles(soa, w, 2000, stage=phd.STAGE_PREDICTED)
+    f.update(z)
+    est, summ = f.extract()
+    assert summ["LT"] > 2 and summ["lt_clamped"] == 1 and len(est["labels"]) == 2
+    f.close()
+    # adaptive count clamp
+    ma = replace(scenario.get("cfg1").model, capacity=2200, births_per_step=200, particles_per_target=500,
+                 p_d=0.0)                           # no detection: the mass (~8) is kept
+    soa, w = scenario.random_particles(1500, 2)
+    w[:] = 8.0 / 1500                              # ~8 targets' mass -> wants 8 * 500 > 2000
+    f = phd.Filter(ma)
+    f.set_particles(soa, w, 1500)
+    f.predict(1)
+    f.update(np.zeros((0, 2), np.float32))
+    est, summ = f.extract()
+    assert summ["count_clamped"] == 1 and summ["N_out"] == ma.capacity - ma.births_per_step
+    f.resample_exchange(1)
+    assert f.resample_meta()["N_out"] == 2000
+    f.close()
+
+
+def test_range_bearing_seam_exact_pi(phd, orc):
+    """Measurements exactly at +pi and -pi (fp32), targets straddling the seam."""
+    m = replace(RB, stphd_all=1)
+    z = np.array([[500.0, np.float32(math.pi)], [500.0, np.float32(-math.pi)], [700.0, 3.1],
+                  [700.0, -3.1], [650.0, 0.0]], np.float32)
+    f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 6000, len(z), 2, z=z)
+    _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
+    f.close()
