@@ -299,11 +299,13 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
     else sweep(std::integral_constant<int, (NP > 3 ? 3 : 1)>{});
 
     if (more) ld.store(recs + (buf ^ 1) * kTileP * L::WIDTH, a.wscale, tid, nthr);
-    // tile sums (<= 64 particles in fp32) -> fp64
+    // tile sums (<= 64 particles in fp32) -> fp64; pass 2 only for the js slot
+    // pairs that carry state sums (the F2F conversions share the XU pipe with EX2)
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
 #pragma unroll
       for (int j = 0; j < NP; ++j) {
+        if (PASS == 2 && j >= js) continue;
         out64[(q * ZL + 2 * j) * nthr + tid] += (double)in[q][j].x;
         out64[(q * ZL + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
         in[q][j] = f2(0.0f, 0.0f);
