@@ -1,8 +1,8 @@
 // The fused two-pass particle x measurement update (§2.2 step 2,
 // Eqs 7-8; §3 Eqs 10-16).  Never materialises the N x M likelihood matrix.
 //
-// Tiling: measurement-stationary.  A CTA owns wz x 128
-// measurement slots (each lane 4 slots = two f32x2 pairs held in registers);
+// Tiling: measurement-stationary.  A CTA owns wz x 32 x ZL
+// measurement slots (each lane ZL = 8 slots = four f32x2 pairs in registers);
 // particles stream through shared memory in tiles of 64 and are broadcast to
 // every lane.  Per (particle, slot) pair the lane evaluates the likelihood with
 // packed FFMA2/FADD2/FMUL2 and one MUFU.EX2:
@@ -10,9 +10,8 @@
 //   pass 1:  C_s += u                                                      (Eq 7)
 //   pass 2:  P_i += u d_s, d_s = 1/(kappa + C_s);  S'_s += u (x_i - z_s), u vx_i, ...
 //            (Eqs 8, 12-16; dW_s = C_s/D_s)
-// Per-slot sums accumulate in fp32 over one tile (64 particles), then in an
-// fp32 mid level over 16 tiles, then in fp64 (DESIGN.md §5 "accumulation
-// precision").  Per-particle sums Pe_i are reduced across lanes with a
+// Per-slot sums accumulate in fp32 over one tile (64 particles), then in fp64
+// in shared memory (DESIGN.md §5 "accumulation precision").  Per-particle sums Pe_i are reduced across lanes with a
 // transposed butterfly and across warps through shared memory, giving one
 // fp32 partial per (particle, z-block).  Cross-CTA sums are fp64 in fixed order.
 #include "phd_internal.h"
@@ -25,12 +24,18 @@
 #ifndef PHD_PP_UNROLL2
 #define PHD_PP_UNROLL2 4
 #endif
+// pass 1: evaluate exp2 of the last slot pair with the FFMA2 polynomial on every
+// PHD_EMU_PERIOD-th particle (0 = never); the rest go to MUFU.EX2
+#ifndef PHD_EMU_PERIOD
+#define PHD_EMU_PERIOD 4
+#endif
 
 namespace phd {
 
 // particles unrolled per lane in the pair loop (pass 1 / pass 2; measured on B200)
 constexpr int kPPUnroll1 = PHD_PP_UNROLL1;
 constexpr int kPPUnroll2 = PHD_PP_UNROLL2;
+constexpr int kEmuPeriod = PHD_EMU_PERIOD;
 
 __device__ __forceinline__ float ex2a(float x) {
   float y;
@@ -39,6 +44,27 @@ __device__ __forceinline__ float ex2a(float x) {
 }
 __device__ __forceinline__ float2 ex2v(float2 a) { return make_float2(ex2a(a.x), ex2a(a.y)); }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// 2^x for a pair on the FMA pipe (MUFU offload):
+// x = j + r with j = rint(x) by the 1.5*2^23 shifter, |r| <= 1/2, 2^r by a
+// degree-5 polynomial (relative error <= 3.2e-7 including fp32 Horner rounding,
+// tools/fit_exp2_poly.py; MUFU.EX2 is ~2 ulp), exponent j added to the bits.
+// x is clamped to -127, where the result is +0 exactly; for x in (-127, -126)
+// it returns a value below 2^-126 that ex2.approx.ftz would flush to 0.
+__device__ __forceinline__ float2 ex2_poly(float2 x) {
+  constexpr float kShift = 12582912.0f;  // 1.5 * 2^23
+  x = f2(fmaxf(x.x, -127.0f), fmaxf(x.y, -127.0f));
+  const float2 t = __fadd2_rn(x, f2(kShift, kShift));
+  const float2 mj = __fadd2_rn(f2(kShift, kShift), f2(-t.x, -t.y));  // -j, exact
+  const float2 r = __fadd2_rn(x, mj);                                // exact
+  float2 p = __ffma2_rn(f2(1.2943478e-3f, 1.2943478e-3f), r, f2(9.6695982e-3f, 9.6695982e-3f));
+  p = __ffma2_rn(p, r, f2(5.5516288e-2f, 5.5516288e-2f));
+  p = __ffma2_rn(p, r, f2(2.4022245e-1f, 2.4022245e-1f));
+  p = __ffma2_rn(p, r, f2(6.9314647e-1f, 6.9314647e-1f));
+  p = __ffma2_rn(p, r, f2(1.0f, 1.0f));
+  return f2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+            __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 
 // Shared-memory particle record widths (floats, multiple of 4).
 template <int MODEL, int PASS>
@@ -266,7 +292,9 @@ __global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a)
           if (PASS == 1) {
             // u = p_D g w = 2^(-alpha q + log2(p_D c w)), flushed to zero below 2^-126
             // exactly as in pass 2 (the two passes see bitwise-identical terms)
-            in[0][j] = __fadd2_rn(in[0][j], ex2v(expo<MODEL>(d0, d1, na0, na1, wv)));
+            const float2 e = expo<MODEL>(d0, d1, na0, na1, wv);
+            const bool emu = kEmuPeriod > 0 && j == NP - 1 && pp % (kEmuPeriod > 0 ? kEmuPeriod : 1) == 0;
+            in[0][j] = __fadd2_rn(in[0][j], emu ? ex2_poly(e) : ex2v(e));
           } else {
             const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
             pacc = __ffma2_rn(u, z.d[j], pacc);
