@@ -34,7 +34,8 @@ class _Model(ctypes.Structure):
                 ("region", ctypes.c_double * 4), ("clutter_rate", ctypes.c_double),
                 ("birth_mass", ctypes.c_double), ("birth_sigma_v", ctypes.c_double),
                 ("seed", ctypes.c_uint64), ("birth_model", ctypes.c_int32), ("pad2_", ctypes.c_int32),
-                ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4)]
+                ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4),
+                ("proposal_scale", ctypes.c_double)]
 
 
 _lib = None
@@ -64,6 +65,8 @@ def lib():
         L.orc_predict.argtypes = [M, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _D, _D, _D, _D, _D]
         L.orc_births.argtypes = [M, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                  ctypes.c_int64, _D, ctypes.c_int32, _D, _D, _D, _D, _D]
+        L.orc_birth_is_weights.argtypes = [M, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _D,
+                                           ctypes.c_int32, _D, _D, _D, _D, _D]
         L.orc_normalizers.argtypes = [M, ctypes.c_int64, _D, _D, _D, _D, ctypes.c_int32, _D]
         L.orc_update.argtypes = [M, ctypes.c_int64, _D, _D, _D, _D, _D, _D, ctypes.c_int32, _D, _D, _D]
         L.orc_extract.argtypes = [M, ctypes.c_int32, _D, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
@@ -94,6 +97,7 @@ def model(m):
     for i in range(4):
         om.birth_mean[i] = float(getattr(m, "birth_mean", (0.0, 0.0, 0.0, 0.0))[i])
         om.birth_std[i] = float(getattr(m, "birth_std", (0.0, 0.0, 0.0, 0.0))[i])
+    om.proposal_scale = float(getattr(m, "proposal_scale", 1.0))
     return om
 
 
@@ -145,12 +149,18 @@ def predict(m, k, soa, w, g0=0):
     return np.stack([x, vx, y, vy]), ww
 
 
-def births(m, k, n_out, J, zprev, b0=0, nb=None):
+def births(m, k, n_out, J, zprev, b0=0, nb=None, blo=0):
+    """Eq 6: births b0 .. b0+nb-1 of this filter's J (global slots n_out + b).
+    birth_model 2 weights them by the full ratio over the filter's births [blo, blo+J)."""
     nb = J - b0 if nb is None else nb
     zp = _f64(np.zeros((0, 2)) if zprev is None else zprev).reshape(-1, 2)
     out = [np.zeros(nb) for _ in range(5)]
-    lib().orc_births(ctypes.byref(model(m)), int(k), int(n_out), int(J), int(b0), int(nb),
+    om = model(m)
+    lib().orc_births(ctypes.byref(om), int(k), int(n_out), int(J), int(b0), int(nb),
                      _d(zp), int(len(zp)), *[_d(a) for a in out])
+    if om.birth_model == 2:
+        lib().orc_birth_is_weights(ctypes.byref(om), int(J), int(blo), int(nb), _d(zp), int(len(zp)),
+                                   *[_d(a) for a in out])
     return np.stack(out[:4]), out[4]
 
 

@@ -87,7 +87,7 @@ def dcp_step(m, k, groups, z, zprev, n_out_rule, L_param=0):
         b0, b1 = block(J, K, j)
         # Eq 6 with the group's own J_k: each group is a separate PHD filter of the full
         # intensity, so its births carry the full birth mass gamma
-        bs, bw = births(m, k, group_base(j, K) + n_j - b0, b1 - b0, zprev, b0=b0, nb=b1 - b0)
+        bs, bw = births(m, k, group_base(j, K) + n_j - b0, b1 - b0, zprev, b0=b0, nb=b1 - b0, blo=b0)
         xs = np.concatenate([ps, bs], axis=1)
         ws = np.concatenate([pw, bw])
         C = normalizers(m, xs, ws, z)                                          # Eq 11 (group-local)

@@ -103,19 +103,36 @@ double orc_likelihood(const orc_model* m, double z0, double z1, double x, double
 }
 
 /* ---------------------------------------------------------------------- */
+/* N(a; mu, sd^2) on the real line. */
+static double normal1(double a, double mu, double sd) {
+  double t = (a - mu) / sd;
+  return exp(-0.5 * t * t) / (sqrt(2.0 * ORC_PI) * sd);
+}
+
 /* 1) Prediction (§2.2 step 1, Eq 5; Algorithm 1).
- * q_k = transition prior (S10), so the Eq 5 ratio phi/q is e_{k|k-1} = p_s and
- * w~ = p_s w.  The transition is the CV model x' = F x + G w_k
- * with w_k = sigma_a (n1, n2), n from Box-Muller of Philox({g, k, 1, g>>32}). */
+ * The transition is the CV model x' = F x + G w_k with
+ * w_k = sigma_a (n1, n2), n from Box-Muller of Philox({g, k, 1, g>>32}).
+ * q_k is the same CV model with noise std s sigma_a (s = proposal_scale; s = 1
+ * is the transition prior of S10).  phi_{k|k-1}(x, x') = e_{k|k-1} f(x|x')
+ * (no spawning), so Eq 5 gives w~ = p_s f(x|x') / q(x|x') w.  f and q are both
+ * carried by the plane x = F x' + G a, so their ratio is the ratio of the noise
+ * densities N(a; 0, sigma_a^2 I) / N(a; 0, s^2 sigma_a^2 I) at the drawn a. */
 void orc_predict(const orc_model* m, int32_t k, int64_t n, int64_t g0,
                  double* x, double* vx, double* y, double* vy, double* w) {
   double T = m->T;
+  double s = m->proposal_scale > 0.0 ? m->proposal_scale : 1.0;
   for (int64_t i = 0; i < n; ++i) {
     uint32_t o[4];
     philox_at(m, (uint64_t)(g0 + i), k, 1u, o);
     double n1, n2;
     orc_box_muller(orc_conv23(o[0]), orc_conv23(o[1]), &n1, &n2);
-    double ax = m->sigma_a * n1, ay = m->sigma_a * n2;
+    double ax = s * m->sigma_a * n1, ay = s * m->sigma_a * n2;
+    double ratio = 1.0;
+    if (s != 1.0 && m->sigma_a > 0.0) {
+      double f = normal1(ax, 0.0, m->sigma_a) * normal1(ay, 0.0, m->sigma_a);
+      double q = normal1(ax, 0.0, s * m->sigma_a) * normal1(ay, 0.0, s * m->sigma_a);
+      ratio = f / q;
+    }
     double x1 = x[i] + T * vx[i] + 0.5 * T * T * ax;
     double vx1 = vx[i] + T * ax;
     double y1 = y[i] + T * vy[i] + 0.5 * T * T * ay;
@@ -124,7 +141,7 @@ void orc_predict(const orc_model* m, int32_t k, int64_t n, int64_t g0,
     vx[i] = vx1;
     y[i] = y1;
     vy[i] = vy1;
-    w[i] = m->p_s * w[i];
+    w[i] = m->p_s * ratio * w[i];
   }
 }
 
@@ -132,7 +149,9 @@ void orc_predict(const orc_model* m, int32_t k, int64_t n, int64_t g0,
  * J_k births drawn from p_k(.|Z) -- measurement-driven around Z_{k-1} (S10),
  * uniform over the region when no previous measurement exists -- each with
  * weight gamma / J_k (importance ratio read as 1, S10).  Birth b uses
- * measurement b mod M_{k-1} and the four normals of Philox({n_out+b, k, 2, .}). */
+ * measurement b mod M_{k-1} and the four normals of Philox({n_out+b, k, 2, .}).
+ * birth_model 2 draws the same way; orc_birth_is_weights then replaces the
+ * weights by the full Eq 6 ratio. */
 void orc_births(const orc_model* m, int32_t k, int64_t n_out, int64_t J, int64_t b0, int64_t nb,
                 const double* zprev, int32_t m_prev,
                 double* x, double* vx, double* y, double* vy, double* w) {
@@ -173,6 +192,61 @@ void orc_births(const orc_model* m, int32_t k, int64_t n_out, int64_t J, int64_t
     vx[i] = m->birth_sigma_v * n3;
     vy[i] = m->birth_sigma_v * n4;
     w[i] = m->birth_mass / (double)J;
+  }
+}
+
+/* Number of birth indices b in [0, e) with b mod M == c. */
+static int64_t count_below(int64_t e, int64_t c, int64_t M) { return e > c ? (e - c - 1) / M + 1 : 0; }
+
+/* Eq 6 with the full importance ratio: w = gamma(x) / (J p_k(x|Z)).
+ * gamma(x) = birth_mass N(x; x-bar, Q) over (x, vx, y, vy).
+ * p_k is the density the births [blo, blo+J) of this filter are drawn from: birth b
+ * takes component c = b mod M_{k-1} deterministically, so p_k is the mixture
+ * sum_c (n_c / J) q_c with n_c the number of those births using c (the balance-heuristic
+ * estimator, unbiased for any n_c).  q_c = (position law) x N(vx; 0, sv^2) N(vy; 0, sv^2),
+ * the position law being
+ *   position sensor:      N(x; z_c0, s0^2) N(y; z_c1, s1^2);
+ *   range-bearing sensor: (a, c) ~ N(z_c, diag(s0^2, s1^2)) mapped by (a cos c, a sin c),
+ *     whose density at (x, y) is the sum over the preimages (r, th) and (-r, th + pi) of
+ *     N(a; z_c0, s0^2) N(wrap(c - z_c1); 0, s1^2) / r (Jacobian |a| = r; bearing wrapped
+ *     into (-pi, pi], the nearest 2 pi image);
+ * with no previous measurements, uniform over the region: 1/V (position) or 1/(V r). */
+void orc_birth_is_weights(const orc_model* m, int64_t J, int64_t blo, int64_t nb,
+                          const double* zprev, int32_t m_prev, const double* x, const double* vx,
+                          const double* y, const double* vy, double* w) {
+  double V = (m->region[1] - m->region[0]) * (m->region[3] - m->region[2]);
+  for (int64_t i = 0; i < nb; ++i) {
+    double r = 0.0, th = 0.0;
+    if (m->meas != 0) {
+      double px = x[i] - m->sensor[0], py = y[i] - m->sensor[1];
+      r = sqrt(px * px + py * py);
+      th = (px == 0.0 && py == 0.0) ? 0.0 : atan2(py, px);
+    }
+    double pos = 0.0;
+    if (m_prev > 0) {
+      for (int32_t c = 0; c < m_prev; ++c) {
+        int64_t n_c = count_below(blo + J, c, m_prev) - count_below(blo, c, m_prev);
+        if (n_c == 0) continue;
+        const double* z = zprev + 2 * c;
+        double q;
+        if (m->meas == 0) {
+          q = normal1(x[i], z[0], m->sigma_z[0]) * normal1(y[i], z[1], m->sigma_z[1]);
+        } else {
+          double qa = normal1(r, z[0], m->sigma_z[0]) * normal1(wrap_pi(th - z[1]), 0.0, m->sigma_z[1]);
+          double qb = normal1(-r, z[0], m->sigma_z[0]) * normal1(wrap_pi(th + ORC_PI - z[1]), 0.0, m->sigma_z[1]);
+          q = (qa + qb) / r;
+        }
+        pos += (double)n_c / (double)J * q;
+      }
+    } else {
+      pos = m->meas == 0 ? 1.0 / V : 1.0 / (V * r);
+    }
+    double p = pos * normal1(vx[i], 0.0, m->birth_sigma_v) * normal1(vy[i], 0.0, m->birth_sigma_v);
+    double g = m->birth_mass * normal1(x[i], m->birth_mean[0], m->birth_std[0]) *
+               normal1(vx[i], m->birth_mean[1], m->birth_std[1]) *
+               normal1(y[i], m->birth_mean[2], m->birth_std[2]) *
+               normal1(vy[i], m->birth_mean[3], m->birth_std[3]);
+    w[i] = p > 0.0 ? g / ((double)J * p) : 0.0;
   }
 }
 

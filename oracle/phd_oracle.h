@@ -32,10 +32,14 @@ typedef struct {
   double birth_mass;     /* gamma: total birth mass per step */
   double birth_sigma_v;  /* birth velocity std */
   uint64_t seed;         /* Philox key {lo32, hi32} */
-  int32_t birth_model;   /* 0: around Z_{k-1} (S10); 1: N(birth_mean, diag(birth_std^2)) */
+  int32_t birth_model;   /* 0: around Z_{k-1} (S10); 1: N(birth_mean, diag(birth_std^2));
+                            2: drawn as 0, weighted by the full Eq 6 ratio gamma(x)/(J p_k(x|Z)) with
+                               gamma(x) = birth_mass N(x; birth_mean, diag(birth_std^2)) */
   int32_t pad2_;
   double birth_mean[4];  /* x-bar (x, vx, y, vy) */
   double birth_std[4];   /* sqrt(diag Q) */
+  double proposal_scale; /* s: Eq 5 proposal q_k = CV transition with noise std s sigma_a
+                            (0 or 1: q_k = transition prior, ratio p_s) */
 } orc_model;
 
 /* Philox4x32-10 block cipher; ctr = {c0,c1,c2,c3}, key = {k0,k1}. */
@@ -59,6 +63,12 @@ void orc_predict(const orc_model* m, int32_t k, int64_t n, int64_t g0,
 void orc_births(const orc_model* m, int32_t k, int64_t n_out, int64_t J, int64_t b0, int64_t nb,
                 const double* zprev, int32_t m_prev,
                 double* x, double* vx, double* y, double* vy, double* w);
+/* Eq 6 importance weights of nb births with states (x, vx, y, vy) (birth_model 2), into w:
+ * w_b = gamma(x_b) / (J p_k(x_b | Z_{k-1})), p_k the stratified proposal mixture
+ * of the births [blo, blo+J) of this filter (birth b uses component b mod m_prev). */
+void orc_birth_is_weights(const orc_model* m, int64_t J, int64_t blo, int64_t nb,
+                          const double* zprev, int32_t m_prev, const double* x, const double* vx,
+                          const double* y, const double* vy, double* w);
 /* Eq 7 / Eq 11: C[p] = sum_i p_D g(z_p | x_i) w_i. */
 void orc_normalizers(const orc_model* m, int64_t n, const double* x, const double* y,
                      const double* w, const double* z, int32_t nz, double* C);

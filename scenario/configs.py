@@ -39,10 +39,12 @@ class Model:
     seed: int = 1
     mode: int = 0                  # 0 exact (global C, exact resampling), 1 DCP (paper-literal groups)
     exchange_count: int = 0        # DCP ring exchange L (0: min_j N_j / 10)
-    birth_model: int = 0           # 0: measurement-driven (S10); 1: N(birth_mean, diag(birth_std^2))
+    birth_model: int = 0           # 0: measurement-driven (S10); 1: N(birth_mean, diag(birth_std^2));
+                                   # 2: drawn as 0, weighted gamma N(x; birth_mean, Q) / (J p_k(x|Z)) (Eq 6)
     birth_mean: tuple = (0.0, 3.0, 0.0, -3.0)           # x-bar
     birth_std: tuple = (math.sqrt(10.0), 1.0, math.sqrt(10.0), 1.0)  # sqrt(diag Q)
     stphd_all: int = 0             # 1: STPHD state sums for every measurement (not only the index set)
+    proposal_scale: float = 1.0    # Eq 5 proposal: CV transition with noise std s sigma_a (1: prior)
 
 
 @dataclass(frozen=True)

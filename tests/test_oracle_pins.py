@@ -472,3 +472,107 @@ def test_births_gaussian_model(orc):
     m0 = Model(birth_model=1, birth_std=(0.0, 0.0, 0.0, 0.0))
     s0, _ = orc.births(m0, 1, 0, 3, None)
     assert np.array_equal(s0, np.tile(np.array([[0.0], [3.0], [0.0], [-3.0]]), (1, 3)))
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: Eq 5 with a proposal q_k != transition prior, Eq 6 with the full ratio
+def test_predict_importance_proposal(orc):
+    """Eq 5: w~ = phi/q w with q the CV model of noise std s sigma_a.
+    Pins: (i) E_q[f/q] = 1 and the weighted noise moments equal the transition's
+    (importance-sampling identities, Monte Carlo); (ii) the closed form through the
+    Box-Muller radius, n1^2 + n2^2 = -2 ln u1, so phi/q = p_s s^2 u1^(s^2 - 1) exactly,
+    with u1 from ATen-pinned Philox; (iii) s = 1 is the transition prior."""
+    n = 400000
+    T, sa, ps, s = 1.0, 5.0, 0.99, 2.0
+    m = Model(T=T, sigma_a=sa, p_s=ps, proposal_scale=s, seed=11)
+    soa = np.tile(np.array([[10.0], [1.0], [-20.0], [-1.0]]), (1, n))
+    x, w = orc.predict(m, 3, soa, np.ones(n), g0=100)
+    a_x, a_y = (x[1] - 1.0) / T, (x[3] + 1.0) / T
+    # (i) unbiasedness and moments
+    assert abs(w.mean() - ps) < 5 * w.std() / math.sqrt(n)
+    assert abs(a_x.std() - s * sa) < 0.01 * s * sa  # drawn from q
+    for a in (a_x, a_y):
+        m2 = np.sum(w * a * a) / np.sum(w)
+        assert abs(m2 - sa * sa) < 0.02 * sa * sa  # weighted: the transition's variance
+    # (ii) closed form via the Box-Muller radius
+    for i in (0, 1, 7, 12345):
+        o = orc.philox([100 + i, 3, 1, 0], [11, 0])
+        u1 = orc.conv23(o[0])
+        assert abs(w[i] - ps * s * s * u1 ** (s * s - 1)) < 1e-12 * max(1.0, w[i])
+    # (iii) s = 1 -> q = f, ratio p_s
+    x1, w1 = orc.predict(Model(T=T, sigma_a=sa, p_s=ps, proposal_scale=1.0, seed=11), 3, soa[:, :10], np.ones(10))
+    assert np.all(w1 == ps)
+
+
+def _is_model(meas, **kw):
+    base = dict(birth_model=2, birth_mass=0.3, birth_sigma_v=4.0, seed=5)
+    if meas == POSITION:
+        base.update(meas=POSITION, sigma_z=(10.0, 10.0), birth_mean=(50.0, 1.0, -30.0, -2.0),
+                    birth_std=(40.0, 2.0, 30.0, 2.0))
+    else:
+        base.update(meas=RANGE_BEARING, sigma_z=(10.0, 0.02), sensor_xy=(0.0, 0.0),
+                    region=(0.0, 2000.0, -math.pi, math.pi),
+                    birth_mean=(400.0, 1.0, 300.0, -2.0), birth_std=(40.0, 2.0, 30.0, 2.0))
+    base.update(kw)
+    return Model(**base)
+
+
+@pytest.mark.parametrize("meas", [POSITION, RANGE_BEARING])
+def test_births_importance_weights_unbiased(orc, meas):
+    """Eq 6 with gamma(x) = gamma N(x; x-bar, Q)
+    and the measurement-driven proposal: the importance-sampling estimator is unbiased,
+    E[sum_b w_b h(x_b)] = gamma E_N[h], for h = 1, x, vy, (x - x-bar)^2.  A dropped
+    velocity density, a missing 1/J or a missing range-bearing Jacobian 1/r breaks it."""
+    m = _is_model(meas)
+    if meas == POSITION:
+        gx, gy = np.meshgrid(np.arange(-150.0, 251.0, 20.0), np.arange(-180.0, 121.0, 20.0))
+        zprev = np.stack([gx.ravel(), gy.ravel()], axis=1)
+    else:
+        r, th = np.meshgrid(np.arange(300.0, 701.0, 15.0), np.arange(0.35, 0.95, 0.02))
+        zprev = np.stack([r.ravel(), th.ravel()], axis=1)
+    J, blo = 200003, 17  # J not a multiple of M_{k-1}; the filter's births start at blo
+    s, w = orc.births(m, 4, 1000, J, zprev, b0=blo, nb=J, blo=blo)
+    tot = w.sum()
+    se = math.sqrt(J) * w.std()
+    assert abs(tot - m.birth_mass) < 5 * se and se < 0.02 * m.birth_mass
+    mx = np.sum(w * s[0]) / tot
+    assert abs(mx - m.birth_mean[0]) < 1.5
+    assert abs(np.sum(w * s[3]) / tot - m.birth_mean[3]) < 0.05
+    assert abs(math.sqrt(np.sum(w * (s[0] - m.birth_mean[0]) ** 2) / tot) - m.birth_std[0]) < 1.0
+
+
+@pytest.mark.parametrize("meas", [POSITION, RANGE_BEARING])
+def test_births_importance_uniform_first_step(orc, meas):
+    """k = 1, no Z_{k-1}: the proposal is uniform over the region (1/V, or 1/(V r) in the
+    Cartesian plane for a uniform (r, theta)); the estimator of gamma stays unbiased.  The
+    region covers the intensity to >= 4.3 std (mass outside < 2e-5)."""
+    if meas == POSITION:
+        m = _is_model(meas, region=(-150.0, 250.0, -180.0, 120.0))
+    else:
+        m = _is_model(meas, region=(300.0, 700.0, 0.35, 0.95))
+    J = 400000
+    s, w = orc.births(m, 1, 0, J, None)
+    se = math.sqrt(J) * w.std()
+    assert abs(w.sum() - m.birth_mass) < 5 * se and se < 0.05 * m.birth_mass
+
+
+def test_births_importance_stratified_counts(orc):
+    """Births [blo, blo+J) take component b mod M deterministically, so p_k is the mixture
+    with weights n_c / J.  With M = 2, J = 3, blo = 1 the counts are (1, 2): over many steps
+    the estimator of gamma is unbiased with those weights; the equal-weight mixture would
+    converge to gamma * int N(x; 6, 9) p(x)/p'(x) dx (computed here by quadrature), which
+    the test tells apart."""
+    m = _is_model(POSITION, birth_mean=(6.0, 0.0, 0.0, 0.0), birth_std=(3.0, 3.0, 3.0, 3.0))
+    zprev = np.array([[-6.0, 0.0], [6.0, 0.0]])
+    tot = []
+    for k in range(1, 20001):
+        s, w = orc.births(m, k, 0, 3, zprev, b0=1, nb=3, blo=1)
+        tot.append(w.sum())
+    tot = np.array(tot)
+    mean, se = tot.mean(), tot.std() / math.sqrt(len(tot))
+    assert abs(mean - m.birth_mass) < 5 * se, (mean, se)
+    x = np.linspace(-40.0, 50.0, 200001)
+    q0, q1 = np.exp(-(x + 6.0) ** 2 / 200.0), np.exp(-(x - 6.0) ** 2 / 200.0)
+    g = np.exp(-(x - 6.0) ** 2 / 18.0) / math.sqrt(18.0 * math.pi)
+    wrong = m.birth_mass * np.trapezoid(g * (q0 / 3 + 2 * q1 / 3) / (q0 / 2 + q1 / 2), x)
+    assert abs(wrong - m.birth_mass) > 8 * se, (wrong, se)
