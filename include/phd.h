@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define PHD_ABI_VERSION 1
+#define PHD_ABI_VERSION 2
 
 typedef struct phd_ctx phd_ctx;
 
@@ -103,8 +103,13 @@ typedef struct {
   int32_t reserved0;          /* must be 0 */
   int64_t exchange_count;     /* DCP ring exchange L per step (0: floor(min_j N_j / 10));
                                  clamped to floor(min_j N_j / 2) */
-  int32_t birth_model;        /* 0: births around Z_{k-1} (uniform when none), S10;
-                                 1: N(birth_mean, diag(birth_std^2)) */
+  int32_t birth_model;        /* 0: births around Z_{k-1} (uniform when none), S10,
+                                    weight gamma/J;
+                                 1: N(birth_mean, diag(birth_std^2)), gamma/J;
+                                 2: drawn as 0, weighted by the full Eq 6 ratio
+                                    gamma N(x; birth_mean, Q) / (J p_k(x|Z_{k-1})), p_k the
+                                    stratified proposal mixture; needs
+                                    birth_sigma_v > 0 and birth_std > 0 */
   int32_t reserved1;          /* must be 0 */
   double birth_mean[4];       /* x-bar (x, vx, y, vy) of birth_model 1 */
   double birth_std[4];        /* sqrt(diag Q) of birth_model 1, >= 0 */
@@ -113,6 +118,9 @@ typedef struct {
                                  pass 1 from dW = C/D and W = (1-pD) W_pred + sum dW; the
                                  accumulators of other labels read 0.  1: for every measurement. */
   int32_t reserved2;          /* must be 0 */
+  double proposal_scale;      /* s in (0, 1e3]: Eq 5 proposal q_k = the CV transition with
+                                 noise std s sigma_a, survivors weighted p_s f/q
+                                 (PAPER.md:148-152); 0 or 1: q_k = transition prior (S10) */
 } phd_params;
 
 /* One labelled estimate: label = measurement index, state =

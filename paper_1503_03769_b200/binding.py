@@ -11,7 +11,7 @@ import numpy as np
 
 from . import build as _build
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 STAGE_RESAMPLED = 0
 STAGE_PREDICTED = 1
 
@@ -36,7 +36,7 @@ class Params(ctypes.Structure):
                 ("capacity", ctypes.c_int64), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32),
                 ("reserved0", ctypes.c_int32), ("exchange_count", ctypes.c_int64), ("birth_model", ctypes.c_int32),
                 ("reserved1", ctypes.c_int32), ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4),
-                ("stphd_all", ctypes.c_int32), ("reserved2", ctypes.c_int32)]
+                ("stphd_all", ctypes.c_int32), ("reserved2", ctypes.c_int32), ("proposal_scale", ctypes.c_double)]
 
 
 class Estimate(ctypes.Structure):
@@ -157,6 +157,7 @@ def params_from(model):
         p.birth_std[i] = float(getattr(model, "birth_std", (0.0, 0.0, 0.0, 0.0))[i])
     p.stphd_all = int(getattr(model, "stphd_all", 0))
     p.reserved2 = 0
+    p.proposal_scale = float(getattr(model, "proposal_scale", 1.0))
     return p
 
 

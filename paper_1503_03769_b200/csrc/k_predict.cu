@@ -1,5 +1,6 @@
 // Prediction step (§2.2 step 1): Eq 5 survivors with the CV model
-// and Eq 6 births (measurement-driven, S10).
+// and Eq 6 births (measurement-driven, S10), plus the
+// Eq 6 importance weights of birth_model 2 (k_birth_is).
 // One thread per particle slot of this rank's block; SoA fp32 in/out, HBM-bound
 // (20 B read + 20 B written per survivor; 20 B written per birth; +32 B of
 // range-bearing representation when that sensor is used).
@@ -36,7 +37,10 @@ __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
   int64_t g = a.g0 + i;
   float x, vx, y, vy, w;
   if (g < a.n_out) {
-    // Eq 5: x~ ~ f(.|x) (q = transition prior), w~ = e_{k|k-1} w.
+    // Eq 5: x~ ~ q(.|x), the CV model with noise std s sigma_a (a.sigma_a holds
+    // s sigma_a), w~ = e_{k|k-1} f/q w.  f/q is the ratio of the noise densities at
+    // the drawn a = s sigma_a n; with n1^2 + n2^2 = -2 ln u1 (Box-Muller radius) it is
+    // s^2 u1^(s^2 - 1), and 1 for s = 1 (transition prior).
     U4 o = philox_at(a.seed, a.ctr_base + (uint64_t)g, (uint32_t)a.k, 1u);
     float u1 = u01(o.x), u2 = u01(o.y);
     float rad = sqrtf(-2.0f * logf(u1));
@@ -54,6 +58,10 @@ __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
     y = y + a.T * vy + hT2 * ay;
     vy = vy + a.T * ay;
     w = a.p_s * w;
+    if (a.prop_s != 1.0f) {
+      const float s2 = a.prop_s * a.prop_s;
+      w *= s2 * exp2f((s2 - 1.0f) * log2f(u1));
+    }
   } else {
     // Eq 6: birth b ~ p_k(.|Z_{k-1}) with weight gamma / J_k.
     int64_t b = g - a.n_out;
@@ -102,6 +110,115 @@ __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
   a.vy[i] = vy;
   a.w[i] = w;
   if (a.rb) rb_repr(x, y, a.sensor_x, a.sensor_y, a.rb, a.rb_stride, i);
+}
+
+// Eq 6 with the full ratio (birth_model 2):
+//   w_b = gamma N(x_b; x-bar, Q) / (J p_k(x_b | Z_{k-1})),
+//   p_k(x) = sum_c (n_c / J) q_c(pos) N(vx; 0, sv^2) N(vy; 0, sv^2),
+// n_c = #{b in [birth_offset, birth_offset + J) : b mod M' = c} (the births take
+// component b mod M' deterministically: a stratified mixture).  q_c is the
+// proposal's position law: N(z_c, diag(s0^2, s1^2)) for the position sensor; for
+// range-bearing the image of N(z_c, .) under (a, c) -> (a cos c, a sin c), whose
+// density at (x, y) sums the preimages (r, th) and (-r, th + pi), each divided by
+// the Jacobian r.  No previous set: uniform, 1/V or 1/(V r).
+// One thread per birth; components staged through shared memory with their
+// mixture weights.  Residuals and exponents in fp64, the exponential by
+// ex2.approx of the fp32-rounded exponent (relative error <= |E| 2^-24 + 2 ulp),
+// the mixture sum in fp64.  J M' terms per step: cold (births only).
+constexpr int kISChunk = 1024;
+
+__device__ __forceinline__ double wrap_pi_d(double d) {
+  const double pi = 3.141592653589793238462643383279503, two_pi = 6.283185307179586476925286766559;
+  d = fmod(d, two_pi);
+  if (d > pi) d -= two_pi;
+  if (d <= -pi) d += two_pi;
+  return d;
+}
+
+__device__ __forceinline__ int64_t count_below(int64_t e, int64_t c, int64_t M) {
+  return e > c ? (e - c - 1) / M + 1 : 0;
+}
+
+__device__ __forceinline__ double ex2d(double e) {  // 2^e via MUFU on the fp32-rounded exponent
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"((float)e));
+  return (double)y;
+}
+
+__global__ void __launch_bounds__(256) k_birth_is(const BirthISArgs a) {
+  __shared__ double zc0[kISChunk], zc1[kISChunk], wc[kISChunk];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = t < a.nb;
+  const double log2e = 1.4426950408889634073599246810019;
+  const double pi = 3.141592653589793238462643383279503;
+  double x = 0, vx = 0, y = 0, vy = 0, r = 0, th = 0;
+  if (live) {
+    const int64_t i = a.i0 + t;
+    x = a.x[i];
+    vx = a.vx[i];
+    y = a.y[i];
+    vy = a.vy[i];
+    if (a.meas != 0) {
+      const double px = x - a.sensor_x, py = y - a.sensor_y;
+      r = sqrt(px * px + py * py);
+      th = (px == 0.0 && py == 0.0) ? 0.0 : atan2(py, px);
+    }
+  }
+  // -log2 e / (2 s^2) per axis
+  const double k0 = -log2e / (2.0 * a.sigma_z0 * a.sigma_z0), k1 = -log2e / (2.0 * a.sigma_z1 * a.sigma_z1);
+  double pos = 0.0;
+  if (a.m_prev > 0) {
+    for (int c0 = 0; c0 < a.m_prev; c0 += kISChunk) {
+      const int nc = min(kISChunk, a.m_prev - c0);
+      __syncthreads();
+      for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+        const int64_t c = c0 + q;
+        zc0[q] = a.zprev[2 * c];
+        zc1[q] = a.zprev[2 * c + 1];
+        const int64_t n_c = count_below(a.birth_offset + a.J, c, a.m_prev) - count_below(a.birth_offset, c, a.m_prev);
+        wc[q] = (double)n_c / (double)a.J;
+      }
+      __syncthreads();
+      if (live) {
+        if (a.meas == 0) {
+          for (int q = 0; q < nc; ++q) {
+            const double d0 = x - zc0[q], d1 = y - zc1[q];
+            pos += wc[q] * ex2d(k0 * d0 * d0 + k1 * d1 * d1);
+          }
+        } else {
+          for (int q = 0; q < nc; ++q) {
+            const double da = r - zc0[q], db = -r - zc0[q];
+            const double ta = wrap_pi_d(th - zc1[q]), tb = wrap_pi_d(th + pi - zc1[q]);
+            pos += wc[q] * (ex2d(k0 * da * da + k1 * ta * ta) + ex2d(k0 * db * db + k1 * tb * tb));
+          }
+        }
+      }
+    }
+    pos *= 1.0 / (2.0 * pi * a.sigma_z0 * a.sigma_z1);
+    if (a.meas != 0) pos = r > 0.0 ? pos / r : 0.0;
+  } else {
+    const double V = (a.region[1] - a.region[0]) * (a.region[3] - a.region[2]);
+    pos = a.meas == 0 ? 1.0 / V : (r > 0.0 ? 1.0 / (V * r) : 0.0);
+  }
+  if (!live) return;
+  const double sv = a.birth_sigma_v;
+  // log of the velocity factor of p_k and of gamma(x) / gamma; 2 pi factors explicit
+  const double lpv = -(vx * vx + vy * vy) / (2.0 * sv * sv) - log(2.0 * pi * sv * sv);
+  const double st[4] = {x, vx, y, vy};
+  double lg = -2.0 * log(2.0 * pi);
+  for (int d = 0; d < 4; ++d) {
+    const double u = (st[d] - a.birth_mean[d]) / a.birth_std[d];
+    lg += -0.5 * u * u - log(a.birth_std[d]);
+  }
+  double w = 0.0;
+  if (pos > 0.0) w = a.gamma / (double)a.J * exp(lg - lpv - log(pos));
+  a.w[a.i0 + t] = (float)w;
+}
+
+cudaError_t launch_birth_is(const BirthISArgs& a, cudaStream_t s) {
+  if (a.nb <= 0) return cudaSuccess;
+  k_birth_is<<<(unsigned)((a.nb + 255) / 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(256) k_rb_repr(const float* __restrict__ x, const float* __restrict__ y,

@@ -244,7 +244,15 @@ phd_status validate(const phd_params* p, int world, phd_ctx* c) {
   if (p->mode != PHD_MODE_EXACT && p->mode != PHD_MODE_DCP) return fail(c, PHD_EINVAL, "mode %d", p->mode);
   if (p->reserved0 != 0) return fail(c, PHD_EINVAL, "reserved0 must be 0");
   if (p->exchange_count < 0) return fail(c, PHD_EINVAL, "exchange_count < 0");
-  if (p->birth_model != 0 && p->birth_model != 1) return fail(c, PHD_EINVAL, "birth_model %d", p->birth_model);
+  if (p->birth_model < 0 || p->birth_model > 2) return fail(c, PHD_EINVAL, "birth_model %d", p->birth_model);
+  if (p->birth_model == 2) {
+    if (!(p->birth_sigma_v > 0)) return fail(c, PHD_EINVAL, "birth_model 2 needs birth_sigma_v > 0");
+    for (int i = 0; i < 4; ++i)
+      if (!(p->birth_std[i] > 0)) return fail(c, PHD_EINVAL, "birth_model 2 needs birth_std > 0");
+    if (p->meas == PHD_MEAS_RANGE_BEARING && p->region[0] < 0)
+      return fail(c, PHD_EINVAL, "birth_model 2 needs a range region with rmin >= 0");
+  }
+  if (!(p->proposal_scale >= 0 && p->proposal_scale <= 1e3)) return fail(c, PHD_EINVAL, "proposal_scale outside [0, 1e3]");
   if (p->reserved1 != 0 || p->reserved2 != 0) return fail(c, PHD_EINVAL, "reserved fields must be 0");
   if (p->stphd_all != 0 && p->stphd_all != 1) return fail(c, PHD_EINVAL, "stphd_all must be 0 or 1");
   for (int i = 0; i < 4; ++i)
@@ -649,7 +657,9 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
   a.k = k;
   a.seed = c->p.seed;
   a.T = (float)c->p.T;
-  a.sigma_a = (float)c->p.sigma_a;
+  const double prop_s = c->p.proposal_scale > 0 ? c->p.proposal_scale : 1.0;
+  a.sigma_a = (float)(prop_s * c->p.sigma_a);  // the proposal's noise std (Eq 5)
+  a.prop_s = (float)prop_s;
   a.p_s = (float)c->p.p_s;
   a.w_uniform = -1.0f;
   a.meas = c->p.meas;
@@ -676,6 +686,34 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
   a.rb = c->rb;
   a.rb_stride = c->L.cap_l;
   KL(launch_predict(a, c->st));
+  if (c->p.birth_model == 2) {
+    // Eq 6 importance weights of this rank's births (slots with global index >= n_out)
+    BirthISArgs b{};
+    b.i0 = std::max<int64_t>(0, a.n_out - a.g0);
+    b.nb = std::max<int64_t>(0, a.n_local - b.i0);
+    b.J = a.J;
+    b.birth_offset = a.birth_offset;
+    b.meas = c->p.meas;
+    b.sigma_z0 = c->p.sigma_z[0];
+    b.sigma_z1 = c->p.sigma_z[1];
+    b.sensor_x = c->p.sensor_xy[0];
+    b.sensor_y = c->p.sensor_xy[1];
+    for (int i = 0; i < 4; ++i) {
+      b.region[i] = c->p.region[i];
+      b.birth_mean[i] = c->p.birth_mean[i];
+      b.birth_std[i] = c->p.birth_std[i];
+    }
+    b.gamma = c->p.birth_mass;
+    b.birth_sigma_v = c->p.birth_sigma_v;
+    b.zprev = zp;
+    b.m_prev = mp;
+    b.x = a.x;
+    b.vx = a.vx;
+    b.y = a.y;
+    b.vy = a.vy;
+    b.w = a.w;
+    if (b.nb > 0) KL(launch_birth_is(b, c->st));
+  }
   timing_record(c, 1);
   c->stage = kPredicted;
   return PHD_OK;

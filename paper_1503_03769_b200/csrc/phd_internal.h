@@ -63,12 +63,13 @@ struct PredictArgs {
   uint64_t ctr_base;         // Philox counter of local slot i is ctr_base + g0 + i (DCP groups: own space)
   int64_t birth_offset;      // global index of this rank's first birth (measurement choice b mod M)
   float T, sigma_a, p_s;
+  float prop_s;              // Eq 5 proposal noise scale s (1: transition prior)
   float w_uniform;           // >= 0: survivors' weight before predict; < 0: read w
   int meas;
   float sigma_z0, sigma_z1, sensor_x, sensor_y;
   float region[4];
   float birth_w, birth_sigma_v;
-  int birth_model;           // 0 around Z_{k-1}; 1 N(birth_mean, diag(birth_std^2))
+  int birth_model;           // 0 around Z_{k-1}; 1 N(birth_mean, diag(birth_std^2)); 2 as 0 + Eq 6 ratio
   float birth_mean[4], birth_std[4];
   const float* zprev;        // device [m_prev][2]
   int32_t m_prev;
@@ -89,8 +90,25 @@ struct ResampleArgs {
   int32_t* marks;            // [hi - lo]
 };
 
+// Eq 6 importance weights of the births (birth_model 2): local slots [i0, i0 + nb)
+// hold births of this filter, whose births are [birth_offset, birth_offset + J).
+struct BirthISArgs {
+  int64_t i0, nb;            // first local birth slot, local birth count
+  int64_t J, birth_offset;
+  int meas;
+  double sigma_z0, sigma_z1, sensor_x, sensor_y;
+  double region[4];
+  double gamma, birth_sigma_v;
+  double birth_mean[4], birth_std[4];
+  const float* zprev;
+  int32_t m_prev;
+  const float *x, *vx, *y, *vy;
+  float* w;
+};
+
 // ---- launchers (return cudaGetLastError of the launch) -----------------------
 cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s);
+cudaError_t launch_birth_is(const BirthISArgs& a, cudaStream_t s);
 cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, float sy, float* rb,
                            int64_t stride, cudaStream_t s);
 cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad,

@@ -27,8 +27,31 @@ def test_library_loads_and_exports_header_symbols():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(binding.EXPORTS)
-    assert L.phd_abi_version() == 1
+    assert L.phd_abi_version() == binding.ABI_VERSION == 2
     assert L.phd_status_str(2) == b"call out of order"
+
+
+def test_params_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of phd_params / phd_summary / phd_estimate has the C layout
+    (sizeof and every field offset, compiled from include/phd.h with gcc)."""
+    import subprocess
+    structs = {"phd_params": binding.Params, "phd_summary": binding.Summary, "phd_estimate": binding.Estimate}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "phd.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append('printf("%s sizeof %%zu\\n", sizeof(%s));' % (cname, cname))
+        for fname, _ in py._fields_:
+            lines.append('printf("%s %s %%zu\\n", offsetof(%s, %s));' % (cname, fname, cname, fname))
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    out = subprocess.run([str(exe)], stdout=subprocess.PIPE, check=True).stdout.decode().split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in structs.items():
+        assert got[(cname, "sizeof")] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
 
 
 def test_host_philox_matches_oracle(orc):

@@ -55,11 +55,18 @@ def _run_parallel(fns):
     assert not errs, errs
 
 
-@pytest.mark.parametrize("K,cname", [(1, "cfg1"), (2, "cfg1"), (3, "cfg1"), (4, "cfg3"), (2, "cfg2")])
+@pytest.mark.parametrize("K,cname", [(1, "cfg1"), (2, "cfg1"), (3, "cfg1"), (4, "cfg3"), (2, "cfg2"),
+                                     (3, "cfg1+is"), (2, "cfg2+is")])
 def test_dcp_stagewise(phd, orc, K, cname):
     from oracle import dcp
+    importance = cname.endswith("+is")
+    cname = cname.replace("+is", "")
     cfg = scenario.get(cname)
     m = replace(cfg.model, mode=MODE_DCP)
+    if importance:  # NEXT-4: Eq 5 proposal s sigma_a and Eq 6 full ratio, per group's own births
+        m = replace(m, proposal_scale=1.3, birth_model=2, birth_sigma_v=10.0,
+                    birth_mean=(0.0, 0.0, 0.0, 0.0), birth_std=(600.0, 8.0, 600.0, 8.0))
+        cfg = replace(cfg, model=m)
     if cname == "cfg3":
         m = replace(m, fixed_count=24000, births_per_step=2000, capacity=40000, max_meas=1024)
         cfg = replace(cfg, model=m, scenario=replace(cfg.scenario, n_targets=30, steps=3))
@@ -112,6 +119,11 @@ def test_dcp_stagewise(phd, orc, K, cname):
             rscale = 0.0 if m.meas == POSITION else 2000.0
             db = np.abs(r["pred"][:, nsv:] - o["pred"][:, nsv:])
             assert np.all(db <= 1e-6 * (np.abs(o["pred"][:, nsv:]) + rscale) + 1e-5)
+            # predicted weights: survivors p_s f/q w (rel 1e-5), births Eq 6 (rel 2e-4, see
+            # test_gpu_parity.test_importance_predict_and_births)
+            wpo = o["w_pred"]
+            assert np.all(np.abs(r["w_pred"][:nsv] - wpo[:nsv]) <= 1e-5 * wpo[:nsv])
+            assert np.all(np.abs(r["w_pred"][nsv:] - wpo[nsv:]) <= 2e-4 * wpo[nsv:] + 1e-7 * wpo.max())
             # Step 2 on the GPU's predicted group (stage-wise): local C_j and weights
             Co = orc.normalizers(m, r["pred"], r["w_pred"], z)
             wo, acco = orc.update(m, r["pred"], r["w_pred"], z, Co)

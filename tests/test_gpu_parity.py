@@ -423,6 +423,50 @@ def test_births_gaussian_model(phd, orc):
 
 
 @pytest.mark.parametrize("mname", ["position", "range_bearing"])
+@pytest.mark.parametrize("k", [1, 3])
+def test_importance_predict_and_births(phd, orc, mname, k):
+    """NEXT-4: Eq 5 with the proposal q_k = CV model of noise std s sigma_a (weights
+    p_s f/q) and Eq 6 with the full ratio gamma N(x; x-bar, Q) / (J p_k(x|Z_{k-1})) over
+    the stratified measurement-driven mixture (k = 1: uniform proposal).  Survivor weights:
+    the kernel's s^2 u1^(s^2-1) in fp32 (<= 23 (s^2-1) 2^-23 ln2 + log2f/exp2f ulps < 1e-5).
+    Birth weights: the fp32 birth states differ from the oracle's fp64 ones by the births
+    tolerance; through d log w / dx (<= |x - z| / sigma_z^2 + |x - x-bar| / std^2 of a few
+    1/m) that moves w by <= 2e-4 relative; the typical error is far smaller."""
+    base = MODELS[mname]
+    if base.meas == POSITION:
+        bm, bsd = (100.0, 2.0, -50.0, -1.0), (400.0, 6.0, 300.0, 6.0)
+    else:
+        bm, bsd = (300.0, 2.0, 400.0, -1.0), (300.0, 6.0, 300.0, 6.0)
+    m = replace(base, proposal_scale=1.7, birth_model=2, birth_sigma_v=8.0, birth_mean=bm, birth_std=bsd,
+                births_per_step=3001, birth_mass=0.2)
+    n_out, J = 4000 + 13, m.births_per_step
+    soa, w = scenario.random_particles(n_out, 4)
+    zprev = _meas(m, 29, 6) if k > 1 else None
+    f = phd.Filter(m)
+    f.set_particles(soa, w, n_out)
+    f.predict(k, zprev)
+    gs, gw, _ = f.get_particles()
+    os_, ow = orc.predict(m, k, soa, w)
+    T, sa = m.T, m.sigma_a * m.proposal_scale
+    tol = 5e-7 * np.abs(os_) + 2e-6 * (0.5 * T * T * sa + T * sa) * 6 + 1e-6
+    assert np.all(np.abs(gs[:, :n_out] - os_) <= tol)
+    assert np.allclose(gw[:n_out], ow, rtol=1e-5, atol=0)
+    assert not np.allclose(ow, m.p_s * w)  # the ratio is really applied
+    bs, bw = orc.births(m, k, n_out, J, None if zprev is None else zprev.astype(np.float64))
+    rscale = 0.0 if (m.meas == POSITION or zprev is None) else float(np.max(zprev[:, 0]))
+    if m.meas != POSITION and zprev is None:
+        rscale = m.region[1]
+    assert np.all(np.abs(gs[:, n_out:] - bs) <= 1e-6 * (np.abs(bs) + rscale) + 1e-5)
+    rel = np.abs(gw[n_out:] - bw) / np.maximum(bw, 1e-300)
+    big = bw > 1e-12 * bw.max()
+    assert np.all(rel[big] <= 2e-4), rel[big].max()
+    assert np.median(rel[big]) < 1e-5
+    assert np.all(np.abs(gw[n_out:] - bw) <= 2e-4 * bw + 1e-7 * bw.max())
+    assert bw.std() > 0.1 * bw.mean()  # weights really vary (not gamma / J)
+    f.close()
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
 def test_index_set_state_sums(phd, orc, mname):
     """stphd_all = 0 (default): the index set I is chosen right after pass 1 from dW = C/D and
     W = (1-pD) W_pred + sum dW; pass 2 accumulates S only for I.  The estimates equal those of
