@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--mode", default="exact", choices=["exact", "dcp"],
                     help="exact: global C + exact resampling (north_star hot path); dcp: the paper's DCPFPHD groups")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gate", type=int, default=0, choices=[0, 1, 2],
+                    help="update algorithm of the main line: 0 dense (the pairs/s roofline line), 1/2 gated")
+    ap.add_argument("--no-gated-leg", action="store_true",
+                    help="skip the extra gated-update measurement reported under \"gated\"")
     ap.add_argument("--cpu-sample", type=int, default=65536, help="particles in the oracle's bounded sample")
     return ap.parse_args()
 
@@ -211,7 +215,7 @@ def run_ours(args):
     steps = args.warmup + args.steps
     cfg = scenario_for(args.config, 2 * steps + 1)
     from dataclasses import replace as _replace
-    cfg = _replace(cfg, model=_replace(cfg.model, mode=1 if args.mode == "dcp" else 0))
+    cfg = _replace(cfg, model=_replace(cfg.model, mode=1 if args.mode == "dcp" else 0, gate=args.gate))
     m = cfg.model
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
@@ -327,6 +331,40 @@ def run_ours(args):
     run_steps(1, args.warmup, Zh, False)
     pairs_e, ms_e = timed_steps(Zh, args.warmup + 1)
 
+    # ---- gated update (NEXT-2): same workload, same steps, gate = 1 ----
+    gated = None
+    if not args.no_gated_leg and args.gate == 0:
+        f.close()
+        del workspace
+        mg = _replace(m, gate=1)
+        workspace = torch.empty(phd.workspace_size(mg, world), dtype=torch.uint8, device=dev)
+        f = phd.Filter(mg, rank=rank, world=world, nccl_id=nid, device=local, stream=stream.cuda_stream,
+                       workspace=workspace)
+        reset()
+        run_steps(1, args.warmup, Zd, False)
+        f.set_timing(True)
+        g_ms = {"pass1": [], "pass2": [], "update": []}
+        g_st = []
+
+        def collect_g():
+            t = f.timing()
+            for key in g_ms:
+                g_ms[key].append(t[key])
+            g_st.append(f.gate_stats())
+
+        pairs_g, ms_g = timed_steps(Zd, args.warmup + 1, collect_g)
+        f.set_timing(False)
+        ev = sum(s_["pairs"] for s_ in g_st)
+        gated = {"ms_per_step": ms_g / args.steps,
+                 "effective_pairs_per_s": pairs_g / (ms_g * 1e-3),
+                 "evaluated_pairs_per_step": ev / max(1, len(g_st)),
+                 "evaluated_fraction": ev / max(1, pairs_g // max(1, world)),
+                 "steps_gated": sum(s_["used"] for s_ in g_st),
+                 "kernel_ms": {k_: statistics.mean(v_) for k_, v_ in g_ms.items()},
+                 "note": "gate = 1: only (tile, measurement) pairs whose largest exponent is >= -130 are "
+                         "evaluated (every skipped term is exactly 0 in fp32 ftz); effective = N*M / step time, "
+                         "not a pairs/s roofline claim"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -392,6 +430,7 @@ def run_ours(args):
         "e2e": {"value": value_e, "unit": "pairs/s", "h2d_bytes_per_step": M * 8,
                 "d2h_bytes_per_step": int(f._sum.n_est) * 24 + 8 * (2 * world + 10)},
         "gpu_launches": int(launches),
+        "gated": gated,
         "clocks": clk,
     }
     print(json.dumps(out), flush=True)

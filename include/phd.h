@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define PHD_ABI_VERSION 2
+#define PHD_ABI_VERSION 3
 
 typedef struct phd_ctx phd_ctx;
 
@@ -117,7 +117,17 @@ typedef struct {
                                  top-LT index set I, selected right after
                                  pass 1 from dW = C/D and W = (1-pD) W_pred + sum dW; the
                                  accumulators of other labels read 0.  1: for every measurement. */
-  int32_t reserved2;          /* must be 0 */
+  int32_t gate;               /* update algorithm (DESIGN.md §5 "Gated update"):
+                                 0: dense -- both passes evaluate all N x M pairs;
+                                 1: gated, automatic -- particles ordered by measurement-space
+                                    cell (a sorted copy; the filter's particle order and hence
+                                    resampling are unchanged), tiles of 512 paired only with the
+                                    measurements whose largest possible exponent over the tile is
+                                    >= -130, i.e. every skipped term underflows to exactly 0 in
+                                    the dense kernels (same non-zero terms, fp64 sums in another
+                                    fixed order).  Falls back to dense for an update whose
+                                    candidate pairs exceed half of N x M or the workspace;
+                                 2: gated whenever the candidate lists fit the workspace. */
   double proposal_scale;      /* s in (0, 1e3]: Eq 5 proposal q_k = the CV transition with
                                  noise std s sigma_a, survivors weighted p_s f/q
                                  (PAPER.md:148-152); 0 or 1: q_k = transition prior (S10) */
@@ -232,6 +242,11 @@ phd_status phd_get_local_estimates(phd_ctx* ctx, phd_estimate* out, int32_t cap,
 phd_status phd_get_ancestors(phd_ctx* ctx, int32_t* anc, int64_t cap, int64_t* n, int64_t* first);
 /* W, U, N_out and the per-rank masses W_r[world] of the last resample. */
 phd_status phd_get_resample_meta(phd_ctx* ctx, double* W, double* U, int64_t* N_out, double* W_r);
+/* Gated update statistics of the last phd_update (gate != 0): out[0] = 1 if the
+ * gated path ran (0: dense), out[1] = candidate entries (tile, measurement),
+ * out[2] = (particle, measurement) pairs evaluated (entries x 512 incl. tile padding),
+ * out[3] = tiles. */
+phd_status phd_get_gate_stats(phd_ctx* ctx, int64_t* out /* [4] */);
 /* Kernel launches issued by this ctx since creation (all streams). */
 int64_t phd_launch_count(const phd_ctx* ctx);
 /* Device time (ms) of the last update's pass-1 and pass-2 kernels, measured

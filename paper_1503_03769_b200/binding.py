@@ -11,7 +11,7 @@ import numpy as np
 
 from . import build as _build
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 STAGE_RESAMPLED = 0
 STAGE_PREDICTED = 1
 
@@ -36,7 +36,7 @@ class Params(ctypes.Structure):
                 ("capacity", ctypes.c_int64), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32),
                 ("reserved0", ctypes.c_int32), ("exchange_count", ctypes.c_int64), ("birth_model", ctypes.c_int32),
                 ("reserved1", ctypes.c_int32), ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4),
-                ("stphd_all", ctypes.c_int32), ("reserved2", ctypes.c_int32), ("proposal_scale", ctypes.c_double)]
+                ("stphd_all", ctypes.c_int32), ("gate", ctypes.c_int32), ("proposal_scale", ctypes.c_double)]
 
 
 class Estimate(ctypes.Structure):
@@ -58,7 +58,8 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_extract", "phd_resample_exchange", "phd_step", "phd_get_normalizers", "phd_get_accumulators",
            "phd_get_ancestors", "phd_get_resample_meta", "phd_launch_count", "phd_set_timing", "phd_get_timing",
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
-           "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates"]
+           "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates",
+           "phd_get_gate_stats"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -113,6 +114,7 @@ def load(build_if_missing=True):
     L.phd_get_ancestors.argtypes = [_P, _I32, ctypes.c_int64, _I64, _I64]
     L.phd_get_local_estimates.argtypes = [_P, ctypes.POINTER(Estimate), ctypes.c_int32, _I32]
     L.phd_get_resample_meta.argtypes = [_P, _D, _D, _I64, _D]
+    L.phd_get_gate_stats.argtypes = [_P, _I64]
     L.phd_launch_count.argtypes = [_P]
     L.phd_launch_count.restype = ctypes.c_int64
     L.phd_set_timing.argtypes = [_P, ctypes.c_int32]
@@ -156,7 +158,7 @@ def params_from(model):
         p.birth_mean[i] = float(getattr(model, "birth_mean", (0.0, 0.0, 0.0, 0.0))[i])
         p.birth_std[i] = float(getattr(model, "birth_std", (0.0, 0.0, 0.0, 0.0))[i])
     p.stphd_all = int(getattr(model, "stphd_all", 0))
-    p.reserved2 = 0
+    p.gate = int(getattr(model, "gate", 0))
     p.proposal_scale = float(getattr(model, "proposal_scale", 1.0))
     return p
 
@@ -388,6 +390,12 @@ class Filter:
         self._check(self.L.phd_get_resample_meta(self.h, ctypes.byref(W), ctypes.byref(U), ctypes.byref(n),
                                                  Wr.ctypes.data_as(_D)), "phd_get_resample_meta")
         return {"W": W.value, "U": U.value, "N_out": n.value, "W_r": Wr}
+
+    def gate_stats(self):
+        """(used, entries, pairs evaluated, tiles) of the last update's gated path."""
+        out = np.zeros(4, dtype=np.int64)
+        self._check(self.L.phd_get_gate_stats(self.h, out.ctypes.data_as(_I64)), "phd_get_gate_stats")
+        return {"used": int(out[0]), "entries": int(out[1]), "pairs": int(out[2]), "tiles": int(out[3])}
 
     def launch_count(self):
         return self.L.phd_launch_count(self.h)

@@ -15,6 +15,7 @@
 // transposed butterfly and across warps through shared memory, giving one
 // fp32 partial per (particle, z-block).  Cross-CTA sums are fp64 in fixed order.
 #include "phd_internal.h"
+#include "pair_math.cuh"
 
 #include <type_traits>
 
@@ -36,14 +37,6 @@ namespace phd {
 constexpr int kPPUnroll1 = PHD_PP_UNROLL1;
 constexpr int kPPUnroll2 = PHD_PP_UNROLL2;
 constexpr int kEmuPeriod = PHD_EMU_PERIOD;
-
-__device__ __forceinline__ float ex2a(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float2 ex2v(float2 a) { return make_float2(ex2a(a.x), ex2a(a.y)); }
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
 // 2^x for a pair on the FMA pipe (MUFU offload):
 // x = j + r with j = rint(x) by the 1.5*2^23 shifter, |r| <= 1/2, 2^r by a
@@ -169,21 +162,6 @@ struct LaneZ {
   }
 };
 
-// Pass-1 exponent: a = -(alpha0 d0^2 + alpha1 d1^2) (log2 units).
-// Pass-2 exponent: the same plus lw = log2(p_D c w_i) folded into the last FFMA,
-// so that 2^a is directly u = p_D g w (one FMUL per pair saved).
-template <int MODEL>
-__device__ __forceinline__ float2 expo(float2 d0, float2 d1, float2 na0, float2 na1, float2 base) {
-  if (MODEL == kPosIso) {
-    float2 q = __fmul2_rn(d0, d0);
-    q = __ffma2_rn(d1, d1, q);
-    return __ffma2_rn(q, na0, base);
-  } else {
-    float2 q = __ffma2_rn(__fmul2_rn(d0, d0), na0, base);
-    return __ffma2_rn(__fmul2_rn(d1, d1), na1, q);
-  }
-}
-
 // Residuals (d0, d1) of the lane's slot pair j against the broadcast particle.
 template <int MODEL, int PASS, int NP>
 __device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS, NP>& z, int j, float2& d0,
@@ -198,32 +176,6 @@ __device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PA
     d0 = __fadd2_rn(f2(P.x, P.y), z.n0[j]);  // x - z_x
     d1 = __fadd2_rn(f2(P.z, P.w), z.n1[j]);  // y - z_y
   }
-}
-
-// Sum of v[0..7] over the 32 lanes of a warp; lane l ends with the total of
-// particle l >> 2 (transposed butterfly: 9 SHFL + 9 FADD for 8 values).
-__device__ __forceinline__ float transpose_reduce8(float (&v)[8], int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float keep = b4 ? v[i + 4] : v[i];
-    float send = b4 ? v[i] : v[i + 4];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    float keep = b3 ? v[i + 2] : v[i];
-    float send = b3 ? v[i] : v[i + 2];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  {
-    float keep = b2 ? v[1] : v[0];
-    float send = b2 ? v[0] : v[1];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  return v[0];
 }
 
 // ZL = measurement slots per lane (4 or 8); the CTA covers wz * 32 * ZL slots.
@@ -712,7 +664,8 @@ cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s
 // of w' and of the predicted w (blocks of kBlockW particles, fixed tree order).
 __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, const float* __restrict__ P,
                                                   int64_t P_stride, int zb, int64_t n, float nu, float wscale,
-                                                  float* w_out, double* blk_w, double* blk_wp) {
+                                                  float* w_out, double* blk_w, double* blk_wp,
+                                                  const int32_t* __restrict__ inv) {
   __shared__ double sw[8], swp[8];
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * kBlockW;
@@ -723,7 +676,11 @@ __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, c
     if (i < n) {
       float wi = w[i];
       float s = 0.0f;
-      for (int k = 0; k < zb; ++k) s += P[(int64_t)k * P_stride + i];
+      if (inv) {
+        if (zb > 0) s = P[inv[i]];  // gated update: one plane in sorted order
+      } else {
+        for (int k = 0; k < zb; ++k) s += P[(int64_t)k * P_stride + i];
+      }
       float wn = wi * nu + s;  // P carries p_D c w (pass 2 folds log2 w into the exponent)
       w_out[i] = wn;
       a += (double)wn;
@@ -752,10 +709,11 @@ __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, c
 }
 
 cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, int zb, int64_t n, float nu,
-                             float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s) {
+                             float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s,
+                             const int32_t* inv) {
   if (n <= 0) return cudaSuccess;
   unsigned nb = (unsigned)((n + kBlockW - 1) / kBlockW);
-  k_finalize<<<nb, 256, 0, s>>>(w, P, P_stride, zb, n, nu, wscale, w_out, blk_w, blk_wp);
+  k_finalize<<<nb, 256, 0, s>>>(w, P, P_stride, zb, n, nu, wscale, w_out, blk_w, blk_wp, inv);
   return cudaGetLastError();
 }
 

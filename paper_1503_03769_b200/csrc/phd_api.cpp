@@ -41,6 +41,11 @@ struct Layout {
   // byte offsets
   size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_sel, o_selinfo, o_D,
       o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_gather, o_ring, o_summ, o_bad;
+  // gated update (p->gate != 0)
+  int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
+  int g_ntiles = 0, g_nsorted = 0;
+  size_t o_gkeys, o_gperm, o_ginv, o_gsorted[13], o_gPs, o_ghist, o_gscan, o_gtstart, o_gcand, o_gk, o_gv, o_gmlist,
+      o_gpart1, o_gpart2, o_gmstart, o_gzkey, o_gzstart, o_gzitems, o_gA;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -92,6 +97,35 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_gather = take(p->mode == PHD_MODE_DCP ? sizeof(phd_estimate) * (size_t)(p->max_meas + 1) * world : 256);
   L.o_summ = take(sizeof(double) * 16);
   L.o_bad = take(sizeof(int) * 4);
+  // gated update buffers (DESIGN.md §5 "Gated update"); 256-byte stubs when gate == 0
+  const bool gt = p->gate != 0;
+  L.g_npad = align_up((size_t)L.cap_l, kGateTP);
+  L.g_ntiles = (int)(L.g_npad / kGateTP);
+  L.g_ecap = std::max<int64_t>((int64_t)1 << 20, (int64_t)L.g_ntiles * std::min(p->max_meas, 256));
+  L.g_hist = std::max<int64_t>((int64_t)kGateBins * ceil_div(L.cap_l, kSortBlock),
+                               (int64_t)kSortMaxBins * ceil_div(L.g_ecap, kSortBlock)) + 1;
+  L.g_scan = ceil_div(std::max<int64_t>(L.g_hist, L.g_ntiles + (int64_t)p->max_meas + 2), 4096) + 2;
+  L.g_nsorted = p->meas == PHD_MEAS_RANGE_BEARING ? 13 : 5;
+  auto gtake = [&](size_t bytes) { return take(gt ? bytes : 256); };
+  L.o_gkeys = gtake(sizeof(int32_t) * L.cap_l);
+  L.o_gperm = gtake(sizeof(int32_t) * L.cap_l);
+  L.o_ginv = gtake(sizeof(int32_t) * L.cap_l);
+  for (int i = 0; i < 13; ++i) L.o_gsorted[i] = gtake(i < L.g_nsorted ? sizeof(float) * L.g_npad : 0);
+  L.o_gPs = gtake(sizeof(float) * L.g_npad);
+  L.o_ghist = gtake(sizeof(int32_t) * L.g_hist);
+  L.o_gscan = gtake(sizeof(int32_t) * L.g_scan);
+  L.o_gtstart = gtake(sizeof(int32_t) * (L.g_ntiles + 1));
+  L.o_gcand = gtake(sizeof(int32_t) * L.g_ecap);
+  L.o_gk = gtake(p->max_meas > kSortMaxBins ? sizeof(int32_t) * L.g_ecap : 0);
+  L.o_gv = gtake(p->max_meas > kSortMaxBins ? sizeof(int32_t) * L.g_ecap : 0);
+  L.o_gmlist = gtake(sizeof(int32_t) * L.g_ecap);
+  L.o_gpart1 = gtake(sizeof(double) * L.g_ecap);
+  L.o_gpart2 = gtake(sizeof(float) * 4 * L.g_ecap);
+  L.o_gmstart = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 2));
+  L.o_gzkey = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 1));
+  L.o_gzstart = gtake(sizeof(int32_t) * (kGateBins + 1));
+  L.o_gzitems = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 1));
+  L.o_gA = gtake(sizeof(double) * 4 * (size_t)L.slots_max);
   L.total = off;
   return L;
 }
@@ -165,6 +199,16 @@ struct phd_ctx {
   int64_t N_out_last = 0, prod_first = 0, prod_n = 0;
   int count_clamped = 0, zero_mass = 0;
   int64_t ring_L = 0;
+  // gated update
+  GateSorted gso{};
+  GateGrid ggrid{};
+  int32_t *gkeys = nullptr, *ghist = nullptr, *gscan = nullptr, *gtstart = nullptr, *gcand = nullptr, *gk = nullptr,
+          *gv = nullptr, *gmlist = nullptr, *gmstart = nullptr, *gzkey = nullptr, *gzstart = nullptr,
+          *gzitems = nullptr;
+  float *gPs = nullptr, *gpart2 = nullptr;
+  double *gpart1 = nullptr, *gA = nullptr;
+  bool gated = false;            // the last update ran the gated path
+  int64_t g_entries = 0, g_tiles = 0;
   // timing
   bool timing = false;
   cudaEvent_t ev[16] = {};
@@ -253,7 +297,8 @@ phd_status validate(const phd_params* p, int world, phd_ctx* c) {
       return fail(c, PHD_EINVAL, "birth_model 2 needs a range region with rmin >= 0");
   }
   if (!(p->proposal_scale >= 0 && p->proposal_scale <= 1e3)) return fail(c, PHD_EINVAL, "proposal_scale outside [0, 1e3]");
-  if (p->reserved1 != 0 || p->reserved2 != 0) return fail(c, PHD_EINVAL, "reserved fields must be 0");
+  if (p->reserved1 != 0) return fail(c, PHD_EINVAL, "reserved fields must be 0");
+  if (p->gate < 0 || p->gate > 2) return fail(c, PHD_EINVAL, "gate must be 0, 1 or 2");
   if (p->stphd_all != 0 && p->stphd_all != 1) return fail(c, PHD_EINVAL, "stphd_all must be 0 or 1");
   for (int i = 0; i < 4; ++i)
     if (!(p->birth_std[i] >= 0)) return fail(c, PHD_EINVAL, "birth_std must be >= 0");
@@ -464,6 +509,48 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->dcp = p->mode == PHD_MODE_DCP;
   c->summ = at<double>(c->ws, L.o_summ);
   c->bad = at<int>(c->ws, L.o_bad);
+  if (p->gate != 0) {
+    c->gkeys = at<int32_t>(c->ws, L.o_gkeys);
+    c->gso.perm = at<int32_t>(c->ws, L.o_gperm);
+    c->gso.inv = at<int32_t>(c->ws, L.o_ginv);
+    float* so[13];
+    for (int i = 0; i < 13; ++i) so[i] = at<float>(c->ws, L.o_gsorted[i]);
+    const int nc = L.g_nsorted - 5;  // range-bearing: 8 representation rows first
+    for (int i = 0; i < 8; ++i) c->gso.c[i] = i < nc ? so[i] : nullptr;
+    c->gso.x = so[nc];
+    c->gso.y = so[nc + 1];
+    c->gso.vx = so[nc + 2];
+    c->gso.vy = so[nc + 3];
+    c->gso.lw = so[nc + 4];
+    c->gPs = at<float>(c->ws, L.o_gPs);
+    c->ghist = at<int32_t>(c->ws, L.o_ghist);
+    c->gscan = at<int32_t>(c->ws, L.o_gscan);
+    c->gtstart = at<int32_t>(c->ws, L.o_gtstart);
+    c->gcand = at<int32_t>(c->ws, L.o_gcand);
+    c->gk = at<int32_t>(c->ws, L.o_gk);
+    c->gv = at<int32_t>(c->ws, L.o_gv);
+    c->gmlist = at<int32_t>(c->ws, L.o_gmlist);
+    c->gpart1 = at<double>(c->ws, L.o_gpart1);
+    c->gpart2 = at<float>(c->ws, L.o_gpart2);
+    c->gmstart = at<int32_t>(c->ws, L.o_gmstart);
+    c->gzkey = at<int32_t>(c->ws, L.o_gzkey);
+    c->gzstart = at<int32_t>(c->ws, L.o_gzstart);
+    c->gzitems = at<int32_t>(c->ws, L.o_gzitems);
+    c->gA = at<double>(c->ws, L.o_gA);
+    if (p->meas == PHD_MEAS_RANGE_BEARING) {
+      c->ggrid.lo0 = (float)p->region[0];
+      c->ggrid.inv_h0 = (float)(kGateG / (p->region[1] - p->region[0]));
+      c->ggrid.lo1 = (float)-kPi;
+      c->ggrid.inv_h1 = (float)(kGateG / (2.0 * kPi));
+      c->ggrid.wrap1 = 1;
+    } else {
+      c->ggrid.lo0 = (float)p->region[0];
+      c->ggrid.inv_h0 = (float)(kGateG / (p->region[1] - p->region[0]));
+      c->ggrid.lo1 = (float)p->region[2];
+      c->ggrid.inv_h1 = (float)(kGateG / (p->region[3] - p->region[2]));
+      c->ggrid.wrap1 = 0;
+    }
+  }
   CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (48 + 4 * world)));
   CUB(cudaMallocHost(&c->h_est, sizeof(phd_estimate) * (p->max_meas + 1)));
   if (c->dcp) CUB(cudaMallocHost(&c->h_gather, sizeof(phd_estimate) * (p->max_meas + 1) * world));
@@ -783,6 +870,54 @@ static void build_slots(phd_ctx* c, int M) {
   for (int s = n_fill; s < c->slots_pad; ++s) c->h_slot[s] = -1;
 }
 
+// Gated update (DESIGN.md §5 "Gated update"): identity slot layout (slot = label).
+static void gate_slots(phd_ctx* c, int M) {
+  c->n_slots = M;
+  c->slots_pad = std::max(2, (M + 1) & ~1);
+  c->zl = 4;
+  c->wz = kMinWarpsZ;
+  c->zb = M > 0 ? 1 : 0;
+  for (int s = 0; s < c->slots_pad; ++s) c->h_slot[s] = s < M ? s : -1;
+}
+
+// Sort the particles by cell, bin Z_k, count every tile's candidates; decide
+// (collectively for world > 1: every rank must use the same slot layout).
+static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
+  *use = false;
+  const int64_t npad = ceil_div(n, kGateTP) * kGateTP;
+  const int ntiles = (int)(npad / kGateTP);
+  const float* A[5] = {c->A[0], c->A[1], c->A[2], c->A[3], c->A[4]};
+  CU(gate_sort_particles(c->model, A, c->rb, c->L.cap_l, n, npad, c->wscale, c->ggrid, c->gkeys, c->ghist, c->gscan,
+                         c->gso, c->st, &c->launches));
+  KL(gate_zbin(c->zlab, M, c->ggrid, c->gzkey, c->gzstart, c->gzitems, c->st));
+  int64_t tot = 0;
+  if (ntiles > 0) {
+    KL(gate_tiles(0, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->zlab, c->gtstart,
+                  nullptr, nullptr, c->st));
+    CU(gate_scan(c->gtstart, ntiles, c->gscan, c->st, &c->launches));
+    int32_t* h = reinterpret_cast<int32_t*>(c->h_meta + 3 * c->world + 40);
+    CU(cudaMemcpyAsync(h, c->gtstart + ntiles, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    tot = *h;
+  }
+  c->g_entries = tot;
+  c->g_tiles = ntiles;
+  const bool fits = tot <= c->L.g_ecap;
+  const bool pays = (double)tot * kGateTP <= 0.5 * (double)n * (double)M;
+  double veto = (fits && (c->p.gate == 2 || pays)) ? 0.0 : 1.0;
+  if (c->world > 1) {
+    double* d = c->C_slot;  // scratch: rewritten by the update
+    c->h_meta[3 * c->world + 44] = veto;
+    CU(cudaMemcpyAsync(d, c->h_meta + 3 * c->world + 44, sizeof(double), cudaMemcpyHostToDevice, c->st));
+    COMM(c->comm->allreduce_f64(d, 1, c->st));
+    CU(cudaMemcpyAsync(c->h_meta + 3 * c->world + 44, d, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    veto = c->h_meta[3 * c->world + 44];
+  }
+  *use = veto == 0.0;
+  return PHD_OK;
+}
+
 phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
@@ -805,8 +940,17 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     CU(cudaMemcpyAsync(c->zlab, c->h_z, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, c->st));
   }
   c->M_z = M;
-  build_slots(c, M);
   const int64_t n = c->n_local;
+  bool gated = false;
+  if (c->p.gate != 0 && M > 0 && !(getenv("PHD_FUSE") && getenv("PHD_FUSE")[0] == '1')) {
+    phd_status st = gate_plan(c, M, n, &gated);
+    if (st != PHD_OK) return st;
+  }
+  c->gated = gated;
+  if (gated)
+    gate_slots(c, M);
+  else
+    build_slots(c, M);
   const int64_t tiles = ceil_div(n, kTileP);
   if (M > 0) {
     CU(cudaMemcpyAsync(c->slot_label, c->h_slot, sizeof(int32_t) * c->slots_pad, cudaMemcpyHostToDevice, c->st));
@@ -816,7 +960,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   // particle-CTA count: one wave of resident CTAs over the z-blocks of one sweep
   int gp = 0;
   const int zb_sweep = c->fused ? 1 : c->zb;
-  if (M > 0 && n > 0) {
+  if (M > 0 && n > 0 && !gated) {
     int occ = c->fused ? fused_occupancy(c->model, c->wz)
                        : std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl));
     occ = std::max(1, occ);
@@ -856,8 +1000,45 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     KL(launch_zconst(c->C_slot, c->slot_label, s0, s1, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
     return PHD_OK;
   };
-  timing_record(c, 3);
-  if (M > 0 && c->fused) {
+  if (M > 0 && gated) {
+    // candidate lists, entries grouped by label, then the two gated passes
+    const int ntiles = (int)c->g_tiles;
+    if (ntiles > 0)
+      KL(gate_tiles(1, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->zlab, nullptr,
+                    c->gtstart, c->gcand, c->st));
+    CU(gate_sort_entries(c->gcand, c->g_entries, M, c->gk, c->gv, c->gmlist, c->ghist, c->gscan, c->gmstart, c->st,
+                         &c->launches));
+    GateArgs ga{};
+    ga.n = n;
+    ga.ntiles = ntiles;
+    ga.model = c->model;
+    ga.so = c->gso;
+    ga.tstart = c->gtstart;
+    ga.cand = c->gcand;
+    ga.sc = pa.sc;
+    ga.sel = nullptr;
+    ga.na0 = c->na0;
+    ga.na1 = c->na1;
+    ga.part1 = c->gpart1;
+    ga.part2 = c->gpart2;
+    ga.Ps = c->gPs;
+    timing_record(c, 3);
+    if (ntiles > 0) KL(launch_gpass(1, ga, c->st));
+    timing_record(c, 4);
+    KL(launch_wsum(c->A[4], n, c->blk_wp, c->C_slot + c->slots_pad, c->st));
+    KL(launch_gate_reduce(1, c->gmstart, c->gmlist, M, c->gpart1, nullptr, nullptr, c->C_slot, c->slots_pad, c->st));
+    if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
+    KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+    if (c->select) {
+      KL(launch_select(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->st));
+      ga.sel = c->sel_flag;
+    }
+    timing_record(c, 5);
+    if (ntiles > 0) KL(launch_gpass(2, ga, c->st));
+    timing_record(c, 6);
+    KL(launch_gate_reduce(2, c->gmstart, c->gmlist, M, nullptr, c->gpart2, ga.sel, c->gA, c->slots_pad, c->st));
+  } else if (M > 0 && c->fused) {
+    timing_record(c, 3);
     // group-pipelined sweeps: sweep j = pass 1 of group j + pass 2 of group j-1
     const int Q = c->zb;
     for (int j = 0; j <= Q; ++j) {
@@ -873,6 +1054,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     }
     timing_record(c, 6);
   } else if (M > 0) {
+    timing_record(c, 3);
     if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 4);
     // local W_pred rides with C in the C1 all-reduce (element slots_pad)
@@ -894,15 +1076,19 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (gp > 0) KL(launch_pass(c->model, 2, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 6);
   } else {
+    timing_record(c, 3);
     timing_record(c, 4);
     timing_record(c, 5);
     timing_record(c, 6);
   }
   int nbw = (int)ceil_div(n, kBlockW);
-  if (n > 0)
+  if (n > 0 && gated)
+    KL(launch_finalize(c->A[4], c->gPs, 0, M > 0 ? 1 : 0, n, c->nu, c->wscale, c->wn, c->blk_w, c->blk_wp, c->st,
+                       c->gso.inv));
+  else if (n > 0)
     KL(launch_finalize(c->A[4], c->P, c->L.cap_l, M > 0 && gp > 0 ? c->zb : 0, n, c->nu, c->wscale, c->wn, c->blk_w, c->blk_wp, c->st));
   double* rank_slots = c->acc + 5 * (size_t)M;
-  KL(launch_reduce_acc(c->Apart, gp, c->slots_pad, M > 0 ? c->slots_pad : 0, c->slot_label, c->C, c->D, c->s[0],
+  KL(launch_reduce_acc(gated ? c->gA : c->Apart, gated ? 1 : gp, c->slots_pad, M > 0 ? c->slots_pad : 0, c->slot_label, c->C, c->D, c->s[0],
                        c->s[1], c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank,
                        c->world, c->dcp || c->rank == 0 ? 1 : 0, c->select ? c->sel_flag : nullptr, c->st));
   // rank slots [W_r | W_pred_r | N_r] (3 per rank); N_r written from the host
@@ -1250,6 +1436,15 @@ phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estima
     cudaEventElapsedTime(&c->t_ms[7], c->ev[13], c->ev[14]);
   }
   return st;
+}
+
+phd_status phd_get_gate_stats(phd_ctx* c, int64_t* out) {
+  if (!c || !out) return PHD_EINVAL;
+  out[0] = c->gated ? 1 : 0;
+  out[1] = c->g_entries;
+  out[2] = c->g_entries * kGateTP;
+  out[3] = c->g_tiles;
+  return PHD_OK;
 }
 
 phd_status phd_get_normalizers(phd_ctx* c, double* C, int32_t cap) {

@@ -122,8 +122,10 @@ cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, 
                             cudaStream_t s);
 cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
                           float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s);
+// inv != nullptr (gated update): P is one plane in sorted order, read as P[inv[i]]
 cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, int zb, int64_t n, float nu,
-                            float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s);
+                            float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s,
+                            const int32_t* inv = nullptr);
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1, const float* s2,
                               const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
@@ -154,5 +156,77 @@ cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const
 cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
                           int32_t* slot_label, int32_t* js, cudaStream_t s);
 cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, float* d, cudaStream_t s);
+
+// ---- gated update (k_gate.cu, DESIGN.md §5 "Gated update") ------------------
+// Particles are ordered by a Morton cell key in measurement space (stable
+// counting sort; the filter's own particle order is untouched, the passes read
+// a sorted copy), cut into tiles of kGateTP, and every tile is paired only with
+// the measurements whose largest possible exponent over the tile's bounding box,
+//   e_max = -alpha0 dx^2 - alpha1 dy^2 + max_i log2(p_D c w_i),
+// is >= kGateLog2Min: every skipped pair has e < -130, so its fp32 term
+// 2^e flushes to exactly 0 in the dense kernels too (ex2.approx.ftz).
+constexpr int kGateG = 64;            // cells per axis (Morton key of 12 bits)
+constexpr int kGateBins = kGateG * kGateG;
+constexpr int kSortBlock = 8192;      // keys per counting-sort block
+constexpr int kSortMaxBins = 4096;    // bins per counting-sort pass (12-bit digits)
+constexpr int kGateTP = 512;          // particles per tile (256 threads x 2, f32x2)
+constexpr int kGateChunk = 256;       // candidates staged in shared memory at a time
+constexpr float kGateLog2Min = -130.0f;
+
+struct GateGrid {
+  float lo0, lo1;                     // grid origin (x, y) or (r, -pi)
+  float inv_h0, inv_h1;               // cells per unit
+  int wrap1;                          // axis 1 is an angle (range-bearing): cells wrap mod kGateG
+};
+
+// Sorted copy of the particle block: position model c[0..1] = x, y;
+// range-bearing c[0..7] = r_hi, r_lo, thA hi/lo, thB hi/lo, thC hi/lo.
+struct GateSorted {
+  float* c[8];
+  float *x, *y, *vx, *vy;             // Cartesian state (pass 2; x, y alias c[0], c[1] for position)
+  float* lw;                          // log2(p_D c w) (-inf for w = 0 and padding)
+  int32_t* perm;                      // sorted position -> local index
+  int32_t* inv;                       // local index -> sorted position
+};
+
+struct GateArgs {
+  int64_t n;                          // local particles
+  int ntiles;
+  int model;
+  GateSorted so;
+  const int32_t* tstart;              // [ntiles + 1] candidate offsets
+  const int32_t* cand;                // [E] candidate labels, tile-major
+  SlotConsts sc;                      // identity slot layout (slot = label)
+  const int32_t* sel;                 // pass 2: label in the index set I (nullptr: all)
+  float na0, na1;
+  double* part1;                      // [E] tile sums of u = p_D g w (pass 1)
+  float* part2;                       // [E][4] tile sums of the centred state terms (pass 2, selected labels)
+  float* Ps;                          // [n_pad] sum_z u d per sorted particle (pass 2)
+};
+
+// key + stable counting sort of the local particles; writes the sorted copy.
+// Launch count added to *launches.
+cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/, const float* rb, int64_t rb_stride,
+                                int64_t n, int64_t n_pad, float wscale, const GateGrid& grid, int32_t* keys,
+                                int32_t* hist, int32_t* scan_tmp, const GateSorted& so, cudaStream_t s,
+                                int64_t* launches);
+// measurements -> grid cells (one CTA): zcell_start[kGateBins + 1], items stable by label
+cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,
+                      int32_t* zcell_items, cudaStream_t s);
+// per-tile bounding boxes + candidate counts (fill = 0) or labels (fill = 1)
+cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1,
+                       const GateGrid& grid, const int32_t* zcell_start, const int32_t* zcell_items,
+                       const float* z_lab, int32_t* tcount, const int32_t* tstart, int32_t* cand, cudaStream_t s);
+// exclusive scan of n int32 (in place); out[n] = total.  tmp >= ceil(n / 4096) + 1 ints.
+cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64_t* launches);
+// stable sort of the E candidate entries by label: mlist = entry indices grouped by
+// label (ascending entry within a label), mstart[l] = first position of label l.
+cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kbuf, int32_t* vbuf, int32_t* mlist,
+                              int32_t* hist, int32_t* scan_tmp, int32_t* mstart, cudaStream_t s, int64_t* launches);
+cudaError_t launch_gpass(int pass, const GateArgs& g, cudaStream_t s);
+// per-label fixed-order fp64 sums over its entries: pass 1 -> C_slot[l];
+// pass 2 -> A[q * slots_pad + l] for labels in I (all with sel == nullptr)
+cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* mlist, int M, const double* part1,
+                               const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s);
 
 }  // namespace phd

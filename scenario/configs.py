@@ -45,6 +45,7 @@ class Model:
     birth_std: tuple = (math.sqrt(10.0), 1.0, math.sqrt(10.0), 1.0)  # sqrt(diag Q)
     stphd_all: int = 0             # 1: STPHD state sums for every measurement (not only the index set)
     proposal_scale: float = 1.0    # Eq 5 proposal: CV transition with noise std s sigma_a (1: prior)
+    gate: int = 0                  # update: 0 dense, 1 gated (auto fallback), 2 gated when it fits
 
 
 @dataclass(frozen=True)

@@ -27,7 +27,7 @@ def test_library_loads_and_exports_header_symbols():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(binding.EXPORTS)
-    assert L.phd_abi_version() == binding.ABI_VERSION == 2
+    assert L.phd_abi_version() == binding.ABI_VERSION == 3
     assert L.phd_status_str(2) == b"call out of order"
 
 

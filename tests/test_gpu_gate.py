@@ -1,0 +1,218 @@
+"""GPU parity of the gated update (gate = 1/2, DESIGN.md §5 "Gated update";
+SURVEY.md §8(f) NEXT-2): the same oracle tolerances as the dense path
+(tests/test_gpu_parity.py), plus agreement with the dense GPU path, which
+evaluates the same non-zero terms and differs only in fp64 summation order.
+"""
+import math
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import scenario
+from scenario.configs import POSITION, RANGE_BEARING, COUNT_FIXED
+
+from test_gpu_parity import MODELS, POS, RB, _meas, _cloud, _check_update, _near_ties  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def phd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1503_03769_b200 as p
+    p.load()
+    return p
+
+
+def _run(phd, m, soa, w, z):
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+    f.update(z)
+    M = len(z)
+    out = dict(C=f.normalizers(M), acc=f.accumulators(M), wn=f.get_particles()[1], gate=f.gate_stats())
+    est, summ = f.extract()
+    out.update(est=est, summ=summ)
+    f.close()
+    return out
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing", "aniso"])
+@pytest.mark.parametrize("n,M", [(512 * 3 + 77, 37), (64 * 150 + 5, 130), (20011, 600), (9000, 1100), (7001, 2500)])
+def test_gated_update_parity(phd, orc, mname, n, M):
+    m = replace(MODELS[mname], gate=2)
+    z = _meas(m, M, n + M)
+    soa, w = _cloud(m, n, z, n + M)
+    g = _run(phd, m, soa, w, z)
+    assert g["gate"]["used"] == 1
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
+    kap = orc.kappa(m)
+    rhs = (1 - m.p_d) * math.fsum(w.astype(np.float64)) + math.fsum(g["C"] / (kap + g["C"]))
+    assert abs(g["summ"]["W"] - rhs) <= 2e-6 * rhs
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
+@pytest.mark.parametrize("stphd_all", [0, 1])
+def test_gated_equals_dense(phd, orc, mname, stphd_all):
+    """Same non-zero terms as the dense kernels: results agree to fp32 summation order."""
+    m0 = replace(MODELS[mname], stphd_all=stphd_all, clutter_rate=20.0)
+    z = _meas(m0, 700, 11)
+    soa, w = _cloud(m0, 30011, z, 11)
+    d = _run(phd, replace(m0, gate=0), soa, w, z)
+    g = _run(phd, replace(m0, gate=2), soa, w, z)
+    assert d["gate"]["used"] == 0 and g["gate"]["used"] == 1
+    assert g["gate"]["pairs"] < 0.5 * soa.shape[1] * len(z)
+    kap = orc.kappa(m0)
+    assert np.all(np.abs(g["C"] - d["C"]) <= 2e-6 * d["C"] + 1e-12 * kap)
+    assert np.all(np.abs(g["wn"] - d["wn"]) <= 2e-6 * d["wn"] + 1e-9 * w)
+    assert list(g["est"]["labels"]) == list(d["est"]["labels"])
+    assert np.all(np.abs(g["est"]["states"] - d["est"]["states"]) <= 2e-4)
+    assert g["summ"]["LT"] == d["summ"]["LT"]
+
+
+def test_gated_degenerate_inputs(phd, orc):
+    """Ragged and degenerate tiles: one particle, zero-weight tiles, a point cloud
+    (every pair a candidate), M = 1, M = 0 (no candidates), measurements outside
+    the region, particles outside the grid."""
+    m = replace(POS, gate=2)
+    kap = orc.kappa(m)
+    rng = np.random.default_rng(3)
+    z = _meas(m, 50, 3)
+    z[5] = (1500.0, -2500.0)  # outside the region: border cells
+    soa, w = _cloud(m, 3001, z, 3)
+    soa[0, :40] = 5000.0      # particles far outside the grid
+    soa[2, 40:80] = -7000.0
+    w[100:700] = 0.0          # zero-weight run (tiles without mass)
+    cases = [(soa[:, :1].copy(), w[:1].copy(), z), (soa, w, z), (soa, w, z[:1]),
+             (np.repeat(soa[:, :1], 1500, axis=1) + rng.normal(0, 1e-3, (4, 1500)).astype(np.float32),
+              np.full(1500, 1e-3, np.float32), z)]
+    for s, ww, zz in cases:
+        g = _run(phd, m, s, ww, zz)
+        assert g["gate"]["used"] == 1
+        Co = orc.normalizers(m, s, ww, zz)
+        wo, acco = orc.update(m, s, ww, zz, Co)
+        _check_update(orc, m, g["C"], g["acc"], g["wn"], ww, Co, wo, acco)
+    # M = 0: the update is the undetected term only
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+    f.update(np.zeros((0, 2), np.float32))
+    _, wn, _ = f.get_particles()
+    assert np.allclose(wn, (1 - m.p_d) * w, rtol=1e-6)
+    f.close()
+
+
+def test_gated_auto_falls_back(phd, orc):
+    """gate = 1 runs dense when the candidates are most of N x M (a point cloud)."""
+    m = replace(POS, gate=1)
+    z = _meas(m, 20, 4)
+    z[:] = z[0]
+    soa = np.zeros((4, 2000), np.float32)
+    soa[0] = z[0, 0]
+    soa[2] = z[0, 1]
+    w = np.full(2000, 1e-3, np.float32)
+    g = _run(phd, m, soa, w, z)
+    assert g["gate"]["used"] == 0
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
+
+
+def test_gated_range_bearing_seam(phd, orc):
+    """Particles and measurements straddling the bearing seam (theta = +-pi)."""
+    m = replace(RB, gate=2)
+    M = 64
+    z = np.zeros((M, 2), np.float32)
+    rng = np.random.default_rng(9)
+    z[:, 0] = rng.uniform(300, 1500, M)
+    u = rng.uniform(0, 0.02, M)
+    z[:, 1] = np.where(np.arange(M) % 2 == 0, math.pi - u, -math.pi + u)
+    z[0, 1] = np.float32(math.pi)   # fp32(pi) is slightly above pi
+    z[1, 1] = np.float32(-math.pi)
+    n = 6000
+    r = rng.uniform(300, 1500, n)
+    th = math.pi + rng.normal(0, 0.02, n)
+    soa = np.zeros((4, n), np.float32)
+    soa[0] = r * np.cos(th)
+    soa[2] = r * np.sin(th)
+    soa[1] = rng.normal(0, 5, n)
+    soa[3] = rng.normal(0, 5, n)
+    w = np.full(n, 3.0 / n, np.float32)
+    g = _run(phd, m, soa, w, z)
+    assert g["gate"]["used"] == 1
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
+
+
+@pytest.mark.parametrize("cname,steps", [("cfg1", 12), ("cfg2", 6)])
+def test_gated_filter_steps_stagewise(phd, orc, cname, steps):
+    cfg = scenario.get(cname)
+    m = replace(cfg.model, gate=2)
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1])
+    for k in range(1, steps + 1):
+        z = Z[k - 1]
+        f.predict(k)
+        ps, pw, _ = f.get_particles()
+        f.update(z)
+        assert f.gate_stats()["used"] == (1 if len(z) > 0 else 0)
+        C = f.normalizers(len(z))
+        acc = f.accumulators(len(z))
+        _, wn, _ = f.get_particles()
+        Co = orc.normalizers(m, ps, pw, z)
+        wo, acco = orc.update(m, ps, pw, z, Co)
+        _check_update(orc, m, C, acc, wn, pw, Co, wo, acco)
+        est, summ = f.extract()
+        eg = orc.extract(m, acc, summ["W"], summ["W_pred"])
+        assert list(est["labels"]) == list(eg["labels"])
+        f.resample_exchange(k)
+        anc, _ = f.ancestors()
+        meta = f.resample_meta()
+        ao, _ = orc.resample(wn.astype(np.float64), meta["U"], meta["N_out"])
+        ties = _near_ties(wn, meta["U"], meta["N_out"])
+        assert np.all(ties[anc != ao])
+    f.close()
+
+
+@pytest.mark.parametrize("cname", ["cfg3", "cfg4", "cfg5"])
+def test_gated_full_size_sampled(phd, orc, cname):
+    """BASELINE sizes with gate = 1 (cfg 5 is the bench configuration of the gated line)."""
+    cfg = scenario.get(cname)
+    m = replace(cfg.model, gate=1)
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1])
+    f.predict(1)
+    ps, pw, _ = f.get_particles()
+    f.update(Z[0])
+    M = len(Z[0])
+    gs = f.gate_stats()
+    assert gs["used"] == 1
+    C = f.normalizers(M)
+    _, wn, _ = f.get_particles()
+    est, summ = f.extract()
+    kap = orc.kappa(m)
+    N = ps.shape[1]
+    rng = np.random.default_rng(1)
+    for p in rng.choice(M, 3, replace=False):
+        Co = orc.normalizers(m, ps, pw, Z[0][p:p + 1])[0]
+        assert abs(C[p] - Co) <= 1e-5 * Co + 1e-9 * kap
+    idx = np.concatenate([rng.choice(N, 64, replace=False), np.argsort(wn)[-64:]])
+    wo, _ = orc.update(m, ps[:, idx], pw[idx], Z[0], C)
+    assert np.all(np.abs(wn[idx] - wo) <= 1e-4 * wo + 1e-7 * pw[idx])
+    rhs = (1 - m.p_d) * summ["W_pred"] + math.fsum(C / (kap + C))
+    assert abs(summ["W"] - rhs) <= 1e-5 * rhs
+    for i in range(min(2, len(est["labels"]))):
+        lab = int(est["labels"][i])
+        _, ao = orc.update(m, ps, pw, Z[0][lab:lab + 1], C[lab:lab + 1])
+        assert np.all(np.abs(est["states"][i] - ao[0, 1:] / ao[0, 0]) <= 1e-3)
+    f.close()
