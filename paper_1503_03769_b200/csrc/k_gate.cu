@@ -19,7 +19,7 @@
 //      with (dx, dy) its distance to the box (wrapped in bearing).  Every term
 //      of a non-candidate pair has e <= e_max < -130 (fp32 rounding of the
 //      kernels' exponent is ~1e-4 here), so it is exactly 0 in the dense path.
-//   4. k_gpass<1>: CTA per tile, two particles per thread (f32x2), candidates
+//   4. k_gpass<1>: CTA per tile, four particles per thread (2 x f32x2), candidates
 //      broadcast from shared memory; the same per-pair arithmetic as the dense
 //      pass (pair_math.cuh), so every term is bitwise the dense kernel's.  Tile
 //      sums per candidate: warp tree (transposed butterfly), fp64 across warps.
@@ -31,11 +31,12 @@
 #include "phd_internal.h"
 #include "pair_math.cuh"
 
+#include <algorithm>
+
 namespace phd {
 
 namespace {
 
-constexpr float kPi = 3.14159265358979323846f;
 constexpr float kTwoPi = 6.28318530717958647692f;
 
 __device__ __forceinline__ uint32_t spread6(uint32_t v) {
@@ -157,106 +158,187 @@ __global__ void __launch_bounds__(1024) k_scan_apply(int32_t* a, int64_t n, cons
 }
 
 // ---------------------------------------------------------------------------
-// Stable counting sort pass on bits [shift, shift + log2 nbins) of keys.
-// hist is bin-major, hist[bin * nblk + blk], so its exclusive scan is the
-// first output position of every (bin, block): stable across blocks; within a
-// block one warp walks the keys in order (match_any ranks equal bins).
-__global__ void __launch_bounds__(256) k_csort_hist(const int32_t* __restrict__ keys, int64_t n, int shift, int nbins,
-                                                    int nblk, int32_t* hist) {
+// Stable counting sort pass (deterministic; no floating point involved).
+// hist is bin-major, hist[bin * nblk + blk], so its exclusive scan gives the
+// first output position of every (bin, block).  A CTA of kMsWarps warps owns
+// per_blk consecutive items, warp w the w-th slice; per-warp 16-bit
+// sub-histograms in shared memory give each warp its offset inside the
+// block's run of a bin, and the warp then walks its slice in order, ranking
+// equal bins with match_any.  Keys come from a functor: the digit of an int
+// array, or a particle's measurement-space cell.
+constexpr int kMsWarps = 8;
+constexpr int kMsRows = 8;  // rows of 32 items whose loads are issued together
+
+struct KeyArr {
+  const int32_t* k;
+  int shift, mask;
+  __device__ __forceinline__ int digit(int32_t raw) const { return (raw >> shift) & mask; }
+  __device__ __forceinline__ int32_t raw(int64_t i) const { return __ldg(k + i); }
+};
+struct KeyCell {
+  const float* a0;
+  const float* a1;
+  GateGrid g;
+  __device__ __forceinline__ int digit(int32_t raw) const { return raw; }
+  __device__ __forceinline__ int32_t raw(int64_t i) const { return cell_key(__ldg(a0 + i), __ldg(a1 + i), g); }
+};
+
+template <class KF>
+__global__ void __launch_bounds__(256) k_ms_hist(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk, int32_t* hist) {
   __shared__ int h[kSortMaxBins];
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
   __syncthreads();
-  const int64_t i0 = (int64_t)blockIdx.x * kSortBlock;
-  const int64_t i1 = min(n, i0 + kSortBlock);
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&h[(keys[i] >> shift) & (nbins - 1)], 1);
+  const int64_t i0 = (int64_t)blockIdx.x * per_blk;
+  const int64_t i1 = min(n, i0 + per_blk);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&h[kf.digit(kf.raw(i))], 1);
   __syncthreads();
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) hist[(int64_t)b * nblk + blockIdx.x] = h[b];
 }
 
-__global__ void __launch_bounds__(32) k_csort_scatter(const int32_t* __restrict__ keys, const int32_t* __restrict__ vals,
-                                                      int64_t n, int shift, int nbins, int nblk,
-                                                      const int32_t* __restrict__ hs, int32_t* out_keys,
-                                                      int32_t* out_vals) {
-  __shared__ int cnt[kSortMaxBins];
-  const int lane = threadIdx.x;
-  for (int b = lane; b < nbins; b += 32) cnt[b] = hs[(int64_t)b * nblk + blockIdx.x];
-  __syncwarp();
-  const int64_t i0 = (int64_t)blockIdx.x * kSortBlock;
-  const int64_t i1 = min(n, i0 + kSortBlock);
-  const unsigned lt = (1u << lane) - 1u;
-  for (int64_t base = i0; base < i1; base += 32) {
-    const int64_t i = base + lane;
-    const bool ok = i < i1;
-    const int key = ok ? keys[i] : 0;
-    const int bin = ok ? ((key >> shift) & (nbins - 1)) : kSortMaxBins + lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    int pos = 0;
-    if (ok) pos = cnt[bin] + __popc(peers & lt);
-    __syncwarp();
-    if (ok) {
-      if (lane == __ffs(peers) - 1) cnt[bin] += __popc(peers);
-      if (out_keys) out_keys[pos] = key;
-      out_vals[pos] = vals ? vals[i] : (int32_t)i;
+// smem: wh[kMsWarps][nbins / 2] packed 16-bit counters, base[nbins]
+template <class KF>
+__global__ void __launch_bounds__(256) k_ms_scatter(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk,
+                                                    const int32_t* __restrict__ hs, const int32_t* __restrict__ vals,
+                                                    int32_t* out_keys, int32_t* out_vals) {
+  extern __shared__ uint32_t sm[];
+  const int nw = nbins >> 1;  // nbins even
+  uint32_t* wh = sm;
+  int* base = reinterpret_cast<int*>(sm + kMsWarps * nw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < kMsWarps * nw; j += blockDim.x) wh[j] = 0u;
+  __syncthreads();
+  const int64_t i0 = (int64_t)blockIdx.x * per_blk;
+  const int64_t i1 = min(n, i0 + per_blk);
+  const int64_t pw = per_blk / kMsWarps;
+  const int64_t w0 = min(i1, i0 + warp * pw), w1 = min(i1, w0 + pw);
+  uint32_t* my = wh + warp * nw;
+  // 1. per-warp sub-histograms
+  for (int64_t b0 = w0; b0 < w1; b0 += 32 * kMsRows) {
+    int32_t raw[kMsRows];
+#pragma unroll
+    for (int r = 0; r < kMsRows; ++r) raw[r] = kf.raw(min(b0 + r * 32 + lane, w1 - 1));
+#pragma unroll
+    for (int r = 0; r < kMsRows; ++r)
+      if (b0 + r * 32 + lane < w1) {
+        const int d = kf.digit(raw[r]);
+        atomicAdd(&my[d >> 1], 1u << (16 * (d & 1)));
+      }
+  }
+  __syncthreads();
+  // 2. exclusive prefix over the warps of every bin; block offsets of the bins
+  for (int j = tid; j < nw; j += blockDim.x) {
+    uint32_t run = 0u;
+#pragma unroll
+    for (int w = 0; w < kMsWarps; ++w) {
+      const uint32_t c = wh[w * nw + j];
+      wh[w * nw + j] = run;
+      run += c;  // the two 16-bit halves never carry: per-block counts < 65536
     }
-    __syncwarp();
+    base[2 * j] = hs[(int64_t)(2 * j) * nblk + blockIdx.x];
+    base[2 * j + 1] = hs[(int64_t)(2 * j + 1) * nblk + blockIdx.x];
+  }
+  __syncthreads();
+  // 3. stable ranking of the warp's slice
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t b0 = w0; b0 < w1; b0 += 32 * kMsRows) {
+    int32_t raw[kMsRows];
+    int32_t val[kMsRows];
+#pragma unroll
+    for (int r = 0; r < kMsRows; ++r) {
+      const int64_t i = min(b0 + r * 32 + lane, w1 - 1);
+      raw[r] = kf.raw(i);
+      val[r] = vals ? __ldg(vals + i) : (int32_t)(b0 + r * 32 + lane);
+    }
+#pragma unroll
+    for (int r = 0; r < kMsRows; ++r) {
+      const bool ok = b0 + r * 32 + lane < w1;
+      const int d = ok ? kf.digit(raw[r]) : nbins + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      int pos = 0;
+      if (ok) pos = base[d] + (int)((my[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) + __popc(peers & lt);
+      __syncwarp();
+      if (ok) {
+        if (lane == __ffs(peers) - 1) atomicAdd(&my[d >> 1], (uint32_t)__popc(peers) << (16 * (d & 1)));
+        if (out_keys) out_keys[pos] = raw[r];
+        out_vals[pos] = val[r];
+      }
+      __syncwarp();
+    }
   }
 }
 
-cudaError_t csort_pass(const int32_t* keys, const int32_t* vals, int64_t n, int shift, int nbins, int32_t* hist,
-                       int32_t* scan_tmp, int32_t* out_keys, int32_t* out_vals, cudaStream_t s, int64_t* launches) {
+template <class KF>
+cudaError_t ms_pass(KF kf, const int32_t* vals, int64_t n, int64_t per_blk, int nbins, int32_t* hist,
+                    int32_t* scan_tmp, int32_t* out_keys, int32_t* out_vals, cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;
-  const int nblk = (int)((n + kSortBlock - 1) / kSortBlock);
-  k_csort_hist<<<nblk, 256, 0, s>>>(keys, n, shift, nbins, nblk, hist);
+  nbins = std::max(2, nbins);
+  const int nblk = (int)((n + per_blk - 1) / per_blk);
+  const size_t smem = sizeof(uint32_t) * (size_t)kMsWarps * (nbins / 2) + sizeof(int) * (size_t)nbins;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ms_scatter<KF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(uint32_t) * kMsWarps * (kSortMaxBins / 2) + sizeof(int) * kSortMaxBins));
+    attr = true;
+  }
+  k_ms_hist<KF><<<nblk, 256, 0, s>>>(kf, n, per_blk, nbins, nblk, hist);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)nbins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
-  k_csort_scatter<<<nblk, 32, 0, s>>>(keys, vals, n, shift, nbins, nblk, hist, out_keys, out_vals);
+  k_ms_scatter<KF><<<nblk, 256, smem, s>>>(kf, n, per_blk, nbins, nblk, hist, vals, out_keys, out_vals);
   ++*launches;
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// particle keys: position (x, y); range-bearing (r_hi, thetaA_hi)
-__global__ void k_gate_keys(int model, const float* __restrict__ a0, const float* __restrict__ a1, int64_t n,
-                            GateGrid g, int32_t* keys) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  keys[i] = cell_key(a0[i], a1[i], g);
+cudaError_t csort_pass(const int32_t* keys, const int32_t* vals, int64_t n, int shift, int nbins, int32_t* hist,
+                       int32_t* scan_tmp, int32_t* out_keys, int32_t* out_vals, cudaStream_t s, int64_t* launches) {
+  KeyArr kf{keys, shift, std::max(2, nbins) - 1};
+  return ms_pass(kf, vals, n, kESortBlock, nbins, hist, scan_tmp, out_keys, out_vals, s, launches);
 }
 
+// ---------------------------------------------------------------------------
+// Particle sort, fused: k_psort_hist computes each particle's cell key from its
+// coordinates (position (x, y); range-bearing (r_hi, thetaA_hi)) into the
+// per-block histograms; k_psort_scatter recomputes the key, ranks it stably
+// and writes the particle straight into the sorted copy (+ inv), loads
+// software-pipelined kPsB warps-rows deep.  Padding [n, n_pad) gets zero state
+// and lw = -inf.
 struct GatherSrc {
   const float* c[8];
   const float *x, *y, *vx, *vy, *w;
 };
 
-// sorted copy; padding positions [n, n_pad) get zero state and lw = -inf
-__global__ void k_gate_gather(int model, GatherSrc src, int64_t n, int64_t n_pad, float wscale, GateSorted so) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// padding of the sorted copy: positions [n, n_pad) get zero state and lw = -inf
+__global__ void k_psort_pad(int64_t n, int64_t n_pad, int model, GateSorted so) {
+  const int64_t p = n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pad) return;
-  const bool rb = model == kRangeBearing;
-  if (p < n) {
-    const int i = so.perm[p];
-    if (rb) {
+  if (model == kRangeBearing) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) so.c[c][p] = src.c[c][i];
-    }
-    so.x[p] = src.x[i];
-    so.y[p] = src.y[i];
-    so.vx[p] = src.vx[i];
-    so.vy[p] = src.vy[i];
-    so.lw[p] = log2f(src.w[i] * wscale);  // the dense TileLoader's exact expression
-    so.inv[i] = (int32_t)p;
-  } else {
-    if (rb) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) so.c[c][p] = 0.0f;
-    }
-    so.x[p] = 0.0f;
-    so.y[p] = 0.0f;
-    so.vx[p] = 0.0f;
-    so.vy[p] = 0.0f;
-    so.lw[p] = -INFINITY;
+    for (int c = 0; c < 8; ++c) so.c[c][p] = 0.0f;
   }
+  so.x[p] = 0.0f;
+  so.y[p] = 0.0f;
+  so.vx[p] = 0.0f;
+  so.vy[p] = 0.0f;
+  so.lw[p] = -INFINITY;
+}
+
+// sorted copy (coalesced writes, gathered reads) + inv
+template <int MODEL>
+__global__ void __launch_bounds__(256) k_psort_gather(GatherSrc src, const int32_t* __restrict__ perm, int64_t n,
+                                                      float wscale, GateSorted so) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int i = perm[p];
+  if (MODEL == kRangeBearing) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) so.c[c][p] = __ldg(src.c[c] + i);
+  }
+  so.x[p] = __ldg(src.x + i);
+  so.y[p] = __ldg(src.y + i);
+  so.vx[p] = __ldg(src.vx + i);
+  so.vy[p] = __ldg(src.vy + i);
+  so.lw[p] = log2f(__ldg(src.w + i) * wscale);  // the dense TileLoader's exact expression
+  so.inv[i] = (int32_t)p;
 }
 
 // ---------------------------------------------------------------------------
@@ -417,74 +499,88 @@ __global__ void k_gate_count_labels(const int32_t* __restrict__ cand, int64_t E,
   if (e < E) atomicAdd(&cnt[cand[e]], 1);
 }
 
+__global__ void k_mstart_from_hist(const int32_t* __restrict__ hs, int nblk, int M, int32_t E, int32_t* mstart) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < M) mstart[l] = hs[(int64_t)l * nblk];
+  if (l == M) mstart[M] = E;
+}
+
 __global__ void k_zero_i32(int32_t* a, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = 0;
 }
 
 // ---------------------------------------------------------------------------
-// The gated passes.  Tile t = sorted particles [t*512, t*512 + 512); thread
-// tid holds particles tid and tid + 256 as one f32x2 pair.
+// The gated passes.  Tile t = sorted particles [t*512, t*512 + 512); a CTA of
+// kGpThreads = 128 threads, thread tid holds four particles as two f32x2 pairs
+// h = 0, 1: (tid + 256 h, tid + 128 + 256 h).  Per candidate the thread sums
+// its four terms before the cross-lane reduction.
+constexpr int kGpThreads = 128;
+constexpr int kGpWarps = kGpThreads / 32;
+
 template <int MODEL>
-struct GPart {
-  float2 X, Y, LW;            // position: x, y (residual coordinates); all: Cartesian x, y for pass 2
-  float2 R_hi, R_lo, T_hi[3], T_lo[3];  // range-bearing representation
+struct GPair {
+  float2 X, Y, LW;                        // Cartesian x, y; log2(p_D c w)
+  float2 R_hi, R_lo, T_hi[3], T_lo[3];    // range-bearing representation
   float2 VX, VY;
 };
 
 template <int MODEL, int PASS>
-__global__ void __launch_bounds__(256, 3) k_gpass(const GateArgs g) {
+__global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS == 2) ? 5 : 8) k_gpass(const GateArgs g) {
   constexpr bool RB = MODEL == kRangeBearing;
   __shared__ float2 zn[kGateChunk];          // (-z0, -z1)
   __shared__ float zd[kGateChunk];           // 1 / (kappa + C)          (pass 2)
   __shared__ int zr[kGateChunk];             // bearing representation   (range-bearing)
   __shared__ float2 zc[kGateChunk];          // -(Cartesian centre)      (range-bearing, pass 2)
   __shared__ int zi[kGateChunk];             // chunk-local entry index  (pass 2: selected first)
-  __shared__ int wcnt[9];
-  __shared__ float wpart[8][kGateChunk];     // pass 1: per-warp candidate sums
-  __shared__ float4 wq[PASS == 2 ? 8 : 1][PASS == 2 ? kGateChunk : 1];  // pass 2: per-warp state sums
+  __shared__ int wcnt[kGpWarps + 1];
+  __shared__ float wpart[PASS == 1 ? kGpWarps : 1][PASS == 1 ? kGateChunk : 1];   // pass 1: per-warp sums
+  __shared__ float4 wq[PASS == 2 ? kGpWarps : 1][PASS == 2 ? kGateChunk : 1];     // pass 2: per-warp state sums
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = blockIdx.x;
-  const int64_t pa = (int64_t)t * kGateTP + tid, pb = pa + 256;
   const float2 na0 = f2(g.na0, g.na0), na1 = f2(g.na1, g.na1);
-  GPart<MODEL> P;
-  P.LW = f2(g.so.lw[pa], g.so.lw[pb]);
-  if (RB) {
-    P.R_hi = f2(g.so.c[0][pa], g.so.c[0][pb]);
-    P.R_lo = f2(g.so.c[1][pa], g.so.c[1][pb]);
+  GPair<MODEL> P[2];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      P.T_hi[r] = f2(g.so.c[2 + 2 * r][pa], g.so.c[2 + 2 * r][pb]);
-      P.T_lo[r] = f2(g.so.c[3 + 2 * r][pa], g.so.c[3 + 2 * r][pb]);
+  for (int h = 0; h < 2; ++h) {
+    const int64_t pa = (int64_t)t * kGateTP + 256 * h + tid, pb = pa + 128;
+    P[h].LW = f2(g.so.lw[pa], g.so.lw[pb]);
+    if (RB) {
+      P[h].R_hi = f2(g.so.c[0][pa], g.so.c[0][pb]);
+      P[h].R_lo = f2(g.so.c[1][pa], g.so.c[1][pb]);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        P[h].T_hi[r] = f2(g.so.c[2 + 2 * r][pa], g.so.c[2 + 2 * r][pb]);
+        P[h].T_lo[r] = f2(g.so.c[3 + 2 * r][pa], g.so.c[3 + 2 * r][pb]);
+      }
     }
-  }
-  if (!RB || PASS == 2) {
-    P.X = f2(g.so.x[pa], g.so.x[pb]);
-    P.Y = f2(g.so.y[pa], g.so.y[pb]);
-  }
-  if (PASS == 2) {
-    P.VX = f2(g.so.vx[pa], g.so.vx[pb]);
-    P.VY = f2(g.so.vy[pa], g.so.vy[pb]);
+    if (!RB || PASS == 2) {
+      P[h].X = f2(g.so.x[pa], g.so.x[pb]);
+      P[h].Y = f2(g.so.y[pa], g.so.y[pb]);
+    }
+    if (PASS == 2) {
+      P[h].VX = f2(g.so.vx[pa], g.so.vx[pb]);
+      P[h].VY = f2(g.so.vy[pa], g.so.vy[pb]);
+    }
   }
   const int e0 = g.tstart[t];
   const int K = g.tstart[t + 1] - e0;
-  float2 pacc = f2(0.0f, 0.0f);
+  float2 pacc[2] = {f2(0.0f, 0.0f), f2(0.0f, 0.0f)};
 
-  // u = p_D g(z_k | x) w for the thread's two particles (bitwise the dense term)
-  auto term = [&](int k, float2& d0, float2& d1) -> float2 {
+  // u = p_D g(z_k | x) w for pair h (bitwise the dense kernel's term)
+  auto term = [&](int k, int h, float2& d0, float2& d1) -> float2 {
     const float2 nz = zn[k];
     if (RB) {
       const int rep = zr[k];
-      const float2 th = rep == 0 ? P.T_hi[0] : (rep == 1 ? P.T_hi[1] : P.T_hi[2]);
-      const float2 tl = rep == 0 ? P.T_lo[0] : (rep == 1 ? P.T_lo[1] : P.T_lo[2]);
-      d0 = __fadd2_rn(__fadd2_rn(P.R_hi, f2(nz.x, nz.x)), P.R_lo);  // (r_hi - z_r) + r_lo
-      d1 = __fadd2_rn(__fadd2_rn(th, f2(nz.y, nz.y)), tl);          // (th_hi - z_th) + th_lo
+      const float2 th = rep == 0 ? P[h].T_hi[0] : (rep == 1 ? P[h].T_hi[1] : P[h].T_hi[2]);
+      const float2 tl = rep == 0 ? P[h].T_lo[0] : (rep == 1 ? P[h].T_lo[1] : P[h].T_lo[2]);
+      d0 = __fadd2_rn(__fadd2_rn(P[h].R_hi, f2(nz.x, nz.x)), P[h].R_lo);  // (r_hi - z_r) + r_lo
+      d1 = __fadd2_rn(__fadd2_rn(th, f2(nz.y, nz.y)), tl);                // (th_hi - z_th) + th_lo
     } else {
-      d0 = __fadd2_rn(P.X, f2(nz.x, nz.x));  // x - z_x
-      d1 = __fadd2_rn(P.Y, f2(nz.y, nz.y));  // y - z_y
+      d0 = __fadd2_rn(P[h].X, f2(nz.x, nz.x));  // x - z_x
+      d1 = __fadd2_rn(P[h].Y, f2(nz.y, nz.y));  // y - z_y
     }
-    return ex2v(expo<MODEL>(d0, d1, na0, na1, P.LW));
+    return ex2v(expo<MODEL>(d0, d1, na0, na1, P[h].LW));
   };
 
   for (int cb = 0; cb < K; cb += kGateChunk) {
@@ -493,43 +589,77 @@ __global__ void __launch_bounds__(256, 3) k_gpass(const GateArgs g) {
     __syncthreads();  // previous chunk fully consumed
     int nsel = 0;
     if (PASS == 1) {
-      if (tid < cl8) {
-        if (tid < cl) {
-          const int l = g.cand[e0 + cb + tid];
-          zn[tid] = f2(g.sc.s0[l], g.sc.s1[l]);
-          if (RB) zr[tid] = g.sc.rep[l];
+      for (int k = tid; k < cl8; k += kGpThreads) {
+        if (k < cl) {
+          const int l = g.cand[e0 + cb + k];
+          zn[k] = f2(g.sc.s0[l], g.sc.s1[l]);
+          if (RB) zr[k] = g.sc.rep[l];
         } else {
-          zn[tid] = f2(-1e30f, -1e30f);  // sentinel: every term exactly 0
-          if (RB) zr[tid] = 0;
+          zn[k] = f2(-1e30f, -1e30f);  // sentinel: every term exactly 0
+          if (RB) zr[k] = 0;
         }
       }
     } else {
       // stable partition: labels in I first (their state sums are reduced), then the rest
-      int l = -1, fl = 0;
-      if (tid < cl) {
-        l = g.cand[e0 + cb + tid];
-        fl = g.sel == nullptr ? 1 : (g.sel[l] != 0);
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, fl);
-      if (lane == 0) wcnt[warp] = __popc(bal);
-      __syncthreads();
-      if (tid == 0) {
-        int s = 0;
-        for (int w = 0; w < 8; ++w) {
-          const int c = wcnt[w];
-          wcnt[w] = s;
-          s += c;
+      int base_sel = 0;
+      for (int k0 = 0; k0 < cl; k0 += kGpThreads) {
+        const int k = k0 + tid;
+        int l = -1, fl = 0;
+        if (k < cl) {
+          l = g.cand[e0 + cb + k];
+          fl = g.sel == nullptr ? 1 : (g.sel[l] != 0);
         }
-        wcnt[8] = s;
+        const unsigned bal = __ballot_sync(0xffffffffu, fl);
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+          int sacc = 0;
+          for (int w = 0; w < kGpWarps; ++w) {
+            const int c = wcnt[w];
+            wcnt[w] = sacc;
+            sacc += c;
+          }
+          wcnt[kGpWarps] = sacc;
+        }
+        __syncthreads();
+        if (k < cl && fl) {
+          const int pos = base_sel + wcnt[warp] + __popc(bal & ((1u << lane) - 1u));
+          zi[pos] = k;
+        }
+        base_sel += wcnt[kGpWarps];
+        __syncthreads();
       }
-      __syncthreads();
-      nsel = wcnt[8];
-      if (tid < cl) {
-        const int before = wcnt[warp] + __popc(bal & ((1u << lane) - 1u));
-        const int pos = fl ? before : nsel + (tid - before);
+      nsel = base_sel;
+      // second sweep: the unselected after the selected, in order
+      int base_un = nsel;
+      for (int k0 = 0; k0 < cl; k0 += kGpThreads) {
+        const int k = k0 + tid;
+        int fl = 0;
+        if (k < cl) {
+          const int l = g.cand[e0 + cb + k];
+          fl = (g.sel == nullptr ? 1 : (g.sel[l] != 0)) ? 0 : 1;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, fl);
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+          int sacc = 0;
+          for (int w = 0; w < kGpWarps; ++w) {
+            const int c = wcnt[w];
+            wcnt[w] = sacc;
+            sacc += c;
+          }
+          wcnt[kGpWarps] = sacc;
+        }
+        __syncthreads();
+        if (k < cl && fl) zi[base_un + wcnt[warp] + __popc(bal & ((1u << lane) - 1u))] = k;
+        base_un += wcnt[kGpWarps];
+        __syncthreads();
+      }
+      for (int pos = tid; pos < cl; pos += kGpThreads) {
+        const int l = g.cand[e0 + cb + zi[pos]];
         zn[pos] = f2(g.sc.s0[l], g.sc.s1[l]);
         zd[pos] = g.sc.d[l];
-        zi[pos] = tid;
         if (RB) {
           zr[pos] = g.sc.rep[l];
           zc[pos] = f2(g.sc.s2[l], g.sc.s3[l]);
@@ -544,43 +674,49 @@ __global__ void __launch_bounds__(256, 3) k_gpass(const GateArgs g) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float2 d0, d1;
-          const float2 u = term(k8 + j, d0, d1);
+          const float2 u = __fadd2_rn(term(k8 + j, 0, d0, d1), term(k8 + j, 1, d0, d1));
           v[j] = u.x + u.y;
         }
         const float r = transpose_reduce8(v, lane);
         if ((lane & 3) == 0) wpart[warp][k8 + (lane >> 2)] = r;
       }
       __syncthreads();
-      if (tid < cl) {
-        double s = 0.0;
+      for (int k = tid; k < cl; k += kGpThreads) {
+        double sum = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) s += (double)wpart[w][tid];
-        g.part1[e0 + cb + tid] = s;
+        for (int w = 0; w < kGpWarps; ++w) sum += (double)wpart[w][k];
+        g.part1[e0 + cb + k] = sum;
       }
     } else {
       // selected candidates, two at a time: weights + the four centred state sums
       for (int k = 0; k < nsel; k += 2) {
         float v[8];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kk = k + h;
+        for (int hh = 0; hh < 2; ++hh) {
+          const int kk = k + hh;
           if (kk < nsel) {
-            float2 d0, d1;
-            const float2 u = term(kk, d0, d1);
-            pacc = __ffma2_rn(u, f2(zd[kk], zd[kk]), pacc);
-            if (RB) {
-              const float2 c = zc[kk];
-              d0 = __fadd2_rn(P.X, f2(c.x, c.x));  // x - centre_x
-              d1 = __fadd2_rn(P.Y, f2(c.y, c.y));  // y - centre_y
+            float2 a0 = f2(0.0f, 0.0f), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float2 d0, d1;
+              const float2 u = term(kk, h, d0, d1);
+              pacc[h] = __ffma2_rn(u, f2(zd[kk], zd[kk]), pacc[h]);
+              if (RB) {
+                const float2 c = zc[kk];
+                d0 = __fadd2_rn(P[h].X, f2(c.x, c.x));  // x - centre_x
+                d1 = __fadd2_rn(P[h].Y, f2(c.y, c.y));  // y - centre_y
+              }
+              a0 = __ffma2_rn(u, d0, a0);
+              a1 = __ffma2_rn(u, P[h].VX, a1);
+              a2 = __ffma2_rn(u, d1, a2);
+              a3 = __ffma2_rn(u, P[h].VY, a3);
             }
-            const float2 a0 = __fmul2_rn(u, d0), a1 = __fmul2_rn(u, P.VX);
-            const float2 a2 = __fmul2_rn(u, d1), a3 = __fmul2_rn(u, P.VY);
-            v[4 * h + 0] = a0.x + a0.y;
-            v[4 * h + 1] = a1.x + a1.y;
-            v[4 * h + 2] = a2.x + a2.y;
-            v[4 * h + 3] = a3.x + a3.y;
+            v[4 * hh + 0] = a0.x + a0.y;
+            v[4 * hh + 1] = a1.x + a1.y;
+            v[4 * hh + 2] = a2.x + a2.y;
+            v[4 * hh + 3] = a3.x + a3.y;
           } else {
-            v[4 * h + 0] = v[4 * h + 1] = v[4 * h + 2] = v[4 * h + 3] = 0.0f;
+            v[4 * hh + 0] = v[4 * hh + 1] = v[4 * hh + 2] = v[4 * hh + 3] = 0.0f;
           }
         }
         const float r = transpose_reduce8(v, lane);
@@ -588,30 +724,37 @@ __global__ void __launch_bounds__(256, 3) k_gpass(const GateArgs g) {
         if ((lane & 3) == 0 && k + (q >> 2) < nsel) reinterpret_cast<float*>(&wq[warp][k + (q >> 2)])[q & 3] = r;
       }
       // the rest: weights only
-#pragma unroll 4
+#pragma unroll 2
       for (int k = nsel; k < cl; ++k) {
-        float2 d0, d1;
-        const float2 u = term(k, d0, d1);
-        pacc = __ffma2_rn(u, f2(zd[k], zd[k]), pacc);
+        const float2 dk = f2(zd[k], zd[k]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float2 d0, d1;
+          pacc[h] = __ffma2_rn(term(k, h, d0, d1), dk, pacc[h]);
+        }
       }
       __syncthreads();
-      if (tid < nsel) {
+      for (int k = tid; k < nsel; k += kGpThreads) {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const float4 a = wq[w][tid];
+        for (int w = 0; w < kGpWarps; ++w) {
+          const float4 a = wq[w][k];
           s0 += (double)a.x;
           s1 += (double)a.y;
           s2 += (double)a.z;
           s3 += (double)a.w;
         }
-        reinterpret_cast<float4*>(g.part2)[e0 + cb + zi[tid]] = make_float4((float)s0, (float)s1, (float)s2, (float)s3);
+        reinterpret_cast<float4*>(g.part2)[e0 + cb + zi[k]] = make_float4((float)s0, (float)s1, (float)s2, (float)s3);
       }
     }
   }
   if (PASS == 2) {
-    g.Ps[pa] = pacc.x;
-    g.Ps[pb] = pacc.y;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t pa = (int64_t)t * kGateTP + 256 * h + tid;
+      g.Ps[pa] = pacc[h].x;
+      g.Ps[pa + 128] = pacc[h].y;
+    }
   }
 }
 
@@ -667,17 +810,17 @@ cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64
 }
 
 cudaError_t gate_sort_particles(int model, const float* const* A, const float* rb, int64_t rb_stride, int64_t n,
-                                int64_t n_pad, float wscale, const GateGrid& grid, int32_t* keys, int32_t* hist,
-                                int32_t* scan_tmp, const GateSorted& so, cudaStream_t s, int64_t* launches) {
+                                int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
+                                int32_t* perm, const GateSorted& so, cudaStream_t s, int64_t* launches) {
   const bool rbm = model == kRangeBearing;
-  if (n > 0) {
-    const float* a0 = rbm ? rb : A[0];
-    const float* a1 = rbm ? rb + 2 * rb_stride : A[2];
-    k_gate_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(model, a0, a1, n, grid, keys);
+  if (n_pad > n) {
+    k_psort_pad<<<(unsigned)((n_pad - n + 255) / 256), 256, 0, s>>>(n, n_pad, model, so);
     ++*launches;
-    cudaError_t e = csort_pass(keys, nullptr, n, 0, kGateBins, hist, scan_tmp, nullptr, so.perm, s, launches);
-    if (e != cudaSuccess) return e;
   }
+  if (n <= 0) return cudaGetLastError();
+  KeyCell kf{rbm ? rb : A[0], rbm ? rb + 2 * rb_stride : A[2], grid};
+  cudaError_t e = ms_pass(kf, nullptr, n, kPSortBlock, kGateBins, hist, scan_tmp, nullptr, perm, s, launches);
+  if (e != cudaSuccess) return e;
   GatherSrc src{};
   for (int c = 0; c < 8; ++c) src.c[c] = rbm ? rb + c * rb_stride : nullptr;
   src.x = A[0];
@@ -685,10 +828,12 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
   src.y = A[2];
   src.vy = A[3];
   src.w = A[4];
-  if (n_pad > 0) {
-    k_gate_gather<<<(unsigned)((n_pad + 255) / 256), 256, 0, s>>>(model, src, n, n_pad, wscale, so);
-    ++*launches;
-  }
+  const unsigned gb = (unsigned)((n + 255) / 256);
+  if (rbm)
+    k_psort_gather<kRangeBearing><<<gb, 256, 0, s>>>(src, perm, n, wscale, so);
+  else
+    k_psort_gather<kPosIso><<<gb, 256, 0, s>>>(src, perm, n, wscale, so);
+  ++*launches;
   return cudaGetLastError();
 }
 
@@ -717,7 +862,18 @@ cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, fl
 
 cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kbuf, int32_t* vbuf, int32_t* mlist,
                               int32_t* hist, int32_t* scan_tmp, int32_t* mstart, cudaStream_t s, int64_t* launches) {
-  // mstart: per-label counts, exclusive scan (mstart[M] = E)
+  int bits = 1;
+  while ((1 << bits) < M) ++bits;
+  if (bits <= 12 && E > 0) {
+    // one pass: the scanned histogram's first column is the label offsets
+    cudaError_t e = csort_pass(cand, nullptr, E, 0, 1 << bits, hist, scan_tmp, nullptr, mlist, s, launches);
+    if (e != cudaSuccess) return e;
+    const int nblk = (int)((E + kESortBlock - 1) / kESortBlock);
+    k_mstart_from_hist<<<(M + 256) / 256, 256, 0, s>>>(hist, nblk, M, (int32_t)E, mstart);
+    ++*launches;
+    return cudaGetLastError();
+  }
+  // mstart: per-label counts (integer atomics), exclusive scan (mstart[M] = E)
   k_zero_i32<<<(M + 256) / 256, 256, 0, s>>>(mstart, M + 1);
   ++*launches;
   if (E > 0) {
@@ -726,12 +882,7 @@ cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kb
   }
   cudaError_t e = gate_scan(mstart, M, scan_tmp, s, launches);
   if (e != cudaSuccess || E <= 0) return e;
-  // LSD passes of 12 bits over the label
-  int bits = 1;
-  while ((1 << bits) < M) ++bits;
-  if (bits <= 12) {
-    return csort_pass(cand, nullptr, E, 0, 1 << bits, hist, scan_tmp, nullptr, mlist, s, launches);
-  }
+  // two LSD passes of 12 + (bits - 12) bits over the label
   e = csort_pass(cand, nullptr, E, 0, kSortMaxBins, hist, scan_tmp, kbuf, vbuf, s, launches);
   if (e != cudaSuccess) return e;
   return csort_pass(kbuf, vbuf, E, 12, 1 << (bits - 12), hist, scan_tmp, nullptr, mlist, s, launches);
@@ -740,9 +891,9 @@ cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kb
 template <int MODEL>
 static cudaError_t gpass_m(int pass, const GateArgs& g, cudaStream_t s) {
   if (pass == 1)
-    k_gpass<MODEL, 1><<<g.ntiles, 256, 0, s>>>(g);
+    k_gpass<MODEL, 1><<<g.ntiles, kGpThreads, 0, s>>>(g);
   else
-    k_gpass<MODEL, 2><<<g.ntiles, 256, 0, s>>>(g);
+    k_gpass<MODEL, 2><<<g.ntiles, kGpThreads, 0, s>>>(g);
   return cudaGetLastError();
 }
 

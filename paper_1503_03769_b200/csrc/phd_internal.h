@@ -167,7 +167,8 @@ cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, 
 // 2^e flushes to exactly 0 in the dense kernels too (ex2.approx.ftz).
 constexpr int kGateG = 64;            // cells per axis (Morton key of 12 bits)
 constexpr int kGateBins = kGateG * kGateG;
-constexpr int kSortBlock = 8192;      // keys per counting-sort block
+constexpr int kPSortBlock = 65536;    // particles per counting-sort block (8 warps)
+constexpr int kESortBlock = 16384;    // candidate entries per counting-sort block
 constexpr int kSortMaxBins = 4096;    // bins per counting-sort pass (12-bit digits)
 constexpr int kGateTP = 512;          // particles per tile (256 threads x 2, f32x2)
 constexpr int kGateChunk = 256;       // candidates staged in shared memory at a time
@@ -179,13 +180,12 @@ struct GateGrid {
   int wrap1;                          // axis 1 is an angle (range-bearing): cells wrap mod kGateG
 };
 
-// Sorted copy of the particle block: position model c[0..1] = x, y;
-// range-bearing c[0..7] = r_hi, r_lo, thA hi/lo, thB hi/lo, thC hi/lo.
+// Sorted copy of the particle block (n_pad = ntiles * kGateTP entries):
+// range-bearing c[0..7] = r_hi, r_lo, thA hi/lo, thB hi/lo, thC hi/lo (unused: nullptr).
 struct GateSorted {
   float* c[8];
-  float *x, *y, *vx, *vy;             // Cartesian state (pass 2; x, y alias c[0], c[1] for position)
+  float *x, *y, *vx, *vy;             // Cartesian state
   float* lw;                          // log2(p_D c w) (-inf for w = 0 and padding)
-  int32_t* perm;                      // sorted position -> local index
   int32_t* inv;                       // local index -> sorted position
 };
 
@@ -207,8 +207,8 @@ struct GateArgs {
 // key + stable counting sort of the local particles; writes the sorted copy.
 // Launch count added to *launches.
 cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/, const float* rb, int64_t rb_stride,
-                                int64_t n, int64_t n_pad, float wscale, const GateGrid& grid, int32_t* keys,
-                                int32_t* hist, int32_t* scan_tmp, const GateSorted& so, cudaStream_t s,
+                                int64_t n, int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist,
+                                int32_t* scan_tmp, int32_t* perm, const GateSorted& so, cudaStream_t s,
                                 int64_t* launches);
 // measurements -> grid cells (one CTA): zcell_start[kGateBins + 1], items stable by label
 cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,

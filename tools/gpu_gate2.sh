@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_gate.py -x -q > gpurun_out/pytest_gate.log 2>&1; echo gate_tests=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_gate.csv python bench.py --gate 1 --no-gated-leg --steps 3 --no-cpu-baseline > gpurun_out/ncu_gate.log 2>&1; echo ncu=$?

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_gate.py -x -q > gpurun_out/pytest_gate.log 2>&1; echo gate_tests=$?
+timeout 600 python bench.py --gate 1 --no-gated-leg --no-cpu-baseline > gpurun_out/bench_g1.json 2> gpurun_out/bench_g1.err; echo bench=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_gate.csv python bench.py --gate 1 --no-gated-leg --steps 3 --no-cpu-baseline > gpurun_out/ncu_gate.log 2>&1; echo ncu=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_gpass|k_psort_gather|k_gate_tiles" --launch-skip 15 -c 5 -o gpurun_out/gate_full python bench.py --gate 1 --no-gated-leg --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_gfull.log 2>&1; echo ncu2=$?
