@@ -345,7 +345,8 @@ __global__ void __launch_bounds__(256) k_psort_gather(GatherSrc src, const int32
 // measurements -> cells (one CTA of 1024): zcell_start[kGateBins + 1], items
 // stable by label within a cell (warp 0 walks the labels in order)
 __global__ void __launch_bounds__(1024) k_gate_zbin(const float* __restrict__ z, int M, GateGrid g,
-                                                    int32_t* zkey, int32_t* zcell_start, int32_t* zcell_items) {
+                                                    int32_t* zkey, int32_t* zcell_start, int32_t* zcell_items,
+                                                    float2* zcell_z) {
   __shared__ int h[kGateBins];
   __shared__ int sh[33];
   for (int b = threadIdx.x; b < kGateBins; b += blockDim.x) h[b] = 0;
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(1024) k_gate_zbin(const float* __restrict__ z,
       if (ok) {
         if (lane == __ffs(peers) - 1) h[k] += __popc(peers);
         zcell_items[pos] = l;
+        zcell_z[pos] = make_float2(z[2 * l], z[2 * l + 1]);
       }
       __syncwarp();
     }
@@ -395,18 +397,16 @@ __global__ void __launch_bounds__(1024) k_gate_zbin(const float* __restrict__ z,
 // ---------------------------------------------------------------------------
 // per tile (one warp): bounding box in measurement space, max log2(p_D c w),
 // then the candidates: cells of the window in rounds of 32 (lane = cell),
-// measurements of a cell in item order; FILL writes them at tstart[t] in
-// (round, lane, item) order -- deterministic.
-template <bool FILL>
-__global__ void __launch_bounds__(256) k_gate_tiles(int model, const float* __restrict__ c0, const float* __restrict__ c1,
-                                                    const float* __restrict__ lw, int ntiles, float na0, float na1,
-                                                    GateGrid g, const int32_t* __restrict__ zcell_start,
-                                                    const int32_t* __restrict__ zcell_items,
-                                                    const float* __restrict__ z, int32_t* tcount,
-                                                    const int32_t* __restrict__ tstart, int32_t* cand) {
+// measurements of a cell in item order, written in (round, lane, item) order
+// -- deterministic.  The count pass also keeps the first kGateKBuf candidates
+// of every tile, so the fill pass copies them instead of enumerating again.
+constexpr int kGateKBuf = kGateKBufH;
+
+__device__ __forceinline__ int tile_enum(int t, const float* __restrict__ c0, const float* __restrict__ c1,
+                                         const float* __restrict__ lw, float na0, float na1, const GateGrid& g,
+                                         const int32_t* __restrict__ zcell_start, const int32_t* __restrict__ zcell_items,
+                                         const float2* __restrict__ zcell_z, int32_t* dst, int cap) {
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= ntiles) return;
   const int64_t p0 = (int64_t)t * kGateTP;
   float b0 = INFINITY, b1 = -INFINITY, e0 = INFINITY, e1 = -INFINITY, lm = -INFINITY;
   for (int j = lane; j < kGateTP; j += 32) {
@@ -430,67 +430,93 @@ __global__ void __launch_bounds__(256) k_gate_tiles(int model, const float* __re
   }
   const float budget = lm - kGateLog2Min;  // e_max >= -130  <=>  alpha0 dx^2 + alpha1 dy^2 <= budget
   int total = 0;
-  int out = FILL ? tstart[t] : 0;
-  if (budget > 0.0f && isfinite(b0) && isfinite(e0) && isfinite(b1) && isfinite(e1)) {
-    const float R0 = sqrtf(budget / -na0) * 1.0001f + 1e-3f;
-    const float R1 = sqrtf(budget / -na1) * 1.0001f + 1e-6f;
-    const int x0 = clampc(cell_raw(b0 - R0, g.lo0, g.inv_h0)), x1 = clampc(cell_raw(b1 + R0, g.lo0, g.inv_h0));
-    int y0, y1;
-    if (g.wrap1) {
-      y0 = cell_raw(e0 - R1, g.lo1, g.inv_h1) - 1;
-      y1 = cell_raw(e1 + R1, g.lo1, g.inv_h1) + 1;
-      if (y1 - y0 + 1 >= kGateG) {
-        y0 = 0;
-        y1 = kGateG - 1;
-      }
-    } else {
-      y0 = clampc(cell_raw(e0 - R1, g.lo1, g.inv_h1));
-      y1 = clampc(cell_raw(e1 + R1, g.lo1, g.inv_h1));
+  if (!(budget > 0.0f && isfinite(b0) && isfinite(e0) && isfinite(b1) && isfinite(e1))) return 0;
+  const float R0 = sqrtf(budget / -na0) * 1.0001f + 1e-3f;
+  const float R1 = sqrtf(budget / -na1) * 1.0001f + 1e-6f;
+  const int x0 = clampc(cell_raw(b0 - R0, g.lo0, g.inv_h0)), x1 = clampc(cell_raw(b1 + R0, g.lo0, g.inv_h0));
+  int y0, y1;
+  if (g.wrap1) {
+    y0 = cell_raw(e0 - R1, g.lo1, g.inv_h1) - 1;
+    y1 = cell_raw(e1 + R1, g.lo1, g.inv_h1) + 1;
+    if (y1 - y0 + 1 >= kGateG) {
+      y0 = 0;
+      y1 = kGateG - 1;
     }
-    const int nx = x1 - x0 + 1, ny = y1 - y0 + 1;
-    const int nc = nx * ny;
-    for (int r = 0; r < nc; r += 32) {
-      const int ci = r + lane;
-      int cnt = 0, j0 = 0, j1 = 0;
-      if (ci < nc) {
-        const int cx = x0 + ci % nx;
-        int cy = y0 + ci / nx;
-        if (g.wrap1) cy = wrapc(cy);
-        const int key = morton(cx, cy);
-        j0 = zcell_start[key];
-        j1 = zcell_start[key + 1];
-        for (int j = j0; j < j1; ++j) {
-          const int l = zcell_items[j];
-          const float z0 = z[2 * l], z1 = z[2 * l + 1];
-          const float dx = dist_iv(z0, b0, b1);
-          const float dy = g.wrap1 ? dist_arc(z1, e0, e1) : dist_iv(z1, e0, e1);
-          const float em = fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm));
-          if (em >= kGateLog2Min) ++cnt;
-        }
-      }
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (FILL && cnt > 0) {
-        int w = out + incl - cnt;
-        for (int j = j0; j < j1; ++j) {
-          const int l = zcell_items[j];
-          const float z0 = z[2 * l], z1 = z[2 * l + 1];
-          const float dx = dist_iv(z0, b0, b1);
-          const float dy = g.wrap1 ? dist_arc(z1, e0, e1) : dist_iv(z1, e0, e1);
-          const float em = fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm));
-          if (em >= kGateLog2Min) cand[w++] = l;
-        }
-      }
-      const int rt = __shfl_sync(0xffffffffu, incl, 31);
-      out += rt;
-      total += rt;
-    }
+  } else {
+    y0 = clampc(cell_raw(e0 - R1, g.lo1, g.inv_h1));
+    y1 = clampc(cell_raw(e1 + R1, g.lo1, g.inv_h1));
   }
-  if (!FILL && lane == 0) tcount[t] = total;
+  const int nx = x1 - x0 + 1, ny = y1 - y0 + 1;
+  const int nc = nx * ny;
+  for (int r = 0; r < nc; r += 32) {
+    const int ci = r + lane;
+    int j0 = 0, j1 = 0;
+    if (ci < nc) {
+      const int cx = x0 + ci % nx;
+      int cy = y0 + ci / nx;
+      if (g.wrap1) cy = wrapc(cy);
+      const int key = morton(cx, cy);
+      j0 = zcell_start[key];
+      j1 = zcell_start[key + 1];
+    }
+    // pass bits of the (at most 32 first) items of this cell; longer cells loop
+    int cnt = 0;
+    for (int j = j0; j < j1; ++j) {
+      const float2 zz = zcell_z[j];
+      const float dx = dist_iv(zz.x, b0, b1);
+      const float dy = g.wrap1 ? dist_arc(zz.y, e0, e1) : dist_iv(zz.y, e0, e1);
+      cnt += fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm)) >= kGateLog2Min;
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (cnt > 0 && dst != nullptr) {
+      int w = total + incl - cnt;
+      for (int j = j0; j < j1 && w < cap; ++j) {
+        const float2 zz = zcell_z[j];
+        const float dx = dist_iv(zz.x, b0, b1);
+        const float dy = g.wrap1 ? dist_arc(zz.y, e0, e1) : dist_iv(zz.y, e0, e1);
+        if (fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm)) >= kGateLog2Min) dst[w++] = zcell_items[j];
+      }
+    }
+    total += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return total;
+}
+
+// count pass: tcount[t] and the first kGateKBuf candidates in cbuf[t][.]
+__global__ void __launch_bounds__(256) k_gate_count(const float* __restrict__ c0, const float* __restrict__ c1,
+                                                    const float* __restrict__ lw, int ntiles, float na0, float na1,
+                                                    GateGrid g, const int32_t* __restrict__ zcell_start,
+                                                    const int32_t* __restrict__ zcell_items,
+                                                    const float2* __restrict__ zcell_z, int32_t* tcount, int32_t* cbuf) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= ntiles) return;
+  const int total = tile_enum(t, c0, c1, lw, na0, na1, g, zcell_start, zcell_items, zcell_z,
+                              cbuf + (int64_t)t * kGateKBuf, kGateKBuf);
+  if ((threadIdx.x & 31) == 0) tcount[t] = total;
+}
+
+// fill pass: copy the buffered candidates to cand[tstart[t]..]; tiles with more
+// than kGateKBuf candidates enumerate again
+__global__ void __launch_bounds__(256) k_gate_fill(const float* __restrict__ c0, const float* __restrict__ c1,
+                                                   const float* __restrict__ lw, int ntiles, float na0, float na1,
+                                                   GateGrid g, const int32_t* __restrict__ zcell_start,
+                                                   const int32_t* __restrict__ zcell_items,
+                                                   const float2* __restrict__ zcell_z, const int32_t* __restrict__ tstart,
+                                                   const int32_t* __restrict__ cbuf, int32_t* cand) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= ntiles) return;
+  const int e0 = tstart[t], K = tstart[t + 1] - e0;
+  if (K <= kGateKBuf) {
+    for (int j = lane; j < K; j += 32) cand[e0 + j] = cbuf[(int64_t)t * kGateKBuf + j];
+  } else {
+    tile_enum(t, c0, c1, lw, na0, na1, g, zcell_start, zcell_items, zcell_z, cand + e0, 0x7fffffff);
+  }
 }
 
 // per-label entry counts (integer atomics: order-independent)
@@ -838,25 +864,25 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
 }
 
 cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,
-                      int32_t* zcell_items, cudaStream_t s) {
-  k_gate_zbin<<<1, 1024, 0, s>>>(z, M, grid, zkey, zcell_start, zcell_items);
+                      int32_t* zcell_items, float2* zcell_z, cudaStream_t s) {
+  k_gate_zbin<<<1, 1024, 0, s>>>(z, M, grid, zkey, zcell_start, zcell_items, zcell_z);
   return cudaGetLastError();
 }
 
 cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1, const GateGrid& grid,
-                       const int32_t* zcell_start, const int32_t* zcell_items, const float* z_lab, int32_t* tcount,
-                       const int32_t* tstart, int32_t* cand, cudaStream_t s) {
+                       const int32_t* zcell_start, const int32_t* zcell_items, const float2* zcell_z, int32_t* tcount,
+                       const int32_t* tstart, int32_t* cbuf, int32_t* cand, cudaStream_t s) {
   if (ntiles <= 0) return cudaSuccess;
   const bool rbm = model == kRangeBearing;
   const float* c0 = rbm ? so.c[0] : so.x;
   const float* c1 = rbm ? so.c[2] : so.y;
   const unsigned blocks = (unsigned)((ntiles + 7) / 8);
   if (fill)
-    k_gate_tiles<true><<<blocks, 256, 0, s>>>(model, c0, c1, so.lw, ntiles, na0, na1, grid, zcell_start, zcell_items,
-                                              z_lab, tcount, tstart, cand);
+    k_gate_fill<<<blocks, 256, 0, s>>>(c0, c1, so.lw, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z,
+                                       tstart, cbuf, cand);
   else
-    k_gate_tiles<false><<<blocks, 256, 0, s>>>(model, c0, c1, so.lw, ntiles, na0, na1, grid, zcell_start, zcell_items,
-                                               z_lab, tcount, tstart, cand);
+    k_gate_count<<<blocks, 256, 0, s>>>(c0, c1, so.lw, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z,
+                                        tcount, cbuf);
   return cudaGetLastError();
 }
 

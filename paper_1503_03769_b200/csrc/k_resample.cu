@@ -57,12 +57,21 @@ __global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
   const int64_t nb = (a.n_local + kBlockW - 1) / kBlockW;
   double w4[4];
   double tsum = 0.0;
+  if (base + 4 * tid + 3 < a.n_local) {  // 16-byte load (base is a multiple of kBlockW)
+    const float4 q = *reinterpret_cast<const float4*>(a.w + base + 4 * tid);
+    w4[0] = (double)q.x;
+    w4[1] = (double)q.y;
+    w4[2] = (double)q.z;
+    w4[3] = (double)q.w;
+  } else {
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    int64_t i = base + 4 * tid + m;
-    w4[m] = i < a.n_local ? (double)a.w[i] : 0.0;
-    tsum += w4[m];
+    for (int m = 0; m < 4; ++m) {
+      int64_t i = base + 4 * tid + m;
+      w4[m] = i < a.n_local ? (double)a.w[i] : 0.0;
+    }
   }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) tsum += w4[m];
   // block exclusive scan of thread sums: warp shuffle + smem over warps
   double incl = tsum;
 #pragma unroll
@@ -218,10 +227,19 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ mark
     }
   } else {
     int m = -1;
+    const int64_t j0 = base + 4 * tid;
+    if (j0 + 3 < n) {  // 16-byte load (base is a multiple of kBlockOff)
+      const int4 q = *reinterpret_cast<const int4*>(marks + j0);
+      a4[0] = q.x;
+      a4[1] = q.y;
+      a4[2] = q.z;
+      a4[3] = q.w;
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a4[r] = j0 + r < n ? marks[j0 + r] : -1;
+    }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      int64_t j = base + 4 * tid + r;
-      a4[r] = j < n ? marks[j] : -1;
       m = max(m, a4[r]);
       a4[r] = m;  // thread-local inclusive running max
     }
@@ -235,9 +253,32 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ mark
 #pragma unroll
     for (int r = 0; r < 4; ++r) a4[r] = max(a4[r], carry);
   }
+  const int64_t j0 = base + 4 * tid;
+  if (j0 + 3 < n) {  // 16-byte stores of four consecutive offspring
+    float4 X, VX, Y, VY;
+    float* px = &X.x;
+    float* pvx = &VX.x;
+    float* py = &Y.x;
+    float* pvy = &VY.x;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t l = (int64_t)a4[r] - g0;
+      px[r] = __ldg(x + l);
+      pvx[r] = __ldg(vx + l);
+      py[r] = __ldg(y + l);
+      pvy[r] = __ldg(vy + l);
+    }
+    *reinterpret_cast<float4*>(ox + j0) = X;
+    *reinterpret_cast<float4*>(ovx + j0) = VX;
+    *reinterpret_cast<float4*>(oy + j0) = Y;
+    *reinterpret_cast<float4*>(ovy + j0) = VY;
+    *reinterpret_cast<float4*>(ow + j0) = make_float4(w_off, w_off, w_off, w_off);
+    *reinterpret_cast<int4*>(anc + j0) = make_int4(a4[0], a4[1], a4[2], a4[3]);
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    int64_t j = base + 4 * tid + r;
+    int64_t j = j0 + r;
     if (j >= n) break;
     int64_t l = (int64_t)a4[r] - g0;
     ox[j] = x[l];

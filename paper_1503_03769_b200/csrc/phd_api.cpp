@@ -45,7 +45,7 @@ struct Layout {
   int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
   int g_ntiles = 0, g_nsorted = 0;
   size_t o_gperm, o_ginv, o_gsorted[13], o_gPs, o_ghist, o_gscan, o_gtstart, o_gcand, o_gk, o_gv, o_gmlist,
-      o_gpart1, o_gpart2, o_gmstart, o_gzkey, o_gzstart, o_gzitems, o_gA;
+      o_gpart1, o_gpart2, o_gmstart, o_gzkey, o_gzstart, o_gzitems, o_gzz, o_gcbuf, o_gA;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -124,6 +124,8 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_gzkey = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 1));
   L.o_gzstart = gtake(sizeof(int32_t) * (kGateBins + 1));
   L.o_gzitems = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 1));
+  L.o_gzz = gtake(sizeof(float) * 2 * ((size_t)p->max_meas + 1));
+  L.o_gcbuf = gtake(sizeof(int32_t) * (size_t)L.g_ntiles * kGateKBufH);
   L.o_gA = gtake(sizeof(double) * 4 * (size_t)L.slots_max);
   L.total = off;
   return L;
@@ -203,7 +205,8 @@ struct phd_ctx {
   GateGrid ggrid{};
   int32_t *gperm = nullptr, *ghist = nullptr, *gscan = nullptr, *gtstart = nullptr, *gcand = nullptr, *gk = nullptr,
           *gv = nullptr, *gmlist = nullptr, *gmstart = nullptr, *gzkey = nullptr, *gzstart = nullptr,
-          *gzitems = nullptr;
+          *gzitems = nullptr, *gcbuf = nullptr;
+  float2* gzz = nullptr;
   float *gPs = nullptr, *gpart2 = nullptr;
   double *gpart1 = nullptr, *gA = nullptr;
   bool gated = false;            // the last update ran the gated path
@@ -534,6 +537,8 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
     c->gzkey = at<int32_t>(c->ws, L.o_gzkey);
     c->gzstart = at<int32_t>(c->ws, L.o_gzstart);
     c->gzitems = at<int32_t>(c->ws, L.o_gzitems);
+    c->gzz = at<float2>(c->ws, L.o_gzz);
+    c->gcbuf = at<int32_t>(c->ws, L.o_gcbuf);
     c->gA = at<double>(c->ws, L.o_gA);
     if (p->meas == PHD_MEAS_RANGE_BEARING) {
       c->ggrid.lo0 = (float)p->region[0];
@@ -887,11 +892,11 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   const float* A[5] = {c->A[0], c->A[1], c->A[2], c->A[3], c->A[4]};
   CU(gate_sort_particles(c->model, A, c->rb, c->L.cap_l, n, npad, c->wscale, c->ggrid, c->ghist, c->gscan,
                          c->gperm, c->gso, c->st, &c->launches));
-  KL(gate_zbin(c->zlab, M, c->ggrid, c->gzkey, c->gzstart, c->gzitems, c->st));
+  KL(gate_zbin(c->zlab, M, c->ggrid, c->gzkey, c->gzstart, c->gzitems, c->gzz, c->st));
   int64_t tot = 0;
   if (ntiles > 0) {
-    KL(gate_tiles(0, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->zlab, c->gtstart,
-                  nullptr, nullptr, c->st));
+    KL(gate_tiles(0, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->gzz, c->gtstart,
+                  nullptr, c->gcbuf, nullptr, c->st));
     CU(gate_scan(c->gtstart, ntiles, c->gscan, c->st, &c->launches));
     int32_t* h = reinterpret_cast<int32_t*>(c->h_meta + 3 * c->world + 40);
     CU(cudaMemcpyAsync(h, c->gtstart + ntiles, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
@@ -1002,8 +1007,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     // candidate lists, entries grouped by label, then the two gated passes
     const int ntiles = (int)c->g_tiles;
     if (ntiles > 0)
-      KL(gate_tiles(1, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->zlab, nullptr,
-                    c->gtstart, c->gcand, c->st));
+      KL(gate_tiles(1, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->gzz, nullptr,
+                    c->gtstart, c->gcbuf, c->gcand, c->st));
     CU(gate_sort_entries(c->gcand, c->g_entries, M, c->gk, c->gv, c->gmlist, c->ghist, c->gscan, c->gmstart, c->st,
                          &c->launches));
     GateArgs ga{};

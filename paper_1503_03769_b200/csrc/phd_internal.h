@@ -212,11 +212,14 @@ cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/
                                 int64_t* launches);
 // measurements -> grid cells (one CTA): zcell_start[kGateBins + 1], items stable by label
 cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,
-                      int32_t* zcell_items, cudaStream_t s);
+                      int32_t* zcell_items, float2* zcell_z, cudaStream_t s);
 // per-tile bounding boxes + candidate counts (fill = 0) or labels (fill = 1)
+// (fill = 0 also buffers the first kGateKBuf candidates per tile in cbuf [ntiles][kGateKBuf])
+constexpr int kGateKBufH = 256;
 cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1,
                        const GateGrid& grid, const int32_t* zcell_start, const int32_t* zcell_items,
-                       const float* z_lab, int32_t* tcount, const int32_t* tstart, int32_t* cand, cudaStream_t s);
+                       const float2* zcell_z, int32_t* tcount, const int32_t* tstart, int32_t* cbuf, int32_t* cand,
+                       cudaStream_t s);
 // exclusive scan of n int32 (in place); out[n] = total.  tmp >= ceil(n / 4096) + 1 ints.
 cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64_t* launches);
 // stable sort of the E candidate entries by label: mlist = entry indices grouped by
