@@ -64,6 +64,29 @@ __device__ __forceinline__ int cell_key(float v0, float v1, const GateGrid& g) {
   return morton(c0, c1);
 }
 
+// Lanes of the warp holding the same NBITS-bit digit d, among the lanes with
+// ok set: one ballot per bit (MATCH.ANY has a much lower throughput).
+template <int NBITS>
+__device__ __forceinline__ unsigned match_digit(int d, bool ok) {
+  unsigned m = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+  for (int b = 0; b < NBITS; ++b) {
+    const bool bit = (d >> b) & 1;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bal : ~bal;
+  }
+  return m;
+}
+__device__ __forceinline__ unsigned match_digit_rt(int d, bool ok, int nbits) {
+  unsigned m = __ballot_sync(0xffffffffu, ok);
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (d >> b) & 1;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bal : ~bal;
+  }
+  return m;
+}
+
 // distance from v to [a, b]
 __device__ __forceinline__ float dist_iv(float v, float a, float b) { return fmaxf(0.0f, fmaxf(a - v, v - b)); }
 // distance from the angle v (any real, e.g. fp32(pi) > pi) to the arc [a, b]
@@ -240,6 +263,8 @@ __global__ void __launch_bounds__(256) k_ms_scatter(KF kf, int64_t n, int64_t pe
   __syncthreads();
   // 3. stable ranking of the warp's slice
   const unsigned lt = (1u << lane) - 1u;
+  int nbits = 1;
+  while ((1 << nbits) < nbins) ++nbits;
   for (int64_t b0 = w0; b0 < w1; b0 += 32 * kMsRows) {
     int32_t raw[kMsRows];
     int32_t val[kMsRows];
@@ -252,8 +277,8 @@ __global__ void __launch_bounds__(256) k_ms_scatter(KF kf, int64_t n, int64_t pe
 #pragma unroll
     for (int r = 0; r < kMsRows; ++r) {
       const bool ok = b0 + r * 32 + lane < w1;
-      const int d = ok ? kf.digit(raw[r]) : nbins + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const int d = ok ? kf.digit(raw[r]) : 0;
+      const unsigned peers = match_digit_rt(d, ok, nbits);
       int pos = 0;
       if (ok) pos = base[d] + (int)((my[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) + __popc(peers & lt);
       __syncwarp();
@@ -296,49 +321,99 @@ cudaError_t csort_pass(const int32_t* keys, const int32_t* vals, int64_t n, int 
 }
 
 // ---------------------------------------------------------------------------
-// Particle sort, fused: k_psort_hist computes each particle's cell key from its
-// coordinates (position (x, y); range-bearing (r_hi, thetaA_hi)) into the
-// per-block histograms; k_psort_scatter recomputes the key, ranks it stably
-// and writes the particle straight into the sorted copy (+ inv), loads
-// software-pipelined kPsB warps-rows deep.  Padding [n, n_pad) gets zero state
-// and lw = -inf.
+// Particle sort.  k_ms_hist<KeyCell> counts the cells; k_psort_scatter ranks
+// each particle stably (as k_ms_scatter) and writes it, read coalesced in the
+// filter's order, as one whole record to its sorted slot: 32 bytes (position)
+// or 64 bytes (range-bearing), i.e. full sectors, never partial-sector writes;
+// inv[i] = sorted slot is written coalesced.
 struct GatherSrc {
   const float* c[8];
   const float *x, *y, *vx, *vy, *w;
 };
 
-// padding of the sorted copy: positions [n, n_pad) get zero state and lw = -inf
-__global__ void k_psort_pad(int64_t n, int64_t n_pad, int model, GateSorted so) {
+// padding records [n, n_pad): zero state, lw = -inf
+__global__ void k_psort_pad(int64_t n, int64_t n_pad, GateSorted so) {
   const int64_t p = n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pad) return;
-  if (model == kRangeBearing) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) so.c[c][p] = 0.0f;
-  }
-  so.x[p] = 0.0f;
-  so.y[p] = 0.0f;
-  so.vx[p] = 0.0f;
-  so.vy[p] = 0.0f;
-  so.lw[p] = -INFINITY;
+  float4* r = so.rec + p * so.n4;
+  for (int k = 0; k < so.n4 - 1; ++k) r[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  r[so.n4 - 1] = make_float4(-INFINITY, 0.0f, 0.0f, 0.0f);
 }
 
-// sorted copy (coalesced writes, gathered reads) + inv
 template <int MODEL>
-__global__ void __launch_bounds__(256) k_psort_gather(GatherSrc src, const int32_t* __restrict__ perm, int64_t n,
-                                                      float wscale, GateSorted so) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int i = perm[p];
-  if (MODEL == kRangeBearing) {
+__global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, KeyCell kf, int64_t n, int nblk,
+                                                       const int32_t* __restrict__ hs, float wscale, GateSorted so) {
+  constexpr bool RB = MODEL == kRangeBearing;
+  constexpr int N4 = RB ? 4 : 2;
+  constexpr int ROWS = RB ? 2 : 4;
+  constexpr int nbins = kGateBins, nw = kGateBins / 2;
+  extern __shared__ uint32_t sm[];
+  uint32_t* wh = sm;
+  int* base = reinterpret_cast<int*>(sm + kMsWarps * nw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < kMsWarps * nw; j += blockDim.x) wh[j] = 0u;
+  __syncthreads();
+  const int64_t i0 = (int64_t)blockIdx.x * kPSortBlock;
+  const int64_t i1 = min(n, i0 + (int64_t)kPSortBlock);
+  const int64_t pw = kPSortBlock / kMsWarps;
+  const int64_t w0 = min(i1, i0 + warp * pw), w1 = min(i1, w0 + pw);
+  uint32_t* my = wh + warp * nw;
+  // 1. per-warp sub-histograms
+  for (int64_t b0 = w0; b0 < w1; b0 += 32 * kMsRows) {
+    int32_t key[kMsRows];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) so.c[c][p] = __ldg(src.c[c] + i);
+    for (int r = 0; r < kMsRows; ++r) key[r] = kf.raw(min(b0 + r * 32 + lane, w1 - 1));
+#pragma unroll
+    for (int r = 0; r < kMsRows; ++r)
+      if (b0 + r * 32 + lane < w1) atomicAdd(&my[key[r] >> 1], 1u << (16 * (key[r] & 1)));
   }
-  so.x[p] = __ldg(src.x + i);
-  so.y[p] = __ldg(src.y + i);
-  so.vx[p] = __ldg(src.vx + i);
-  so.vy[p] = __ldg(src.vy + i);
-  so.lw[p] = log2f(__ldg(src.w + i) * wscale);  // the dense TileLoader's exact expression
-  so.inv[i] = (int32_t)p;
+  __syncthreads();
+  // 2. exclusive prefix over the warps of every cell; block offsets
+  for (int j = tid; j < nw; j += blockDim.x) {
+    uint32_t run = 0u;
+#pragma unroll
+    for (int w = 0; w < kMsWarps; ++w) {
+      const uint32_t c = wh[w * nw + j];
+      wh[w * nw + j] = run;
+      run += c;
+    }
+    base[2 * j] = hs[(int64_t)(2 * j) * nblk + blockIdx.x];
+    base[2 * j + 1] = hs[(int64_t)(2 * j + 1) * nblk + blockIdx.x];
+  }
+  __syncthreads();
+  // 3. rank and write the records
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t b0 = w0; b0 < w1; b0 += 32 * ROWS) {
+    float4 q[ROWS][N4];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int64_t i = min(b0 + r * 32 + lane, w1 - 1);
+      if (RB) {
+        q[r][0] = make_float4(__ldg(src.c[0] + i), __ldg(src.c[1] + i), __ldg(src.c[2] + i), __ldg(src.c[3] + i));
+        q[r][1] = make_float4(__ldg(src.c[4] + i), __ldg(src.c[5] + i), __ldg(src.c[6] + i), __ldg(src.c[7] + i));
+      }
+      q[r][N4 - 2] = make_float4(__ldg(src.x + i), __ldg(src.y + i), __ldg(src.vx + i), __ldg(src.vy + i));
+      q[r][N4 - 1] = make_float4(log2f(__ldg(src.w + i) * wscale), 0.0f, 0.0f, 0.0f);  // the dense TileLoader's expression
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int64_t i = b0 + r * 32 + lane;
+      const bool ok = i < w1;
+      const int d = ok ? (RB ? cell_key(q[r][0].x, q[r][0].z, kf.g) : cell_key(q[r][0].x, q[r][0].y, kf.g)) : 0;
+      const unsigned peers = match_digit<12>(d, ok);
+      int pos = 0;
+      if (ok) pos = base[d] + (int)((my[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) + __popc(peers & lt);
+      __syncwarp();
+      if (ok) {
+        if (lane == __ffs(peers) - 1) atomicAdd(&my[d >> 1], (uint32_t)__popc(peers) << (16 * (d & 1)));
+        float4* dst = so.rec + (int64_t)pos * N4;
+#pragma unroll
+        for (int k = 0; k < N4; ++k) dst[k] = q[r][k];
+        so.inv[i] = pos;
+      }
+      __syncwarp();
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -402,17 +477,26 @@ __global__ void __launch_bounds__(1024) k_gate_zbin(const float* __restrict__ z,
 // of every tile, so the fill pass copies them instead of enumerating again.
 constexpr int kGateKBuf = kGateKBufH;
 
-__device__ __forceinline__ int tile_enum(int t, const float* __restrict__ c0, const float* __restrict__ c1,
-                                         const float* __restrict__ lw, float na0, float na1, const GateGrid& g,
+// the tile kernels' view of the sorted records: c0, c1 (measurement-space
+// coordinates) and lw of record p at [p * stride]
+struct RecView {
+  const float* c0;
+  const float* c1;
+  const float* lw;
+  int stride;
+};
+
+__device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, float na1, const GateGrid& g,
                                          const int32_t* __restrict__ zcell_start, const int32_t* __restrict__ zcell_items,
                                          const float2* __restrict__ zcell_z, int32_t* dst, int cap) {
   const int lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)t * kGateTP;
   float b0 = INFINITY, b1 = -INFINITY, e0 = INFINITY, e1 = -INFINITY, lm = -INFINITY;
   for (int j = lane; j < kGateTP; j += 32) {
-    const float l = lw[p0 + j];
+    const int64_t o = (p0 + j) * rv.stride;
+    const float l = __ldg(rv.lw + o);
     if (l > -INFINITY) {  // zero-weight particles and padding contribute nothing
-      const float v0 = c0[p0 + j], v1 = c1[p0 + j];
+      const float v0 = __ldg(rv.c0 + o), v1 = __ldg(rv.c1 + o);
       b0 = fminf(b0, v0);
       b1 = fmaxf(b1, v0);
       e0 = fminf(e0, v1);
@@ -488,22 +572,20 @@ __device__ __forceinline__ int tile_enum(int t, const float* __restrict__ c0, co
 }
 
 // count pass: tcount[t] and the first kGateKBuf candidates in cbuf[t][.]
-__global__ void __launch_bounds__(256) k_gate_count(const float* __restrict__ c0, const float* __restrict__ c1,
-                                                    const float* __restrict__ lw, int ntiles, float na0, float na1,
+__global__ void __launch_bounds__(256) k_gate_count(const RecView rv, int ntiles, float na0, float na1,
                                                     GateGrid g, const int32_t* __restrict__ zcell_start,
                                                     const int32_t* __restrict__ zcell_items,
                                                     const float2* __restrict__ zcell_z, int32_t* tcount, int32_t* cbuf) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
-  const int total = tile_enum(t, c0, c1, lw, na0, na1, g, zcell_start, zcell_items, zcell_z,
+  const int total = tile_enum(t, rv, na0, na1, g, zcell_start, zcell_items, zcell_z,
                               cbuf + (int64_t)t * kGateKBuf, kGateKBuf);
   if ((threadIdx.x & 31) == 0) tcount[t] = total;
 }
 
 // fill pass: copy the buffered candidates to cand[tstart[t]..]; tiles with more
 // than kGateKBuf candidates enumerate again
-__global__ void __launch_bounds__(256) k_gate_fill(const float* __restrict__ c0, const float* __restrict__ c1,
-                                                   const float* __restrict__ lw, int ntiles, float na0, float na1,
+__global__ void __launch_bounds__(256) k_gate_fill(const RecView rv, int ntiles, float na0, float na1,
                                                    GateGrid g, const int32_t* __restrict__ zcell_start,
                                                    const int32_t* __restrict__ zcell_items,
                                                    const float2* __restrict__ zcell_z, const int32_t* __restrict__ tstart,
@@ -515,7 +597,7 @@ __global__ void __launch_bounds__(256) k_gate_fill(const float* __restrict__ c0,
   if (K <= kGateKBuf) {
     for (int j = lane; j < K; j += 32) cand[e0 + j] = cbuf[(int64_t)t * kGateKBuf + j];
   } else {
-    tile_enum(t, c0, c1, lw, na0, na1, g, zcell_start, zcell_items, zcell_z, cand + e0, 0x7fffffff);
+    tile_enum(t, rv, na0, na1, g, zcell_start, zcell_items, zcell_z, cand + e0, 0x7fffffff);
   }
 }
 
@@ -554,39 +636,44 @@ struct GPair {
 template <int MODEL, int PASS>
 __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS == 2) ? 5 : 8) k_gpass(const GateArgs g) {
   constexpr bool RB = MODEL == kRangeBearing;
-  __shared__ float2 zn[kGateChunk];          // (-z0, -z1)
-  __shared__ float zd[kGateChunk];           // 1 / (kappa + C)          (pass 2)
-  __shared__ int zr[kGateChunk];             // bearing representation   (range-bearing)
-  __shared__ float2 zc[kGateChunk];          // -(Cartesian centre)      (range-bearing, pass 2)
-  __shared__ int zi[kGateChunk];             // chunk-local entry index  (pass 2: selected first)
+  // + 2: pass 2 pads an odd selected count with one sentinel candidate
+  __shared__ float2 zn[kGateChunk + 2];      // (-z0, -z1)
+  __shared__ float zd[kGateChunk + 2];       // 1 / (kappa + C)          (pass 2)
+  __shared__ int zr[kGateChunk + 2];         // bearing representation   (range-bearing)
+  __shared__ float2 zc[kGateChunk + 2];      // -(Cartesian centre)      (range-bearing, pass 2)
+  __shared__ int zi[kGateChunk + 2];         // chunk-local entry index  (pass 2: selected first)
   __shared__ int wcnt[kGpWarps + 1];
   __shared__ float wpart[PASS == 1 ? kGpWarps : 1][PASS == 1 ? kGateChunk : 1];   // pass 1: per-warp sums
-  __shared__ float4 wq[PASS == 2 ? kGpWarps : 1][PASS == 2 ? kGateChunk : 1];     // pass 2: per-warp state sums
+  __shared__ float4 wq[PASS == 2 ? kGpWarps : 1][PASS == 2 ? kGateChunk + 2 : 1];     // pass 2: per-warp state sums
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = blockIdx.x;
   const float2 na0 = f2(g.na0, g.na0), na1 = f2(g.na1, g.na1);
   GPair<MODEL> P[2];
+  constexpr int N4 = RB ? 4 : 2;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t pa = (int64_t)t * kGateTP + 256 * h + tid, pb = pa + 128;
-    P[h].LW = f2(g.so.lw[pa], g.so.lw[pb]);
+    const float4* ra = g.so.rec + pa * N4;
+    const float4* rbp = g.so.rec + pb * N4;
+    P[h].LW = f2(__ldg(ra + N4 - 1).x, __ldg(rbp + N4 - 1).x);
     if (RB) {
-      P[h].R_hi = f2(g.so.c[0][pa], g.so.c[0][pb]);
-      P[h].R_lo = f2(g.so.c[1][pa], g.so.c[1][pb]);
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        P[h].T_hi[r] = f2(g.so.c[2 + 2 * r][pa], g.so.c[2 + 2 * r][pb]);
-        P[h].T_lo[r] = f2(g.so.c[3 + 2 * r][pa], g.so.c[3 + 2 * r][pb]);
-      }
+      const float4 a0 = __ldg(ra), b0 = __ldg(rbp), a1 = __ldg(ra + 1), b1 = __ldg(rbp + 1);
+      P[h].R_hi = f2(a0.x, b0.x);
+      P[h].R_lo = f2(a0.y, b0.y);
+      P[h].T_hi[0] = f2(a0.z, b0.z);
+      P[h].T_lo[0] = f2(a0.w, b0.w);
+      P[h].T_hi[1] = f2(a1.x, b1.x);
+      P[h].T_lo[1] = f2(a1.y, b1.y);
+      P[h].T_hi[2] = f2(a1.z, b1.z);
+      P[h].T_lo[2] = f2(a1.w, b1.w);
     }
     if (!RB || PASS == 2) {
-      P[h].X = f2(g.so.x[pa], g.so.x[pb]);
-      P[h].Y = f2(g.so.y[pa], g.so.y[pb]);
-    }
-    if (PASS == 2) {
-      P[h].VX = f2(g.so.vx[pa], g.so.vx[pb]);
-      P[h].VY = f2(g.so.vy[pa], g.so.vy[pb]);
+      const float4 a = __ldg(ra + N4 - 2), b = __ldg(rbp + N4 - 2);
+      P[h].X = f2(a.x, b.x);
+      P[h].Y = f2(a.y, b.y);
+      P[h].VX = f2(a.z, b.z);
+      P[h].VY = f2(a.w, b.w);
     }
   }
   const int e0 = g.tstart[t];
@@ -613,7 +700,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
     const int cl = min(kGateChunk, K - cb);
     const int cl8 = (cl + 7) & ~7;
     __syncthreads();  // previous chunk fully consumed
-    int nsel = 0;
+    int nsel = 0, base_sel_unpadded = 0;
     if (PASS == 1) {
       for (int k = tid; k < cl8; k += kGpThreads) {
         if (k < cl) {
@@ -656,8 +743,13 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
         __syncthreads();
       }
       nsel = base_sel;
+      base_sel_unpadded = base_sel;
+      // an odd selected count is padded with one sentinel candidate (every term
+      // exactly 0, zi = -1: never written), so the selected loop runs in pairs
+      const int nsel2 = (nsel + 1) & ~1;
+      if (tid == 0 && nsel2 > nsel) zi[nsel] = -1;
       // second sweep: the unselected after the selected, in order
-      int base_un = nsel;
+      int base_un = nsel2;
       for (int k0 = 0; k0 < cl; k0 += kGpThreads) {
         const int k = k0 + tid;
         int fl = 0;
@@ -682,8 +774,18 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
         base_un += wcnt[kGpWarps];
         __syncthreads();
       }
-      for (int pos = tid; pos < cl; pos += kGpThreads) {
-        const int l = g.cand[e0 + cb + zi[pos]];
+      for (int pos = tid; pos < cl + (nsel2 - nsel); pos += kGpThreads) {
+        const int ki = zi[pos];
+        if (ki < 0) {  // sentinel
+          zn[pos] = f2(-1e30f, -1e30f);
+          zd[pos] = 0.0f;
+          if (RB) {
+            zr[pos] = 0;
+            zc[pos] = f2(0.0f, 0.0f);
+          }
+          continue;
+        }
+        const int l = g.cand[e0 + cb + ki];
         zn[pos] = f2(g.sc.s0[l], g.sc.s1[l]);
         zd[pos] = g.sc.d[l];
         if (RB) {
@@ -691,6 +793,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
           zc[pos] = f2(g.sc.s2[l], g.sc.s3[l]);
         }
       }
+      nsel = nsel2;
     }
     __syncthreads();
 
@@ -720,7 +823,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int kk = k + hh;
-          if (kk < nsel) {
+          {
             float2 a0 = f2(0.0f, 0.0f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -741,17 +844,16 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
             v[4 * hh + 1] = a1.x + a1.y;
             v[4 * hh + 2] = a2.x + a2.y;
             v[4 * hh + 3] = a3.x + a3.y;
-          } else {
-            v[4 * hh + 0] = v[4 * hh + 1] = v[4 * hh + 2] = v[4 * hh + 3] = 0.0f;
           }
         }
         const float r = transpose_reduce8(v, lane);
         const int q = lane >> 2;  // value index 0..7: candidate k + q / 4, quantity q % 4
-        if ((lane & 3) == 0 && k + (q >> 2) < nsel) reinterpret_cast<float*>(&wq[warp][k + (q >> 2)])[q & 3] = r;
+        if ((lane & 3) == 0) reinterpret_cast<float*>(&wq[warp][k + (q >> 2)])[q & 3] = r;
       }
       // the rest: weights only
+      const int kend = cl + (nsel - base_sel_unpadded);
 #pragma unroll 2
-      for (int k = nsel; k < cl; ++k) {
+      for (int k = nsel; k < kend; ++k) {
         const float2 dk = f2(zd[k], zd[k]);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -761,6 +863,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
       }
       __syncthreads();
       for (int k = tid; k < nsel; k += kGpThreads) {
+        if (zi[k] < 0) continue;  // sentinel
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int w = 0; w < kGpWarps; ++w) {
@@ -837,16 +940,14 @@ cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64
 
 cudaError_t gate_sort_particles(int model, const float* const* A, const float* rb, int64_t rb_stride, int64_t n,
                                 int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
-                                int32_t* perm, const GateSorted& so, cudaStream_t s, int64_t* launches) {
+                                const GateSorted& so, cudaStream_t s, int64_t* launches) {
   const bool rbm = model == kRangeBearing;
   if (n_pad > n) {
-    k_psort_pad<<<(unsigned)((n_pad - n + 255) / 256), 256, 0, s>>>(n, n_pad, model, so);
+    k_psort_pad<<<(unsigned)((n_pad - n + 255) / 256), 256, 0, s>>>(n, n_pad, so);
     ++*launches;
   }
   if (n <= 0) return cudaGetLastError();
   KeyCell kf{rbm ? rb : A[0], rbm ? rb + 2 * rb_stride : A[2], grid};
-  cudaError_t e = ms_pass(kf, nullptr, n, kPSortBlock, kGateBins, hist, scan_tmp, nullptr, perm, s, launches);
-  if (e != cudaSuccess) return e;
   GatherSrc src{};
   for (int c = 0; c < 8; ++c) src.c[c] = rbm ? rb + c * rb_stride : nullptr;
   src.x = A[0];
@@ -854,11 +955,22 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
   src.y = A[2];
   src.vy = A[3];
   src.w = A[4];
-  const unsigned gb = (unsigned)((n + 255) / 256);
+  const int nblk = (int)((n + kPSortBlock - 1) / kPSortBlock);
+  const size_t smem = sizeof(uint32_t) * (size_t)kMsWarps * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_psort_scatter<kRangeBearing>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_psort_scatter<kPosIso>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_ms_hist<KeyCell><<<nblk, 256, 0, s>>>(kf, n, kPSortBlock, kGateBins, nblk, hist);
+  ++*launches;
+  cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);
+  if (e != cudaSuccess) return e;
   if (rbm)
-    k_psort_gather<kRangeBearing><<<gb, 256, 0, s>>>(src, perm, n, wscale, so);
+    k_psort_scatter<kRangeBearing><<<nblk, 256, smem, s>>>(src, kf, n, nblk, hist, wscale, so);
   else
-    k_psort_gather<kPosIso><<<gb, 256, 0, s>>>(src, perm, n, wscale, so);
+    k_psort_scatter<kPosIso><<<nblk, 256, smem, s>>>(src, kf, n, nblk, hist, wscale, so);
   ++*launches;
   return cudaGetLastError();
 }
@@ -874,15 +986,14 @@ cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, fl
                        const int32_t* tstart, int32_t* cbuf, int32_t* cand, cudaStream_t s) {
   if (ntiles <= 0) return cudaSuccess;
   const bool rbm = model == kRangeBearing;
-  const float* c0 = rbm ? so.c[0] : so.x;
-  const float* c1 = rbm ? so.c[2] : so.y;
+  const float* f = reinterpret_cast<const float*>(so.rec);
+  RecView rv{f, f + (rbm ? 2 : 1), f + 4 * (so.n4 - 1), 4 * so.n4};
   const unsigned blocks = (unsigned)((ntiles + 7) / 8);
   if (fill)
-    k_gate_fill<<<blocks, 256, 0, s>>>(c0, c1, so.lw, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z,
-                                       tstart, cbuf, cand);
+    k_gate_fill<<<blocks, 256, 0, s>>>(rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tstart, cbuf,
+                                       cand);
   else
-    k_gate_count<<<blocks, 256, 0, s>>>(c0, c1, so.lw, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z,
-                                        tcount, cbuf);
+    k_gate_count<<<blocks, 256, 0, s>>>(rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tcount, cbuf);
   return cudaGetLastError();
 }
 

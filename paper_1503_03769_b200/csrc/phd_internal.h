@@ -180,12 +180,13 @@ struct GateGrid {
   int wrap1;                          // axis 1 is an angle (range-bearing): cells wrap mod kGateG
 };
 
-// Sorted copy of the particle block (n_pad = ntiles * kGateTP entries):
-// range-bearing c[0..7] = r_hi, r_lo, thA hi/lo, thB hi/lo, thC hi/lo (unused: nullptr).
+// Sorted copy of the particle block (n_pad = ntiles * kGateTP records of n4 float4):
+//   position      (x, y, vx, vy), (lw, 0, 0, 0)
+//   range-bearing (r_hi, r_lo, thA hi, thA lo), (thB hi, thB lo, thC hi, thC lo), (x, y, vx, vy), (lw, 0, 0, 0)
+// with lw = log2(p_D c w) (-inf for w = 0 and padding).
 struct GateSorted {
-  float* c[8];
-  float *x, *y, *vx, *vy;             // Cartesian state
-  float* lw;                          // log2(p_D c w) (-inf for w = 0 and padding)
+  float4* rec;
+  int n4;
   int32_t* inv;                       // local index -> sorted position
 };
 
@@ -208,14 +209,13 @@ struct GateArgs {
 // Launch count added to *launches.
 cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/, const float* rb, int64_t rb_stride,
                                 int64_t n, int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist,
-                                int32_t* scan_tmp, int32_t* perm, const GateSorted& so, cudaStream_t s,
-                                int64_t* launches);
+                                int32_t* scan_tmp, const GateSorted& so, cudaStream_t s, int64_t* launches);
 // measurements -> grid cells (one CTA): zcell_start[kGateBins + 1], items stable by label
 cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,
                       int32_t* zcell_items, float2* zcell_z, cudaStream_t s);
 // per-tile bounding boxes + candidate counts (fill = 0) or labels (fill = 1)
 // (fill = 0 also buffers the first kGateKBuf candidates per tile in cbuf [ntiles][kGateKBuf])
-constexpr int kGateKBufH = 256;
+constexpr int kGateKBufH = 512;
 cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1,
                        const GateGrid& grid, const int32_t* zcell_start, const int32_t* zcell_items,
                        const float2* zcell_z, int32_t* tcount, const int32_t* tstart, int32_t* cbuf, int32_t* cand,
