@@ -921,17 +921,20 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (M > 0 && !z) return fail(c, PHD_EINVAL, "z is NULL");
   timing_record(c, 2);
   c->M = M;
+  bool h_z_valid = true;
   if (M > 0) {
     cudaPointerAttributes pa{};
     bool dev = cudaPointerGetAttributes(&pa, z) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
     cudaGetLastError();
     if (dev) {
-      CU(cudaMemcpyAsync(c->h_z, z, sizeof(float) * 2 * M, cudaMemcpyDeviceToHost, c->st));
-      CU(cudaStreamSynchronize(c->st));
+      // device-resident Z: stays on the device (no host round trip) unless the
+      // dense range-bearing slot layout needs it on the host (build_slots)
+      CU(cudaMemcpyAsync(c->zlab, z, sizeof(float) * 2 * M, cudaMemcpyDeviceToDevice, c->st));
     } else {
       memcpy(c->h_z, z, sizeof(float) * 2 * M);
+      CU(cudaMemcpyAsync(c->zlab, c->h_z, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, c->st));
     }
-    CU(cudaMemcpyAsync(c->zlab, c->h_z, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, c->st));
+    h_z_valid = !dev;
   }
   c->M_z = M;
   const int64_t n = c->n_local;
@@ -941,6 +944,10 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (st != PHD_OK) return st;
   }
   c->gated = gated;
+  if (!gated && c->model == kRangeBearing && M > 0 && !h_z_valid) {
+    CU(cudaMemcpyAsync(c->h_z, c->zlab, sizeof(float) * 2 * M, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
   if (gated)
     gate_slots(c, M);
   else
@@ -1236,14 +1243,19 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     KL(launch_extract(c->acc, c->M, rank_slots, rank_slots + c->world, c->world, c->p.p_d, c->est + 1, capd, c->summ,
                       &c->est[0].label, c->select ? c->sel_info : nullptr, c->st));
     CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
+    // the estimate count is min(LT, eligible, cap) <= min(LT, cap): copy that many with the
+    // summary, so the extraction costs one synchronisation
+    const int64_t ncopy = out ? std::min<int64_t>(std::max<int64_t>(c->LT, 0), capd) : 0;
+    if (ncopy > 0)
+      CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * ncopy, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
     nest = (int)smh[5];
     lt_clamped = (int)smh[6];
-    if (nest > 0 && out) {
+    if (nest > ncopy && out) {  // not expected (nest <= min(LT, cap)); stay correct anyway
       CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * nest, cudaMemcpyDeviceToHost, c->st));
       CU(cudaStreamSynchronize(c->st));
-      memcpy(out, c->h_est, sizeof(phd_estimate) * nest);
     }
+    if (nest > 0 && out) memcpy(out, c->h_est, sizeof(phd_estimate) * nest);
     timing_record(c, 9);
     if (c->timing) cudaEventElapsedTime(&c->t_ms[4], c->ev[8], c->ev[9]);
   }

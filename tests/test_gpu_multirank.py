@@ -90,9 +90,12 @@ def _run(phd, cfg, world, steps):
 
 
 @pytest.mark.parametrize("cname", ["cfg3", "cfg4"])
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_p_invariance(phd, cname, world):
+@pytest.mark.parametrize("world,gate", [(2, 0), (3, 0), (4, 0), (2, 2), (3, 1)])
+def test_p_invariance(phd, cname, world, gate):
+    """gate = 1/2: the gated update (collective gated/dense decision, per-rank
+    tiles) against its own world = 1 run."""
     cfg = _cfg(cname)
+    cfg = replace(cfg, model=replace(cfg.model, gate=gate))
     steps = 3
     ref = _run(phd, cfg, 1, steps)
     got = _run(phd, cfg, world, steps)
@@ -156,12 +159,13 @@ def test_exchange_moves_mass_to_every_rank(phd):
     group.close()
 
 
-def test_rank_with_no_particles(phd):
+@pytest.mark.parametrize("gate", [0, 2])
+def test_rank_with_no_particles(phd, gate):
     """Tiny population over 4 ranks: some ranks hold no survivors (and no births) in a step;
     the collectives still line up and the result equals the 1-rank run."""
     from dataclasses import replace as rp
     cfg = _cfg("cfg3")
-    m = rp(cfg.model, fixed_count=3, births_per_step=2, capacity=64, max_meas=4096)
+    m = rp(cfg.model, fixed_count=3, births_per_step=2, capacity=64, max_meas=4096, gate=gate)
     cfg = rp(cfg, model=m)
     ref = _run(phd, cfg, 1, 2)
     got = _run(phd, cfg, 4, 2)
