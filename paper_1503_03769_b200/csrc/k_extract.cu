@@ -1,9 +1,12 @@
 // STPHD local estimation on the central unit (rank 0):
 // W = sum_r W_r, LT = round(W) (half away from zero, S7), labels with
 // dW > 0 sorted by (dW desc, label asc) (S8), zeta_l = S_l / dW_l (Eq 18, S9),
-// undetected mass (1 - p_D) W_pred (Eq 17).  One CTA; bitonic sort in shared
-// memory over the next power of two >= M (M <= 8192).
+// undetected mass (1 - p_D) W_pred (Eq 17).  One CTA: radix select of the
+// top-LT labels, bitonic sort of those (M <= 8192).
 #include "phd_internal.h"
+#include "topk.cuh"
+
+#include <algorithm>
 
 namespace phd {
 
@@ -17,51 +20,31 @@ __device__ __forceinline__ bool before(double wa, int la, double wb, int lb) {
   return wa > wb || (wa == wb && la < lb);
 }
 
-__global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc, int M, int n2,
-                                                  const double* __restrict__ Wv, const double* __restrict__ Wpv,
-                                                  int count, double p_d, EstOut* est, int cap, double* summary,
-                                                  int32_t* count_out, const double* sel_info) {
+// One CTA.  The n_sel = min(LT, eligible, cap) largest dW are found by radix
+// select (topk.cuh), compacted in label order, then bitonic-sorted by (dW desc,
+// label asc) -- n_sel (~ the target count) instead of all M labels.
+__global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restrict__ acc, int M,
+                                                          const double* __restrict__ Wv, const double* __restrict__ Wpv,
+                                                          int count, double p_d, EstOut* est, int cap, double* summary,
+                                                          int32_t* count_out, const double* sel_info) {
   extern __shared__ __align__(16) unsigned char sm[];
-  double* kw = reinterpret_cast<double*>(sm);
-  int* kl = reinterpret_cast<int*>(kw + n2);
-  __shared__ int n_elig;
+  const int n2m = M <= 1 ? 1 : 1 << (32 - __clz(M - 1));  // next power of two >= M
+  unsigned long long* kw = reinterpret_cast<unsigned long long*>(sm);
+  double* cw = reinterpret_cast<double*>(kw + M);
+  int* cl = reinterpret_cast<int*>(cw + n2m);
+  __shared__ TopkShared sh;
+  __shared__ int n_elig, snsel;
   const int tid = threadIdx.x, nthr = blockDim.x;
   if (tid == 0) n_elig = 0;
   __syncthreads();
   int cnt = 0;
-  for (int i = tid; i < n2; i += nthr) {
-    double w = -1.0;
-    if (i < M) {
-      w = acc[5 * (int64_t)i];
-      if (w > 0.0) ++cnt; else w = -1.0;
-    }
-    kw[i] = w;
-    kl[i] = i;
+  for (int i = tid; i < M; i += nthr) {
+    const double w = acc[5 * (int64_t)i];
+    kw[i] = w > 0.0 ? (unsigned long long)__double_as_longlong(w) : 0ull;
+    cnt += w > 0.0;
   }
   if (cnt) atomicAdd(&n_elig, cnt);
   __syncthreads();
-  // bitonic sort, order = before()
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < n2; i += nthr) {
-        int p = i ^ j;
-        if (p > i) {
-          bool up = (i & k) == 0;
-          double wi = kw[i], wp = kw[p];
-          int li = kl[i], lp = kl[p];
-          bool swap = up ? before(wp, lp, wi, li) : before(wi, li, wp, lp);
-          if (swap) {
-            kw[i] = wp;
-            kw[p] = wi;
-            kl[i] = lp;
-            kl[p] = li;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  __shared__ int snsel;
   if (tid == 0) {
     double W = 0.0, Wp = 0.0;
     for (int r = 0; r < count; ++r) {
@@ -86,8 +69,59 @@ __global__ void __launch_bounds__(1024) k_extract(const double* __restrict__ acc
     if (count_out) *count_out = (int32_t)nsel;
   }
   __syncthreads();
-  for (int s = tid; s < snsel; s += nthr) {
-    int l = kl[s];
+  const int nsel = snsel;
+  if (nsel <= 0) return;
+  unsigned long long T;
+  int keq;
+  topk_threshold(kw, M, nsel, sh, &T, &keq);
+  // compact the selected labels in label order
+  int carry = 0, carry_eq = 0;
+  for (int r = 0; r < M; r += nthr) {
+    const int i = r + tid;
+    const unsigned long long key = i < M ? kw[i] : 0ull;
+    const bool eq = i < M && key == T;
+    int tot_eq;
+    const int before_eq = carry_eq + topk_round_scan(eq, sh, &tot_eq);
+    const bool take = i < M && (key > T || (eq && before_eq < keq));
+    int tot;
+    const int pos = carry + topk_round_scan(take, sh, &tot);
+    if (take) {
+      cw[pos] = __longlong_as_double((long long)key);
+      cl[pos] = i;
+    }
+    carry += tot;
+    carry_eq += tot_eq;
+  }
+  int n2 = 1;
+  while (n2 < nsel) n2 <<= 1;
+  for (int i = nsel + tid; i < n2; i += nthr) {
+    cw[i] = -1.0;
+    cl[i] = 0x7fffffff;
+  }
+  __syncthreads();
+  // bitonic sort of the n_sel selected, order = before()
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n2; i += nthr) {
+        int p = i ^ j;
+        if (p > i) {
+          bool up = (i & k) == 0;
+          double wi = cw[i], wp = cw[p];
+          int li = cl[i], lp = cl[p];
+          bool swap = up ? before(wp, lp, wi, li) : before(wi, li, wp, lp);
+          if (swap) {
+            cw[i] = wp;
+            cw[p] = wi;
+            cl[i] = lp;
+            cl[p] = li;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int s = tid; s < nsel; s += nthr) {
+    int l = cl[s];
     const double* a = acc + 5 * (int64_t)l;
     double dW = a[0];
     EstOut e;
@@ -103,14 +137,14 @@ cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const 
                            cudaStream_t s) {
   int n2 = 1;
   while (n2 < M) n2 <<= 1;
-  size_t smem = (size_t)n2 * (sizeof(double) + sizeof(int));
+  size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long) + (size_t)n2 * (sizeof(double) + sizeof(int));
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 12);
+    cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 20);
     attr_set = true;
   }
-  k_extract<<<1, 1024, smem, s>>>(acc_lab, M, n2, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
-                                  count_out, sel_info);
+  k_extract<<<1, kTopkThreads, smem, s>>>(acc_lab, M, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
+                                          count_out, sel_info);
   return cudaGetLastError();
 }
 

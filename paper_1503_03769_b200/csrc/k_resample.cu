@@ -16,29 +16,50 @@ __device__ __forceinline__ int64_t n_of(double B, double scale, double U, int64_
   return n;
 }
 
-// Exclusive fp64 scan of the per-block masses (one CTA; fixed order).
+// Exclusive fp64 scan of the per-block masses (one CTA; fixed order): thread t
+// owns the contiguous chunk [t c, t c + c) (loads issued together), warp-shuffle
+// scan of the chunk sums, then the chunk is rewritten with its offsets.
 __global__ void __launch_bounds__(1024) k_scan_blocks(const double* __restrict__ blk, int nb, double* off) {
-  __shared__ double s[1024];
-  const int tid = threadIdx.x;
+  __shared__ double ws[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = (nb + 1023) / 1024;
-  const int b0 = tid * chunk, b1 = min(b0 + chunk, nb);
+  const int b0 = min(nb, tid * chunk), b1 = min(nb, b0 + chunk);
   double loc = 0.0;
-  for (int b = b0; b < b1; ++b) loc += blk[b];
-  s[tid] = loc;
+  int b = b0;
+  for (; b + 8 <= b1; b += 8) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = __ldg(blk + b + r);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) loc += v[r];
+  }
+  for (; b < b1; ++b) loc += __ldg(blk + b);
+  double incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) ws[warp] = incl;
   __syncthreads();
-  // Hillis-Steele inclusive scan over thread sums
-  for (int o = 1; o < 1024; o <<= 1) {
-    double v = tid >= o ? s[tid - o] : 0.0;
-    __syncthreads();
-    s[tid] += v;
-    __syncthreads();
+  if (warp == 0) {
+    const double t = ws[lane];
+    double x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double v = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += v;
+    }
+    ws[lane] = x - t;  // exclusive warp offsets
+    if (lane == 31) off[nb] = x;
   }
-  double run = tid > 0 ? s[tid - 1] : 0.0;
-  for (int b = b0; b < b1; ++b) {
+  __syncthreads();
+  const double prevl = __shfl_up_sync(0xffffffffu, incl, 1);  // exclusive, exact (no subtraction)
+  double run = lane > 0 ? ws[warp] + prevl : ws[warp];
+  for (b = b0; b < b1; ++b) {
     off[b] = run;
-    run += blk[b];
+    run += __ldg(blk + b);
   }
-  if (tid == 1023) off[nb] = s[1023];
 }
 
 cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s) {
@@ -177,25 +198,47 @@ cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cud
   return cudaGetLastError();
 }
 
-// In place: bmax[b] <- max(bmax[0..b-1]) (exclusive; -1 for b = 0).
+// In place: bmax[b] <- max(bmax[0..b-1]) (exclusive; -1 for b = 0).  Chunked as k_scan_blocks.
 __global__ void __launch_bounds__(1024) k_scan_max(int32_t* bmax, int nb) {
-  __shared__ int s[1024];
-  const int tid = threadIdx.x;
+  __shared__ int ws[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = (nb + 1023) / 1024;
-  const int b0 = tid * chunk, b1 = min(b0 + chunk, nb);
+  const int b0 = min(nb, tid * chunk), b1 = min(nb, b0 + chunk);
   int loc = -1;
-  for (int b = b0; b < b1; ++b) loc = max(loc, bmax[b]);
-  s[tid] = loc;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    int v = tid >= o ? s[tid - o] : -1;
-    __syncthreads();
-    s[tid] = max(s[tid], v);
-    __syncthreads();
+  int b = b0;
+  for (; b + 8 <= b1; b += 8) {
+    int v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = bmax[b + r];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) loc = max(loc, v[r]);
   }
-  int run = tid > 0 ? s[tid - 1] : -1;
-  for (int b = b0; b < b1; ++b) {
-    int v = bmax[b];
+  for (; b < b1; ++b) loc = max(loc, bmax[b]);
+  int incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = max(incl, v);
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int t = ws[lane];
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = max(x, v);
+    }
+    const int prev = __shfl_up_sync(0xffffffffu, x, 1);
+    ws[lane] = lane > 0 ? prev : -1;  // exclusive warp maxima
+  }
+  __syncthreads();
+  int run = ws[warp];
+  const int prevl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane > 0) run = max(run, prevl);
+  for (b = b0; b < b1; ++b) {
+    const int v = bmax[b];
     bmax[b] = run;
     run = max(run, v);
   }

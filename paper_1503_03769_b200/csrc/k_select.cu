@@ -9,6 +9,9 @@
 // -- the labels whose states the paper estimates -- in a
 // slot layout that puts I first, so the choice is warp-uniform.
 #include "phd_internal.h"
+#include "topk.cuh"
+
+#include <algorithm>
 
 namespace phd {
 
@@ -34,17 +37,33 @@ __global__ void __launch_bounds__(256) k_block_sum(const float* __restrict__ w, 
   }
 }
 
-__global__ void __launch_bounds__(256) k_sum_blocks(const double* __restrict__ blk, int nb, double* out) {
-  __shared__ double s[256];
+// One CTA of 1024: thread t sums the contiguous chunk [t c, t c + c) of the
+// block sums (loads issued together), then a fixed-order warp/block tree.
+__global__ void __launch_bounds__(1024) k_sum_blocks(const double* __restrict__ blk, int nb, double* out) {
+  __shared__ double s[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunk = (nb + 1023) / 1024;
+  const int b0 = min(nb, tid * chunk), b1 = min(nb, b0 + chunk);
   double a = 0.0;
-  for (int k = threadIdx.x; k < nb; k += blockDim.x) a += blk[k];
-  s[threadIdx.x] = a;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
-    __syncthreads();
+  int b = b0;
+  for (; b + 8 <= b1; b += 8) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = __ldg(blk + b + r);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a += v[r];
   }
-  if (threadIdx.x == 0) *out = s[0];
+  for (; b < b1; ++b) a += __ldg(blk + b);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) s[warp] = a;
+  __syncthreads();
+  if (warp == 0) {
+    a = s[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) *out = a;
+  }
 }
 
 cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cudaStream_t s) {
@@ -54,76 +73,46 @@ cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cud
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  k_sum_blocks<<<1, 256, 0, s>>>(blk, nb, out);
+  k_sum_blocks<<<1, 1024, 0, s>>>(blk, nb, out);
   return cudaGetLastError();
 }
 
-__device__ __forceinline__ bool sel_before(double wa, int la, double wb, int lb) {
-  return wa > wb || (wa == wb && la < lb);
-}
-
 // One CTA.  sel_flag[l] = 1 for l in I; info = (W_id, LT, n_eligible, n_sel).
-__global__ void __launch_bounds__(1024) k_select(const double* __restrict__ C_lab, const double* __restrict__ D_lab,
-                                                 int M, int n2, const double* __restrict__ W_pred, double p_d,
-                                                 int32_t* sel_flag, double* info) {
+// I = the n_sel largest dW (ties: lowest labels), by radix select (topk.cuh).
+__global__ void __launch_bounds__(kTopkThreads) k_select(const double* __restrict__ C_lab,
+                                                         const double* __restrict__ D_lab, int M,
+                                                         const double* __restrict__ W_pred, double p_d,
+                                                         int32_t* sel_flag, double* info) {
   extern __shared__ __align__(16) unsigned char sm[];
-  double* kw = reinterpret_cast<double*>(sm);
-  int* kl = reinterpret_cast<int*>(kw + n2);
-  __shared__ double red[1024];
-  __shared__ int n_elig;
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  unsigned long long* kw = reinterpret_cast<unsigned long long*>(sm);
+  __shared__ TopkShared sh;
+  __shared__ double red[32];
+  __shared__ int n_elig, snsel;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) n_elig = 0;
   __syncthreads();
   double part = 0.0;
   int cnt = 0;
-  for (int i = tid; i < n2; i += nthr) {
-    double w = -1.0;
-    if (i < M) {
-      double D = D_lab[i];
-      double dW = C_lab[i] * (D > 0.0 ? 1.0 / D : 0.0);  // same arithmetic as k_reduce_acc
-      part += dW;
-      sel_flag[i] = 0;
-      if (dW > 0.0) {
-        w = dW;
-        ++cnt;
-      }
-    }
-    kw[i] = w;
-    kl[i] = i;
+  for (int i = tid; i < M; i += nthr) {
+    const double D = D_lab[i];
+    const double dW = C_lab[i] * (D > 0.0 ? 1.0 / D : 0.0);  // same arithmetic as k_reduce_acc
+    part += dW;
+    sel_flag[i] = 0;
+    kw[i] = dW > 0.0 ? (unsigned long long)__double_as_longlong(dW) : 0ull;
+    cnt += dW > 0.0;
   }
-  red[tid] = part;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[warp] = part;
   if (cnt) atomicAdd(&n_elig, cnt);
   __syncthreads();
-  for (int o = nthr / 2; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
-  }
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < n2; i += nthr) {
-        int p = i ^ j;
-        if (p > i) {
-          bool up = (i & k) == 0;
-          double wi = kw[i], wp = kw[p];
-          int li = kl[i], lp = kl[p];
-          bool swap = up ? sel_before(wp, lp, wi, li) : sel_before(wi, li, wp, lp);
-          if (swap) {
-            kw[i] = wp;
-            kw[p] = wi;
-            kl[i] = lp;
-            kl[p] = li;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  __shared__ int snsel;
   if (tid == 0) {
-    double W = (1.0 - p_d) * (*W_pred) + red[0];
+    double sum = 0.0;
+    for (int w = 0; w < (nthr >> 5); ++w) sum += red[w];
+    const double W = (1.0 - p_d) * (*W_pred) + sum;
     long long LT = (long long)floor(W + 0.5);
     if (LT < 0) LT = 0;
-    long long nsel = LT < n_elig ? LT : n_elig;
+    const long long nsel = LT < n_elig ? LT : n_elig;
     snsel = (int)nsel;
     info[0] = W;
     info[1] = (double)LT;
@@ -131,20 +120,32 @@ __global__ void __launch_bounds__(1024) k_select(const double* __restrict__ C_la
     info[3] = (double)nsel;
   }
   __syncthreads();
-  for (int s = tid; s < snsel; s += nthr) sel_flag[kl[s]] = 1;
+  const int nsel = snsel;
+  if (nsel <= 0) return;
+  unsigned long long T;
+  int keq;
+  topk_threshold(kw, M, nsel, sh, &T, &keq);
+  int carry = 0;
+  for (int r = 0; r < M; r += nthr) {
+    const int i = r + tid;
+    const unsigned long long key = i < M ? kw[i] : 0ull;
+    const bool eq = i < M && key == T;
+    int tot;
+    const int before = carry + topk_round_scan(eq, sh, &tot);
+    if (i < M && (key > T || (eq && before < keq))) sel_flag[i] = 1;
+    carry += tot;
+  }
 }
 
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                           int32_t* sel_flag, double* info, cudaStream_t s) {
-  int n2 = 1;
-  while (n2 < M) n2 <<= 1;
-  size_t smem = (size_t)n2 * (sizeof(double) + sizeof(int));
+  size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 12);
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
     attr = true;
   }
-  k_select<<<1, 1024, smem, s>>>(C_lab, D_lab, M, n2, W_pred, p_d, sel_flag, info);
+  k_select<<<1, kTopkThreads, smem, s>>>(C_lab, D_lab, M, W_pred, p_d, sel_flag, info);
   return cudaGetLastError();
 }
 
