@@ -620,11 +620,9 @@ __global__ void k_zero_i32(int32_t* a, int64_t n) {
 
 // ---------------------------------------------------------------------------
 // The gated passes.  Tile t = sorted particles [t*512, t*512 + 512); a CTA of
-// kGpThreads = 128 threads, thread tid holds four particles as two f32x2 pairs
+// kGateTP / (2 NPAIR) threads, thread tid holds 2 NPAIR particles as NPAIR f32x2 pairs
 // h = 0, 1: (tid + 256 h, tid + 128 + 256 h).  Per candidate the thread sums
 // its four terms before the cross-lane reduction.
-constexpr int kGpThreads = 128;
-constexpr int kGpWarps = kGpThreads / 32;
 
 template <int MODEL>
 struct GPair {
@@ -633,27 +631,30 @@ struct GPair {
   float2 VX, VY;
 };
 
-template <int MODEL, int PASS>
-__global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS == 2) ? 5 : 8) k_gpass(const GateArgs g) {
+template <int MODEL, int PASS, int NPAIR>
+__global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing && PASS == 2) ? 5 : 8)
+    k_gpass(const GateArgs g) {
   constexpr bool RB = MODEL == kRangeBearing;
+  constexpr int THREADS = kGateTP / (2 * NPAIR);  // particle pairs (tid + 2 THREADS h, + THREADS) per thread
+  constexpr int WARPS = THREADS / 32;
   // + 2: pass 2 pads an odd selected count with one sentinel candidate
   __shared__ float2 zn[kGateChunk + 2];      // (-z0, -z1)
   __shared__ float zd[kGateChunk + 2];       // 1 / (kappa + C)          (pass 2)
   __shared__ int zr[kGateChunk + 2];         // bearing representation   (range-bearing)
   __shared__ float2 zc[kGateChunk + 2];      // -(Cartesian centre)      (range-bearing, pass 2)
   __shared__ int zi[kGateChunk + 2];         // chunk-local entry index  (pass 2: selected first)
-  __shared__ int wcnt[kGpWarps + 1];
-  __shared__ float wpart[PASS == 1 ? kGpWarps : 1][PASS == 1 ? kGateChunk : 1];   // pass 1: per-warp sums
-  __shared__ float4 wq[PASS == 2 ? kGpWarps : 1][PASS == 2 ? kGateChunk + 2 : 1];     // pass 2: per-warp state sums
+  __shared__ int wcnt[WARPS + 1];
+  __shared__ float wpart[PASS == 1 ? WARPS : 1][PASS == 1 ? kGateChunk : 1];   // pass 1: per-warp sums
+  __shared__ float4 wq[PASS == 2 ? WARPS : 1][PASS == 2 ? kGateChunk + 2 : 1];     // pass 2: per-warp state sums
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = blockIdx.x;
   const float2 na0 = f2(g.na0, g.na0), na1 = f2(g.na1, g.na1);
-  GPair<MODEL> P[2];
+  GPair<MODEL> P[NPAIR];
   constexpr int N4 = RB ? 4 : 2;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int64_t pa = (int64_t)t * kGateTP + 256 * h + tid, pb = pa + 128;
+  for (int h = 0; h < NPAIR; ++h) {
+    const int64_t pa = (int64_t)t * kGateTP + 2 * THREADS * h + tid, pb = pa + THREADS;
     const float4* ra = g.so.rec + pa * N4;
     const float4* rbp = g.so.rec + pb * N4;
     P[h].LW = f2(__ldg(ra + N4 - 1).x, __ldg(rbp + N4 - 1).x);
@@ -678,7 +679,9 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
   }
   const int e0 = g.tstart[t];
   const int K = g.tstart[t + 1] - e0;
-  float2 pacc[2] = {f2(0.0f, 0.0f), f2(0.0f, 0.0f)};
+  float2 pacc[NPAIR];
+#pragma unroll
+  for (int h = 0; h < NPAIR; ++h) pacc[h] = f2(0.0f, 0.0f);
 
   // u = p_D g(z_k | x) w for pair h (bitwise the dense kernel's term)
   auto term = [&](int k, int h, float2& d0, float2& d1) -> float2 {
@@ -702,7 +705,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
     __syncthreads();  // previous chunk fully consumed
     int nsel = 0, base_sel_unpadded = 0;
     if (PASS == 1) {
-      for (int k = tid; k < cl8; k += kGpThreads) {
+      for (int k = tid; k < cl8; k += THREADS) {
         if (k < cl) {
           const int l = g.cand[e0 + cb + k];
           zn[k] = f2(g.sc.s0[l], g.sc.s1[l]);
@@ -715,7 +718,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
     } else {
       // stable partition: labels in I first (their state sums are reduced), then the rest
       int base_sel = 0;
-      for (int k0 = 0; k0 < cl; k0 += kGpThreads) {
+      for (int k0 = 0; k0 < cl; k0 += THREADS) {
         const int k = k0 + tid;
         int l = -1, fl = 0;
         if (k < cl) {
@@ -727,19 +730,19 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
         __syncthreads();
         if (tid == 0) {
           int sacc = 0;
-          for (int w = 0; w < kGpWarps; ++w) {
+          for (int w = 0; w < WARPS; ++w) {
             const int c = wcnt[w];
             wcnt[w] = sacc;
             sacc += c;
           }
-          wcnt[kGpWarps] = sacc;
+          wcnt[WARPS] = sacc;
         }
         __syncthreads();
         if (k < cl && fl) {
           const int pos = base_sel + wcnt[warp] + __popc(bal & ((1u << lane) - 1u));
           zi[pos] = k;
         }
-        base_sel += wcnt[kGpWarps];
+        base_sel += wcnt[WARPS];
         __syncthreads();
       }
       nsel = base_sel;
@@ -750,7 +753,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
       if (tid == 0 && nsel2 > nsel) zi[nsel] = -1;
       // second sweep: the unselected after the selected, in order
       int base_un = nsel2;
-      for (int k0 = 0; k0 < cl; k0 += kGpThreads) {
+      for (int k0 = 0; k0 < cl; k0 += THREADS) {
         const int k = k0 + tid;
         int fl = 0;
         if (k < cl) {
@@ -762,19 +765,19 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
         __syncthreads();
         if (tid == 0) {
           int sacc = 0;
-          for (int w = 0; w < kGpWarps; ++w) {
+          for (int w = 0; w < WARPS; ++w) {
             const int c = wcnt[w];
             wcnt[w] = sacc;
             sacc += c;
           }
-          wcnt[kGpWarps] = sacc;
+          wcnt[WARPS] = sacc;
         }
         __syncthreads();
         if (k < cl && fl) zi[base_un + wcnt[warp] + __popc(bal & ((1u << lane) - 1u))] = k;
-        base_un += wcnt[kGpWarps];
+        base_un += wcnt[WARPS];
         __syncthreads();
       }
-      for (int pos = tid; pos < cl + (nsel2 - nsel); pos += kGpThreads) {
+      for (int pos = tid; pos < cl + (nsel2 - nsel); pos += THREADS) {
         const int ki = zi[pos];
         if (ki < 0) {  // sentinel
           zn[pos] = f2(-1e30f, -1e30f);
@@ -803,17 +806,18 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float2 d0, d1;
-          const float2 u = __fadd2_rn(term(k8 + j, 0, d0, d1), term(k8 + j, 1, d0, d1));
+          float2 u = __fadd2_rn(term(k8 + j, 0, d0, d1), term(k8 + j, 1, d0, d1));
+          if (NPAIR == 4) u = __fadd2_rn(u, __fadd2_rn(term(k8 + j, 2, d0, d1), term(k8 + j, 3, d0, d1)));
           v[j] = u.x + u.y;
         }
         const float r = transpose_reduce8(v, lane);
         if ((lane & 3) == 0) wpart[warp][k8 + (lane >> 2)] = r;
       }
       __syncthreads();
-      for (int k = tid; k < cl; k += kGpThreads) {
+      for (int k = tid; k < cl; k += THREADS) {
         double sum = 0.0;
 #pragma unroll
-        for (int w = 0; w < kGpWarps; ++w) sum += (double)wpart[w][k];
+        for (int w = 0; w < WARPS; ++w) sum += (double)wpart[w][k];
         g.part1[e0 + cb + k] = sum;
       }
     } else {
@@ -826,7 +830,7 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
           {
             float2 a0 = f2(0.0f, 0.0f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < NPAIR; ++h) {
               float2 d0, d1;
               const float2 u = term(kk, h, d0, d1);
               pacc[h] = __ffma2_rn(u, f2(zd[kk], zd[kk]), pacc[h]);
@@ -856,17 +860,17 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
       for (int k = nsel; k < kend; ++k) {
         const float2 dk = f2(zd[k], zd[k]);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NPAIR; ++h) {
           float2 d0, d1;
           pacc[h] = __ffma2_rn(term(k, h, d0, d1), dk, pacc[h]);
         }
       }
       __syncthreads();
-      for (int k = tid; k < nsel; k += kGpThreads) {
+      for (int k = tid; k < nsel; k += THREADS) {
         if (zi[k] < 0) continue;  // sentinel
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-        for (int w = 0; w < kGpWarps; ++w) {
+        for (int w = 0; w < WARPS; ++w) {
           const float4 a = wq[w][k];
           s0 += (double)a.x;
           s1 += (double)a.y;
@@ -879,10 +883,10 @@ __global__ void __launch_bounds__(kGpThreads, (MODEL == kRangeBearing && PASS ==
   }
   if (PASS == 2) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t pa = (int64_t)t * kGateTP + 256 * h + tid;
+    for (int h = 0; h < NPAIR; ++h) {
+      const int64_t pa = (int64_t)t * kGateTP + 2 * THREADS * h + tid;
       g.Ps[pa] = pacc[h].x;
-      g.Ps[pa + 128] = pacc[h].y;
+      g.Ps[pa + THREADS] = pacc[h].y;
     }
   }
 }
@@ -1025,12 +1029,20 @@ cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kb
   return csort_pass(kbuf, vbuf, E, 12, 1 << (bits - 12), hist, scan_tmp, nullptr, mlist, s, launches);
 }
 
+#ifndef PHD_GATE_NPAIR_POS
+#define PHD_GATE_NPAIR_POS 4
+#endif
 template <int MODEL>
 static cudaError_t gpass_m(int pass, const GateArgs& g, cudaStream_t s) {
+  // pass 2, position: 8 particles per thread (64 threads per tile); range-bearing
+  // holds 8 representation registers per pair: 4 particles per thread (128 threads)
+  // (measured at cfg 5: pass 2 0.73 -> 0.64 ms with 8 particles per thread, pass 1
+  // 0.42 -> 0.44 ms, so pass 1 keeps 4)
+  constexpr int NP2 = MODEL == kRangeBearing ? 2 : PHD_GATE_NPAIR_POS;
   if (pass == 1)
-    k_gpass<MODEL, 1><<<g.ntiles, kGpThreads, 0, s>>>(g);
+    k_gpass<MODEL, 1, 2><<<g.ntiles, kGateTP / 4, 0, s>>>(g);
   else
-    k_gpass<MODEL, 2><<<g.ntiles, kGpThreads, 0, s>>>(g);
+    k_gpass<MODEL, 2, NP2><<<g.ntiles, kGateTP / (2 * NP2), 0, s>>>(g);
   return cudaGetLastError();
 }
 
