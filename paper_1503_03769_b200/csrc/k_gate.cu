@@ -64,8 +64,9 @@ __device__ __forceinline__ int cell_key(float v0, float v1, const GateGrid& g) {
   return morton(c0, c1);
 }
 
-// Lanes of the warp holding the same NBITS-bit digit d, among the lanes with
-// ok set: one ballot per bit (MATCH.ANY has a much lower throughput).
+// Lanes of the warp holding the same digit d, among the lanes with ok set: one
+// ballot per key bit (MATCH.ANY has a much lower throughput; ballots over only
+// the bits that vary in the warp, found with REDUX, measured slower still).
 template <int NBITS>
 __device__ __forceinline__ unsigned match_digit(int d, bool ok) {
   unsigned m = __ballot_sync(0xffffffffu, ok);
@@ -207,13 +208,18 @@ struct KeyCell {
 };
 
 template <class KF>
-__global__ void __launch_bounds__(256) k_ms_hist(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk, int32_t* hist) {
+__global__ void __launch_bounds__(256) k_ms_hist(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk, int32_t* hist,
+                                                 int32_t* keys_out = nullptr) {
   __shared__ int h[kSortMaxBins];
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
   __syncthreads();
   const int64_t i0 = (int64_t)blockIdx.x * per_blk;
   const int64_t i1 = min(n, i0 + per_blk);
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&h[kf.digit(kf.raw(i))], 1);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const int32_t raw = kf.raw(i);
+    if (keys_out) keys_out[i] = raw;  // the particle sort keeps its cell keys for the ranking pass
+    atomicAdd(&h[kf.digit(raw)], 1);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) hist[(int64_t)b * nblk + blockIdx.x] = h[b];
 }
@@ -341,8 +347,9 @@ __global__ void k_psort_pad(int64_t n, int64_t n_pad, GateSorted so) {
 }
 
 template <int MODEL>
-__global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, KeyCell kf, int64_t n, int nblk,
-                                                       const int32_t* __restrict__ hs, float wscale, GateSorted so) {
+__global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int32_t* __restrict__ keys, int64_t n,
+                                                       int nblk, const int32_t* __restrict__ hs, float wscale,
+                                                       GateSorted so) {
   constexpr bool RB = MODEL == kRangeBearing;
   constexpr int N4 = RB ? 4 : 2;
   constexpr int ROWS = RB ? 2 : 4;
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, KeyCell kf
   for (int64_t b0 = w0; b0 < w1; b0 += 32 * kMsRows) {
     int32_t key[kMsRows];
 #pragma unroll
-    for (int r = 0; r < kMsRows; ++r) key[r] = kf.raw(min(b0 + r * 32 + lane, w1 - 1));
+    for (int r = 0; r < kMsRows; ++r) key[r] = __ldg(keys + min(b0 + r * 32 + lane, w1 - 1));
 #pragma unroll
     for (int r = 0; r < kMsRows; ++r)
       if (b0 + r * 32 + lane < w1) atomicAdd(&my[key[r] >> 1], 1u << (16 * (key[r] & 1)));
@@ -385,9 +392,11 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, KeyCell kf
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t b0 = w0; b0 < w1; b0 += 32 * ROWS) {
     float4 q[ROWS][N4];
+    int kr[ROWS];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
       const int64_t i = min(b0 + r * 32 + lane, w1 - 1);
+      kr[r] = __ldg(keys + i);
       if (RB) {
         q[r][0] = make_float4(__ldg(src.c[0] + i), __ldg(src.c[1] + i), __ldg(src.c[2] + i), __ldg(src.c[3] + i));
         q[r][1] = make_float4(__ldg(src.c[4] + i), __ldg(src.c[5] + i), __ldg(src.c[6] + i), __ldg(src.c[7] + i));
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, KeyCell kf
     for (int r = 0; r < ROWS; ++r) {
       const int64_t i = b0 + r * 32 + lane;
       const bool ok = i < w1;
-      const int d = ok ? (RB ? cell_key(q[r][0].x, q[r][0].z, kf.g) : cell_key(q[r][0].x, q[r][0].y, kf.g)) : 0;
+      const int d = ok ? kr[r] : 0;
       const unsigned peers = match_digit<12>(d, ok);
       int pos = 0;
       if (ok) pos = base[d] + (int)((my[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) + __popc(peers & lt);
@@ -944,7 +953,7 @@ cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64
 
 cudaError_t gate_sort_particles(int model, const float* const* A, const float* rb, int64_t rb_stride, int64_t n,
                                 int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
-                                const GateSorted& so, cudaStream_t s, int64_t* launches) {
+                                int32_t* keys, const GateSorted& so, cudaStream_t s, int64_t* launches) {
   const bool rbm = model == kRangeBearing;
   if (n_pad > n) {
     k_psort_pad<<<(unsigned)((n_pad - n + 255) / 256), 256, 0, s>>>(n, n_pad, so);
@@ -967,14 +976,14 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
     cudaFuncSetAttribute(k_psort_scatter<kPosIso>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_ms_hist<KeyCell><<<nblk, 256, 0, s>>>(kf, n, kPSortBlock, kGateBins, nblk, hist);
+  k_ms_hist<KeyCell><<<nblk, 256, 0, s>>>(kf, n, kPSortBlock, kGateBins, nblk, hist, keys);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
   if (rbm)
-    k_psort_scatter<kRangeBearing><<<nblk, 256, smem, s>>>(src, kf, n, nblk, hist, wscale, so);
+    k_psort_scatter<kRangeBearing><<<nblk, 256, smem, s>>>(src, keys, n, nblk, hist, wscale, so);
   else
-    k_psort_scatter<kPosIso><<<nblk, 256, smem, s>>>(src, kf, n, nblk, hist, wscale, so);
+    k_psort_scatter<kPosIso><<<nblk, 256, smem, s>>>(src, keys, n, nblk, hist, wscale, so);
   ++*launches;
   return cudaGetLastError();
 }

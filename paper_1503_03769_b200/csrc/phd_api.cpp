@@ -44,7 +44,7 @@ struct Layout {
   // gated update (p->gate != 0)
   int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
   int g_ntiles = 0, g_nsorted = 0;
-  size_t o_ginv, o_gsorted[13], o_gPs, o_ghist, o_gscan, o_gtstart, o_gcand, o_gk, o_gv, o_gmlist,
+  size_t o_gkeys, o_ginv, o_gsorted[13], o_gPs, o_ghist, o_gscan, o_gtstart, o_gcand, o_gk, o_gv, o_gmlist,
       o_gpart1, o_gpart2, o_gmstart, o_gzkey, o_gzstart, o_gzitems, o_gzz, o_gcbuf, o_gA;
 };
 
@@ -107,6 +107,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.g_scan = ceil_div(std::max<int64_t>(L.g_hist, L.g_ntiles + (int64_t)p->max_meas + 2), 4096) + 2;
   L.g_nsorted = p->meas == PHD_MEAS_RANGE_BEARING ? 13 : 5;
   auto gtake = [&](size_t bytes) { return take(gt ? bytes : 256); };
+  L.o_gkeys = gtake(sizeof(int32_t) * L.cap_l);
   L.o_ginv = gtake(sizeof(int32_t) * L.cap_l);
   L.o_gsorted[0] = gtake(sizeof(float) * (p->meas == PHD_MEAS_RANGE_BEARING ? 16 : 8) * L.g_npad);
   L.o_gPs = gtake(sizeof(float) * L.g_npad);
@@ -202,7 +203,7 @@ struct phd_ctx {
   // gated update
   GateSorted gso{};
   GateGrid ggrid{};
-  int32_t *ghist = nullptr, *gscan = nullptr, *gtstart = nullptr, *gcand = nullptr, *gk = nullptr,
+  int32_t *gkeys = nullptr, *ghist = nullptr, *gscan = nullptr, *gtstart = nullptr, *gcand = nullptr, *gk = nullptr,
           *gv = nullptr, *gmlist = nullptr, *gmstart = nullptr, *gzkey = nullptr, *gzstart = nullptr,
           *gzitems = nullptr, *gcbuf = nullptr;
   float2* gzz = nullptr;
@@ -512,6 +513,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->bad = at<int>(c->ws, L.o_bad);
   if (p->gate != 0) {
     c->gso.inv = at<int32_t>(c->ws, L.o_ginv);
+    c->gkeys = at<int32_t>(c->ws, L.o_gkeys);
     c->gso.rec = at<float4>(c->ws, L.o_gsorted[0]);
     c->gso.n4 = p->meas == PHD_MEAS_RANGE_BEARING ? 4 : 2;
     c->gPs = at<float>(c->ws, L.o_gPs);
@@ -882,7 +884,7 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   const int ntiles = (int)(npad / kGateTP);
   const float* A[5] = {c->A[0], c->A[1], c->A[2], c->A[3], c->A[4]};
   CU(gate_sort_particles(c->model, A, c->rb, c->L.cap_l, n, npad, c->wscale, c->ggrid, c->ghist, c->gscan,
-                         c->gso, c->st, &c->launches));
+                         c->gkeys, c->gso, c->st, &c->launches));
   KL(gate_zbin(c->zlab, M, c->ggrid, c->gzkey, c->gzstart, c->gzitems, c->gzz, c->st));
   int64_t tot = 0;
   if (ntiles > 0) {

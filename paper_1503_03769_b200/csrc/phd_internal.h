@@ -209,7 +209,8 @@ struct GateArgs {
 // Launch count added to *launches.
 cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/, const float* rb, int64_t rb_stride,
                                 int64_t n, int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist,
-                                int32_t* scan_tmp, const GateSorted& so, cudaStream_t s, int64_t* launches);
+                                int32_t* scan_tmp, int32_t* keys /*[n] scratch*/, const GateSorted& so, cudaStream_t s,
+                                int64_t* launches);
 // measurements -> grid cells (one CTA): zcell_start[kGateBins + 1], items stable by label
 cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,
                       int32_t* zcell_items, float2* zcell_z, cudaStream_t s);

@@ -56,13 +56,16 @@ def _run_parallel(fns):
 
 
 @pytest.mark.parametrize("K,cname", [(1, "cfg1"), (2, "cfg1"), (3, "cfg1"), (4, "cfg3"), (2, "cfg2"),
-                                     (3, "cfg1+is"), (2, "cfg2+is")])
+                                     (3, "cfg1+is"), (2, "cfg2+is"), (3, "cfg1+gate"), (2, "cfg2+gate"),
+                                     (4, "cfg3+gate")])
 def test_dcp_stagewise(phd, orc, K, cname):
+    """+is: NEXT-4 importance weights; +gate: the gated update (gate = 2) in every group."""
     from oracle import dcp
     importance = cname.endswith("+is")
-    cname = cname.replace("+is", "")
+    gate = 2 if cname.endswith("+gate") else 0
+    cname = cname.replace("+is", "").replace("+gate", "")
     cfg = scenario.get(cname)
-    m = replace(cfg.model, mode=MODE_DCP)
+    m = replace(cfg.model, mode=MODE_DCP, gate=gate)
     if importance:  # NEXT-4: Eq 5 proposal s sigma_a and Eq 6 full ratio, per group's own births
         m = replace(m, proposal_scale=1.3, birth_model=2, birth_sigma_v=10.0,
                     birth_mean=(0.0, 0.0, 0.0, 0.0), birth_std=(600.0, 8.0, 600.0, 8.0))
