@@ -410,6 +410,28 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(cfg.name, {}).get("k_pass2")
         except Exception:
             traffic = None
+    # HBM-bound steps (north_star: predict / resample achieved GB/s against the B200 peak):
+    # algorithmic bytes per launch / mean event time; peak = MEASURED_PEAKS.json hbm_gbs
+    hbm_peak = 6460.5
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        peak_src = "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write bytes)"
+    except Exception:
+        peak_src = "fallback 6460.5 GB/s"
+    n_loc = hi - lo
+    n_surv_loc = max(0, min(hi, n0) - min(lo, n0))
+    rb_bytes = 32 if m.meas == 1 else 0
+    b_pred = n_surv_loc * (40 + rb_bytes) + (n_loc - n_surv_loc) * (20 + rb_bytes)
+    b_res = n_loc * 4 + n0 // world * 48
+    t_pred = statistics.mean(pass_ms["predict"])
+    t_res = statistics.mean(pass_ms["resample"])
+    hbm = {"peak_gbs": hbm_peak, "peak_basis": peak_src,
+           "predict": {"bytes": b_pred, "ms": t_pred, "gbs": b_pred / (t_pred * 1e6), "frac": b_pred / (t_pred * 1e6) / hbm_peak,
+                       "basis": "survivor 40 B (state + w read and written), birth 20 B written%s" %
+                                (", + 32 B range-bearing representation" if rb_bytes else "")},
+           "resample": {"bytes": b_res, "ms": t_res, "gbs": b_res / (t_res * 1e6), "frac": b_res / (t_res * 1e6) / hbm_peak,
+                        "basis": "w read 4 B per particle; per offspring: mark 4+4, ancestor state 16 read, "
+                                 "state + w 20 written, ancestor index 4 (all resampling kernels incl. scans)"}}
     cpu = None
     if not args.no_cpu_baseline:
         r = cpu_oracle_sample(cfg, Z, soa, w, args.cpu_sample, k=1)
@@ -449,6 +471,7 @@ def run_ours(args):
         "e2e": {"value": value_e, "unit": "pairs/s", "h2d_bytes_per_step": M * 8,
                 "d2h_bytes_per_step": int(f._sum.n_est) * 24 + 8 * (2 * world + 10)},
         "gpu_launches": int(launches),
+        "hbm_kernels": hbm,
         "gated": gated,
         "clocks": clk,
     }
