@@ -125,8 +125,9 @@ typedef struct {
                                     measurements whose largest possible exponent over the tile is
                                     >= -130, i.e. every skipped term underflows to exactly 0 in
                                     the dense kernels (same non-zero terms, fp64 sums in another
-                                    fixed order).  Falls back to dense for an update whose
-                                    candidate pairs exceed half of N x M or the workspace;
+                                    fixed order).  Runs dense for an update whose candidate
+                                    pairs exceed half of N x M or the workspace, or with
+                                    N x M < 2^29 in exact mode (the sort would dominate);
                                  2: gated whenever the candidate lists fit the workspace. */
   double proposal_scale;      /* s in (0, 1e3]: Eq 5 proposal q_k = the CV transition with
                                  noise std s sigma_a, survivors weighted p_s f/q

@@ -619,17 +619,21 @@ cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_labe
 // for the slot range [s0, s1) (one measurement group).
 __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_pad, int s0, int s1,
                            double* C_slot) {
-  int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per slot, lanes over the particle-CTA partials, fixed-order xor tree
+  const int lane = threadIdx.x & 31;
+  int s = s0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= s1) return;
   double c = 0.0;
-  for (int b = 0; b < gp; ++b) c += Cpart[(int64_t)b * slots_pad + s];
-  C_slot[s] = c;
+  for (int b = lane; b < gp; b += 32) c += Cpart[(int64_t)b * slots_pad + s];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) C_slot[s] = c;
 }
 
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
                             cudaStream_t s) {
   if (s1 <= s0) return cudaSuccess;
-  k_reduce_C<<<(s1 - s0 + 127) / 128, 128, 0, s>>>(Cpart, gp, slots_pad, s0, s1, C_slot);
+  k_reduce_C<<<(s1 - s0 + 7) / 8, 256, 0, s>>>(Cpart, gp, slots_pad, s0, s1, C_slot);
   return cudaGetLastError();
 }
 
@@ -755,16 +759,24 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
     }
     return;
   }
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per slot: lanes stride over the particle-CTA partials, fixed-order
+  // xor tree (deterministic); the last block handles the rank masses above
+  const int lane = threadIdx.x & 31;
+  int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= n_slots) return;
   int lab = slot_label[s];
   if (lab < 0) return;
   double A[4] = {0, 0, 0, 0};
-  for (int b = 0; b < gp; ++b) {
+  for (int b = lane; b < gp; b += 32) {
     const double* p = Apart + (int64_t)b * 4 * slots_pad + s;
 #pragma unroll
     for (int q = 0; q < 4; ++q) A[q] += p[(int64_t)q * slots_pad];
   }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) A[q] += __shfl_xor_sync(0xffffffffu, A[q], o);
+  if (lane != 0) return;
   double D = D_lab[lab];
   double inv = D > 0.0 ? 1.0 / D : 0.0;
   double cx, cy;
@@ -796,7 +808,7 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
                               const float* s2, const float* s3, int model, const double* blk_w, const double* blk_wp,
                               int nb, double* acc_lab, double* rank_slots, int rank, int world, int lead,
                               const int32_t* sel_flag, cudaStream_t s) {
-  int blocks = (n_slots + 255) / 256 + 1;
+  int blocks = (n_slots + 7) / 8 + 1;  // 8 slots (warps) per block + the rank-mass block
   k_reduce_acc<<<blocks, 256, 0, s>>>(Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
                                       blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead, sel_flag);
   return cudaGetLastError();

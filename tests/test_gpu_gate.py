@@ -106,7 +106,8 @@ def test_gated_degenerate_inputs(phd, orc):
 
 
 def test_gated_auto_falls_back(phd, orc):
-    """gate = 1 runs dense when the candidates are most of N x M (a point cloud)."""
+    """gate = 1 runs dense when the candidates are most of N x M (a point cloud) or the
+    update is small (< 2^29 pairs, as here)."""
     m = replace(POS, gate=1)
     z = _meas(m, 20, 4)
     z[:] = z[0]
@@ -185,7 +186,8 @@ def test_gated_filter_steps_stagewise(phd, orc, cname, steps):
 def test_gated_full_size_sampled(phd, orc, cname):
     """BASELINE sizes with gate = 1 (cfg 5 is the bench configuration of the gated line)."""
     cfg = scenario.get(cname)
-    m = replace(cfg.model, gate=1)
+    # gate = 1 (automatic) at cfg 4-5; cfg 3 is below the automatic small-update limit (2^29 pairs)
+    m = replace(cfg.model, gate=2 if cname == "cfg3" else 1)
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
     soa, w = scenario.initial_population(cfg, truth)
