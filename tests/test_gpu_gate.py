@@ -105,6 +105,19 @@ def test_gated_degenerate_inputs(phd, orc):
     f.close()
 
 
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
+def test_gated_many_measurements(phd, orc, mname):
+    """M > 4096: the label sort of the candidate entries takes two LSD passes (12 + 1 bits)."""
+    m = replace(MODELS[mname], gate=2, max_meas=8192, clutter_rate=200.0)
+    z = _meas(m, 6000, 17)
+    soa, w = _cloud(m, 20000, z, 17)
+    g = _run(phd, m, soa, w, z)
+    assert g["gate"]["used"] == 1
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
+
+
 def test_gated_auto_falls_back(phd, orc):
     """gate = 1 runs dense when the candidates are most of N x M (a point cloud) or the
     update is small (< 2^29 pairs, as here)."""
