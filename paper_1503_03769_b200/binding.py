@@ -329,6 +329,10 @@ class Filter:
                     "phd_extract")
         return self._estimates(), self._sum.as_dict()
 
+    def estimates(self):
+        """Estimates of the last extract / step: labels, states (x, vx, y, vy), masses."""
+        return self._estimates()
+
     def _estimates(self):
         n = self._n.value
         labels = np.array([self._est[i].label for i in range(n)], dtype=np.int32)
