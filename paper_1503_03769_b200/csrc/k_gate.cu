@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(256) k_ms_scatter(KF kf, int64_t n, int64_t pe
       __syncwarp();
       if (ok) {
         if (lane == __ffs(peers) - 1) atomicAdd(&my[d >> 1], (uint32_t)__popc(peers) << (16 * (d & 1)));
+        PHD_DCHECK(pos >= 0 && pos < n);
         if (out_keys) out_keys[pos] = raw[r];
         out_vals[pos] = val[r];
       }
@@ -415,6 +416,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
       __syncwarp();
       if (ok) {
         if (lane == __ffs(peers) - 1) atomicAdd(&my[d >> 1], (uint32_t)__popc(peers) << (16 * (d & 1)));
+        PHD_DCHECK(pos >= 0 && pos < n && d >= 0 && d < nbins);
         float4* dst = so.rec + (int64_t)pos * N4;
 #pragma unroll
         for (int k = 0; k < N4; ++k) dst[k] = q[r][k];
@@ -549,6 +551,7 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
       int cy = y0 + ci / nx;
       if (g.wrap1) cy = wrapc(cy);
       const int key = morton(cx, cy);
+      PHD_DCHECK(key >= 0 && key < kGateBins);
       j0 = zcell_start[key];
       j1 = zcell_start[key + 1];
     }
@@ -572,7 +575,10 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
         const float2 zz = zcell_z[j];
         const float dx = dist_iv(zz.x, b0, b1);
         const float dy = g.wrap1 ? dist_arc(zz.y, e0, e1) : dist_iv(zz.y, e0, e1);
-        if (fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm)) >= kGateLog2Min) dst[w++] = zcell_items[j];
+        if (fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm)) >= kGateLog2Min) {
+          PHD_DCHECK(w < cap);
+          dst[w++] = zcell_items[j];
+        }
       }
     }
     total += __shfl_sync(0xffffffffu, incl, 31);
@@ -716,7 +722,9 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
     if (PASS == 1) {
       for (int k = tid; k < cl8; k += THREADS) {
         if (k < cl) {
+          PHD_DCHECK(e0 + cb + k < g.E);
           const int l = g.cand[e0 + cb + k];
+          PHD_DCHECK(l >= 0 && l < g.M);
           zn[k] = f2(g.sc.s0[l], g.sc.s1[l]);
           if (RB) zr[k] = g.sc.rep[l];
         } else {
@@ -749,6 +757,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
         __syncthreads();
         if (k < cl && fl) {
           const int pos = base_sel + wcnt[warp] + __popc(bal & ((1u << lane) - 1u));
+          PHD_DCHECK(pos < kGateChunk + 2);
           zi[pos] = k;
         }
         base_sel += wcnt[WARPS];
@@ -782,7 +791,10 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
           wcnt[WARPS] = sacc;
         }
         __syncthreads();
-        if (k < cl && fl) zi[base_un + wcnt[warp] + __popc(bal & ((1u << lane) - 1u))] = k;
+        if (k < cl && fl) {
+          PHD_DCHECK(base_un + wcnt[warp] + __popc(bal & ((1u << lane) - 1u)) < kGateChunk + 2);
+          zi[base_un + wcnt[warp] + __popc(bal & ((1u << lane) - 1u))] = k;
+        }
         base_un += wcnt[WARPS];
         __syncthreads();
       }
@@ -797,7 +809,9 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
           }
           continue;
         }
+        PHD_DCHECK(pos < kGateChunk + 2 && ki < cl && e0 + cb + ki < g.E);
         const int l = g.cand[e0 + cb + ki];
+        PHD_DCHECK(l >= 0 && l < g.M);
         zn[pos] = f2(g.sc.s0[l], g.sc.s1[l]);
         zd[pos] = g.sc.d[l];
         if (RB) {
@@ -820,13 +834,17 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
           v[j] = u.x + u.y;
         }
         const float r = transpose_reduce8(v, lane);
-        if ((lane & 3) == 0) wpart[warp][k8 + (lane >> 2)] = r;
+        if ((lane & 3) == 0) {
+          PHD_DCHECK(k8 + (lane >> 2) < kGateChunk);
+          wpart[warp][k8 + (lane >> 2)] = r;
+        }
       }
       __syncthreads();
       for (int k = tid; k < cl; k += THREADS) {
         double sum = 0.0;
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) sum += (double)wpart[w][k];
+        PHD_DCHECK(e0 + cb + k < g.E);
         g.part1[e0 + cb + k] = sum;
       }
     } else {
@@ -861,7 +879,10 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
         }
         const float r = transpose_reduce8(v, lane);
         const int q = lane >> 2;  // value index 0..7: candidate k + q / 4, quantity q % 4
-        if ((lane & 3) == 0) reinterpret_cast<float*>(&wq[warp][k + (q >> 2)])[q & 3] = r;
+        if ((lane & 3) == 0) {
+          PHD_DCHECK(k + (q >> 2) < kGateChunk + 2);
+          reinterpret_cast<float*>(&wq[warp][k + (q >> 2)])[q & 3] = r;
+        }
       }
       // the rest: weights only
       const int kend = cl + (nsel - base_sel_unpadded);
@@ -886,6 +907,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
           s2 += (double)a.z;
           s3 += (double)a.w;
         }
+        PHD_DCHECK(zi[k] < cl && e0 + cb + zi[k] < g.E);
         reinterpret_cast<float4*>(g.part2)[e0 + cb + zi[k]] = make_float4((float)s0, (float)s1, (float)s2, (float)s3);
       }
     }
@@ -894,6 +916,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
 #pragma unroll
     for (int h = 0; h < NPAIR; ++h) {
       const int64_t pa = (int64_t)t * kGateTP + 2 * THREADS * h + tid;
+      PHD_DCHECK(pa + THREADS < (int64_t)g.ntiles * kGateTP);
       g.Ps[pa] = pacc[h].x;
       g.Ps[pa + THREADS] = pacc[h].y;
     }
@@ -913,7 +936,10 @@ __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__
   const int j0 = live ? mstart[l] : 0, j1 = live ? mstart[l + 1] : 0;
   if (PASS == 1) {
     double s = 0.0;
-    for (int j = j0 + lane; j < j1; j += 32) s += part1[mlist[j]];
+    for (int j = j0 + lane; j < j1; j += 32) {
+      PHD_DCHECK(mlist[j] >= 0 && mlist[j] < mstart[M]);
+      s += part1[mlist[j]];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) out[l] = s;

@@ -1031,6 +1031,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     ga.part1 = c->gpart1;
     ga.part2 = c->gpart2;
     ga.Ps = c->gPs;
+    ga.E = c->g_entries;
+    ga.M = M;
     timing_record(c, 3);
     if (ntiles > 0) KL(launch_gpass(1, ga, c->st));
     timing_record(c, 4);

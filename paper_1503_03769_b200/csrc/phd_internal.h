@@ -2,9 +2,27 @@
 // CUDA kernels (k_*.cu).  Not installed; not part of the ABI.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 namespace phd {
+
+// Device bounds checks, compiled in only with -DPHD_DEBUG_BOUNDS (a build
+// variant for the tests; compute-sanitizer is unavailable on the GPU pool).
+#ifdef PHD_DEBUG_BOUNDS
+#define PHD_DCHECK(cond)                                                                         \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("PHD_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define PHD_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // ---- tiling constants ----------------------------------------
 // measurement slots per lane: 4 or 8 (kernel template), i.e. 128 or 256 per warp
@@ -203,6 +221,8 @@ struct GateArgs {
   double* part1;                      // [E] tile sums of u = p_D g w (pass 1)
   float* part2;                       // [E][4] tile sums of the centred state terms (pass 2, selected labels)
   float* Ps;                          // [n_pad] sum_z u d per sorted particle (pass 2)
+  int64_t E;                          // candidate entries (bounds checks of the debug build)
+  int M;                              // measurements (bounds checks of the debug build)
 };
 
 // key + stable counting sort of the local particles; writes the sorted copy.
