@@ -248,6 +248,10 @@ phd_status phd_get_resample_meta(phd_ctx* ctx, double* W, double* U, int64_t* N_
  * out[2] = (particle, measurement) pairs evaluated (entries x 512 incl. tile padding),
  * out[3] = tiles. */
 phd_status phd_get_gate_stats(phd_ctx* ctx, int64_t* out /* [4] */);
+/* Particle exchange path of the last resampling: 0 none (world 1, or DCP ring only),
+ * 1 send/recv (NCCL grouped send/recv, or device copies in an in-process group),
+ * 2 fused gather + exchange over the peer-memory window. */
+int32_t phd_exchange_path(const phd_ctx* ctx);
 /* Kernel launches issued by this ctx since creation (all streams). */
 int64_t phd_launch_count(const phd_ctx* ctx);
 /* Device time (ms) of the last update's pass-1 and pass-2 kernels, measured

@@ -59,7 +59,7 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_get_ancestors", "phd_get_resample_meta", "phd_launch_count", "phd_set_timing", "phd_get_timing",
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
            "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates",
-           "phd_get_gate_stats"]
+           "phd_get_gate_stats", "phd_exchange_path"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -115,6 +115,8 @@ def load(build_if_missing=True):
     L.phd_get_local_estimates.argtypes = [_P, ctypes.POINTER(Estimate), ctypes.c_int32, _I32]
     L.phd_get_resample_meta.argtypes = [_P, _D, _D, _I64, _D]
     L.phd_get_gate_stats.argtypes = [_P, _I64]
+    L.phd_exchange_path.argtypes = [_P]
+    L.phd_exchange_path.restype = ctypes.c_int32
     L.phd_launch_count.argtypes = [_P]
     L.phd_launch_count.restype = ctypes.c_int64
     L.phd_set_timing.argtypes = [_P, ctypes.c_int32]
@@ -400,6 +402,10 @@ class Filter:
         out = np.zeros(4, dtype=np.int64)
         self._check(self.L.phd_get_gate_stats(self.h, out.ctypes.data_as(_I64)), "phd_get_gate_stats")
         return {"used": int(out[0]), "entries": int(out[1]), "pairs": int(out[2]), "tiles": int(out[3])}
+
+    def exchange_path(self):
+        """0 none, 1 send/recv, 2 fused gather + exchange over peer memory."""
+        return int(self.L.phd_exchange_path(self.h))
 
     def launch_count(self):
         return self.L.phd_launch_count(self.h)

@@ -14,6 +14,7 @@ class NcclComm : public Comm {
  public:
   NcclComm(ncclComm_t c, int world, int rank) : c_(c), world_(world), rank_(rank) {}
   ~NcclComm() override {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
     if (c_) ncclCommDestroy(c_);
   }
   const char* name() const override { return "nccl"; }
@@ -46,9 +47,72 @@ class NcclComm : public Comm {
     return r == ncclSuccess ? "" : std::string("ncclAllGather: ") + ncclGetErrorString(r);
   }
 
+  std::string share_buffers(void* const* local, int nbuf, std::vector<void*>* all, cudaStream_t s) override {
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    std::vector<cudaIpcMemHandle_t> mine(nbuf), every((size_t)nbuf * world_);
+    // every rank must take the same path through the collectives below: a local
+    // failure is all-reduced before anyone opens a handle
+    int bad = 0;
+    for (int b = 0; b < nbuf; ++b)
+      if (cudaIpcGetMemHandle(&mine[b], local[b]) != cudaSuccess) bad = 1;
+    cudaGetLastError();
+    void* dev = nullptr;
+    if (cudaMalloc(&dev, hb * nbuf * (world_ + 1) + sizeof(double)) != cudaSuccess) return "share_buffers: cudaMalloc";
+    char* dsend = (char*)dev;
+    char* drecv = dsend + hb * nbuf;
+    double* dflag = reinterpret_cast<double*>(drecv + hb * nbuf * world_);
+    std::string err;
+    double flag = bad;
+    cudaError_t e = cudaMemcpyAsync(dflag, &flag, sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) err = allreduce_f64(dflag, 1, s);
+    if (e == cudaSuccess && err.empty()) e = cudaMemcpyAsync(&flag, dflag, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && err.empty()) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && err.empty() && flag == 0.0) {
+      e = cudaMemcpyAsync(dsend, mine.data(), hb * nbuf, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) err = allgather_bytes(dsend, drecv, hb * nbuf, s);
+      if (e == cudaSuccess && err.empty())
+        e = cudaMemcpyAsync(every.data(), drecv, hb * nbuf * world_, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess && err.empty()) e = cudaStreamSynchronize(s);
+    }
+    cudaFree(dev);
+    if (e != cudaSuccess) return std::string("share_buffers: ") + cudaGetErrorString(e);
+    if (!err.empty()) return err;
+    if (flag != 0.0) return "share_buffers: cudaIpcGetMemHandle failed on some rank";
+    all->assign((size_t)world_ * nbuf, nullptr);
+    int open_bad = 0;
+    for (int r = 0; r < world_; ++r)
+      for (int b = 0; b < nbuf; ++b) {
+        if (r == rank_) {
+          (*all)[(size_t)r * nbuf + b] = local[b];
+          continue;
+        }
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, every[(size_t)r * nbuf + b], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          open_bad = 1;
+          continue;
+        }
+        opened_.push_back(ptr);
+        (*all)[(size_t)r * nbuf + b] = ptr;
+      }
+    // collective verdict: every rank uses the peer window, or none does
+    flag = open_bad;
+    if (cudaMalloc(&dev, sizeof(double)) != cudaSuccess) return "share_buffers: cudaMalloc";
+    e = cudaMemcpyAsync(dev, &flag, sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) err = allreduce_f64((double*)dev, 1, s);
+    if (e == cudaSuccess && err.empty()) e = cudaMemcpyAsync(&flag, dev, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && err.empty()) e = cudaStreamSynchronize(s);
+    cudaFree(dev);
+    if (e != cudaSuccess) return std::string("share_buffers: ") + cudaGetErrorString(e);
+    if (!err.empty()) return err;
+    if (flag != 0.0) return "share_buffers: cudaIpcOpenMemHandle failed on some rank (no peer access)";
+    return "";
+  }
+
  private:
   ncclComm_t c_;
   int world_, rank_;
+  std::vector<void*> opened_;
 };
 
 Comm* make_nccl_comm(const uint8_t* id128, int world, int rank, std::string* err) {
@@ -82,8 +146,9 @@ struct LocalGroup {
   std::vector<std::vector<float*>> srcs;
   std::vector<ExchangePlan> plans;
   std::vector<const void*> gsrc;
+  std::vector<std::vector<void*>> shared;
 
-  explicit LocalGroup(int w) : world(w), bufs(w, nullptr), srcs(w), plans(w), gsrc(w, nullptr) {}
+  explicit LocalGroup(int w) : world(w), bufs(w, nullptr), srcs(w), plans(w), gsrc(w, nullptr), shared(w) {}
 
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
@@ -148,6 +213,21 @@ class LocalComm : public Comm {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     g_->barrier();  // peers may reuse their source buffers only after every pull
     return e == cudaSuccess ? "" : std::string("local exchange: ") + cudaGetErrorString(e);
+  }
+
+  std::string share_buffers(void* const* local, int nbuf, std::vector<void*>* all, cudaStream_t s) override {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cudaGetErrorString(e);
+    g_->shared[rank_].assign(local, local + nbuf);
+    g_->barrier();
+    all->clear();
+    bool null = false;
+    for (int r = 0; r < g_->world; ++r) {
+      all->insert(all->end(), g_->shared[r].begin(), g_->shared[r].end());
+      for (void* p : g_->shared[r]) null = null || p == nullptr;
+    }
+    g_->barrier();
+    return null ? "local share_buffers: a rank has no buffer" : "";  // same verdict on every rank
   }
 
   std::string allgather_bytes(const void* send, void* recv, size_t bytes, cudaStream_t s) override {

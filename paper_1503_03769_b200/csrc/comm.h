@@ -30,6 +30,13 @@ class Comm {
                                cudaStream_t s) = 0;
   // recv[r * bytes .. ) = rank r's send[0 .. bytes) for every rank r (device buffers).
   virtual std::string allgather_bytes(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+  // Peer-memory window for the fused resample + exchange: every rank registers nbuf
+  // device buffers (cudaMalloc allocations of its own); all[r * nbuf + b] receives
+  // rank r's buffer b as a pointer this rank's kernels can store to.  NCCL transport:
+  // CUDA IPC handles all-gathered and opened with peer access (NVLink / NVSwitch);
+  // in-process group: the pointers themselves.  Collective.  "" or an error (the
+  // caller then keeps the NCCL send/recv exchange).
+  virtual std::string share_buffers(void* const* local, int nbuf, std::vector<void*>* all, cudaStream_t s) = 0;
 };
 
 Comm* make_nccl_comm(const uint8_t* id128, int world, int rank, std::string* err);

@@ -343,6 +343,77 @@ cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_
   return cudaGetLastError();
 }
 
+// Fused resample + exchange: offspring g = first + j goes straight
+// to its owner q of the next step's block partition (blo), at local slot
+// g - blo[q], stored through the peer-memory window (NVLink P2P for one process
+// per GPU).  Consecutive offspring have consecutive destinations, so the remote
+// stores of a warp coalesce.  The caller's collective barrier after this kernel
+// orders the stores before any rank reads its next-step array.
+__global__ void __launch_bounds__(256) k_gather_p2p(const int32_t* __restrict__ marks, const int32_t* __restrict__ bex,
+                                                    int64_t n, int64_t g0, const float* __restrict__ x,
+                                                    const float* __restrict__ vx, const float* __restrict__ y,
+                                                    const float* __restrict__ vy, float w_off, const PeerOut po,
+                                                    int32_t* anc, int zero_mass, int64_t first, int64_t n_upd,
+                                                    int64_t n_out) {
+  __shared__ int wm[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kBlockOff;
+  int a4[4];
+  if (zero_mass) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int64_t j = base + 4 * tid + r;
+      a4[r] = (int)(((first + j) * n_upd) / n_out);
+    }
+  } else {
+    int m = -1;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int64_t j = base + 4 * tid + r;
+      a4[r] = j < n ? marks[j] : -1;
+      m = max(m, a4[r]);
+      a4[r] = m;
+    }
+    int incl = warp_max_scan(m, lane);
+    if (lane == 31) wm[warp] = incl;
+    __syncthreads();
+    int carry = bex[blockIdx.x];
+    for (int k = 0; k < warp; ++k) carry = max(carry, wm[k]);
+    int prev = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane > 0) carry = max(carry, prev);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a4[r] = max(a4[r], carry);
+  }
+  int q = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t j = base + 4 * tid + r;
+    if (j >= n) break;
+    const int64_t g = first + j;
+    while (q + 1 < po.world && po.blo[q + 1] <= g) ++q;
+    const int64_t off = g - po.blo[q];
+    const int64_t l = (int64_t)a4[r] - g0;
+    po.dst[q][0][off] = x[l];
+    po.dst[q][1][off] = vx[l];
+    po.dst[q][2][off] = y[l];
+    po.dst[q][3][off] = vy[l];
+    po.dst[q][4][off] = w_off;
+    anc[j] = a4[r];
+  }
+  __threadfence_system();
+}
+
+cudaError_t launch_gather_p2p(const int32_t* marks, const int32_t* bmax_excl, int64_t n, int64_t g0, const float* x,
+                              const float* vx, const float* y, const float* vy, float w_off, const PeerOut& po,
+                              int32_t* anc, int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out,
+                              cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_gather_p2p<<<(unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s>>>(
+      marks, bmax_excl, n, g0, x, vx, y, vy, w_off, po, anc, zero_mass, first, n_global_upd, n_out);
+  return cudaGetLastError();
+}
+
+
 // DCP ring exchange: the L slots s_i = floor(((i + v) n) / L)
 // of this group (fp64, one rounding per operation, as in the oracle).
 struct Arr5 {

@@ -200,6 +200,12 @@ struct phd_ctx {
   int64_t N_out_last = 0, prod_first = 0, prod_n = 0;
   int count_clamped = 0, zero_mass = 0;
   int64_t ring_L = 0;
+  // fused resample + exchange over the peer-memory window (world > 1, exact mode)
+  int p2p_state = 0;                       // 0 not set up yet, 1 active, -1 unavailable (send/recv exchange)
+  bool p2p_live = false;                   // A currently points into pbuf
+  float* pbuf[2] = {nullptr, nullptr};     // this rank's two particle buffers [5][cap_l] (A / B alternate)
+  std::vector<float*> peer_buf;            // [world][2]: every rank's pbuf[0], pbuf[1]
+  int par = 0;                             // A = pbuf[par] once live; all ranks flip together
   // gated update
   GateSorted gso{};
   GateGrid ggrid{};
@@ -576,6 +582,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   }
   CUB(cudaMemsetAsync(c->ws, 0, L.total, c->st));
   CUB(cudaStreamSynchronize(c->st));
+
 #undef CUB
   *out = c;
   return PHD_OK;
@@ -596,6 +603,8 @@ void phd_destroy(phd_ctx* c) {
   if (!c) return;
   if (c->st) cudaStreamSynchronize(c->st);
   delete c->comm;
+  for (int b = 0; b < 2; ++b)
+    if (c->pbuf[b]) cudaFree(c->pbuf[b]);
   for (int i = 0; i < 16; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   if (c->own_ws && c->ws) cudaFree(c->ws);
@@ -609,6 +618,11 @@ void phd_destroy(phd_ctx* c) {
 }
 
 int64_t phd_launch_count(const phd_ctx* c) { return c ? c->launches : 0; }
+
+int32_t phd_exchange_path(const phd_ctx* c) {
+  if (!c || c->world <= 1 || c->dcp) return 0;
+  return c->p2p_state == 1 ? 2 : 1;
+}
 
 phd_status phd_set_timing(phd_ctx* c, int32_t enable) {
   if (!c) return PHD_EINVAL;
@@ -1296,6 +1310,44 @@ phd_status phd_get_local_estimates(phd_ctx* c, phd_estimate* out, int32_t cap, i
   return PHD_OK;
 }
 
+// Peer-memory window for the fused resample + exchange, set up at
+// the first multi-rank resampling (a collective point: the ranks of an in-process
+// group are created one after another, but step in parallel).  The particle double
+// buffers become library allocations every rank maps; any failure (no IPC / peer
+// access, PHD_EXCHANGE=nccl) keeps the send/recv exchange.
+static phd_status p2p_setup(phd_ctx* c) {
+  const char* xch = getenv("PHD_EXCHANGE");
+  if (c->world <= 1 || c->dcp || c->world > kMaxPeers || (xch && strcmp(xch, "nccl") == 0)) {
+    c->p2p_state = -1;
+    return PHD_OK;
+  }
+  const size_t bytes = sizeof(float) * 5 * (size_t)c->L.cap_l;
+  bool ok = cudaMalloc(&c->pbuf[0], bytes) == cudaSuccess;
+  ok = (cudaMalloc(&c->pbuf[1], bytes) == cudaSuccess) && ok;
+  cudaGetLastError();
+  if (ok) {
+    CU(cudaMemsetAsync(c->pbuf[0], 0, bytes, c->st));
+    CU(cudaMemsetAsync(c->pbuf[1], 0, bytes, c->st));
+  }
+  std::vector<void*> all;
+  void* loc[2] = {c->pbuf[0], c->pbuf[1]};
+  // collective on every rank; a rank without buffers fails IPC and the verdict falls back everywhere
+  std::string e = c->comm->share_buffers(loc, 2, &all, c->st);
+  if (e.empty() && ok) {
+    c->p2p_state = 1;
+    c->peer_buf.resize((size_t)c->world * 2);
+    for (size_t i = 0; i < all.size(); ++i) c->peer_buf[i] = (float*)all[i];
+  } else {
+    for (int b = 0; b < 2; ++b)
+      if (c->pbuf[b]) cudaFree(c->pbuf[b]);
+    c->pbuf[0] = c->pbuf[1] = nullptr;
+    cudaGetLastError();
+    c->p2p_state = -1;
+  }
+  CU(cudaStreamSynchronize(c->st));
+  return PHD_OK;
+}
+
 phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
@@ -1359,8 +1411,30 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     KL(launch_block_max(c->marks, nprod, c->bmax, c->st));
     KL(launch_scan_max(c->bmax, nbo, c->st));
   }
-  KL(launch_gather(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, c->B[0], c->B[1],
-                   c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->dcp ? c->n_local : c->N, n_out, c->st));
+  if (!c->dcp && c->world > 1 && c->p2p_state == 0) {
+    phd_status st = p2p_setup(c);
+    if (st != PHD_OK) return st;
+  }
+  const int dst_b = c->p2p_live ? 1 - c->par : 0;  // the buffer that becomes A on every rank
+  if (c->p2p_state == 1 && !c->dcp) {
+    // fused gather + exchange: offspring stored straight into their owners' next-step
+    // arrays, then one collective barrier
+    PeerOut po{};
+    po.world = c->world;
+    for (int q = 0; q < c->world; ++q) {
+      int64_t blo, bhi;
+      block_of(n_out + J, c->world, q, &blo, &bhi);
+      po.blo[q] = blo;
+      float* base = c->peer_buf[(size_t)q * 2 + dst_b];
+      for (int i = 0; i < 5; ++i) po.dst[q][i] = base + (size_t)i * c->L.cap_l;
+    }
+    po.blo[c->world] = n_out + J;
+    KL(launch_gather_p2p(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, po, c->anc,
+                         c->zero_mass, lo, c->N, n_out, c->st));
+  } else {
+    KL(launch_gather(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, c->B[0], c->B[1],
+                     c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->dcp ? c->n_local : c->N, n_out, c->st));
+  }
   timing_record(c, 11);
   // exchange: the next step's survivors [0, n_out) are block-partitioned over N' = n_out + J
   if (c->dcp) {
@@ -1405,6 +1479,22 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   } else if (c->world == 1) {
     for (int i = 0; i < 5; ++i) std::swap(c->A[i], c->B[i]);
     c->n_surv_local = n_out;
+  } else if (c->p2p_state == 1) {
+    // every rank's stores into the peers' next-step arrays are complete once all ranks
+    // pass this stream-ordered barrier (a one-element all-reduce); then every rank's A
+    // is its buffer dst_b, B the other one
+    c->h_meta[3 * c->world + 46] = 0.0;
+    CU(cudaMemcpyAsync(c->ring, c->h_meta + 3 * c->world + 46, sizeof(double), cudaMemcpyHostToDevice, c->st));
+    COMM(c->comm->allreduce_f64(c->ring, 1, c->st));
+    for (int i = 0; i < 5; ++i) {
+      c->A[i] = c->pbuf[dst_b] + (size_t)i * c->L.cap_l;
+      c->B[i] = c->pbuf[1 - dst_b] + (size_t)i * c->L.cap_l;
+    }
+    c->par = dst_b;
+    c->p2p_live = true;
+    int64_t blo, bhi;
+    block_of(n_out + J, c->world, c->rank, &blo, &bhi);
+    c->n_surv_local = std::max<int64_t>(0, std::min(bhi, n_out) - std::min(blo, n_out));
   } else {
     std::vector<int64_t> sc(c->world), so(c->world), rc(c->world), ro(c->world);
     phd_plan_exchange(c->world, c->rank, bounds.data(), n_out, J, sc.data(), so.data(), rc.data(), ro.data());

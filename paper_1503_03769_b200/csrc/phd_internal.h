@@ -166,6 +166,17 @@ cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_
                           const float* x, const float* vx, const float* y, const float* vy, float w_off,
                           float* ox, float* ovx, float* oy, float* ovy, float* ow, int32_t* anc,
                           int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out, cudaStream_t s);
+// fused resample + exchange (world > 1, peer-memory window)
+constexpr int kMaxPeers = 16;
+struct PeerOut {
+  float* dst[kMaxPeers][5];   // owner q's next-step arrays x, vx, y, vy, w (peer pointers)
+  int64_t blo[kMaxPeers + 1]; // next-step block partition of N' = n_out + J
+  int world;
+};
+cudaError_t launch_gather_p2p(const int32_t* marks, const int32_t* bmax_excl, int64_t n, int64_t g0, const float* x,
+                              const float* vx, const float* y, const float* vy, float w_off, const PeerOut& po,
+                              int32_t* anc, int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out,
+                              cudaStream_t s);
 cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 // label selection before pass 2 (k_select.cu)
 cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cudaStream_t s);

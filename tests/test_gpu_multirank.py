@@ -73,6 +73,7 @@ def _run(phd, cfg, world, steps):
             t.join(timeout=300)
         assert not errs, errs
         out["summ"].append(fs[0]._sum.as_dict())
+        out.setdefault("xpath", set()).add(fs[0].exchange_path())
         out["est"].append(fs[0]._estimates())
         anc = []
         for f in fs:
@@ -90,15 +91,20 @@ def _run(phd, cfg, world, steps):
 
 
 @pytest.mark.parametrize("cname", ["cfg3", "cfg4"])
-@pytest.mark.parametrize("world,gate", [(2, 0), (3, 0), (4, 0), (2, 2), (3, 1)])
-def test_p_invariance(phd, cname, world, gate):
+@pytest.mark.parametrize("world,gate,xch", [(2, 0, "p2p"), (3, 0, "p2p"), (4, 0, "p2p"), (2, 2, "p2p"), (3, 1, "p2p"),
+                                            (3, 0, "nccl"), (4, 2, "nccl")])
+def test_p_invariance(phd, cname, world, gate, xch, monkeypatch):
     """gate = 1/2: the gated update (collective gated/dense decision, per-rank
-    tiles) against its own world = 1 run."""
+    tiles) against its own world = 1 run.  xch: the fused gather + exchange over
+    the peer-memory window (default) or the send/recv exchange (PHD_EXCHANGE=nccl)."""
+    if xch == "nccl":
+        monkeypatch.setenv("PHD_EXCHANGE", "nccl")
     cfg = _cfg(cname)
     cfg = replace(cfg, model=replace(cfg.model, gate=gate))
     steps = 3
     ref = _run(phd, cfg, 1, steps)
     got = _run(phd, cfg, world, steps)
+    assert got["xpath"] == {2 if xch == "p2p" else 1}
     identical_so_far = True
     for k in range(steps):
         s1, sp = ref["summ"][k], got["summ"][k]
