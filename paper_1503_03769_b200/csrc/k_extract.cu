@@ -99,7 +99,44 @@ __global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restri
     cl[i] = 0x7fffffff;
   }
   __syncthreads();
-  // bitonic sort of the n_sel selected, order = before()
+  if (n2 <= nthr) {
+    // one element per thread in registers: partner exchanges by shuffle for
+    // j < 32, through shared memory above (labels are unique: before() is strict)
+    double w = tid < n2 ? cw[tid] : -1.0;
+    int l = tid < n2 ? cl[tid] : 0x7fffffff;
+    for (int k = 2; k <= n2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        double pw;
+        int pl;
+        if (j >= 32) {
+          __syncthreads();
+          if (tid < n2) {
+            cw[tid] = w;
+            cl[tid] = l;
+          }
+          __syncthreads();
+          pw = tid < n2 ? cw[tid ^ j] : -1.0;
+          pl = tid < n2 ? cl[tid ^ j] : 0x7fffffff;
+        } else {
+          pw = __shfl_xor_sync(0xffffffffu, w, j);
+          pl = __shfl_xor_sync(0xffffffffu, l, j);
+        }
+        const bool want_first = ((tid & j) == 0) == ((tid & k) == 0);
+        const bool take = want_first ? before(pw, pl, w, l) : before(w, l, pw, pl);
+        if (take && tid < n2) {
+          w = pw;
+          l = pl;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < n2) {
+      cw[tid] = w;
+      cl[tid] = l;
+    }
+    __syncthreads();
+  } else
+  // bitonic sort of the n_sel selected in shared memory, order = before()
   for (int k = 2; k <= n2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = tid; i < n2; i += nthr) {

@@ -12,7 +12,7 @@
 //      range-bearing sensor); a stable counting sort orders the particle
 //      indices by cell, and k_gate_gather writes a sorted copy of the state
 //      (the filter's own particle order, which defines resampling, is untouched).
-//   2. k_gate_zbin: measurements binned into the same cells (one CTA).
+//   2. gate_zbin: measurements binned into the same cells (the same counting sort).
 //   3. k_gate_tiles: per tile of kGateTP sorted particles, the bounding box and
 //      max log2(p_D c w); a measurement is a candidate of the tile iff
 //         e_max = -alpha0 dx^2 - alpha1 dy^2 + max_i log2(p_D c w_i) >= -130
@@ -207,6 +207,13 @@ struct KeyCell {
   __device__ __forceinline__ int32_t raw(int64_t i) const { return cell_key(__ldg(a0 + i), __ldg(a1 + i), g); }
 };
 
+struct KeyZ {  // measurement l = (z[2l], z[2l+1]) -> its cell
+  const float* z;
+  GateGrid g;
+  __device__ __forceinline__ int digit(int32_t raw) const { return raw; }
+  __device__ __forceinline__ int32_t raw(int64_t i) const { return cell_key(__ldg(z + 2 * i), __ldg(z + 2 * i + 1), g); }
+};
+
 template <class KF>
 __global__ void __launch_bounds__(256) k_ms_hist(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk, int32_t* hist,
                                                  int32_t* keys_out = nullptr) {
@@ -324,7 +331,7 @@ cudaError_t ms_pass(KF kf, const int32_t* vals, int64_t n, int64_t per_blk, int 
 cudaError_t csort_pass(const int32_t* keys, const int32_t* vals, int64_t n, int shift, int nbins, int32_t* hist,
                        int32_t* scan_tmp, int32_t* out_keys, int32_t* out_vals, cudaStream_t s, int64_t* launches) {
   KeyArr kf{keys, shift, std::max(2, nbins) - 1};
-  return ms_pass(kf, vals, n, kESortBlock, nbins, hist, scan_tmp, out_keys, out_vals, s, launches);
+  return ms_pass(kf, vals, n, sort_block(n), nbins, hist, scan_tmp, out_keys, out_vals, s, launches);
 }
 
 // ---------------------------------------------------------------------------
@@ -349,8 +356,8 @@ __global__ void k_psort_pad(int64_t n, int64_t n_pad, GateSorted so) {
 
 template <int MODEL>
 __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int32_t* __restrict__ keys, int64_t n,
-                                                       int nblk, const int32_t* __restrict__ hs, float wscale,
-                                                       GateSorted so) {
+                                                       int64_t per_blk, int nblk, const int32_t* __restrict__ hs,
+                                                       float wscale, GateSorted so) {
   constexpr bool RB = MODEL == kRangeBearing;
   constexpr int N4 = RB ? 4 : 2;
   constexpr int ROWS = RB ? 2 : 4;
@@ -361,9 +368,9 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int j = tid; j < kMsWarps * nw; j += blockDim.x) wh[j] = 0u;
   __syncthreads();
-  const int64_t i0 = (int64_t)blockIdx.x * kPSortBlock;
-  const int64_t i1 = min(n, i0 + (int64_t)kPSortBlock);
-  const int64_t pw = kPSortBlock / kMsWarps;
+  const int64_t i0 = (int64_t)blockIdx.x * per_blk;
+  const int64_t i1 = min(n, i0 + per_blk);
+  const int64_t pw = per_blk / kMsWarps;
   const int64_t w0 = min(i1, i0 + warp * pw), w1 = min(i1, w0 + pw);
   uint32_t* my = wh + warp * nw;
   // 1. per-warp sub-histograms
@@ -421,59 +428,6 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
 #pragma unroll
         for (int k = 0; k < N4; ++k) dst[k] = q[r][k];
         so.inv[i] = pos;
-      }
-      __syncwarp();
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// measurements -> cells (one CTA of 1024): zcell_start[kGateBins + 1], items
-// stable by label within a cell (warp 0 walks the labels in order)
-__global__ void __launch_bounds__(1024) k_gate_zbin(const float* __restrict__ z, int M, GateGrid g,
-                                                    int32_t* zkey, int32_t* zcell_start, int32_t* zcell_items,
-                                                    float2* zcell_z) {
-  __shared__ int h[kGateBins];
-  __shared__ int sh[33];
-  for (int b = threadIdx.x; b < kGateBins; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  for (int l = threadIdx.x; l < M; l += blockDim.x) {
-    int k = cell_key(z[2 * l], z[2 * l + 1], g);
-    zkey[l] = k;
-    atomicAdd(&h[k], 1);
-  }
-  __syncthreads();
-  // exclusive scan of 4096 bins (4 per thread)
-  int v[4], s = 0;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    v[r] = h[threadIdx.x * 4 + r];
-    s += v[r];
-  }
-  int tot;
-  int e = block_excl_scan_1024(s, sh, &tot);
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    zcell_start[threadIdx.x * 4 + r] = e;
-    h[threadIdx.x * 4 + r] = e;
-    e += v[r];
-  }
-  if (threadIdx.x == 0) zcell_start[kGateBins] = tot;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int b = 0; b < M; b += 32) {
-      int l = b + lane;
-      bool ok = l < M;
-      int k = ok ? zkey[l] : kGateBins + lane;
-      unsigned peers = __match_any_sync(0xffffffffu, k);
-      int pos = ok ? h[k] + __popc(peers & lt) : 0;
-      __syncwarp();
-      if (ok) {
-        if (lane == __ffs(peers) - 1) h[k] += __popc(peers);
-        zcell_items[pos] = l;
-        zcell_z[pos] = make_float2(z[2 * l], z[2 * l + 1]);
       }
       __syncwarp();
     }
@@ -994,7 +948,8 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
   src.y = A[2];
   src.vy = A[3];
   src.w = A[4];
-  const int nblk = (int)((n + kPSortBlock - 1) / kPSortBlock);
+  const int64_t per_blk = sort_block(n);
+  const int nblk = (int)((n + per_blk - 1) / per_blk);
   const size_t smem = sizeof(uint32_t) * (size_t)kMsWarps * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins;
   static bool attr = false;
   if (!attr) {
@@ -1002,21 +957,43 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
     cudaFuncSetAttribute(k_psort_scatter<kPosIso>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_ms_hist<KeyCell><<<nblk, 256, 0, s>>>(kf, n, kPSortBlock, kGateBins, nblk, hist, keys);
+  k_ms_hist<KeyCell><<<nblk, 256, 0, s>>>(kf, n, per_blk, kGateBins, nblk, hist, keys);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
   if (rbm)
-    k_psort_scatter<kRangeBearing><<<nblk, 256, smem, s>>>(src, keys, n, nblk, hist, wscale, so);
+    k_psort_scatter<kRangeBearing><<<nblk, 256, smem, s>>>(src, keys, n, per_blk, nblk, hist, wscale, so);
   else
-    k_psort_scatter<kPosIso><<<nblk, 256, smem, s>>>(src, keys, n, nblk, hist, wscale, so);
+    k_psort_scatter<kPosIso><<<nblk, 256, smem, s>>>(src, keys, n, per_blk, nblk, hist, wscale, so);
   ++*launches;
   return cudaGetLastError();
 }
 
-cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,
-                      int32_t* zcell_items, float2* zcell_z, cudaStream_t s) {
-  k_gate_zbin<<<1, 1024, 0, s>>>(z, M, grid, zkey, zcell_start, zcell_items, zcell_z);
+// measurement bins by the same stable counting sort (multi-warp; the single-CTA
+// k_gate_zbin took ~40 us at M = 4096): zcell_items = labels by cell, zcell_start
+// = the scanned histogram's first column, zcell_z = coordinates in cell order
+__global__ void k_zbin_finish(const int32_t* __restrict__ hs, int nblk, const float* __restrict__ z,
+                              const int32_t* __restrict__ items, int M, int32_t* zcell_start, float2* zcell_z) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < kGateBins) zcell_start[i] = hs[(int64_t)i * nblk];
+  if (i == kGateBins) zcell_start[kGateBins] = M;
+  if (i < M) {
+    const int l = items[i];
+    zcell_z[i] = make_float2(z[2 * l], z[2 * l + 1]);
+  }
+}
+
+cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
+                      int32_t* zcell_start, int32_t* zcell_items, float2* zcell_z, cudaStream_t s, int64_t* launches) {
+  if (M <= 0) return cudaSuccess;
+  KeyZ kf{z, grid};
+  const int64_t per_blk = sort_block(M);
+  const int nblk = (int)((M + per_blk - 1) / per_blk);
+  cudaError_t e = ms_pass(kf, nullptr, M, per_blk, kGateBins, hist, scan_tmp, nullptr, zcell_items, s, launches);
+  if (e != cudaSuccess) return e;
+  const int nt = std::max(M, kGateBins + 1);
+  k_zbin_finish<<<(nt + 255) / 256, 256, 0, s>>>(hist, nblk, z, zcell_items, M, zcell_start, zcell_z);
+  ++*launches;
   return cudaGetLastError();
 }
 
@@ -1044,7 +1021,7 @@ cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kb
     // one pass: the scanned histogram's first column is the label offsets
     cudaError_t e = csort_pass(cand, nullptr, E, 0, 1 << bits, hist, scan_tmp, nullptr, mlist, s, launches);
     if (e != cudaSuccess) return e;
-    const int nblk = (int)((E + kESortBlock - 1) / kESortBlock);
+    const int nblk = (int)((E + sort_block(E) - 1) / sort_block(E));
     k_mstart_from_hist<<<(M + 256) / 256, 256, 0, s>>>(hist, nblk, M, (int32_t)E, mstart);
     ++*launches;
     return cudaGetLastError();

@@ -102,8 +102,8 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.g_npad = align_up((size_t)L.cap_l, kGateTP);
   L.g_ntiles = (int)(L.g_npad / kGateTP);
   L.g_ecap = std::max<int64_t>((int64_t)1 << 20, (int64_t)L.g_ntiles * std::min(p->max_meas, 256));
-  L.g_hist = std::max<int64_t>((int64_t)kGateBins * ceil_div(L.cap_l, kPSortBlock),
-                               (int64_t)kSortMaxBins * ceil_div(L.g_ecap, kESortBlock)) + 1;
+  L.g_hist = std::max<int64_t>((int64_t)kGateBins * sort_blocks_max(L.cap_l),
+                               (int64_t)kSortMaxBins * sort_blocks_max(L.g_ecap)) + 1;
   L.g_scan = ceil_div(std::max<int64_t>(L.g_hist, L.g_ntiles + (int64_t)p->max_meas + 2), 4096) + 2;
   L.g_nsorted = p->meas == PHD_MEAS_RANGE_BEARING ? 13 : 5;
   auto gtake = [&](size_t bytes) { return take(gt ? bytes : 256); };
@@ -899,7 +899,7 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   const float* A[5] = {c->A[0], c->A[1], c->A[2], c->A[3], c->A[4]};
   CU(gate_sort_particles(c->model, A, c->rb, c->L.cap_l, n, npad, c->wscale, c->ggrid, c->ghist, c->gscan,
                          c->gkeys, c->gso, c->st, &c->launches));
-  KL(gate_zbin(c->zlab, M, c->ggrid, c->gzkey, c->gzstart, c->gzitems, c->gzz, c->st));
+  CU(gate_zbin(c->zlab, M, c->ggrid, c->ghist, c->gscan, c->gzstart, c->gzitems, c->gzz, c->st, &c->launches));
   int64_t tot = 0;
   if (ntiles > 0) {
     KL(gate_tiles(0, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->gzz, c->gtstart,

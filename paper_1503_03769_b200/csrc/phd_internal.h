@@ -196,8 +196,19 @@ cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, 
 // 2^e flushes to exactly 0 in the dense kernels too (ex2.approx.ftz).
 constexpr int kGateG = 64;            // cells per axis (Morton key of 12 bits)
 constexpr int kGateBins = kGateG * kGateG;
-constexpr int kPSortBlock = 65536;    // particles per counting-sort block (8 warps)
-constexpr int kESortBlock = 16384;    // candidate entries per counting-sort block
+// Counting-sort blocks (8 warps each): sort_block(n) items per block, a power of two
+// in [kSortBlockMin, kSortBlockMax] giving about kSortBlocks blocks, so small sorts
+// still fill the GPU and the 16-bit per-warp counters never overflow.
+constexpr int kSortBlockMin = 2048;
+constexpr int kSortBlockMax = 65536;
+constexpr int kSortBlocks = 256;
+inline int64_t sort_block(int64_t n) {
+  int64_t b = kSortBlockMin;
+  while (b < kSortBlockMax && b * kSortBlocks < n) b <<= 1;
+  return b;
+}
+// upper bound of the block count for n <= cap items (hist / scan buffers)
+inline int64_t sort_blocks_max(int64_t cap) { return (cap + sort_block(cap) - 1) / sort_block(cap) + kSortBlocks + 1; }
 constexpr int kSortMaxBins = 4096;    // bins per counting-sort pass (12-bit digits)
 constexpr int kGateTP = 512;          // particles per tile (256 threads x 2, f32x2)
 constexpr int kGateChunk = 256;       // candidates staged in shared memory at a time
@@ -243,8 +254,8 @@ cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/
                                 int32_t* scan_tmp, int32_t* keys /*[n] scratch*/, const GateSorted& so, cudaStream_t s,
                                 int64_t* launches);
 // measurements -> grid cells (one CTA): zcell_start[kGateBins + 1], items stable by label
-cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* zkey, int32_t* zcell_start,
-                      int32_t* zcell_items, float2* zcell_z, cudaStream_t s);
+cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
+                      int32_t* zcell_start, int32_t* zcell_items, float2* zcell_z, cudaStream_t s, int64_t* launches);
 // per-tile bounding boxes + candidate counts (fill = 0) or labels (fill = 1)
 // (fill = 0 also buffers the first kGateKBuf candidates per tile in cbuf [ntiles][kGateKBuf])
 constexpr int kGateKBufH = 512;
