@@ -179,8 +179,11 @@ __device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PA
 }
 
 // ZL = measurement slots per lane (4 or 8); the CTA covers wz * 32 * ZL slots.
+#ifndef PHD_PASS_MINB8
+#define PHD_PASS_MINB8 2
+#endif
 template <int MODEL, int PASS, int ZL>
-__global__ void __launch_bounds__(256, ZL == 8 ? 2 : 3) k_pass(const PassArgs a) {
+__global__ void __launch_bounds__(256, ZL == 8 ? PHD_PASS_MINB8 : 3) k_pass(const PassArgs a) {
   using L = RecLayout<MODEL, PASS>;
   constexpr int NQ = PASS == 1 ? 1 : 4;  // pass 2: S'x, Svx, S'y, Svy (dW = C/D from pass 1)
   constexpr int NP = ZL / 2;

@@ -45,7 +45,7 @@ struct Layout {
   int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
   int g_ntiles = 0, g_nsorted = 0;
   size_t o_gkeys, o_ginv, o_gsorted[13], o_gPs, o_ghist, o_gscan, o_gtstart, o_gcand, o_gk, o_gv, o_gmlist,
-      o_gpart1, o_gpart2, o_gmstart, o_gzkey, o_gzstart, o_gzitems, o_gzz, o_gcbuf, o_gA;
+      o_gpart1, o_gpart2, o_gmstart, o_gzstart, o_gzitems, o_gzz, o_gcbuf, o_gA;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -121,7 +121,6 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_gpart1 = gtake(sizeof(double) * L.g_ecap);
   L.o_gpart2 = gtake(sizeof(float) * 4 * L.g_ecap);
   L.o_gmstart = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 2));
-  L.o_gzkey = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 1));
   L.o_gzstart = gtake(sizeof(int32_t) * (kGateBins + 1));
   L.o_gzitems = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 1));
   L.o_gzz = gtake(sizeof(float) * 2 * ((size_t)p->max_meas + 1));
@@ -210,7 +209,7 @@ struct phd_ctx {
   GateSorted gso{};
   GateGrid ggrid{};
   int32_t *gkeys = nullptr, *ghist = nullptr, *gscan = nullptr, *gtstart = nullptr, *gcand = nullptr, *gk = nullptr,
-          *gv = nullptr, *gmlist = nullptr, *gmstart = nullptr, *gzkey = nullptr, *gzstart = nullptr,
+          *gv = nullptr, *gmlist = nullptr, *gmstart = nullptr, *gzstart = nullptr,
           *gzitems = nullptr, *gcbuf = nullptr;
   float2* gzz = nullptr;
   float *gPs = nullptr, *gpart2 = nullptr;
@@ -533,7 +532,6 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
     c->gpart1 = at<double>(c->ws, L.o_gpart1);
     c->gpart2 = at<float>(c->ws, L.o_gpart2);
     c->gmstart = at<int32_t>(c->ws, L.o_gmstart);
-    c->gzkey = at<int32_t>(c->ws, L.o_gzkey);
     c->gzstart = at<int32_t>(c->ws, L.o_gzstart);
     c->gzitems = at<int32_t>(c->ws, L.o_gzitems);
     c->gzz = at<float2>(c->ws, L.o_gzz);
