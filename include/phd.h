@@ -23,6 +23,10 @@
  *  - Ownership: the ctx owns its device memory (allocated once in phd_create,
  *    or carved from a caller workspace of phd_workspace_size() bytes that the
  *    caller keeps alive until phd_destroy).  No allocation happens in a step.
+ *    With world > 1 (exact mode) phd_create also allocates, outside the
+ *    workspace, the particle double buffers that the ranks map into each other
+ *    (CUDA IPC) for the fused resample + exchange (2 x 20 bytes x the rank's
+ *    capacity).
  *    Host arrays passed in are borrowed for the duration of the call; outputs
  *    are caller-allocated.  Pointers to measurement / particle arrays may be
  *    host or device pointers (copied with cudaMemcpyDefault).

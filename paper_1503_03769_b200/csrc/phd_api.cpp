@@ -579,6 +579,23 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
     if (!c->comm) return bail(fail(c, PHD_ENCCL, "%s", e.c_str()));
   }
   CUB(cudaMemsetAsync(c->ws, 0, L.total, c->st));
+  {
+    // particle double buffers of the peer-memory window (world > 1, exact mode), mapped
+    // by the other ranks at the first resampling (p2p_setup); allocated here so that no
+    // step allocates.  A failed allocation just keeps the send/recv exchange.
+    const char* xch = getenv("PHD_EXCHANGE");
+    if (world > 1 && !c->dcp && world <= kMaxPeers && !(xch && strcmp(xch, "nccl") == 0)) {
+      const size_t bytes = sizeof(float) * 5 * (size_t)L.cap_l;
+      for (int b = 0; b < 2; ++b) {
+        if (cudaMalloc(&c->pbuf[b], bytes) != cudaSuccess) {
+          c->pbuf[b] = nullptr;
+          cudaGetLastError();
+        } else {
+          CUB(cudaMemsetAsync(c->pbuf[b], 0, bytes, c->st));
+        }
+      }
+    }
+  }
   CUB(cudaStreamSynchronize(c->st));
 
 #undef CUB
@@ -1308,25 +1325,18 @@ phd_status phd_get_local_estimates(phd_ctx* c, phd_estimate* out, int32_t cap, i
   return PHD_OK;
 }
 
-// Peer-memory window for the fused resample + exchange, set up at
+// Peer-memory window for the fused resample + exchange, shared at
 // the first multi-rank resampling (a collective point: the ranks of an in-process
 // group are created one after another, but step in parallel).  The particle double
-// buffers become library allocations every rank maps; any failure (no IPC / peer
-// access, PHD_EXCHANGE=nccl) keeps the send/recv exchange.
+// buffers are library allocations (phd_create) every rank maps; any failure (no
+// IPC / peer access, PHD_EXCHANGE=nccl) keeps the send/recv exchange.
 static phd_status p2p_setup(phd_ctx* c) {
   const char* xch = getenv("PHD_EXCHANGE");
   if (c->world <= 1 || c->dcp || c->world > kMaxPeers || (xch && strcmp(xch, "nccl") == 0)) {
     c->p2p_state = -1;
     return PHD_OK;
   }
-  const size_t bytes = sizeof(float) * 5 * (size_t)c->L.cap_l;
-  bool ok = cudaMalloc(&c->pbuf[0], bytes) == cudaSuccess;
-  ok = (cudaMalloc(&c->pbuf[1], bytes) == cudaSuccess) && ok;
-  cudaGetLastError();
-  if (ok) {
-    CU(cudaMemsetAsync(c->pbuf[0], 0, bytes, c->st));
-    CU(cudaMemsetAsync(c->pbuf[1], 0, bytes, c->st));
-  }
+  const bool ok = c->pbuf[0] && c->pbuf[1];  // allocated by phd_create
   std::vector<void*> all;
   void* loc[2] = {c->pbuf[0], c->pbuf[1]};
   // collective on every rank; a rank without buffers fails IPC and the verdict falls back everywhere
