@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restri
                                                           const double* __restrict__ Wv, const double* __restrict__ Wpv,
                                                           int count, double p_d, EstOut* est, int cap, double* summary,
                                                           int32_t* count_out, const double* sel_info) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char sm[];
   const int n2m = M <= 1 ? 1 : 1 << (32 - __clz(M - 1));  // next power of two >= M
   unsigned long long* kw = reinterpret_cast<unsigned long long*>(sm);
@@ -180,7 +181,7 @@ cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const 
     cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 20);
     attr_set = true;
   }
-  k_extract<<<1, kTopkThreads, smem, s>>>(acc_lab, M, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
+  pdl_launch(k_extract, 1, kTopkThreads, smem, s, acc_lab, M, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
                                           count_out, sel_info);
   return cudaGetLastError();
 }

@@ -133,6 +133,7 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* sh, int* total) 
 }
 
 __global__ void __launch_bounds__(1024) k_scan_sum(const int32_t* __restrict__ a, int64_t n, int32_t* csum) {
+  pdl_wait();
   __shared__ int sh[33];
   const int64_t base = (int64_t)blockIdx.x * kScanChunk + threadIdx.x * 4;
   int s = 0;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(1024) k_scan_sum(const int32_t* __restrict__ a
 
 // one CTA: exclusive scan of csum[0..nc), csum[nc] = total, *total_out = total
 __global__ void __launch_bounds__(1024) k_scan_top(int32_t* csum, int nc, int32_t* total_out) {
+  pdl_wait();
   __shared__ int sh[33];
   int carry = 0;
   for (int b = 0; b < nc; b += 1024) {
@@ -163,6 +165,7 @@ __global__ void __launch_bounds__(1024) k_scan_top(int32_t* csum, int nc, int32_
 }
 
 __global__ void __launch_bounds__(1024) k_scan_apply(int32_t* a, int64_t n, const int32_t* __restrict__ csum) {
+  pdl_wait();
   __shared__ int sh[33];
   const int64_t base = (int64_t)blockIdx.x * kScanChunk + threadIdx.x * 4;
   int v[4];
@@ -217,6 +220,7 @@ struct KeyZ {  // measurement l = (z[2l], z[2l+1]) -> its cell
 template <class KF>
 __global__ void __launch_bounds__(256) k_ms_hist(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk, int32_t* hist,
                                                  int32_t* keys_out = nullptr) {
+  pdl_wait();
   __shared__ int h[kSortMaxBins];
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
   __syncthreads();
@@ -236,6 +240,7 @@ template <class KF>
 __global__ void __launch_bounds__(256) k_ms_scatter(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk,
                                                     const int32_t* __restrict__ hs, const int32_t* __restrict__ vals,
                                                     int32_t* out_keys, int32_t* out_vals) {
+  pdl_wait();
   extern __shared__ uint32_t sm[];
   const int nw = nbins >> 1;  // nbins even
   uint32_t* wh = sm;
@@ -319,11 +324,11 @@ cudaError_t ms_pass(KF kf, const int32_t* vals, int64_t n, int64_t per_blk, int 
                          (int)(sizeof(uint32_t) * kMsWarps * (kSortMaxBins / 2) + sizeof(int) * kSortMaxBins));
     attr = true;
   }
-  k_ms_hist<KF><<<nblk, 256, 0, s>>>(kf, n, per_blk, nbins, nblk, hist);
+  pdl_launch(k_ms_hist<KF>, nblk, 256, 0, s, kf, n, per_blk, nbins, nblk, hist, nullptr);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)nbins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
-  k_ms_scatter<KF><<<nblk, 256, smem, s>>>(kf, n, per_blk, nbins, nblk, hist, vals, out_keys, out_vals);
+  pdl_launch(k_ms_scatter<KF>, nblk, 256, smem, s, kf, n, per_blk, nbins, nblk, hist, vals, out_keys, out_vals);
   ++*launches;
   return cudaGetLastError();
 }
@@ -347,6 +352,7 @@ struct GatherSrc {
 
 // padding records [n, n_pad): zero state, lw = -inf
 __global__ void k_psort_pad(int64_t n, int64_t n_pad, GateSorted so) {
+  pdl_wait();
   const int64_t p = n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pad) return;
   float4* r = so.rec + p * so.n4;
@@ -358,6 +364,7 @@ template <int MODEL>
 __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int32_t* __restrict__ keys, int64_t n,
                                                        int64_t per_blk, int nblk, const int32_t* __restrict__ hs,
                                                        float wscale, GateSorted so) {
+  pdl_wait();
   constexpr bool RB = MODEL == kRangeBearing;
   constexpr int N4 = RB ? 4 : 2;
   constexpr int ROWS = RB ? 2 : 4;
@@ -545,6 +552,7 @@ __global__ void __launch_bounds__(256) k_gate_count(const RecView rv, int ntiles
                                                     GateGrid g, const int32_t* __restrict__ zcell_start,
                                                     const int32_t* __restrict__ zcell_items,
                                                     const float2* __restrict__ zcell_z, int32_t* tcount, int32_t* cbuf) {
+  pdl_wait();
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
   const int total = tile_enum(t, rv, na0, na1, g, zcell_start, zcell_items, zcell_z,
@@ -559,6 +567,7 @@ __global__ void __launch_bounds__(256) k_gate_fill(const RecView rv, int ntiles,
                                                    const int32_t* __restrict__ zcell_items,
                                                    const float2* __restrict__ zcell_z, const int32_t* __restrict__ tstart,
                                                    const int32_t* __restrict__ cbuf, int32_t* cand) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
@@ -572,17 +581,20 @@ __global__ void __launch_bounds__(256) k_gate_fill(const RecView rv, int ntiles,
 
 // per-label entry counts (integer atomics: order-independent)
 __global__ void k_gate_count_labels(const int32_t* __restrict__ cand, int64_t E, int32_t* cnt) {
+  pdl_wait();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < E) atomicAdd(&cnt[cand[e]], 1);
 }
 
 __global__ void k_mstart_from_hist(const int32_t* __restrict__ hs, int nblk, int M, int32_t E, int32_t* mstart) {
+  pdl_wait();
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l < M) mstart[l] = hs[(int64_t)l * nblk];
   if (l == M) mstart[M] = E;
 }
 
 __global__ void k_zero_i32(int32_t* a, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = 0;
 }
@@ -603,6 +615,7 @@ struct GPair {
 template <int MODEL, int PASS, int NPAIR>
 __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing && PASS == 2) ? 5 : 8)
     k_gpass(const GateArgs g) {
+  pdl_wait();
   constexpr bool RB = MODEL == kRangeBearing;
   constexpr int THREADS = kGateTP / (2 * NPAIR);  // particle pairs (tid + 2 THREADS h, + THREADS) per thread
   constexpr int WARPS = THREADS / 32;
@@ -883,6 +896,7 @@ __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__
                                                      int M, const double* __restrict__ part1,
                                                      const float4* __restrict__ part2, const int32_t* __restrict__ sel,
                                                      double* out, int slots_pad) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (l >= slots_pad) return;
@@ -924,9 +938,9 @@ __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__
 cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;
   const int nc = (int)((n + kScanChunk - 1) / kScanChunk);
-  k_scan_sum<<<nc, 1024, 0, s>>>(a, n, tmp);
-  k_scan_top<<<1, 1024, 0, s>>>(tmp, nc, a + n);
-  k_scan_apply<<<nc, 1024, 0, s>>>(a, n, tmp);
+  pdl_launch(k_scan_sum, nc, 1024, 0, s, a, n, tmp);
+  pdl_launch(k_scan_top, 1, 1024, 0, s, tmp, nc, a + n);
+  pdl_launch(k_scan_apply, nc, 1024, 0, s, a, n, tmp);
   *launches += 3;
   return cudaGetLastError();
 }
@@ -936,7 +950,7 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
                                 int32_t* keys, const GateSorted& so, cudaStream_t s, int64_t* launches) {
   const bool rbm = model == kRangeBearing;
   if (n_pad > n) {
-    k_psort_pad<<<(unsigned)((n_pad - n + 255) / 256), 256, 0, s>>>(n, n_pad, so);
+    pdl_launch(k_psort_pad, (unsigned)((n_pad - n + 255) / 256), 256, 0, s, n, n_pad, so);
     ++*launches;
   }
   if (n <= 0) return cudaGetLastError();
@@ -957,14 +971,14 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
     cudaFuncSetAttribute(k_psort_scatter<kPosIso>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_ms_hist<KeyCell><<<nblk, 256, 0, s>>>(kf, n, per_blk, kGateBins, nblk, hist, keys);
+  pdl_launch(k_ms_hist<KeyCell>, nblk, 256, 0, s, kf, n, per_blk, kGateBins, nblk, hist, keys);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
   if (rbm)
-    k_psort_scatter<kRangeBearing><<<nblk, 256, smem, s>>>(src, keys, n, per_blk, nblk, hist, wscale, so);
+    pdl_launch(k_psort_scatter<kRangeBearing>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so);
   else
-    k_psort_scatter<kPosIso><<<nblk, 256, smem, s>>>(src, keys, n, per_blk, nblk, hist, wscale, so);
+    pdl_launch(k_psort_scatter<kPosIso>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so);
   ++*launches;
   return cudaGetLastError();
 }
@@ -974,6 +988,7 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
 // = the scanned histogram's first column, zcell_z = coordinates in cell order
 __global__ void k_zbin_finish(const int32_t* __restrict__ hs, int nblk, const float* __restrict__ z,
                               const int32_t* __restrict__ items, int M, int32_t* zcell_start, float2* zcell_z) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < kGateBins) zcell_start[i] = hs[(int64_t)i * nblk];
   if (i == kGateBins) zcell_start[kGateBins] = M;
@@ -992,7 +1007,7 @@ cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* hist
   cudaError_t e = ms_pass(kf, nullptr, M, per_blk, kGateBins, hist, scan_tmp, nullptr, zcell_items, s, launches);
   if (e != cudaSuccess) return e;
   const int nt = std::max(M, kGateBins + 1);
-  k_zbin_finish<<<(nt + 255) / 256, 256, 0, s>>>(hist, nblk, z, zcell_items, M, zcell_start, zcell_z);
+  pdl_launch(k_zbin_finish, (nt + 255) / 256, 256, 0, s, hist, nblk, z, zcell_items, M, zcell_start, zcell_z);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1006,10 +1021,10 @@ cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, fl
   RecView rv{f, f + (rbm ? 2 : 1), f + 4 * (so.n4 - 1), 4 * so.n4};
   const unsigned blocks = (unsigned)((ntiles + 7) / 8);
   if (fill)
-    k_gate_fill<<<blocks, 256, 0, s>>>(rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tstart, cbuf,
+    pdl_launch(k_gate_fill, blocks, 256, 0, s, rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tstart, cbuf,
                                        cand);
   else
-    k_gate_count<<<blocks, 256, 0, s>>>(rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tcount, cbuf);
+    pdl_launch(k_gate_count, blocks, 256, 0, s, rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tcount, cbuf);
   return cudaGetLastError();
 }
 
@@ -1022,15 +1037,15 @@ cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kb
     cudaError_t e = csort_pass(cand, nullptr, E, 0, 1 << bits, hist, scan_tmp, nullptr, mlist, s, launches);
     if (e != cudaSuccess) return e;
     const int nblk = (int)((E + sort_block(E) - 1) / sort_block(E));
-    k_mstart_from_hist<<<(M + 256) / 256, 256, 0, s>>>(hist, nblk, M, (int32_t)E, mstart);
+    pdl_launch(k_mstart_from_hist, (M + 256) / 256, 256, 0, s, hist, nblk, M, (int32_t)E, mstart);
     ++*launches;
     return cudaGetLastError();
   }
   // mstart: per-label counts (integer atomics), exclusive scan (mstart[M] = E)
-  k_zero_i32<<<(M + 256) / 256, 256, 0, s>>>(mstart, M + 1);
+  pdl_launch(k_zero_i32, (M + 256) / 256, 256, 0, s, mstart, M + 1);
   ++*launches;
   if (E > 0) {
-    k_gate_count_labels<<<(unsigned)((E + 255) / 256), 256, 0, s>>>(cand, E, mstart);
+    pdl_launch(k_gate_count_labels, (unsigned)((E + 255) / 256), 256, 0, s, cand, E, mstart);
     ++*launches;
   }
   cudaError_t e = gate_scan(mstart, M, scan_tmp, s, launches);
@@ -1052,9 +1067,9 @@ static cudaError_t gpass_m(int pass, const GateArgs& g, cudaStream_t s) {
   // 0.42 -> 0.44 ms, so pass 1 keeps 4)
   constexpr int NP2 = MODEL == kRangeBearing ? 2 : PHD_GATE_NPAIR_POS;
   if (pass == 1)
-    k_gpass<MODEL, 1, 2><<<g.ntiles, kGateTP / 4, 0, s>>>(g);
+    pdl_launch(k_gpass<MODEL, 1, 2>, g.ntiles, kGateTP / 4, 0, s, g);
   else
-    k_gpass<MODEL, 2, NP2><<<g.ntiles, kGateTP / (2 * NP2), 0, s>>>(g);
+    pdl_launch(k_gpass<MODEL, 2, NP2>, g.ntiles, kGateTP / (2 * NP2), 0, s, g);
   return cudaGetLastError();
 }
 
@@ -1070,9 +1085,9 @@ cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* m
   if (slots_pad <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((slots_pad + 7) / 8);
   if (pass == 1)
-    k_gate_reduce<1><<<blocks, 256, 0, s>>>(mstart, mlist, M, part1, nullptr, nullptr, out, slots_pad);
+    pdl_launch(k_gate_reduce<1>, blocks, 256, 0, s, mstart, mlist, M, part1, nullptr, nullptr, out, slots_pad);
   else
-    k_gate_reduce<2><<<blocks, 256, 0, s>>>(mstart, mlist, M, nullptr, reinterpret_cast<const float4*>(part2), sel,
+    pdl_launch(k_gate_reduce<2>, blocks, 256, 0, s, mstart, mlist, M, nullptr, reinterpret_cast<const float4*>(part2), sel,
                                             out, slots_pad);
   return cudaGetLastError();
 }

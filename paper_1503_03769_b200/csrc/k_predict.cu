@@ -5,9 +5,19 @@
 // (20 B read + 20 B written per survivor; 20 B written per birth; +32 B of
 // range-bearing representation when that sensor is used).
 #include "phd_internal.h"
+
+#include <cstdlib>
 #include "philox.cuh"
 
 namespace phd {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PHD_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // Per-particle range-bearing representation, computed once in fp64 and split
 // into fp32 hi + lo (DESIGN.md §5 "seam-free residual"):
@@ -32,6 +42,7 @@ __device__ __forceinline__ void rb_repr(float xf, float yf, float sx, float sy, 
 }
 
 __global__ void __launch_bounds__(256) k_predict(const PredictArgs a) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n_local) return;
   int64_t g = a.g0 + i;
@@ -146,6 +157,7 @@ __device__ __forceinline__ double ex2d(double e) {  // 2^e via MUFU on the fp32-
 }
 
 __global__ void __launch_bounds__(256) k_birth_is(const BirthISArgs a) {
+  pdl_wait();
   __shared__ double zc0[kISChunk], zc1[kISChunk], wc[kISChunk];
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = t < a.nb;
@@ -217,17 +229,19 @@ __global__ void __launch_bounds__(256) k_birth_is(const BirthISArgs a) {
 
 cudaError_t launch_birth_is(const BirthISArgs& a, cudaStream_t s) {
   if (a.nb <= 0) return cudaSuccess;
-  k_birth_is<<<(unsigned)((a.nb + 255) / 256), 256, 0, s>>>(a);
+  pdl_launch(k_birth_is, (unsigned)((a.nb + 255) / 256), 256, 0, s, a);
   return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(256) k_rb_repr(const float* __restrict__ x, const float* __restrict__ y,
                                                  int64_t n, float sx, float sy, float* rb, int64_t stride) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) rb_repr(x[i], y[i], sx, sy, rb, stride, i);
 }
 
 __global__ void k_fill(float* p, float v, int64_t n) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
@@ -235,20 +249,20 @@ __global__ void k_fill(float* p, float v, int64_t n) {
 cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s) {
   if (a.n_local <= 0) return cudaSuccess;
   int64_t blocks = (a.n_local + 255) / 256;
-  k_predict<<<(unsigned)blocks, 256, 0, s>>>(a);
+  pdl_launch(k_predict, (unsigned)blocks, 256, 0, s, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, float sy, float* rb,
                            int64_t stride, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_rb_repr<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, y, n, sx, sy, rb, stride);
+  pdl_launch(k_rb_repr, (unsigned)((n + 255) / 256), 256, 0, s, x, y, n, sx, sy, rb, stride);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, v, n);
+  pdl_launch(k_fill, (unsigned)((n + 255) / 256), 256, 0, s, p, v, n);
   return cudaGetLastError();
 }
 
@@ -266,6 +280,7 @@ struct RankPtrs {
 };
 
 __global__ void k_sum_ranks(RankPtrs ptrs, int world, double* dst, size_t n) {
+  pdl_wait();
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -277,7 +292,7 @@ cudaError_t launch_sum_ranks(const double* const* srcs, int world, double* dst, 
   if (world > 16) return cudaErrorInvalidValue;
   RankPtrs rp{};
   for (int r = 0; r < world; ++r) rp.p[r] = srcs[r];
-  k_sum_ranks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rp, world, dst, n);
+  pdl_launch(k_sum_ranks, (unsigned)((n + 255) / 256), 256, 0, s, rp, world, dst, n);
   return cudaGetLastError();
 }
 

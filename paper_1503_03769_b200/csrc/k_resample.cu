@@ -20,6 +20,7 @@ __device__ __forceinline__ int64_t n_of(double B, double scale, double U, int64_
 // owns the contiguous chunk [t c, t c + c) (loads issued together), warp-shuffle
 // scan of the chunk sums, then the chunk is rewritten with its offsets.
 __global__ void __launch_bounds__(1024) k_scan_blocks(const double* __restrict__ blk, int nb, double* off) {
+  pdl_wait();
   __shared__ double ws[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = (nb + 1023) / 1024;
@@ -63,13 +64,14 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(const double* __restrict__
 }
 
 cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s) {
-  k_scan_blocks<<<1, 1024, 0, s>>>(blk, nb, blk_off);
+  pdl_launch(k_scan_blocks, 1, 1024, 0, s, blk, nb, blk_off);
   return cudaGetLastError();
 }
 
 // Per block of kBlockW particles: local fp64 inclusive prefix, offspring ranges,
 // and a mark at the first offspring of every particle with a non-empty range.
 __global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
+  pdl_wait();
   __shared__ double wsum[8];
   __shared__ int64_t his[kBlockW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
 cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s) {
   if (a.n_local <= 0) return cudaSuccess;
   unsigned nb = (unsigned)((a.n_local + kBlockW - 1) / kBlockW);
-  k_resample_mark<<<nb, 256, 0, s>>>(a);
+  pdl_launch(k_resample_mark, nb, 256, 0, s, a);
   return cudaGetLastError();
 }
 
@@ -172,6 +174,7 @@ __device__ __forceinline__ int warp_max_scan(int v, int lane) {
 }
 
 __global__ void __launch_bounds__(256) k_block_max(const int32_t* __restrict__ marks, int64_t n, int32_t* bmax) {
+  pdl_wait();
   __shared__ int wm[8];
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * kBlockOff;
@@ -194,12 +197,13 @@ __global__ void __launch_bounds__(256) k_block_max(const int32_t* __restrict__ m
 
 cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_block_max<<<(unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s>>>(marks, n, bmax);
+  pdl_launch(k_block_max, (unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s, marks, n, bmax);
   return cudaGetLastError();
 }
 
 // In place: bmax[b] <- max(bmax[0..b-1]) (exclusive; -1 for b = 0).  Chunked as k_scan_blocks.
 __global__ void __launch_bounds__(1024) k_scan_max(int32_t* bmax, int nb) {
+  pdl_wait();
   __shared__ int ws[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = (nb + 1023) / 1024;
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(1024) k_scan_max(int32_t* bmax, int nb) {
 
 cudaError_t launch_scan_max(int32_t* bmax, int nb, cudaStream_t s) {
   if (nb <= 0) return cudaSuccess;
-  k_scan_max<<<1, 1024, 0, s>>>(bmax, nb);
+  pdl_launch(k_scan_max, 1, 1024, 0, s, bmax, nb);
   return cudaGetLastError();
 }
 
@@ -258,6 +262,7 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ mark
                                                 const float* __restrict__ vy, float w_off, float* ox, float* ovx,
                                                 float* oy, float* ovy, float* ow, int32_t* anc, int zero_mass,
                                                 int64_t first, int64_t n_upd, int64_t n_out) {
+  pdl_wait();
   __shared__ int wm[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * kBlockOff;
@@ -338,7 +343,7 @@ cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_
                           float* oy, float* ovy, float* ow, int32_t* anc, int zero_mass, int64_t first,
                           int64_t n_global_upd, int64_t n_out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_gather<<<(unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s>>>(
+  pdl_launch(k_gather, (unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s, 
       marks, bmax_excl, n, g0, x, vx, y, vy, w_off, ox, ovx, oy, ovy, ow, anc, zero_mass, first, n_global_upd, n_out);
   return cudaGetLastError();
 }
@@ -355,6 +360,7 @@ __global__ void __launch_bounds__(256) k_gather_p2p(const int32_t* __restrict__ 
                                                     const float* __restrict__ vy, float w_off, const PeerOut po,
                                                     int32_t* anc, int zero_mass, int64_t first, int64_t n_upd,
                                                     int64_t n_out) {
+  pdl_wait();
   __shared__ int wm[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * kBlockOff;
@@ -408,7 +414,7 @@ cudaError_t launch_gather_p2p(const int32_t* marks, const int32_t* bmax_excl, in
                               int32_t* anc, int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out,
                               cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_gather_p2p<<<(unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s>>>(
+  pdl_launch(k_gather_p2p, (unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s, 
       marks, bmax_excl, n, g0, x, vx, y, vy, w_off, po, anc, zero_mass, first, n_global_upd, n_out);
   return cudaGetLastError();
 }
@@ -426,6 +432,7 @@ __device__ __forceinline__ int64_t ring_slot(int64_t i, int64_t n, int64_t L, do
 }
 
 __global__ void k_ring_pack(Arr5 src, Arr5 dst, int narr, int64_t L, int64_t n, double v) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L) return;
   int64_t sl = ring_slot(i, n, L, v);
@@ -433,6 +440,7 @@ __global__ void k_ring_pack(Arr5 src, Arr5 dst, int narr, int64_t L, int64_t n, 
 }
 
 __global__ void k_ring_unpack(Arr5 src, Arr5 dst, int narr, int64_t L, int64_t n, double v) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L) return;
   int64_t sl = ring_slot(i, n, L, v);
@@ -447,7 +455,7 @@ cudaError_t launch_ring_pack(float* const* src, float* const* dst, int narr, int
     a.p[q] = src[q];
     b.p[q] = dst[q];
   }
-  k_ring_pack<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(a, b, narr, L, n, v);
+  pdl_launch(k_ring_pack, (unsigned)((L + 255) / 256), 256, 0, s, a, b, narr, L, n, v);
   return cudaGetLastError();
 }
 
@@ -459,7 +467,7 @@ cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, i
     a.p[q] = src[q];
     b.p[q] = dst[q];
   }
-  k_ring_unpack<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(a, b, narr, L, n, v);
+  pdl_launch(k_ring_unpack, (unsigned)((L + 255) / 256), 256, 0, s, a, b, narr, L, n, v);
   return cudaGetLastError();
 }
 

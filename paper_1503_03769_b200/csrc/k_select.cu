@@ -17,6 +17,7 @@ namespace phd {
 
 // fp64 block sums of w (kBlockW per block), then one CTA reduces them to *out.
 __global__ void __launch_bounds__(256) k_block_sum(const float* __restrict__ w, int64_t n, double* blk) {
+  pdl_wait();
   __shared__ double sw[8];
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * kBlockW;
@@ -40,6 +41,7 @@ __global__ void __launch_bounds__(256) k_block_sum(const float* __restrict__ w, 
 // One CTA of 1024: thread t sums the contiguous chunk [t c, t c + c) of the
 // block sums (loads issued together), then a fixed-order warp/block tree.
 __global__ void __launch_bounds__(1024) k_sum_blocks(const double* __restrict__ blk, int nb, double* out) {
+  pdl_wait();
   __shared__ double s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = (nb + 1023) / 1024;
@@ -69,11 +71,11 @@ __global__ void __launch_bounds__(1024) k_sum_blocks(const double* __restrict__ 
 cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cudaStream_t s) {
   int nb = (int)((n + kBlockW - 1) / kBlockW);
   if (nb > 0) {
-    k_block_sum<<<nb, 256, 0, s>>>(w, n, blk);
+    pdl_launch(k_block_sum, nb, 256, 0, s, w, n, blk);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  k_sum_blocks<<<1, 1024, 0, s>>>(blk, nb, out);
+  pdl_launch(k_sum_blocks, 1, 1024, 0, s, blk, nb, out);
   return cudaGetLastError();
 }
 
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_select(const double* __restric
                                                          const double* __restrict__ D_lab, int M,
                                                          const double* __restrict__ W_pred, double p_d,
                                                          int32_t* sel_flag, double* info) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char sm[];
   unsigned long long* kw = reinterpret_cast<unsigned long long*>(sm);
   __shared__ TopkShared sh;
@@ -145,7 +148,7 @@ cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
     attr = true;
   }
-  k_select<<<1, kTopkThreads, smem, s>>>(C_lab, D_lab, M, W_pred, p_d, sel_flag, info);
+  pdl_launch(k_select, 1, kTopkThreads, smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info);
   return cudaGetLastError();
 }
 
@@ -168,6 +171,7 @@ __device__ __forceinline__ int seq_slot(int p, int n_s, int lanes, int zl, int j
 __global__ void __launch_bounds__(1024) k_slots2(const float* __restrict__ z, const int32_t* __restrict__ sel_flag,
                                                  int M, int model, int zl, int slots_pad, int32_t* slot_label,
                                                  int32_t* js_out) {
+  pdl_wait();
   __shared__ int wsum[32];
   __shared__ int base_s;
   __shared__ int cat_start[7];
@@ -256,12 +260,13 @@ __global__ void __launch_bounds__(1024) k_slots2(const float* __restrict__ z, co
 
 cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
                           int32_t* slot_label, int32_t* js, cudaStream_t s) {
-  k_slots2<<<1, 1024, 0, s>>>(z, sel_flag, M, model, zl, slots_pad, slot_label, js);
+  pdl_launch(k_slots2, 1, 1024, 0, s, z, sel_flag, M, model, zl, slots_pad, slot_label, js);
   return cudaGetLastError();
 }
 
 // Per-slot d = 1/D(label) for the pass-2 layout (0 for padding).
 __global__ void k_dslot(const int32_t* __restrict__ slot_label, const double* __restrict__ D_lab, int n, float* d) {
+  pdl_wait();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   int lab = slot_label[s];
@@ -275,7 +280,7 @@ __global__ void k_dslot(const int32_t* __restrict__ slot_label, const double* __
 
 cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, float* d, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_dslot<<<(n + 255) / 256, 256, 0, s>>>(slot_label, D_lab, n, d);
+  pdl_launch(k_dslot, (n + 255) / 256, 256, 0, s, slot_label, D_lab, n, d);
   return cudaGetLastError();
 }
 

@@ -184,6 +184,7 @@ __device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PA
 #endif
 template <int MODEL, int PASS, int ZL>
 __global__ void __launch_bounds__(256, ZL == 8 ? PHD_PASS_MINB8 : 3) k_pass(const PassArgs a) {
+  pdl_wait();
   using L = RecLayout<MODEL, PASS>;
   constexpr int NQ = PASS == 1 ? 1 : 4;  // pass 2: S'x, Svx, S'y, Svy (dW = C/D from pass 1)
   constexpr int NP = ZL / 2;
@@ -338,7 +339,7 @@ template <int MODEL, int PASS, int ZL>
 static cudaError_t launch_one(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
   set_attr<MODEL, PASS, ZL>();
   dim3 grid((unsigned)gp, (unsigned)zb);
-  k_pass<MODEL, PASS, ZL><<<grid, wz * 32, pass_smem<MODEL, PASS, ZL>(wz), s>>>(a);
+  pdl_launch(k_pass<MODEL, PASS, ZL>, grid, wz * 32, pass_smem<MODEL, PASS, ZL>(wz), s, a);
   return cudaGetLastError();
 }
 
@@ -395,6 +396,7 @@ struct FusedArgs {
 
 template <int MODEL, bool H1, bool H2>
 __global__ void __launch_bounds__(256, 2) k_fused(const FusedArgs fa) {
+  pdl_wait();
   using L = RecLayout<MODEL, 2>;
   constexpr int NP = 2;  // slot pairs per lane per pass
   const PassArgs& a = fa.a;
@@ -542,7 +544,7 @@ static cudaError_t launch_fused_t(const FusedArgs& fa, int gp, int zbg, int wz, 
                          (int)fused_smem<MODEL>(kMaxWarpsZ));
     attr = true;
   }
-  k_fused<MODEL, H1, H2><<<dim3((unsigned)gp, (unsigned)zbg), wz * 32, fused_smem<MODEL>(wz), s>>>(fa);
+  pdl_launch(k_fused<MODEL, H1, H2>, dim3((unsigned)gp, (unsigned)zbg), wz * 32, fused_smem<MODEL>(wz), s, fa);
   return cudaGetLastError();
 }
 
@@ -583,6 +585,7 @@ int fused_occupancy(int model, int wz) {
 // slots get a sentinel that makes every likelihood term exactly 0.
 __global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* __restrict__ slot_label, int n,
                         float sx, float sy, SlotConsts sc) {
+  pdl_wait();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   int lab = slot_label[s];
@@ -614,7 +617,7 @@ __global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* _
 cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad, float sensor_x,
                          float sensor_y, SlotConsts sc, cudaStream_t s) {
   if (n_slots_pad <= 0) return cudaSuccess;
-  k_zprep<<<(n_slots_pad + 255) / 256, 256, 0, s>>>(model, z_lab, slot_label, n_slots_pad, sensor_x, sensor_y, sc);
+  pdl_launch(k_zprep, (n_slots_pad + 255) / 256, 256, 0, s, model, z_lab, slot_label, n_slots_pad, sensor_x, sensor_y, sc);
   return cudaGetLastError();
 }
 
@@ -622,6 +625,7 @@ cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_labe
 // for the slot range [s0, s1) (one measurement group).
 __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_pad, int s0, int s1,
                            double* C_slot) {
+  pdl_wait();
   // one warp per slot, lanes over the particle-CTA partials, fixed-order xor tree
   const int lane = threadIdx.x & 31;
   int s = s0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -636,7 +640,7 @@ __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_p
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
                             cudaStream_t s) {
   if (s1 <= s0) return cudaSuccess;
-  k_reduce_C<<<(s1 - s0 + 7) / 8, 256, 0, s>>>(Cpart, gp, slots_pad, s0, s1, C_slot);
+  pdl_launch(k_reduce_C, (s1 - s0 + 7) / 8, 256, 0, s, Cpart, gp, slots_pad, s0, s1, C_slot);
   return cudaGetLastError();
 }
 
@@ -645,6 +649,7 @@ cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, 
 // label-order copies C_lab, D_lab used by the STPHD reduction and the getters.
 __global__ void k_zconst(const double* __restrict__ C_slot, const int32_t* __restrict__ slot_label, int s0, int s1,
                          double kappa, float* d_slot, double* C_lab, double* D_lab, int* bad) {
+  pdl_wait();
   int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= s1) return;
   int lab = slot_label[s];
@@ -663,7 +668,7 @@ __global__ void k_zconst(const double* __restrict__ C_slot, const int32_t* __res
 cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
                           float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s) {
   if (s1 <= s0) return cudaSuccess;
-  k_zconst<<<(s1 - s0 + 255) / 256, 256, 0, s>>>(C_slot, slot_label, s0, s1, kappa, d_slot, C_lab, D_lab, bad);
+  pdl_launch(k_zconst, (s1 - s0 + 255) / 256, 256, 0, s, C_slot, slot_label, s0, s1, kappa, d_slot, C_lab, D_lab, bad);
   return cudaGetLastError();
 }
 
@@ -673,6 +678,7 @@ __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, c
                                                   int64_t P_stride, int zb, int64_t n, float nu, float wscale,
                                                   float* w_out, double* blk_w, double* blk_wp,
                                                   const int32_t* __restrict__ inv) {
+  pdl_wait();
   __shared__ double sw[8], swp[8];
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * kBlockW;
@@ -720,7 +726,7 @@ cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, in
                              const int32_t* inv) {
   if (n <= 0) return cudaSuccess;
   unsigned nb = (unsigned)((n + kBlockW - 1) / kBlockW);
-  k_finalize<<<nb, 256, 0, s>>>(w, P, P_stride, zb, n, nu, wscale, w_out, blk_w, blk_wp, inv);
+  pdl_launch(k_finalize, nb, 256, 0, s, w, P, P_stride, zb, n, nu, wscale, w_out, blk_w, blk_wp, inv);
   return cudaGetLastError();
 }
 
@@ -737,6 +743,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
                              const float* __restrict__ s3, int model, const double* __restrict__ blk_w,
                              const double* __restrict__ blk_wp, int nb, double* acc_lab, double* rank_slots,
                              int rank, int world, int lead, const int32_t* __restrict__ sel_flag) {
+  pdl_wait();
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double sa[256], sb[256];
     double a = 0.0, b = 0.0;
@@ -812,7 +819,7 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
                               int nb, double* acc_lab, double* rank_slots, int rank, int world, int lead,
                               const int32_t* sel_flag, cudaStream_t s) {
   int blocks = (n_slots + 7) / 8 + 1;  // 8 slots (warps) per block + the rank-mass block
-  k_reduce_acc<<<blocks, 256, 0, s>>>(Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
+  pdl_launch(k_reduce_acc, blocks, 256, 0, s, Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
                                       blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead, sel_flag);
   return cudaGetLastError();
 }

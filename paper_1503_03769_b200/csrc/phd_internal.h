@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <utility>
 #include <stdint.h>
 
 namespace phd {
@@ -23,6 +24,35 @@ namespace phd {
   do {                   \
   } while (0)
 #endif
+
+// ---- programmatic dependent launch (PDL) -------------------------------------
+// Every kernel is launched with programmatic stream serialization and starts
+// with griddepcontrol.wait, which blocks until the preceding grid has completed
+// and its memory is visible -- so the semantics are those of plain stream order,
+// but the launch and block scheduling of a kernel overlap the tail of the one
+// before it (the step is a chain of ~20-45 kernels, many of them short).
+// PHD_PDL=0 in the environment launches without the attribute.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- tiling constants ----------------------------------------
 // measurement slots per lane: 4 or 8 (kernel template), i.e. 128 or 256 per warp
