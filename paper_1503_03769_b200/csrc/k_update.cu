@@ -182,8 +182,12 @@ __device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PA
 #ifndef PHD_PASS_MINB8
 #define PHD_PASS_MINB8 2
 #endif
+#ifndef PHD_PASS1_MINB8
+#define PHD_PASS1_MINB8 2
+#endif
 template <int MODEL, int PASS, int ZL>
-__global__ void __launch_bounds__(256, ZL == 8 ? PHD_PASS_MINB8 : 3) k_pass(const PassArgs a) {
+__global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : PHD_PASS_MINB8) : 3)
+    k_pass(const PassArgs a) {
   pdl_wait();
   using L = RecLayout<MODEL, PASS>;
   constexpr int NQ = PASS == 1 ? 1 : 4;  // pass 2: S'x, Svx, S'y, Svy (dW = C/D from pass 1)
