@@ -160,6 +160,28 @@ def cpu_oracle_sample(cfg, Z, soa, w, n_sample, k=1):
     return {"pairs": pairs, "seconds": dt, "n": n + J, "M": len(z)}
 
 
+def cpu_oracle_all_cores(cfg, Z, soa, w, n_sample, k=1):
+    """Context, not the contract's cpu_baseline: the oracle's normaliser and update
+    loops (the O(N M) part of a step) split over particles on every host core
+    (oracle/phd_oracle_mt.c, fixed-order fp64 reduction), on a bounded sample."""
+    import numpy as np
+    import oracle
+    m = cfg.model
+    n = min(n_sample, soa.shape[1])
+    nt = os.cpu_count() or 1
+    sub = np.ascontiguousarray(soa[:, :n])
+    ws = np.ascontiguousarray(w[:n]) + np.float32(1e-9)
+    z = Z[k - 1]
+    t0 = time.perf_counter()
+    C = oracle.normalizers_mt(m, sub, ws, z, nt)
+    oracle.update_mt(m, sub, ws, z, C, nt)
+    dt = time.perf_counter() - t0
+    pairs = n * len(z)
+    return {"value": pairs / dt, "unit": "pairs/s", "cores": nt, "kind": "oracle (threaded timing variant)",
+            "sample": "normalisers + weight/STPHD update of the first %d particles against all M=%d measurements "
+                      "of Z_1, split over %d threads; %.1f s" % (n, len(z), nt, dt)}
+
+
 def run_reference(args):
     import numpy as np
     rank = int(os.environ.get("RANK", "0"))
@@ -439,6 +461,9 @@ def run_ours(args):
                "sample": "one full serial fp64 step (predict, births, normalisers, update, extraction, resampling) "
                          "of the first %d particles (+%d proportional births) against all M=%d measurements of "
                          "Z_1; %.1f s" % (args.cpu_sample, r["n"] - args.cpu_sample, r["M"], r["seconds"])}
+    cpu_all = None
+    if not args.no_cpu_baseline:
+        cpu_all = cpu_oracle_all_cores(cfg, Z, soa, w, args.cpu_sample * 4)
     out = {
         "metric": "particle-measurement update pairs/sec and filter step ms",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -468,6 +493,7 @@ def run_ours(args):
                             "frac_vs_survey_17fp32_2ex2": ach_upd / roofline_pairs_per_s(m.meas, "update", n_sm,
                                                                                          SM_MAX_MHZ, 1.25)},
         "cpu_baseline": cpu,
+        "cpu_baseline_all_cores": cpu_all,
         "e2e": {"value": value_e, "unit": "pairs/s", "h2d_bytes_per_step": M * 8,
                 "d2h_bytes_per_step": int(f._sum.n_est) * 24 + 8 * (2 * world + 10)},
         "gpu_launches": int(launches),

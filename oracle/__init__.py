@@ -15,14 +15,16 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "libphd_oracle.so")
 SRC = os.path.join(HERE, "phd_oracle.c")
+SRC_MT = os.path.join(HERE, "phd_oracle_mt.c")
 
 
 def build(force=False):
     """Compile the oracle shared library with gcc (plain -O2, no fast-math, no FMA contraction)."""
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= os.path.getmtime(SRC):
+    srcs = [SRC, SRC_MT, os.path.join(HERE, "phd_oracle.h")]
+    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(f) for f in srcs):
         return LIB
-    cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
-           "-o", LIB, SRC, "-lm"]
+    cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math", "-pthread",
+           "-o", LIB, SRC, SRC_MT, "-lm"]
     subprocess.check_call(cmd, cwd=HERE)
     return LIB
 
@@ -69,6 +71,9 @@ def lib():
                                            ctypes.c_int32, _D, _D, _D, _D, _D]
         L.orc_normalizers.argtypes = [M, ctypes.c_int64, _D, _D, _D, _D, ctypes.c_int32, _D]
         L.orc_update.argtypes = [M, ctypes.c_int64, _D, _D, _D, _D, _D, _D, ctypes.c_int32, _D, _D, _D]
+        L.orc_normalizers_mt.argtypes = [M, ctypes.c_int64, _D, _D, _D, _D, ctypes.c_int32, _D, ctypes.c_int32]
+        L.orc_update_mt.argtypes = [M, ctypes.c_int64, _D, _D, _D, _D, _D, _D, ctypes.c_int32, _D, _D, _D,
+                                    ctypes.c_int32]
         L.orc_extract.argtypes = [M, ctypes.c_int32, _D, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                                   _I32, _D, _D, _I64, _I32, _D]
         L.orc_extract.restype = ctypes.c_int32
@@ -184,6 +189,32 @@ def update(m, soa, w, z, C):
     acc = np.zeros((len(zz), 5))
     lib().orc_update(ctypes.byref(model(m)), len(ww), _d(x), _d(vx), _d(y), _d(vy), _d(ww),
                      _d(zz), len(zz), _d(CC), _d(wo), _d(acc))
+    return wo, acc
+
+
+def normalizers_mt(m, soa, w, z, nthreads):
+    """normalizers() split over particles across threads (all-core CPU baseline; timing)."""
+    s = _f64(soa)
+    x, y = np.ascontiguousarray(s[0]), np.ascontiguousarray(s[2])
+    ww = _f64(w)
+    zz = _f64(z).reshape(-1, 2)
+    C = np.zeros(len(zz))
+    lib().orc_normalizers_mt(ctypes.byref(model(m)), len(ww), _d(x), _d(y), _d(ww), _d(zz), len(zz), _d(C),
+                             int(nthreads))
+    return C
+
+
+def update_mt(m, soa, w, z, C, nthreads):
+    """update() split over particles across threads (all-core CPU baseline; timing)."""
+    s = _f64(soa)
+    x, vx, y, vy = [np.ascontiguousarray(s[i]) for i in range(4)]
+    ww = _f64(w)
+    zz = _f64(z).reshape(-1, 2)
+    CC = _f64(C)
+    wo = np.zeros(len(ww))
+    acc = np.zeros((len(zz), 5))
+    lib().orc_update_mt(ctypes.byref(model(m)), len(ww), _d(x), _d(vx), _d(y), _d(vy), _d(ww),
+                        _d(zz), len(zz), _d(CC), _d(wo), _d(acc), int(nthreads))
     return wo, acc
 
 

@@ -76,6 +76,13 @@ void orc_normalizers(const orc_model* m, int64_t n, const double* x, const doubl
 void orc_update(const orc_model* m, int64_t n, const double* x, const double* vx,
                 const double* y, const double* vy, const double* w,
                 const double* z, int32_t nz, const double* C, double* w_out, double* acc);
+/* All-core timing variants (oracle/phd_oracle_mt.c): the same loops split over
+ * particles across nthreads threads, per-thread partial sums added in thread order. */
+void orc_normalizers_mt(const orc_model* m, int64_t n, const double* x, const double* y, const double* w,
+                        const double* z, int32_t nz, double* C, int32_t nthreads);
+void orc_update_mt(const orc_model* m, int64_t n, const double* x, const double* vx, const double* y,
+                   const double* vy, const double* w, const double* z, int32_t nz, const double* C,
+                   double* w_out, double* acc, int32_t nthreads);
 /* LT = round(W); top-LT labels by (dW desc, label asc); zeta = S/dW.
  * Returns the number of estimates written (<= cap). */
 int32_t orc_extract(const orc_model* m, int32_t nz, const double* acc, double W, double W_pred,

@@ -576,3 +576,24 @@ def test_births_importance_stratified_counts(orc):
     g = np.exp(-(x - 6.0) ** 2 / 18.0) / math.sqrt(18.0 * math.pi)
     wrong = m.birth_mass * np.trapezoid(g * (q0 / 3 + 2 * q1 / 3) / (q0 / 2 + q1 / 2), x)
     assert abs(wrong - m.birth_mass) > 8 * se, (wrong, se)
+
+
+def test_all_core_timing_variant_matches_oracle(orc):
+    """The all-core CPU baseline (oracle/phd_oracle_mt.c) computes the oracle's
+    normalisers and update: identical per-particle weights, sums over particles
+    equal up to fp64 summation order."""
+    import scenario
+    rng = np.random.default_rng(3)
+    for cname in ("cfg1", "cfg2"):
+        m = scenario.get(cname).model
+        soa = rng.uniform(-1000, 1000, (4, 3001)).astype(np.float32)
+        w = rng.uniform(0, 1e-3, 3001).astype(np.float32)
+        z = scenario.random_measurements(37, 5, meas=m.meas, region=m.region)
+        C = orc.normalizers(m, soa, w, z)
+        wo, acc = orc.update(m, soa, w, z, C)
+        for nt in (1, 3, 8):
+            Cm = orc.normalizers_mt(m, soa, w, z, nt)
+            wm, am = orc.update_mt(m, soa, w, z, C, nt)
+            assert np.allclose(Cm, C, rtol=1e-13, atol=0)
+            assert np.array_equal(wm, wo)
+            assert np.allclose(am, acc, rtol=1e-12, atol=1e-300)
