@@ -9,3 +9,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_pass --launch-skip 6 -c 2 -o gpurun_out/pass_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-gated-leg > gpurun_out/ncu_full.log 2>&1; echo ncu3=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_gpass|k_psort_scatter" --launch-skip 9 -c 3 -o gpurun_out/gpass_full python bench.py --gate 1 --steps 1 --warmup 3 --no-cpu-baseline --no-gated-leg > gpurun_out/ncu_gfull.log 2>&1; echo ncu4=$?
 timeout 900 ncu --set full --clock-control none -k regex:"k_predict|k_resample_mark|k_gather" --launch-skip 9 -c 3 -o gpurun_out/hbm_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-gated-leg > gpurun_out/ncu_hbm.log 2>&1; echo ncu5=$?
+timeout 900 python tools/table1_study.py --runs 10 --out gpurun_out/r01_table1_study > gpurun_out/table1.log 2>&1; echo table1=$?
