@@ -208,6 +208,12 @@ phd_status phd_create_in_group(const phd_params* p, phd_group* g, int32_t rank, 
  * Errors: PHD_EINVAL (n_local does not match the block), PHD_ECAPACITY. */
 phd_status phd_set_particles(phd_ctx* ctx, const float* soa4, const float* w, int64_t n_local,
                              int64_t n_global, double mass, int32_t stage);
+/* Checkpoint / resume: set the measurement set Z_{k-1} that the next
+ * phd_predict(k, NULL) / phd_step draws its births around (the set an update
+ * retains; M = 0: none, births uniform).  With phd_set_particles of a saved
+ * resampled population this resumes a run exactly (the noise is counter-based:
+ * Philox at (slot, k, stream)).  z: host or device [M][2].  Errors: PHD_EINVAL. */
+phd_status phd_set_retained_measurements(phd_ctx* ctx, const float* z, int32_t M);
 /* Copy this rank's particles (SoA [4][n] and weights) to host; synchronous.
  * n_local receives the count, global_offset the global index of element 0. */
 phd_status phd_get_particles(phd_ctx* ctx, float* soa4, float* w, int64_t cap, int64_t* n_local,

@@ -59,7 +59,7 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_get_ancestors", "phd_get_resample_meta", "phd_launch_count", "phd_set_timing", "phd_get_timing",
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
            "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates",
-           "phd_get_gate_stats", "phd_exchange_path"]
+           "phd_get_gate_stats", "phd_exchange_path", "phd_set_retained_measurements"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -115,6 +115,7 @@ def load(build_if_missing=True):
     L.phd_get_local_estimates.argtypes = [_P, ctypes.POINTER(Estimate), ctypes.c_int32, _I32]
     L.phd_get_resample_meta.argtypes = [_P, _D, _D, _I64, _D]
     L.phd_get_gate_stats.argtypes = [_P, _I64]
+    L.phd_set_retained_measurements.argtypes = [_P, _P, ctypes.c_int32]
     L.phd_exchange_path.argtypes = [_P]
     L.phd_exchange_path.restype = ctypes.c_int32
     L.phd_launch_count.argtypes = [_P]
@@ -402,6 +403,32 @@ class Filter:
         out = np.zeros(4, dtype=np.int64)
         self._check(self.L.phd_get_gate_stats(self.h, out.ctypes.data_as(_I64)), "phd_get_gate_stats")
         return {"used": int(out[0]), "entries": int(out[1]), "pairs": int(out[2]), "tiles": int(out[3])}
+
+    def set_retained_measurements(self, z):
+        """Z_{k-1} for the births of the next predict/step (checkpoint resume)."""
+        z = _f32(z)
+        self._zkeep = z
+        self._check(self.L.phd_set_retained_measurements(self.h, _ptr(z), int(z.shape[0])),
+                    "phd_set_retained_measurements")
+
+    def checkpoint(self, path, k, z):
+        """Save this rank's resampled population after step k with Z_k (which the
+        births of step k + 1 are drawn around): an npz that restore() resumes from
+        exactly (counter-based noise)."""
+        soa, w, g0 = self.get_particles()
+        meta = self.resample_meta()
+        np.savez(path, soa=soa, w=w, g0=g0, k=int(k), n_out=int(meta["N_out"]), z=_f32(z), rank=self.rank,
+                 world=self.world)
+
+    def restore(self, path):
+        """Load a checkpoint() of this rank; returns the step k it was taken after."""
+        d = np.load(path)
+        if int(d["rank"]) != self.rank or int(d["world"]) != self.world:
+            raise ValueError("checkpoint of rank %d/%d, filter is %d/%d" % (int(d["rank"]), int(d["world"]),
+                                                                         self.rank, self.world))
+        self.set_particles(np.ascontiguousarray(d["soa"]), np.ascontiguousarray(d["w"]), int(d["n_out"]))
+        self.set_retained_measurements(d["z"])
+        return int(d["k"])
 
     def exchange_path(self):
         """0 none, 1 send/recv, 2 fused gather + exchange over peer memory."""

@@ -24,9 +24,18 @@
 #include "phd_internal.h"
 #include "philox.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 using namespace phd;
 
 namespace {
+
+// NVTX range per ABI stage (SURVEY.md §5 tracing): visible in nsys / ncu
+// timelines, a no-op without an attached tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr double kPi = 3.14159265358979323846264338327950288;
 constexpr double kLog2e = 1.44269504088896340735992468100189214;
@@ -701,6 +710,20 @@ phd_status phd_set_particles(phd_ctx* c, const float* soa4, const float* w, int6
   return PHD_OK;
 }
 
+phd_status phd_set_retained_measurements(phd_ctx* c, const float* z, int32_t M) {
+  if (!c) return PHD_EINVAL;
+  cudaSetDevice(c->device);
+  c->err.clear();
+  if (M < 0 || M > c->p.max_meas) return fail(c, PHD_EINVAL, "M = %d outside [0, max_meas = %d]", M, c->p.max_meas);
+  if (M > 0 && !z) return fail(c, PHD_EINVAL, "z is NULL");
+  if (M > 0) {
+    CU(cudaMemcpyAsync(c->zlab, z, sizeof(float) * 2 * M, cudaMemcpyDefault, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  c->M_z = M;
+  return PHD_OK;
+}
+
 phd_status phd_get_particles(phd_ctx* c, float* soa4, float* w, int64_t cap, int64_t* n_local, int64_t* global_offset) {
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
@@ -725,6 +748,7 @@ phd_status phd_get_particles(phd_ctx* c, float* soa4, float* w, int64_t cap, int
 }
 
 phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_prev) {
+  NvtxRange nvtx_("phd_predict");
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
   c->err.clear();
@@ -945,6 +969,7 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
 }
 
 phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
+  NvtxRange nvtx_("phd_update");
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
   c->err.clear();
@@ -1240,6 +1265,7 @@ static int fuse_estimates(phd_ctx* c, phd_estimate* out, int cap) {
 }
 
 phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s) {
+  NvtxRange nvtx_("phd_extract");
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
   c->err.clear();
@@ -1357,6 +1383,7 @@ static phd_status p2p_setup(phd_ctx* c) {
 }
 
 phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
+  NvtxRange nvtx_("phd_resample_exchange");
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);
   c->err.clear();
@@ -1535,6 +1562,7 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
 
 phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estimate* out, int32_t cap, int32_t* n_out,
                     phd_summary* s) {
+  NvtxRange nvtx_("phd_step");
   if (!c) return PHD_EINVAL;
   timing_record(c, 13);
   phd_status st = phd_predict(c, k, nullptr, 0);
