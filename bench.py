@@ -363,6 +363,10 @@ def run_ours(args):
         f.close()
         del workspace
         mg = _replace(m, gate=1)
+        if world > 1:  # an NCCL unique id bootstraps one communicator: a fresh one for this filter
+            obj = [phd.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
         workspace = torch.empty(phd.workspace_size(mg, world), dtype=torch.uint8, device=dev)
         f = phd.Filter(mg, rank=rank, world=world, nccl_id=nid, device=local, stream=stream.cuda_stream,
                        workspace=workspace)
