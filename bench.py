@@ -501,6 +501,12 @@ def run_ours(args):
         "e2e": {"value": value_e, "unit": "pairs/s", "h2d_bytes_per_step": M * 8,
                 "d2h_bytes_per_step": int(f._sum.n_est) * 24 + 8 * (2 * world + 10)},
         "gpu_launches": int(launches),
+        "paper_context": {"hardware": "a Dell computer using MATLAB (PAPER.md:494); no CPU model, cores or "
+                                      "precision stated",
+                          "workload": "BOT range-bearing scenario, 2000 particles, K = 4 groups, 50 scans "
+                                      "(PAPER.md:444-448)",
+                          "table1_dcpphd_speedup_vs_phd": {"r=0": 2.04, "r=10": 2.66, "r=20": 2.97},
+                          "note": "Table 1 (PAPER.md:497-513), context only: not this metric or workload"},
         "hbm_kernels": hbm,
         "gated": gated,
         "clocks": clk,
