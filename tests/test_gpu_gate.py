@@ -300,3 +300,17 @@ def test_checkpoint_resume_is_exact(phd, gate, tmp_path):
     pb = fb.get_particles()
     assert np.array_equal(pa[0], pb[0]) and np.array_equal(pa[1], pb[1])
     fb.close()
+
+
+def test_gated_range_bearing_offset_sensor(phd, orc):
+    """Range-bearing sensor away from the origin: the cell grid is in (r, theta)
+    about the sensor; particles beyond the range region use the border cells."""
+    m = replace(RB, gate=2, sensor_xy=(300.0, -200.0), region=(0.0, 1500.0, -math.pi, math.pi))
+    z = scenario.random_measurements(300, 21, meas=m.meas, region=m.region)
+    soa, w = scenario.clustered_particles(12000, z, 21, meas=m.meas, sensor=m.sensor_xy,
+                                          box=(-1000.0, 1000.0, -1000.0, 1000.0))
+    g = _run(phd, m, soa, w, z)
+    assert g["gate"]["used"] == 1
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
