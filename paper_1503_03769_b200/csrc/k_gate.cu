@@ -88,6 +88,13 @@ __device__ __forceinline__ unsigned match_digit_rt(int d, bool ok, int nbits) {
   return m;
 }
 
+// float <-> int with the same order (for integer atomicMax on floats)
+__device__ __forceinline__ int f2ord(float f) {
+  const int b = __float_as_int(f);
+  return b >= 0 ? b : b ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord2f(int o) { return __int_as_float(o >= 0 ? o : o ^ 0x7FFFFFFF); }
+
 // distance from v to [a, b]
 __device__ __forceinline__ float dist_iv(float v, float a, float b) { return fmaxf(0.0f, fmaxf(a - v, v - b)); }
 // distance from the angle v (any real, e.g. fp32(pi) > pi) to the arc [a, b]
@@ -353,6 +360,7 @@ struct GatherSrc {
 // padding records [n, n_pad): zero state, lw = -inf
 __global__ void k_psort_pad(int64_t n, int64_t n_pad, GateSorted so) {
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *so.lw_max = f2ord(-INFINITY);  // reset before the scatter's max
   const int64_t p = n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pad) return;
   float4* r = so.rec + p * so.n4;
@@ -403,8 +411,9 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
     base[2 * j + 1] = hs[(int64_t)(2 * j + 1) * nblk + blockIdx.x];
   }
   __syncthreads();
-  // 3. rank and write the records
+  // 3. rank and write the records (and the max of lw, for the tile kernels' fast path)
   const unsigned lt = (1u << lane) - 1u;
+  float lwm = -INFINITY;
   for (int64_t b0 = w0; b0 < w1; b0 += 32 * ROWS) {
     float4 q[ROWS][N4];
     int kr[ROWS];
@@ -418,6 +427,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
       }
       q[r][N4 - 2] = make_float4(__ldg(src.x + i), __ldg(src.y + i), __ldg(src.vx + i), __ldg(src.vy + i));
       q[r][N4 - 1] = make_float4(log2f(__ldg(src.w + i) * wscale), 0.0f, 0.0f, 0.0f);  // the dense TileLoader's expression
+      lwm = fmaxf(lwm, q[r][N4 - 1].x);  // clamped duplicates of the last item do not change the max
     }
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
@@ -439,6 +449,9 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
       __syncwarp();
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lwm = fmaxf(lwm, __shfl_xor_sync(0xffffffffu, lwm, o));
+  if (lane == 0 && w0 < w1) atomicMax(so.lw_max, f2ord(lwm));
 }
 
 // ---------------------------------------------------------------------------
@@ -456,7 +469,10 @@ struct RecView {
   const float* c1;
   const float* lw;
   int stride;
+  int64_t n;             // particles (records [n, n_pad) are padding)
+  const int* lw_max;     // ordered-int encoding of max lw over all particles (k_psort_scatter)
 };
+
 
 __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, float na1, const GateGrid& g,
                                          const int32_t* __restrict__ zcell_start, const int32_t* __restrict__ zcell_items,
@@ -464,7 +480,26 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
   const int lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)t * kGateTP;
   float b0 = INFINITY, b1 = -INFINITY, e0 = INFINITY, e1 = -INFINITY, lm = -INFINITY;
-  for (int j = lane; j < kGateTP; j += 32) {
+  // Fast path: a full tile whose first and last particles share an interior cell holds
+  // only particles of that cell (the tiles are in cell-key order), so the cell's box
+  // (a little widened against the fp32 rounding of the cell index) and the global
+  // max of log2(p_D c w) bound the tile conservatively: never fewer candidates.
+  bool fast = false;
+  if (p0 + kGateTP <= rv.n) {
+    const int64_t oa = p0 * rv.stride, ob = (p0 + kGateTP - 1) * rv.stride;
+    const int ax = cell_raw(__ldg(rv.c0 + oa), g.lo0, g.inv_h0), ay = cell_raw(__ldg(rv.c1 + oa), g.lo1, g.inv_h1);
+    const int bx = cell_raw(__ldg(rv.c0 + ob), g.lo0, g.inv_h0), by = cell_raw(__ldg(rv.c1 + ob), g.lo1, g.inv_h1);
+    if (ax == bx && ay == by && ax > 0 && ax < kGateG - 1 && ay > 0 && ay < kGateG - 1) {
+      fast = true;
+      const float w0 = 1.0f / g.inv_h0, w1 = 1.0f / g.inv_h1;
+      b0 = g.lo0 + ((float)ax - 0.01f) * w0;
+      b1 = g.lo0 + ((float)ax + 1.01f) * w0;
+      e0 = g.lo1 + ((float)ay - 0.01f) * w1;
+      e1 = g.lo1 + ((float)ay + 1.01f) * w1;
+      lm = ord2f(__ldg(rv.lw_max));
+    }
+  }
+  for (int j = lane; j < (fast ? 0 : kGateTP); j += 32) {
     const int64_t o = (p0 + j) * rv.stride;
     const float l = __ldg(rv.lw + o);
     if (l > -INFINITY) {  // zero-weight particles and padding contribute nothing
@@ -949,10 +984,9 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
                                 int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
                                 int32_t* keys, const GateSorted& so, cudaStream_t s, int64_t* launches) {
   const bool rbm = model == kRangeBearing;
-  if (n_pad > n) {
-    pdl_launch(k_psort_pad, (unsigned)((n_pad - n + 255) / 256), 256, 0, s, n, n_pad, so);
-    ++*launches;
-  }
+  // always launched: it also resets the lw max
+  pdl_launch(k_psort_pad, (unsigned)std::max<int64_t>(1, (n_pad - n + 255) / 256), 256, 0, s, n, n_pad, so);
+  ++*launches;
   if (n <= 0) return cudaGetLastError();
   KeyCell kf{rbm ? rb : A[0], rbm ? rb + 2 * rb_stride : A[2], grid};
   GatherSrc src{};
@@ -1018,7 +1052,7 @@ cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, fl
   if (ntiles <= 0) return cudaSuccess;
   const bool rbm = model == kRangeBearing;
   const float* f = reinterpret_cast<const float*>(so.rec);
-  RecView rv{f, f + (rbm ? 2 : 1), f + 4 * (so.n4 - 1), 4 * so.n4};
+  RecView rv{f, f + (rbm ? 2 : 1), f + 4 * (so.n4 - 1), 4 * so.n4, so.n, so.lw_max};
   const unsigned blocks = (unsigned)((ntiles + 7) / 8);
   if (fill)
     pdl_launch(k_gate_fill, blocks, 256, 0, s, rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tstart, cbuf,

@@ -54,7 +54,7 @@ struct Layout {
   int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
   int g_ntiles = 0, g_nsorted = 0;
   size_t o_gkeys, o_ginv, o_gsorted[13], o_gPs, o_ghist, o_gscan, o_gtstart, o_gcand, o_gk, o_gv, o_gmlist,
-      o_gpart1, o_gpart2, o_gmstart, o_gzstart, o_gzitems, o_gzz, o_gcbuf, o_gA;
+      o_gpart1, o_gpart2, o_gmstart, o_gzstart, o_gzitems, o_gzz, o_gcbuf, o_glwmax, o_gA;
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -135,6 +135,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_gzz = gtake(sizeof(float) * 2 * ((size_t)p->max_meas + 1));
   L.o_gcbuf = gtake(sizeof(int32_t) * (size_t)L.g_ntiles * kGateKBufH);
   L.o_gA = gtake(sizeof(double) * 4 * (size_t)L.slots_max);
+  L.o_glwmax = gtake(sizeof(int) * 4);
   L.total = off;
   return L;
 }
@@ -530,6 +531,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
     c->gkeys = at<int32_t>(c->ws, L.o_gkeys);
     c->gso.rec = at<float4>(c->ws, L.o_gsorted[0]);
     c->gso.n4 = p->meas == PHD_MEAS_RANGE_BEARING ? 4 : 2;
+    c->gso.lw_max = at<int>(c->ws, L.o_glwmax);
     c->gPs = at<float>(c->ws, L.o_gPs);
     c->ghist = at<int32_t>(c->ws, L.o_ghist);
     c->gscan = at<int32_t>(c->ws, L.o_gscan);
@@ -936,6 +938,7 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   const int64_t npad = ceil_div(n, kGateTP) * kGateTP;
   const int ntiles = (int)(npad / kGateTP);
   const float* A[5] = {c->A[0], c->A[1], c->A[2], c->A[3], c->A[4]};
+  c->gso.n = n;
   CU(gate_sort_particles(c->model, A, c->rb, c->L.cap_l, n, npad, c->wscale, c->ggrid, c->ghist, c->gscan,
                          c->gkeys, c->gso, c->st, &c->launches));
   CU(gate_zbin(c->zlab, M, c->ggrid, c->ghist, c->gscan, c->gzstart, c->gzitems, c->gzz, c->st, &c->launches));

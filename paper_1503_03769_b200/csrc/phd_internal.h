@@ -258,6 +258,8 @@ struct GateSorted {
   float4* rec;
   int n4;
   int32_t* inv;                       // local index -> sorted position
+  int* lw_max;                        // max lw over the particles (ordered-int encoding)
+  int64_t n;                          // particles sorted (records [n, n_pad) are padding)
 };
 
 struct GateArgs {
