@@ -368,6 +368,13 @@ __global__ void k_psort_pad(int64_t n, int64_t n_pad, GateSorted so) {
   r[so.n4 - 1] = make_float4(-INFINITY, 0.0f, 0.0f, 0.0f);
 }
 
+// one 256-bit store (STG.E.ENL2.256, sm_100) of two float4: a whole 32-byte sector
+__device__ __forceinline__ void st_v8(float4* dst, float4 a, float4 b) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(a.x), "f"(a.y), "f"(a.z),
+               "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+               : "memory");
+}
+
 template <int MODEL>
 __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int32_t* __restrict__ keys, int64_t n,
                                                        int64_t per_blk, int nblk, const int32_t* __restrict__ hs,
@@ -443,7 +450,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
         PHD_DCHECK(pos >= 0 && pos < n && d >= 0 && d < nbins);
         float4* dst = so.rec + (int64_t)pos * N4;
 #pragma unroll
-        for (int k = 0; k < N4; ++k) dst[k] = q[r][k];
+        for (int k = 0; k < N4; k += 2) st_v8(dst + k, q[r][k], q[r][k + 1]);
         so.inv[i] = pos;
       }
       __syncwarp();
