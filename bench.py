@@ -485,15 +485,19 @@ def run_ours(args):
                      "achieved": ach2 / 1e9, "peak": peak2 / 1e9, "unit": "Gpair/s", "frac": ach2 / peak2,
                      "traffic": traffic,
                      "peak_basis": "min(128 FP32 lanes / %.2f, 16 EX2 / 1) per SM-clk x %d SMs x %.0f MHz (max clock); "
-                                   "%.2f FP32 = 6 + 4 f, f = |I|/M = %.3f (state sums for the estimated index set); "
+                                   "%.2f FP32 = %s, f = |I|/M = %.3f (state sums for the estimated index set); "
                                    "pipe rates measured (profiles/r01_pipes_microbench.jsonl)"
                                    % (pass_ops(m.meas, "pass2", frac_sel)[0], n_sm, SM_MAX_MHZ,
-                                      pass_ops(m.meas, "pass2", frac_sel)[0], frac_sel),
+                                      pass_ops(m.meas, "pass2", frac_sel)[0],
+                                      "7 + 6 f (range-bearing: + anisotropy multiply, + centring on the "
+                                      "Cartesian image; the hi/lo residual is not counted)"
+                                      if m.meas == 1 else "6 + 4 f", frac_sel),
                      "frac_at_observed_clock": ach2 / roofline_pairs_per_s(m.meas, "pass2", n_sm, mhz, frac_sel),
                      "frac_survey_count": ach2 / peak2_survey},
         "update_roofline": {"achieved": ach_upd / 1e9, "peak": peak_upd / 1e9, "unit": "Gpair/s",
                             "frac": ach_upd / peak_upd, "bound": bound_of(m.meas, "update", frac_sel),
-                            "basis": "both passes: (12 + 4 f) FP32 + 2 EX2 per pair, f = %.3f" % frac_sel,
+                            "basis": "both passes: (%s) FP32 + 2 EX2 per pair, f = %.3f"
+                                     % ("14 + 6 f" if m.meas == 1 else "12 + 4 f", frac_sel),
                             "frac_vs_survey_17fp32_2ex2": ach_upd / roofline_pairs_per_s(m.meas, "update", n_sm,
                                                                                          SM_MAX_MHZ, 1.25)},
         "cpu_baseline": cpu,
