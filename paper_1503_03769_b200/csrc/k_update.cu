@@ -635,6 +635,7 @@ __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_p
   int s = s0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= s1) return;
   double c = 0.0;
+#pragma unroll 4
   for (int b = lane; b < gp; b += 32) c += Cpart[(int64_t)b * slots_pad + s];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -780,8 +781,11 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
   if (s >= n_slots) return;
   int lab = slot_label[s];
   if (lab < 0) return;
+  // state sums outside the index set I were not accumulated: their partials are not read
+  const bool sums = sel_flag == nullptr || sel_flag[lab] != 0;
   double A[4] = {0, 0, 0, 0};
-  for (int b = lane; b < gp; b += 32) {
+#pragma unroll 2
+  for (int b = sums ? lane : gp; b < gp; b += 32) {
     const double* p = Apart + (int64_t)b * 4 * slots_pad + s;
 #pragma unroll
     for (int q = 0; q < 4; ++q) A[q] += p[(int64_t)q * slots_pad];
@@ -805,7 +809,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
   // terms, every rank its own centred partial sums (the C2 all-reduce adds them).
   double dW = lead ? C_lab[lab] * inv : 0.0;
   double* o = acc_lab + 5 * (int64_t)lab;
-  if (sel_flag && !sel_flag[lab]) {  // state sums not accumulated outside the index set I
+  if (!sums) {
     o[0] = dW;
     o[1] = o[2] = o[3] = o[4] = 0.0;
     return;
