@@ -212,6 +212,8 @@ struct phd_ctx {
   // fused resample + exchange over the peer-memory window (world > 1, exact mode)
   int p2p_state = 0;                       // 0 not set up yet, 1 active, -1 unavailable (send/recv exchange)
   bool p2p_live = false;                   // A currently points into pbuf
+  // phd_step: the update's host bookkeeping waits for the extraction's synchronisation
+  bool defer_update_sync = false, update_pending = false;
   float* pbuf[2] = {nullptr, nullptr};     // this rank's two particle buffers [5][cap_l] (A / B alternate)
   std::vector<float*> peer_buf;            // [world][2]: every rank's pbuf[0], pbuf[1]
   int par = 0;                             // A = pbuf[par] once live; all ranks flip together
@@ -971,6 +973,9 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   return PHD_OK;
 }
 
+static phd_status update_finish(phd_ctx* c);
+constexpr int64_t kEstEager = 256;  // estimates copied with the summary inside phd_step
+
 phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   NvtxRange nvtx_("phd_update");
   if (!c) return PHD_EINVAL;
@@ -1173,7 +1178,19 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   CU(cudaMemcpyAsync(c->h_meta + 3 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
   if (c->select) CU(cudaMemcpyAsync(c->h_meta + 3 * c->world + 32, c->sel_info, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
   timing_record(c, 7);
+  if (c->defer_update_sync) {  // phd_step: finished by phd_extract after its one synchronisation
+    c->update_pending = true;
+    c->stage = kUpdated;
+    return PHD_OK;
+  }
   CU(cudaStreamSynchronize(c->st));
+  return update_finish(c);
+}
+
+// Host side of the end of an update, once its D2H copies (rank masses, NaN flags,
+// index-set meta) have completed.
+static phd_status update_finish(phd_ctx* c) {
+  c->update_pending = false;
   c->W = 0.0;
   c->W_pred = 0.0;
   c->N_all = 0;
@@ -1287,6 +1304,10 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     if (c->world > 1)
       COMM(c->comm->allgather_bytes(c->est, c->gather, sizeof(phd_estimate) * (size_t)(c->p.max_meas + 1), c->st));
     CU(cudaStreamSynchronize(c->st));
+    if (c->update_pending) {
+      phd_status st = update_finish(c);
+      if (st != PHD_OK) return st;
+    }
     const int nloc = (int)smh[5];
     lt_clamped = (int)smh[6];
     c->local_est.resize(nloc);
@@ -1313,19 +1334,32 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
     // the estimate count is min(LT, eligible, cap) <= min(LT, cap): copy that many with the
     // summary, so the extraction costs one synchronisation
-    const int64_t ncopy = out ? std::min<int64_t>(std::max<int64_t>(c->LT, 0), capd) : 0;
+    // (inside phd_step LT is not on the host yet: copy up to kEstEager estimates, the
+    // rest, if any, after the synchronisation)
+    const int64_t ncopy = !out ? 0
+                          : c->update_pending ? std::min<int64_t>(kEstEager, capd)
+                                              : std::min<int64_t>(std::max<int64_t>(c->LT, 0), capd);
     if (ncopy > 0)
       CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * ncopy, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
+    if (c->update_pending) {
+      phd_status st = update_finish(c);
+      if (st != PHD_OK) return st;
+    }
     nest = (int)smh[5];
     lt_clamped = (int)smh[6];
-    if (nest > ncopy && out) {  // not expected (nest <= min(LT, cap)); stay correct anyway
-      CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * nest, cudaMemcpyDeviceToHost, c->st));
+    if (nest > ncopy && out) {  // more estimates than the eager copy (phd_step, LT > kEstEager)
+      CU(cudaMemcpyAsync(c->h_est + ncopy, c->est + 1 + ncopy, sizeof(phd_estimate) * (nest - ncopy),
+                         cudaMemcpyDeviceToHost, c->st));
       CU(cudaStreamSynchronize(c->st));
     }
     if (nest > 0 && out) memcpy(out, c->h_est, sizeof(phd_estimate) * nest);
     timing_record(c, 9);
     if (c->timing) cudaEventElapsedTime(&c->t_ms[4], c->ev[8], c->ev[9]);
+  } else if (c->update_pending) {  // ranks other than the CU: only the update's bookkeeping
+    CU(cudaStreamSynchronize(c->st));
+    phd_status st = update_finish(c);
+    if (st != PHD_OK) return st;
   }
   if (n_out) *n_out = nest;
   if (s) {
@@ -1570,7 +1604,11 @@ phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estima
   timing_record(c, 13);
   phd_status st = phd_predict(c, k, nullptr, 0);
   if (st != PHD_OK) return st;
+  // one host synchronisation for update + extraction: the update's bookkeeping (masses,
+  // LT, the non-finite guard) completes inside phd_extract
+  c->defer_update_sync = true;
   st = phd_update(c, z, M);
+  c->defer_update_sync = false;
   if (st != PHD_OK) return st;
   st = phd_extract(c, out, cap, n_out, s);
   if (st != PHD_OK) return st;
