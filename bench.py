@@ -305,6 +305,9 @@ def run_ours(args):
             z = zs[k - 1]
             if flush:
                 flush_buf.zero_()
+                # the flush's write-back otherwise lands in the step's first kernel (the
+                # library's predict timer read ~50 us more; the step events are unaffected)
+                torch.cuda.synchronize(dev)
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
             f.step_raw(k, z.data_ptr(), int(z.shape[0]))
