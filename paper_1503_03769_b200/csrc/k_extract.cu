@@ -26,7 +26,8 @@ __device__ __forceinline__ bool before(double wa, int la, double wb, int lb) {
 __global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restrict__ acc, int M,
                                                           const double* __restrict__ Wv, const double* __restrict__ Wpv,
                                                           int count, double p_d, EstOut* est, int cap, double* summary,
-                                                          int32_t* count_out, const double* sel_info) {
+                                                          int32_t* count_out, const double* sel_info,
+                                                          const int32_t* __restrict__ sel_flag) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char sm[];
   const int n2m = M <= 1 ? 1 : 1 << (32 - __clz(M - 1));  // next power of two >= M
@@ -72,18 +73,22 @@ __global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restri
   __syncthreads();
   const int nsel = snsel;
   if (nsel <= 0) return;
-  unsigned long long T;
-  int keq;
-  topk_threshold(kw, M, nsel, sh, &T, &keq);
+  // the index set I of k_select is exactly this top-nsel set when nsel is its size
+  // (same keys: k_select and k_reduce_acc compute dW = C (1/D) alike): compact it
+  // instead of selecting again
+  const bool use_sel = sel_flag != nullptr && sel_info != nullptr && (double)nsel == sel_info[3];
+  unsigned long long T = 0ull;
+  int keq = 0;
+  if (!use_sel) topk_threshold(kw, M, nsel, sh, &T, &keq);
   // compact the selected labels in label order
   int carry = 0, carry_eq = 0;
   for (int r = 0; r < M; r += nthr) {
     const int i = r + tid;
     const unsigned long long key = i < M ? kw[i] : 0ull;
-    const bool eq = i < M && key == T;
+    const bool eq = !use_sel && i < M && key == T;
     int tot_eq;
     const int before_eq = carry_eq + topk_round_scan(eq, sh, &tot_eq);
-    const bool take = i < M && (key > T || (eq && before_eq < keq));
+    const bool take = i < M && (use_sel ? sel_flag[i] != 0 : (key > T || (eq && before_eq < keq)));
     int tot;
     const int pos = carry + topk_round_scan(take, sh, &tot);
     if (take) {
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restri
 
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
                            void* est, int cap, double* summary, int32_t* count_out, const double* sel_info,
-                           cudaStream_t s) {
+                           const int32_t* sel_flag, cudaStream_t s) {
   int n2 = 1;
   while (n2 < M) n2 <<= 1;
   size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long) + (size_t)n2 * (sizeof(double) + sizeof(int));
@@ -182,7 +187,7 @@ cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const 
     attr_set = true;
   }
   pdl_launch(k_extract, 1, kTopkThreads, smem, s, acc_lab, M, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
-                                          count_out, sel_info);
+                                          count_out, sel_info, sel_flag);
   return cudaGetLastError();
 }
 

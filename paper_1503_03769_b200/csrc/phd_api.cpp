@@ -1299,7 +1299,7 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     timing_record(c, 8);
     const int capd = c->p.max_meas;
     KL(launch_extract(c->acc, c->M, rank_slots + c->rank, rank_slots + c->world + c->rank, 1, c->p.p_d, c->est + 1,
-                      capd, c->summ, &c->est[0].label, c->select ? c->sel_info : nullptr, c->st));
+                      capd, c->summ, &c->est[0].label, c->select ? c->sel_info : nullptr, nullptr, c->st));
     CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
     if (c->world > 1)
       COMM(c->comm->allgather_bytes(c->est, c->gather, sizeof(phd_estimate) * (size_t)(c->p.max_meas + 1), c->st));
@@ -1330,7 +1330,8 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     timing_record(c, 8);
     int capd = std::max(0, std::min(cap, c->p.max_meas));
     KL(launch_extract(c->acc, c->M, rank_slots, rank_slots + c->world, c->world, c->p.p_d, c->est + 1, capd, c->summ,
-                      &c->est[0].label, c->select ? c->sel_info : nullptr, c->st));
+                      &c->est[0].label, c->select ? c->sel_info : nullptr, c->select ? c->sel_flag : nullptr,
+                      c->st));
     CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
     // the estimate count is min(LT, eligible, cap) <= min(LT, cap): copy that many with the
     // summary, so the extraction costs one synchronisation

@@ -183,7 +183,8 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
 // and their count to *count_out (the header entry of the gather block).
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
                            void* est /*phd_estimate*/, int cap, double* summary /*[8]*/, int32_t* count_out,
-                           const double* sel_info /*nullptr or (W_id, LT, ...) of k_select*/, cudaStream_t s);
+                           const double* sel_info /*nullptr or (W_id, LT, ...) of k_select*/,
+                           const int32_t* sel_flag /*nullptr or k_select's index-set flags*/, cudaStream_t s);
 cudaError_t launch_ring_pack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
                              cudaStream_t s);
 cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
