@@ -361,6 +361,24 @@ def test_full_size_sampled(phd, orc, cname):
     f.set_particles(soa, w, soa.shape[1])
     f.predict(1)
     ps, pw, _ = f.get_particles()
+    # sampled prediction (the launch the bench times: at cfg 5 the float4 path, four
+    # survivors per thread): blocks of survivors, unaligned ones and the block at the
+    # survivor / birth boundary, against the oracle at the same global indices
+    n_out, J = m.fixed_count, m.births_per_step
+    T, sa = m.T, m.sigma_a
+    rng0 = np.random.default_rng(1)
+    for g in [0, 4 * int(rng0.integers(1, n_out // 4 - 300)), int(rng0.integers(1, n_out - 300)) | 1, n_out - 257]:
+        L = min(256, n_out - g)
+        os_, ow = orc.predict(m, 1, soa[:, g:g + L], w[g:g + L], g0=g)
+        tol = 5e-7 * np.abs(os_) + 2e-6 * (0.5 * T * T * sa + T * sa) * 6 + 1e-6
+        assert np.all(np.abs(ps[:, g:g + L] - os_) <= tol), (g, np.max(np.abs(ps[:, g:g + L] - os_) / tol))
+        assert np.allclose(pw[g:g + L], ow, rtol=2e-7, atol=0)
+    if getattr(m, "birth_model", 0) == 0:
+        bs, bw = orc.births(m, 1, n_out, J, None, 0, 64)
+        rscale = 0.0 if m.meas == POSITION else float(m.region[1])
+        tolb = 1e-6 * (np.abs(bs) + rscale) + 1e-5
+        assert np.all(np.abs(ps[:, n_out:n_out + 64] - bs) <= tolb)
+        assert np.allclose(pw[n_out:n_out + 64], bw, rtol=1e-7)
     f.update(Z[0])
     M = len(Z[0])
     C = f.normalizers(M)
