@@ -16,51 +16,110 @@ __device__ __forceinline__ int64_t n_of(double B, double scale, double U, int64_
   return n;
 }
 
-// Exclusive fp64 scan of the per-block masses (one CTA; fixed order): thread t
-// owns the contiguous chunk [t c, t c + c) (loads issued together), warp-shuffle
-// scan of the chunk sums, then the chunk is rewritten with its offsets.
-__global__ void __launch_bounds__(1024) k_scan_blocks(const double* __restrict__ blk, int nb, double* off) {
-  pdl_wait();
-  __shared__ double ws[32];
+// One-CTA exclusive scan of a long array (1024 threads): tiles of 4096 loaded
+// coalesced into shared memory, each thread folds 4 consecutive elements, a warp
+// shuffle scan and a scan of the 32 warp totals give the offsets, the tile is
+// written back coalesced, and the carry moves to the next tile.  Fixed order
+// (deterministic); Op is associative (fp64 add in this order, or int max).
+constexpr int kCtaScanTile = 4096;
+
+template <class T, class Op>
+__device__ __forceinline__ T cta_exclusive_scan(const T* in, T* out, int n, T ident, Op op, T* sm, T* ws) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int chunk = (nb + 1023) / 1024;
-  const int b0 = min(nb, tid * chunk), b1 = min(nb, b0 + chunk);
-  double loc = 0.0;
-  int b = b0;
-  for (; b + 8 <= b1; b += 8) {
-    double v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = __ldg(blk + b + r);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) loc += v[r];
-  }
-  for (; b < b1; ++b) loc += __ldg(blk + b);
-  double incl = loc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) ws[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const double t = ws[lane];
-    double x = t;
+  T carry = ident;
+  if (n <= 1024) {  // one element per thread, no shared-memory staging
+    const T v = tid < n ? in[tid] : ident;
+    T incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const double v = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += v;
+      const T y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = op(y, incl);
     }
-    ws[lane] = x - t;  // exclusive warp offsets
-    if (lane == 31) off[nb] = x;
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      T x = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = op(y, x);
+      }
+      const T prev = __shfl_up_sync(0xffffffffu, x, 1);
+      ws[lane] = lane > 0 ? prev : ident;
+      if (lane == 31) ws[32] = x;
+    }
+    __syncthreads();
+    const T prevl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (tid < n) out[tid] = lane > 0 ? op(ws[warp], prevl) : ws[warp];
+    return ws[32];
   }
-  __syncthreads();
-  const double prevl = __shfl_up_sync(0xffffffffu, incl, 1);  // exclusive, exact (no subtraction)
-  double run = lane > 0 ? ws[warp] + prevl : ws[warp];
-  for (b = b0; b < b1; ++b) {
-    off[b] = run;
-    run += __ldg(blk + b);
+  for (int t0 = 0; t0 < n; t0 += kCtaScanTile) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = t0 + r * 1024 + tid;
+      sm[r * 1024 + tid] = i < n ? in[i] : ident;
+    }
+    __syncthreads();
+    T v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = sm[4 * tid + k];
+    T tot = v[0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) tot = op(tot, v[k]);
+    T incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = op(y, incl);
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const T x0 = ws[lane];
+      T x = x0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = op(y, x);
+      }
+      const T prev = __shfl_up_sync(0xffffffffu, x, 1);
+      ws[lane] = lane > 0 ? op(carry, prev) : carry;  // exclusive warp offsets incl. the carry
+      if (lane == 31) ws[32] = op(carry, x);          // carry after this tile
+    }
+    __syncthreads();
+    const T prevl = __shfl_up_sync(0xffffffffu, incl, 1);  // exclusive within the warp
+    T run = lane > 0 ? op(ws[warp], prevl) : ws[warp];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      sm[4 * tid + k] = run;
+      run = op(run, v[k]);
+    }
+    carry = ws[32];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = t0 + r * 1024 + tid;
+      if (i < n) out[i] = sm[r * 1024 + tid];
+    }
+    __syncthreads();
   }
+  return carry;
+}
+
+struct AddF64 {
+  __device__ __forceinline__ double operator()(double a, double b) const { return a + b; }
+};
+struct MaxI32 {
+  __device__ __forceinline__ int operator()(int a, int b) const { return max(a, b); }
+};
+
+// Exclusive fp64 scan of the per-block masses (one CTA; fixed order); off[nb] = total.
+__global__ void __launch_bounds__(1024) k_scan_blocks(const double* __restrict__ blk, int nb, double* off) {
+  pdl_wait();
+  __shared__ double sm[kCtaScanTile];
+  __shared__ double ws[33];
+  const double tot = cta_exclusive_scan(blk, off, nb, 0.0, AddF64{}, sm, ws);
+  if (threadIdx.x == 0) off[nb] = tot;
 }
 
 cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s) {
@@ -201,51 +260,12 @@ cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cud
   return cudaGetLastError();
 }
 
-// In place: bmax[b] <- max(bmax[0..b-1]) (exclusive; -1 for b = 0).  Chunked as k_scan_blocks.
+// In place: bmax[b] <- max(bmax[0..b-1]) (exclusive; -1 for b = 0).
 __global__ void __launch_bounds__(1024) k_scan_max(int32_t* bmax, int nb) {
   pdl_wait();
-  __shared__ int ws[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int chunk = (nb + 1023) / 1024;
-  const int b0 = min(nb, tid * chunk), b1 = min(nb, b0 + chunk);
-  int loc = -1;
-  int b = b0;
-  for (; b + 8 <= b1; b += 8) {
-    int v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = bmax[b + r];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) loc = max(loc, v[r]);
-  }
-  for (; b < b1; ++b) loc = max(loc, bmax[b]);
-  int incl = loc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl = max(incl, v);
-  }
-  if (lane == 31) ws[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const int t = ws[lane];
-    int x = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x = max(x, v);
-    }
-    const int prev = __shfl_up_sync(0xffffffffu, x, 1);
-    ws[lane] = lane > 0 ? prev : -1;  // exclusive warp maxima
-  }
-  __syncthreads();
-  int run = ws[warp];
-  const int prevl = __shfl_up_sync(0xffffffffu, incl, 1);
-  if (lane > 0) run = max(run, prevl);
-  for (b = b0; b < b1; ++b) {
-    const int v = bmax[b];
-    bmax[b] = run;
-    run = max(run, v);
-  }
+  __shared__ int sm[kCtaScanTile];
+  __shared__ int ws[33];
+  cta_exclusive_scan(bmax, bmax, nb, -1, MaxI32{}, sm, ws);
 }
 
 cudaError_t launch_scan_max(int32_t* bmax, int nb, cudaStream_t s) {

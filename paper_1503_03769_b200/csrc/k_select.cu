@@ -38,24 +38,23 @@ __global__ void __launch_bounds__(256) k_block_sum(const float* __restrict__ w, 
   }
 }
 
-// One CTA of 1024: thread t sums the contiguous chunk [t c, t c + c) of the
-// block sums (loads issued together), then a fixed-order warp/block tree.
+// One CTA of 1024: thread t sums the block sums t, t + 1024, ... (coalesced, eight
+// loads in flight), then a fixed-order warp/block tree.
 __global__ void __launch_bounds__(1024) k_sum_blocks(const double* __restrict__ blk, int nb, double* out) {
   pdl_wait();
   __shared__ double s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int chunk = (nb + 1023) / 1024;
-  const int b0 = min(nb, tid * chunk), b1 = min(nb, b0 + chunk);
   double a = 0.0;
-  int b = b0;
-  for (; b + 8 <= b1; b += 8) {
+  for (int b0 = 0; b0 < nb; b0 += 8 * 1024) {
     double v[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = __ldg(blk + b + r);
+    for (int r = 0; r < 8; ++r) {
+      const int b = b0 + r * 1024 + tid;
+      v[r] = b < nb ? __ldg(blk + b) : 0.0;
+    }
 #pragma unroll
     for (int r = 0; r < 8; ++r) a += v[r];
   }
-  for (; b < b1; ++b) a += __ldg(blk + b);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   if (lane == 0) s[warp] = a;
