@@ -933,6 +933,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
 }
 
 // one warp per label: fixed-order fp64 sum of its entries (lane-strided + xor tree)
+constexpr int kGR = 8;
 template <int PASS>
 __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__ mstart, const int32_t* __restrict__ mlist,
                                                      int M, const double* __restrict__ part1,
@@ -946,21 +947,39 @@ __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__
   const int j0 = live ? mstart[l] : 0, j1 = live ? mstart[l + 1] : 0;
   if (PASS == 1) {
     double s = 0.0;
-    for (int j = j0 + lane; j < j1; j += 32) {
-      PHD_DCHECK(mlist[j] >= 0 && mlist[j] < mstart[M]);
-      s += part1[mlist[j]];
+    // kGR entries per lane per round: index loads, then partial loads, in flight
+    for (int j = j0 + lane; j < j1; j += 32 * kGR) {
+      int e[kGR];
+#pragma unroll
+      for (int r = 0; r < kGR; ++r) e[r] = j + 32 * r < j1 ? mlist[j + 32 * r] : -1;
+      double v[kGR];
+#pragma unroll
+      for (int r = 0; r < kGR; ++r) {
+        PHD_DCHECK(e[r] < mstart[M]);
+        v[r] = e[r] >= 0 ? part1[e[r]] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kGR; ++r) s += v[r];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) out[l] = s;
   } else {
     double s[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int j = j0 + lane; j < j1; j += 32) {
-      const float4 a = part2[mlist[j]];
-      s[0] += (double)a.x;
-      s[1] += (double)a.y;
-      s[2] += (double)a.z;
-      s[3] += (double)a.w;
+    for (int j = j0 + lane; j < j1; j += 32 * kGR) {
+      int e[kGR];
+#pragma unroll
+      for (int r = 0; r < kGR; ++r) e[r] = j + 32 * r < j1 ? mlist[j + 32 * r] : -1;
+      float4 v[kGR];
+#pragma unroll
+      for (int r = 0; r < kGR; ++r) v[r] = e[r] >= 0 ? part2[e[r]] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int r = 0; r < kGR; ++r) {
+        s[0] += (double)v[r].x;
+        s[1] += (double)v[r].y;
+        s[2] += (double)v[r].z;
+        s[3] += (double)v[r].w;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {

@@ -752,9 +752,21 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double sa[256], sb[256];
     double a = 0.0, b = 0.0;
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-      a += blk_w[k];
-      b += blk_wp[k];
+    // eight loads of each array in flight per round (one round trip each, not one
+    // per element); the sums keep the element order k = tid, tid + 256, ...
+    for (int k0 = threadIdx.x; k0 < nb; k0 += 8 * (int)blockDim.x) {
+      double va[8], vb[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int k = k0 + r * (int)blockDim.x;
+        va[r] = k < nb ? blk_w[k] : 0.0;
+        vb[r] = k < nb ? blk_wp[k] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        a += va[r];
+        b += vb[r];
+      }
     }
     sa[threadIdx.x] = a;
     sb[threadIdx.x] = b;
