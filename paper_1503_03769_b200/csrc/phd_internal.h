@@ -291,7 +291,7 @@ cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* hist
                       int32_t* zcell_start, int32_t* zcell_items, float2* zcell_z, cudaStream_t s, int64_t* launches);
 // per-tile bounding boxes + candidate counts (fill = 0) or labels (fill = 1)
 // (fill = 0 also buffers the first kGateKBuf candidates per tile in cbuf [ntiles][kGateKBuf])
-constexpr int kGateKBufH = 512;
+constexpr int kGateKBufH = 1024;
 cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1,
                        const GateGrid& grid, const int32_t* zcell_start, const int32_t* zcell_items,
                        const float2* zcell_z, int32_t* tcount, const int32_t* tstart, int32_t* cbuf, int32_t* cand,

@@ -60,3 +60,19 @@ for q in (50, 75, 90, 95, 99, 99.9, 100):
 print("  tiles with K > 512: %d (%.2f%%), their entries %.1f%% of E" % ((K > 512).sum(), 100 * (K > 512).mean(),
       100 * K[K > 512].sum() / max(1, K.sum())))
 print("  tiles with K > 256: %d, entries %.1f%% of E" % ((K > 256).sum(), 100 * K[K > 256].sum() / max(1, K.sum())))
+# window sizes in cells (the enumeration rounds of k_gate_count / tile_enum) and the fast path
+full = np.arange(nt) < n // T
+kf = key[order]
+kpad = np.concatenate([kf, np.full(pad, -1)]).reshape(nt, T)
+cx0 = np.concatenate([c0[order], np.full(pad, -1)]).reshape(nt, T)
+cy0 = np.concatenate([c1[order], np.full(pad, -1)]).reshape(nt, T)
+fast = full & (kpad[:, 0] == kpad[:, -1]) & (cx0[:, 0] > 0) & (cx0[:, 0] < G - 1) & (cy0[:, 0] > 0) & (cy0[:, 0] < G - 1)
+Rw = np.sqrt(np.maximum(lwm + 130, 0) / alpha)
+h = (hi0 - lo0) / G
+nx = np.floor((bx1 + Rw - lo0) / h).clip(0, G - 1) - np.floor((bx0 - Rw - lo0) / h).clip(0, G - 1) + 1
+ny = np.floor((by1 + Rw - lo1) / h).clip(0, G - 1) - np.floor((by0 - Rw - lo1) / h).clip(0, G - 1) + 1
+nc = (nx * ny).astype(np.int64)
+print("fast-path tiles %.1f%%" % (100 * fast.mean()))
+for q in (50, 90, 99, 99.9, 100):
+    print("  window cells p%-5s %d  (rounds of 32: %d)" % (q, np.percentile(nc, q), -(-np.percentile(nc, q) // 32)))
+print("  tiles with > 1024 window cells: %d" % (nc > 1024).sum())
