@@ -305,8 +305,10 @@ def run_ours(args):
             z = zs[k - 1]
             if flush:
                 flush_buf.zero_()
-                # the flush's write-back otherwise lands in the step's first kernel (the
-                # library's predict timer read ~50 us more; the step events are unaffected)
+                # wait for the flush: otherwise its tail overlaps the step (the library's
+                # predict timer read ~50 us more) and hides the host's launch latency of the
+                # step's first kernels, which a filter loop does pay (the GPU idles at the
+                # step's start, after the previous step's estimates were read back)
                 torch.cuda.synchronize(dev)
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
