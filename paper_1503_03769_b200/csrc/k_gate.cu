@@ -961,8 +961,13 @@ template <int PASS>
 __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__ mstart, const int32_t* __restrict__ mlist,
                                                      int M, const double* __restrict__ part1,
                                                      const float4* __restrict__ part2, const int32_t* __restrict__ sel,
-                                                     double* out, int slots_pad) {
+                                                     double* out, int slots_pad, const double* __restrict__ wblk,
+                                                     int nwb, double* wout) {
   pdl_wait();
+  if (PASS == 1 && wblk != nullptr && blockIdx.x == gridDim.x - 1) {  // the rank's W_pred (rides in C1)
+    block_sum_f64(wblk, nwb, wout);
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (l >= slots_pad) return;
@@ -1164,14 +1169,17 @@ cudaError_t launch_gpass(int pass, const GateArgs& g, cudaStream_t s) {
 }
 
 cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* mlist, int M, const double* part1,
-                               const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s) {
-  if (slots_pad <= 0) return cudaSuccess;
-  const unsigned blocks = (unsigned)((slots_pad + 7) / 8);
+                               const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s,
+                               const double* wblk, int nwb, double* wout) {
+  if (pass != 1) wblk = nullptr;
+  const unsigned blocks = (unsigned)((std::max(slots_pad, 0) + 7) / 8 + (wblk ? 1 : 0));
+  if (blocks == 0) return cudaSuccess;
   if (pass == 1)
-    pdl_launch(k_gate_reduce<1>, blocks, 256, 0, s, mstart, mlist, M, part1, nullptr, nullptr, out, slots_pad);
+    pdl_launch(k_gate_reduce<1>, blocks, 256, 0, s, mstart, mlist, M, part1, nullptr, nullptr, out, slots_pad, wblk,
+               nwb, wout);
   else
     pdl_launch(k_gate_reduce<2>, blocks, 256, 0, s, mstart, mlist, M, nullptr, reinterpret_cast<const float4*>(part2), sel,
-                                            out, slots_pad);
+                                            out, slots_pad, nullptr, 0, nullptr);
   return cudaGetLastError();
 }
 

@@ -15,7 +15,8 @@
 
 namespace phd {
 
-// fp64 block sums of w (kBlockW per block), then one CTA reduces them to *out.
+// fp64 block sums of w (kBlockW per block); the rank total is summed by an extra
+// block of the C reduction (block_sum_f64) so that it rides in the C1 all-reduce.
 __global__ void __launch_bounds__(256) k_block_sum(const float* __restrict__ w, int64_t n, double* blk) {
   pdl_wait();
   __shared__ double sw[8];
@@ -38,43 +39,9 @@ __global__ void __launch_bounds__(256) k_block_sum(const float* __restrict__ w, 
   }
 }
 
-// One CTA of 1024: thread t sums the block sums t, t + 1024, ... (coalesced, eight
-// loads in flight), then a fixed-order warp/block tree.
-__global__ void __launch_bounds__(1024) k_sum_blocks(const double* __restrict__ blk, int nb, double* out) {
-  pdl_wait();
-  __shared__ double s[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double a = 0.0;
-  for (int b0 = 0; b0 < nb; b0 += 8 * 1024) {
-    double v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int b = b0 + r * 1024 + tid;
-      v[r] = b < nb ? __ldg(blk + b) : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) a += v[r];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  if (lane == 0) s[warp] = a;
-  __syncthreads();
-  if (warp == 0) {
-    a = s[lane];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) *out = a;
-  }
-}
-
-cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cudaStream_t s) {
+cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream_t s) {
   int nb = (int)((n + kBlockW - 1) / kBlockW);
-  if (nb > 0) {
-    pdl_launch(k_block_sum, nb, 256, 0, s, w, n, blk);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  pdl_launch(k_sum_blocks, 1, 1024, 0, s, blk, nb, out);
+  if (nb > 0) pdl_launch(k_block_sum, nb, 256, 0, s, w, n, blk);
   return cudaGetLastError();
 }
 
@@ -169,7 +136,8 @@ __device__ __forceinline__ int seq_slot(int p, int n_s, int lanes, int zl, int j
 
 __global__ void __launch_bounds__(1024) k_slots2(const float* __restrict__ z, const int32_t* __restrict__ sel_flag,
                                                  int M, int model, int zl, int slots_pad, int32_t* slot_label,
-                                                 int32_t* js_out) {
+                                                 int32_t* js_out, float sx, float sy, SlotConsts sc,
+                                                 const double* __restrict__ D_lab) {
   pdl_wait();
   __shared__ int wsum[32];
   __shared__ int base_s;
@@ -255,31 +223,42 @@ __global__ void __launch_bounds__(1024) k_slots2(const float* __restrict__ z, co
     if (phase == 0 && tid == 0) cat_start[6] = base_s;
     __syncthreads();
   }
+  // per-slot constants of the new layout (as k_zprep) and d = 1/D (as k_zconst):
+  // padding slots get the sentinel that makes every term exactly 0
+  for (int s = tid; s < slots_pad; s += nthr) {
+    const int lab = slot_label[s];
+    float s0 = -1e30f, s1 = -1e30f, s2 = 0.0f, s3 = 0.0f, d = 0.0f;
+    int rep = 0;
+    if (lab >= 0) {
+      const float z0 = z[2 * lab], z1 = z[2 * lab + 1];
+      s0 = -z0;
+      s1 = -z1;
+      if (model == kRangeBearing) {
+        rep = (z1 > hp) ? 1 : ((z1 < -hp) ? 2 : 0);
+        float sn, cs;
+        sincosf(z1, &sn, &cs);
+        s2 = -(sx + z0 * cs);
+        s3 = -(sy + z0 * sn);
+      }
+      const double D = D_lab[lab];
+      d = D > 0.0 ? (float)fmin(1.0 / D, 3.0e38) : 0.0f;
+    }
+    sc.s0[s] = s0;
+    sc.s1[s] = s1;
+    if (sc.s2) {
+      sc.s2[s] = s2;
+      sc.s3[s] = s3;
+    }
+    if (sc.rep) sc.rep[s] = rep;
+    sc.d[s] = d;
+  }
 }
 
 cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
-                          int32_t* slot_label, int32_t* js, cudaStream_t s) {
-  pdl_launch(k_slots2, 1, 1024, 0, s, z, sel_flag, M, model, zl, slots_pad, slot_label, js);
-  return cudaGetLastError();
-}
-
-// Per-slot d = 1/D(label) for the pass-2 layout (0 for padding).
-__global__ void k_dslot(const int32_t* __restrict__ slot_label, const double* __restrict__ D_lab, int n, float* d) {
-  pdl_wait();
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  int lab = slot_label[s];
-  float v = 0.0f;
-  if (lab >= 0) {
-    double D = D_lab[lab];
-    v = D > 0.0 ? (float)fmin(1.0 / D, 3.0e38) : 0.0f;
-  }
-  d[s] = v;
-}
-
-cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, float* d, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  pdl_launch(k_dslot, (n + 255) / 256, 256, 0, s, slot_label, D_lab, n, d);
+                          int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
+                          const double* D_lab, cudaStream_t s) {
+  pdl_launch(k_slots2, 1, 1024, 0, s, z, sel_flag, M, model, zl, slots_pad, slot_label, js, sensor_x, sensor_y, sc,
+             D_lab);
   return cudaGetLastError();
 }
 

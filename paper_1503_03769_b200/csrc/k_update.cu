@@ -628,8 +628,12 @@ cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_labe
 // C_slot[s] = sum over particle-CTAs (fixed order) of the pass-1 partials (fp64),
 // for the slot range [s0, s1) (one measurement group).
 __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_pad, int s0, int s1,
-                           double* C_slot) {
+                           double* C_slot, const double* __restrict__ wblk, int nwb, double* wout) {
   pdl_wait();
+  if (wblk != nullptr && blockIdx.x == gridDim.x - 1) {  // the rank's W_pred (rides in C1)
+    block_sum_f64(wblk, nwb, wout);
+    return;
+  }
   // one warp per slot, lanes over the particle-CTA partials, fixed-order xor tree
   const int lane = threadIdx.x & 31;
   int s = s0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -643,9 +647,10 @@ __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_p
 }
 
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
-                            cudaStream_t s) {
-  if (s1 <= s0) return cudaSuccess;
-  pdl_launch(k_reduce_C, (s1 - s0 + 7) / 8, 256, 0, s, Cpart, gp, slots_pad, s0, s1, C_slot);
+                            cudaStream_t s, const double* wblk, int nwb, double* wout) {
+  const int blocks = (std::max(s1 - s0, 0) + 7) / 8 + (wblk ? 1 : 0);
+  if (blocks == 0) return cudaSuccess;
+  pdl_launch(k_reduce_C, blocks, 256, 0, s, Cpart, gp, slots_pad, s0, s1, C_slot, wblk, nwb, wout);
   return cudaGetLastError();
 }
 

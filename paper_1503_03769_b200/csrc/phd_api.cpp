@@ -1098,8 +1098,9 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     timing_record(c, 3);
     if (ntiles > 0) KL(launch_gpass(1, ga, c->st));
     timing_record(c, 4);
-    KL(launch_wsum(c->A[4], n, c->blk_wp, c->C_slot + c->slots_pad, c->st));
-    KL(launch_gate_reduce(1, c->gmstart, c->gmlist, M, c->gpart1, nullptr, nullptr, c->C_slot, c->slots_pad, c->st));
+    KL(launch_block_sums(c->A[4], n, c->blk_wp, c->st));
+    KL(launch_gate_reduce(1, c->gmstart, c->gmlist, M, c->gpart1, nullptr, nullptr, c->C_slot, c->slots_pad, c->st,
+                          c->blk_wp, (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad));
     if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
     KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
     if (c->select) {
@@ -1131,18 +1132,17 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 4);
     // local W_pred rides with C in the C1 all-reduce (element slots_pad)
-    KL(launch_wsum(c->A[4], n, c->blk_wp, c->C_slot + c->slots_pad, c->st));
-    KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, 0, c->slots_pad, c->C_slot, c->st));
+    KL(launch_block_sums(c->A[4], n, c->blk_wp, c->st));
+    KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, 0, c->slots_pad, c->C_slot, c->st, c->blk_wp,
+                       (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad));
     if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
     KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
     if (c->select) {
       // index set I from dW = C/D and the mass identity; pass-2 slot layout with I first
       KL(launch_select(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->st));
-      KL(launch_slots2(c->zlab, c->sel_flag, M, c->model, c->zl, c->slots_pad, c->slot_label, c->s_lim, c->st));
       SlotConsts sc2{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
-      KL(launch_zprep(c->model, c->zlab, c->slot_label, c->slots_pad, (float)c->p.sensor_xy[0],
-                      (float)c->p.sensor_xy[1], sc2, c->st));
-      KL(launch_dslot(c->slot_label, c->D, c->slots_pad, c->s[4], c->st));
+      KL(launch_slots2(c->zlab, c->sel_flag, M, c->model, c->zl, c->slots_pad, c->slot_label, c->s_lim,
+                       (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc2, c->D, c->st));
       pa.js = c->s_lim;
     }
     timing_record(c, 5);

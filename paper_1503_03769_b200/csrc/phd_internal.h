@@ -166,8 +166,10 @@ int pass_occupancy(int model, int pass, int wz, int zl);
 cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,
                          int zbg, int wz, cudaStream_t s);
 int fused_occupancy(int model, int wz);
+// (wblk != nullptr: one extra block also writes *wout = sum of wblk[0..nwb), the
+// rank's W_pred from the block sums of launch_block_sums, which then rides in C1)
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
-                            cudaStream_t s);
+                            cudaStream_t s, const double* wblk = nullptr, int nwb = 0, double* wout = nullptr);
 cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
                           float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s);
 // inv != nullptr (gated update): P is one plane in sorted order, read as P[inv[i]]
@@ -210,12 +212,13 @@ cudaError_t launch_gather_p2p(const int32_t* marks, const int32_t* bmax_excl, in
                               cudaStream_t s);
 cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 // label selection before pass 2 (k_select.cu)
-cudaError_t launch_wsum(const float* w, int64_t n, double* blk, double* out, cudaStream_t s);
+cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream_t s);  // blk only
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                           int32_t* sel_flag, double* info, cudaStream_t s);
+// also writes the per-slot constants of the new layout (as k_zprep) and d = 1/D
 cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
-                          int32_t* slot_label, int32_t* js, cudaStream_t s);
-cudaError_t launch_dslot(const int32_t* slot_label, const double* D_lab, int n, float* d, cudaStream_t s);
+                          int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
+                          const double* D_lab, cudaStream_t s);
 
 // ---- gated update (k_gate.cu, DESIGN.md §5 "Gated update") ------------------
 // Particles are ordered by a Morton cell key in measurement space (stable
@@ -230,6 +233,31 @@ constexpr int kGateBins = kGateG * kGateG;
 // Counting-sort blocks (8 warps each): sort_block(n) items per block, a power of two
 // in [kSortBlockMin, kSortBlockMax] giving about kSortBlocks blocks, so small sorts
 // still fill the GPU and the 16-bit per-warp counters never overflow.
+// One block sums a[0..n) in fixed order (thread t: t, t + blockDim, ..., eight loads
+// in flight; then a warp tree and a tree over the warps); thread 0 writes *out.
+__device__ __forceinline__ void block_sum_f64(const double* __restrict__ a, int n, double* out) {
+  __shared__ double ws_[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  double acc = 0.0;
+  for (int k0 = tid; k0 < n; k0 += 8 * nt) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = k0 + r * nt < n ? a[k0 + r * nt] : 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc += v[r];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) ws_[warp] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    acc = lane < (nt >> 5) ? ws_[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) *out = acc;
+  }
+}
+
 constexpr int kSortBlockMin = 2048;
 constexpr int kSortBlockMax = 65536;
 constexpr int kSortBlocks = 256;
@@ -305,7 +333,9 @@ cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kb
 cudaError_t launch_gpass(int pass, const GateArgs& g, cudaStream_t s);
 // per-label fixed-order fp64 sums over its entries: pass 1 -> C_slot[l];
 // pass 2 -> A[q * slots_pad + l] for labels in I (all with sel == nullptr)
+// pass 1 with wblk != nullptr: one extra block writes *wout = sum of wblk[0..nwb) (see launch_reduce_C)
 cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* mlist, int M, const double* part1,
-                               const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s);
+                               const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s,
+                               const double* wblk = nullptr, int nwb = 0, double* wout = nullptr);
 
 }  // namespace phd
