@@ -962,7 +962,7 @@ __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__
                                                      int M, const double* __restrict__ part1,
                                                      const float4* __restrict__ part2, const int32_t* __restrict__ sel,
                                                      double* out, int slots_pad, const double* __restrict__ wblk,
-                                                     int nwb, double* wout) {
+                                                     int nwb, double* wout, ZConstArgs zc) {
   pdl_wait();
   if (PASS == 1 && wblk != nullptr && blockIdx.x == gridDim.x - 1) {  // the rank's W_pred (rides in C1)
     block_sum_f64(wblk, nwb, wout);
@@ -991,7 +991,10 @@ __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[l] = s;
+    if (lane == 0) {
+      out[l] = s;
+      if (zc.slot_label) zconst_one(zc, l, s);  // one rank: C is final here
+    }
   } else {
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = j0 + lane; j < j1; j += 32 * kGR) {
@@ -1170,16 +1173,17 @@ cudaError_t launch_gpass(int pass, const GateArgs& g, cudaStream_t s) {
 
 cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* mlist, int M, const double* part1,
                                const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s,
-                               const double* wblk, int nwb, double* wout) {
+                               const double* wblk, int nwb, double* wout, const ZConstArgs* zc) {
   if (pass != 1) wblk = nullptr;
+  const ZConstArgs z = zc && pass == 1 ? *zc : ZConstArgs{};
   const unsigned blocks = (unsigned)((std::max(slots_pad, 0) + 7) / 8 + (wblk ? 1 : 0));
   if (blocks == 0) return cudaSuccess;
   if (pass == 1)
     pdl_launch(k_gate_reduce<1>, blocks, 256, 0, s, mstart, mlist, M, part1, nullptr, nullptr, out, slots_pad, wblk,
-               nwb, wout);
+               nwb, wout, z);
   else
     pdl_launch(k_gate_reduce<2>, blocks, 256, 0, s, mstart, mlist, M, nullptr, reinterpret_cast<const float4*>(part2), sel,
-                                            out, slots_pad, nullptr, 0, nullptr);
+                                            out, slots_pad, nullptr, 0, nullptr, z);
   return cudaGetLastError();
 }
 

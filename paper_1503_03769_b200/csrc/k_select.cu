@@ -47,13 +47,9 @@ cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream
 
 // One CTA.  sel_flag[l] = 1 for l in I; info = (W_id, LT, n_eligible, n_sel).
 // I = the n_sel largest dW (ties: lowest labels), by radix select (topk.cuh).
-__global__ void __launch_bounds__(kTopkThreads) k_select(const double* __restrict__ C_lab,
-                                                         const double* __restrict__ D_lab, int M,
-                                                         const double* __restrict__ W_pred, double p_d,
-                                                         int32_t* sel_flag, double* info) {
-  pdl_wait();
-  extern __shared__ __align__(16) unsigned char sm[];
-  unsigned long long* kw = reinterpret_cast<unsigned long long*>(sm);
+__device__ __forceinline__ void select_body(const double* __restrict__ C_lab, const double* __restrict__ D_lab,
+                                            int M, const double* __restrict__ W_pred, double p_d, int32_t* sel_flag,
+                                            double* info, unsigned long long* kw) {
   __shared__ TopkShared sh;
   __shared__ double red[32];
   __shared__ int n_elig, snsel;
@@ -90,7 +86,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_select(const double* __restric
   }
   __syncthreads();
   const int nsel = snsel;
-  if (nsel <= 0) return;
+  if (nsel <= 0) return;  // uniform over the CTA
   unsigned long long T;
   int keq;
   topk_threshold(kw, M, nsel, sh, &T, &keq);
@@ -104,6 +100,15 @@ __global__ void __launch_bounds__(kTopkThreads) k_select(const double* __restric
     if (i < M && (key > T || (eq && before < keq))) sel_flag[i] = 1;
     carry += tot;
   }
+}
+
+__global__ void __launch_bounds__(kTopkThreads) k_select(const double* __restrict__ C_lab,
+                                                         const double* __restrict__ D_lab, int M,
+                                                         const double* __restrict__ W_pred, double p_d,
+                                                         int32_t* sel_flag, double* info) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char sm[];
+  select_body(C_lab, D_lab, M, W_pred, p_d, sel_flag, info, reinterpret_cast<unsigned long long*>(sm));
 }
 
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
@@ -134,11 +139,9 @@ __device__ __forceinline__ int seq_slot(int p, int n_s, int lanes, int zl, int j
   return l * zl + 2 * js + q % rest;
 }
 
-__global__ void __launch_bounds__(1024) k_slots2(const float* __restrict__ z, const int32_t* __restrict__ sel_flag,
-                                                 int M, int model, int zl, int slots_pad, int32_t* slot_label,
-                                                 int32_t* js_out, float sx, float sy, SlotConsts sc,
-                                                 const double* __restrict__ D_lab) {
-  pdl_wait();
+__device__ __forceinline__ void slots2_body(const float* __restrict__ z, const int32_t* sel_flag, int M, int model,
+                                            int zl, int slots_pad, int32_t* slot_label, int32_t* js_out, float sx,
+                                            float sy, const SlotConsts& sc, const double* __restrict__ D_lab) {
   __shared__ int wsum[32];
   __shared__ int base_s;
   __shared__ int cat_start[7];
@@ -254,11 +257,33 @@ __global__ void __launch_bounds__(1024) k_slots2(const float* __restrict__ z, co
   }
 }
 
-cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
-                          int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
-                          const double* D_lab, cudaStream_t s) {
-  pdl_launch(k_slots2, 1, 1024, 0, s, z, sel_flag, M, model, zl, slots_pad, slot_label, js, sensor_x, sensor_y, sc,
-             D_lab);
+// Dense path: the index set and the pass-2 layout in one CTA (one launch).
+__global__ void __launch_bounds__(kTopkThreads) k_select_slots(const double* __restrict__ C_lab,
+                                                               const double* __restrict__ D_lab, int M,
+                                                               const double* __restrict__ W_pred, double p_d,
+                                                               int32_t* sel_flag, double* info,
+                                                               const float* __restrict__ z, int model, int zl,
+                                                               int slots_pad, int32_t* slot_label, int32_t* js_out,
+                                                               float sx, float sy, SlotConsts sc) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char sm[];
+  select_body(C_lab, D_lab, M, W_pred, p_d, sel_flag, info, reinterpret_cast<unsigned long long*>(sm));
+  __syncthreads();  // sel_flag (global) complete and visible to the CTA
+  slots2_body(z, sel_flag, M, model, zl, slots_pad, slot_label, js_out, sx, sy, sc, D_lab);
+}
+
+cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
+                                int32_t* sel_flag, double* info, const float* z, int model, int zl, int slots_pad,
+                                int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
+                                cudaStream_t s) {
+  size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_select_slots, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    attr = true;
+  }
+  pdl_launch(k_select_slots, 1, kTopkThreads, smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info, z, model, zl,
+             slots_pad, slot_label, js, sensor_x, sensor_y, sc);
   return cudaGetLastError();
 }
 

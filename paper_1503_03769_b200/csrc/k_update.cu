@@ -627,8 +627,9 @@ cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_labe
 
 // C_slot[s] = sum over particle-CTAs (fixed order) of the pass-1 partials (fp64),
 // for the slot range [s0, s1) (one measurement group).
+// zc != nullptr (one rank: no all-reduce between): also the per-slot constants of k_zconst.
 __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_pad, int s0, int s1,
-                           double* C_slot, const double* __restrict__ wblk, int nwb, double* wout) {
+                           double* C_slot, const double* __restrict__ wblk, int nwb, double* wout, ZConstArgs zc) {
   pdl_wait();
   if (wblk != nullptr && blockIdx.x == gridDim.x - 1) {  // the rank's W_pred (rides in C1)
     block_sum_f64(wblk, nwb, wout);
@@ -643,42 +644,36 @@ __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_p
   for (int b = lane; b < gp; b += 32) c += Cpart[(int64_t)b * slots_pad + s];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0) C_slot[s] = c;
+  if (lane == 0) {
+    C_slot[s] = c;
+    if (zc.slot_label) zconst_one(zc, s, c);
+  }
 }
 
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
-                            cudaStream_t s, const double* wblk, int nwb, double* wout) {
+                            cudaStream_t s, const double* wblk, int nwb, double* wout, const ZConstArgs* zc) {
   const int blocks = (std::max(s1 - s0, 0) + 7) / 8 + (wblk ? 1 : 0);
   if (blocks == 0) return cudaSuccess;
-  pdl_launch(k_reduce_C, blocks, 256, 0, s, Cpart, gp, slots_pad, s0, s1, C_slot, wblk, nwb, wout);
+  const ZConstArgs z = zc ? *zc : ZConstArgs{};
+  pdl_launch(k_reduce_C, blocks, 256, 0, s, Cpart, gp, slots_pad, s0, s1, C_slot, wblk, nwb, wout, z);
   return cudaGetLastError();
 }
 
 // For slots [s0, s1) of one group, with C_slot global (after the C1 all-reduce):
 // D = kappa + C, per-slot d = 1/D as fp32 (0 when D == 0 or padding), and the
 // label-order copies C_lab, D_lab used by the STPHD reduction and the getters.
-__global__ void k_zconst(const double* __restrict__ C_slot, const int32_t* __restrict__ slot_label, int s0, int s1,
-                         double kappa, float* d_slot, double* C_lab, double* D_lab, int* bad) {
+__global__ void k_zconst(const double* __restrict__ C_slot, int s0, int s1, ZConstArgs zc) {
   pdl_wait();
   int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= s1) return;
-  int lab = slot_label[s];
-  float d = 0.0f;
-  if (lab >= 0) {
-    double C = C_slot[s];
-    double D = kappa + C;
-    C_lab[lab] = C;
-    D_lab[lab] = D;
-    if (!isfinite(D)) atomicAdd(bad, 1);
-    d = D > 0.0 ? (float)fmin(1.0 / D, 3.0e38) : 0.0f;
-  }
-  d_slot[s] = d;
+  zconst_one(zc, s, C_slot[s]);
 }
 
 cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
                           float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s) {
   if (s1 <= s0) return cudaSuccess;
-  pdl_launch(k_zconst, (s1 - s0 + 255) / 256, 256, 0, s, C_slot, slot_label, s0, s1, kappa, d_slot, C_lab, D_lab, bad);
+  ZConstArgs zc{slot_label, kappa, d_slot, C_lab, D_lab, bad};
+  pdl_launch(k_zconst, (s1 - s0 + 255) / 256, 256, 0, s, C_slot, s0, s1, zc);
   return cudaGetLastError();
 }
 

@@ -1099,10 +1099,14 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (ntiles > 0) KL(launch_gpass(1, ga, c->st));
     timing_record(c, 4);
     KL(launch_block_sums(c->A[4], n, c->blk_wp, c->st));
+    const bool c_final = c->world == 1 || c->dcp;  // else the constants follow the C1 all-reduce
+    const ZConstArgs zc{c->slot_label, c->kappa, c->s[4], c->C, c->D, c->bad};
     KL(launch_gate_reduce(1, c->gmstart, c->gmlist, M, c->gpart1, nullptr, nullptr, c->C_slot, c->slots_pad, c->st,
-                          c->blk_wp, (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad));
-    if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
-    KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+                          c->blk_wp, (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad, c_final ? &zc : nullptr));
+    if (!c_final) {
+      COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
+      KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+    }
     if (c->select) {
       KL(launch_select(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->st));
       ga.sel = c->sel_flag;
@@ -1133,16 +1137,22 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     timing_record(c, 4);
     // local W_pred rides with C in the C1 all-reduce (element slots_pad)
     KL(launch_block_sums(c->A[4], n, c->blk_wp, c->st));
+    // one rank (or a DCP group): C is final after the reduction, which then also writes
+    // the per-slot constants; otherwise they follow the C1 all-reduce
+    const bool c_final = c->world == 1 || c->dcp;
+    const ZConstArgs zc{c->slot_label, c->kappa, c->s[4], c->C, c->D, c->bad};
     KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, 0, c->slots_pad, c->C_slot, c->st, c->blk_wp,
-                       (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad));
-    if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
-    KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+                       (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad, c_final ? &zc : nullptr));
+    if (!c_final) {
+      COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
+      KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+    }
     if (c->select) {
       // index set I from dW = C/D and the mass identity; pass-2 slot layout with I first
-      KL(launch_select(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->st));
       SlotConsts sc2{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
-      KL(launch_slots2(c->zlab, c->sel_flag, M, c->model, c->zl, c->slots_pad, c->slot_label, c->s_lim,
-                       (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc2, c->D, c->st));
+      KL(launch_select_slots(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->zlab,
+                             c->model, c->zl, c->slots_pad, c->slot_label, c->s_lim, (float)c->p.sensor_xy[0],
+                             (float)c->p.sensor_xy[1], sc2, c->st));
       pa.js = c->s_lim;
     }
     timing_record(c, 5);

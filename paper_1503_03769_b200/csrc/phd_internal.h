@@ -166,10 +166,35 @@ int pass_occupancy(int model, int pass, int wz, int zl);
 cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,
                          int zbg, int wz, cudaStream_t s);
 int fused_occupancy(int model, int wz);
+// per-slot constants after C: D = kappa + C, C_lab / D_lab by label, d = 1/D (fp32), non-finite count
+struct ZConstArgs {
+  const int32_t* slot_label;
+  double kappa;
+  float* d_slot;
+  double* C_lab;
+  double* D_lab;
+  int* bad;
+};
+// one slot: D = kappa + C, C_lab / D_lab, d = 1/D (0 for padding or D <= 0), NaN count
+__device__ __forceinline__ void zconst_one(const ZConstArgs& zc, int s, double C) {
+  const int lab = zc.slot_label[s];
+  float d = 0.0f;
+  if (lab >= 0) {
+    const double D = zc.kappa + C;
+    zc.C_lab[lab] = C;
+    zc.D_lab[lab] = D;
+    if (!isfinite(D)) atomicAdd(zc.bad, 1);
+    d = D > 0.0 ? (float)fmin(1.0 / D, 3.0e38) : 0.0f;
+  }
+  zc.d_slot[s] = d;
+}
+
 // (wblk != nullptr: one extra block also writes *wout = sum of wblk[0..nwb), the
-// rank's W_pred from the block sums of launch_block_sums, which then rides in C1)
+// rank's W_pred from the block sums of launch_block_sums, which then rides in C1;
+// zc != nullptr, one rank only: the per-slot constants of launch_zconst as well)
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
-                            cudaStream_t s, const double* wblk = nullptr, int nwb = 0, double* wout = nullptr);
+                            cudaStream_t s, const double* wblk = nullptr, int nwb = 0, double* wout = nullptr,
+                            const ZConstArgs* zc = nullptr);
 cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
                           float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s);
 // inv != nullptr (gated update): P is one plane in sorted order, read as P[inv[i]]
@@ -215,10 +240,11 @@ cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream_t s);  // blk only
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                           int32_t* sel_flag, double* info, cudaStream_t s);
-// also writes the per-slot constants of the new layout (as k_zprep) and d = 1/D
-cudaError_t launch_slots2(const float* z, const int32_t* sel_flag, int M, int model, int zl, int slots_pad,
-                          int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
-                          const double* D_lab, cudaStream_t s);
+// k_select + the pass-2 slot layout with its per-slot constants (as k_zprep) and 1/D
+cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
+                                int32_t* sel_flag, double* info, const float* z, int model, int zl, int slots_pad,
+                                int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
+                                cudaStream_t s);
 
 // ---- gated update (k_gate.cu, DESIGN.md §5 "Gated update") ------------------
 // Particles are ordered by a Morton cell key in measurement space (stable
@@ -336,6 +362,7 @@ cudaError_t launch_gpass(int pass, const GateArgs& g, cudaStream_t s);
 // pass 1 with wblk != nullptr: one extra block writes *wout = sum of wblk[0..nwb) (see launch_reduce_C)
 cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* mlist, int M, const double* part1,
                                const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s,
-                               const double* wblk = nullptr, int nwb = 0, double* wout = nullptr);
+                               const double* wblk = nullptr, int nwb = 0, double* wout = nullptr,
+                               const ZConstArgs* zc = nullptr);
 
 }  // namespace phd
