@@ -132,7 +132,7 @@ cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaS
 __global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
   pdl_wait();
   __shared__ double wsum[8];
-  __shared__ int64_t his[kBlockW];
+  __shared__ int his[kBlockW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = blockIdx.x;
   const int64_t base = b * kBlockW;
@@ -175,44 +175,45 @@ __global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
   // the bounds non-decreasing so the ranges [his[k-1], his[k]) tile the block's
   // offspring exactly (rounding of the fp64 partial sums cannot create gaps or
   // overlaps).
-  __shared__ long long wmax[8];
+  // offspring bounds as 32-bit offsets from n(E_b) (a rank produces < 2^31 offspring)
+  __shared__ int wmax[8];
   double L = excl;
-  long long run = nEb;
-  long long h[4];
+  int run = 0;
+  int h[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
     int k = 4 * tid + m;
     int64_t i = base + k;
     L += w4[m];
-    long long hi;
+    int64_t hi;
     if (i >= a.n_local - 1 || k == kBlockW - 1) hi = nEb1;
     else hi = n_of(Eb + L, a.scale, a.U, nEb, nEb1);
-    run = run > hi ? run : hi;
+    run = max(run, (int)(hi - nEb));
     h[m] = run;
   }
-  long long incl_m = run;
+  int incl_m = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    long long v = __shfl_up_sync(0xffffffffu, incl_m, o);
-    if (lane >= o) incl_m = incl_m > v ? incl_m : v;
+    const int v = __shfl_up_sync(0xffffffffu, incl_m, o);
+    if (lane >= o) incl_m = max(incl_m, v);
   }
   if (lane == 31) wmax[warp] = incl_m;
   __syncthreads();
-  long long carry = nEb;
-  for (int k = 0; k < warp; ++k) carry = carry > wmax[k] ? carry : wmax[k];
-  long long prev = __shfl_up_sync(0xffffffffu, incl_m, 1);
-  if (lane > 0) carry = carry > prev ? carry : prev;
+  int carry = 0;
+  for (int k = 0; k < warp; ++k) carry = max(carry, wmax[k]);
+  const int prev = __shfl_up_sync(0xffffffffu, incl_m, 1);
+  if (lane > 0) carry = max(carry, prev);
 #pragma unroll
-  for (int m = 0; m < 4; ++m) his[4 * tid + m] = h[m] > carry ? h[m] : carry;
+  for (int m = 0; m < 4; ++m) his[4 * tid + m] = max(h[m], carry);
   __syncthreads();
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
     int k = 4 * tid + m;
     int64_t i = base + k;
     if (i >= a.n_local) break;
-    int64_t lo = k == 0 ? nEb : his[k - 1];
-    int64_t hi = his[k];
-    if (hi > lo) a.marks[lo - a.lo] = (int32_t)(a.g0 + i);
+    const int lo = k == 0 ? 0 : his[k - 1];
+    const int hi = his[k];
+    if (hi > lo) a.marks[nEb + lo - a.lo] = (int32_t)(a.g0 + i);
   }
 }
 
