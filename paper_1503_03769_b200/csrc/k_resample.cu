@@ -129,31 +129,36 @@ cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaS
 
 // Per block of kBlockW particles: local fp64 inclusive prefix, offspring ranges,
 // and a mark at the first offspring of every particle with a non-empty range.
-__global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
+// kMP particles per thread (the per-thread scans and bounds are amortised over them).
+constexpr int kMP = 8, kMT = kBlockW / kMP;
+__global__ void __launch_bounds__(kMT) k_resample_mark(const ResampleArgs a) {
   pdl_wait();
-  __shared__ double wsum[8];
-  __shared__ int his[kBlockW];
+  __shared__ double wsum[kMT / 32];
+  __shared__ int his[kMT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = blockIdx.x;
   const int64_t base = b * kBlockW;
   const int64_t nb = (a.n_local + kBlockW - 1) / kBlockW;
-  double w4[4];
+  double w4[kMP];
   double tsum = 0.0;
-  if (base + 4 * tid + 3 < a.n_local) {  // 16-byte load (base is a multiple of kBlockW)
-    const float4 q = *reinterpret_cast<const float4*>(a.w + base + 4 * tid);
-    w4[0] = (double)q.x;
-    w4[1] = (double)q.y;
-    w4[2] = (double)q.z;
-    w4[3] = (double)q.w;
+  if (base + kMP * tid + kMP - 1 < a.n_local) {  // 16-byte loads (base is a multiple of kBlockW)
+#pragma unroll
+    for (int v = 0; v < kMP / 4; ++v) {
+      const float4 q = *reinterpret_cast<const float4*>(a.w + base + kMP * tid + 4 * v);
+      w4[4 * v + 0] = (double)q.x;
+      w4[4 * v + 1] = (double)q.y;
+      w4[4 * v + 2] = (double)q.z;
+      w4[4 * v + 3] = (double)q.w;
+    }
   } else {
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      int64_t i = base + 4 * tid + m;
+    for (int m = 0; m < kMP; ++m) {
+      int64_t i = base + kMP * tid + m;
       w4[m] = i < a.n_local ? (double)a.w[i] : 0.0;
     }
   }
 #pragma unroll
-  for (int m = 0; m < 4; ++m) tsum += w4[m];
+  for (int m = 0; m < kMP; ++m) tsum += w4[m];
   // block exclusive scan of thread sums: warp shuffle + smem over warps
   double incl = tsum;
 #pragma unroll
@@ -176,13 +181,13 @@ __global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
   // offspring exactly (rounding of the fp64 partial sums cannot create gaps or
   // overlaps).
   // offspring bounds as 32-bit offsets from n(E_b) (a rank produces < 2^31 offspring)
-  __shared__ int wmax[8];
+  __shared__ int wmax[kMT / 32];
   double L = excl;
   int run = 0;
-  int h[4];
+  int h[kMP];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    int k = 4 * tid + m;
+  for (int m = 0; m < kMP; ++m) {
+    int k = kMP * tid + m;
     int64_t i = base + k;
     L += w4[m];
     int64_t hi;
@@ -204,23 +209,23 @@ __global__ void __launch_bounds__(256) k_resample_mark(const ResampleArgs a) {
   const int prev = __shfl_up_sync(0xffffffffu, incl_m, 1);
   if (lane > 0) carry = max(carry, prev);
 #pragma unroll
-  for (int m = 0; m < 4; ++m) his[4 * tid + m] = max(h[m], carry);
+  for (int m = 0; m < kMP; ++m) h[m] = max(h[m], carry);
+  his[tid] = h[kMP - 1];  // each thread's last bound: the next thread's first lower bound
   __syncthreads();
+  int lo = tid == 0 ? 0 : his[tid - 1];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    int k = 4 * tid + m;
-    int64_t i = base + k;
+  for (int m = 0; m < kMP; ++m) {
+    const int64_t i = base + kMP * tid + m;
     if (i >= a.n_local) break;
-    const int lo = k == 0 ? 0 : his[k - 1];
-    const int hi = his[k];
-    if (hi > lo) a.marks[nEb + lo - a.lo] = (int32_t)(a.g0 + i);
+    if (h[m] > lo) a.marks[nEb + lo - a.lo] = (int32_t)(a.g0 + i);
+    lo = h[m];
   }
 }
 
 cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s) {
   if (a.n_local <= 0) return cudaSuccess;
   unsigned nb = (unsigned)((a.n_local + kBlockW - 1) / kBlockW);
-  pdl_launch(k_resample_mark, nb, 256, 0, s, a);
+  pdl_launch(k_resample_mark, nb, kMT, 0, s, a);
   return cudaGetLastError();
 }
 
