@@ -213,11 +213,21 @@ __global__ void __launch_bounds__(kMT) k_resample_mark(const ResampleArgs a) {
   his[tid] = h[kMP - 1];  // each thread's last bound: the next thread's first lower bound
   __syncthreads();
   int lo = tid == 0 ? 0 : his[tid - 1];
+  const int end = (int)(nEb1 - nEb);
 #pragma unroll
   for (int m = 0; m < kMP; ++m) {
     const int64_t i = base + kMP * tid + m;
     if (i >= a.n_local) break;
-    if (h[m] > lo) a.marks[nEb + lo - a.lo] = (int32_t)(a.g0 + i);
+    if (h[m] > lo) {
+      const int64_t p = nEb + lo - a.lo;  // first offspring, local produced index
+      a.marks[p] = (int32_t)(a.g0 + i);
+      // the ranges tile the offspring, so the block's next mark (if any) sits at h[m]:
+      // this mark is the block's last in its offspring block iff that position is
+      // past the block's range or in another offspring block -> max per offspring
+      // block (integer atomicMax: order-independent, k_scan_max then scans it)
+      if (h[m] == end || (p + (h[m] - lo)) / kBlockOff != p / kBlockOff)
+        atomicMax(&a.bmax[p / kBlockOff], (int32_t)(a.g0 + i));
+    }
     lo = h[m];
   }
 }
@@ -236,34 +246,6 @@ __device__ __forceinline__ int warp_max_scan(int v, int lane) {
     if (lane >= o) v = max(v, u);
   }
   return v;
-}
-
-__global__ void __launch_bounds__(256) k_block_max(const int32_t* __restrict__ marks, int64_t n, int32_t* bmax) {
-  pdl_wait();
-  __shared__ int wm[8];
-  const int tid = threadIdx.x;
-  const int64_t base = (int64_t)blockIdx.x * kBlockOff;
-  int m = -1;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    int64_t j = base + 4 * tid + r;
-    if (j < n) m = max(m, marks[j]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((tid & 31) == 0) wm[tid >> 5] = m;
-  __syncthreads();
-  if (tid == 0) {
-    int r = -1;
-    for (int k = 0; k < 8; ++k) r = max(r, wm[k]);
-    bmax[blockIdx.x] = r;
-  }
-}
-
-cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  pdl_launch(k_block_max, (unsigned)((n + kBlockOff - 1) / kBlockOff), 256, 0, s, marks, n, bmax);
-  return cudaGetLastError();
 }
 
 // In place: bmax[b] <- max(bmax[0..b-1]) (exclusive; -1 for b = 0).

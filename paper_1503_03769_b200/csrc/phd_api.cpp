@@ -7,7 +7,7 @@
 //             -> k_pass<2> -> k_finalize -> k_reduce_acc -> [C2 all-reduce]
 //             -> one 8*(2W+2) byte D2H (the step's only host sync)
 //   extract   k_extract on rank 0 (the central unit) + D2H of the estimates
-//   resample  k_scan_blocks -> k_resample_mark -> k_block_max -> k_scan_max -> k_gather
+//   resample  k_scan_blocks -> k_resample_mark (+ per-offspring-block max) -> k_scan_max -> k_gather
 //   exchange  world 1: buffer swap; world > 1: grouped ncclSend/ncclRecv (C3)
 #include <algorithm>
 #include <climits>
@@ -1478,6 +1478,7 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   const int nbo = (int)ceil_div(nprod, kBlockOff);
   if (!c->zero_mass && nprod > 0) {
     CU(cudaMemsetAsync(c->marks, 0xFF, sizeof(int32_t) * nprod, c->st));
+    CU(cudaMemsetAsync(c->bmax, 0xFF, sizeof(int32_t) * nbo, c->st));
     KL(launch_scan_blocks(c->blk_w, nbw, c->blk_off, c->st));
     ResampleArgs ra{};
     ra.n_local = n;
@@ -1490,8 +1491,8 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     ra.lo = lo;
     ra.hi = hi;
     ra.marks = c->marks;
+    ra.bmax = c->bmax;
     KL(launch_resample_mark(ra, c->st));
-    KL(launch_block_max(c->marks, nprod, c->bmax, c->st));
     KL(launch_scan_max(c->bmax, nbo, c->st));
   }
   if (!c->dcp && c->world > 1 && c->p2p_state == 0) {

@@ -136,6 +136,7 @@ struct ResampleArgs {
   double U;
   int64_t lo, hi;            // bounds[r], bounds[r+1]
   int32_t* marks;            // [hi - lo]
+  int32_t* bmax;             // [ceil((hi - lo) / kBlockOff)], preset to -1: max mark per offspring block
 };
 
 // Eq 6 importance weights of the births (birth_model 2): local slots [i0, i0 + nb)
@@ -218,7 +219,6 @@ cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, i
                                cudaStream_t s);
 cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s);
 cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s);
-cudaError_t launch_block_max(const int32_t* marks, int64_t n, int32_t* bmax, cudaStream_t s);
 cudaError_t launch_scan_max(int32_t* bmax, int nb, cudaStream_t s);
 cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_t n, int64_t g0,
                           const float* x, const float* vx, const float* y, const float* vy, float w_off,
