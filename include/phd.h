@@ -234,7 +234,11 @@ phd_status phd_extract(phd_ctx* ctx, phd_estimate* out, int32_t cap, int32_t* n_
  * (adaptive: max(LT,1) R clamped to capacity - J; fixed: fixed_count), then
  * the exchange that leaves every rank its block of the next step's array. */
 phd_status phd_resample_exchange(phd_ctx* ctx, int32_t k);
-/* predict(k, NULL) + update(z, M) + extract + resample_exchange(k). */
+/* predict(k, NULL) + update(z, M) + extract + resample_exchange(k), with one host
+ * synchronisation (the update's end-of-stage bookkeeping -- rank masses, LT, the
+ * non-finite guard -- completes with the extraction's read-back; a PHD_EMODEL of
+ * the update is then reported by phd_step after the extraction kernel ran).
+ * Results equal those of the four calls. */
 phd_status phd_step(phd_ctx* ctx, int32_t k, const float* z, int32_t M, phd_estimate* out,
                     int32_t cap, int32_t* n_out, phd_summary* s);
 
