@@ -88,6 +88,33 @@ __device__ __forceinline__ unsigned match_digit_rt(int d, bool ok, int nbits) {
   return m;
 }
 
+// The same peer mask as match_digit, faster for rows of one digit (cell keys of
+// particles in ancestor order are clustered): the first lane's digit is peeled
+// off by a broadcast and one ballot, the remaining lanes (rows with more distinct
+// digits) go through the per-bit ballots.  Warp-uniform control flow.
+template <int NBITS>
+__device__ __forceinline__ unsigned match_digit_peel(int d, bool ok) {
+  constexpr int kPeel = 1;  // measured: 1 / 2 / 3 peels 0.295 / 0.301 / 0.311 ms at cfg 5 (0.322 none)
+  const int lane = threadIdx.x & 31;
+  unsigned rem = __ballot_sync(0xffffffffu, ok);
+  unsigned peers = 0u;
+#pragma unroll
+  for (int it = 0; it < kPeel; ++it) {
+    if (rem == 0u) break;  // uniform
+    const int dl = __shfl_sync(0xffffffffu, d, __ffs(rem) - 1);
+    const bool mine = ((rem >> lane) & 1u) && d == dl;
+    const unsigned m = __ballot_sync(0xffffffffu, mine);
+    if (mine) peers = m;
+    rem &= ~m;
+  }
+  if (rem != 0u) {  // uniform
+    const bool in = (rem >> lane) & 1u;
+    const unsigned m = match_digit<NBITS>(d, in);
+    if (in) peers = m;
+  }
+  return peers;
+}
+
 // float <-> int with the same order (for integer atomicMax on floats)
 __device__ __forceinline__ int f2ord(float f) {
   const int b = __float_as_int(f);
@@ -441,7 +468,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
       const int64_t i = b0 + r * 32 + lane;
       const bool ok = i < w1;
       const int d = ok ? kr[r] : 0;
-      const unsigned peers = match_digit<12>(d, ok);
+      const unsigned peers = match_digit_peel<12>(d, ok);
       int pos = 0;
       if (ok) pos = base[d] + (int)((my[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) + __popc(peers & lt);
       __syncwarp();
