@@ -3,12 +3,15 @@
 //
 // Per step:
 //   predict   k_predict                                     (HBM)
-//   update    k_zprep -> k_pass<1> -> k_reduce_C -> [C1 all-reduce] -> k_zconst
+//   update    k_zprep -> k_pass<1> -> k_block_sum -> k_reduce_C (+ W_pred; one rank: + the
+//             per-slot constants) -> [C1 all-reduce -> k_zconst] -> k_select_slots
 //             -> k_pass<2> -> k_finalize -> k_reduce_acc -> [C2 all-reduce]
-//             -> one 8*(2W+2) byte D2H (the step's only host sync)
-//   extract   k_extract on rank 0 (the central unit) + D2H of the estimates
+//             -> D2H of the rank masses and flags (gated: k_gate.cu kernels instead)
+//   extract   k_extract on rank 0 (the central unit) + D2H of the estimates; inside
+//             phd_step one host synchronisation covers the update's D2H and this one
 //   resample  k_scan_blocks -> k_resample_mark (+ per-offspring-block max) -> k_scan_max -> k_gather
-//   exchange  world 1: buffer swap; world > 1: grouped ncclSend/ncclRecv (C3)
+//   exchange  world 1: buffer swap; world > 1: k_gather_p2p into the owners' arrays over the
+//             peer-memory window + one barrier, or grouped ncclSend/ncclRecv (C3)
 #include <algorithm>
 #include <climits>
 #include <cmath>
