@@ -462,6 +462,11 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
       q[r][N4 - 2] = make_float4(__ldg(src.x + i), __ldg(src.y + i), __ldg(src.vx + i), __ldg(src.vy + i));
       q[r][N4 - 1] = make_float4(log2f(__ldg(src.w + i) * wscale), 0.0f, 0.0f, 0.0f);  // the dense TileLoader's expression
       lwm = fmaxf(lwm, q[r][N4 - 1].x);  // clamped duplicates of the last item do not change the max
+      // a NaN particle makes every dense term NaN (C, D non-finite -> PHD_EMODEL); the
+      // gated path might not evaluate it, so it is counted here (last-item clamps excluded)
+      const float4 st = q[r][N4 - 2];
+      if (b0 + r * 32 + lane < w1 && (st.x != st.x || st.y != st.y || q[r][N4 - 1].x != q[r][N4 - 1].x))
+        atomicAdd(so.bad, 1);
     }
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
@@ -536,8 +541,10 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
   for (int j = lane; j < (fast ? 0 : kGateTP); j += 32) {
     const int64_t o = (p0 + j) * rv.stride;
     const float l = __ldg(rv.lw + o);
-    if (l > -INFINITY) {  // zero-weight particles and padding contribute nothing
-      const float v0 = __ldg(rv.c0 + o), v1 = __ldg(rv.c1 + o);
+    const float v0 = __ldg(rv.c0 + o), v1 = __ldg(rv.c1 + o);
+    // zero-weight particles, padding and non-finite coordinates (whose dense terms
+    // are 0, or NaN and flagged by the sort) do not widen the box
+    if (l > -INFINITY && isfinite(v0) && isfinite(v1)) {
       b0 = fminf(b0, v0);
       b1 = fmaxf(b1, v0);
       e0 = fminf(e0, v1);
@@ -989,10 +996,13 @@ __global__ void __launch_bounds__(256) k_gate_reduce(const int32_t* __restrict__
                                                      int M, const double* __restrict__ part1,
                                                      const float4* __restrict__ part2, const int32_t* __restrict__ sel,
                                                      double* out, int slots_pad, const double* __restrict__ wblk,
-                                                     int nwb, double* wout, ZConstArgs zc) {
+                                                     int nwb, double* wout, ZConstArgs zc, const int* poison) {
   pdl_wait();
   if (PASS == 1 && wblk != nullptr && blockIdx.x == gridDim.x - 1) {  // the rank's W_pred (rides in C1)
     block_sum_f64(wblk, nwb, wout);
+    // NaN particles (counted by the sort): poison W_pred so that every rank sees a
+    // non-finite W_pred after C1 and reports PHD_EMODEL, as the dense path's NaN C does
+    if (threadIdx.x == 0 && poison != nullptr && *poison != 0) *wout = __longlong_as_double(0x7ff8000000000000ll);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -1200,17 +1210,17 @@ cudaError_t launch_gpass(int pass, const GateArgs& g, cudaStream_t s) {
 
 cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* mlist, int M, const double* part1,
                                const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s,
-                               const double* wblk, int nwb, double* wout, const ZConstArgs* zc) {
+                               const double* wblk, int nwb, double* wout, const ZConstArgs* zc, const int* poison) {
   if (pass != 1) wblk = nullptr;
   const ZConstArgs z = zc && pass == 1 ? *zc : ZConstArgs{};
   const unsigned blocks = (unsigned)((std::max(slots_pad, 0) + 7) / 8 + (wblk ? 1 : 0));
   if (blocks == 0) return cudaSuccess;
   if (pass == 1)
     pdl_launch(k_gate_reduce<1>, blocks, 256, 0, s, mstart, mlist, M, part1, nullptr, nullptr, out, slots_pad, wblk,
-               nwb, wout, z);
+               nwb, wout, z, poison);
   else
     pdl_launch(k_gate_reduce<2>, blocks, 256, 0, s, mstart, mlist, M, nullptr, reinterpret_cast<const float4*>(part2), sel,
-                                            out, slots_pad, nullptr, 0, nullptr, z);
+                                            out, slots_pad, nullptr, 0, nullptr, z, nullptr);
   return cudaGetLastError();
 }
 

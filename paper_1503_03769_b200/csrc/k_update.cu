@@ -663,18 +663,21 @@ cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, 
 // For slots [s0, s1) of one group, with C_slot global (after the C1 all-reduce):
 // D = kappa + C, per-slot d = 1/D as fp32 (0 when D == 0 or padding), and the
 // label-order copies C_lab, D_lab used by the STPHD reduction and the getters.
-__global__ void k_zconst(const double* __restrict__ C_slot, int s0, int s1, ZConstArgs zc) {
+__global__ void k_zconst(const double* __restrict__ C_slot, int s0, int s1, ZConstArgs zc,
+                         const double* __restrict__ wpred) {
   pdl_wait();
+  if (wpred != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && !isfinite(*wpred)) atomicAdd(zc.bad, 1);
   int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= s1) return;
   zconst_one(zc, s, C_slot[s]);
 }
 
 cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
-                          float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s) {
+                          float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s,
+                          const double* wpred) {
   if (s1 <= s0) return cudaSuccess;
   ZConstArgs zc{slot_label, kappa, d_slot, C_lab, D_lab, bad};
-  pdl_launch(k_zconst, (s1 - s0 + 255) / 256, 256, 0, s, C_slot, s0, s1, zc);
+  pdl_launch(k_zconst, (s1 - s0 + 255) / 256, 256, 0, s, C_slot, s0, s1, zc, wpred);
   return cudaGetLastError();
 }
 

@@ -944,6 +944,7 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   const int ntiles = (int)(npad / kGateTP);
   const float* A[5] = {c->A[0], c->A[1], c->A[2], c->A[3], c->A[4]};
   c->gso.n = n;
+  c->gso.bad = c->bad;
   CU(gate_sort_particles(c->model, A, c->rb, c->L.cap_l, n, npad, c->wscale, c->ggrid, c->ghist, c->gscan,
                          c->gkeys, c->gso, c->st, &c->launches));
   CU(gate_zbin(c->zlab, M, c->ggrid, c->ghist, c->gscan, c->gzstart, c->gzitems, c->gzz, c->st, &c->launches));
@@ -1007,6 +1008,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   c->M_z = M;
   const int64_t n = c->n_local;
   bool gated = false;
+  // non-finite counters (k_zconst: C/D; the gated sort: NaN particles), before any of them runs
+  CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
   // gate = 1 skips the gated path for small updates (< 2^29 pairs, where the cell
   // sort and candidate lists cost more than the dense passes: measured at cfg 3,
   // 6.8e7 pairs, 0.28 ms dense vs 0.50 ms gated).  N is global in exact mode, so
@@ -1064,7 +1067,6 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   pa.Apart = c->Apart;
   pa.P = c->P;
   pa.P_stride = c->L.cap_l;
-  CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
   c->select = M > 0 && !c->fused && c->p.stphd_all == 0;
   pa.js = nullptr;
   // C of slots [s0, s1): fixed-order reduction, C1 all-reduce, per-slot constants
@@ -1105,10 +1107,12 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     const bool c_final = c->world == 1 || c->dcp;  // else the constants follow the C1 all-reduce
     const ZConstArgs zc{c->slot_label, c->kappa, c->s[4], c->C, c->D, c->bad};
     KL(launch_gate_reduce(1, c->gmstart, c->gmlist, M, c->gpart1, nullptr, nullptr, c->C_slot, c->slots_pad, c->st,
-                          c->blk_wp, (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad, c_final ? &zc : nullptr));
+                          c->blk_wp, (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad, c_final ? &zc : nullptr,
+                          c->bad));
     if (!c_final) {
       COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
-      KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+      KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st,
+                       c->C_slot + c->slots_pad));
     }
     if (c->select) {
       KL(launch_select(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->st));
@@ -1148,7 +1152,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
                        (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad, c_final ? &zc : nullptr));
     if (!c_final) {
       COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));
-      KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
+      KL(launch_zconst(c->C_slot, c->slot_label, 0, c->slots_pad, c->kappa, c->s[4], c->C, c->D, c->bad, c->st,
+                       c->C_slot + c->slots_pad));
     }
     if (c->select) {
       // index set I from dW = C/D and the mass identity; pass-2 slot layout with I first

@@ -196,8 +196,11 @@ __device__ __forceinline__ void zconst_one(const ZConstArgs& zc, int s, double C
 cudaError_t launch_reduce_C(const double* Cpart, int gp, int slots_pad, int s0, int s1, double* C_slot,
                             cudaStream_t s, const double* wblk = nullptr, int nwb = 0, double* wout = nullptr,
                             const ZConstArgs* zc = nullptr);
+// (wpred != nullptr: a non-finite all-reduced W_pred -- a rank's NaN particles, see the
+// gated sort -- is counted in bad too, so every rank reports PHD_EMODEL)
 cudaError_t launch_zconst(const double* C_slot, const int32_t* slot_label, int s0, int s1, double kappa,
-                          float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s);
+                          float* d_slot, double* C_lab, double* D_lab, int* bad, cudaStream_t s,
+                          const double* wpred = nullptr);
 // inv != nullptr (gated update): P is one plane in sorted order, read as P[inv[i]]
 cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, int zb, int64_t n, float nu,
                             float wscale, float* w_out, double* blk_w, double* blk_wp, cudaStream_t s,
@@ -315,6 +318,7 @@ struct GateSorted {
   int32_t* inv;                       // local index -> sorted position
   int* lw_max;                        // max lw over the particles (ordered-int encoding)
   int64_t n;                          // particles sorted (records [n, n_pad) are padding)
+  int* bad;                           // += NaN particles (x, y or w): the dense C would be NaN
 };
 
 struct GateArgs {
@@ -363,6 +367,6 @@ cudaError_t launch_gpass(int pass, const GateArgs& g, cudaStream_t s);
 cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* mlist, int M, const double* part1,
                                const float* part2, const int32_t* sel, double* out, int slots_pad, cudaStream_t s,
                                const double* wblk = nullptr, int nwb = 0, double* wout = nullptr,
-                               const ZConstArgs* zc = nullptr);
+                               const ZConstArgs* zc = nullptr, const int* poison = nullptr);
 
 }  // namespace phd

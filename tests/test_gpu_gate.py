@@ -331,3 +331,45 @@ def test_gated_range_bearing_offset_sensor(phd, orc):
     Co = orc.normalizers(m, soa, w, z)
     wo, acco = orc.update(m, soa, w, z, Co)
     _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
+
+
+@pytest.mark.parametrize("gate", [0, 2])
+@pytest.mark.parametrize("via_step", [False, True])
+def test_nan_particle_is_reported(phd, gate, via_step):
+    """A NaN particle makes every dense term NaN, so the update reports PHD_EMODEL
+    (include/phd.h); the gated path reports it too even when the particle's tile has
+    no candidates (the sort counts NaN particles), through phd_step's deferred check
+    as well as through phd_update."""
+    m = replace(POS, gate=gate)
+    z = _meas(m, 40, 31)
+    soa, w = _cloud(m, 20000, z, 31)
+    soa[0, 777] = np.nan
+    soa[2, 777] = 5000.0  # far from every measurement: its tile has no candidates
+    f = phd.Filter(m)
+    with pytest.raises(phd.PhdError) as e:
+        if via_step:
+            f.set_particles(soa, w, soa.shape[1])
+            f.step(1, z)
+        else:
+            f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+            f.update(z)
+    assert e.value.status == 4  # PHD_EMODEL
+    f.close()
+
+
+def test_inf_particle_gated_equals_dense(phd, orc):
+    """An infinite position contributes exactly 0 to every term in the dense path
+    (exponent -inf); in the gated path it must not widen its tile's box (which would
+    drop the candidates of the tile's other particles)."""
+    rng = np.random.default_rng(41)
+    z = rng.uniform(-300.0, 300.0, (300, 2)).astype(np.float32)
+    soa, w = _cloud(POS, 9000, z, 41)
+    soa[0, 100] = np.inf
+    soa[0, 4000] = -np.inf
+    out = {}
+    for gate in (0, 2):
+        out[gate] = _run(phd, replace(POS, gate=gate), soa, w, z)
+    assert out[2]["gate"]["used"] == 1 and out[0]["gate"]["used"] == 0
+    assert np.all(np.isfinite(out[2]["C"])) and np.all(np.isfinite(out[2]["wn"]))
+    assert np.allclose(out[2]["C"], out[0]["C"], rtol=2e-6, atol=0)
+    assert np.allclose(out[2]["wn"], out[0]["wn"], rtol=2e-6, atol=1e-30)

@@ -178,3 +178,42 @@ def test_rank_with_no_particles(phd, gate):
     for k in range(2):
         assert abs(ref["summ"][k]["W"] - got["summ"][k]["W"]) <= 1e-6 * max(1.0, ref["summ"][k]["W"])
         assert np.array_equal(ref["anc"][k], got["anc"][k])
+
+
+@pytest.mark.parametrize("gate", [0, 2])
+def test_nan_particle_reported_on_every_rank(phd, gate):
+    """A NaN particle held by one rank: every rank's step reports PHD_EMODEL (the dense
+    C is NaN after C1; the gated sort poisons the rank's W_pred, which C1 spreads)."""
+    cfg = _cfg()
+    m = replace(cfg.model, gate=gate)
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    soa, w = scenario.initial_population(cfg, truth)
+    n0, world = soa.shape[1], 2
+    soa[0, n0 - 10] = np.nan  # on the last rank
+    soa[2, n0 - 10] = 9000.0
+    group = phd.LocalGroup(world)
+    fs, status = [], [None] * world
+    for r in range(world):
+        f = phd.Filter(m, rank=r, world=world, group=group)
+        lo, hi = phd.rank_block(n0 + m.births_per_step, world, r)
+        a, b = min(lo, n0), min(hi, n0)
+        f.set_particles(np.ascontiguousarray(soa[:, a:b]), np.ascontiguousarray(w[a:b]), n0)
+        fs.append(f)
+
+    def drive(r):
+        try:
+            fs[r].step(1, Z[0])
+            status[r] = 0
+        except phd.PhdError as e:
+            status[r] = e.status
+
+    th = [threading.Thread(target=drive, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert status == [4] * world, status
+    for f in fs:
+        f.close()
+    group.close()
