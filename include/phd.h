@@ -60,7 +60,8 @@ typedef enum {
   PHD_EINVAL = 1,     /* invalid argument or parameter (message says which) */
   PHD_ESTATE = 2,     /* call out of order (predict -> update -> [extract] -> resample) */
   PHD_ECAPACITY = 3,  /* particle count exceeds capacity (fixed mode) */
-  PHD_EMODEL = 4,     /* non-finite C, D or W detected */
+  PHD_EMODEL = 4,     /* non-finite C, D or W detected (a NaN particle makes every C NaN; the gated
+                         update counts NaN particles itself, on every rank) */
   PHD_ENOMEM = 5,     /* device allocation failed / workspace too small */
   PHD_ECUDA = 6,      /* CUDA runtime error (message has the CUDA string) */
   PHD_ENCCL = 7,      /* NCCL error or NCCL unavailable for world > 1 */
