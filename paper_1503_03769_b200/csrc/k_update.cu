@@ -589,7 +589,7 @@ int fused_occupancy(int model, int wz) {
 // Measurement-slot preparation.  Slots hold labels (or -1 = padding); padding
 // slots get a sentinel that makes every likelihood term exactly 0.
 __global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* __restrict__ slot_label, int n,
-                        float sx, float sy, SlotConsts sc) {
+                        float sx, float sy, SlotConsts sc, int* bad) {
   pdl_wait();
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
@@ -598,6 +598,9 @@ __global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* _
   int rep = 0;
   if (lab >= 0) {
     float z0 = z[2 * lab], z1 = z[2 * lab + 1];
+    // a NaN measurement makes its dense C NaN (PHD_EMODEL); counted here because the
+    // gated update may give it no candidate at all
+    if (bad != nullptr && (z0 != z0 || z1 != z1)) atomicAdd(bad, 1);
     s0 = -z0;
     s1 = -z1;
     if (model == kRangeBearing) {
@@ -620,9 +623,10 @@ __global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* _
 }
 
 cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad, float sensor_x,
-                         float sensor_y, SlotConsts sc, cudaStream_t s) {
+                         float sensor_y, SlotConsts sc, cudaStream_t s, int* bad) {
   if (n_slots_pad <= 0) return cudaSuccess;
-  pdl_launch(k_zprep, (n_slots_pad + 255) / 256, 256, 0, s, model, z_lab, slot_label, n_slots_pad, sensor_x, sensor_y, sc);
+  pdl_launch(k_zprep, (n_slots_pad + 255) / 256, 256, 0, s, model, z_lab, slot_label, n_slots_pad, sensor_x, sensor_y, sc,
+             bad);
   return cudaGetLastError();
 }
 

@@ -1032,7 +1032,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (M > 0) {
     CU(cudaMemcpyAsync(c->slot_label, c->h_slot, sizeof(int32_t) * c->slots_pad, cudaMemcpyHostToDevice, c->st));
     SlotConsts sc{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
-    KL(launch_zprep(c->model, c->zlab, c->slot_label, c->slots_pad, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->st));
+    KL(launch_zprep(c->model, c->zlab, c->slot_label, c->slots_pad, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->st,
+                    c->bad));
   }
   // particle-CTA count: one wave of resident CTAs over the z-blocks of one sweep
   int gp = 0;

@@ -161,7 +161,7 @@ cudaError_t launch_birth_is(const BirthISArgs& a, cudaStream_t s);
 cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, float sy, float* rb,
                            int64_t stride, cudaStream_t s);
 cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad,
-                         float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s);
+                         float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s, int* bad = nullptr);
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
 int pass_occupancy(int model, int pass, int wz, int zl);
 cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,

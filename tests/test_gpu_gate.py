@@ -373,3 +373,19 @@ def test_inf_particle_gated_equals_dense(phd, orc):
     assert np.all(np.isfinite(out[2]["C"])) and np.all(np.isfinite(out[2]["wn"]))
     assert np.allclose(out[2]["C"], out[0]["C"], rtol=2e-6, atol=0)
     assert np.allclose(out[2]["wn"], out[0]["wn"], rtol=2e-6, atol=1e-30)
+
+
+@pytest.mark.parametrize("gate", [0, 2])
+def test_nan_measurement_is_reported(phd, gate):
+    """A NaN measurement makes its dense C NaN (PHD_EMODEL); the gated update reports it
+    even when no tile's window reaches the cell it is binned into."""
+    m = replace(POS, gate=gate)
+    z = _meas(m, 40, 37)
+    soa, w = _cloud(m, 20000, z, 37)
+    z[5] = (np.nan, 300.0)
+    f = phd.Filter(m)
+    f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+    with pytest.raises(phd.PhdError) as e:
+        f.update(z)
+    assert e.value.status == 4  # PHD_EMODEL
+    f.close()
