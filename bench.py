@@ -464,14 +464,14 @@ def run_ours(args):
                         "basis": "w read 4 B per particle; per offspring: mark 4+4, ancestor state 16 read, "
                                  "state + w 20 written, ancestor index 4 (all resampling kernels incl. scans)"}}
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the contract's CPU baseline: rank 0 at N = 1 only
         r = cpu_oracle_sample(cfg, Z, soa, w, args.cpu_sample, k=1)
         cpu = {"value": r["pairs"] / r["seconds"], "unit": "pairs/s", "cores": 1, "kind": "oracle",
                "sample": "one full serial fp64 step (predict, births, normalisers, update, extraction, resampling) "
                          "of the first %d particles (+%d proportional births) against all M=%d measurements of "
                          "Z_1; %.1f s" % (args.cpu_sample, r["n"] - args.cpu_sample, r["M"], r["seconds"])}
     cpu_all = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         cpu_all = cpu_oracle_all_cores(cfg, Z, soa, w, args.cpu_sample * 4)
     out = {
         "metric": "particle-measurement update pairs/sec and filter step ms",
