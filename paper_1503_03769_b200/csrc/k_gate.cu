@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   // 3. rank and write the records (and the max of lw, for the tile kernels' fast path)
   const unsigned lt = (1u << lane) - 1u;
   float lwm = -INFINITY;
+  bool nanp = false;  // clamped duplicates of the last item repeat a real item: no false flag
   for (int64_t b0 = w0; b0 < w1; b0 += 32 * ROWS) {
     float4 q[ROWS][N4];
     int kr[ROWS];
@@ -463,10 +464,9 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
       q[r][N4 - 1] = make_float4(log2f(__ldg(src.w + i) * wscale), 0.0f, 0.0f, 0.0f);  // the dense TileLoader's expression
       lwm = fmaxf(lwm, q[r][N4 - 1].x);  // clamped duplicates of the last item do not change the max
       // a NaN particle makes every dense term NaN (C, D non-finite -> PHD_EMODEL); the
-      // gated path might not evaluate it, so it is counted here (last-item clamps excluded)
+      // gated path might not evaluate it, so it is flagged here (one atomic per warp at the end)
       const float4 st = q[r][N4 - 2];
-      if (b0 + r * 32 + lane < w1 && (st.x != st.x || st.y != st.y || q[r][N4 - 1].x != q[r][N4 - 1].x))
-        atomicAdd(so.bad, 1);
+      nanp |= isnan(st.x) | isnan(st.y) | isnan(q[r][N4 - 1].x);
     }
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) lwm = fmaxf(lwm, __shfl_xor_sync(0xffffffffu, lwm, o));
   if (lane == 0 && w0 < w1) atomicMax(so.lw_max, f2ord(lwm));
+  if (__any_sync(0xffffffffu, nanp) && lane == 0) atomicAdd(so.bad, 1);
 }
 
 // ---------------------------------------------------------------------------
