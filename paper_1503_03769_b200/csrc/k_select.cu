@@ -130,6 +130,7 @@ cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const
 // js = ceil(#selected / (2 * lanes)) -- then the remaining slots, so that every
 // warp carries the same share of state-sum work.  *js_out = js.
 __device__ __forceinline__ int seq_slot(int p, int n_s, int lanes, int zl, int js) {
+  if (js < 0) return p;  // whole-z-block layout: the sequence in slot order
   if (p < n_s) {
     int l = p / (2 * js);
     return l * zl + p % (2 * js);
@@ -140,8 +141,9 @@ __device__ __forceinline__ int seq_slot(int p, int n_s, int lanes, int zl, int j
 }
 
 __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const int32_t* sel_flag, int M, int model,
-                                            int zl, int slots_pad, int32_t* slot_label, int32_t* js_out, float sx,
-                                            float sy, const SlotConsts& sc, const double* __restrict__ D_lab) {
+                                            int zl, int wz, int layout, int slots_pad, int32_t* slot_label,
+                                            int32_t* js_out, float sx, float sy, const SlotConsts& sc,
+                                            const double* __restrict__ D_lab) {
   __shared__ int wsum[32];
   __shared__ int base_s;
   __shared__ int cat_start[7];
@@ -161,7 +163,18 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
       js = max(js, 0);
       js = min(js, zl / 2);
       n_s = 2 * js * lanes;
-      if (tid == 0) *js_out = js;
+      // whole z-blocks instead (every slot of the first zb_sum z-blocks carries sums, the
+      // rest none; CTA-uniform) when that needs fewer state-sum slots than js pairs on
+      // every lane: *js_out = kJsZBlock | zb_sum
+      const int spz = wz * 32 * zl;
+      const int zb_sum = (n_sel + spz - 1) / spz;
+      if (layout == 2 || (layout == 0 && zb_sum * spz < n_s)) {
+        js = -1;
+        n_s = zb_sum * spz;
+        if (tid == 0) *js_out = kJsZBlock | zb_sum;
+      } else if (tid == 0) {
+        *js_out = js;
+      }
       if (tid == 0) base_s = 0;
       __syncthreads();
     }
@@ -263,19 +276,19 @@ __global__ void __launch_bounds__(kTopkThreads) k_select_slots(const double* __r
                                                                const double* __restrict__ W_pred, double p_d,
                                                                int32_t* sel_flag, double* info,
                                                                const float* __restrict__ z, int model, int zl,
-                                                               int slots_pad, int32_t* slot_label, int32_t* js_out,
-                                                               float sx, float sy, SlotConsts sc) {
+                                                               int wz, int layout, int slots_pad, int32_t* slot_label,
+                                                               int32_t* js_out, float sx, float sy, SlotConsts sc) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char sm[];
   select_body(C_lab, D_lab, M, W_pred, p_d, sel_flag, info, reinterpret_cast<unsigned long long*>(sm));
   __syncthreads();  // sel_flag (global) complete and visible to the CTA
-  slots2_body(z, sel_flag, M, model, zl, slots_pad, slot_label, js_out, sx, sy, sc, D_lab);
+  slots2_body(z, sel_flag, M, model, zl, wz, layout, slots_pad, slot_label, js_out, sx, sy, sc, D_lab);
 }
 
 cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
-                                int32_t* sel_flag, double* info, const float* z, int model, int zl, int slots_pad,
-                                int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
-                                cudaStream_t s) {
+                                int32_t* sel_flag, double* info, const float* z, int model, int zl, int wz,
+                                int layout, int slots_pad, int32_t* slot_label, int32_t* js, float sensor_x,
+                                float sensor_y, SlotConsts sc, cudaStream_t s) {
   size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long);
   static bool attr = false;
   if (!attr) {
@@ -283,7 +296,7 @@ cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M,
     attr = true;
   }
   pdl_launch(k_select_slots, 1, kTopkThreads, smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info, z, model, zl,
-             slots_pad, slot_label, js, sensor_x, sensor_y, sc);
+             wz, layout, slots_pad, slot_label, js, sensor_x, sensor_y, sc);
   return cudaGetLastError();
 }
 

@@ -202,7 +202,12 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
   const int zb = blockIdx.y;
   const int slot0 = (zb * wz + warp) * (32 * ZL) + lane * ZL;
   // pass 2: state sums for the first js slot pairs of every lane (the index set I sits there)
-  const int js = PASS == 2 ? (a.js == nullptr ? NP : min(*a.js, NP)) : 0;
+  int js = 0;
+  if (PASS == 2) {
+    const int v = a.js == nullptr ? NP : *a.js;
+    // kJsZBlock | b: all slot pairs of the first b z-blocks (CTA-uniform), none elsewhere
+    js = (v & kJsZBlock) ? (zb < (v & (kJsZBlock - 1)) ? NP : 0) : min(v, NP);
+  }
   LaneZ<MODEL, PASS, NP> z;
   z.load(a, slot0);
   const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);

@@ -989,6 +989,13 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
 }
 
 static phd_status update_finish(phd_ctx* c);
+// pass-2 state-sum layout: 0 automatic, 1 per-lane slot pairs, 2 whole z-blocks (PHD_SUM_LAYOUT, tests)
+static int sum_layout() {
+  const char* e = getenv("PHD_SUM_LAYOUT");
+  if (e && strcmp(e, "lane") == 0) return 1;
+  if (e && strcmp(e, "zblock") == 0) return 2;
+  return 0;
+}
 constexpr int64_t kEstEager = 256;  // estimates copied with the summary inside phd_step
 
 phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
@@ -1171,8 +1178,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
       // index set I from dW = C/D and the mass identity; pass-2 slot layout with I first
       SlotConsts sc2{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
       KL(launch_select_slots(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->zlab,
-                             c->model, c->zl, c->slots_pad, c->slot_label, c->s_lim, (float)c->p.sensor_xy[0],
-                             (float)c->p.sensor_xy[1], sc2, c->st));
+                             c->model, c->zl, c->wz, sum_layout(), c->slots_pad, c->slot_label, c->s_lim,
+                             (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc2, c->st));
       pa.js = c->s_lim;
     }
     timing_record(c, 5);

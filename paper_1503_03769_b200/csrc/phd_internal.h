@@ -244,10 +244,14 @@ cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                           int32_t* sel_flag, double* info, cudaStream_t s);
 // k_select + the pass-2 slot layout with its per-slot constants (as k_zprep) and 1/D
+// *js = j (0..ZL/2): the first j slot pairs of every lane carry the state sums, or
+// kJsZBlock | b: every slot of the first b z-blocks does (layout 0: whichever needs fewer
+// sum slots; 1 / 2 force the per-lane / whole-z-block layout, for tests: PHD_SUM_LAYOUT)
+constexpr int32_t kJsZBlock = 0x10000;
 cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
-                                int32_t* sel_flag, double* info, const float* z, int model, int zl, int slots_pad,
-                                int32_t* slot_label, int32_t* js, float sensor_x, float sensor_y, SlotConsts sc,
-                                cudaStream_t s);
+                                int32_t* sel_flag, double* info, const float* z, int model, int zl, int wz,
+                                int layout, int slots_pad, int32_t* slot_label, int32_t* js, float sensor_x,
+                                float sensor_y, SlotConsts sc, cudaStream_t s);
 
 // ---- gated update (k_gate.cu, DESIGN.md §5 "Gated update") ------------------
 // Particles are ordered by a Morton cell key in measurement space (stable

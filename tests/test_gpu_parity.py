@@ -485,13 +485,18 @@ def test_importance_predict_and_births(phd, orc, mname, k):
 
 
 @pytest.mark.parametrize("mname", ["position", "range_bearing"])
-def test_index_set_state_sums(phd, orc, mname):
+@pytest.mark.parametrize("layout,M", [("auto", 700), ("lane", 700), ("zblock", 700), ("auto", 2992),
+                                      ("lane", 2992), ("zblock", 2992)])
+def test_index_set_state_sums(phd, orc, mname, layout, M, monkeypatch):
     """stphd_all = 0 (default): the index set I is chosen right after pass 1 from dW = C/D and
     W = (1-pD) W_pred + sum dW; pass 2 accumulates S only for I.  The estimates equal those of
-    the all-measurement run (same labels, states to fp32 rounding) and S is 0 outside I."""
+    the all-measurement run (same labels, states to fp32 rounding) and S is 0 outside I --
+    with I on the first slot pairs of every lane and on whole z-blocks (PHD_SUM_LAYOUT)."""
+    if layout != "auto":
+        monkeypatch.setenv("PHD_SUM_LAYOUT", layout)
     m_all = replace(MODELS[mname], clutter_rate=5.0)
     m_sel = replace(m_all, stphd_all=0)
-    z = _meas(m_all, 700, 9)
+    z = _meas(m_all, M, 9)
     soa, w = _cloud(m_all, 15001, z, 9)
     res = []
     for m in (m_all, m_sel):
