@@ -198,7 +198,7 @@ struct phd_ctx {
   double* C_slot = nullptr;
   int32_t* sel_flag = nullptr;   // k_select: label in the estimated index set I
   double* sel_info = nullptr;    // (W_id, LT, n_eligible, n_sel, ..)
-  int32_t* s_lim = nullptr;      // pass 2: state-sum slot pairs per lane (js, written by k_slots2)
+  int32_t* s_lim = nullptr;      // pass 2: state-sum layout (js pairs per lane or kJsZBlock|b; k_select_slots)
   bool select = false;           // this update selected I before pass 2
   int m_prev_ext = -1;   // >= 0: zprev holds an explicit Z_{k-1} of this size
   double W = 0, W_pred = 0;
@@ -881,7 +881,7 @@ static void build_slots(phd_ctx* c, int M) {
   }
   c->n_slots = n;
   const int n_fill = n;  // slots [n_fill, slots_pad) are padding
-  if (c->model == kRangeBearing && M > 0) n = std::max(n, M + 6);  // room for the pass-2 layout (k_slots2)
+  if (c->model == kRangeBearing && M > 0) n = std::max(n, M + 6);  // room for the pass-2 layout (k_select_slots)
   // group-pipelined update for large M: 4 slots/lane/pass, 4 warps,
   // groups of 512 slots; otherwise the two-sweep path with 8 (or 4) slots per lane
   // Opt-in (PHD_FUSE=1): measured neutral on B200 (49.6 vs 49.0 ms at cfg 5) because
