@@ -7,21 +7,23 @@
 // ex2.approx.ftz) once |x - z| exceeds ~120 m.  This path computes the same
 // non-zero terms and skips only pairs whose exponent is provably below -130:
 //
-//   1. k_gate_keys + counting sort: each particle gets the Morton key of its
-//      64 x 64 cell in measurement space ((x, y), or (r, theta) for the
-//      range-bearing sensor); a stable counting sort orders the particle
-//      indices by cell, and k_gate_gather writes a sorted copy of the state
+//   1. k_ms_hist<KeyCell> + gate_scan + k_psort_scatter: each particle gets the
+//      Morton key of its 64 x 64 cell in measurement space ((x, y), or (r, theta)
+//      for the range-bearing sensor); a stable counting sort writes every particle
+//      as one whole record (state + log2(p_D c w)) to its sorted slot and inv[i]
 //      (the filter's own particle order, which defines resampling, is untouched).
+//      NaN particles are counted here (the dense C would be NaN).
 //   2. gate_zbin: measurements binned into the same cells (the same counting sort).
-//   3. k_gate_tiles: per tile of kGateTP sorted particles, the bounding box and
-//      max log2(p_D c w); a measurement is a candidate of the tile iff
+//   3. k_gate_count / k_gate_fill (tile_enum): per tile of kGateTP sorted particles,
+//      the bounding box and max log2(p_D c w); a measurement is a candidate of the
+//      tile iff
 //         e_max = -alpha0 dx^2 - alpha1 dy^2 + max_i log2(p_D c w_i) >= -130
 //      with (dx, dy) its distance to the box (wrapped in bearing).  Every term
 //      of a non-candidate pair has e <= e_max < -130 (fp32 rounding of the
 //      kernels' exponent is ~1e-4 here), so it is exactly 0 in the dense path.
 //   4. k_gpass<1>: CTA per tile, four particles per thread (2 x f32x2), candidates
 //      broadcast from shared memory; the same per-pair arithmetic as the dense
-//      pass (pair_math.cuh), so every term is bitwise the dense kernel's.  Tile
+//      pass (pair_math.cuh), so every term is bitwise the dense pass 2's.  Tile
 //      sums per candidate: warp tree (transposed butterfly), fp64 across warps.
 //   5. the entries (tile, candidate) are stably sorted by label and k_gate_reduce
 //      sums each label's tile partials in entry order (fp64, warp tree):
