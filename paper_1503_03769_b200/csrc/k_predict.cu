@@ -1,9 +1,10 @@
 // Prediction step (§2.2 step 1): Eq 5 survivors with the CV model
 // and Eq 6 births (measurement-driven, S10), plus the
 // Eq 6 importance weights of birth_model 2 (k_birth_is).
-// One thread per particle slot of this rank's block; SoA fp32 in/out, HBM-bound
-// (20 B read + 20 B written per survivor; 20 B written per birth; +32 B of
-// range-bearing representation when that sensor is used).
+// SoA fp32 in/out, HBM-bound (20 B read + 20 B written per survivor; 20 B written
+// per birth; +32 B of range-bearing representation when that sensor is used): four
+// survivors per thread with float4 loads/stores for large position-sensor
+// populations, one slot per thread otherwise (k_predict<VEC>).
 #include "phd_internal.h"
 
 #include <cstdlib>

@@ -7,7 +7,8 @@
 //   LT   = round(W), index set I = the LT largest dW (dW desc, label asc).
 // Pass 2 then accumulates the weighted-state sums S_l (Eq 18) only for l in I
 // -- the labels whose states the paper estimates -- in a
-// slot layout that puts I first, so the choice is warp-uniform.
+// slot layout that puts I first (on every lane's first slot pairs, or on whole
+// z-blocks), so the choice is warp- or CTA-uniform.
 #include "phd_internal.h"
 #include "topk.cuh"
 
