@@ -362,6 +362,37 @@ def run_ours(args):
     run_steps(1, args.warmup, Zh, False)
     pairs_e, ms_e = timed_steps(Zh, args.warmup + 1)
 
+    # ---- near-tie counts (north_star: resampled indices bit-exact except thresholds within
+    # 1e-9 of a cumulative-sum boundary, "with that count reported"; S8 label sets) ----
+    # one more step through the separate calls, after the timed regions: the weights the
+    # kernels resampled are read back and the thresholds near a boundary counted on the host
+    near = None
+    if args.mode == "exact":
+        from paper_1503_03769_b200.diag import resample_near_ties, label_threshold_near_ties
+        kx = args.warmup + args.steps + 1
+        f.predict(kx)
+        f.update(Z[kx - 1])
+        _, wn_loc, _ = f.get_particles()
+        _, sx = f.extract()
+        f.resample_exchange(kx)
+        anc_loc, first = f.ancestors()
+        meta = f.resample_meta()
+        O_r = float(sum(meta["W_r"][:rank]))
+        ties = int(np.sum(resample_near_ties(wn_loc, meta["U"], meta["N_out"], W=meta["W"], O=O_r,
+                                             j_lo=first, j_hi=first + len(anc_loc))))
+        if world > 1:
+            t = torch.tensor([ties], device=dev, dtype=torch.int64)
+            dist.all_reduce(t)
+            ties = int(t.item())
+        lab = label_threshold_near_ties(f.accumulators(int(Z[kx - 1].shape[0]))[:, 0], int(sx["LT"])) \
+            if rank == 0 else None
+        near = {"step": kx, "resample_thresholds_within_1e-9": ties, "N_out": int(meta["N_out"]),
+                "label_threshold_near_ties": lab, "LT": int(sx["LT"]),
+                "basis": "thresholds t_j = (j+U)W/N_out within 1e-9 (unnormalised mass) of a cumulative sum of "
+                         "the resampled fp32 weights (where the GPU's fp64 scan order may pick the neighbour); "
+                         "labels whose dW is within 1e-5 relative of the LT-th (S8). Ancestor mismatches vs the "
+                         "oracle are checked element-wise in tests/test_gpu_parity.py::test_full_size_sampled"}
+
     # ---- gated update (NEXT-2): same workload, same steps, gate = 1 ----
     gated = None
     if not args.no_gated_leg and args.gate == 0:
@@ -518,6 +549,7 @@ def run_ours(args):
                           "note": "Table 1 (PAPER.md:497-513), context only: not this metric or workload"},
         "hbm_kernels": hbm,
         "gated": gated,
+        "near_ties": near,
         "clocks": clk,
     }
     print(json.dumps(out), flush=True)

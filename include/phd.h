@@ -148,8 +148,10 @@ typedef struct {
 } phd_estimate;
 
 typedef struct {
-  double W;               /* sum of updated weights over all ranks (N_k) */
-  double W_pred;          /* sum of predicted weights */
+  double W;               /* sum of updated weights over all ranks (N_k); DCP mode:
+                             the mean over the K groups (each group is a full-intensity filter,
+                             PAPER.md:221, so the mean, not the sum, estimates the count) */
+  double W_pred;          /* sum of predicted weights (DCP: mean over the groups) */
   double undetected_mass; /* dW^0 = (1 - p_D) W_pred (Eq 17) */
   int64_t LT;             /* round half away from zero of W */
   int64_t N;              /* global particle count of this update */

@@ -147,8 +147,10 @@ struct LocalGroup {
   std::vector<ExchangePlan> plans;
   std::vector<const void*> gsrc;
   std::vector<std::vector<void*>> shared;
+  std::vector<int> dev;
 
-  explicit LocalGroup(int w) : world(w), bufs(w, nullptr), srcs(w), plans(w), gsrc(w, nullptr), shared(w) {}
+  explicit LocalGroup(int w)
+      : world(w), bufs(w, nullptr), srcs(w), plans(w), gsrc(w, nullptr), shared(w), dev(w, -1) {}
 
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
@@ -169,11 +171,33 @@ int local_group_world(const LocalGroup* g) { return g ? g->world : 0; }
 
 class LocalComm : public Comm {
  public:
-  LocalComm(LocalGroup* g, int rank) : g_(g), rank_(rank) {}
+  LocalComm(LocalGroup* g, int rank, int device) : g_(g), rank_(rank) { g_->dev[rank] = device; }
   ~LocalComm() override {
     if (tmp_) cudaFree(tmp_);
   }
   const char* name() const override { return "local"; }
+
+  // Called after a barrier (every rank has registered its device): kernels of this
+  // rank read / write the other ranks' buffers, so ranks on other GPUs need peer access.
+  std::string peers() {
+    if (peers_done_) return "";
+    peers_done_ = true;
+    int me = g_->dev[rank_];
+    for (int r = 0; r < g_->world; ++r) {
+      int d = g_->dev[r];
+      if (d == me || d < 0) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, me, d) != cudaSuccess || !can)
+        return "local group: device " + std::to_string(me) + " has no peer access to device " + std::to_string(d);
+      cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return std::string("local group: cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e);
+      }
+    }
+    return "";
+  }
 
   std::string allreduce_f64(double* buf, size_t n, cudaStream_t s) override {
     if (n > tmp_n_) {
@@ -185,6 +209,13 @@ class LocalComm : public Comm {
     if (e != cudaSuccess) return cudaGetErrorString(e);
     g_->bufs[rank_] = buf;
     g_->barrier();
+    {
+      std::string pe = peers();
+      if (!pe.empty()) {
+        g_->barrier();
+        return pe;
+      }
+    }
     // every rank sums all ranks' buffers in rank order (identical bits on every rank)
     if (n) {
       e = launch_sum_ranks(g_->bufs.data(), g_->world, tmp_, n, s);
@@ -203,6 +234,13 @@ class LocalComm : public Comm {
     g_->srcs[rank_].assign(src, src + narr);
     g_->plans[rank_] = p;
     g_->barrier();
+    {
+      std::string pe = peers();
+      if (!pe.empty()) {
+        g_->barrier();
+        return pe;
+      }
+    }
     for (int q = 0; q < g_->world && e == cudaSuccess; ++q) {
       if (q == rank_ || p.recv_count[q] <= 0) continue;
       int64_t off = g_->plans[q].send_off[rank_];
@@ -220,6 +258,13 @@ class LocalComm : public Comm {
     if (e != cudaSuccess) return cudaGetErrorString(e);
     g_->shared[rank_].assign(local, local + nbuf);
     g_->barrier();
+    {
+      std::string pe = peers();
+      if (!pe.empty()) {
+        g_->barrier();
+        return pe;
+      }
+    }
     all->clear();
     bool null = false;
     for (int r = 0; r < g_->world; ++r) {
@@ -235,6 +280,13 @@ class LocalComm : public Comm {
     if (e != cudaSuccess) return cudaGetErrorString(e);
     g_->gsrc[rank_] = send;
     g_->barrier();
+    {
+      std::string pe = peers();
+      if (!pe.empty()) {
+        g_->barrier();
+        return pe;
+      }
+    }
     for (int r = 0; r < g_->world && e == cudaSuccess; ++r)
       e = cudaMemcpyAsync((char*)recv + r * bytes, g_->gsrc[r], bytes, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -247,14 +299,15 @@ class LocalComm : public Comm {
   int rank_;
   double* tmp_ = nullptr;
   size_t tmp_n_ = 0;
+  bool peers_done_ = false;
 };
 
-Comm* make_local_comm(LocalGroup* g, int rank, std::string* err) {
+Comm* make_local_comm(LocalGroup* g, int rank, int device, std::string* err) {
   if (!g || rank < 0 || rank >= g->world) {
     *err = "bad local group / rank";
     return nullptr;
   }
-  return new LocalComm(g, rank);
+  return new LocalComm(g, rank, device);
 }
 
 }  // namespace phd

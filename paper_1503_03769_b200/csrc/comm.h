@@ -46,7 +46,9 @@ struct LocalGroup;
 LocalGroup* local_group_create(int world);
 void local_group_destroy(LocalGroup* g);
 int local_group_world(const LocalGroup* g);
-Comm* make_local_comm(LocalGroup* g, int rank, std::string* err);
+// device: the rank's GPU; ranks of one group on different GPUs get peer access
+// (or the first collective fails with an error).
+Comm* make_local_comm(LocalGroup* g, int rank, int device, std::string* err);
 
 cudaError_t launch_sum_ranks(const double* const* srcs, int world, double* dst, size_t n, cudaStream_t s);
 

@@ -181,11 +181,7 @@ cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const 
   int n2 = 1;
   while (n2 < M) n2 <<= 1;
   size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long) + (size_t)n2 * (sizeof(double) + sizeof(int));
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 20);
-    attr_set = true;
-  }
+  ensure_max_smem(k_extract, 8192 * 20);
   pdl_launch(k_extract, 1, kTopkThreads, smem, s, acc_lab, M, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
                                           count_out, sel_info, sel_flag);
   return cudaGetLastError();

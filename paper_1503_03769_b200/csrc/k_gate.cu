@@ -354,12 +354,7 @@ cudaError_t ms_pass(KF kf, const int32_t* vals, int64_t n, int64_t per_blk, int 
   nbins = std::max(2, nbins);
   const int nblk = (int)((n + per_blk - 1) / per_blk);
   const size_t smem = sizeof(uint32_t) * (size_t)kMsWarps * (nbins / 2) + sizeof(int) * (size_t)nbins;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ms_scatter<KF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(uint32_t) * kMsWarps * (kSortMaxBins / 2) + sizeof(int) * kSortMaxBins));
-    attr = true;
-  }
+  ensure_max_smem(k_ms_scatter<KF>, sizeof(uint32_t) * kMsWarps * (kSortMaxBins / 2) + sizeof(int) * kSortMaxBins);
   pdl_launch(k_ms_hist<KF>, nblk, 256, 0, s, kf, n, per_blk, nbins, nblk, hist, nullptr);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)nbins * nblk, scan_tmp, s, launches);
@@ -1098,12 +1093,8 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
   const int64_t per_blk = sort_block(n);
   const int nblk = (int)((n + per_blk - 1) / per_blk);
   const size_t smem = sizeof(uint32_t) * (size_t)kMsWarps * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_psort_scatter<kRangeBearing>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_psort_scatter<kPosIso>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_max_smem(k_psort_scatter<kRangeBearing>, smem);
+  ensure_max_smem(k_psort_scatter<kPosIso>, smem);
   pdl_launch(k_ms_hist<KeyCell>, nblk, 256, 0, s, kf, n, per_blk, kGateBins, nblk, hist, keys);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);

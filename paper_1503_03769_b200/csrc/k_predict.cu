@@ -8,9 +8,25 @@
 #include "phd_internal.h"
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include "philox.cuh"
 
 namespace phd {
+
+cudaError_t ensure_max_smem_impl(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[std::make_pair(func, dev)];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 bool pdl_enabled() {
   static const bool on = [] {

@@ -115,11 +115,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_select(const double* __restric
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                           int32_t* sel_flag, double* info, cudaStream_t s) {
   size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    attr = true;
-  }
+  ensure_max_smem(k_select, 8192 * 8);
   pdl_launch(k_select, 1, kTopkThreads, smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info);
   return cudaGetLastError();
 }
@@ -291,11 +287,7 @@ cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M,
                                 int layout, int slots_pad, int32_t* slot_label, int32_t* js, float sensor_x,
                                 float sensor_y, SlotConsts sc, cudaStream_t s) {
   size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_select_slots, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    attr = true;
-  }
+  ensure_max_smem(k_select_slots, 8192 * 8);
   pdl_launch(k_select_slots, 1, kTopkThreads, smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info, z, model, zl,
              wz, layout, slots_pad, slot_label, js, sensor_x, sensor_y, sc);
   return cudaGetLastError();

@@ -337,12 +337,7 @@ static size_t pass_smem(int wz) {
 
 template <int MODEL, int PASS, int ZL>
 static void set_attr() {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_pass<MODEL, PASS, ZL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)pass_smem<MODEL, PASS, ZL>(kMaxWarpsZ));
-    attr = true;
-  }
+  ensure_max_smem(k_pass<MODEL, PASS, ZL>, pass_smem<MODEL, PASS, ZL>(kMaxWarpsZ));
 }
 
 template <int MODEL, int PASS, int ZL>
@@ -548,12 +543,7 @@ static size_t fused_smem(int wz) {
 
 template <int MODEL, bool H1, bool H2>
 static cudaError_t launch_fused_t(const FusedArgs& fa, int gp, int zbg, int wz, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fused<MODEL, H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)fused_smem<MODEL>(kMaxWarpsZ));
-    attr = true;
-  }
+  ensure_max_smem(k_fused<MODEL, H1, H2>, fused_smem<MODEL>(kMaxWarpsZ));
   pdl_launch(k_fused<MODEL, H1, H2>, dim3((unsigned)gp, (unsigned)zbg), wz * 32, fused_smem<MODEL>(wz), s, fa);
   return cudaGetLastError();
 }
@@ -577,8 +567,7 @@ cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_
 template <int MODEL>
 static int fused_occ_m(int wz) {
   int n = 0, m;
-  cudaFuncSetAttribute(k_fused<MODEL, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)fused_smem<MODEL>(kMaxWarpsZ));
+  ensure_max_smem(k_fused<MODEL, true, true>, fused_smem<MODEL>(kMaxWarpsZ));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<MODEL, true, true>, wz * 32, fused_smem<MODEL>(wz));
   m = n;
   return m;

@@ -69,8 +69,11 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.cap_g = p->capacity;
   L.cap_l = align_up((size_t)(ceil_div(p->capacity, world) + 1), kBlockW);
   L.cap_off = align_up((size_t)p->capacity, kBlockOff);
-  L.slots_max = (int)align_up((size_t)p->max_meas + 2, 2048);
-  L.zb_max = std::max(1, L.slots_max / std::min(1024, kFuseGroup));  // P planes: one per CTA z-block / group
+  // slots: M labels + up to 3 bearing-class pads + the pass-2 select layout's M + 6;
+  // every z-block size (wz * 32 * zl, 256 ... 2048 slots) divides 2048
+  L.slots_max = (int)align_up((size_t)p->max_meas + 8, 2048);
+  // P planes: one per CTA z-block (smallest: kMinWarpsZ warps x 32 lanes x 4 slots) or group
+  L.zb_max = std::max(1, L.slots_max / std::min(kMinWarpsZ * 32 * 4, kFuseGroup));
   L.part_cap = (int64_t)64 * sms * 256 + 8192;
   L.nbw_max = ceil_div(L.cap_l, kBlockW) + 1;
   L.nbo_max = ceil_div(L.cap_off, kBlockOff) + 1;
@@ -587,7 +590,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   if (world > 1) {
     std::string e;
     if (group) {
-      c->comm = make_local_comm(group->g, rank, &e);
+      c->comm = make_local_comm(group->g, rank, device, &e);
     } else {
       if (!nccl_id) return bail(fail(c, PHD_EINVAL, "nccl_id required for world > 1"));
       c->comm = make_nccl_comm(nccl_id, world, rank, &e);
@@ -862,7 +865,7 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
   return PHD_OK;
 }
 
-static void build_slots(phd_ctx* c, int M) {
+static phd_status build_slots(phd_ctx* c, int M) {
   // slot -> label map; range-bearing: measurements grouped by bearing class so
   // that every f32x2 slot pair uses one bearing representation
   int n = 0;
@@ -934,7 +937,12 @@ static void build_slots(phd_ctx* c, int M) {
   c->zb = M > 0 ? best_zb : 0;
   c->slots_pad = (int)best_pad;
   }
+  // the P planes and the slot arrays are sized for the worst layout (make_layout)
+  if (c->slots_pad > c->L.slots_max || c->zb > c->L.zb_max)
+    return fail(c, PHD_ECAPACITY, "slot layout %d slots / %d z-blocks exceeds %d / %d", c->slots_pad, c->zb,
+                c->L.slots_max, c->L.zb_max);
   for (int s = n_fill; s < c->slots_pad; ++s) c->h_slot[s] = -1;
+  return PHD_OK;
 }
 
 // Gated update (DESIGN.md §5 "Gated update"): identity slot layout (slot = label).
@@ -1033,7 +1041,10 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   // 6.8e7 pairs, 0.28 ms dense vs 0.50 ms gated).  N is global in exact mode, so
   // every rank takes the same branch; DCP groups always plan (collectively).
   const bool small = c->p.gate == 1 && !c->dcp && (double)c->N * (double)M < 536870912.0;
-  if (c->p.gate != 0 && M > 0 && !small && !(getenv("PHD_FUSE") && getenv("PHD_FUSE")[0] == '1')) {
+  // the candidate offsets are an int32 scan: at most M candidates per tile, so a
+  // capacity whose tiles x M could exceed INT32_MAX runs dense (same on every rank)
+  const bool fits32 = (double)c->L.g_ntiles * (double)M <= (double)INT32_MAX;
+  if (c->p.gate != 0 && M > 0 && !small && fits32 && !(getenv("PHD_FUSE") && getenv("PHD_FUSE")[0] == '1')) {
     phd_status st = gate_plan(c, M, n, &gated);
     if (st != PHD_OK) return st;
   }
@@ -1042,10 +1053,12 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     CU(cudaMemcpyAsync(c->h_z, c->zlab, sizeof(float) * 2 * M, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
   }
-  if (gated)
+  if (gated) {
     gate_slots(c, M);
-  else
-    build_slots(c, M);
+  } else {
+    phd_status st = build_slots(c, M);
+    if (st != PHD_OK) return st;
+  }
   const int64_t tiles = ceil_div(n, kTileP);
   if (M > 0) {
     CU(cudaMemcpyAsync(c->slot_label, c->h_slot, sizeof(int32_t) * c->slots_pad, cudaMemcpyHostToDevice, c->st));
@@ -1237,6 +1250,12 @@ static phd_status update_finish(phd_ctx* c) {
     c->W += c->Wr[r];
     c->W_pred += c->Wpr[r];
     c->N_all += (int64_t)c->h_meta[2 * c->world + r];
+  }
+  if (c->dcp) {
+    // every group is a full-intensity PHD filter: the summary reports the
+    // mean over the K groups; each group resamples from its own W_r (next_count_dcp)
+    c->W /= c->world;
+    c->W_pred /= c->world;
   }
   c->bad_flag = reinterpret_cast<int*>(c->h_meta + 3 * c->world)[0];
   double Wsel = c->W;

@@ -38,6 +38,15 @@ __device__ __forceinline__ void pdl_wait() {
 #endif
 }
 bool pdl_enabled();
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute: set it
+// once per (kernel, device) -- and again if a launch needs more -- so that one
+// process driving several GPUs can launch the >48 KB kernels on every device.
+cudaError_t ensure_max_smem_impl(const void* func, int bytes);
+template <typename... KArgs>
+inline cudaError_t ensure_max_smem(void (*kernel)(KArgs...), size_t bytes) {
+  return ensure_max_smem_impl(reinterpret_cast<const void*>(kernel), (int)bytes);
+}
 template <typename... KArgs, typename... Args>
 inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {

@@ -217,3 +217,70 @@ def test_nan_particle_reported_on_every_rank(phd, gate):
     for f in fs:
         f.close()
     group.close()
+
+
+def _parallel(fs, fn):
+    errs = []
+
+    def drive(r):
+        try:
+            fn(r, fs[r])
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=drive, args=(r,)) for r in range(len(fs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+
+
+@pytest.mark.parametrize("xch", ["p2p", "nccl"])
+def test_rank_local_resampling_equals_oracle_large(phd, orc, xch, monkeypatch, near_tie_report):
+    """P = 4 in-process ranks with 1.15 M particles each (rank-local fp64 scans over
+    > 1024 weight blocks, > 1024 offspring blocks per rank, imbalanced mass: the lower
+    half of the ranks holds 1e-3 of it): the concatenated ancestors equal the oracle's
+    sequential systematic resampling of the concatenated updated weights
+     except near-ties, which are counted."""
+    from scenario.configs import Model, POSITION
+    if xch == "nccl":
+        monkeypatch.setenv("PHD_EXCHANGE", "nccl")
+    world, N, M = 4, 4 * 1150 * 1024, 256
+    J = 8192
+    m = Model(meas=POSITION, sigma_z=(10.0, 10.0), p_d=0.98, p_s=0.99, clutter_rate=50.0,
+              region=(-1000.0, 1000.0, -1000.0, 1000.0), births_per_step=J, fixed_count=N - J,
+              count_mode=COUNT_FIXED, capacity=N, max_meas=4096, seed=3)
+    z = scenario.random_measurements(M, 9)
+    soa, w = scenario.clustered_particles(N, z, 4)
+    w = w.astype(np.float64)
+    w[: N // 2] *= 1e-3  # ranks 0, 1 carry little mass
+    w = (w * (100.0 / w.sum())).astype(np.float32)
+    group = phd.LocalGroup(world)
+    fs = [phd.Filter(m, rank=r, world=world, group=group) for r in range(world)]
+    blocks = [phd.rank_block(N, world, r) for r in range(world)]
+    for r, f in enumerate(fs):
+        lo, hi = blocks[r]
+        f.set_particles(np.ascontiguousarray(soa[:, lo:hi]), np.ascontiguousarray(w[lo:hi]), N,
+                        stage=phd.STAGE_PREDICTED)
+    _parallel(fs, lambda r, f: f.update(z))
+    wn = np.concatenate([fs[r].get_particles()[1] for r in range(world)])
+    _parallel(fs, lambda r, f: f.extract())
+    k = 2
+    _parallel(fs, lambda r, f: f.resample_exchange(k))
+    parts = sorted((f.ancestors()[1], f.ancestors()[0]) for f in fs)
+    anc = np.concatenate([a for _, a in parts])
+    meta = fs[0].resample_meta()
+    assert meta["N_out"] == N - J and len(anc) == N - J and np.all(np.diff(anc) >= 0)
+    assert fs[0].exchange_path() == (2 if xch == "p2p" else 1)
+    from test_gpu_parity import check_ancestors
+    check_ancestors(orc, anc, wn, meta["U"], meta["N_out"], near_tie_report, world=world, exchange=xch)
+    # the exchanged population: every rank holds its block of the offspring
+    for r, f in enumerate(fs):
+        s, ww, g0 = f.get_particles()
+        lo, hi = phd.rank_block(N, world, r)
+        assert g0 == lo and s.shape[1] == min(hi, N - J) - min(lo, N - J)
+        assert np.array_equal(s, soa[:, anc[min(lo, N - J):min(hi, N - J)]])
+    for f in fs:
+        f.close()
+    group.close()
