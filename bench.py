@@ -374,6 +374,8 @@ def run_ours(args):
         f.update(Z[kx - 1])
         _, wn_loc, _ = f.get_particles()
         _, sx = f.extract()
+        lab = label_threshold_near_ties(f.accumulators(int(Z[kx - 1].shape[0]))[:, 0], int(sx["LT"])) \
+            if rank == 0 else None
         f.resample_exchange(kx)
         anc_loc, first = f.ancestors()
         meta = f.resample_meta()
@@ -384,8 +386,6 @@ def run_ours(args):
             t = torch.tensor([ties], device=dev, dtype=torch.int64)
             dist.all_reduce(t)
             ties = int(t.item())
-        lab = label_threshold_near_ties(f.accumulators(int(Z[kx - 1].shape[0]))[:, 0], int(sx["LT"])) \
-            if rank == 0 else None
         near = {"step": kx, "resample_thresholds_within_1e-9": ties, "N_out": int(meta["N_out"]),
                 "label_threshold_near_ties": lab, "LT": int(sx["LT"]),
                 "basis": "thresholds t_j = (j+U)W/N_out within 1e-9 (unnormalised mass) of a cumulative sum of "

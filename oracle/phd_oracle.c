@@ -65,6 +65,46 @@ static void philox_at(const orc_model* m, uint64_t g, int32_t k, uint32_t stream
 }
 
 /* ---------------------------------------------------------------------- */
+/* 0) Initialisation ("t=0: Generate M particles for each group. The
+ * number of all particles is N. All these particles are shared with same weights
+ * omega_0 = 1/M"), with the reading S23 of SURVEY.md §8(c): the population of
+ * n_out particles is index-stratified in y over box = (x0, x1, y0, y1),
+ *   y_g = y0 + (y1 - y0) (g + u0) / n_out,  x_g = x0 + (x1 - x0) u1,
+ *   (vx, vy) = v_max (2 u2 - 1, 2 u3 - 1),
+ * u_c = conv23 of word c of Philox({g, 0, 5, g >> 32}) (stream 5, step 0); every
+ * state is rounded to fp32, the precision the filter stores it in.  Particles
+ * g_lo .. g_hi-1 are generated (one group or the whole population); their weights
+ * share total_mass equally (omega_0 = mass / M), or, with a mass box, equally among
+ * the generated particles whose stored (fp32) position lies inside it (closed box),
+ * 0 elsewhere.  No particle inside: every weight 0.  Returns the inside count. */
+int64_t orc_init_population(const orc_model* m, int64_t n_out, int64_t g_lo, int64_t g_hi, const double box[4],
+                            double v_max, double total_mass, const double* mass_box, double* x, double* vx,
+                            double* y, double* vy, double* w) {
+  int64_t n = g_hi - g_lo, inside = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t g = g_lo + i;
+    uint32_t ctr[4] = {(uint32_t)g, 0u, 5u, (uint32_t)((uint64_t)g >> 32)};
+    uint32_t key[2] = {(uint32_t)m->seed, (uint32_t)(m->seed >> 32)};
+    uint32_t o[4];
+    orc_philox4x32_10(ctr, key, o);
+    double u0 = orc_conv23(o[0]), u1 = orc_conv23(o[1]), u2 = orc_conv23(o[2]), u3 = orc_conv23(o[3]);
+    y[i] = (double)(float)(box[2] + (box[3] - box[2]) * ((double)g + u0) / (double)n_out);
+    x[i] = (double)(float)(box[0] + (box[1] - box[0]) * u1);
+    vx[i] = (double)(float)(v_max * (2.0 * u2 - 1.0));
+    vy[i] = (double)(float)(v_max * (2.0 * u3 - 1.0));
+    if (mass_box && x[i] >= mass_box[0] && x[i] <= mass_box[1] && y[i] >= mass_box[2] && y[i] <= mass_box[3])
+      ++inside;
+  }
+  if (!mass_box) inside = n;
+  for (int64_t i = 0; i < n; ++i) {
+    int in = !mass_box ||
+             (x[i] >= mass_box[0] && x[i] <= mass_box[1] && y[i] >= mass_box[2] && y[i] <= mass_box[3]);
+    w[i] = (in && inside > 0) ? (double)(float)(total_mass / (double)inside) : 0.0;
+  }
+  return inside;
+}
+
+/* ---------------------------------------------------------------------- */
 /* Models (§4). */
 
 /* kappa_k(z) = lambda_k V u(z), read as the uniform clutter

@@ -51,6 +51,14 @@ double orc_u52(uint32_t w0, uint32_t w1);
 /* Box-Muller: n1 = sqrt(-2 ln u1) cos(2 pi u2), n2 = sqrt(-2 ln u1) sin(2 pi u2). */
 void orc_box_muller(double u1, double u2, double* n1, double* n2);
 
+/* t = 0 population (reading S23): particles g_lo .. g_hi-1 of n_out,
+ * y-stratified over box = (x0, x1, y0, y1), x uniform, v = v_max (2u - 1), u from
+ * Philox({g, 0, 5, g>>32}); states rounded to fp32; weights total_mass shared equally
+ * (over the particles inside mass_box when given, 0 outside).  Returns the inside count. */
+int64_t orc_init_population(const orc_model* m, int64_t n_out, int64_t g_lo, int64_t g_hi, const double box[4],
+                            double v_max, double total_mass, const double* mass_box, double* x, double* vx,
+                            double* y, double* vy, double* w);
+
 /* kappa(z) = lambda / V, V the area of the measurement region. */
 double orc_kappa(const orc_model* m);
 /* g(z | x) of the sensor model; (x, y) is the target position. */
