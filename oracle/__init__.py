@@ -77,6 +77,9 @@ def lib():
         L.orc_extract.argtypes = [M, ctypes.c_int32, _D, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                                   _I32, _D, _D, _I64, _I32, _D]
         L.orc_extract.restype = ctypes.c_int32
+        L.orc_init_population.argtypes = [M, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _D, ctypes.c_double,
+                                          ctypes.c_double, _D, _D, _D, _D, _D, _D]
+        L.orc_init_population.restype = ctypes.c_int64
         L.orc_resample_U.argtypes = [ctypes.c_uint64, ctypes.c_int32]
         L.orc_resample_U.restype = ctypes.c_double
         L.orc_resample.argtypes = [ctypes.c_int64, _D, ctypes.c_double, ctypes.c_int64, _I64]
@@ -134,6 +137,20 @@ def box_muller(u1, u2):
     a, b = ctypes.c_double(), ctypes.c_double()
     lib().orc_box_muller(float(u1), float(u2), ctypes.byref(a), ctypes.byref(b))
     return a.value, b.value
+
+
+def init_population(m, n_out, box, v_max, total_mass, mass_box=None, g_lo=0, g_hi=None):
+    """t = 0 population (S23): particles g_lo .. g_hi-1 of n_out.
+    Returns (soa [4, n] fp64 in (x, vx, y, vy) order, holding fp32 values; w [n]; inside count)."""
+    g_hi = n_out if g_hi is None else g_hi
+    n = g_hi - g_lo
+    x, vx, y, vy, w = (np.zeros(max(n, 1)) for _ in range(5))
+    b = _f64(box)
+    mb = _f64(mass_box) if mass_box is not None else None
+    inside = lib().orc_init_population(ctypes.byref(model(m)), int(n_out), int(g_lo), int(g_hi), _d(b), float(v_max),
+                                       float(total_mass), _d(mb) if mb is not None else None, _d(x), _d(vx), _d(y),
+                                       _d(vy), _d(w))
+    return np.stack([x[:n], vx[:n], y[:n], vy[:n]]), w[:n], int(inside)
 
 
 def kappa(m):
