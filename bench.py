@@ -139,6 +139,22 @@ def scenario_for(name, steps):
     return cfg
 
 
+def oracle_population_sample(cfg, truth, n):
+    """The first n particles of the config's t = 0 population, from the oracle's own
+    orc_init_population (cpu_baseline / reference arm only), each with the uniform share
+    m0 / N_out of the mass (a timing sample: the mass box of cfg 5 would leave the
+    lowest y-band with zero weight)."""
+    import scenario
+    import oracle
+    ia = scenario.init_args(cfg, truth)
+    n_out = scenario.initial_count(cfg, truth)[0]
+    n = min(n, n_out)
+    soa, w, _ = oracle.init_population(cfg.model, n_out, ia["box"], ia["v_max"], ia["total_mass"] * n / n_out,
+                                       None, 0, n)
+    import numpy as np
+    return np.ascontiguousarray(soa.astype(np.float32)), np.ascontiguousarray(w.astype(np.float32)), n_out
+
+
 def cpu_oracle_sample(cfg, Z, soa, w, n_sample, k=1):
     """The oracle, as it stands, on a bounded sample: one full serial step
     (predict, births, normalisers, update, extraction, resampling) of the
@@ -192,8 +208,8 @@ def run_reference(args):
     import scenario
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
-    soa, w = scenario.initial_population(cfg, truth)
     n_s = 16384
+    soa, w, _ = oracle_population_sample(cfg, truth, n_s)
     times, pairs = [], []
     for s in range(steps):
         r = cpu_oracle_sample(cfg, Z, soa, w, n_s, k=s + 1)
@@ -209,7 +225,7 @@ def run_reference(args):
            "value": val, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * T / len(times), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": cfg.name, "N": int(soa.shape[1] + cfg.model.births_per_step),
+           "config": {"workload": cfg.name, "N": int(scenario.initial_count(cfg, truth)[0] + cfg.model.births_per_step),
                       "M": len(Z[0]), "sample_particles": n_s},
            "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -241,16 +257,13 @@ def run_ours(args):
     m = cfg.model
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
-    soa, w = scenario.initial_population(cfg, truth)
-    n0 = soa.shape[1]
+    ia = scenario.init_args(cfg, truth)   # t = 0 population recipe (phd_init_population)
+    n0 = scenario.initial_count(cfg, truth)[0]
     J = m.births_per_step
     if args.mode == "dcp":   # every rank is one DCPFPHD group holding its block of the population
         lo, hi = phd.rank_block(n0, world, rank)
-        a, b = lo, hi
-        w = w * np.float32(world)  # each group is a full-intensity filter
     else:
         lo, hi = phd.rank_block(n0 + J, world, rank)
-        a, b = min(lo, n0), min(hi, n0)
     nid = None
     if world > 1:
         obj = [phd.nccl_unique_id() if rank == 0 else None]
@@ -263,7 +276,8 @@ def run_ours(args):
                    workspace=workspace)
 
     def reset():
-        f.set_particles(np.ascontiguousarray(soa[:, a:b]), np.ascontiguousarray(w[a:b]), n0)
+        # the t = 0 population on the device (each DCP group: its block, full mass)
+        f.init_population(**ia)
 
     # device-resident measurement sets (value) and pinned host copies (e2e)
     Zd = [torch.from_numpy(z).to(dev) for z in Z]
@@ -495,15 +509,21 @@ def run_ours(args):
                         "basis": "w read 4 B per particle; per offspring: mark 4+4, ancestor state 16 read, "
                                  "state + w 20 written, ancestor index 4 (all resampling kernels incl. scans)"}}
     cpu = None
+    cpu_all = None
     if not args.no_cpu_baseline and world == 1:  # the contract's CPU baseline: rank 0 at N = 1 only
+        soa, w, _ = oracle_population_sample(cfg, truth, args.cpu_sample * 4)
         r = cpu_oracle_sample(cfg, Z, soa, w, args.cpu_sample, k=1)
+        full_pairs = N_glob * M
         cpu = {"value": r["pairs"] / r["seconds"], "unit": "pairs/s", "cores": 1, "kind": "oracle",
                "sample": "one full serial fp64 step (predict, births, normalisers, update, extraction, resampling) "
-                         "of the first %d particles (+%d proportional births) against all M=%d measurements of "
-                         "Z_1; %.1f s" % (args.cpu_sample, r["n"] - args.cpu_sample, r["M"], r["seconds"])}
-    cpu_all = None
-    if not args.no_cpu_baseline and world == 1:
+                         "of the first %d particles of the t=0 population (+%d proportional births) against all "
+                         "M=%d measurements of Z_1; %.1f s" % (args.cpu_sample, r["n"] - args.cpu_sample, r["M"],
+                                                               r["seconds"]),
+               "extrapolated_full_step_s": full_pairs / (r["pairs"] / r["seconds"]),
+               "extrapolated_note": "EXTRAPOLATED, not measured: N*M = %d pairs of one full step at the sample's "
+                                    "pairs/s (the step is O(N M); its O(N) parts are < 1%% at this M)" % full_pairs}
         cpu_all = cpu_oracle_all_cores(cfg, Z, soa, w, args.cpu_sample * 4)
+        cpu_all["extrapolated_full_step_s"] = full_pairs / cpu_all["value"]
     out = {
         "metric": "particle-measurement update pairs/sec and filter step ms",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

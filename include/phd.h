@@ -7,6 +7,7 @@
  * contiguous block of the global particle array and the full measurement set.
  *
  * Step order (Algorithm 1):
+ *   phd_init_population    t = 0: the initial population, once
  *   phd_predict            Eq 5 survivors (CV model PAPER.md:370-388) + Eq 6 births
  *   phd_update             Eq 7/11 normaliser C(z) (all-reduced), Eq 8/12-16 weights
  *                          and STPHD accumulators (all-reduced)
@@ -198,6 +199,30 @@ phd_status phd_group_create(int32_t world, phd_group** out);
 void phd_group_destroy(phd_group* g);
 phd_status phd_create_in_group(const phd_params* p, phd_group* g, int32_t rank, int32_t device, void* stream,
                                void* workspace, phd_ctx** out);
+
+/* ---- t = 0: the initial population ---------------------------------------
+ * PAPER.md:260 ("t=0: Generate M particles for each group. The number of all
+ * particles is N. All these particles are shared with same weights omega_0 = 1/M"),
+ * with the reading S23 of DESIGN.md §2.  Generates on the device, in this rank's
+ * block, the N_out particles of the population (fixed count: fixed_count; adaptive:
+ * max(round(total_mass), 1) R clamped to capacity - J, flag count_clamped):
+ *   y_g = y0 + (y1 - y0)(g + u0)/N_out   (index-stratified: contiguous rank blocks are y-bands)
+ *   x_g = x0 + (x1 - x0) u1,  (vx, vy) = v_max (2 u2 - 1, 2 u3 - 1)
+ * with u_c = ((w_c >> 9) + 1/2) 2^-23 of Philox4x32-10 word c at counter
+ * (g lo32, 0, 5, g hi32), key = seed; fp64 arithmetic, one rounding to fp32.
+ * box = (x0, x1, y0, y1), host array of 4 doubles; NULL: the position region, or
+ *   for range-bearing the square of side r_max centred on the sensor.
+ * Weights: total_mass / N_out each (omega_0 = 1/M per unit mass); with mass_box
+ *   (host, 4 doubles, closed) total_mass / (number of particles whose fp32
+ *   position lies inside it, over all ranks) inside and 0 outside; none inside:
+ *   all 0.  DCP mode: group j holds block j of the population and its own
+ *   total_mass (each group is a full-intensity filter).
+ * Stream-ordered, no host synchronisation; collective for world > 1.  The next
+ * call must be phd_predict (k = 1: births uniform over the region).
+ * Errors: PHD_EINVAL (total_mass or v_max negative / non-finite, empty box),
+ * PHD_ECAPACITY (DCP group above capacity). */
+phd_status phd_init_population(phd_ctx* ctx, double total_mass, const double* box, const double* mass_box,
+                               double v_max);
 
 /* ---- population injection / inspection (parity, checkpoint) ---------------
  * The global particle array at a step is [survivors 0..N_out-1, births

@@ -59,7 +59,7 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_get_ancestors", "phd_get_resample_meta", "phd_launch_count", "phd_set_timing", "phd_get_timing",
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
            "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates",
-           "phd_get_gate_stats", "phd_exchange_path", "phd_set_retained_measurements"]
+           "phd_get_gate_stats", "phd_exchange_path", "phd_set_retained_measurements", "phd_init_population"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -116,6 +116,7 @@ def load(build_if_missing=True):
     L.phd_get_resample_meta.argtypes = [_P, _D, _D, _I64, _D]
     L.phd_get_gate_stats.argtypes = [_P, _I64]
     L.phd_set_retained_measurements.argtypes = [_P, _P, ctypes.c_int32]
+    L.phd_init_population.argtypes = [_P, ctypes.c_double, _D, _D, ctypes.c_double]
     L.phd_exchange_path.argtypes = [_P]
     L.phd_exchange_path.restype = ctypes.c_int32
     L.phd_launch_count.argtypes = [_P]
@@ -304,6 +305,14 @@ class Filter:
         self._keep = (soa4, w)
         self._check(self.L.phd_set_particles(self.h, _ptr(soa4), _ptr(w), int(n_local), int(n_global),
                                              float(mass), int(stage)), "phd_set_particles")
+
+    def init_population(self, total_mass, box=None, mass_box=None, v_max=20.0):
+        """t = 0 population on the device: y-stratified over box, total mass
+        total_mass (only inside mass_box when given).  Collective."""
+        b = None if box is None else (ctypes.c_double * 4)(*[float(v) for v in box])
+        mb = None if mass_box is None else (ctypes.c_double * 4)(*[float(v) for v in mass_box])
+        self._check(self.L.phd_init_population(self.h, float(total_mass), b, mb, float(v_max)),
+                    "phd_init_population")
 
     def get_particles(self, cap=None):
         n = ctypes.c_int64()

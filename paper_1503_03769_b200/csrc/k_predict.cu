@@ -7,6 +7,7 @@
 // populations, one slot per thread otherwise (k_predict<VEC>).
 #include "phd_internal.h"
 
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -297,6 +298,75 @@ __global__ void __launch_bounds__(256) k_rb_repr(const float* __restrict__ x, co
   pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) rb_repr(x[i], y[i], sx, sy, rb, stride, i);
+}
+
+// ---------------------------------------------------------------------------
+// t = 0 population ("Generate M particles for each group ... same weights
+// omega_0 = 1/M"; reading S23): particle g is y-stratified over the box,
+//   y = y0 + (y1 - y0)(g + u0)/n_out,  x = x0 + (x1 - x0) u1,  v = v_max (2 u2 - 1, 2 u3 - 1),
+// u_c = word c of Philox({g, 0, 5, g >> 32}); fp64 with explicit IEEE roundings (no
+// contraction) then one rounding to fp32, so the states are bitwise the oracle's.
+// HBM-bound: 20 B written per particle.
+__device__ __forceinline__ bool in_box(float x, float y, const double* b) {
+  const double xd = x, yd = y;
+  return xd >= b[0] && xd <= b[1] && yd >= b[2] && yd <= b[3];
+}
+
+__global__ void __launch_bounds__(256) k_init_population(const InitArgs a) {
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int cnt = 0;
+  const float wu = a.has_mbox ? 0.0f : __double2float_rn(__ddiv_rn(a.total_mass, a.n_norm));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_local; i += stride) {
+    const int64_t g = a.g0 + i;
+    const U4 o = philox_at(a.seed, (uint64_t)g, 0u, 5u);
+    const double u0 = u01(o.x), u1 = u01(o.y), u2 = u01(o.z), u3 = u01(o.w);
+    const double y = __dadd_rn(a.box[2], __ddiv_rn(__dmul_rn(__dsub_rn(a.box[3], a.box[2]), __dadd_rn((double)g, u0)),
+                                                   (double)a.n_out));
+    const double x = __dadd_rn(a.box[0], __dmul_rn(__dsub_rn(a.box[1], a.box[0]), u1));
+    const double vx = __dmul_rn(a.v_max, __dsub_rn(__dmul_rn(2.0, u2), 1.0));
+    const double vy = __dmul_rn(a.v_max, __dsub_rn(__dmul_rn(2.0, u3), 1.0));
+    const float xf = __double2float_rn(x), yf = __double2float_rn(y);
+    a.x[i] = xf;
+    a.vx[i] = __double2float_rn(vx);
+    a.y[i] = yf;
+    a.vy[i] = __double2float_rn(vy);
+    if (a.has_mbox) {
+      cnt += in_box(xf, yf, a.mbox) ? 1 : 0;
+    } else {
+      a.w[i] = wu;
+    }
+  }
+  if (a.has_mbox) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt > 0) atomicAdd(a.count, (double)cnt);  // integers: exact in any order
+  }
+}
+
+__global__ void __launch_bounds__(256) k_init_weights(const InitArgs a) {
+  pdl_wait();
+  const double c = *a.count;
+  const float wv = c > 0.0 ? __double2float_rn(__ddiv_rn(a.total_mass, c)) : 0.0f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_local; i += stride)
+    a.w[i] = in_box(a.x[i], a.y[i], a.mbox) ? wv : 0.0f;
+}
+
+static unsigned init_grid(int64_t n) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+}
+
+cudaError_t launch_init_population(const InitArgs& a, cudaStream_t s) {
+  if (a.n_local <= 0) return cudaSuccess;
+  pdl_launch(k_init_population, init_grid(a.n_local), 256, 0, s, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_weights(const InitArgs& a, cudaStream_t s) {
+  if (a.n_local <= 0) return cudaSuccess;
+  pdl_launch(k_init_weights, init_grid(a.n_local), 256, 0, s, a);
+  return cudaGetLastError();
 }
 
 __global__ void k_fill(float* p, float v, int64_t n) {

@@ -720,6 +720,87 @@ phd_status phd_set_particles(phd_ctx* c, const float* soa4, const float* w, int6
   return PHD_OK;
 }
 
+phd_status phd_init_population(phd_ctx* c, double total_mass, const double* box, const double* mass_box,
+                               double v_max) {
+  NvtxRange nvtx_("phd_init_population");
+  if (!c) return PHD_EINVAL;
+  cudaSetDevice(c->device);
+  c->err.clear();
+  if (!(total_mass >= 0.0) || !std::isfinite(total_mass)) return fail(c, PHD_EINVAL, "total_mass must be finite and >= 0");
+  if (!(v_max >= 0.0) || !std::isfinite(v_max)) return fail(c, PHD_EINVAL, "v_max must be finite and >= 0");
+  double b[4];
+  if (box) {
+    for (int i = 0; i < 4; ++i) b[i] = box[i];
+  } else if (c->p.meas == PHD_MEAS_POSITION) {
+    for (int i = 0; i < 4; ++i) b[i] = c->p.region[i];
+  } else {  // range-bearing: the Cartesian square of side r_max centred on the sensor (S27)
+    const double h = 0.5 * c->p.region[1];
+    b[0] = c->p.sensor_xy[0] - h;
+    b[1] = c->p.sensor_xy[0] + h;
+    b[2] = c->p.sensor_xy[1] - h;
+    b[3] = c->p.sensor_xy[1] + h;
+  }
+  for (int i = 0; i < 4; ++i)
+    if (!std::isfinite(b[i]) || (mass_box && std::isnan(mass_box[i]))) return fail(c, PHD_EINVAL, "non-finite box");
+  if (!(b[1] > b[0] && b[3] > b[2])) return fail(c, PHD_EINVAL, "empty box");
+  // population size: N_out of the count mode (adaptive: max(round(m0), 1) R, clamped as next_count)
+  int64_t n_out;
+  int clamped = 0;
+  if (c->p.count_mode == PHD_COUNT_FIXED) {
+    n_out = c->p.fixed_count;
+  } else {
+    const int64_t m0 = std::max<int64_t>(1, (int64_t)std::floor(total_mass + 0.5));
+    n_out = m0 * c->p.particles_per_target;
+    const int64_t lim = c->p.capacity - c->p.births_per_step;
+    if (m0 > lim / c->p.particles_per_target || n_out > lim) {
+      n_out = lim;
+      clamped = 1;
+    }
+  }
+  InitArgs a{};
+  int64_t lo, hi;
+  if (c->dcp) {  // group j holds block j of the population, with its own mass (omega_0 = 1/M per group)
+    block_of(n_out, c->world, c->rank, &lo, &hi);
+    int64_t jlo, jhi;
+    group_births(c, &jlo, &jhi);
+    if ((hi - lo) + (jhi - jlo) > c->L.cap_l - 1) return fail(c, PHD_ECAPACITY, "group size exceeds capacity");
+  } else {
+    block_of(n_out + c->p.births_per_step, c->world, c->rank, &lo, &hi);
+    lo = std::min(lo, n_out);
+    hi = std::min(hi, n_out);
+  }
+  a.n_local = hi - lo;
+  a.g0 = lo;
+  a.n_out = n_out;
+  a.seed = c->p.seed;
+  for (int i = 0; i < 4; ++i) a.box[i] = b[i];
+  a.v_max = v_max;
+  a.has_mbox = mass_box != nullptr;
+  if (mass_box)
+    for (int i = 0; i < 4; ++i) a.mbox[i] = mass_box[i];
+  a.total_mass = total_mass;
+  a.n_norm = c->dcp ? (double)(hi - lo) : (double)n_out;
+  a.x = c->A[0];
+  a.vx = c->A[1];
+  a.y = c->A[2];
+  a.vy = c->A[3];
+  a.w = c->A[4];
+  a.count = c->ring;  // scratch (the DCP ring counts are rewritten at every resampling)
+  if (a.has_mbox) CU(cudaMemsetAsync(a.count, 0, sizeof(double), c->st));
+  KL(launch_init_population(a, c->st));
+  if (a.has_mbox) {
+    if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(a.count, 1, c->st));
+    KL(launch_init_weights(a, c->st));
+  }
+  c->n_out = c->dcp ? hi - lo : n_out;
+  c->n_surv_local = hi - lo;
+  c->count_clamped = clamped;
+  c->M_z = -1;  // t = 0: no Z_{k-1}, the first births are uniform over the region
+  c->stage = kResampled;
+  c->populated = true;
+  return PHD_OK;
+}
+
 phd_status phd_set_retained_measurements(phd_ctx* c, const float* z, int32_t M) {
   if (!c) return PHD_EINVAL;
   cudaSetDevice(c->device);

@@ -135,6 +135,24 @@ struct PredictArgs {
   int64_t rb_stride;
 };
 
+// t = 0 population (reading S23): local slots [0, n_local) hold the
+// global particles [g0, g0 + n_local) of a population of n_out.
+struct InitArgs {
+  int64_t n_local, g0, n_out;
+  uint64_t seed;
+  double box[4];             // x0, x1, y0, y1 (y-stratified)
+  double v_max;
+  int has_mbox;              // mass only inside mbox (closed)
+  double mbox[4];
+  double total_mass;
+  double n_norm;             // particles sharing the mass without a mass box (population or DCP group)
+  float *x, *vx, *y, *vy, *w;
+  double* count;             // particles inside the mass box (fp64 integer sum; all-reduced over ranks)
+};
+cudaError_t launch_init_population(const InitArgs& a, cudaStream_t s);
+// second pass (mass box): w = total_mass / count inside, 0 outside
+cudaError_t launch_init_weights(const InitArgs& a, cudaStream_t s);
+
 struct ResampleArgs {
   int64_t n_local;
   int64_t g0;

@@ -3,5 +3,5 @@
 Holds none of the filter's arithmetic ("Input recipe")."""
 from . import configs
 from .configs import CONFIGS, ORDER, get, scaled, POSITION, RANGE_BEARING, COUNT_FIXED, COUNT_ADAPTIVE
-from .generate import (simulate_truth, measurements, initial_population, initial_count,
+from .generate import (simulate_truth, measurements, initial_population, initial_count, init_args,
                        random_particles, clustered_particles, random_measurements)

@@ -137,6 +137,18 @@ def initial_population(cfg, truth=None, n=None):
     return np.ascontiguousarray(soa), w
 
 
+def init_args(cfg, truth=None):
+    """Arguments of phd_init_population for a config (the t = 0 population recipe of
+    SURVEY.md §8(d); parameters only): total mass m0 = targets alive at step 0 (min 1),
+    the Cartesian box, the mass box (cfg 5) and the velocity bound."""
+    m, s = cfg.model, cfg.scenario
+    truth = truth or simulate_truth(cfg)
+    m0 = max(int(truth.alive[0].sum()), 1)
+    box = s.init_box or (m.region if m.meas == POSITION else (-1000.0, 1000.0, -1000.0, 1000.0))
+    return {"total_mass": float(m0), "box": tuple(float(v) for v in box),
+            "mass_box": s.init_mass_box, "v_max": 20.0}
+
+
 def random_particles(n, seed, box=(-1000.0, 1000.0, -1000.0, 1000.0), vmax=20.0,
                      w_range=(1e-4, 1e-2), stream=21):
     """Generic seeded particle cloud for parity tests (fp32 SoA + fp32 weights)."""

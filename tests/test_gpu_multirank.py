@@ -46,18 +46,22 @@ def _run(phd, cfg, world, steps):
     m = cfg.model
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
-    soa, w = scenario.initial_population(cfg, truth)
-    n0 = soa.shape[1]
     group = phd.LocalGroup(world) if world > 1 else None
-    fs = []
-    for r in range(world):
-        f = phd.Filter(m, rank=r, world=world, group=group)
-        lo, hi = phd.rank_block(n0 + m.births_per_step, world, r)
-        a, b = min(lo, n0), min(hi, n0)
-        f.set_particles(np.ascontiguousarray(soa[:, a:b]), np.ascontiguousarray(w[a:b]), n0)
-        fs.append(f)
+    fs = [phd.Filter(m, rank=r, world=world, group=group) for r in range(world)]
+    ia = scenario.init_args(cfg, truth)
     out = {"summ": [], "est": [], "anc": [], "pop": []}
     errs = []
+
+    def init(r):
+        try:
+            fs[r].init_population(**ia)  # t = 0 on the device, collective (mass-box count)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=init, args=(r,)) for r in range(world)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not errs, errs
 
     def drive(r, k):
         try:

@@ -372,9 +372,13 @@ def test_full_size_sampled(phd, orc, cname, near_tie_report):
     m = cfg.model
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
-    soa, w = scenario.initial_population(cfg, truth)
     f = phd.Filter(m)
-    f.set_particles(soa, w, soa.shape[1])
+    ia = scenario.init_args(cfg, truth)
+    f.init_population(**ia)  # the bench's t = 0 population, on the device
+    soa, w, _ = f.get_particles()
+    if cname == "cfg5":  # bit-exact against the oracle's t = 0 population
+        so, wo, _ = orc.init_population(m, soa.shape[1], ia["box"], ia["v_max"], ia["total_mass"], ia["mass_box"])
+        assert np.array_equal(soa, so.astype(np.float32)) and np.array_equal(w, wo.astype(np.float32))
     f.predict(1)
     ps, pw, _ = f.get_particles()
     # sampled prediction (the launch the bench times: at cfg 5 the float4 path, four
