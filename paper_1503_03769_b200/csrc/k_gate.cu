@@ -779,6 +779,23 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
     }
     return ex2v(expo<MODEL>(d0, d1, na0, na1, P[h].LW));
   };
+  // pass 2 with 1/D folded into the exponent (zd = log2(d)/na0): u d = p_D g w / (kappa + C),
+  // bitwise the dense pass 2's term
+  auto term_fold = [&](int k, int h, float2& d0, float2& d1) -> float2 {
+    const float2 nz = zn[k];
+    if (RB) {
+      const int rep = zr[k];
+      const float2 th = rep == 0 ? P[h].T_hi[0] : (rep == 1 ? P[h].T_hi[1] : P[h].T_hi[2]);
+      const float2 tl = rep == 0 ? P[h].T_lo[0] : (rep == 1 ? P[h].T_lo[1] : P[h].T_lo[2]);
+      d0 = __fadd2_rn(__fadd2_rn(P[h].R_hi, f2(nz.x, nz.x)), P[h].R_lo);
+      d1 = __fadd2_rn(__fadd2_rn(th, f2(nz.y, nz.y)), tl);
+    } else {
+      d0 = __fadd2_rn(P[h].X, f2(nz.x, nz.x));
+      d1 = __fadd2_rn(P[h].Y, f2(nz.y, nz.y));
+    }
+    return ex2v(expo_fold<MODEL>(d0, d1, na0, na1, P[h].LW, f2(zd[k], zd[k])));
+  };
+  constexpr bool FOLD = PHD_FOLD_D != 0;
 
   for (int cb = 0; cb < K; cb += kGateChunk) {
     const int cl = min(kGateChunk, K - cb);
@@ -868,7 +885,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
         const int ki = zi[pos];
         if (ki < 0) {  // sentinel
           zn[pos] = f2(-1e30f, -1e30f);
-          zd[pos] = 0.0f;
+          zd[pos] = FOLD ? INFINITY : 0.0f;
           if (RB) {
             zr[pos] = 0;
             zc[pos] = f2(0.0f, 0.0f);
@@ -879,7 +896,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
         const int l = g.cand[e0 + cb + ki];
         PHD_DCHECK(l >= 0 && l < g.M);
         zn[pos] = f2(g.sc.s0[l], g.sc.s1[l]);
-        zd[pos] = g.sc.d[l];
+        zd[pos] = FOLD ? log2f(g.sc.d[l]) / g.na0 : g.sc.d[l];  // fold: d = 0 -> +inf
         if (RB) {
           zr[pos] = g.sc.rep[l];
           zc[pos] = f2(g.sc.s2[l], g.sc.s3[l]);
@@ -925,8 +942,14 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
 #pragma unroll
             for (int h = 0; h < NPAIR; ++h) {
               float2 d0, d1;
-              const float2 u = term(kk, h, d0, d1);
-              pacc[h] = __ffma2_rn(u, f2(zd[kk], zd[kk]), pacc[h]);
+              float2 u;
+              if (FOLD) {
+                u = term_fold(kk, h, d0, d1);
+                pacc[h] = __fadd2_rn(pacc[h], u);
+              } else {
+                u = term(kk, h, d0, d1);
+                pacc[h] = __ffma2_rn(u, f2(zd[kk], zd[kk]), pacc[h]);
+              }
               if (RB) {
                 const float2 c = zc[kk];
                 d0 = __fadd2_rn(P[h].X, f2(c.x, c.x));  // x - centre_x
@@ -958,7 +981,10 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
 #pragma unroll
         for (int h = 0; h < NPAIR; ++h) {
           float2 d0, d1;
-          pacc[h] = __ffma2_rn(term(k, h, d0, d1), dk, pacc[h]);
+          if (FOLD)
+            pacc[h] = __fadd2_rn(pacc[h], term_fold(k, h, d0, d1));
+          else
+            pacc[h] = __ffma2_rn(term(k, h, d0, d1), dk, pacc[h]);
         }
       }
       __syncthreads();

@@ -16,7 +16,9 @@
 // fp32 partial per (particle, z-block).  Cross-CTA sums are fp64 in fixed order.
 #include "phd_internal.h"
 #include "pair_math.cuh"
+#include "bulk.cuh"
 
+#include <algorithm>
 #include <type_traits>
 
 #ifndef PHD_PP_UNROLL1
@@ -25,6 +27,7 @@
 #ifndef PHD_PP_UNROLL2
 #define PHD_PP_UNROLL2 4
 #endif
+
 // pass 1: evaluate exp2 of the last slot pair with the FFMA2 polynomial on every
 // PHD_EMU_PERIOD-th particle (0 = never); the rest go to MUFU.EX2
 #ifndef PHD_EMU_PERIOD
@@ -36,7 +39,9 @@ namespace phd {
 // particles unrolled per lane in the pair loop (pass 1 / pass 2; measured on B200)
 constexpr int kPPUnroll1 = PHD_PP_UNROLL1;
 constexpr int kPPUnroll2 = PHD_PP_UNROLL2;
+
 constexpr int kEmuPeriod = PHD_EMU_PERIOD;
+constexpr bool kFoldD = PHD_FOLD_D != 0;
 
 // 2^x for a pair on the FMA pipe (MUFU offload):
 // x = j + r with j = rint(x) by the 1.5*2^23 shifter, |r| <= 1/2, 2^r by a
@@ -59,7 +64,9 @@ __device__ __forceinline__ float2 ex2_poly(float2 x) {
             __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// Shared-memory particle record widths (floats, multiple of 4).
+// Particle records (floats, multiple of 4).  TileLoader (group-pipelined update) builds
+// them per pass in shared memory; the dense passes read the pass-2 layout, built once
+// per update in global memory by k_records, both passes.
 template <int MODEL, int PASS>
 struct RecLayout {
   static constexpr bool RB = MODEL == kRangeBearing;
@@ -69,6 +76,10 @@ struct RecLayout {
   static constexpr int V = RB ? 24 : 4;
   static constexpr int NV = RB ? (PASS == 1 ? 9 : 13) : (PASS == 1 ? 3 : 5);  // floats fetched per particle
 };
+template <int MODEL>
+using GRec = RecLayout<MODEL, 2>;  // the global record: (x,x,y,y | vx,vx,vy,vy | lw,lw,0,0) or the range-bearing 28
+
+constexpr int kPassStages = 2;  // record tiles in flight per CTA (bulk copies)
 
 template <int MODEL, int PASS>
 struct TileLoader {
@@ -137,10 +148,10 @@ struct TileLoader {
 };
 
 // Per-lane measurement constants for its NP slot pairs.
-template <int MODEL, int PASS, int NP>
+template <int MODEL, int PASS, int NP, bool FOLD = false>
 struct LaneZ {
   float2 n0[NP], n1[NP];  // -z components
-  float2 d[NP];           // 1/(kappa + C)   (pass 2)
+  float2 d[NP];           // pass 2: 1/(kappa + C), or with FOLD c = log2(1/(kappa + C)) / na0
   float2 c0[NP], c1[NP];  // -(Cartesian centre) (range-bearing, pass 2)
   int roff[NP];           // bearing-representation offset in the record (range-bearing)
 
@@ -150,7 +161,10 @@ struct LaneZ {
       int s = slot0 + 2 * j;
       n0[j] = f2(a.sc.s0[s], a.sc.s0[s + 1]);
       n1[j] = f2(a.sc.s1[s], a.sc.s1[s + 1]);
-      if (PASS == 2) d[j] = f2(a.sc.d[s], a.sc.d[s + 1]);
+      if (PASS == 2) {
+        d[j] = f2(a.sc.d[s], a.sc.d[s + 1]);
+        if (FOLD) d[j] = f2(log2f(d[j].x) / a.na0, log2f(d[j].y) / a.na0);  // d = 0: +inf
+      }
       if (MODEL == kRangeBearing) {
         roff[j] = 4 + 4 * a.sc.rep[s];
         if (PASS == 2) {
@@ -163,8 +177,8 @@ struct LaneZ {
 };
 
 // Residuals (d0, d1) of the lane's slot pair j against the broadcast particle.
-template <int MODEL, int PASS, int NP>
-__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS, NP>& z, int j, float2& d0,
+template <int MODEL, int PASS, int NP, bool FOLD>
+__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS, NP, FOLD>& z, int j, float2& d0,
                                          float2& d1) {
   if (MODEL == kRangeBearing) {
     float4 R = *reinterpret_cast<const float4*>(rec);
@@ -189,13 +203,15 @@ template <int MODEL, int PASS, int ZL>
 __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : PHD_PASS_MINB8) : 3)
     k_pass(const PassArgs a) {
   pdl_wait();
-  using L = RecLayout<MODEL, PASS>;
+  using L = GRec<MODEL>;
   constexpr int NQ = PASS == 1 ? 1 : 4;  // pass 2: S'x, Svx, S'y, Svy (dW = C/D from pass 1)
   constexpr int NP = ZL / 2;
-  extern __shared__ __align__(16) float smem[];
+  constexpr uint32_t kTileBytes = sizeof(float) * kTileP * L::WIDTH;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t mbar[kPassStages];
   const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, wz = nthr >> 5;
-  float* recs = smem;                                   // [2][kTileP][WIDTH]
-  float* psum = recs + 2 * kTileP * L::WIDTH;            // [2][wz][kTileP] (pass 2)
+  float* recs = smem;                                            // [kPassStages][kTileP][WIDTH]
+  float* psum = recs + kPassStages * kTileP * L::WIDTH;           // [2][wz][kTileP] (pass 2)
   // fp64 accumulators per lane slot in shared memory, [NQ*ZL][nthr] (conflict-free)
   double* out64 = reinterpret_cast<double*>(psum + (PASS == 2 ? 2 * wz * kTileP : 0));
 
@@ -208,7 +224,8 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
     // kJsZBlock | b: all slot pairs of the first b z-blocks (CTA-uniform), none elsewhere
     js = (v & kJsZBlock) ? (zb < (v & (kJsZBlock - 1)) ? NP : 0) : min(v, NP);
   }
-  LaneZ<MODEL, PASS, NP> z;
+  constexpr bool FOLD = PASS == 2 && kFoldD;
+  LaneZ<MODEL, PASS, NP, FOLD> z;
   z.load(a, slot0);
   const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
 
@@ -224,18 +241,30 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
   const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
   const int64_t t_end = min(t_begin + a.tiles_per_cta, ntiles);
 
-  TileLoader<MODEL, PASS> ld;
-  if (t_begin < t_end) {
-    ld.fetch(a, t_begin * kTileP, tid, nthr);
-    ld.store(recs, a.wscale, tid, nthr);
+  // record tiles stream into shared memory by bulk copies (one thread issues them), a
+  // tile of kTileP records per stage; the records of padding slots past n are zero with
+  // log2(p_D c w) = -inf, so every term of theirs is exactly 0
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kPassStages; ++s) mbar_init(&mbar[s], 1);
+    fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kPassStages; ++s)
+      if (t_begin + s < t_end) {
+        mbar_arrive_expect_tx(&mbar[s], kTileBytes);
+        bulk_g2s(recs + s * kTileP * L::WIDTH, a.rec + (t_begin + s) * kTileP * L::WIDTH, kTileBytes, &mbar[s]);
+      }
+  }
 
   for (int64_t t = t_begin; t < t_end; ++t) {
-    const int buf = (int)((t - t_begin) & 1);
-    const bool more = t + 1 < t_end;
-    if (more) ld.fetch(a, (t + 1) * kTileP, tid, nthr);
-    const float* rb = recs + buf * kTileP * L::WIDTH;
+    const int it = (int)(t - t_begin);
+    const int buf = it & 1;                   // psum double buffer
+    const int stage = it % kPassStages;
+    mbar_wait(&mbar[stage], (uint32_t)((it / kPassStages) & 1));
+    const float* rb = recs + stage * kTileP * L::WIDTH;
 
     // pass 2: state sums only in the first JS slot pairs of each lane, where the
     // index set I lives (uniform over the warp; one instance of the loop per JS)
@@ -249,11 +278,11 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
         const float* rec = rb + (p0 + pp) * L::WIDTH;
         // (log2(p_D c w), .) for both passes
         const float2 wv = *reinterpret_cast<const float2*>(rec + L::WC);
-        float2 pacc = f2(0.0f, 0.0f);
+        float2 pacc = f2(0.0f, 0.0f), pacc1 = f2(0.0f, 0.0f);
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
           float2 d0, d1;
-          residual<MODEL, PASS, NP>(rec, z, j, d0, d1);
+          residual<MODEL, PASS, NP, FOLD>(rec, z, j, d0, d1);
           if (PASS == 1) {
             // u = p_D g w = 2^(-alpha q + log2(p_D c w)), flushed to zero below 2^-126
             // exactly as in pass 2 (the same exponent bits; the polynomial-offloaded
@@ -261,6 +290,25 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
             const float2 e = expo<MODEL>(d0, d1, na0, na1, wv);
             const bool emu = kEmuPeriod > 0 && j == NP - 1 && pp % (kEmuPeriod > 0 ? kEmuPeriod : 1) == 0;
             in[0][j] = __fadd2_rn(in[0][j], emu ? ex2_poly(e) : ex2v(e));
+          } else if (FOLD) {
+            // u = p_D g w / (kappa + C_s): two interleaved FADD2 chains over the slot pairs
+            const float2 u = ex2v(expo_fold<MODEL>(d0, d1, na0, na1, wv, z.d[j]));
+            if (j == 0) pacc = u;
+            else if (j == 1) pacc1 = u;
+            else if (j & 1) pacc1 = __fadd2_rn(pacc1, u);
+            else pacc = __fadd2_rn(pacc, u);
+            if (j < JS && MODEL == kRangeBearing) {
+              const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
+              d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
+              d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
+            }
+            if (j < JS) {
+              const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+              in[0][j] = __ffma2_rn(u, d0, in[0][j]);
+              in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+              in[2][j] = __ffma2_rn(u, d1, in[2][j]);
+              in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+            }
           } else {
             const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
             pacc = __ffma2_rn(u, z.d[j], pacc);
@@ -278,6 +326,7 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
             }
           }
         }
+        if (FOLD && NP > 1) pacc = __fadd2_rn(pacc, pacc1);
         pe[pp] = pacc.x + pacc.y;
       }
       if (PASS == 2) {
@@ -292,7 +341,6 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
     else if (NP > 2 && js == 2) sweep(std::integral_constant<int, (NP > 2 ? 2 : 1)>{});
     else sweep(std::integral_constant<int, (NP > 3 ? 3 : 1)>{});
 
-    if (more) ld.store(recs + (buf ^ 1) * kTileP * L::WIDTH, a.wscale, tid, nthr);
     // tile sums (<= 64 particles in fp32) -> fp64; pass 2 only for the js slot
     // pairs that carry state sums (the F2F conversions share the XU pipe with EX2)
 #pragma unroll
@@ -305,6 +353,13 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
         in[q][j] = f2(0.0f, 0.0f);
       }
     __syncthreads();
+    // every thread is done with this stage's records: refill it with tile t + kPassStages
+    if (tid == 0 && t + kPassStages < t_end) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&mbar[stage], kTileBytes);
+      bulk_g2s(recs + stage * kTileP * L::WIDTH, a.rec + (t + kPassStages) * kTileP * L::WIDTH, kTileBytes,
+               &mbar[stage]);
+    }
 
     if (PASS == 2) {
       // per-particle partial over this CTA's slots: fixed-order sum over warps
@@ -328,8 +383,8 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
 
 template <int MODEL, int PASS, int ZL>
 static size_t pass_smem(int wz) {
-  using L = RecLayout<MODEL, PASS>;
-  size_t b = sizeof(float) * 2 * kTileP * L::WIDTH;
+  using L = GRec<MODEL>;
+  size_t b = sizeof(float) * kPassStages * kTileP * L::WIDTH;
   if (PASS == 2) b += sizeof(float) * 2 * wz * kTileP;
   b += sizeof(double) * (PASS == 1 ? 1 : 4) * ZL * wz * 32;
   return b;
@@ -358,6 +413,56 @@ static cudaError_t launch_z(int model, int pass, const PassArgs& a, int gp, int 
   if (model == kPosIso) return launch_m<kPosIso, ZL>(pass, a, gp, zb, wz, s);
   if (model == kPosAniso) return launch_m<kPosAniso, ZL>(pass, a, gp, zb, wz, s);
   return launch_m<kRangeBearing, ZL>(pass, a, gp, zb, wz, s);
+}
+
+bool pass2_sums_scaled() { return kFoldD; }
+
+// Per-particle records of the dense passes, once per update (HBM-bound: 20 B read,
+// 48 B written per particle; range-bearing 52 B read, 112 B written):
+// position (x,x,y,y | vx,vx,vy,vy | lw,lw,0,0), lw = log2(p_D c w_i), every operand a
+// native f32x2 pair; range-bearing (r hi,hi,lo,lo | three bearing representations
+// hi,hi,lo,lo | lw,lw,0,0 | x,x,y,y | vx,vx,vy,vy).  Slots [n, n_pad) get zero records
+// with lw = -inf (terms exactly 0).
+template <int MODEL>
+__global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad) {
+  pdl_wait();
+  using L = GRec<MODEL>;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
+    float4* d = reinterpret_cast<float4*>(a.rec + i * L::WIDTH);
+    const bool ok = i < a.n;
+    const float x = ok ? a.x[i] : 0.0f, y = ok ? a.y[i] : 0.0f;
+    const float vx = ok ? a.vx[i] : 0.0f, vy = ok ? a.vy[i] : 0.0f;
+    const float wc = ok ? log2f(a.w[i] * a.wscale) : -INFINITY;
+    if (MODEL == kRangeBearing) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float hi = ok ? a.rb[(2 * c) * a.rb_stride + i] : 0.0f;
+        const float lo = ok ? a.rb[(2 * c + 1) * a.rb_stride + i] : 0.0f;
+        d[c] = make_float4(hi, hi, lo, lo);
+      }
+      d[4] = make_float4(wc, wc, 0.0f, 0.0f);
+      d[5] = make_float4(x, x, y, y);
+      d[6] = make_float4(vx, vx, vy, vy);
+    } else {
+      d[0] = make_float4(x, x, y, y);
+      d[1] = make_float4(vx, vx, vy, vy);
+      d[2] = make_float4(wc, wc, 0.0f, 0.0f);
+    }
+  }
+}
+
+int record_width(int model) { return model == kRangeBearing ? GRec<kRangeBearing>::WIDTH : GRec<kPosIso>::WIDTH; }
+
+cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s) {
+  const int64_t n_pad = (a.n + kTileP - 1) / kTileP * kTileP;
+  if (n_pad <= 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<int64_t>((n_pad + 255) / 256, 148 * 8);
+  if (model == kRangeBearing)
+    pdl_launch(k_records<kRangeBearing>, grid, 256, 0, s, a, n_pad);
+  else
+    pdl_launch(k_records<kPosIso>, grid, 256, 0, s, a, n_pad);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s) {
@@ -458,7 +563,7 @@ __global__ void __launch_bounds__(256, 2) k_fused(const FusedArgs fa) {
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             float2 d0, d1;
-            residual<MODEL, 1, NP>(rec, z1, j, d0, d1);
+            residual(rec, z1, j, d0, d1);
             c1[j] = __fadd2_rn(c1[j], ex2v(expo<MODEL>(d0, d1, na0, na1, lw)));
           }
         }
@@ -467,7 +572,7 @@ __global__ void __launch_bounds__(256, 2) k_fused(const FusedArgs fa) {
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             float2 d0, d1;
-            residual<MODEL, 2, NP>(rec, z2, j, d0, d1);
+            residual(rec, z2, j, d0, d1);
             const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, lw));  // u = p_D g w
             pacc = __ffma2_rn(u, z2.d[j], pacc);
             if (MODEL == kRangeBearing) {
@@ -749,7 +854,8 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
                              const float* __restrict__ s1, const float* __restrict__ s2,
                              const float* __restrict__ s3, int model, const double* __restrict__ blk_w,
                              const double* __restrict__ blk_wp, int nb, double* acc_lab, double* rank_slots,
-                             int rank, int world, int lead, const int32_t* __restrict__ sel_flag) {
+                             int rank, int world, int lead, const int32_t* __restrict__ sel_flag,
+                             int sums_scaled) {
   pdl_wait();
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double sa[256], sb[256];
@@ -828,21 +934,23 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
     o[1] = o[2] = o[3] = o[4] = 0.0;
     return;
   }
+  // sums_scaled: the dense pass 2 folded 1/D into its terms (expo_fold)
+  const double sc = sums_scaled ? 1.0 : inv;
   o[0] = dW;
-  o[1] = A[0] * inv + cx * dW;
-  o[2] = A[1] * inv;
-  o[3] = A[2] * inv + cy * dW;
-  o[4] = A[3] * inv;
+  o[1] = A[0] * sc + cx * dW;
+  o[2] = A[1] * sc;
+  o[3] = A[2] * sc + cy * dW;
+  o[4] = A[3] * sc;
 }
 
 cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_slots, const int32_t* slot_label,
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1,
                               const float* s2, const float* s3, int model, const double* blk_w, const double* blk_wp,
                               int nb, double* acc_lab, double* rank_slots, int rank, int world, int lead,
-                              const int32_t* sel_flag, cudaStream_t s) {
+                              const int32_t* sel_flag, cudaStream_t s, int sums_scaled) {
   int blocks = (n_slots + 7) / 8 + 1;  // 8 slots (warps) per block + the rank-mass block
   pdl_launch(k_reduce_acc, blocks, 256, 0, s, Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
-                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead, sel_flag);
+                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead, sel_flag, sums_scaled);
   return cudaGetLastError();
 }
 

@@ -5,6 +5,12 @@
 #pragma once
 #include "phd_internal.h"
 
+// pass 2 (dense and gated) folds 1/D_s into the exponent (expo_fold); 0 = multiply by
+// d_s (A/B builds)
+#ifndef PHD_FOLD_D
+#define PHD_FOLD_D 1
+#endif
+
 namespace phd {
 
 __device__ __forceinline__ float ex2a(float x) {
@@ -26,6 +32,22 @@ __device__ __forceinline__ float2 expo(float2 d0, float2 d1, float2 na0, float2 
     return __ffma2_rn(q, na0, base);
   } else {
     float2 q = __ffma2_rn(__fmul2_rn(d0, d0), na0, base);
+    return __ffma2_rn(__fmul2_rn(d1, d1), na1, q);
+  }
+}
+
+// Pass-2 exponent with 1/D_s folded in (dense pass 2): c = log2(d_s)/na0
+// is added to the first squared residual, so 2^e = u d_s = p_D g w / (kappa + C_s) and
+// the per-particle weight sum needs one FADD2 instead of an FFMA2 (no d_s operand);
+// d_s = 0 (padding, D = 0) gives c = +inf and a term of exactly 0.
+template <int MODEL>
+__device__ __forceinline__ float2 expo_fold(float2 d0, float2 d1, float2 na0, float2 na1, float2 base, float2 c) {
+  if (MODEL == kPosIso) {
+    float2 q = __ffma2_rn(d0, d0, c);
+    q = __ffma2_rn(d1, d1, q);
+    return __ffma2_rn(q, na0, base);
+  } else {
+    float2 q = __ffma2_rn(__ffma2_rn(d0, d0, c), na0, base);
     return __ffma2_rn(__fmul2_rn(d1, d1), na1, q);
   }
 }

@@ -51,7 +51,7 @@ struct Layout {
   int64_t nbw_max = 0, nbo_max = 0;
   size_t total = 0;
   // byte offsets
-  size_t o_A[5], o_B[5], o_wn, o_rb, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_sel, o_selinfo, o_D,
+  size_t o_A[5], o_B[5], o_wn, o_rb, o_rec, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_sel, o_selinfo, o_D,
       o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_gather, o_ring, o_summ, o_bad;
   // gated update (p->gate != 0)
   int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
@@ -88,6 +88,9 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_wn = take(sizeof(float) * L.cap_l);
   L.o_rb = take(p->meas == PHD_MEAS_RANGE_BEARING ? sizeof(float) * 8 * L.cap_l : 256);
   L.o_P = take(sizeof(float) * (size_t)L.zb_max * L.cap_l);
+  // dense-pass particle records (k_records): [cap_l rounded up to kTileP][record_width]
+  L.o_rec = take(sizeof(float) * align_up((size_t)L.cap_l, kTileP) *
+                 (p->meas == PHD_MEAS_RANGE_BEARING ? 28 : 12));
   L.o_Cpart = take(sizeof(double) * L.part_cap);
   L.o_Apart = take(sizeof(double) * 4 * L.part_cap);
   L.o_zlab = take(sizeof(float) * 2 * (size_t)(p->max_meas + 1));
@@ -168,6 +171,7 @@ struct phd_ctx {
   float* wn;
   float* rb;
   float* P;
+  float* rec;
   double *Cpart, *Apart;
   float *zlab, *zprev;
   int32_t* slot_label;
@@ -509,6 +513,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->wn = at<float>(c->ws, L.o_wn);
   c->rb = p->meas == PHD_MEAS_RANGE_BEARING ? at<float>(c->ws, L.o_rb) : nullptr;
   c->P = at<float>(c->ws, L.o_P);
+  c->rec = at<float>(c->ws, L.o_rec);
   c->Cpart = at<double>(c->ws, L.o_Cpart);
   c->Apart = at<double>(c->ws, L.o_Apart);
   c->zlab = at<float>(c->ws, L.o_zlab);
@@ -1180,6 +1185,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   pa.Apart = c->Apart;
   pa.P = c->P;
   pa.P_stride = c->L.cap_l;
+  pa.rec = c->rec;
   c->select = M > 0 && !c->fused && c->p.stphd_all == 0;
   pa.js = nullptr;
   // C of slots [s0, s1): fixed-order reduction, C1 all-reduce, per-slot constants
@@ -1252,6 +1258,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     }
     timing_record(c, 6);
   } else if (M > 0) {
+    if (gp > 0) KL(launch_records(c->model, pa, c->st));
     timing_record(c, 3);
     if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 4);
@@ -1294,7 +1301,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   double* rank_slots = c->acc + 5 * (size_t)M;
   KL(launch_reduce_acc(gated ? c->gA : c->Apart, gated ? 1 : gp, c->slots_pad, M > 0 ? c->slots_pad : 0, c->slot_label, c->C, c->D, c->s[0],
                        c->s[1], c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank,
-                       c->world, c->dcp || c->rank == 0 ? 1 : 0, c->select ? c->sel_flag : nullptr, c->st));
+                       c->world, c->dcp || c->rank == 0 ? 1 : 0, c->select ? c->sel_flag : nullptr, c->st,
+                       !c->fused && pass2_sums_scaled() ? 1 : 0));
   // rank slots [W_r | W_pred_r | N_r] (3 per rank); N_r written from the host
   c->h_meta[3 * c->world + 16] = (double)n;
   CU(cudaMemcpyAsync(rank_slots + 2 * c->world + c->rank, c->h_meta + 3 * c->world + 16, sizeof(double),

@@ -108,6 +108,7 @@ struct PassArgs {
   float* P;                  // [zb][P_stride]
   int64_t P_stride;
   const int32_t* js;         // pass 2: state sums for the first *js slot pairs of every lane (nullptr: all)
+  float* rec;                // per-particle records of the dense passes [n_pad][record_width] (k_records)
 };
 
 struct PredictArgs {
@@ -190,6 +191,11 @@ cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, 
 cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad,
                          float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s, int* bad = nullptr);
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
+// the dense pass 2 folds 1/D into its terms: its state-sum partials already carry 1/D
+bool pass2_sums_scaled();
+// floats per particle record of the dense passes; build them (once per update, before pass 1)
+int record_width(int model);
+cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s);
 int pass_occupancy(int model, int pass, int wz, int zl);
 cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,
                          int zbg, int wz, cudaStream_t s);
@@ -236,7 +242,7 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1, const float* s2,
                               const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
                               double* acc_lab, double* rank_slots, int rank, int world, int lead,
-                              const int32_t* sel_flag, cudaStream_t s);
+                              const int32_t* sel_flag, cudaStream_t s, int sums_scaled = 0);
 // W = sum_{r < count} W[r], W_pred = sum Wp[r]; writes the estimates to est[0..)
 // and their count to *count_out (the header entry of the gather block).
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,

@@ -126,10 +126,14 @@ def test_p_invariance(phd, cname, world, gate, xch, monkeypatch):
             same = e1["labels"] == ep["labels"]
             assert np.mean(same) >= 0.99
             assert np.all(np.abs(e1["states"][same] - ep["states"][same]) <= 1e-3)
-            # ancestors: equal except thresholds within rounding of a cumsum boundary
-            assert np.mean(a1 != ap) <= 1e-4, int(np.sum(a1 != ap))
+            # ancestors: equal except thresholds within rounding of a cumsum boundary.  The
+            # rank partition changes C in its last fp64 bits; 1/D rounds to a neighbouring
+            # fp32 now and then, and pass 2 folds log2(1/D) into the exponent,
+            # where one ulp of the folded constant moves a slot's terms by <= 1e-6 relative:
+            # offspring boundaries that close to a threshold may go to the neighbour
+            assert np.mean(a1 != ap) <= 4e-4, int(np.sum(a1 != ap))
             same_pop = np.all(p1[0] == pp[0], axis=0)
-            assert np.mean(same_pop) >= 1.0 - 1e-4
+            assert np.mean(same_pop) >= 1.0 - 4e-4
             identical_so_far = bool(np.all(a1 == ap))
         else:
             # a near-tie changed an ancestor earlier: the filters stay statistically equal
