@@ -148,7 +148,7 @@ struct TileLoader {
 };
 
 // Per-lane measurement constants for its NP slot pairs.
-template <int MODEL, int PASS, int NP, bool FOLD = false>
+template <int MODEL, int PASS, int NP, bool FOLD = false, int JS = NP>
 struct LaneZ {
   float2 n0[NP], n1[NP];  // -z components
   float2 d[NP];           // pass 2: 1/(kappa + C), or with FOLD c = log2(1/(kappa + C)) / na0
@@ -167,7 +167,7 @@ struct LaneZ {
       }
       if (MODEL == kRangeBearing) {
         roff[j] = 4 + 4 * a.sc.rep[s];
-        if (PASS == 2) {
+        if (PASS == 2 && j < JS) {  // the centres are used by the state sums only
           c0[j] = f2(a.sc.s2[s], a.sc.s2[s + 1]);
           c1[j] = f2(a.sc.s3[s], a.sc.s3[s + 1]);
         }
@@ -177,9 +177,9 @@ struct LaneZ {
 };
 
 // Residuals (d0, d1) of the lane's slot pair j against the broadcast particle.
-template <int MODEL, int PASS, int NP, bool FOLD>
-__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS, NP, FOLD>& z, int j, float2& d0,
-                                         float2& d1) {
+template <int MODEL, int PASS, int NP, bool FOLD, int JS>
+__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS, NP, FOLD, JS>& z, int j,
+                                         float2& d0, float2& d1) {
   if (MODEL == kRangeBearing) {
     float4 R = *reinterpret_cast<const float4*>(rec);
     float4 T = *reinterpret_cast<const float4*>(rec + z.roff[j]);
@@ -224,161 +224,164 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
     // kJsZBlock | b: all slot pairs of the first b z-blocks (CTA-uniform), none elsewhere
     js = (v & kJsZBlock) ? (zb < (v & (kJsZBlock - 1)) ? NP : 0) : min(v, NP);
   }
-  constexpr bool FOLD = PASS == 2 && kFoldD;
-  LaneZ<MODEL, PASS, NP, FOLD> z;
-  z.load(a, slot0);
-  const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
+  // one instance of the whole sweep per JS (pass 2: state sums for the first JS slot pairs
+  // of every lane, where the index set I lives), so that each instance holds only the
+  // per-lane constants it uses
+  auto run = [&](auto js_tag) {
+    constexpr int JS = decltype(js_tag)::value;
+    constexpr bool FOLD = PASS == 2 && kFoldD;
+    LaneZ<MODEL, PASS, NP, FOLD, JS> z;
+    z.load(a, slot0);
+    const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
 
-  float2 in[NQ][NP];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q)
-#pragma unroll
-    for (int j = 0; j < NP; ++j) in[q][j] = f2(0.0f, 0.0f);
-#pragma unroll
-  for (int q = 0; q < NQ * ZL; ++q) out64[q * nthr + tid] = 0.0;
+    float2 in[NQ][NP];
+  #pragma unroll
+    for (int q = 0; q < NQ; ++q)
+  #pragma unroll
+      for (int j = 0; j < NP; ++j) in[q][j] = f2(0.0f, 0.0f);
+  #pragma unroll
+    for (int q = 0; q < NQ * ZL; ++q) out64[q * nthr + tid] = 0.0;
 
-  const int64_t ntiles = (a.n + kTileP - 1) / kTileP;
-  const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
-  const int64_t t_end = min(t_begin + a.tiles_per_cta, ntiles);
+    const int64_t ntiles = (a.n + kTileP - 1) / kTileP;
+    const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
+    const int64_t t_end = min(t_begin + a.tiles_per_cta, ntiles);
 
-  // record tiles stream into shared memory by bulk copies (one thread issues them), a
-  // tile of kTileP records per stage; the records of padding slots past n are zero with
-  // log2(p_D c w) = -inf, so every term of theirs is exactly 0
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < kPassStages; ++s) mbar_init(&mbar[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < kPassStages; ++s)
-      if (t_begin + s < t_end) {
-        mbar_arrive_expect_tx(&mbar[s], kTileBytes);
-        bulk_g2s(recs + s * kTileP * L::WIDTH, a.rec + (t_begin + s) * kTileP * L::WIDTH, kTileBytes, &mbar[s]);
-      }
-  }
+    // record tiles stream into shared memory by bulk copies (one thread issues them), a
+    // tile of kTileP records per stage; the records of padding slots past n are zero with
+    // log2(p_D c w) = -inf, so every term of theirs is exactly 0
+    if (tid == 0) {
+  #pragma unroll
+      for (int s = 0; s < kPassStages; ++s) mbar_init(&mbar[s], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+  #pragma unroll
+      for (int s = 0; s < kPassStages; ++s)
+        if (t_begin + s < t_end) {
+          mbar_arrive_expect_tx(&mbar[s], kTileBytes);
+          bulk_g2s(recs + s * kTileP * L::WIDTH, a.rec + (t_begin + s) * kTileP * L::WIDTH, kTileBytes, &mbar[s]);
+        }
+    }
 
-  for (int64_t t = t_begin; t < t_end; ++t) {
-    const int it = (int)(t - t_begin);
-    const int buf = it & 1;                   // psum double buffer
-    const int stage = it % kPassStages;
-    mbar_wait(&mbar[stage], (uint32_t)((it / kPassStages) & 1));
-    const float* rb = recs + stage * kTileP * L::WIDTH;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int it = (int)(t - t_begin);
+      const int buf = it & 1;                   // psum double buffer
+      const int stage = it % kPassStages;
+      mbar_wait(&mbar[stage], (uint32_t)((it / kPassStages) & 1));
+      const float* rb = recs + stage * kTileP * L::WIDTH;
 
-    // pass 2: state sums only in the first JS slot pairs of each lane, where the
-    // index set I lives (uniform over the warp; one instance of the loop per JS)
-    auto sweep = [&](auto js_tag) {
-      constexpr int JS = decltype(js_tag)::value;
-#pragma unroll 1
-    for (int p0 = 0; p0 < kTileP; p0 += 8) {
-      float pe[8];
-#pragma unroll(PASS == 1 ? kPPUnroll1 : kPPUnroll2)
-      for (int pp = 0; pp < 8; ++pp) {
-        const float* rec = rb + (p0 + pp) * L::WIDTH;
-        // (log2(p_D c w), .) for both passes
-        const float2 wv = *reinterpret_cast<const float2*>(rec + L::WC);
-        float2 pacc = f2(0.0f, 0.0f), pacc1 = f2(0.0f, 0.0f);
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          float2 d0, d1;
-          residual<MODEL, PASS, NP, FOLD>(rec, z, j, d0, d1);
-          if (PASS == 1) {
-            // u = p_D g w = 2^(-alpha q + log2(p_D c w)), flushed to zero below 2^-126
-            // exactly as in pass 2 (the same exponent bits; the polynomial-offloaded
-            // terms differ from MUFU.EX2 by <= 3.2e-7 relative)
-            const float2 e = expo<MODEL>(d0, d1, na0, na1, wv);
-            const bool emu = kEmuPeriod > 0 && j == NP - 1 && pp % (kEmuPeriod > 0 ? kEmuPeriod : 1) == 0;
-            in[0][j] = __fadd2_rn(in[0][j], emu ? ex2_poly(e) : ex2v(e));
-          } else if (FOLD) {
-            // u = p_D g w / (kappa + C_s): two interleaved FADD2 chains over the slot pairs
-            const float2 u = ex2v(expo_fold<MODEL>(d0, d1, na0, na1, wv, z.d[j]));
-            if (j == 0) pacc = u;
-            else if (j == 1) pacc1 = u;
-            else if (j & 1) pacc1 = __fadd2_rn(pacc1, u);
-            else pacc = __fadd2_rn(pacc, u);
-            if (j < JS && MODEL == kRangeBearing) {
-              const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
-              d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
-              d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
-            }
-            if (j < JS) {
-              const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
-              in[0][j] = __ffma2_rn(u, d0, in[0][j]);
-              in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
-              in[2][j] = __ffma2_rn(u, d1, in[2][j]);
-              in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
-            }
-          } else {
-            const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
-            pacc = __ffma2_rn(u, z.d[j], pacc);
-            if (j < JS && MODEL == kRangeBearing) {
-              const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
-              d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
-              d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
-            }
-            if (j < JS) {
-              const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
-              in[0][j] = __ffma2_rn(u, d0, in[0][j]);
-              in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
-              in[2][j] = __ffma2_rn(u, d1, in[2][j]);
-              in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+      // pass 2: state sums only in the first JS slot pairs of each lane, where the
+      // index set I lives (uniform over the warp; one instance of the loop per JS)
+  #pragma unroll 1
+      for (int p0 = 0; p0 < kTileP; p0 += 8) {
+        float pe[8];
+  #pragma unroll(PASS == 1 ? kPPUnroll1 : kPPUnroll2)
+        for (int pp = 0; pp < 8; ++pp) {
+          const float* rec = rb + (p0 + pp) * L::WIDTH;
+          // (log2(p_D c w), .) for both passes
+          const float2 wv = *reinterpret_cast<const float2*>(rec + L::WC);
+          float2 pacc = f2(0.0f, 0.0f), pacc1 = f2(0.0f, 0.0f);
+  #pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            float2 d0, d1;
+            residual(rec, z, j, d0, d1);
+            if (PASS == 1) {
+              // u = p_D g w = 2^(-alpha q + log2(p_D c w)), flushed to zero below 2^-126
+              // exactly as in pass 2 (the same exponent bits; the polynomial-offloaded
+              // terms differ from MUFU.EX2 by <= 3.2e-7 relative)
+              const float2 e = expo<MODEL>(d0, d1, na0, na1, wv);
+              const bool emu = kEmuPeriod > 0 && j == NP - 1 && pp % (kEmuPeriod > 0 ? kEmuPeriod : 1) == 0;
+              in[0][j] = __fadd2_rn(in[0][j], emu ? ex2_poly(e) : ex2v(e));
+            } else if (FOLD) {
+              // u = p_D g w / (kappa + C_s): two interleaved FADD2 chains over the slot pairs
+              const float2 u = ex2v(expo_fold<MODEL>(d0, d1, na0, na1, wv, z.d[j]));
+              if (j == 0) pacc = u;
+              else if (j == 1) pacc1 = u;
+              else if (j & 1) pacc1 = __fadd2_rn(pacc1, u);
+              else pacc = __fadd2_rn(pacc, u);
+              if (j < JS && MODEL == kRangeBearing) {
+                const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
+                d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
+                d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
+              }
+              if (j < JS) {
+                const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+                in[0][j] = __ffma2_rn(u, d0, in[0][j]);
+                in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+                in[2][j] = __ffma2_rn(u, d1, in[2][j]);
+                in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+              }
+            } else {
+              const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
+              pacc = __ffma2_rn(u, z.d[j], pacc);
+              if (j < JS && MODEL == kRangeBearing) {
+                const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
+                d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
+                d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
+              }
+              if (j < JS) {
+                const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+                in[0][j] = __ffma2_rn(u, d0, in[0][j]);
+                in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+                in[2][j] = __ffma2_rn(u, d1, in[2][j]);
+                in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+              }
             }
           }
+          if (FOLD && NP > 1) pacc = __fadd2_rn(pacc, pacc1);
+          pe[pp] = pacc.x + pacc.y;
         }
-        if (FOLD && NP > 1) pacc = __fadd2_rn(pacc, pacc1);
-        pe[pp] = pacc.x + pacc.y;
+        if (PASS == 2) {
+          float s = transpose_reduce8(pe, lane);
+          if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = s;
+        }
       }
+
+      // tile sums (<= 64 particles in fp32) -> fp64; pass 2 only for the js slot
+      // pairs that carry state sums (the F2F conversions share the XU pipe with EX2)
+  #pragma unroll
+      for (int q = 0; q < NQ; ++q)
+  #pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          if (PASS == 2 && j >= js) continue;
+          out64[(q * ZL + 2 * j) * nthr + tid] += (double)in[q][j].x;
+          out64[(q * ZL + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
+          in[q][j] = f2(0.0f, 0.0f);
+        }
+      __syncthreads();
+      // every thread is done with this stage's records: refill it with tile t + kPassStages
+      if (tid == 0 && t + kPassStages < t_end) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&mbar[stage], kTileBytes);
+        bulk_g2s(recs + stage * kTileP * L::WIDTH, a.rec + (t + kPassStages) * kTileP * L::WIDTH, kTileBytes,
+                 &mbar[stage]);
+      }
+
       if (PASS == 2) {
-        float s = transpose_reduce8(pe, lane);
-        if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = s;
-      }
-    }
-    };
-    if (PASS == 1 || js >= NP) sweep(std::integral_constant<int, NP>{});
-    else if (js == 0) sweep(std::integral_constant<int, 0>{});
-    else if (js == 1) sweep(std::integral_constant<int, 1>{});
-    else if (NP > 2 && js == 2) sweep(std::integral_constant<int, (NP > 2 ? 2 : 1)>{});
-    else sweep(std::integral_constant<int, (NP > 3 ? 3 : 1)>{});
-
-    // tile sums (<= 64 particles in fp32) -> fp64; pass 2 only for the js slot
-    // pairs that carry state sums (the F2F conversions share the XU pipe with EX2)
-#pragma unroll
-    for (int q = 0; q < NQ; ++q)
-#pragma unroll
-      for (int j = 0; j < NP; ++j) {
-        if (PASS == 2 && j >= js) continue;
-        out64[(q * ZL + 2 * j) * nthr + tid] += (double)in[q][j].x;
-        out64[(q * ZL + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
-        in[q][j] = f2(0.0f, 0.0f);
-      }
-    __syncthreads();
-    // every thread is done with this stage's records: refill it with tile t + kPassStages
-    if (tid == 0 && t + kPassStages < t_end) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&mbar[stage], kTileBytes);
-      bulk_g2s(recs + stage * kTileP * L::WIDTH, a.rec + (t + kPassStages) * kTileP * L::WIDTH, kTileBytes,
-               &mbar[stage]);
-    }
-
-    if (PASS == 2) {
-      // per-particle partial over this CTA's slots: fixed-order sum over warps
-      for (int p = tid; p < kTileP; p += nthr) {
-        int64_t i = t * kTileP + p;
-        if (i < a.n) {
-          float s = 0.0f;
-          for (int w2 = 0; w2 < wz; ++w2) s += psum[(buf * wz + w2) * kTileP + p];
-          a.P[(int64_t)zb * a.P_stride + i] = s;
+        // per-particle partial over this CTA's slots: fixed-order sum over warps
+        for (int p = tid; p < kTileP; p += nthr) {
+          int64_t i = t * kTileP + p;
+          if (i < a.n) {
+            float s = 0.0f;
+            for (int w2 = 0; w2 < wz; ++w2) s += psum[(buf * wz + w2) * kTileP + p];
+            a.P[(int64_t)zb * a.P_stride + i] = s;
+          }
         }
       }
     }
-  }
-  const int64_t base = (int64_t)blockIdx.x * NQ * a.slots_pad;
-  double* dst = PASS == 1 ? a.Cpart : a.Apart;
-#pragma unroll
-  for (int q = 0; q < NQ; ++q)
-#pragma unroll
-    for (int m = 0; m < ZL; ++m) dst[base + (int64_t)q * a.slots_pad + slot0 + m] = out64[(q * ZL + m) * nthr + tid];
+    const int64_t base = (int64_t)blockIdx.x * NQ * a.slots_pad;
+    double* dst = PASS == 1 ? a.Cpart : a.Apart;
+  #pragma unroll
+    for (int q = 0; q < NQ; ++q)
+  #pragma unroll
+      for (int m = 0; m < ZL; ++m) dst[base + (int64_t)q * a.slots_pad + slot0 + m] = out64[(q * ZL + m) * nthr + tid];
+  };
+  if (PASS == 1 || js >= NP) run(std::integral_constant<int, NP>{});
+  else if (js == 0) run(std::integral_constant<int, 0>{});
+  else if (js == 1) run(std::integral_constant<int, 1>{});
+  else if (NP > 2 && js == 2) run(std::integral_constant<int, (NP > 2 ? 2 : 1)>{});
+  else run(std::integral_constant<int, (NP > 3 ? 3 : 1)>{});
 }
 
 template <int MODEL, int PASS, int ZL>
