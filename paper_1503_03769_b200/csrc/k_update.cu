@@ -25,7 +25,7 @@
 #define PHD_PP_UNROLL1 8
 #endif
 #ifndef PHD_PP_UNROLL2
-#define PHD_PP_UNROLL2 4
+#define PHD_PP_UNROLL2 8
 #endif
 
 // pass 1: evaluate exp2 of the last slot pair with the FFMA2 polynomial on every
