@@ -508,7 +508,7 @@ def run_ours(args):
     n_surv_loc = max(0, min(hi, n0) - min(lo, n0))
     rb_bytes = 32 if m.meas == 1 else 0
     b_pred = n_surv_loc * (40 + rb_bytes) + (n_loc - n_surv_loc) * (20 + rb_bytes)
-    b_res = n_loc * 4 + n0 // world * 48
+    b_res = n_loc * 20 + n0 // world * 24
     t_pred = statistics.mean(pass_ms["predict"])
     t_res = statistics.mean(pass_ms["resample"])
     hbm = {"peak_gbs": hbm_peak, "peak_basis": peak_src,
@@ -516,8 +516,8 @@ def run_ours(args):
                        "basis": "survivor 40 B (state + w read and written), birth 20 B written%s" %
                                 (", + 32 B range-bearing representation" if rb_bytes else "")},
            "resample": {"bytes": b_res, "ms": t_res, "gbs": b_res / (t_res * 1e6), "frac": b_res / (t_res * 1e6) / hbm_peak,
-                        "basis": "w read 4 B per particle; per offspring: mark 4+4, ancestor state 16 read, "
-                                 "state + w 20 written, ancestor index 4 (all resampling kernels incl. scans)"}}
+                        "basis": "per particle w + state read (20 B); per offspring state + w written (20 B) and the "
+                                 "ancestor index (4 B); k_scan_chunks + k_resample_gather (both kernels)"}}
     cpu = None
     cpu_all = None
     if not args.no_cpu_baseline and world == 1:  # the contract's CPU baseline: rank 0 at N = 1 only

@@ -122,6 +122,67 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(const double* __restrict__
   if (threadIdx.x == 0) off[nb] = tot;
 }
 
+// Multi-CTA exclusive scan of the block masses, deterministic: CTA c scans its chunk of
+// kResScanChunk (warp shuffles, then the warp totals: a fixed tree), writes the local
+// exclusive prefixes and its chunk total; the last CTA to finish (atomic ticket) adds the
+// chunk totals in order.  Readers form off(b) = coff[b / kResScanChunk] + loc[b].
+__global__ void __launch_bounds__(1024) k_scan_chunks(const double* __restrict__ blk, int nb, double* loc,
+                                                      double* ctot, double* coff, unsigned* counter) {
+  pdl_wait();
+  __shared__ double ws[33];
+  __shared__ bool last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i = blockIdx.x * kResScanChunk + tid;
+  const double v = i < nb ? blk[i] : 0.0;
+  double incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    double x = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const double prev = __shfl_up_sync(0xffffffffu, x, 1);
+    ws[lane] = lane > 0 ? prev : 0.0;
+    if (lane == 31) ws[32] = x;
+  }
+  __syncthreads();
+  const double prevl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (i < nb) loc[i] = lane > 0 ? ws[warp] + prevl : ws[warp];
+  if (tid == 0) {
+    ctot[blockIdx.x] = ws[32];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && tid == 0) {
+    __threadfence();
+    double acc = 0.0;
+    for (unsigned c = 0; c < gridDim.x; ++c) {
+      const double t = __ldcg(ctot + c);
+      coff[c] = acc;
+      acc += t;
+    }
+    coff[gridDim.x] = acc;
+    *counter = 0u;  // ready for the next scan
+  }
+}
+
+cudaError_t launch_scan_chunks(const double* blk, int nb, double* loc, double* ctot, double* coff, unsigned* counter,
+                               cudaStream_t s) {
+  if (nb <= 0) return cudaSuccess;
+  pdl_launch(k_scan_chunks, (unsigned)((nb + kResScanChunk - 1) / kResScanChunk), kResScanChunk, 0, s, blk, nb, loc, ctot, coff,
+             counter);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s) {
   pdl_launch(k_scan_blocks, 1, 1024, 0, s, blk, nb, blk_off);
   return cudaGetLastError();
@@ -236,6 +297,133 @@ cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s) {
   if (a.n_local <= 0) return cudaSuccess;
   unsigned nb = (unsigned)((a.n_local + kBlockW - 1) / kBlockW);
   pdl_launch(k_resample_mark, nb, kMT, 0, s, a);
+  return cudaGetLastError();
+}
+
+// Systematic resampling and the offspring gather in one pass: per block
+// of kBlockW particles the bounds of k_resample_mark (same fp64 formula and pinning),
+// all kBlockW upper bounds in shared memory; then every offspring k of the block finds
+// its particle by binary search over those bounds (balanced whatever the weights) and
+// copies its state (coalesced writes at consecutive produced indices).  Reads w + state
+// (20 B) per particle, writes state + w + ancestor (24 B) per offspring; no marks, no
+// memsets, no max-scan.
+template <bool P2P>
+__global__ void __launch_bounds__(kMT) k_resample_gather(const ResampleGatherArgs g, const PeerOut po) {
+  pdl_wait();
+  const ResampleArgs& a = g.r;
+  __shared__ double wsum[kMT / 32];
+  __shared__ int wmax[kMT / 32];
+  __shared__ int hb[kBlockW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b = blockIdx.x;
+  const int64_t base = b * kBlockW;
+  const int64_t nb = (a.n_local + kBlockW - 1) / kBlockW;
+  double w4[kMP];
+  if (base + kMP * tid + kMP - 1 < a.n_local) {
+#pragma unroll
+    for (int v = 0; v < kMP / 4; ++v) {
+      const float4 q = *reinterpret_cast<const float4*>(a.w + base + kMP * tid + 4 * v);
+      w4[4 * v + 0] = (double)q.x;
+      w4[4 * v + 1] = (double)q.y;
+      w4[4 * v + 2] = (double)q.z;
+      w4[4 * v + 3] = (double)q.w;
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < kMP; ++m) {
+      const int64_t i = base + kMP * tid + m;
+      w4[m] = i < a.n_local ? (double)a.w[i] : 0.0;
+    }
+  }
+  double tsum = 0.0;
+#pragma unroll
+  for (int m = 0; m < kMP; ++m) tsum += w4[m];
+  double incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  double wpre = 0.0;
+  for (int k = 0; k < warp; ++k) wpre += wsum[k];
+  const double excl = wpre + (incl - tsum);
+  // block bounds from off(b) = coff[b / kResScanChunk] + loc[b] (every reader forms the same bits)
+  auto off = [&](int64_t bb) { return g.coff[bb / kResScanChunk] + a.blk_off[bb]; };
+  const double Eb = a.O_r + off(b);
+  const int64_t nEb = (b == 0) ? a.lo : n_of(Eb, a.scale, a.U, a.lo, a.hi);
+  const int64_t nEb1 = (b == nb - 1) ? a.hi : n_of(a.O_r + off(b + 1), a.scale, a.U, a.lo, a.hi);
+  double L = excl;
+  int run = 0;
+  int h[kMP];
+#pragma unroll
+  for (int m = 0; m < kMP; ++m) {
+    const int k = kMP * tid + m;
+    const int64_t i = base + k;
+    L += w4[m];
+    int64_t hi;
+    if (i >= a.n_local - 1 || k == kBlockW - 1) hi = nEb1;
+    else hi = n_of(Eb + L, a.scale, a.U, nEb, nEb1);
+    run = max(run, (int)(hi - nEb));
+    h[m] = run;
+  }
+  int incl_m = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl_m, o);
+    if (lane >= o) incl_m = max(incl_m, v);
+  }
+  if (lane == 31) wmax[warp] = incl_m;
+  __syncthreads();
+  int carry = 0;
+  for (int k = 0; k < warp; ++k) carry = max(carry, wmax[k]);
+  const int prev = __shfl_up_sync(0xffffffffu, incl_m, 1);
+  if (lane > 0) carry = max(carry, prev);
+#pragma unroll
+  for (int m = 0; m < kMP; ++m) hb[kMP * tid + m] = max(h[m], carry);
+  __syncthreads();
+  // offspring [0, end) of this block: produced indices pbase + k
+  const int end = (int)(nEb1 - nEb);
+  const int64_t pbase = nEb - a.lo;
+  int q = 0;
+  for (int k = tid; k < end; k += kMT) {
+    int pos = 0;  // number of particles whose upper bound is <= k: the ancestor
+#pragma unroll
+    for (int step = kBlockW / 2; step > 0; step >>= 1)
+      if (hb[pos + step - 1] <= k) pos += step;
+    PHD_DCHECK(pos < kBlockW && base + pos < a.n_local);
+    const int64_t l = base + pos;
+    const int64_t j = pbase + k;
+    const float X = g.x[l], VX = g.vx[l], Y = g.y[l], VY = g.vy[l];
+    if (P2P) {
+      const int64_t gj = a.lo + j;  // global offspring index -> owner of the next step's block
+      while (q + 1 < po.world && po.blo[q + 1] <= gj) ++q;
+      const int64_t o = gj - po.blo[q];
+      po.dst[q][0][o] = X;
+      po.dst[q][1][o] = VX;
+      po.dst[q][2][o] = Y;
+      po.dst[q][3][o] = VY;
+      po.dst[q][4][o] = g.w_off;
+    } else {
+      g.ox[j] = X;
+      g.ovx[j] = VX;
+      g.oy[j] = Y;
+      g.ovy[j] = VY;
+      g.ow[j] = g.w_off;
+    }
+    g.anc[j] = (int32_t)(a.g0 + l);
+  }
+  if (P2P) __threadfence_system();
+}
+
+cudaError_t launch_resample_gather(const ResampleGatherArgs& a, const PeerOut* po, cudaStream_t s) {
+  if (a.r.n_local <= 0) return cudaSuccess;
+  const unsigned nb = (unsigned)((a.r.n_local + kBlockW - 1) / kBlockW);
+  if (po)
+    pdl_launch(k_resample_gather<true>, nb, kMT, 0, s, a, *po);
+  else
+    pdl_launch(k_resample_gather<false>, nb, kMT, 0, s, a, PeerOut{});
   return cudaGetLastError();
 }
 

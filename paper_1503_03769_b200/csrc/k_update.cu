@@ -64,88 +64,22 @@ __device__ __forceinline__ float2 ex2_poly(float2 x) {
             __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// Particle records (floats, multiple of 4).  TileLoader (group-pipelined update) builds
-// them per pass in shared memory; the dense passes read the pass-2 layout, built once
-// per update in global memory by k_records, both passes.
-template <int MODEL, int PASS>
-struct RecLayout {
-  static constexpr bool RB = MODEL == kRangeBearing;
-  static constexpr int WIDTH = RB ? (PASS == 1 ? 20 : 28) : (PASS == 1 ? 8 : 12);
-  static constexpr int WC = RB ? 16 : (PASS == 1 ? 4 : 8);
-  static constexpr int XY = RB ? 20 : 0;
-  static constexpr int V = RB ? 24 : 4;
-  static constexpr int NV = RB ? (PASS == 1 ? 9 : 13) : (PASS == 1 ? 3 : 5);  // floats fetched per particle
-};
+// Particle records of the dense passes (floats, multiple of 4), built once per update
+// in global memory by k_records and streamed into shared memory by bulk copies.  Scalars,
+// read as broadcast f32x2 operands (FADD2 Rd, Ra.F32, Rb.F32x2):
+//   position (8):        x, y, lw, 0 | vx, vy, 0, 0
+//   range-bearing (16):  r_hi, r_lo, lw, 0 | thA hi, lo, thB hi, lo | thC hi, lo, x, y | vx, vy, 0, 0
+// with lw = log2(p_D c w); the bearing representation c of a slot pair sits at 4 + 2c.
 template <int MODEL>
-using GRec = RecLayout<MODEL, 2>;  // the global record: (x,x,y,y | vx,vx,vy,vy | lw,lw,0,0) or the range-bearing 28
+struct GRec {
+  static constexpr bool RB = MODEL == kRangeBearing;
+  static constexpr int WIDTH = RB ? 16 : 8;
+  static constexpr int LW = 2;
+  static constexpr int XY = RB ? 10 : 0;
+  static constexpr int V = RB ? 12 : 4;
+};
 
 constexpr int kPassStages = 2;  // record tiles in flight per CTA (bulk copies)
-
-template <int MODEL, int PASS>
-struct TileLoader {
-  using L = RecLayout<MODEL, PASS>;
-  // one particle per loader thread: the CTA has >= kTileP threads (wz >= 2)
-  float v[1][L::NV];
-
-  __device__ __forceinline__ void fetch(const PassArgs& a, int64_t tile_base, int tid, int nthr) {
-    {
-      const int r = 0;
-      int p = tid;
-      if (p >= kTileP) return;
-      int64_t i = tile_base + p;
-      bool ok = i < a.n;
-      if (L::RB) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) v[r][c] = ok ? __ldg(a.rb + c * a.rb_stride + i) : 1e30f;
-        v[r][8] = ok ? __ldg(a.w + i) : 0.0f;
-        if (PASS == 2) {
-          v[r][9] = ok ? __ldg(a.x + i) : 0.0f;
-          v[r][10] = ok ? __ldg(a.y + i) : 0.0f;
-          v[r][11] = ok ? __ldg(a.vx + i) : 0.0f;
-          v[r][12] = ok ? __ldg(a.vy + i) : 0.0f;
-        }
-      } else {
-        v[r][0] = ok ? __ldg(a.x + i) : 0.0f;
-        v[r][1] = ok ? __ldg(a.y + i) : 0.0f;
-        v[r][2] = ok ? __ldg(a.w + i) : 0.0f;
-        if (PASS == 2) {
-          v[r][3] = ok ? __ldg(a.vx + i) : 0.0f;
-          v[r][4] = ok ? __ldg(a.vy + i) : 0.0f;
-        }
-      }
-    }
-  }
-
-  __device__ __forceinline__ void store(float* rec, float wscale, int tid, int nthr) {
-    {
-      const int r = 0;
-      int p = tid;
-      if (p >= kTileP) return;
-      float* d = rec + p * L::WIDTH;
-      if (L::RB) {
-        reinterpret_cast<float4*>(d)[0] = make_float4(v[r][0], v[r][0], v[r][1], v[r][1]);
-        reinterpret_cast<float4*>(d)[1] = make_float4(v[r][2], v[r][2], v[r][3], v[r][3]);
-        reinterpret_cast<float4*>(d)[2] = make_float4(v[r][4], v[r][4], v[r][5], v[r][5]);
-        reinterpret_cast<float4*>(d)[3] = make_float4(v[r][6], v[r][6], v[r][7], v[r][7]);
-        float wc = log2f(v[r][8] * wscale);
-        reinterpret_cast<float4*>(d)[4] = make_float4(wc, wc, 0.0f, 0.0f);
-        if (PASS == 2) {
-          reinterpret_cast<float4*>(d)[5] = make_float4(v[r][9], v[r][9], v[r][10], v[r][10]);
-          reinterpret_cast<float4*>(d)[6] = make_float4(v[r][11], v[r][11], v[r][12], v[r][12]);
-        }
-      } else {
-        reinterpret_cast<float4*>(d)[0] = make_float4(v[r][0], v[r][0], v[r][1], v[r][1]);
-        float wc = log2f(v[r][2] * wscale);
-        if (PASS == 2) {
-          reinterpret_cast<float4*>(d)[1] = make_float4(v[r][3], v[r][3], v[r][4], v[r][4]);
-          reinterpret_cast<float4*>(d)[2] = make_float4(wc, wc, 0.0f, 0.0f);
-        } else {
-          reinterpret_cast<float4*>(d)[1] = make_float4(wc, wc, 0.0f, 0.0f);
-        }
-      }
-    }
-  }
-};
 
 // Per-lane measurement constants for its NP slot pairs.
 template <int MODEL, int PASS, int NP, bool FOLD = false, int JS = NP>
@@ -166,7 +100,7 @@ struct LaneZ {
         if (FOLD) d[j] = f2(log2f(d[j].x) / a.na0, log2f(d[j].y) / a.na0);  // d = 0: +inf
       }
       if (MODEL == kRangeBearing) {
-        roff[j] = 4 + 4 * a.sc.rep[s];
+        roff[j] = 4 + 2 * a.sc.rep[s];
         if (PASS == 2 && j < JS) {  // the centres are used by the state sums only
           c0[j] = f2(a.sc.s2[s], a.sc.s2[s + 1]);
           c1[j] = f2(a.sc.s3[s], a.sc.s3[s + 1]);
@@ -177,18 +111,17 @@ struct LaneZ {
 };
 
 // Residuals (d0, d1) of the lane's slot pair j against the broadcast particle.
+// P = the record's first float4: (x, y, lw, 0) or (r_hi, r_lo, lw, 0).
 template <int MODEL, int PASS, int NP, bool FOLD, int JS>
-__device__ __forceinline__ void residual(const float* rec, const LaneZ<MODEL, PASS, NP, FOLD, JS>& z, int j,
-                                         float2& d0, float2& d1) {
+__device__ __forceinline__ void residual(const float* rec, const float4& P, const LaneZ<MODEL, PASS, NP, FOLD, JS>& z,
+                                         int j, float2& d0, float2& d1) {
   if (MODEL == kRangeBearing) {
-    float4 R = *reinterpret_cast<const float4*>(rec);
-    float4 T = *reinterpret_cast<const float4*>(rec + z.roff[j]);
-    d0 = __fadd2_rn(__fadd2_rn(f2(R.x, R.y), z.n0[j]), f2(R.z, R.w));  // (r_hi - z_r) + r_lo
-    d1 = __fadd2_rn(__fadd2_rn(f2(T.x, T.y), z.n1[j]), f2(T.z, T.w));  // (th_hi - z_th) + th_lo
+    const float2 T = *reinterpret_cast<const float2*>(rec + z.roff[j]);  // (th_hi, th_lo) of the pair's class
+    d0 = __fadd2_rn(__fadd2_rn(f2(P.x, P.x), z.n0[j]), f2(P.y, P.y));  // (r_hi - z_r) + r_lo
+    d1 = __fadd2_rn(__fadd2_rn(f2(T.x, T.x), z.n1[j]), f2(T.y, T.y));  // (th_hi - z_th) + th_lo
   } else {
-    float4 P = *reinterpret_cast<const float4*>(rec);
-    d0 = __fadd2_rn(f2(P.x, P.y), z.n0[j]);  // x - z_x
-    d1 = __fadd2_rn(f2(P.z, P.w), z.n1[j]);  // y - z_y
+    d0 = __fadd2_rn(f2(P.x, P.x), z.n0[j]);  // x - z_x
+    d1 = __fadd2_rn(f2(P.y, P.y), z.n1[j]);  // y - z_y
   }
 }
 
@@ -279,13 +212,13 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
   #pragma unroll(PASS == 1 ? kPPUnroll1 : kPPUnroll2)
         for (int pp = 0; pp < 8; ++pp) {
           const float* rec = rb + (p0 + pp) * L::WIDTH;
-          // (log2(p_D c w), .) for both passes
-          const float2 wv = *reinterpret_cast<const float2*>(rec + L::WC);
+          const float4 P = *reinterpret_cast<const float4*>(rec);
+          const float2 wv = f2(P.z, P.z);  // log2(p_D c w), both passes
           float2 pacc = f2(0.0f, 0.0f), pacc1 = f2(0.0f, 0.0f);
   #pragma unroll
           for (int j = 0; j < NP; ++j) {
             float2 d0, d1;
-            residual(rec, z, j, d0, d1);
+            residual(rec, P, z, j, d0, d1);
             if (PASS == 1) {
               // u = p_D g w = 2^(-alpha q + log2(p_D c w)), flushed to zero below 2^-126
               // exactly as in pass 2 (the same exponent bits; the polynomial-offloaded
@@ -301,31 +234,31 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
               else if (j & 1) pacc1 = __fadd2_rn(pacc1, u);
               else pacc = __fadd2_rn(pacc, u);
               if (j < JS && MODEL == kRangeBearing) {
-                const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
-                d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
-                d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
+                const float2 XY = *reinterpret_cast<const float2*>(rec + L::XY);
+                d0 = __fadd2_rn(f2(XY.x, XY.x), z.c0[j]);  // x - centre_x
+                d1 = __fadd2_rn(f2(XY.y, XY.y), z.c1[j]);  // y - centre_y
               }
               if (j < JS) {
-                const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+                const float2 V = *reinterpret_cast<const float2*>(rec + L::V);
                 in[0][j] = __ffma2_rn(u, d0, in[0][j]);
-                in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+                in[1][j] = __ffma2_rn(u, f2(V.x, V.x), in[1][j]);
                 in[2][j] = __ffma2_rn(u, d1, in[2][j]);
-                in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+                in[3][j] = __ffma2_rn(u, f2(V.y, V.y), in[3][j]);
               }
             } else {
               const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
               pacc = __ffma2_rn(u, z.d[j], pacc);
               if (j < JS && MODEL == kRangeBearing) {
-                const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
-                d0 = __fadd2_rn(f2(XY.x, XY.y), z.c0[j]);  // x - centre_x
-                d1 = __fadd2_rn(f2(XY.z, XY.w), z.c1[j]);  // y - centre_y
+                const float2 XY = *reinterpret_cast<const float2*>(rec + L::XY);
+                d0 = __fadd2_rn(f2(XY.x, XY.x), z.c0[j]);  // x - centre_x
+                d1 = __fadd2_rn(f2(XY.y, XY.y), z.c1[j]);  // y - centre_y
               }
               if (j < JS) {
-                const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
+                const float2 V = *reinterpret_cast<const float2*>(rec + L::V);
                 in[0][j] = __ffma2_rn(u, d0, in[0][j]);
-                in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
+                in[1][j] = __ffma2_rn(u, f2(V.x, V.x), in[1][j]);
                 in[2][j] = __ffma2_rn(u, d1, in[2][j]);
-                in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
+                in[3][j] = __ffma2_rn(u, f2(V.y, V.y), in[3][j]);
               }
             }
           }
@@ -420,38 +353,40 @@ static cudaError_t launch_z(int model, int pass, const PassArgs& a, int gp, int 
 
 bool pass2_sums_scaled() { return kFoldD; }
 
-// Per-particle records of the dense passes, once per update (HBM-bound: 20 B read,
-// 48 B written per particle; range-bearing 52 B read, 112 B written):
-// position (x,x,y,y | vx,vx,vy,vy | lw,lw,0,0), lw = log2(p_D c w_i), every operand a
-// native f32x2 pair; range-bearing (r hi,hi,lo,lo | three bearing representations
-// hi,hi,lo,lo | lw,lw,0,0 | x,x,y,y | vx,vx,vy,vy).  Slots [n, n_pad) get zero records
-// with lw = -inf (terms exactly 0).
+// Per-particle records of the dense passes (GRec), once per update: HBM-bound, 20 B read
+// and 32 B written per particle (range-bearing: 52 B read, 64 B written).  One float4 of
+// the record per thread, so that a warp's stores are contiguous.  Slots [n, n_pad) get
+// zero records with lw = -inf (their terms are exactly 0).
 template <int MODEL>
 __global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad) {
   pdl_wait();
-  using L = GRec<MODEL>;
+  constexpr int Q = GRec<MODEL>::WIDTH / 4;  // float4 per record
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
-    float4* d = reinterpret_cast<float4*>(a.rec + i * L::WIDTH);
+  float4* out = reinterpret_cast<float4*>(a.rec);
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < n_pad * Q; f += stride) {
+    const int64_t i = f / Q;
+    const int q = (int)(f % Q);
     const bool ok = i < a.n;
-    const float x = ok ? a.x[i] : 0.0f, y = ok ? a.y[i] : 0.0f;
-    const float vx = ok ? a.vx[i] : 0.0f, vy = ok ? a.vy[i] : 0.0f;
-    const float wc = ok ? log2f(a.w[i] * a.wscale) : -INFINITY;
+    float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (MODEL == kRangeBearing) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float hi = ok ? a.rb[(2 * c) * a.rb_stride + i] : 0.0f;
-        const float lo = ok ? a.rb[(2 * c + 1) * a.rb_stride + i] : 0.0f;
-        d[c] = make_float4(hi, hi, lo, lo);
+      if (q == 0) {
+        v = ok ? make_float4(a.rb[i], a.rb[a.rb_stride + i], log2f(a.w[i] * a.wscale), 0.0f)
+               : make_float4(0.0f, 0.0f, -INFINITY, 0.0f);
+      } else if (ok && q == 1) {
+        v = make_float4(a.rb[2 * a.rb_stride + i], a.rb[3 * a.rb_stride + i], a.rb[4 * a.rb_stride + i],
+                        a.rb[5 * a.rb_stride + i]);
+      } else if (ok && q == 2) {
+        v = make_float4(a.rb[6 * a.rb_stride + i], a.rb[7 * a.rb_stride + i], a.x[i], a.y[i]);
+      } else if (ok) {
+        v = make_float4(a.vx[i], a.vy[i], 0.0f, 0.0f);
       }
-      d[4] = make_float4(wc, wc, 0.0f, 0.0f);
-      d[5] = make_float4(x, x, y, y);
-      d[6] = make_float4(vx, vx, vy, vy);
     } else {
-      d[0] = make_float4(x, x, y, y);
-      d[1] = make_float4(vx, vx, vy, vy);
-      d[2] = make_float4(wc, wc, 0.0f, 0.0f);
+      if (q == 0)
+        v = ok ? make_float4(a.x[i], a.y[i], log2f(a.w[i] * a.wscale), 0.0f) : make_float4(0.0f, 0.0f, -INFINITY, 0.0f);
+      else if (ok)
+        v = make_float4(a.vx[i], a.vy[i], 0.0f, 0.0f);
     }
+    out[f] = v;
   }
 }
 
@@ -460,7 +395,7 @@ int record_width(int model) { return model == kRangeBearing ? GRec<kRangeBearing
 cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s) {
   const int64_t n_pad = (a.n + kTileP - 1) / kTileP * kTileP;
   if (n_pad <= 0) return cudaSuccess;
-  const unsigned grid = (unsigned)std::min<int64_t>((n_pad + 255) / 256, 148 * 8);
+  const unsigned grid = (unsigned)std::min<int64_t>((n_pad * (record_width(model) / 4) + 255) / 256, 148 * 16);
   if (model == kRangeBearing)
     pdl_launch(k_records<kRangeBearing>, grid, 256, 0, s, a, n_pad);
   else
@@ -490,201 +425,6 @@ static int occ_z(int model, int pass, int wz) {
 
 int pass_occupancy(int model, int pass, int wz, int zl) {
   return zl == 8 ? occ_z<8>(model, pass, wz) : occ_z<4>(model, pass, wz);
-}
-
-// ---------------------------------------------------------------------------
-// Group-pipelined update: one particle sweep evaluates pass 1
-// (C) for measurement group j and pass 2 (weights, STPHD sums) for group j-1,
-// whose C is already reduced.  Pass 1 is EX2-bound and pass 2 FMA-bound; with
-// both in the same instruction stream the two pipes overlap.  H1 / H2 select
-// the halves (the first sweep has only pass 1, the last only pass 2).  4 slots
-// per lane per pass; both passes fold log2(p_D c w_i) into the exponent, so the
-// pass-1 and pass-2 terms u = p_D g w are bitwise identical.
-struct FusedArgs {
-  PassArgs a;
-  int s1_base;   // first slot of the pass-1 group
-  int s2_base;   // first slot of the pass-2 group
-  int p_plane;   // P plane of the pass-2 group's first CTA z-block
-};
-
-template <int MODEL, bool H1, bool H2>
-__global__ void __launch_bounds__(256, 2) k_fused(const FusedArgs fa) {
-  pdl_wait();
-  using L = RecLayout<MODEL, 2>;
-  constexpr int NP = 2;  // slot pairs per lane per pass
-  const PassArgs& a = fa.a;
-  extern __shared__ __align__(16) float smem[];
-  const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, wz = nthr >> 5;
-  float* recs = smem;                                  // [2][kTileP][WIDTH]
-  float* psum = recs + 2 * kTileP * L::WIDTH;          // [2][wz][kTileP]
-  double* out64 = reinterpret_cast<double*>(psum + 2 * wz * kTileP);  // [4 + 16][nthr]
-
-  const int zb = blockIdx.y;
-  const int off = (zb * wz + warp) * 128 + lane * 4;
-  const int slot1 = fa.s1_base + off, slot2 = fa.s2_base + off;
-  LaneZ<MODEL, 1, NP> z1;
-  LaneZ<MODEL, 2, NP> z2;
-  if (H1) z1.load(a, slot1);
-  if (H2) z2.load(a, slot2);
-  const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
-
-  float2 c1[NP], in[4][NP];
-#pragma unroll
-  for (int j = 0; j < NP; ++j) {
-    c1[j] = f2(0.0f, 0.0f);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) in[q][j] = f2(0.0f, 0.0f);
-  }
-#pragma unroll
-  for (int q = 0; q < 20; ++q) out64[q * nthr + tid] = 0.0;
-
-  const int64_t ntiles = (a.n + kTileP - 1) / kTileP;
-  const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
-  const int64_t t_end = min(t_begin + a.tiles_per_cta, ntiles);
-
-  TileLoader<MODEL, 2> ld;
-  if (t_begin < t_end) {
-    ld.fetch(a, t_begin * kTileP, tid, nthr);
-    ld.store(recs, a.wscale, tid, nthr);
-  }
-  __syncthreads();
-
-  for (int64_t t = t_begin; t < t_end; ++t) {
-    const int buf = (int)((t - t_begin) & 1);
-    const bool more = t + 1 < t_end;
-    if (more) ld.fetch(a, (t + 1) * kTileP, tid, nthr);
-    const float* rb = recs + buf * kTileP * L::WIDTH;
-
-#pragma unroll 1
-    for (int p0 = 0; p0 < kTileP; p0 += 8) {
-      float pe[8];
-#pragma unroll
-      for (int pp = 0; pp < 8; ++pp) {
-        const float* rec = rb + (p0 + pp) * L::WIDTH;
-        const float2 lw = *reinterpret_cast<const float2*>(rec + L::WC);
-        if (H1) {
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            float2 d0, d1;
-            residual(rec, z1, j, d0, d1);
-            c1[j] = __fadd2_rn(c1[j], ex2v(expo<MODEL>(d0, d1, na0, na1, lw)));
-          }
-        }
-        if (H2) {
-          float2 pacc = f2(0.0f, 0.0f);
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            float2 d0, d1;
-            residual(rec, z2, j, d0, d1);
-            const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, lw));  // u = p_D g w
-            pacc = __ffma2_rn(u, z2.d[j], pacc);
-            if (MODEL == kRangeBearing) {
-              const float4 XY = *reinterpret_cast<const float4*>(rec + L::XY);
-              d0 = __fadd2_rn(f2(XY.x, XY.y), z2.c0[j]);
-              d1 = __fadd2_rn(f2(XY.z, XY.w), z2.c1[j]);
-            }
-            const float4 V = *reinterpret_cast<const float4*>(rec + L::V);
-            in[0][j] = __ffma2_rn(u, d0, in[0][j]);
-            in[1][j] = __ffma2_rn(u, f2(V.x, V.y), in[1][j]);
-            in[2][j] = __ffma2_rn(u, d1, in[2][j]);
-            in[3][j] = __ffma2_rn(u, f2(V.z, V.w), in[3][j]);
-          }
-          pe[pp] = pacc.x + pacc.y;
-        }
-      }
-      if (H2) {
-        float sres = transpose_reduce8(pe, lane);
-        if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = sres;
-      }
-    }
-
-    if (more) ld.store(recs + (buf ^ 1) * kTileP * L::WIDTH, a.wscale, tid, nthr);
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      if (H1) {
-        out64[(2 * j) * nthr + tid] += (double)c1[j].x;
-        out64[(2 * j + 1) * nthr + tid] += (double)c1[j].y;
-        c1[j] = f2(0.0f, 0.0f);
-      }
-      if (H2) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          out64[(4 + q * 4 + 2 * j) * nthr + tid] += (double)in[q][j].x;
-          out64[(4 + q * 4 + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
-          in[q][j] = f2(0.0f, 0.0f);
-        }
-      }
-    }
-    __syncthreads();
-
-    if (H2) {
-      for (int p = tid; p < kTileP; p += nthr) {
-        int64_t i = t * kTileP + p;
-        if (i < a.n) {
-          float sres = 0.0f;
-          for (int w2 = 0; w2 < wz; ++w2) sres += psum[(buf * wz + w2) * kTileP + p];
-          a.P[(int64_t)(fa.p_plane + zb) * a.P_stride + i] = sres;
-        }
-      }
-    }
-  }
-  if (H1) {
-    const int64_t base = (int64_t)blockIdx.x * a.slots_pad;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) a.Cpart[base + slot1 + m] = out64[m * nthr + tid];
-  }
-  if (H2) {
-    const int64_t base = (int64_t)blockIdx.x * 4 * a.slots_pad;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-        a.Apart[base + (int64_t)q * a.slots_pad + slot2 + m] = out64[(4 + q * 4 + m) * nthr + tid];
-  }
-}
-
-template <int MODEL>
-static size_t fused_smem(int wz) {
-  using L = RecLayout<MODEL, 2>;
-  return sizeof(float) * 2 * kTileP * L::WIDTH + sizeof(float) * 2 * wz * kTileP + sizeof(double) * 20 * wz * 32;
-}
-
-template <int MODEL, bool H1, bool H2>
-static cudaError_t launch_fused_t(const FusedArgs& fa, int gp, int zbg, int wz, cudaStream_t s) {
-  ensure_max_smem(k_fused<MODEL, H1, H2>, fused_smem<MODEL>(kMaxWarpsZ));
-  pdl_launch(k_fused<MODEL, H1, H2>, dim3((unsigned)gp, (unsigned)zbg), wz * 32, fused_smem<MODEL>(wz), s, fa);
-  return cudaGetLastError();
-}
-
-template <int MODEL>
-static cudaError_t launch_fused_m(bool h1, bool h2, const FusedArgs& fa, int gp, int zbg, int wz, cudaStream_t s) {
-  if (h1 && h2) return launch_fused_t<MODEL, true, true>(fa, gp, zbg, wz, s);
-  if (h1) return launch_fused_t<MODEL, true, false>(fa, gp, zbg, wz, s);
-  return launch_fused_t<MODEL, false, true>(fa, gp, zbg, wz, s);
-}
-
-cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,
-                         int zbg, int wz, cudaStream_t s) {
-  if (gp <= 0 || zbg <= 0 || (!h1 && !h2)) return cudaSuccess;
-  FusedArgs fa{a, s1_base, s2_base, p_plane};
-  if (model == kPosIso) return launch_fused_m<kPosIso>(h1, h2, fa, gp, zbg, wz, s);
-  if (model == kPosAniso) return launch_fused_m<kPosAniso>(h1, h2, fa, gp, zbg, wz, s);
-  return launch_fused_m<kRangeBearing>(h1, h2, fa, gp, zbg, wz, s);
-}
-
-template <int MODEL>
-static int fused_occ_m(int wz) {
-  int n = 0, m;
-  ensure_max_smem(k_fused<MODEL, true, true>, fused_smem<MODEL>(kMaxWarpsZ));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<MODEL, true, true>, wz * 32, fused_smem<MODEL>(wz));
-  m = n;
-  return m;
-}
-
-int fused_occupancy(int model, int wz) {
-  if (model == kPosIso) return fused_occ_m<kPosIso>(wz);
-  if (model == kPosAniso) return fused_occ_m<kPosAniso>(wz);
-  return fused_occ_m<kRangeBearing>(wz);
 }
 
 // ---------------------------------------------------------------------------

@@ -52,7 +52,7 @@ struct Layout {
   size_t total = 0;
   // byte offsets
   size_t o_A[5], o_B[5], o_wn, o_rb, o_rec, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_sel, o_selinfo, o_D,
-      o_acc, o_blk_w, o_blk_wp, o_blk_off, o_marks, o_bmax, o_anc, o_est, o_gather, o_ring, o_summ, o_bad;
+      o_acc, o_blk_w, o_blk_wp, o_blk_off, o_ctot, o_coff, o_counter, o_marks, o_bmax, o_anc, o_est, o_gather, o_ring, o_summ, o_bad;
   // gated update (p->gate != 0)
   int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
   int g_ntiles = 0, g_nsorted = 0;
@@ -73,7 +73,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   // every z-block size (wz * 32 * zl, 256 ... 2048 slots) divides 2048
   L.slots_max = (int)align_up((size_t)p->max_meas + 8, 2048);
   // P planes: one per CTA z-block (smallest: kMinWarpsZ warps x 32 lanes x 4 slots) or group
-  L.zb_max = std::max(1, L.slots_max / std::min(kMinWarpsZ * 32 * 4, kFuseGroup));
+  L.zb_max = std::max(1, L.slots_max / (kMinWarpsZ * 32 * 4));
   L.part_cap = (int64_t)64 * sms * 256 + 8192;
   L.nbw_max = ceil_div(L.cap_l, kBlockW) + 1;
   L.nbo_max = ceil_div(L.cap_off, kBlockOff) + 1;
@@ -90,7 +90,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_P = take(sizeof(float) * (size_t)L.zb_max * L.cap_l);
   // dense-pass particle records (k_records): [cap_l rounded up to kTileP][record_width]
   L.o_rec = take(sizeof(float) * align_up((size_t)L.cap_l, kTileP) *
-                 (p->meas == PHD_MEAS_RANGE_BEARING ? 28 : 12));
+                 (p->meas == PHD_MEAS_RANGE_BEARING ? 16 : 8));
   L.o_Cpart = take(sizeof(double) * L.part_cap);
   L.o_Apart = take(sizeof(double) * 4 * L.part_cap);
   L.o_zlab = take(sizeof(float) * 2 * (size_t)(p->max_meas + 1));
@@ -108,6 +108,9 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_blk_w = take(sizeof(double) * L.nbw_max);
   L.o_blk_wp = take(sizeof(double) * L.nbw_max);
   L.o_blk_off = take(sizeof(double) * (L.nbw_max + 1));
+  L.o_ctot = take(sizeof(double) * (L.nbw_max / kResScanChunk + 2));
+  L.o_coff = take(sizeof(double) * (L.nbw_max / kResScanChunk + 3));
+  L.o_counter = take(sizeof(unsigned) * 4);
   L.o_marks = take(sizeof(int32_t) * L.cap_off);
   L.o_bmax = take(sizeof(int32_t) * L.nbo_max);
   L.o_anc = take(sizeof(int32_t) * L.cap_off);
@@ -178,7 +181,8 @@ struct phd_ctx {
   float* s[5];   // s0, s1, s2, s3, d
   int32_t* rep;
   double *C, *D, *acc;
-  double *blk_w, *blk_wp, *blk_off;
+  double *blk_w, *blk_wp, *blk_off, *ctot, *coff;
+  unsigned* scan_counter;
   int32_t *marks, *bmax, *anc;
   phd_estimate* est;      // gather block: est[0].label = count, est[1..] = estimates
   phd_estimate* gather;   // DCP: every rank's gather block
@@ -201,7 +205,6 @@ struct phd_ctx {
   int64_t n_local = 0, g0 = 0;
   int64_t n_surv_local = 0;
   int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zl = 4, zb = 0, gp = 0, M_z = -1;
-  bool fused = false;    // group-pipelined update (pass 1 of group j with pass 2 of group j-1)
   double* C_slot = nullptr;
   int32_t* sel_flag = nullptr;   // k_select: label in the estimated index set I
   double* sel_info = nullptr;    // (W_id, LT, n_eligible, n_sel, ..)
@@ -530,6 +533,9 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->blk_w = at<double>(c->ws, L.o_blk_w);
   c->blk_wp = at<double>(c->ws, L.o_blk_wp);
   c->blk_off = at<double>(c->ws, L.o_blk_off);
+  c->ctot = at<double>(c->ws, L.o_ctot);
+  c->coff = at<double>(c->ws, L.o_coff);
+  c->scan_counter = at<unsigned>(c->ws, L.o_counter);
   c->marks = at<int32_t>(c->ws, L.o_marks);
   c->bmax = at<int32_t>(c->ws, L.o_bmax);
   c->anc = at<int32_t>(c->ws, L.o_anc);
@@ -971,18 +977,7 @@ static phd_status build_slots(phd_ctx* c, int M) {
   c->n_slots = n;
   const int n_fill = n;  // slots [n_fill, slots_pad) are padding
   if (c->model == kRangeBearing && M > 0) n = std::max(n, M + 6);  // room for the pass-2 layout (k_select_slots)
-  // group-pipelined update for large M: 4 slots/lane/pass, 4 warps,
-  // groups of 512 slots; otherwise the two-sweep path with 8 (or 4) slots per lane
-  // Opt-in (PHD_FUSE=1): measured neutral on B200 (49.6 vs 49.0 ms at cfg 5) because
-  // both passes are register-file-read bound, not pipe bound.
-  const char* fz = getenv("PHD_FUSE");
-  c->fused = n >= kFuseMinSlots && fz && fz[0] == '1';
-  if (c->fused) {
-    c->zl = 4;
-    c->wz = kFuseWarps;
-    c->zb = M > 0 ? (int)ceil_div(n, kFuseGroup) : 0;
-    c->slots_pad = (int)ceil_div(std::max(n, 1), kFuseGroup) * kFuseGroup;
-  } else {
+  {
   // slots per lane: 8 (halves the per-particle overheads) unless it pads much more than 4;
   // warps per CTA: the fewest padded slots among {the warps needed, 8, 4, 2} (ties: more
   // warps).  Padding slots cost full pair work: cfg 4 (M ~ 3000) pads to 4096 slots with
@@ -1130,7 +1125,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   // the candidate offsets are an int32 scan: at most M candidates per tile, so a
   // capacity whose tiles x M could exceed INT32_MAX runs dense (same on every rank)
   const bool fits32 = (double)c->L.g_ntiles * (double)M <= (double)INT32_MAX;
-  if (c->p.gate != 0 && M > 0 && !small && fits32 && !(getenv("PHD_FUSE") && getenv("PHD_FUSE")[0] == '1')) {
+  if (c->p.gate != 0 && M > 0 && !small && fits32) {
     phd_status st = gate_plan(c, M, n, &gated);
     if (st != PHD_OK) return st;
   }
@@ -1154,10 +1149,9 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   }
   // particle-CTA count: one wave of resident CTAs over the z-blocks of one sweep
   int gp = 0;
-  const int zb_sweep = c->fused ? 1 : c->zb;
+  const int zb_sweep = c->zb;
   if (M > 0 && n > 0 && !gated) {
-    int occ = c->fused ? fused_occupancy(c->model, c->wz)
-                       : std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl));
+    int occ = std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl));
     occ = std::max(1, occ);
     int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / zb_sweep);
     int64_t cap_gp = std::max<int64_t>(1, c->L.part_cap / c->slots_pad);
@@ -1186,15 +1180,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   pa.P = c->P;
   pa.P_stride = c->L.cap_l;
   pa.rec = c->rec;
-  c->select = M > 0 && !c->fused && c->p.stphd_all == 0;
+  c->select = M > 0 && c->p.stphd_all == 0;
   pa.js = nullptr;
-  // C of slots [s0, s1): fixed-order reduction, C1 all-reduce, per-slot constants
-  auto normalise = [&](int s0, int s1) -> phd_status {
-    KL(launch_reduce_C(c->Cpart, gp, c->slots_pad, s0, s1, c->C_slot, c->st));
-    if (c->world > 1 && !c->dcp) COMM(c->comm->allreduce_f64(c->C_slot + s0, (size_t)(s1 - s0), c->st));
-    KL(launch_zconst(c->C_slot, c->slot_label, s0, s1, c->kappa, c->s[4], c->C, c->D, c->bad, c->st));
-    return PHD_OK;
-  };
   if (M > 0 && gated) {
     // candidate lists, entries grouped by label, then the two gated passes
     const int ntiles = (int)c->g_tiles;
@@ -1241,22 +1228,6 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (ntiles > 0) KL(launch_gpass(2, ga, c->st));
     timing_record(c, 6);
     KL(launch_gate_reduce(2, c->gmstart, c->gmlist, M, nullptr, c->gpart2, ga.sel, c->gA, c->slots_pad, c->st));
-  } else if (M > 0 && c->fused) {
-    timing_record(c, 3);
-    // group-pipelined sweeps: sweep j = pass 1 of group j + pass 2 of group j-1
-    const int Q = c->zb;
-    for (int j = 0; j <= Q; ++j) {
-      const bool h1 = j < Q, h2 = j >= 1;
-      if (gp > 0)
-        KL(launch_fused(c->model, h1, h2, pa, j * kFuseGroup, (j - 1) * kFuseGroup, j - 1, gp, 1, c->wz, c->st));
-      if (j == 0) timing_record(c, 4);
-      if (h1) {
-        phd_status st = normalise(j * kFuseGroup, (j + 1) * kFuseGroup);
-        if (st != PHD_OK) return st;
-      }
-      if (j == 0) timing_record(c, 5);
-    }
-    timing_record(c, 6);
   } else if (M > 0) {
     if (gp > 0) KL(launch_records(c->model, pa, c->st));
     timing_record(c, 3);
@@ -1302,7 +1273,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   KL(launch_reduce_acc(gated ? c->gA : c->Apart, gated ? 1 : gp, c->slots_pad, M > 0 ? c->slots_pad : 0, c->slot_label, c->C, c->D, c->s[0],
                        c->s[1], c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank,
                        c->world, c->dcp || c->rank == 0 ? 1 : 0, c->select ? c->sel_flag : nullptr, c->st,
-                       !c->fused && pass2_sums_scaled() ? 1 : 0));
+                       pass2_sums_scaled() ? 1 : 0));
   // rank slots [W_r | W_pred_r | N_r] (3 per rank); N_r written from the host
   c->h_meta[3 * c->world + 16] = (double)n;
   CU(cudaMemcpyAsync(rank_slots + 2 * c->world + c->rank, c->h_meta + 3 * c->world + 16, sizeof(double),
@@ -1565,6 +1536,24 @@ static phd_status p2p_setup(phd_ctx* c) {
   return PHD_OK;
 }
 
+static ResampleGatherArgs rg_args(phd_ctx* c, const ResampleArgs& ra, float w_off) {
+  ResampleGatherArgs g{};
+  g.r = ra;
+  g.coff = c->coff;
+  g.x = c->A[0];
+  g.vx = c->A[1];
+  g.y = c->A[2];
+  g.vy = c->A[3];
+  g.w_off = w_off;
+  g.ox = c->B[0];
+  g.ovx = c->B[1];
+  g.oy = c->B[2];
+  g.ovy = c->B[3];
+  g.ow = c->B[4];
+  g.anc = c->anc;
+  return g;
+}
+
 phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   NvtxRange nvtx_("phd_resample_exchange");
   if (!c) return PHD_EINVAL;
@@ -1610,12 +1599,9 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   const float w_off = n_out > 0 ? (float)(W / (double)n_out) : 0.0f;
   const int64_t n = c->n_local;
   const int nbw = (int)ceil_div(n, kBlockW);
-  const int nbo = (int)ceil_div(nprod, kBlockOff);
+  ResampleArgs ra{};
   if (!c->zero_mass && nprod > 0) {
-    CU(cudaMemsetAsync(c->marks, 0xFF, sizeof(int32_t) * nprod, c->st));
-    CU(cudaMemsetAsync(c->bmax, 0xFF, sizeof(int32_t) * nbo, c->st));
-    KL(launch_scan_blocks(c->blk_w, nbw, c->blk_off, c->st));
-    ResampleArgs ra{};
+    KL(launch_scan_chunks(c->blk_w, nbw, c->blk_off, c->ctot, c->coff, c->scan_counter, c->st));
     ra.n_local = n;
     ra.g0 = c->g0;
     ra.w = c->wn;
@@ -1625,11 +1611,9 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     ra.U = U;
     ra.lo = lo;
     ra.hi = hi;
-    ra.marks = c->marks;
-    ra.bmax = c->bmax;
-    KL(launch_resample_mark(ra, c->st));
-    KL(launch_scan_max(c->bmax, nbo, c->st));
   }
+  // systematic resampling + gather in one kernel (k_resample_gather); zero mass: the
+  // deterministic spread of k_gather
   if (!c->dcp && c->world > 1 && c->p2p_state == 0) {
     phd_status st = p2p_setup(c);
     if (st != PHD_OK) return st;
@@ -1648,11 +1632,17 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
       for (int i = 0; i < 5; ++i) po.dst[q][i] = base + (size_t)i * c->L.cap_l;
     }
     po.blo[c->world] = n_out + J;
-    KL(launch_gather_p2p(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, po, c->anc,
-                         c->zero_mass, lo, c->N, n_out, c->st));
+    if (c->zero_mass)
+      KL(launch_gather_p2p(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, po, c->anc,
+                           c->zero_mass, lo, c->N, n_out, c->st));
+    else if (nprod > 0)
+      KL(launch_resample_gather(rg_args(c, ra, w_off), &po, c->st));
   } else {
-    KL(launch_gather(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, c->B[0], c->B[1],
-                     c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->dcp ? c->n_local : c->N, n_out, c->st));
+    if (c->zero_mass)
+      KL(launch_gather(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, c->B[0], c->B[1],
+                       c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->dcp ? c->n_local : c->N, n_out, c->st));
+    else if (nprod > 0)
+      KL(launch_resample_gather(rg_args(c, ra, w_off), nullptr, c->st));
   }
   timing_record(c, 11);
   // exchange: the next step's survivors [0, n_out) are block-partitioned over N' = n_out + J

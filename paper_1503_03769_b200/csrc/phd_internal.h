@@ -67,9 +67,6 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 // measurement slots per lane: 4 or 8 (kernel template), i.e. 128 or 256 per warp
 constexpr int kMaxWarpsZ = 8;                   // warps per CTA (each owns 128 slots)
 constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one particle per loader thread
-constexpr int kFuseGroup = 512;                 // slots per measurement group (group-pipelined update)
-constexpr int kFuseWarps = 4;                   // warps per CTA in the group-pipelined update (4 x 128 = 512)
-constexpr int kFuseMinSlots = 2048;             // use the group-pipelined update from 4 groups up
 constexpr int kTileP = 64;                      // particles per smem tile
 constexpr int kFlushTiles = 16;                 // fp32 mid-level -> fp64 every 16 tiles
 constexpr int kBlockW = 1024;                   // particles per finalize / scan block
@@ -197,9 +194,7 @@ bool pass2_sums_scaled();
 int record_width(int model);
 cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s);
 int pass_occupancy(int model, int pass, int wz, int zl);
-cudaError_t launch_fused(int model, bool h1, bool h2, const PassArgs& a, int s1_base, int s2_base, int p_plane, int gp,
-                         int zbg, int wz, cudaStream_t s);
-int fused_occupancy(int model, int wz);
+
 // per-slot constants after C: D = kappa + C, C_lab / D_lab by label, d = 1/D (fp32), non-finite count
 struct ZConstArgs {
   const int32_t* slot_label;
@@ -262,6 +257,24 @@ cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_
                           int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out, cudaStream_t s);
 // fused resample + exchange (world > 1, peer-memory window)
 constexpr int kMaxPeers = 16;
+// Resampling + gather in one kernel (k_resample_gather): the block offsets are
+// off(b) = coff[b / kResScanChunk] + loc[b] (k_scan_chunks, fixed association).
+constexpr int kResScanChunk = 1024;
+struct ResampleGatherArgs {
+  ResampleArgs r;            // weights, O_r, scale, U, produced range [lo, hi); r.blk_off = loc
+  const double* coff;        // [nchunks + 1] chunk offsets
+  const float *x, *vx, *y, *vy;  // predicted states (local)
+  float w_off;               // offspring weight W / n_out
+  float *ox, *ovx, *oy, *ovy, *ow;  // local outputs at the produced index (p2p == 0)
+  int32_t* anc;              // [produced]: global ancestor
+};
+// exclusive fp64 scan of nb block masses: loc[b] (within its chunk of kResScanChunk), coff[c]
+// (chunk prefix; coff[nchunks] = total); deterministic, one launch (last CTA combines)
+cudaError_t launch_scan_chunks(const double* blk, int nb, double* loc, double* ctot, double* coff, unsigned* counter,
+                               cudaStream_t s);
+struct PeerOut;
+cudaError_t launch_resample_gather(const ResampleGatherArgs& a, const PeerOut* po, cudaStream_t s);
+
 struct PeerOut {
   float* dst[kMaxPeers][5];   // owner q's next-step arrays x, vx, y, vy, w (peer pointers)
   int64_t blo[kMaxPeers + 1]; // next-step block partition of N' = n_out + J

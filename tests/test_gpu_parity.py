@@ -440,15 +440,6 @@ def test_full_size_sampled(phd, orc, cname, near_tie_report):
     f.close()
 
 
-def test_group_pipelined_update_parity(phd, orc, monkeypatch):
-    """The opt-in group-pipelined update (PHD_FUSE=1) on both sensor models."""
-    monkeypatch.setenv("PHD_FUSE", "1")
-    for m in (POS, RB):
-        f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 9001, 2600, seed=5)
-        _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
-        f.close()
-
-
 def test_births_gaussian_model(phd, orc):
     """NEXT-4: the paper's fixed Gaussian birth intensity N(x-bar, Q)."""
     for base in (POS, RB):
