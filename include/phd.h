@@ -305,6 +305,12 @@ phd_status phd_get_timing(phd_ctx* ctx, float* ms /* [8]: predict, pass1, pass2,
 /* ---- host-only helpers (no device needed; used by the CPU tests) ---------- */
 /* Library's own Philox4x32-10 (host build of the device generator). */
 void phd_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* The same block cipher as the device code of the filter runs it (the kernels' own
+ * Philox, known-answer tests against cuRAND's curand_Philox4x32_10): out[i] =
+ * Philox4x32-10(ctr[i], key = {seed lo32, seed hi32}) for i < n.  ctr and out are
+ * DEVICE arrays of n x 4 uint32; stream: cudaStream_t (NULL: the legacy stream);
+ * synchronous.  Errors: PHD_EINVAL (n < 0, NULL arrays), PHD_ECUDA. */
+phd_status phd_philox4x32_10_device(uint64_t seed, const uint32_t* ctr, int64_t n, uint32_t* out, void* stream);
 /* Block [lo, hi) of n items owned by rank (floor(r n / world) bounds). */
 phd_status phd_rank_block(int64_t n, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
 /* Resampling bounds: W = sum W_r (rank order), O_r = exclusive prefix,

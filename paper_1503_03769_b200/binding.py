@@ -59,7 +59,8 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_get_ancestors", "phd_get_resample_meta", "phd_launch_count", "phd_set_timing", "phd_get_timing",
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
            "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates",
-           "phd_get_gate_stats", "phd_exchange_path", "phd_set_retained_measurements", "phd_init_population"]
+           "phd_get_gate_stats", "phd_exchange_path", "phd_set_retained_measurements", "phd_init_population",
+           "phd_philox4x32_10_device"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -117,6 +118,7 @@ def load(build_if_missing=True):
     L.phd_get_gate_stats.argtypes = [_P, _I64]
     L.phd_set_retained_measurements.argtypes = [_P, _P, ctypes.c_int32]
     L.phd_init_population.argtypes = [_P, ctypes.c_double, _D, _D, ctypes.c_double]
+    L.phd_philox4x32_10_device.argtypes = [ctypes.c_uint64, _P, ctypes.c_int64, _P, _P]
     L.phd_exchange_path.argtypes = [_P]
     L.phd_exchange_path.restype = ctypes.c_int32
     L.phd_launch_count.argtypes = [_P]
@@ -198,6 +200,16 @@ def philox(ctr, key):
     o = (ctypes.c_uint32 * 4)()
     load().phd_philox4x32_10(c, k, o)
     return [int(o[i]) for i in range(4)]
+
+
+def philox_device(seed, ctr, out):
+    """The kernels' Philox on n counters: ctr and out are device buffers of n x 4 uint32
+    (e.g. torch int32 CUDA tensors of shape [n, 4]); synchronous."""
+    n = int(ctr.shape[0])
+    st = load().phd_philox4x32_10_device(int(seed), ctypes.c_void_p(ctr.data_ptr()), n,
+                                         ctypes.c_void_p(out.data_ptr()), None)
+    if st != 0:
+        raise PhdError(st, "phd_philox4x32_10_device")
 
 
 def rank_block(n, world, rank):

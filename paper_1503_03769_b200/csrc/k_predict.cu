@@ -369,6 +369,22 @@ cudaError_t launch_init_weights(const InitArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Known-answer hook: the kernels' Philox (philox.cuh) on n device counters.
+__global__ void k_philox_kat(uint64_t seed, const uint4* __restrict__ ctr, int64_t n, uint4* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 c = ctr[i];
+  const U4 o = philox10(U4{c.x, c.y, c.z, c.w}, (uint32_t)seed, (uint32_t)(seed >> 32));
+  out[i] = make_uint4(o.x, o.y, o.z, o.w);
+}
+
+cudaError_t launch_philox_kat(uint64_t seed, const uint32_t* ctr, int64_t n, uint32_t* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_philox_kat<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(seed, reinterpret_cast<const uint4*>(ctr), n,
+                                                           reinterpret_cast<uint4*>(out));
+  return cudaGetLastError();
+}
+
 __global__ void k_fill(float* p, float v, int64_t n) {
   pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -386,6 +386,13 @@ void phd_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
   out[3] = o.w;
 }
 
+phd_status phd_philox4x32_10_device(uint64_t seed, const uint32_t* ctr, int64_t n, uint32_t* out, void* stream) {
+  if (n < 0 || (n > 0 && (!ctr || !out))) return PHD_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (launch_philox_kat(seed, ctr, n, out, s) != cudaSuccess) return PHD_ECUDA;
+  return cudaStreamSynchronize(s) == cudaSuccess ? PHD_OK : PHD_ECUDA;
+}
+
 phd_status phd_rank_block(int64_t n, int32_t world, int32_t rank, int64_t* lo, int64_t* hi) {
   if (n < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi) return PHD_EINVAL;
   block_of(n, world, rank, lo, hi);

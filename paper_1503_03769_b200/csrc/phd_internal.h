@@ -285,6 +285,7 @@ cudaError_t launch_gather_p2p(const int32_t* marks, const int32_t* bmax_excl, in
                               int32_t* anc, int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out,
                               cudaStream_t s);
 cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s);
+cudaError_t launch_philox_kat(uint64_t seed, const uint32_t* ctr, int64_t n, uint32_t* out, cudaStream_t s);
 // label selection before pass 2 (k_select.cu)
 cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream_t s);  // blk only
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,

@@ -597,3 +597,43 @@ def test_all_core_timing_variant_matches_oracle(orc):
             assert np.allclose(Cm, C, rtol=1e-13, atol=0)
             assert np.array_equal(wm, wo)
             assert np.allclose(am, acc, rtol=1e-12, atol=1e-300)
+
+
+# --------------------------------------------------------------------------
+# Worked examples of SURVEY.md §8(c) (values computed there independently of this
+# oracle, from the closed forms of PAPER.md Eqs 7-8, 12-18)
+def test_worked_example_two_particles_two_measurements(orc):
+    """Ex2: position sigma = 10, p_D = 0.98, kappa = 2.5e-6; particles (0,0) w = 0.6 and
+    (15,5) w = 0.9; z = (10,0), (12,9): C, w', dW, zeta and the mass identity."""
+    m = Model(meas=POSITION, sigma_z=(10.0, 10.0), p_d=0.98, clutter_rate=10.0,
+              region=(-1000.0, 1000.0, -1000.0, 1000.0))
+    assert orc.kappa(m) == 2.5e-6
+    soa = np.array([[0.0, 15.0], [0.0, 0.0], [0.0, 5.0], [0.0, 0.0]])
+    w = np.array([0.6, 0.9])
+    z = np.array([[10.0, 0.0], [12.0, 9.0]])
+    C = orc.normalizers(m, soa, w, z)
+    wn, acc = orc.update(m, soa, w, z, C)
+    rel = lambda a, b: np.max(np.abs(np.asarray(a) - np.asarray(b)) / np.abs(np.asarray(b)))
+    assert rel(C, [1.66084918327586e-3, 1.54262188921722e-3]) < 1e-12
+    assert rel(wn, [0.549877034245137, 1.47700197873555]) < 1e-12
+    assert rel(acc[:, 0], [0.998497008310019, 0.998382004670669]) < 1e-12
+    zeta = np.stack([acc[:, 1] / acc[:, 0], acc[:, 3] / acc[:, 0]], axis=1)
+    assert np.max(np.abs(zeta - [[9.87361430062, 3.29120476687], [12.0457453003, 4.01524843343]])) < 1e-9
+    assert abs(math.fsum(wn) - 2.0268790129806885) < 1e-14
+    assert abs(math.fsum(wn) - ((1 - 0.98) * 1.5 + math.fsum(C / (2.5e-6 + C)))) < 1e-14
+
+
+def test_worked_example_range_bearing(orc):
+    """Ex3: sensor at the origin, sigma_r = 10, sigma_theta = 0.01, kappa = 50 / (2000 2 pi);
+    particle (3, 4) (h = (5, atan2(4, 3))), w = 1, z = (15, atan2(4, 3)): a one-sigma range
+    residual, g = e^(-1/2) / (2 pi sigma_r sigma_theta), w' = 1.0158116940774555."""
+    m = Model(meas=RANGE_BEARING, sigma_z=(10.0, 0.01), p_d=0.98, clutter_rate=50.0,
+              region=(0.0, 2000.0, -math.pi, math.pi), sensor_xy=(0.0, 0.0))
+    assert abs(orc.kappa(m) - 3.9788735772973834e-3) < 1e-18
+    soa = np.array([[3.0], [0.0], [4.0], [0.0]])
+    z = np.array([[15.0, 0.92729521800161223]])
+    C = orc.normalizers(m, soa, np.array([1.0]), z)
+    assert abs(C[0] / 0.98 - 0.96532352630053908) < 1e-14
+    wn, acc = orc.update(m, soa, np.array([1.0]), z, C)
+    assert abs(wn[0] - 1.0158116940774555) < 1e-14
+    assert abs(acc[0, 1] / acc[0, 0] - 3.0) < 1e-12 and abs(acc[0, 3] / acc[0, 0] - 4.0) < 1e-12
