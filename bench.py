@@ -252,6 +252,9 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
+    if world > 1:  # NCCL's init log (transports, NVLS) stays visible on stderr for the scaling runs
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -458,6 +461,19 @@ def run_ours(args):
                          "evaluated (every skipped term is exactly 0 in fp32 ftz); effective = N*M / step time, "
                          "not a pairs/s roofline claim"}
 
+    # per-rank stage times (max / mean over ranks): passes, resampling, exchange incl. its
+    # barrier, and the share of particles each rank updated (load balance)
+    per_rank = None
+    if world > 1:
+        mine = {k_: statistics.mean(v_) for k_, v_ in pass_ms.items()}
+        mine["particles"] = float(hi - lo)
+        if gated is not None:  # the gated update's evaluated pairs on this rank (its candidate balance)
+            mine["gated_evaluated_pairs"] = float(gated["evaluated_pairs_per_step"])
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        per_rank = {k_: {"max": max(r_[k_] for r_ in allr), "mean": statistics.mean(r_[k_] for r_ in allr),
+                         "per_rank": [r_[k_] for r_ in allr]} for k_ in mine}
+        per_rank["exchange_path"] = f.exchange_path()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -593,6 +609,7 @@ def run_ours(args):
                           "note": "Table 1 (PAPER.md:497-513), context only: not this metric or workload"},
         "hbm_kernels": hbm,
         "gated": gated,
+        "per_rank": per_rank,
         "near_ties": near,
         "clocks": clk,
     }

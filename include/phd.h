@@ -200,6 +200,22 @@ void phd_group_destroy(phd_group* g);
 phd_status phd_create_in_group(const phd_params* p, phd_group* g, int32_t rank, int32_t device, void* stream,
                                void* workspace, phd_ctx** out);
 
+/* Host transport: a multi-process rank group whose collectives run through caller
+ * callbacks on HOST buffers (test infrastructure: several processes on one GPU, where
+ * NCCL refuses duplicate devices).  Everything else is the product path: the peer-memory
+ * window (CUDA IPC handles, all-gathered through allgather_bytes), the fused gather with
+ * its P2P stores, the kernels.  Callbacks are synchronous and collective (every rank calls
+ * them in the same order): allreduce_f64 sums buf[0..n) over the ranks in rank order, in
+ * place; allgather_bytes writes rank r's send[0..bytes) to recv + r * bytes.  They return
+ * 0 on success.  The struct is copied; user must outlive the ctx. */
+typedef struct {
+  void* user;
+  int32_t (*allreduce_f64)(void* user, double* buf, size_t n);
+  int32_t (*allgather_bytes)(void* user, const void* send, void* recv, size_t bytes);
+} phd_host_transport;
+phd_status phd_create_with_transport(const phd_params* p, int32_t rank, int32_t world, const phd_host_transport* t,
+                                     int32_t device, void* stream, void* workspace, phd_ctx** out);
+
 /* ---- t = 0: the initial population ---------------------------------------
  * PAPER.md:260 ("t=0: Generate M particles for each group. The number of all
  * particles is N. All these particles are shared with same weights omega_0 = 1/M"),

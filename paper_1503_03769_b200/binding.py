@@ -39,6 +39,40 @@ class Params(ctypes.Structure):
                 ("stphd_all", ctypes.c_int32), ("gate", ctypes.c_int32), ("proposal_scale", ctypes.c_double)]
 
 
+_AR_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t)
+_AG_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+
+
+class HostTransport(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("allreduce_f64", _AR_FN), ("allgather_bytes", _AG_FN)]
+
+
+def host_transport(allreduce, allgather):
+    """phd_host_transport from two Python collectives on host data (test infrastructure):
+    allreduce(list of float) -> list of float summed over the ranks in rank order;
+    allgather(bytes) -> list of bytes, one per rank."""
+    def ar(_user, buf, n):
+        try:
+            vals = allreduce([buf[i] for i in range(n)])
+            for i in range(n):
+                buf[i] = vals[i]
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    def ag(_user, send, recv, nbytes):
+        try:
+            parts = allgather(ctypes.string_at(send, nbytes))
+            ctypes.memmove(recv, b"".join(parts), nbytes * len(parts))
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    t = HostTransport(None, _AR_FN(ar), _AG_FN(ag))
+    t._keep = (t.allreduce_f64, t.allgather_bytes)
+    return t
+
+
 class Estimate(ctypes.Structure):
     _fields_ = [("label", ctypes.c_int32), ("state", ctypes.c_float * 4), ("mass", ctypes.c_float)]
 
@@ -60,7 +94,7 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
            "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates",
            "phd_get_gate_stats", "phd_exchange_path", "phd_set_retained_measurements", "phd_init_population",
-           "phd_philox4x32_10_device"]
+           "phd_philox4x32_10_device", "phd_create_with_transport"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -97,6 +131,8 @@ def load(build_if_missing=True):
                              ctypes.c_int32, _P, _P, ctypes.POINTER(_P)]
     L.phd_create_in_group.argtypes = [ctypes.POINTER(Params), _P, ctypes.c_int32, ctypes.c_int32, _P, _P,
                                       ctypes.POINTER(_P)]
+    L.phd_create_with_transport.argtypes = [ctypes.POINTER(Params), ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.POINTER(HostTransport), ctypes.c_int32, _P, _P, ctypes.POINTER(_P)]
     L.phd_group_create.argtypes = [ctypes.c_int32, ctypes.POINTER(_P)]
     L.phd_group_destroy.argtypes = [_P]
     L.phd_group_destroy.restype = None
@@ -271,7 +307,8 @@ class LocalGroup:
 class Filter:
     """One rank's filter context (phd_ctx)."""
 
-    def __init__(self, model, rank=0, world=1, nccl_id=None, device=0, stream=None, workspace=None, group=None):
+    def __init__(self, model, rank=0, world=1, nccl_id=None, device=0, stream=None, workspace=None, group=None,
+                 transport=None):
         self.L = load()
         self.model = model
         self.params = params_from(model)
@@ -279,9 +316,14 @@ class Filter:
         self._ws = workspace  # keep the caller's buffer alive
         self._group = group
         h = _P()
+        self._transport = transport
         if group is not None:
             st = self.L.phd_create_in_group(ctypes.byref(self.params), group.h, int(rank), int(device), stream,
                                             _ptr(workspace), ctypes.byref(h))
+        elif transport is not None:
+            st = self.L.phd_create_with_transport(ctypes.byref(self.params), int(rank), int(world),
+                                                  ctypes.byref(transport), int(device), stream, _ptr(workspace),
+                                                  ctypes.byref(h))
         else:
             st = self.L.phd_create(ctypes.byref(self.params), int(rank), int(world), nccl_id, int(device),
                                    stream, _ptr(workspace), ctypes.byref(h))

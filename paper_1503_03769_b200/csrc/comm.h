@@ -39,7 +39,24 @@ class Comm {
   virtual std::string share_buffers(void* const* local, int nbuf, std::vector<void*>* all, cudaStream_t s) = 0;
 };
 
+// CUDA IPC peer window shared by any transport: handles of the local buffers are
+// all-gathered with c.allgather_bytes, the peers' opened (collective verdicts through
+// c.allreduce_f64, so every rank takes the same path).  Opened pointers are appended to
+// *opened (the caller closes them).
+std::string ipc_share_buffers(Comm& c, int world, int rank, void* const* local, int nbuf, std::vector<void*>* all,
+                              std::vector<void*>* opened, cudaStream_t s);
+
 Comm* make_nccl_comm(const uint8_t* id128, int world, int rank, std::string* err);
+
+// Host transport (test infrastructure for the multi-process path on one GPU): the
+// collectives go through caller callbacks on HOST buffers; the data path (IPC peer
+// window, P2P stores, kernels) is the product's.
+struct HostTransport {
+  void* user;
+  int (*allreduce_f64)(void* user, double* buf, size_t n);
+  int (*allgather_bytes)(void* user, const void* send, void* recv, size_t bytes);
+};
+Comm* make_host_comm(const HostTransport& t, int world, int rank, std::string* err);
 bool nccl_unique_id(uint8_t* out128);
 
 struct LocalGroup;

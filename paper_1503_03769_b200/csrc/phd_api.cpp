@@ -468,7 +468,8 @@ phd_status phd_workspace_size(const phd_params* p, int32_t world, size_t* bytes)
 }
 
 static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, const uint8_t* nccl_id,
-                              phd_group* group, int32_t device, void* stream, void* workspace, phd_ctx** out) {
+                              phd_group* group, int32_t device, void* stream, void* workspace, phd_ctx** out,
+                              const phd_host_transport* ht = nullptr) {
   if (!out) return PHD_EINVAL;
   *out = nullptr;
   phd_ctx* c = new phd_ctx();
@@ -609,6 +610,10 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
     std::string e;
     if (group) {
       c->comm = make_local_comm(group->g, rank, device, &e);
+    } else if (ht) {
+      HostTransport t{ht->user, reinterpret_cast<int (*)(void*, double*, size_t)>(ht->allreduce_f64),
+                      reinterpret_cast<int (*)(void*, const void*, void*, size_t)>(ht->allgather_bytes)};
+      c->comm = make_host_comm(t, world, rank, &e);
     } else {
       if (!nccl_id) return bail(fail(c, PHD_EINVAL, "nccl_id required for world > 1"));
       c->comm = make_nccl_comm(nccl_id, world, rank, &e);
@@ -643,6 +648,12 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
 phd_status phd_create(const phd_params* p, int32_t rank, int32_t world, const uint8_t* nccl_id, int32_t device,
                       void* stream, void* workspace, phd_ctx** out) {
   return create_impl(p, rank, world, nccl_id, nullptr, device, stream, workspace, out);
+}
+
+phd_status phd_create_with_transport(const phd_params* p, int32_t rank, int32_t world, const phd_host_transport* t,
+                                     int32_t device, void* stream, void* workspace, phd_ctx** out) {
+  if (!t) return PHD_EINVAL;
+  return create_impl(p, rank, world, nullptr, nullptr, device, stream, workspace, out, t);
 }
 
 phd_status phd_create_in_group(const phd_params* p, phd_group* g, int32_t rank, int32_t device, void* stream,
