@@ -196,7 +196,6 @@ struct phd_ctx {
   double* h_meta = nullptr;  // [16 + 2 world + 2]
   phd_estimate* h_est = nullptr;
   float* h_z = nullptr;
-  int32_t* h_slot = nullptr;
   // step state
   int stage = kResampled;
   bool populated = false;
@@ -593,7 +592,6 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   CUB(cudaMallocHost(&c->h_est, sizeof(phd_estimate) * (p->max_meas + 1)));
   if (c->dcp) CUB(cudaMallocHost(&c->h_gather, sizeof(phd_estimate) * (p->max_meas + 1) * world));
   CUB(cudaMallocHost(&c->h_z, sizeof(float) * 2 * (p->max_meas + 1)));
-  CUB(cudaMallocHost(&c->h_slot, sizeof(int32_t) * L.slots_max));
   for (int i = 0; i < 16; ++i) CUB(cudaEventCreate(&c->ev[i]));
   // derived model constants (fp32 for the pair kernels, fp64 for kappa)
   double s0 = p->sigma_z[0], s1 = p->sigma_z[1];
@@ -675,7 +673,6 @@ void phd_destroy(phd_ctx* c) {
   if (c->h_est) cudaFreeHost(c->h_est);
   if (c->h_gather) cudaFreeHost(c->h_gather);
   if (c->h_z) cudaFreeHost(c->h_z);
-  if (c->h_slot) cudaFreeHost(c->h_slot);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -975,26 +972,13 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
   return PHD_OK;
 }
 
+// Slot layout parameters of the dense passes: a function of M only (the slot -> label map
+// itself is built on the device by k_build_slots).  Range-bearing: measurements grouped by
+// bearing class with pair padding (<= M + 3 slots), room for the pass-2 layout (M + 6).
 static phd_status build_slots(phd_ctx* c, int M) {
-  // slot -> label map; range-bearing: measurements grouped by bearing class so
-  // that every f32x2 slot pair uses one bearing representation
-  int n = 0;
-  if (c->model == kRangeBearing) {
-    const float hp = 1.57079632679489662f;
-    for (int cls = 0; cls < 3; ++cls) {
-      for (int l = 0; l < M; ++l) {
-        float t = c->h_z[2 * l + 1];
-        int r = t > hp ? 1 : (t < -hp ? 2 : 0);
-        if (r == cls) c->h_slot[n++] = l;
-      }
-      if (n & 1) c->h_slot[n++] = -1;
-    }
-  } else {
-    for (int l = 0; l < M; ++l) c->h_slot[n++] = l;
-  }
+  int n = M;
+  if (c->model == kRangeBearing && M > 0) n = M + 6;
   c->n_slots = n;
-  const int n_fill = n;  // slots [n_fill, slots_pad) are padding
-  if (c->model == kRangeBearing && M > 0) n = std::max(n, M + 6);  // room for the pass-2 layout (k_select_slots)
   {
   // slots per lane: 8 (halves the per-particle overheads) unless it pads much more than 4;
   // warps per CTA: the fewest padded slots among {the warps needed, 8, 4, 2} (ties: more
@@ -1040,7 +1024,6 @@ static phd_status build_slots(phd_ctx* c, int M) {
   if (c->slots_pad > c->L.slots_max || c->zb > c->L.zb_max)
     return fail(c, PHD_ECAPACITY, "slot layout %d slots / %d z-blocks exceeds %d / %d", c->slots_pad, c->zb,
                 c->L.slots_max, c->L.zb_max);
-  for (int s = n_fill; s < c->slots_pad; ++s) c->h_slot[s] = -1;
   return PHD_OK;
 }
 
@@ -1051,7 +1034,6 @@ static void gate_slots(phd_ctx* c, int M) {
   c->zl = 4;
   c->wz = kMinWarpsZ;
   c->zb = M > 0 ? 1 : 0;
-  for (int s = 0; s < c->slots_pad; ++s) c->h_slot[s] = s < M ? s : -1;
 }
 
 // Sort the particles by cell, bin Z_k, count every tile's candidates; decide
@@ -1115,20 +1097,16 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (M > 0 && !z) return fail(c, PHD_EINVAL, "z is NULL");
   timing_record(c, 2);
   c->M = M;
-  bool h_z_valid = true;
   if (M > 0) {
     cudaPointerAttributes pa{};
     bool dev = cudaPointerGetAttributes(&pa, z) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
     cudaGetLastError();
-    if (dev) {
-      // device-resident Z: stays on the device (no host round trip) unless the
-      // dense range-bearing slot layout needs it on the host (build_slots)
+    if (dev) {  // device-resident Z stays on the device (the slot layout is built there)
       CU(cudaMemcpyAsync(c->zlab, z, sizeof(float) * 2 * M, cudaMemcpyDeviceToDevice, c->st));
     } else {
       memcpy(c->h_z, z, sizeof(float) * 2 * M);
       CU(cudaMemcpyAsync(c->zlab, c->h_z, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, c->st));
     }
-    h_z_valid = !dev;
   }
   c->M_z = M;
   const int64_t n = c->n_local;
@@ -1148,10 +1126,6 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (st != PHD_OK) return st;
   }
   c->gated = gated;
-  if (!gated && c->model == kRangeBearing && M > 0 && !h_z_valid) {
-    CU(cudaMemcpyAsync(c->h_z, c->zlab, sizeof(float) * 2 * M, cudaMemcpyDeviceToHost, c->st));
-    CU(cudaStreamSynchronize(c->st));
-  }
   if (gated) {
     gate_slots(c, M);
   } else {
@@ -1159,11 +1133,10 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (st != PHD_OK) return st;
   }
   const int64_t tiles = ceil_div(n, kTileP);
-  if (M > 0) {
-    CU(cudaMemcpyAsync(c->slot_label, c->h_slot, sizeof(int32_t) * c->slots_pad, cudaMemcpyHostToDevice, c->st));
+  if (M > 0) {  // slot -> label map and per-slot constants, on the device
     SlotConsts sc{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
-    KL(launch_zprep(c->model, c->zlab, c->slot_label, c->slots_pad, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->st,
-                    c->bad));
+    KL(launch_build_slots(c->zlab, nullptr, M, c->model, gated ? 1 : 0, c->slots_pad, c->slot_label,
+                          (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->bad, c->st));
   }
   // particle-CTA count: one wave of resident CTAs over the z-blocks of one sweep
   int gp = 0;

@@ -185,6 +185,10 @@ cudaError_t launch_predict(const PredictArgs& a, cudaStream_t s);
 cudaError_t launch_birth_is(const BirthISArgs& a, cudaStream_t s);
 cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, float sy, float* rb,
                            int64_t stride, cudaStream_t s);
+// pass-1 slot layout + per-slot constants on the device (k_build_slots, k_select.cu)
+cudaError_t launch_build_slots(const float* z, const int* Mp, int M, int model, int identity, int slots_pad,
+                               int32_t* slot_label, float sensor_x, float sensor_y, SlotConsts sc, int* bad,
+                               cudaStream_t s);
 cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad,
                          float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s, int* bad = nullptr);
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
