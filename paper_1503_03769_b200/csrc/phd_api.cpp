@@ -52,7 +52,7 @@ struct Layout {
   size_t total = 0;
   // byte offsets
   size_t o_A[5], o_B[5], o_wn, o_rb, o_rec, o_P, o_Cpart, o_Apart, o_zlab, o_zprev, o_slot, o_s[5], o_rep, o_C, o_Cslot, o_sel, o_selinfo, o_D,
-      o_acc, o_blk_w, o_blk_wp, o_blk_off, o_ctot, o_coff, o_counter, o_marks, o_bmax, o_anc, o_est, o_gather, o_ring, o_summ, o_bad;
+      o_acc, o_blk_w, o_blk_wp, o_blk_off, o_ctot, o_coff, o_counter, o_anc, o_step, o_est, o_gather, o_ring, o_summ, o_bad;
   // gated update (p->gate != 0)
   int64_t g_npad = 0, g_ecap = 0, g_hist = 0, g_scan = 0;
   int g_ntiles = 0, g_nsorted = 0;
@@ -111,9 +111,8 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_ctot = take(sizeof(double) * (L.nbw_max / kResScanChunk + 2));
   L.o_coff = take(sizeof(double) * (L.nbw_max / kResScanChunk + 3));
   L.o_counter = take(sizeof(unsigned) * 4);
-  L.o_marks = take(sizeof(int32_t) * L.cap_off);
-  L.o_bmax = take(sizeof(int32_t) * L.nbo_max);
   L.o_anc = take(sizeof(int32_t) * L.cap_off);
+  L.o_step = take(sizeof(DevStep));
   L.o_est = take(sizeof(phd_estimate) * (size_t)(p->max_meas + 1));  // [0] header (count), [1..] estimates
   L.o_gather = take(p->mode == PHD_MODE_DCP ? sizeof(phd_estimate) * (size_t)(p->max_meas + 1) * world : 256);
   L.o_summ = take(sizeof(double) * 16);
@@ -180,10 +179,11 @@ struct phd_ctx {
   int32_t* slot_label;
   float* s[5];   // s0, s1, s2, s3, d
   int32_t* rep;
-  double *C, *D, *acc;
+  double *C, *D, *acc, *rslots;
   double *blk_w, *blk_wp, *blk_off, *ctot, *coff;
   unsigned* scan_counter;
-  int32_t *marks, *bmax, *anc;
+  int32_t* anc;
+  DevStep* dstep;          // graph replays: this step's scalars on the device
   phd_estimate* est;      // gather block: est[0].label = count, est[1..] = estimates
   phd_estimate* gather;   // DCP: every rank's gather block
   phd_estimate* h_gather = nullptr;
@@ -536,15 +536,17 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   c->sel_info = at<double>(c->ws, L.o_selinfo);
   c->s_lim = reinterpret_cast<int32_t*>(c->sel_info + 6);
   c->D = at<double>(c->ws, L.o_D);
-  c->acc = at<double>(c->ws, L.o_acc);
+  // C2 buffer: the rank slots [W_r | W_pred_r | N_r] (3 per rank) first, at a fixed
+  // offset, then the label accumulators [M][5] -- one contiguous all-reduce of 3W + 5M
+  c->rslots = at<double>(c->ws, L.o_acc);
+  c->acc = c->rslots + align_up((size_t)3 * world, 4);
   c->blk_w = at<double>(c->ws, L.o_blk_w);
   c->blk_wp = at<double>(c->ws, L.o_blk_wp);
   c->blk_off = at<double>(c->ws, L.o_blk_off);
   c->ctot = at<double>(c->ws, L.o_ctot);
   c->coff = at<double>(c->ws, L.o_coff);
   c->scan_counter = at<unsigned>(c->ws, L.o_counter);
-  c->marks = at<int32_t>(c->ws, L.o_marks);
-  c->bmax = at<int32_t>(c->ws, L.o_bmax);
+  c->dstep = at<DevStep>(c->ws, L.o_step);
   c->anc = at<int32_t>(c->ws, L.o_anc);
   c->est = at<phd_estimate>(c->ws, L.o_est);
   c->gather = at<phd_estimate>(c->ws, L.o_gather);
@@ -1260,7 +1262,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
                        c->gso.inv));
   else if (n > 0)
     KL(launch_finalize(c->A[4], c->P, c->L.cap_l, M > 0 && gp > 0 ? c->zb : 0, n, c->nu, c->wscale, c->wn, c->blk_w, c->blk_wp, c->st));
-  double* rank_slots = c->acc + 5 * (size_t)M;
+  double* rank_slots = c->rslots;
   KL(launch_reduce_acc(gated ? c->gA : c->Apart, gated ? 1 : gp, c->slots_pad, M > 0 ? c->slots_pad : 0, c->slot_label, c->C, c->D, c->s[0],
                        c->s[1], c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank,
                        c->world, c->dcp || c->rank == 0 ? 1 : 0, c->select ? c->sel_flag : nullptr, c->st,
@@ -1273,7 +1275,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (c->dcp)  // groups keep their own accumulators; only the per-group masses are shared
       COMM(c->comm->allreduce_f64(rank_slots, (size_t)(3 * c->world), c->st));
     else
-      COMM(c->comm->allreduce_f64(c->acc, (size_t)(5 * M + 3 * c->world), c->st));
+      COMM(c->comm->allreduce_f64(c->rslots, (size_t)(c->acc - c->rslots) + 5 * (size_t)M, c->st));
   }
   CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 3 * c->world, cudaMemcpyDeviceToHost, c->st));
   CU(cudaMemcpyAsync(c->h_meta + 3 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
@@ -1399,7 +1401,7 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_extract needs an updated population");
   int nest = 0;
   int lt_clamped = 0;
-  double* rank_slots = c->acc + 5 * (size_t)c->M;
+  double* rank_slots = c->rslots;
   double* smh = c->h_meta + 3 * c->world + 4;
   if (c->dcp) {
     // every group extracts locally (Step 3); the CU (rank 0) fuses (Step 4)
@@ -1590,21 +1592,23 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   const float w_off = n_out > 0 ? (float)(W / (double)n_out) : 0.0f;
   const int64_t n = c->n_local;
   const int nbw = (int)ceil_div(n, kBlockW);
-  ResampleArgs ra{};
-  if (!c->zero_mass && nprod > 0) {
-    KL(launch_scan_chunks(c->blk_w, nbw, c->blk_off, c->ctot, c->coff, c->scan_counter, c->st));
-    ra.n_local = n;
-    ra.g0 = c->g0;
-    ra.w = c->wn;
-    ra.blk_off = c->blk_off;
-    ra.O_r = O_r;
-    ra.scale = (double)n_out / W;
-    ra.U = U;
-    ra.lo = lo;
-    ra.hi = hi;
-  }
   // systematic resampling + gather in one kernel (k_resample_gather); zero mass: the
-  // deterministic spread of k_gather
+  // deterministic spread (offspring j copies particle floor(j N / n_out), weight 0)
+  ResampleArgs ra{};
+  ra.n_local = n;
+  ra.g0 = c->g0;
+  ra.w = c->wn;
+  ra.blk_off = c->blk_off;
+  ra.O_r = O_r;
+  ra.scale = c->zero_mass ? 0.0 : (double)n_out / W;
+  ra.U = U;
+  ra.lo = lo;
+  ra.hi = hi;
+  ra.zero_mass = c->zero_mass ? 1 : 0;
+  ra.n_upd = c->dcp ? c->n_local : c->N;
+  ra.n_out = n_out;
+  if (!c->zero_mass && nprod > 0)
+    KL(launch_scan_chunks(c->blk_w, nbw, c->blk_off, c->ctot, c->coff, c->scan_counter, c->st));
   if (!c->dcp && c->world > 1 && c->p2p_state == 0) {
     phd_status st = p2p_setup(c);
     if (st != PHD_OK) return st;
@@ -1623,17 +1627,9 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
       for (int i = 0; i < 5; ++i) po.dst[q][i] = base + (size_t)i * c->L.cap_l;
     }
     po.blo[c->world] = n_out + J;
-    if (c->zero_mass)
-      KL(launch_gather_p2p(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, po, c->anc,
-                           c->zero_mass, lo, c->N, n_out, c->st));
-    else if (nprod > 0)
-      KL(launch_resample_gather(rg_args(c, ra, w_off), &po, c->st));
+    if (nprod > 0) KL(launch_resample_gather(rg_args(c, ra, w_off), &po, c->st));
   } else {
-    if (c->zero_mass)
-      KL(launch_gather(c->marks, c->bmax, nprod, c->g0, c->A[0], c->A[1], c->A[2], c->A[3], w_off, c->B[0], c->B[1],
-                       c->B[2], c->B[3], c->B[4], c->anc, c->zero_mass, lo, c->dcp ? c->n_local : c->N, n_out, c->st));
-    else if (nprod > 0)
-      KL(launch_resample_gather(rg_args(c, ra, w_off), nullptr, c->st));
+    if (nprod > 0) KL(launch_resample_gather(rg_args(c, ra, w_off), nullptr, c->st));
   }
   timing_record(c, 11);
   // exchange: the next step's survivors [0, n_out) are block-partitioned over N' = n_out + J

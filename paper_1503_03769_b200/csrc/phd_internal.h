@@ -151,17 +151,30 @@ cudaError_t launch_init_population(const InitArgs& a, cudaStream_t s);
 // second pass (mass box): w = total_mass / count inside, 0 outside
 cudaError_t launch_init_weights(const InitArgs& a, cudaStream_t s);
 
+// Per-step scalars of a CUDA-graph replay of phd_step (world 1, DESIGN.md §4 "graph
+// step"): the host stages k, M, M_prev (copied by the graph's first node); the
+// resampling setup kernel (k_resample_setup) fills the rest from the update's results.
+// Kernels read them when handed a DevStep pointer, their by-value arguments otherwise.
+struct DevStep {
+  int32_t k, M, M_prev, zero_mass;
+  int64_t n_out;             // offspring of this step's resampling
+  double U, W, scale;        // resampling offset, mass, n_out / W
+  float w_off;               // offspring weight W / n_out
+  int32_t count_clamped;
+};
+
 struct ResampleArgs {
   int64_t n_local;
   int64_t g0;
   const float* w;            // updated weights
-  const double* blk_off;     // exclusive prefix of block sums (nb + 1 entries)
+  const double* blk_off;     // exclusive prefix of block sums (within its scan chunk)
   double O_r;                // exclusive prefix of the per-rank masses
   double scale;              // n_out / W
   double U;
   int64_t lo, hi;            // bounds[r], bounds[r+1]
-  int32_t* marks;            // [hi - lo]
-  int32_t* bmax;             // [ceil((hi - lo) / kBlockOff)], preset to -1: max mark per offspring block
+  int zero_mass;             // W == 0: particle g gets [ceil(g n_out / N), ceil((g+1) n_out / N))
+  int64_t n_upd, n_out;      // N (global particles updated) and n_out, for the zero-mass spread
+  const DevStep* ds;         // graph replay: lo = 0, hi = n_out, scale, U, zero_mass from here (world 1)
 };
 
 // Eq 6 importance weights of the births (birth_model 2): local slots [i0, i0 + nb)
@@ -252,13 +265,6 @@ cudaError_t launch_ring_pack(float* const* src, float* const* dst, int narr, int
                              cudaStream_t s);
 cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
                                cudaStream_t s);
-cudaError_t launch_scan_blocks(const double* blk, int nb, double* blk_off, cudaStream_t s);
-cudaError_t launch_resample_mark(const ResampleArgs& a, cudaStream_t s);
-cudaError_t launch_scan_max(int32_t* bmax, int nb, cudaStream_t s);
-cudaError_t launch_gather(const int32_t* marks, const int32_t* bmax_excl, int64_t n, int64_t g0,
-                          const float* x, const float* vx, const float* y, const float* vy, float w_off,
-                          float* ox, float* ovx, float* oy, float* ovy, float* ow, int32_t* anc,
-                          int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out, cudaStream_t s);
 // fused resample + exchange (world > 1, peer-memory window)
 constexpr int kMaxPeers = 16;
 // Resampling + gather in one kernel (k_resample_gather): the block offsets are
@@ -268,7 +274,7 @@ struct ResampleGatherArgs {
   ResampleArgs r;            // weights, O_r, scale, U, produced range [lo, hi); r.blk_off = loc
   const double* coff;        // [nchunks + 1] chunk offsets
   const float *x, *vx, *y, *vy;  // predicted states (local)
-  float w_off;               // offspring weight W / n_out
+  float w_off;               // offspring weight W / n_out (graph replay: ds->w_off)
   float *ox, *ovx, *oy, *ovy, *ow;  // local outputs at the produced index (p2p == 0)
   int32_t* anc;              // [produced]: global ancestor
 };
@@ -278,16 +284,21 @@ cudaError_t launch_scan_chunks(const double* blk, int nb, double* loc, double* c
                                cudaStream_t s);
 struct PeerOut;
 cudaError_t launch_resample_gather(const ResampleGatherArgs& a, const PeerOut* po, cudaStream_t s);
+// graph replay (world 1): n_out, U, W, scale, w_off, zero_mass of this step into ds
+struct SetupArgs {
+  const double* rslots;      // rank slots [W_r | ...] (C2 buffer)
+  const double* sel_info;    // (W by the mass identity, LT, ...) of k_select_slots
+  int fixed;                 // count mode fixed
+  int64_t fixed_count, R, lim;  // N_out (fixed), particles per target, capacity - J (adaptive)
+  uint64_t seed;
+};
+cudaError_t launch_resample_setup(const SetupArgs& a, DevStep* ds, cudaStream_t s);
 
 struct PeerOut {
   float* dst[kMaxPeers][5];   // owner q's next-step arrays x, vx, y, vy, w (peer pointers)
   int64_t blo[kMaxPeers + 1]; // next-step block partition of N' = n_out + J
   int world;
 };
-cudaError_t launch_gather_p2p(const int32_t* marks, const int32_t* bmax_excl, int64_t n, int64_t g0, const float* x,
-                              const float* vx, const float* y, const float* vy, float w_off, const PeerOut& po,
-                              int32_t* anc, int zero_mass, int64_t first, int64_t n_global_upd, int64_t n_out,
-                              cudaStream_t s);
 cudaError_t launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 cudaError_t launch_philox_kat(uint64_t seed, const uint32_t* ctr, int64_t n, uint32_t* out, cudaStream_t s);
 // label selection before pass 2 (k_select.cu)
