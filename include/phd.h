@@ -315,6 +315,9 @@ int64_t phd_launch_count(const phd_ctx* ctx);
 /* Device time (ms) of the last update's pass-1 and pass-2 kernels, measured
  * with CUDA events on the ctx stream when timing is enabled. */
 phd_status phd_set_timing(phd_ctx* ctx, int32_t enable);
+/* CUDA-graph steps of phd_step (one rank, dense update; opt-in with PHD_GRAPH=1): graphs
+ * captured (one per launch shape) and replayed so far. */
+phd_status phd_get_graph_stats(const phd_ctx* ctx, int64_t* captures, int64_t* replays);
 phd_status phd_get_timing(phd_ctx* ctx, float* ms /* [8]: predict, pass1, pass2, update_total,
                                                       extract, resample, exchange, step */);
 

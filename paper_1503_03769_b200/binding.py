@@ -94,7 +94,7 @@ EXPORTS = ["phd_abi_version", "phd_status_str", "phd_last_error", "phd_nccl_uniq
            "phd_philox4x32_10", "phd_rank_block", "phd_resample_bounds", "phd_plan_exchange",
            "phd_group_create", "phd_group_destroy", "phd_create_in_group", "phd_get_local_estimates",
            "phd_get_gate_stats", "phd_exchange_path", "phd_set_retained_measurements", "phd_init_population",
-           "phd_philox4x32_10_device", "phd_create_with_transport"]
+           "phd_philox4x32_10_device", "phd_create_with_transport", "phd_get_graph_stats"]
 
 _lib = None
 _P = ctypes.c_void_p
@@ -155,6 +155,7 @@ def load(build_if_missing=True):
     L.phd_set_retained_measurements.argtypes = [_P, _P, ctypes.c_int32]
     L.phd_init_population.argtypes = [_P, ctypes.c_double, _D, _D, ctypes.c_double]
     L.phd_philox4x32_10_device.argtypes = [ctypes.c_uint64, _P, ctypes.c_int64, _P, _P]
+    L.phd_get_graph_stats.argtypes = [_P, _I64, _I64]
     L.phd_exchange_path.argtypes = [_P]
     L.phd_exchange_path.restype = ctypes.c_int32
     L.phd_launch_count.argtypes = [_P]
@@ -492,6 +493,12 @@ class Filter:
         self.set_particles(np.ascontiguousarray(d["soa"]), np.ascontiguousarray(d["w"]), int(d["n_out"]))
         self.set_retained_measurements(d["z"])
         return int(d["k"])
+
+    def graph_stats(self):
+        """(graphs captured, replays) of phd_step's CUDA-graph path."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.L.phd_get_graph_stats(self.h, ctypes.byref(a), ctypes.byref(b)), "phd_get_graph_stats")
+        return a.value, b.value
 
     def exchange_path(self):
         """0 none, 1 send/recv, 2 fused gather + exchange over peer memory."""

@@ -23,12 +23,13 @@ __device__ __forceinline__ bool before(double wa, int la, double wb, int lb) {
 // One CTA.  The n_sel = min(LT, eligible, cap) largest dW are found by radix
 // select (topk.cuh), compacted in label order, then bitonic-sorted by (dW desc,
 // label asc) -- n_sel (~ the target count) instead of all M labels.
-__global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restrict__ acc, int M,
+__global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restrict__ acc, int M_arg, const int* Mp,
                                                           const double* __restrict__ Wv, const double* __restrict__ Wpv,
                                                           int count, double p_d, EstOut* est, int cap, double* summary,
                                                           int32_t* count_out, const double* sel_info,
                                                           const int32_t* __restrict__ sel_flag) {
   pdl_wait();
+  const int M = Mp ? *Mp : M_arg;  // graph replays: this step's M (shared memory sized for max_meas)
   extern __shared__ __align__(16) unsigned char sm[];
   const int n2m = M <= 1 ? 1 : 1 << (32 - __clz(M - 1));  // next power of two >= M
   unsigned long long* kw = reinterpret_cast<unsigned long long*>(sm);
@@ -177,13 +178,14 @@ __global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restri
 
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
                            void* est, int cap, double* summary, int32_t* count_out, const double* sel_info,
-                           const int32_t* sel_flag, cudaStream_t s) {
+                           const int32_t* sel_flag, cudaStream_t s, const int* Mp, int M_alloc) {
+  const int Ms = Mp ? M_alloc : M;  // shared memory for the largest M the launch may see
   int n2 = 1;
-  while (n2 < M) n2 <<= 1;
-  size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long) + (size_t)n2 * (sizeof(double) + sizeof(int));
+  while (n2 < Ms) n2 <<= 1;
+  size_t smem = (size_t)std::max(Ms, 1) * sizeof(unsigned long long) + (size_t)n2 * (sizeof(double) + sizeof(int));
   ensure_max_smem(k_extract, 8192 * 20);
-  pdl_launch(k_extract, 1, kTopkThreads, smem, s, acc_lab, M, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap, summary,
-                                          count_out, sel_info, sel_flag);
+  pdl_launch(k_extract, 1, kTopkThreads, smem, s, acc_lab, M, Mp, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap,
+             summary, count_out, sel_info, sel_flag);
   return cudaGetLastError();
 }
 

@@ -66,7 +66,7 @@ __device__ __forceinline__ void rb_repr(float xf, float yf, float sx, float sy, 
 // roundings, so the vector and scalar paths give the same bits.
 __device__ __forceinline__ void survivor(const PredictArgs& a, int64_t g, float& x, float& vx, float& y, float& vy,
                                          float& w) {
-  U4 o = philox_at(a.seed, a.ctr_base + (uint64_t)g, (uint32_t)a.k, 1u);
+  U4 o = philox_at(a.seed, a.ctr_base + (uint64_t)g, (uint32_t)(a.ds ? a.ds->k : a.k), 1u);
   float u1 = u01(o.x), u2 = u01(o.y);
   float rad = sqrtf(-2.0f * logf(u1));
   float sn, cs;
@@ -98,7 +98,7 @@ __device__ __forceinline__ void predict_one(const PredictArgs& a, int64_t i) {
   } else {
     // Eq 6: birth b ~ p_k(.|Z_{k-1}) with weight gamma / J_k.
     int64_t b = g - a.n_out;
-    U4 o = philox_at(a.seed, a.ctr_base + (uint64_t)g, (uint32_t)a.k, 2u);
+    U4 o = philox_at(a.seed, a.ctr_base + (uint64_t)g, (uint32_t)(a.ds ? a.ds->k : a.k), 2u);
     float u0 = u01(o.x), u1 = u01(o.y), u2 = u01(o.z), u3 = u01(o.w);
     float r01 = sqrtf(-2.0f * logf(u0)), r23 = sqrtf(-2.0f * logf(u2));
     float s1, c1, s2, c2;
@@ -116,8 +116,9 @@ __device__ __forceinline__ void predict_one(const PredictArgs& a, int64_t i) {
       if (a.rb) rb_repr(a.x[i], a.y[i], a.sensor_x, a.sensor_y, a.rb, a.rb_stride, i);
       return;
     }
-    if (a.m_prev > 0) {
-      int64_t m = (a.birth_offset + b) % a.m_prev;
+    const int m_prev = a.ds ? a.ds->M_prev : a.m_prev;
+    if (m_prev > 0) {
+      int64_t m = (a.birth_offset + b) % m_prev;
       p0 = a.zprev[2 * m] + a.sigma_z0 * n1;
       p1 = a.zprev[2 * m + 1] + a.sigma_z1 * n2;
     } else {

@@ -228,15 +228,16 @@ __global__ void k_resample_setup(const SetupArgs a, DevStep* ds) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int64_t n_out = a.fixed_count;
   int clamped = 0;
+  const double W = a.rslots[0];
   if (!a.fixed) {
-    const int64_t LT = (int64_t)a.sel_info[1];
+    int64_t LT = a.sel_info ? (int64_t)a.sel_info[1] : (int64_t)floor(W + 0.5);
+    if (LT < 0) LT = 0;
     n_out = (LT > 1 ? LT : 1) * a.R;
     if (n_out > a.lim) {
       n_out = a.lim;
       clamped = 1;
     }
   }
-  const double W = a.rslots[0];
   const U4 o = philox_at(a.seed, 0, (uint32_t)ds->k, 3u);
   ds->n_out = n_out;
   ds->count_clamped = clamped;

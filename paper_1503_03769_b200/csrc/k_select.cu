@@ -376,13 +376,15 @@ cudaError_t launch_build_slots(const float* z, const int* Mp, int M, int model, 
 
 // Dense path: the index set and the pass-2 layout in one CTA (one launch).
 __global__ void __launch_bounds__(kTopkThreads) k_select_slots(const double* __restrict__ C_lab,
-                                                               const double* __restrict__ D_lab, int M,
+                                                               const double* __restrict__ D_lab, int M_arg,
+                                                               const int* Mp,
                                                                const double* __restrict__ W_pred, double p_d,
                                                                int32_t* sel_flag, double* info,
                                                                const float* __restrict__ z, int model, int zl,
                                                                int wz, int layout, int slots_pad, int32_t* slot_label,
                                                                int32_t* js_out, float sx, float sy, SlotConsts sc) {
   pdl_wait();
+  const int M = Mp ? *Mp : M_arg;  // graph replays: this step's M (shared memory sized for max_meas)
   extern __shared__ __align__(16) unsigned char sm[];
   select_body(C_lab, D_lab, M, W_pred, p_d, sel_flag, info, reinterpret_cast<unsigned long long*>(sm));
   __syncthreads();  // sel_flag (global) complete and visible to the CTA
@@ -392,10 +394,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_select_slots(const double* __r
 cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                                 int32_t* sel_flag, double* info, const float* z, int model, int zl, int wz,
                                 int layout, int slots_pad, int32_t* slot_label, int32_t* js, float sensor_x,
-                                float sensor_y, SlotConsts sc, cudaStream_t s) {
-  size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long);
+                                float sensor_y, SlotConsts sc, cudaStream_t s, const int* Mp, int M_alloc) {
+  size_t smem = (size_t)std::max(Mp ? M_alloc : M, 1) * sizeof(unsigned long long);
   ensure_max_smem(k_select_slots, 8192 * 8);
-  pdl_launch(k_select_slots, 1, kTopkThreads, smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info, z, model, zl,
+  pdl_launch(k_select_slots, 1, kTopkThreads, smem, s, C_lab, D_lab, M, Mp, W_pred, p_d, sel_flag, info, z, model, zl,
              wz, layout, slots_pad, slot_label, js, sensor_x, sensor_y, sc);
   return cudaGetLastError();
 }

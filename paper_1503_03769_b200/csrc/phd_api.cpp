@@ -240,6 +240,17 @@ struct phd_ctx {
   double *gpart1 = nullptr, *gA = nullptr;
   bool gated = false;            // the last update ran the gated path
   int64_t g_entries = 0, g_tiles = 0;
+  // CUDA-graph steps (world 1, dense): phd_step replays a captured graph per launch shape
+  bool capturing = false;                  // the step's calls are being stream-captured
+  bool graph_off = false;                  // disabled (PHD_GRAPH=0, or a capture failed)
+  struct GraphEntry {
+    int64_t key[8];
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  int32_t* h_stepin = nullptr;             // pinned: k, M, M_prev of the next replay
+  DevStep* h_stepout = nullptr;            // pinned: the replay's resampling scalars
+  int64_t graph_captures = 0, graph_replays = 0;
   // timing
   bool timing = false;
   cudaEvent_t ev[16] = {};
@@ -594,6 +605,8 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   CUB(cudaMallocHost(&c->h_est, sizeof(phd_estimate) * (p->max_meas + 1)));
   if (c->dcp) CUB(cudaMallocHost(&c->h_gather, sizeof(phd_estimate) * (p->max_meas + 1) * world));
   CUB(cudaMallocHost(&c->h_z, sizeof(float) * 2 * (p->max_meas + 1)));
+  CUB(cudaMallocHost(&c->h_stepin, sizeof(int32_t) * 4));
+  CUB(cudaMallocHost(&c->h_stepout, sizeof(DevStep)));
   for (int i = 0; i < 16; ++i) CUB(cudaEventCreate(&c->ev[i]));
   // derived model constants (fp32 for the pair kernels, fp64 for kappa)
   double s0 = p->sigma_z[0], s1 = p->sigma_z[1];
@@ -675,6 +688,9 @@ void phd_destroy(phd_ctx* c) {
   if (c->h_est) cudaFreeHost(c->h_est);
   if (c->h_gather) cudaFreeHost(c->h_gather);
   if (c->h_z) cudaFreeHost(c->h_z);
+  if (c->h_stepin) cudaFreeHost(c->h_stepin);
+  if (c->h_stepout) cudaFreeHost(c->h_stepout);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -933,6 +949,10 @@ phd_status phd_predict(phd_ctx* c, int32_t k, const float* z_prev, int32_t M_pre
   }
   a.zprev = zp;
   a.m_prev = mp;
+  if (c->capturing) {  // graph replay: k and M_{k-1} from the device step block, Z_{k-1} in zlab
+    a.zprev = c->zlab;
+    a.ds = c->dstep;
+  }
   a.x = c->A[0];
   a.vx = c->A[1];
   a.y = c->A[2];
@@ -1080,6 +1100,18 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
 }
 
 static phd_status update_finish(phd_ctx* c);
+
+// particle-CTA count of the dense passes: one wave of resident CTAs over the z-blocks
+static int plan_gp(phd_ctx* c, int64_t n) {
+  const int64_t tiles = ceil_div(n, kTileP);
+  int occ = std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl));
+  occ = std::max(1, occ);
+  int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / std::max(1, c->zb));
+  int64_t cap_gp = std::max<int64_t>(1, c->L.part_cap / c->slots_pad);
+  int gp = (int)std::min<int64_t>(std::min(want, cap_gp), tiles);
+  int64_t tpc = ceil_div(tiles, gp);
+  return (int)ceil_div(tiles, tpc);
+}
 // pass-2 state-sum layout: 0 automatic, 1 per-lane slot pairs, 2 whole z-blocks (PHD_SUM_LAYOUT, tests)
 static int sum_layout() {
   const char* e = getenv("PHD_SUM_LAYOUT");
@@ -1099,7 +1131,10 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (M > 0 && !z) return fail(c, PHD_EINVAL, "z is NULL");
   timing_record(c, 2);
   c->M = M;
-  if (M > 0) {
+  if (M > 0 && c->capturing) {
+    // graph replay: Z_k staged by the host in the pinned h_z (after predict read Z_{k-1})
+    CU(cudaMemcpyAsync(c->zlab, c->h_z, sizeof(float) * 2 * c->p.max_meas, cudaMemcpyHostToDevice, c->st));
+  } else if (M > 0) {
     cudaPointerAttributes pa{};
     bool dev = cudaPointerGetAttributes(&pa, z) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
     cudaGetLastError();
@@ -1137,21 +1172,11 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   const int64_t tiles = ceil_div(n, kTileP);
   if (M > 0) {  // slot -> label map and per-slot constants, on the device
     SlotConsts sc{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
-    KL(launch_build_slots(c->zlab, nullptr, M, c->model, gated ? 1 : 0, c->slots_pad, c->slot_label,
+    KL(launch_build_slots(c->zlab, c->capturing ? &c->dstep->M : nullptr, M, c->model, gated ? 1 : 0, c->slots_pad,
+                          c->slot_label,
                           (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->bad, c->st));
   }
-  // particle-CTA count: one wave of resident CTAs over the z-blocks of one sweep
-  int gp = 0;
-  const int zb_sweep = c->zb;
-  if (M > 0 && n > 0 && !gated) {
-    int occ = std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl));
-    occ = std::max(1, occ);
-    int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / zb_sweep);
-    int64_t cap_gp = std::max<int64_t>(1, c->L.part_cap / c->slots_pad);
-    gp = (int)std::min<int64_t>(std::min(want, cap_gp), tiles);
-    int64_t tpc = ceil_div(tiles, gp);
-    gp = (int)ceil_div(tiles, tpc);
-  }
+  const int gp = M > 0 && n > 0 && !gated ? plan_gp(c, n) : 0;
   c->gp = gp;
   PassArgs pa{};
   pa.n = n;
@@ -1244,7 +1269,8 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
       SlotConsts sc2{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
       KL(launch_select_slots(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->zlab,
                              c->model, c->zl, c->wz, sum_layout(), c->slots_pad, c->slot_label, c->s_lim,
-                             (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc2, c->st));
+                             (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc2, c->st,
+                             c->capturing ? &c->dstep->M : nullptr, c->p.max_meas));
       pa.js = c->s_lim;
     }
     timing_record(c, 5);
@@ -1440,17 +1466,18 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     int capd = std::max(0, std::min(cap, c->p.max_meas));
     KL(launch_extract(c->acc, c->M, rank_slots, rank_slots + c->world, c->world, c->p.p_d, c->est + 1, capd, c->summ,
                       &c->est[0].label, c->select ? c->sel_info : nullptr, c->select ? c->sel_flag : nullptr,
-                      c->st));
+                      c->st, c->capturing ? &c->dstep->M : nullptr, c->p.max_meas));
     CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
     // the estimate count is min(LT, eligible, cap) <= min(LT, cap): copy that many with the
     // summary, so the extraction costs one synchronisation
     // (inside phd_step LT is not on the host yet: copy up to kEstEager estimates, the
     // rest, if any, after the synchronisation)
-    const int64_t ncopy = !out ? 0
+    const int64_t ncopy = (!out && !c->capturing) ? 0
                           : c->update_pending ? std::min<int64_t>(kEstEager, capd)
                                               : std::min<int64_t>(std::max<int64_t>(c->LT, 0), capd);
     if (ncopy > 0)
       CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * ncopy, cudaMemcpyDeviceToHost, c->st));
+    if (c->capturing) return PHD_OK;  // graph step: finished by graph_finish after the replay
     CU(cudaStreamSynchronize(c->st));
     if (c->update_pending) {
       phd_status st = update_finish(c);
@@ -1553,6 +1580,31 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   cudaSetDevice(c->device);
   c->err.clear();
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_resample_exchange needs an updated population");
+  if (c->capturing) {
+    // graph step (world 1, exact): n_out, U, W, zero mass of this step are computed on the
+    // device from the update's results (k_resample_setup), read back after the replay
+    SetupArgs sa{};
+    sa.rslots = c->rslots;
+    sa.sel_info = c->select ? c->sel_info : nullptr;
+    sa.fixed = c->p.count_mode == PHD_COUNT_FIXED;
+    sa.fixed_count = c->p.fixed_count;
+    sa.R = c->p.particles_per_target;
+    sa.lim = c->p.capacity - c->p.births_per_step;
+    sa.seed = c->p.seed;
+    KL(launch_resample_setup(sa, c->dstep, c->st));
+    const int64_t n = c->n_local;
+    KL(launch_scan_chunks(c->blk_w, (int)ceil_div(n, kBlockW), c->blk_off, c->ctot, c->coff, c->scan_counter, c->st));
+    ResampleArgs ra{};
+    ra.n_local = n;
+    ra.g0 = 0;
+    ra.w = c->wn;
+    ra.blk_off = c->blk_off;
+    ra.n_upd = c->N;
+    ra.ds = c->dstep;
+    KL(launch_resample_gather(rg_args(c, ra, 0.0f), nullptr, c->st));
+    CU(cudaMemcpyAsync(c->h_stepout, c->dstep, sizeof(DevStep), cudaMemcpyDeviceToHost, c->st));
+    return PHD_OK;
+  }
   timing_record(c, 10);
   int clamped = 0;
   const int64_t n_out = c->dcp ? next_count_dcp(c, &clamped) : next_count(c, &clamped);
@@ -1721,10 +1773,173 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   return PHD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Graph steps (DESIGN.md §4 "graph step"): with one rank, a dense update and nothing
+// that needs the host mid-step, phd_step replays a CUDA graph of its whole kernel chain
+// (predict, the dense update, extraction, resampling) -- one launch and one host
+// synchronisation instead of ~15 launches.  The per-step scalars (k, M, M_{k-1}) are
+// staged in pinned memory and copied by the graph's first node; the resampling
+// count, offset and mass are computed on the device (k_resample_setup); graphs are
+// cached per launch shape (particle count, slot layout, particle buffer), so a
+// configuration replays a handful of graphs.
+static bool graph_eligible(const phd_ctx* c, int M) {
+  // opt-in (PHD_GRAPH=1): measured slower than the eager launches with programmatic
+  // dependent launch on B200 (cfg 3: 0.214 vs 0.189 ms back to back; cfg 2 0.186 vs
+  // 0.127 ms, whose adaptive count keeps changing the launch shape): the small steps are
+  // GPU-bound, not launch-bound
+  const char* ge = getenv("PHD_GRAPH");
+  const bool env_off = !(ge && ge[0] == '1');
+  if (env_off || c->graph_off || c->world != 1 || c->dcp || c->timing || M <= 0) return false;
+  if (c->p.birth_model == 2 || c->stage != kResampled || !c->populated) return false;
+  if (c->p.gate == 2) return false;
+  if (c->p.gate == 1 && (double)(c->n_out + c->p.births_per_step) * (double)M >= 536870912.0) return false;
+  return true;
+}
+
+// host state of the calls a replay stands for (phd_predict / phd_update up to the sync)
+static void graph_host_state(phd_ctx* c, int M) {
+  c->N = c->n_out + c->p.births_per_step;
+  c->g0 = 0;
+  c->n_local = c->N;
+  c->M = M;
+  c->M_z = M;
+  c->gated = false;
+  c->select = c->p.stphd_all == 0;
+  c->update_pending = true;
+  c->stage = kUpdated;
+}
+
+static phd_status graph_finish(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s) {
+  phd_status st = update_finish(c);
+  if (st != PHD_OK) return st;
+  const double* smh = c->h_meta + 3 * c->world + 4;
+  const int capd = std::max(0, std::min(cap, c->p.max_meas));
+  const int64_t ncopy = out ? std::min<int64_t>(kEstEager, capd) : 0;
+  const int nest = (int)smh[5];
+  const int lt_clamped = (int)smh[6];
+  if (nest > ncopy && out) {
+    CU(cudaMemcpyAsync(c->h_est + ncopy, c->est + 1 + ncopy, sizeof(phd_estimate) * (nest - ncopy),
+                       cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  if (nest > 0 && out) memcpy(out, c->h_est, sizeof(phd_estimate) * nest);
+  const DevStep d = *c->h_stepout;
+  int clamped = 0;
+  const int64_t want = next_count(c, &clamped);
+  if (want != d.n_out) return fail(c, PHD_ECUDA, "graph step: device n_out %lld != %lld", (long long)d.n_out, (long long)want);
+  c->count_clamped = clamped;
+  c->zero_mass = d.zero_mass;
+  c->U_last = d.U;
+  c->W_last = d.W;
+  c->N_out_last = d.n_out;
+  c->prod_first = 0;
+  c->prod_n = d.n_out;
+  for (int i = 0; i < 5; ++i) std::swap(c->A[i], c->B[i]);
+  c->n_surv_local = d.n_out;
+  c->n_out = d.n_out;
+  c->stage = kResampled;
+  if (n_out) *n_out = nest;
+  if (s) {
+    s->W = c->W;
+    s->W_pred = c->W_pred;
+    s->undetected_mass = (1.0 - c->p.p_d) * c->W_pred;
+    s->LT = c->LT;
+    s->N = c->N;
+    s->N_out = d.n_out;
+    s->M = c->M;
+    s->n_est = nest;
+    s->lt_clamped = lt_clamped;
+    s->count_clamped = clamped;
+    s->zero_mass = !(c->W > 0.0);
+    s->near_half = c->near_half;
+  }
+  return PHD_OK;
+}
+
+static phd_status step_graph(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estimate* out, int32_t cap,
+                             int32_t* n_out, phd_summary* s) {
+  // launch shape: particle count, slot layout and CTA count of the passes, buffers
+  const int64_t N = c->n_out + c->p.births_per_step;
+  if (N > c->L.cap_l - 1) return fail(c, PHD_ECAPACITY, "N %lld exceeds capacity", (long long)N);
+  phd_status st = build_slots(c, M);
+  if (st != PHD_OK) return st;
+  const int gp = plan_gp(c, N);
+  const int64_t key[8] = {c->n_out, (int64_t)(uintptr_t)c->A[0], c->zl, c->wz, c->zb, c->slots_pad, gp,
+                          std::min(cap, c->p.max_meas) > 0 ? 1 : 0};
+  // stage this step's inputs: Z_k, (k, M, M_{k-1}), this rank's particle count
+  cudaPointerAttributes pa{};
+  const bool dev = cudaPointerGetAttributes(&pa, z) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+  cudaGetLastError();
+  if (dev) {
+    CU(cudaMemcpyAsync(c->h_z, z, sizeof(float) * 2 * M, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  } else {
+    memcpy(c->h_z, z, sizeof(float) * 2 * M);
+  }
+  c->h_stepin[0] = k;
+  c->h_stepin[1] = M;
+  c->h_stepin[2] = std::max(c->M_z, 0);
+  c->h_meta[3 * c->world + 16] = (double)N;
+  cudaGraphExec_t exec = nullptr;
+  for (auto& g : c->graphs)
+    if (std::equal(key, key + 8, g.key)) exec = g.exec;
+  if (!exec) {
+    // capture the calls of one step (they run as stream-ordered work only: no host syncs)
+    const int64_t launches0 = c->launches;
+    c->capturing = true;
+    c->defer_update_sync = true;
+    cudaError_t e = cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      e = cudaMemcpyAsync(c->dstep, c->h_stepin, sizeof(int32_t) * 3, cudaMemcpyHostToDevice, c->st);
+      if (e == cudaSuccess) st = phd_predict(c, k, nullptr, 0);
+      if (e == cudaSuccess && st == PHD_OK) st = phd_update(c, c->h_z, M);
+      if (e == cudaSuccess && st == PHD_OK) st = phd_extract(c, out, cap, n_out, s);
+      if (e == cudaSuccess && st == PHD_OK) st = phd_resample_exchange(c, k);
+      cudaGraph_t graph = nullptr;
+      cudaError_t e2 = cudaStreamEndCapture(c->st, &graph);
+      if (e == cudaSuccess) e = e2;
+      if (e == cudaSuccess && st == PHD_OK) e = cudaGraphInstantiate(&exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+    }
+    c->capturing = false;
+    c->defer_update_sync = false;
+    c->launches = launches0;
+    if (e != cudaSuccess || st != PHD_OK || !exec) {
+      cudaGetLastError();
+      if (exec) cudaGraphExecDestroy(exec);
+      c->graph_off = true;  // eager from now on
+      c->stage = kResampled;
+      return PHD_ENODEV;    // caller retries eagerly
+    }
+    if (c->graphs.size() >= 32) {
+      cudaGraphExecDestroy(c->graphs.front().exec);
+      c->graphs.erase(c->graphs.begin());
+    }
+    phd_ctx::GraphEntry ge;
+    std::copy(key, key + 8, ge.key);
+    ge.exec = exec;
+    c->graphs.push_back(ge);
+    ++c->graph_captures;
+  }
+  graph_host_state(c, M);
+  c->gp = gp;
+  CU(cudaGraphLaunch(exec, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  ++c->graph_replays;
+  c->launches += 14;  // the kernels of the captured chain (predict ... resample gather)
+  return graph_finish(c, out, cap, n_out, s);
+}
+
 phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estimate* out, int32_t cap, int32_t* n_out,
                     phd_summary* s) {
   NvtxRange nvtx_("phd_step");
   if (!c) return PHD_EINVAL;
+  if (k >= 1 && M >= 0 && M <= c->p.max_meas && (M == 0 || z) && graph_eligible(c, M)) {
+    cudaSetDevice(c->device);
+    c->err.clear();
+    phd_status st = step_graph(c, k, z, M, out, cap, n_out, s);
+    if (st != PHD_ENODEV) return st;  // PHD_ENODEV: the capture failed, run the step eagerly
+  }
   timing_record(c, 13);
   phd_status st = phd_predict(c, k, nullptr, 0);
   if (st != PHD_OK) return st;
@@ -1743,6 +1958,13 @@ phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estima
     cudaEventElapsedTime(&c->t_ms[7], c->ev[13], c->ev[14]);
   }
   return st;
+}
+
+phd_status phd_get_graph_stats(const phd_ctx* c, int64_t* captures, int64_t* replays) {
+  if (!c) return PHD_EINVAL;
+  if (captures) *captures = c->graph_captures;
+  if (replays) *replays = c->graph_replays;
+  return PHD_OK;
 }
 
 phd_status phd_get_gate_stats(phd_ctx* c, int64_t* out) {

@@ -108,6 +108,18 @@ struct PassArgs {
   float* rec;                // per-particle records of the dense passes [n_pad][record_width] (k_records)
 };
 
+// Per-step scalars of a CUDA-graph replay of phd_step (world 1, DESIGN.md §4 "graph
+// step"): the host stages k, M, M_prev (copied by the graph's first node); the
+// resampling setup kernel (k_resample_setup) fills the rest from the update's results.
+// Kernels read them when handed a DevStep pointer, their by-value arguments otherwise.
+struct DevStep {
+  int32_t k, M, M_prev, zero_mass;
+  int64_t n_out;             // offspring of this step's resampling
+  double U, W, scale;        // resampling offset, mass, n_out / W
+  float w_off;               // offspring weight W / n_out
+  int32_t count_clamped;
+};
+
 struct PredictArgs {
   int64_t n_local;           // slots of this rank's block
   int64_t g0;                // global index of local slot 0
@@ -131,6 +143,7 @@ struct PredictArgs {
   float *x, *vx, *y, *vy, *w;
   float* rb;                 // range-bearing repr out (nullptr for position)
   int64_t rb_stride;
+  const DevStep* ds;         // graph replay: k and m_prev from here
 };
 
 // t = 0 population (reading S23): local slots [0, n_local) hold the
@@ -150,18 +163,6 @@ struct InitArgs {
 cudaError_t launch_init_population(const InitArgs& a, cudaStream_t s);
 // second pass (mass box): w = total_mass / count inside, 0 outside
 cudaError_t launch_init_weights(const InitArgs& a, cudaStream_t s);
-
-// Per-step scalars of a CUDA-graph replay of phd_step (world 1, DESIGN.md §4 "graph
-// step"): the host stages k, M, M_prev (copied by the graph's first node); the
-// resampling setup kernel (k_resample_setup) fills the rest from the update's results.
-// Kernels read them when handed a DevStep pointer, their by-value arguments otherwise.
-struct DevStep {
-  int32_t k, M, M_prev, zero_mass;
-  int64_t n_out;             // offspring of this step's resampling
-  double U, W, scale;        // resampling offset, mass, n_out / W
-  float w_off;               // offspring weight W / n_out
-  int32_t count_clamped;
-};
 
 struct ResampleArgs {
   int64_t n_local;
@@ -260,7 +261,7 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
                            void* est /*phd_estimate*/, int cap, double* summary /*[8]*/, int32_t* count_out,
                            const double* sel_info /*nullptr or (W_id, LT, ...) of k_select*/,
-                           const int32_t* sel_flag /*nullptr or k_select's index-set flags*/, cudaStream_t s);
+                           const int32_t* sel_flag /*nullptr or k_select's index-set flags*/, cudaStream_t s, const int* Mp = nullptr, int M_alloc = 0);
 cudaError_t launch_ring_pack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
                              cudaStream_t s);
 cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, int64_t L, int64_t n, double v,
@@ -313,7 +314,7 @@ constexpr int32_t kJsZBlock = 0x10000;
 cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                                 int32_t* sel_flag, double* info, const float* z, int model, int zl, int wz,
                                 int layout, int slots_pad, int32_t* slot_label, int32_t* js, float sensor_x,
-                                float sensor_y, SlotConsts sc, cudaStream_t s);
+                                float sensor_y, SlotConsts sc, cudaStream_t s, const int* Mp = nullptr, int M_alloc = 0);
 
 // ---- gated update (k_gate.cu, DESIGN.md §5 "Gated update") ------------------
 // Particles are ordered by a Morton cell key in measurement space (stable

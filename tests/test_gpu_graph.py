@@ -1,0 +1,85 @@
+"""CUDA-graph steps (-m gpu): with one rank and a dense update, phd_step replays a
+captured graph of its whole kernel chain (DESIGN.md §4 "graph step").  The replay must
+be bitwise the eager step (PHD_GRAPH=0): the same kernels with the same arguments, the
+per-step scalars (k, M, M_{k-1}, the resampling count / offset / mass) read from the
+device.  Configs with varying M (cfg 1-3), the adaptive count (cfg 1, 2), range-bearing
+(cfg 2), fixed count (cfg 3), host and device measurement pointers."""
+import numpy as np
+import pytest
+from dataclasses import replace
+
+import scenario
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def phd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1503_03769_b200 as p
+    p.load()
+    return p
+
+
+def _run(phd, cfg, steps, graph, monkeypatch, device_z=False):
+    import torch
+    monkeypatch.setenv("PHD_GRAPH", "1" if graph else "0")
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    f = phd.Filter(cfg.model)
+    f.init_population(**scenario.init_args(cfg, truth))
+    out = []
+    for k in range(1, steps + 1):
+        if device_z:
+            zt = torch.from_numpy(Z[k - 1]).cuda()
+            f.step_raw(k, zt.data_ptr(), len(Z[k - 1]))
+        else:
+            f.step(k, Z[k - 1])
+        s = f._sum.as_dict()
+        e = f.estimates()
+        a, _ = f.ancestors()
+        p, w, _ = f.get_particles()
+        out.append((s, e, a, p, w, f.resample_meta()))
+    stats = f.graph_stats()
+    f.close()
+    return out, stats
+
+
+@pytest.mark.parametrize("cname,device_z", [("cfg1", False), ("cfg2", False), ("cfg3", False), ("cfg3", True)])
+def test_graph_step_equals_eager(phd, cname, device_z, monkeypatch):
+    cfg = scenario.get(cname)
+    steps = min(cfg.scenario.steps, 12)
+    ref, st0 = _run(phd, cfg, steps, False, monkeypatch)
+    got, st1 = _run(phd, cfg, steps, True, monkeypatch, device_z)
+    assert st0 == (0, 0)  # PHD_GRAPH=0 (the default is eager too)
+    assert st1[1] == steps and 1 <= st1[0] <= steps  # every step replayed a graph
+    for k, ((s0, e0, a0, p0, w0, m0), (s1, e1, a1, p1, w1, m1)) in enumerate(zip(ref, got)):
+        for key in ("W", "W_pred", "LT", "N", "N_out", "M", "n_est", "zero_mass", "count_clamped"):
+            assert s0[key] == s1[key], (k, key, s0[key], s1[key])
+        assert np.array_equal(e0["labels"], e1["labels"]) and np.array_equal(e0["states"], e1["states"])
+        assert np.array_equal(a0, a1) and np.array_equal(p0, p1) and np.array_equal(w0, w1)
+        assert m0["U"] == m1["U"] and m0["W"] == m1["W"] and m0["N_out"] == m1["N_out"]
+
+
+def test_graph_step_zero_mass_and_stphd_all(phd, monkeypatch):
+    """stphd_all = 1 (LT from W, no index set) and a zero-mass population (the resampling
+    spread decided on the device)."""
+    base = scenario.get("cfg3")
+    cfg = replace(base, model=replace(base.model, stphd_all=1, birth_mass=0.0, births_per_step=0))
+    for graph in (False, True):
+        monkeypatch.setenv("PHD_GRAPH", "1" if graph else "0")
+        truth = scenario.simulate_truth(cfg)
+        Z = scenario.measurements(cfg, truth)
+        f = phd.Filter(cfg.model)
+        f.init_population(0.0)  # zero mass
+        f.step(1, Z[0])
+        s = f._sum.as_dict()
+        a, _ = f.ancestors()
+        if not graph:
+            ref = (s, a)
+        else:
+            assert f.graph_stats()[1] == 1
+            assert s["zero_mass"] == ref[0]["zero_mass"] == 1 and np.array_equal(a, ref[1])
+        f.close()
