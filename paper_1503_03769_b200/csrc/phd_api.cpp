@@ -242,6 +242,10 @@ struct phd_ctx {
   int64_t g_entries = 0, g_tiles = 0;
   // CUDA-graph steps (world 1, dense): phd_step replays a captured graph per launch shape
   bool capturing = false;                  // the step's calls are being stream-captured
+  bool dev_scalars = false;                // one-sync step: resampling scalars on the device,
+                                           // extraction on st2 overlapping the resampling
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   bool graph_off = false;                  // disabled (PHD_GRAPH=0, or a capture failed)
   struct GraphEntry {
     int64_t key[8];
@@ -608,6 +612,9 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   CUB(cudaMallocHost(&c->h_stepin, sizeof(int32_t) * 4));
   CUB(cudaMallocHost(&c->h_stepout, sizeof(DevStep)));
   for (int i = 0; i < 16; ++i) CUB(cudaEventCreate(&c->ev[i]));
+  CUB(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  CUB(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+  CUB(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
   // derived model constants (fp32 for the pair kernels, fp64 for kappa)
   double s0 = p->sigma_z[0], s1 = p->sigma_z[1];
   bool rbm = p->meas == PHD_MEAS_RANGE_BEARING;
@@ -683,6 +690,9 @@ void phd_destroy(phd_ctx* c) {
     if (c->pbuf[b]) cudaFree(c->pbuf[b]);
   for (int i = 0; i < 16; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
+  if (c->st2) cudaStreamDestroy(c->st2);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->h_meta) cudaFreeHost(c->h_meta);
   if (c->h_est) cudaFreeHost(c->h_est);
@@ -1464,20 +1474,31 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
   } else if (c->rank == 0) {
     timing_record(c, 8);
     int capd = std::max(0, std::min(cap, c->p.max_meas));
+    // one-sync step: the extraction runs on st2, overlapping the resampling (it reads the
+    // accumulators only); the resampling joins it before the step's synchronisation
+    cudaStream_t es = c->st;
+    if (c->dev_scalars) {
+      CU(cudaEventRecord(c->fork_ev, c->st));
+      CU(cudaStreamWaitEvent(c->st2, c->fork_ev, 0));
+      es = c->st2;
+    }
     KL(launch_extract(c->acc, c->M, rank_slots, rank_slots + c->world, c->world, c->p.p_d, c->est + 1, capd, c->summ,
                       &c->est[0].label, c->select ? c->sel_info : nullptr, c->select ? c->sel_flag : nullptr,
-                      c->st, c->capturing ? &c->dstep->M : nullptr, c->p.max_meas));
-    CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st));
+                      es, c->capturing ? &c->dstep->M : nullptr, c->p.max_meas));
+    CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, es));
     // the estimate count is min(LT, eligible, cap) <= min(LT, cap): copy that many with the
     // summary, so the extraction costs one synchronisation
     // (inside phd_step LT is not on the host yet: copy up to kEstEager estimates, the
     // rest, if any, after the synchronisation)
-    const int64_t ncopy = (!out && !c->capturing) ? 0
+    const int64_t ncopy = (!out && !c->dev_scalars) ? 0
                           : c->update_pending ? std::min<int64_t>(kEstEager, capd)
                                               : std::min<int64_t>(std::max<int64_t>(c->LT, 0), capd);
     if (ncopy > 0)
-      CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * ncopy, cudaMemcpyDeviceToHost, c->st));
-    if (c->capturing) return PHD_OK;  // graph step: finished by graph_finish after the replay
+      CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * ncopy, cudaMemcpyDeviceToHost, es));
+    if (c->dev_scalars) {  // one-sync step: finished by step_finish after the step's synchronisation
+      CU(cudaEventRecord(c->join_ev, c->st2));
+      return PHD_OK;
+    }
     CU(cudaStreamSynchronize(c->st));
     if (c->update_pending) {
       phd_status st = update_finish(c);
@@ -1580,9 +1601,10 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   cudaSetDevice(c->device);
   c->err.clear();
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_resample_exchange needs an updated population");
-  if (c->capturing) {
-    // graph step (world 1, exact): n_out, U, W, zero mass of this step are computed on the
-    // device from the update's results (k_resample_setup), read back after the replay
+  if (c->dev_scalars) {
+    // one-sync / graph step (world 1, exact): n_out, U, W, zero mass of this step are
+    // computed on the device from the update's results (k_resample_setup), read back after
+    // the step's synchronisation
     SetupArgs sa{};
     sa.rslots = c->rslots;
     sa.sel_info = c->select ? c->sel_info : nullptr;
@@ -1603,6 +1625,7 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     ra.ds = c->dstep;
     KL(launch_resample_gather(rg_args(c, ra, 0.0f), nullptr, c->st));
     CU(cudaMemcpyAsync(c->h_stepout, c->dstep, sizeof(DevStep), cudaMemcpyDeviceToHost, c->st));
+    if (c->rank == 0) CU(cudaStreamWaitEvent(c->st, c->join_ev, 0));  // the extraction on st2
     return PHD_OK;
   }
   timing_record(c, 10);
@@ -1809,7 +1832,9 @@ static void graph_host_state(phd_ctx* c, int M) {
   c->stage = kUpdated;
 }
 
-static phd_status graph_finish(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s) {
+// host side of a one-sync (or graph) step after its synchronisation: the update's
+// bookkeeping, the estimates, the resampling scalars the device computed
+static phd_status step_finish(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_out, phd_summary* s) {
   phd_status st = update_finish(c);
   if (st != PHD_OK) return st;
   const double* smh = c->h_meta + 3 * c->world + 4;
@@ -1887,6 +1912,7 @@ static phd_status step_graph(phd_ctx* c, int32_t k, const float* z, int32_t M, p
     // capture the calls of one step (they run as stream-ordered work only: no host syncs)
     const int64_t launches0 = c->launches;
     c->capturing = true;
+    c->dev_scalars = true;
     c->defer_update_sync = true;
     cudaError_t e = cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
@@ -1902,6 +1928,7 @@ static phd_status step_graph(phd_ctx* c, int32_t k, const float* z, int32_t M, p
       if (graph) cudaGraphDestroy(graph);
     }
     c->capturing = false;
+    c->dev_scalars = false;
     c->defer_update_sync = false;
     c->launches = launches0;
     if (e != cudaSuccess || st != PHD_OK || !exec) {
@@ -1927,18 +1954,51 @@ static phd_status step_graph(phd_ctx* c, int32_t k, const float* z, int32_t M, p
   CU(cudaStreamSynchronize(c->st));
   ++c->graph_replays;
   c->launches += 14;  // the kernels of the captured chain (predict ... resample gather)
-  return graph_finish(c, out, cap, n_out, s);
+  return step_finish(c, out, cap, n_out, s);
+}
+
+// One-sync step (world 1, exact mode): the resampling count / offset / mass are computed
+// on the device (k_resample_setup), so predict -> update -> [extraction on st2 |
+// resampling] run without the host in between and the step synchronises once, at its end.
+static phd_status step_onesync(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estimate* out, int32_t cap,
+                               int32_t* n_out, phd_summary* s) {
+  c->h_stepin[0] = k;
+  c->h_stepin[1] = M;
+  c->h_stepin[2] = std::max(c->M_z, 0);
+  CU(cudaMemcpyAsync(c->dstep, c->h_stepin, sizeof(int32_t) * 3, cudaMemcpyHostToDevice, c->st));
+  c->dev_scalars = true;
+  c->defer_update_sync = true;
+  phd_status st = phd_predict(c, k, nullptr, 0);
+  if (st == PHD_OK) st = phd_update(c, z, M);
+  if (st == PHD_OK) st = phd_extract(c, out, cap, n_out, s);
+  if (st == PHD_OK) st = phd_resample_exchange(c, k);
+  c->dev_scalars = false;
+  c->defer_update_sync = false;
+  if (st != PHD_OK) {
+    cudaStreamSynchronize(c->st2);
+    cudaStreamSynchronize(c->st);
+    return st;
+  }
+  CU(cudaStreamSynchronize(c->st));
+  return step_finish(c, out, cap, n_out, s);
 }
 
 phd_status phd_step(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estimate* out, int32_t cap, int32_t* n_out,
                     phd_summary* s) {
   NvtxRange nvtx_("phd_step");
   if (!c) return PHD_EINVAL;
-  if (k >= 1 && M >= 0 && M <= c->p.max_meas && (M == 0 || z) && graph_eligible(c, M)) {
+  const bool args_ok = k >= 1 && M >= 0 && M <= c->p.max_meas && (M == 0 || z);
+  if (args_ok && graph_eligible(c, M)) {
     cudaSetDevice(c->device);
     c->err.clear();
     phd_status st = step_graph(c, k, z, M, out, cap, n_out, s);
     if (st != PHD_ENODEV) return st;  // PHD_ENODEV: the capture failed, run the step eagerly
+  }
+  if (args_ok && c->world == 1 && !c->dcp && !c->timing && c->populated && c->stage == kResampled &&
+      !(getenv("PHD_ONESYNC") && getenv("PHD_ONESYNC")[0] == '0')) {
+    cudaSetDevice(c->device);
+    c->err.clear();
+    return step_onesync(c, k, z, M, out, cap, n_out, s);
   }
   timing_record(c, 13);
   phd_status st = phd_predict(c, k, nullptr, 0);

@@ -1,8 +1,9 @@
-"""CUDA-graph steps (-m gpu): with one rank and a dense update, phd_step replays a
-captured graph of its whole kernel chain (DESIGN.md §4 "graph step").  The replay must
-be bitwise the eager step (PHD_GRAPH=0): the same kernels with the same arguments, the
-per-step scalars (k, M, M_{k-1}, the resampling count / offset / mass) read from the
-device.  Configs with varying M (cfg 1-3), the adaptive count (cfg 1, 2), range-bearing
+"""One-sync and CUDA-graph steps (-m gpu).  With one rank, phd_step computes the
+resampling count / offset / mass on the device and synchronises once (the default,
+DESIGN.md §4 "one-sync step"); with PHD_GRAPH=1 and a dense update it replays a captured
+graph of its whole kernel chain.  Both must be bitwise the classic step (PHD_ONESYNC=0:
+host-computed resampling scalars, a synchronisation before the resampling): the same
+kernels with the same arguments, the per-step scalars read from the device.  Configs with varying M (cfg 1-3), the adaptive count (cfg 1, 2), range-bearing
 (cfg 2), fixed count (cfg 3), host and device measurement pointers."""
 import numpy as np
 import pytest
@@ -23,9 +24,10 @@ def phd():
     return p
 
 
-def _run(phd, cfg, steps, graph, monkeypatch, device_z=False):
+def _run(phd, cfg, steps, graph, monkeypatch, device_z=False, onesync=True):
     import torch
     monkeypatch.setenv("PHD_GRAPH", "1" if graph else "0")
+    monkeypatch.setenv("PHD_ONESYNC", "1" if onesync else "0")
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
     f = phd.Filter(cfg.model)
@@ -51,11 +53,15 @@ def _run(phd, cfg, steps, graph, monkeypatch, device_z=False):
 def test_graph_step_equals_eager(phd, cname, device_z, monkeypatch):
     cfg = scenario.get(cname)
     steps = min(cfg.scenario.steps, 12)
-    ref, st0 = _run(phd, cfg, steps, False, monkeypatch)
+    ref, st0 = _run(phd, cfg, steps, False, monkeypatch, onesync=False)
+    one, _ = _run(phd, cfg, steps, False, monkeypatch, device_z)
     got, st1 = _run(phd, cfg, steps, True, monkeypatch, device_z)
-    assert st0 == (0, 0)  # PHD_GRAPH=0 (the default is eager too)
+    assert st0 == (0, 0)
     assert st1[1] == steps and 1 <= st1[0] <= steps  # every step replayed a graph
-    for k, ((s0, e0, a0, p0, w0, m0), (s1, e1, a1, p1, w1, m1)) in enumerate(zip(ref, got)):
+    for k, ((s0, e0, a0, p0, w0, m0), (s1, e1, a1, p1, w1, m1), (s2, e2, a2, p2, w2, m2)) in \
+            enumerate(zip(ref, got, one)):
+        assert s2 == s0 and np.array_equal(e2["labels"], e0["labels"]) and np.array_equal(e2["states"], e0["states"])
+        assert np.array_equal(a2, a0) and np.array_equal(p2, p0) and np.array_equal(w2, w0) and m2["U"] == m0["U"]
         for key in ("W", "W_pred", "LT", "N", "N_out", "M", "n_est", "zero_mass", "count_clamped"):
             assert s0[key] == s1[key], (k, key, s0[key], s1[key])
         assert np.array_equal(e0["labels"], e1["labels"]) and np.array_equal(e0["states"], e1["states"])
@@ -70,6 +76,7 @@ def test_graph_step_zero_mass_and_stphd_all(phd, monkeypatch):
     cfg = replace(base, model=replace(base.model, stphd_all=1, birth_mass=0.0, births_per_step=0))
     for graph in (False, True):
         monkeypatch.setenv("PHD_GRAPH", "1" if graph else "0")
+        monkeypatch.setenv("PHD_ONESYNC", "1" if graph else "0")
         truth = scenario.simulate_truth(cfg)
         Z = scenario.measurements(cfg, truth)
         f = phd.Filter(cfg.model)
