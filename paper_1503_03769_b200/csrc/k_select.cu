@@ -141,101 +141,108 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
                                             int zl, int wz, int layout, int slots_pad, int32_t* slot_label,
                                             int32_t* js_out, float sx, float sy, const SlotConsts& sc,
                                             const double* __restrict__ D_lab) {
-  __shared__ int wsum[32];
-  __shared__ int base_s;
-  __shared__ int cat_start[7];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  // categories 0-2: selected labels of bearing class 0, 1, 2; 3-5: the unselected ones
+  // (position sensor: class 0 only).  Every thread owns a contiguous run of labels: one
+  // counting pass, one block-wide scan of the six counts, one placement pass.
+  constexpr int NC = 6;
+  __shared__ int wsum[32][NC];
+  __shared__ int cat_start[NC + 1];
+  __shared__ int s_js;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nw = nthr >> 5;
   const int per = (M + nthr - 1) / nthr;
   const float hp = 1.57079632679489662f;
   const int lanes = slots_pad / zl;
+  const bool rb = model == kRangeBearing;
   for (int s = tid; s < slots_pad; s += nthr) slot_label[s] = -1;
-  if (tid == 0) base_s = 0;
-  __syncthreads();
-  // pass A: category sizes (with pair padding) -> sequence offsets; pass B: placement
-  for (int phase = 0; phase < 2; ++phase) {
-    int js = 1, n_s = 0;
-    if (phase == 1) {
-      int n_sel = cat_start[3];
-      js = (n_sel + 2 * lanes - 1) / (2 * lanes);
-      js = max(js, 0);
-      js = min(js, zl / 2);
-      n_s = 2 * js * lanes;
-      // whole z-blocks instead (every slot of the first zb_sum z-blocks carries sums, the
-      // rest none; CTA-uniform) when that needs fewer state-sum slots than js pairs on
-      // every lane: *js_out = kJsZBlock | zb_sum
-      const int spz = wz * 32 * zl;
-      const int zb_sum = (n_sel + spz - 1) / spz;
-      if (layout == 2 || (layout == 0 && zb_sum * spz < n_s)) {
-        js = -1;
-        n_s = zb_sum * spz;
-        if (tid == 0) *js_out = kJsZBlock | zb_sum;
-      } else if (tid == 0) {
-        *js_out = js;
-      }
-      if (tid == 0) base_s = 0;
-      __syncthreads();
+  auto cat_of = [&](int l) {
+    int cls = 0;
+    if (rb) {
+      const float t = z[2 * l + 1];
+      cls = t > hp ? 1 : (t < -hp ? 2 : 0);
     }
-    for (int cat = 0; cat < 6; ++cat) {
-      const int want_sel = cat < 3 ? 1 : 0, want_cls = cat % 3;
-      if (phase == 0 && tid == 0) cat_start[cat] = base_s;
-      if (model != kRangeBearing && want_cls != 0) {
-        __syncthreads();
-        continue;
-      }
-      int c = 0;
-      for (int q = 0; q < per; ++q) {
-        int l = tid * per + q;
-        if (l >= M) break;
-        int cls = 0;
-        if (model == kRangeBearing) {
-          float t = z[2 * l + 1];
-          cls = t > hp ? 1 : (t < -hp ? 2 : 0);
-        }
-        if ((sel_flag[l] != 0) == (want_sel != 0) && cls == want_cls) ++c;
-      }
-      int incl = c;
+    return (sel_flag[l] != 0 ? 0 : 3) + cls;
+  };
+  int cnt[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) cnt[c] = 0;
+  for (int q = 0; q < per; ++q) {
+    const int l = tid * per + q;
+    if (l >= M) break;
+    const int c = cat_of(l);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) cnt[cc] += c == cc;
+  }
+  // exclusive prefix of every count over the threads (warp shuffles, then the warp totals)
+  int excl[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    int incl = cnt[c];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    excl[c] = incl - cnt[c];
+    if (lane == 31) wsum[warp][c] = incl;
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int v = lane < nw ? wsum[lane][c] : 0;
+      int inc2 = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+        const int u = __shfl_up_sync(0xffffffffu, inc2, o);
+        if (lane >= o) inc2 += u;
       }
-      if (lane == 31) wsum[warp] = incl;
-      __syncthreads();
-      if (warp == 0) {
-        int v = lane < nthr / 32 ? wsum[lane] : 0;
-        int inc2 = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int u = __shfl_up_sync(0xffffffffu, inc2, o);
-          if (lane >= o) inc2 += u;
-        }
-        if (lane < nthr / 32) wsum[lane] = inc2 - v;
-      }
-      __syncthreads();
-      if (phase == 1) {
-        int pos = base_s + wsum[warp] + (incl - c);
-        for (int q = 0; q < per; ++q) {
-          int l = tid * per + q;
-          if (l >= M) break;
-          int cls = 0;
-          if (model == kRangeBearing) {
-            float t = z[2 * l + 1];
-            cls = t > hp ? 1 : (t < -hp ? 2 : 0);
-          }
-          if ((sel_flag[l] != 0) == (want_sel != 0) && cls == want_cls) slot_label[seq_slot(pos++, n_s, lanes, zl, js)] = l;
-        }
-      }
-      __syncthreads();
-      if (tid == nthr - 1) {
-        int total = base_s + wsum[warp] + incl;
-        if (model == kRangeBearing && (total & 1)) ++total;  // pair padding (slot stays -1)
-        base_s = total;
-      }
-      __syncthreads();
+      if (lane < nw) wsum[lane][c] = inc2 - v;
+      const int tot = __shfl_sync(0xffffffffu, inc2, 31);
+      if (lane == 0) cat_start[c + 1] = tot;  // category total for now
     }
-    if (phase == 0 && tid == 0) cat_start[6] = base_s;
-    __syncthreads();
+    if (lane == 0) {
+      // category offsets in the sequence, each category padded to an even count
+      // (range-bearing: class-homogeneous f32x2 slot pairs)
+      int base = 0;
+      for (int c = 0; c < NC; ++c) {
+        const int tot = cat_start[c + 1];
+        cat_start[c] = base;
+        base += tot + (rb && (tot & 1) ? 1 : 0);
+      }
+      cat_start[NC] = base;
+      // state-sum layout: js slot pairs on every lane, or whole z-blocks (CTA-uniform)
+      // when that needs fewer state-sum slots: *js_out = kJsZBlock | zb_sum
+      const int n_sel = cat_start[3];
+      int js = (n_sel + 2 * lanes - 1) / (2 * lanes);
+      js = min(max(js, 0), zl / 2);
+      const int spz = wz * 32 * zl;
+      const int zb_sum = (n_sel + spz - 1) / spz;
+      if (layout == 2 || (layout == 0 && zb_sum * spz < 2 * js * lanes)) {
+        *js_out = kJsZBlock | zb_sum;
+        s_js = -1;
+      } else {
+        *js_out = js;
+        s_js = js;
+      }
+    }
   }
+  __syncthreads();
+  const int js = s_js;
+  const int n_s = js < 0 ? 0 : 2 * js * lanes;
+  int pos[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) pos[c] = cat_start[c] + wsum[warp][c] + excl[c];
+  for (int q = 0; q < per; ++q) {
+    const int l = tid * per + q;
+    if (l >= M) break;
+    const int c = cat_of(l);
+    int p = 0;
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+      if (c == cc) p = pos[cc]++;
+    slot_label[seq_slot(p, n_s, lanes, zl, js)] = l;
+  }
+  __syncthreads();
   // per-slot constants of the new layout (as k_zprep) and d = 1/D (as k_zconst):
   // padding slots get the sentinel that makes every term exactly 0
   for (int s = tid; s < slots_pad; s += nthr) {
