@@ -69,7 +69,9 @@ __device__ __forceinline__ float2 ex2_poly(float2 x) {
 // read as broadcast f32x2 operands (FADD2 Rd, Ra.F32, Rb.F32x2):
 //   position (8):        x, y, lw, 0 | vx, vy, 0, 0
 //   range-bearing (16):  r_hi, r_lo, lw, 0 | thA hi, lo, thB hi, lo | thC hi, lo, x, y | vx, vy, 0, 0
-// with lw = log2(p_D c w); the bearing representation c of a slot pair sits at 4 + 2c.
+// with lw = log2(p_D c w); the bearing representation c of a slot pair sits at 4 + 2c, its
+// lo part pre-scaled by s = sigma_r / sigma_theta (the dense kernels measure the bearing
+// residual in range units, see residual()).
 template <int MODEL>
 struct GRec {
   static constexpr bool RB = MODEL == kRangeBearing;
@@ -111,14 +113,18 @@ struct LaneZ {
 };
 
 // Residuals (d0, d1) of the lane's slot pair j against the broadcast particle.
-// P = the record's first float4: (x, y, lw, 0) or (r_hi, r_lo, lw, 0).
+// P = the record's first float4: (x, y, lw, 0) or (r_hi, r_lo, lw, 0).  Range-bearing: the
+// bearing residual is returned in range units, d1 = s (th_hi - z_th) + s th_lo with
+// s = sigma_r / sigma_theta (one FFMA2; s th_lo from the record), so the exponent is the
+// isotropic alpha_r (d0^2 + d1^2) -- one FMUL2 fewer per slot pair than two coefficients.
+// The residual th_hi - z_th is exact and the FFMA rounds once (as the FADD it replaces).
 template <int MODEL, int PASS, int NP, bool FOLD, int JS>
 __device__ __forceinline__ void residual(const float* rec, const float4& P, const LaneZ<MODEL, PASS, NP, FOLD, JS>& z,
-                                         int j, float2& d0, float2& d1) {
+                                         int j, float2& d0, float2& d1, float2 s) {
   if (MODEL == kRangeBearing) {
-    const float2 T = *reinterpret_cast<const float2*>(rec + z.roff[j]);  // (th_hi, th_lo) of the pair's class
-    d0 = __fadd2_rn(__fadd2_rn(f2(P.x, P.x), z.n0[j]), f2(P.y, P.y));  // (r_hi - z_r) + r_lo
-    d1 = __fadd2_rn(__fadd2_rn(f2(T.x, T.x), z.n1[j]), f2(T.y, T.y));  // (th_hi - z_th) + th_lo
+    const float2 T = *reinterpret_cast<const float2*>(rec + z.roff[j]);  // (th_hi, s th_lo) of the pair's class
+    d0 = __fadd2_rn(__fadd2_rn(f2(P.x, P.x), z.n0[j]), f2(P.y, P.y));   // (r_hi - z_r) + r_lo
+    d1 = __ffma2_rn(__fadd2_rn(f2(T.x, T.x), z.n1[j]), s, f2(T.y, T.y)); // s (th_hi - z_th) + s th_lo
   } else {
     d0 = __fadd2_rn(f2(P.x, P.x), z.n0[j]);  // x - z_x
     d1 = __fadd2_rn(f2(P.y, P.y), z.n1[j]);  // y - z_y
@@ -165,7 +171,10 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
     constexpr bool FOLD = PASS == 2 && kFoldD;
     LaneZ<MODEL, PASS, NP, FOLD, JS> z;
     z.load(a, slot0);
-    const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1);
+    const float2 na0 = f2(a.na0, a.na0), na1 = f2(a.na1, a.na1), rbs = f2(a.rbs, a.rbs);
+    // exponent form: range-bearing residuals are both in range units (residual()), so the
+    // isotropic form with alpha_r applies
+    constexpr int EM = MODEL == kRangeBearing ? kPosIso : MODEL;
 
     float2 in[NQ][NP];
   #pragma unroll
@@ -218,17 +227,17 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
   #pragma unroll
           for (int j = 0; j < NP; ++j) {
             float2 d0, d1;
-            residual(rec, P, z, j, d0, d1);
+            residual(rec, P, z, j, d0, d1, rbs);
             if (PASS == 1) {
               // u = p_D g w = 2^(-alpha q + log2(p_D c w)), flushed to zero below 2^-126
               // exactly as in pass 2 (the same exponent bits; the polynomial-offloaded
               // terms differ from MUFU.EX2 by <= 3.2e-7 relative)
-              const float2 e = expo<MODEL>(d0, d1, na0, na1, wv);
+              const float2 e = expo<EM>(d0, d1, na0, na1, wv);
               const bool emu = kEmuPeriod > 0 && j == NP - 1 && pp % (kEmuPeriod > 0 ? kEmuPeriod : 1) == 0;
               in[0][j] = __fadd2_rn(in[0][j], emu ? ex2_poly(e) : ex2v(e));
             } else if (FOLD) {
               // u = p_D g w / (kappa + C_s): two interleaved FADD2 chains over the slot pairs
-              const float2 u = ex2v(expo_fold<MODEL>(d0, d1, na0, na1, wv, z.d[j]));
+              const float2 u = ex2v(expo_fold<EM>(d0, d1, na0, na1, wv, z.d[j]));
               if (j == 0) pacc = u;
               else if (j == 1) pacc1 = u;
               else if (j & 1) pacc1 = __fadd2_rn(pacc1, u);
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
                 in[3][j] = __ffma2_rn(u, f2(V.y, V.y), in[3][j]);
               }
             } else {
-              const float2 u = ex2v(expo<MODEL>(d0, d1, na0, na1, wv));  // u = p_D g w
+              const float2 u = ex2v(expo<EM>(d0, d1, na0, na1, wv));  // u = p_D g w
               pacc = __ffma2_rn(u, z.d[j], pacc);
               if (j < JS && MODEL == kRangeBearing) {
                 const float2 XY = *reinterpret_cast<const float2*>(rec + L::XY);
@@ -373,10 +382,10 @@ __global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad
         v = ok ? make_float4(a.rb[i], a.rb[a.rb_stride + i], log2f(a.w[i] * a.wscale), 0.0f)
                : make_float4(0.0f, 0.0f, -INFINITY, 0.0f);
       } else if (ok && q == 1) {
-        v = make_float4(a.rb[2 * a.rb_stride + i], a.rb[3 * a.rb_stride + i], a.rb[4 * a.rb_stride + i],
-                        a.rb[5 * a.rb_stride + i]);
+        v = make_float4(a.rb[2 * a.rb_stride + i], a.rbs * a.rb[3 * a.rb_stride + i], a.rb[4 * a.rb_stride + i],
+                        a.rbs * a.rb[5 * a.rb_stride + i]);
       } else if (ok && q == 2) {
-        v = make_float4(a.rb[6 * a.rb_stride + i], a.rb[7 * a.rb_stride + i], a.x[i], a.y[i]);
+        v = make_float4(a.rb[6 * a.rb_stride + i], a.rbs * a.rb[7 * a.rb_stride + i], a.x[i], a.y[i]);
       } else if (ok) {
         v = make_float4(a.vx[i], a.vy[i], 0.0f, 0.0f);
       }

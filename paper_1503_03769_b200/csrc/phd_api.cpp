@@ -1202,6 +1202,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   pa.slots_pad = c->slots_pad;
   pa.na0 = c->na0;
   pa.na1 = c->na1;
+  pa.rbs = (float)(c->p.sigma_z[0] / c->p.sigma_z[1]);
   pa.wscale = c->wscale;
   pa.Cpart = c->Cpart;
   pa.Apart = c->Apart;

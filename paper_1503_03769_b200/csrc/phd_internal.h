@@ -99,6 +99,7 @@ struct PassArgs {
   SlotConsts sc;
   int slots_pad;             // stride of slot-major partials
   float na0, na1;            // -alpha_0, -alpha_1 (log2 units)
+  float rbs;                 // range-bearing: sigma_r / sigma_theta (bearing residuals in range units)
   float wscale;              // p_D * c, c = 1 / (2 pi sigma_0 sigma_1)
   double* Cpart;             // [gp][slots_pad]
   double* Apart;             // [gp][4][slots_pad]
