@@ -67,7 +67,10 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 // measurement slots per lane: 4 or 8 (kernel template), i.e. 128 or 256 per warp
 constexpr int kMaxWarpsZ = 8;                   // warps per CTA (each owns 128 slots)
 constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one particle per loader thread
-constexpr int kTileP = 64;                      // particles per smem tile
+#ifndef PHD_TILE_P
+#define PHD_TILE_P 128
+#endif
+constexpr int kTileP = PHD_TILE_P;              // particles per smem tile
 constexpr int kFlushTiles = 16;                 // fp32 mid-level -> fp64 every 16 tiles
 constexpr int kBlockW = 1024;                   // particles per finalize / scan block
 constexpr int kBlockOff = 1024;                 // offspring per gather block
