@@ -63,6 +63,12 @@ EMU_FRAC = 1.0 / 16.0
 POLY_FP32 = 8.0
 
 
+def emu_frac(meas):
+    """share of pass-1 terms on the FMA polynomial (k_update.cu: every 4th particle's last
+    slot pair of 4, i.e. 1/16; range-bearing every 8th: 1/32)"""
+    return EMU_FRAC / 2 if meas == 1 else EMU_FRAC
+
+
 def pass_ops(meas, which, f, hilo=False):
     """(FP32 ops, MUFU.EX2 ops) per pair.  hilo: also the seam-free hi/lo residual of the
     range-bearing sensor (+2 FP32 per pair per pass), implementation overhead rather than
@@ -70,7 +76,7 @@ def pass_ops(meas, which, f, hilo=False):
     rb = 1 if meas == 1 else 0
     hl = 2 * rb if hilo else 0
     if which == "pass1":  # joint bound: the polynomial-offloaded terms move from EX2 to FP32
-        return 6 + rb + hl + EMU_FRAC * POLY_FP32, 1.0 - EMU_FRAC
+        return 6 + rb + hl + emu_frac(meas) * POLY_FP32, 1.0 - emu_frac(meas)
     if which == "pass2":
         return 6 + rb + hl + (4 + 2 * rb) * f, 1
     if which == "pass2_survey":

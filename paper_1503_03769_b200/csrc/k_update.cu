@@ -40,7 +40,13 @@ namespace phd {
 constexpr int kPPUnroll1 = PHD_PP_UNROLL1;
 constexpr int kPPUnroll2 = PHD_PP_UNROLL2;
 
+// range-bearing pass 1 carries 8 FP32x2 per slot pair against 2 MUFU (balanced pipes): half
+// the offload (measured cfg 4 pass 1 1.80 -> 1.76 ms; position keeps 1/16: 15.3 vs 15.7 ms)
+#ifndef PHD_EMU_PERIOD_RB
+#define PHD_EMU_PERIOD_RB 8
+#endif
 constexpr int kEmuPeriod = PHD_EMU_PERIOD;
+constexpr int kEmuPeriodRB = PHD_EMU_PERIOD_RB;
 constexpr bool kFoldD = PHD_FOLD_D != 0;
 
 // 2^x for a pair on the FMA pipe (MUFU offload):
@@ -81,7 +87,10 @@ struct GRec {
   static constexpr int V = RB ? 12 : 4;
 };
 
-constexpr int kPassStages = 2;  // record tiles in flight per CTA (bulk copies)
+#ifndef PHD_PASS_STAGES
+#define PHD_PASS_STAGES 2
+#endif
+constexpr int kPassStages = PHD_PASS_STAGES;  // record tiles in flight per CTA (bulk copies)
 
 // Per-lane measurement constants for its NP slot pairs.
 template <int MODEL, int PASS, int NP, bool FOLD = false, int JS = NP>
@@ -233,7 +242,8 @@ __global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : 
               // exactly as in pass 2 (the same exponent bits; the polynomial-offloaded
               // terms differ from MUFU.EX2 by <= 3.2e-7 relative)
               const float2 e = expo<EM>(d0, d1, na0, na1, wv);
-              const bool emu = kEmuPeriod > 0 && j == NP - 1 && pp % (kEmuPeriod > 0 ? kEmuPeriod : 1) == 0;
+              constexpr int EP = MODEL == kRangeBearing ? kEmuPeriodRB : kEmuPeriod;
+              const bool emu = EP > 0 && j == NP - 1 && pp % (EP > 0 ? EP : 1) == 0;
               in[0][j] = __fadd2_rn(in[0][j], emu ? ex2_poly(e) : ex2v(e));
             } else if (FOLD) {
               // u = p_D g w / (kappa + C_s): two interleaved FADD2 chains over the slot pairs
