@@ -243,7 +243,7 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
     slot_label[seq_slot(p, n_s, lanes, zl, js)] = l;
   }
   __syncthreads();
-  // per-slot constants of the new layout (as k_zprep) and d = 1/D (as k_zconst):
+  // per-slot constants of the new layout (as k_build_slots) and d = 1/D (as k_zconst):
   // padding slots get the sentinel that makes every term exactly 0
   for (int s = tid; s < slots_pad; s += nthr) {
     const int lab = slot_label[s];
@@ -278,7 +278,7 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
 // identity (position sensor, gated path: slot = label), or, range-bearing, the labels
 // grouped by bearing class 0, 1, 2 (label order inside, every class padded to an even
 // count so each f32x2 slot pair is class-homogeneous); slots past the sequence are
-// padding (-1).  Then the per-slot constants (as k_zprep).  M from *Mp when given
+// padding (-1).  Then the per-slot constants.  M from *Mp when given
 // (graph replays), else M.
 __global__ void __launch_bounds__(kTopkThreads) k_build_slots(const float* __restrict__ z, const int* Mp, int M_arg,
                                                               int model, int identity, int slots_pad,

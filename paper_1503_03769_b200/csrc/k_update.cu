@@ -446,51 +446,6 @@ int pass_occupancy(int model, int pass, int wz, int zl) {
   return zl == 8 ? occ_z<8>(model, pass, wz) : occ_z<4>(model, pass, wz);
 }
 
-// ---------------------------------------------------------------------------
-// Measurement-slot preparation.  Slots hold labels (or -1 = padding); padding
-// slots get a sentinel that makes every likelihood term exactly 0.
-__global__ void k_zprep(int model, const float* __restrict__ z, const int32_t* __restrict__ slot_label, int n,
-                        float sx, float sy, SlotConsts sc, int* bad) {
-  pdl_wait();
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  int lab = slot_label[s];
-  float s0 = -1e30f, s1 = -1e30f, s2 = 0.0f, s3 = 0.0f;
-  int rep = 0;
-  if (lab >= 0) {
-    float z0 = z[2 * lab], z1 = z[2 * lab + 1];
-    // a NaN measurement makes its dense C NaN (PHD_EMODEL); counted here because the
-    // gated update may give it no candidate at all
-    if (bad != nullptr && (z0 != z0 || z1 != z1)) atomicAdd(bad, 1);
-    s0 = -z0;
-    s1 = -z1;
-    if (model == kRangeBearing) {
-      const float half_pi = 1.57079632679489662f;
-      rep = (z1 > half_pi) ? 1 : ((z1 < -half_pi) ? 2 : 0);
-      float sn, cs;
-      sincosf(z1, &sn, &cs);
-      s2 = -(sx + z0 * cs);
-      s3 = -(sy + z0 * sn);
-    }
-  }
-  sc.s0[s] = s0;
-  sc.s1[s] = s1;
-  if (sc.s2) {
-    sc.s2[s] = s2;
-    sc.s3[s] = s3;
-  }
-  if (sc.rep) sc.rep[s] = rep;
-  sc.d[s] = 0.0f;
-}
-
-cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad, float sensor_x,
-                         float sensor_y, SlotConsts sc, cudaStream_t s, int* bad) {
-  if (n_slots_pad <= 0) return cudaSuccess;
-  pdl_launch(k_zprep, (n_slots_pad + 255) / 256, 256, 0, s, model, z_lab, slot_label, n_slots_pad, sensor_x, sensor_y, sc,
-             bad);
-  return cudaGetLastError();
-}
-
 // C_slot[s] = sum over particle-CTAs (fixed order) of the pass-1 partials (fp64),
 // for the slot range [s0, s1) (one measurement group).
 // zc != nullptr (one rank: no all-reduce between): also the per-slot constants of k_zconst.

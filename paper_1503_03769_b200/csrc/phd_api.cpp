@@ -3,15 +3,15 @@
 //
 // Per step:
 //   predict   k_predict                                     (HBM)
-//   update    k_zprep -> k_pass<1> -> k_block_sum -> k_reduce_C (+ W_pred; one rank: + the
-//             per-slot constants) -> [C1 all-reduce -> k_zconst] -> k_select_slots
-//             -> k_pass<2> -> k_finalize -> k_reduce_acc -> [C2 all-reduce]
+//   update    k_build_slots -> k_records -> k_pass<1> -> k_block_sum -> k_reduce_C (+ W_pred;
+//             one rank: + the per-slot constants) -> [C1 all-reduce -> k_zconst] ->
+//             k_select_slots -> k_pass<2> -> k_finalize -> k_reduce_acc -> [C2 all-reduce]
 //             -> D2H of the rank masses and flags (gated: k_gate.cu kernels instead)
-//   extract   k_extract on rank 0 (the central unit) + D2H of the estimates; inside
-//             phd_step one host synchronisation covers the update's D2H and this one
-//   resample  k_scan_blocks -> k_resample_mark (+ per-offspring-block max) -> k_scan_max -> k_gather
-//   exchange  world 1: buffer swap; world > 1: k_gather_p2p into the owners' arrays over the
-//             peer-memory window + one barrier, or grouped ncclSend/ncclRecv (C3)
+//   extract   k_extract on rank 0 (the central unit) + D2H of the estimates
+//   resample  k_scan_chunks -> k_resample_gather (one rank inside phd_step: k_resample_setup
+//             first, the extraction on a second stream, one host synchronisation per step)
+//   exchange  world 1: buffer swap; world > 1: k_resample_gather<true> into the owners'
+//             arrays over the peer-memory window + one barrier, or grouped ncclSend/ncclRecv (C3)
 #include <algorithm>
 #include <climits>
 #include <cmath>

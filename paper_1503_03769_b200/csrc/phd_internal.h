@@ -207,8 +207,6 @@ cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, 
 cudaError_t launch_build_slots(const float* z, const int* Mp, int M, int model, int identity, int slots_pad,
                                int32_t* slot_label, float sensor_x, float sensor_y, SlotConsts sc, int* bad,
                                cudaStream_t s);
-cudaError_t launch_zprep(int model, const float* z_lab, const int32_t* slot_label, int n_slots_pad,
-                         float sensor_x, float sensor_y, SlotConsts sc, cudaStream_t s, int* bad = nullptr);
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
 // the dense pass 2 folds 1/D into its terms: its state-sum partials already carry 1/D
 bool pass2_sums_scaled();
@@ -310,7 +308,7 @@ cudaError_t launch_philox_kat(uint64_t seed, const uint32_t* ctr, int64_t n, uin
 cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream_t s);  // blk only
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                           int32_t* sel_flag, double* info, cudaStream_t s);
-// k_select + the pass-2 slot layout with its per-slot constants (as k_zprep) and 1/D
+// k_select + the pass-2 slot layout with its per-slot constants (as k_build_slots) and 1/D
 // *js = j (0..ZL/2): the first j slot pairs of every lane carry the state sums, or
 // kJsZBlock | b: every slot of the first b z-blocks does (layout 0: whichever needs fewer
 // sum slots; 1 / 2 force the per-lane / whole-z-block layout, for tests: PHD_SUM_LAYOUT)
