@@ -148,7 +148,8 @@ __device__ __forceinline__ void residual(const float* rec, const float4& P, cons
 #define PHD_PASS1_MINB8 2
 #endif
 template <int MODEL, int PASS, int ZL>
-__global__ void __launch_bounds__(256, ZL == 8 ? (PASS == 1 ? PHD_PASS1_MINB8 : PHD_PASS_MINB8) : 3)
+__global__ void __launch_bounds__(max_warps_z(ZL) * 32,
+                                  ZL == 8 ? (kMaxWarpsZ > 8 ? 1 : (PASS == 1 ? PHD_PASS1_MINB8 : PHD_PASS_MINB8)) : 3)
     k_pass(const PassArgs a) {
   pdl_wait();
   using L = GRec<MODEL>;
@@ -347,7 +348,7 @@ static size_t pass_smem(int wz) {
 
 template <int MODEL, int PASS, int ZL>
 static void set_attr() {
-  ensure_max_smem(k_pass<MODEL, PASS, ZL>, pass_smem<MODEL, PASS, ZL>(kMaxWarpsZ));
+  ensure_max_smem(k_pass<MODEL, PASS, ZL>, pass_smem<MODEL, PASS, ZL>(max_warps_z(ZL)));
 }
 
 template <int MODEL, int PASS, int ZL>

@@ -1020,11 +1020,11 @@ static phd_status build_slots(phd_ctx* c, int M) {
   int64_t best_pad = -1;
   for (int zl : {8, 4}) {
     const int64_t per_warp = 32 * zl;
-    const int need = (int)std::min<int64_t>(kMaxWarpsZ, std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), per_warp)));
+    const int need = (int)std::min<int64_t>(max_warps_z(zl), std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), per_warp)));
     int wz_z = need;
     int64_t pad_z = -1;
-    for (int cand : {need, 8, 4, 2}) {
-      const int wz = std::min(kMaxWarpsZ, std::max(kMinWarpsZ, cand));
+    for (int cand : {need, 16, 8, 4, 2}) {
+      const int wz = std::min(max_warps_z(zl), std::max(kMinWarpsZ, cand));
       const int64_t pad = ceil_div(std::max(n, 1), (int64_t)wz * per_warp) * wz * per_warp;
       if (pad_z < 0 || pad < pad_z || (pad == pad_z && wz > wz_z)) {
         pad_z = pad;
@@ -1042,7 +1042,7 @@ static phd_status build_slots(phd_ctx* c, int M) {
     int zl = atoi(fz);
     if (zl == 4 || zl == 8) {
       best_zl = zl;
-      best_wz = (int)std::min<int64_t>(kMaxWarpsZ, std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), 32 * zl)));
+      best_wz = (int)std::min<int64_t>(max_warps_z(zl), std::max<int64_t>(kMinWarpsZ, ceil_div(std::max(n, 1), 32 * zl)));
       best_zb = (int)ceil_div(std::max(n, 1), (int64_t)best_wz * 32 * zl);
       best_pad = (int64_t)best_zb * best_wz * 32 * zl;
     }

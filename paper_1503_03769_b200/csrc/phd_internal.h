@@ -65,7 +65,14 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 // ---- tiling constants ----------------------------------------
 // measurement slots per lane: 4 or 8 (kernel template), i.e. 128 or 256 per warp
-constexpr int kMaxWarpsZ = 8;                   // warps per CTA (each owns 128 slots)
+#ifndef PHD_MAX_WARPS_Z
+#define PHD_MAX_WARPS_Z 16
+#endif
+// warps per CTA of the dense passes: up to 16 with 8 slots per lane (one CTA row covers
+// 4096 slots: cfg 5's particle records are read once, not once per z-block), 8 with 4
+constexpr int kMaxWarpsZ = PHD_MAX_WARPS_Z;
+constexpr int kMaxWarpsZ4 = 8;
+constexpr int max_warps_z(int zl) { return zl == 8 ? kMaxWarpsZ : kMaxWarpsZ4; }
 constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one particle per loader thread
 #ifndef PHD_TILE_P
 #define PHD_TILE_P 128
