@@ -91,6 +91,12 @@ struct GRec {
 #define PHD_PASS_STAGES 2
 #endif
 constexpr int kPassStages = PHD_PASS_STAGES;  // record tiles in flight per CTA (bulk copies)
+// fp32 runs of the per-slot sums before they are added in fp64 (DESIGN.md §5 "accumulation
+// precision"): at most 128 particles, whatever the tile size
+#ifndef PHD_FLUSH_P
+#define PHD_FLUSH_P 128
+#endif
+constexpr int kFlushP = PHD_FLUSH_P < kTileP ? PHD_FLUSH_P : kTileP;
 
 // Per-lane measurement constants for its NP slot pairs.
 template <int MODEL, int PASS, int NP, bool FOLD = false, int JS = NP>
@@ -222,11 +228,26 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
       const int stage = it % kPassStages;
       mbar_wait(&mbar[stage], (uint32_t)((it / kPassStages) & 1));
       const float* rb = recs + stage * kTileP * L::WIDTH;
+      // per-slot sums of <= kFlushP particles in fp32 -> fp64; pass 2 only for the js
+      // slot pairs that carry state sums (the F2F conversions share the XU pipe with EX2)
+      auto flush64 = [&]() {
+  #pragma unroll
+        for (int q = 0; q < NQ; ++q)
+  #pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            if (PASS == 2 && j >= js) continue;
+            out64[(q * ZL + 2 * j) * nthr + tid] += (double)in[q][j].x;
+            out64[(q * ZL + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
+            in[q][j] = f2(0.0f, 0.0f);
+          }
+      };
 
       // pass 2: state sums only in the first JS slot pairs of each lane, where the
       // index set I lives (uniform over the warp; one instance of the loop per JS)
   #pragma unroll 1
-      for (int p0 = 0; p0 < kTileP; p0 += 8) {
+      for (int c0 = 0; c0 < kTileP; c0 += kFlushP) {
+  #pragma unroll 1
+      for (int p0 = c0; p0 < c0 + kFlushP; p0 += 8) {
         float pe[8];
   #pragma unroll(PASS == 1 ? kPPUnroll1 : kPPUnroll2)
         for (int pp = 0; pp < 8; ++pp) {
@@ -290,18 +311,8 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
           if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = s;
         }
       }
-
-      // tile sums (<= 64 particles in fp32) -> fp64; pass 2 only for the js slot
-      // pairs that carry state sums (the F2F conversions share the XU pipe with EX2)
-  #pragma unroll
-      for (int q = 0; q < NQ; ++q)
-  #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          if (PASS == 2 && j >= js) continue;
-          out64[(q * ZL + 2 * j) * nthr + tid] += (double)in[q][j].x;
-          out64[(q * ZL + 2 * j + 1) * nthr + tid] += (double)in[q][j].y;
-          in[q][j] = f2(0.0f, 0.0f);
-        }
+      flush64();
+      }
       __syncthreads();
       // every thread is done with this stage's records: refill it with tile t + kPassStages
       if (tid == 0 && t + kPassStages < t_end) {

@@ -75,7 +75,7 @@ constexpr int kMaxWarpsZ4 = 8;
 constexpr int max_warps_z(int zl) { return zl == 8 ? kMaxWarpsZ : kMaxWarpsZ4; }
 constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one particle per loader thread
 #ifndef PHD_TILE_P
-#define PHD_TILE_P 128
+#define PHD_TILE_P 256
 #endif
 constexpr int kTileP = PHD_TILE_P;              // particles per smem tile
 constexpr int kFlushTiles = 16;                 // fp32 mid-level -> fp64 every 16 tiles
