@@ -78,18 +78,19 @@ __global__ void __launch_bounds__(kTopkThreads) k_extract(const double* __restri
   // (same keys: k_select and k_reduce_acc compute dW = C (1/D) alike): compact it
   // instead of selecting again
   const bool use_sel = sel_flag != nullptr && sel_info != nullptr && (double)nsel == sel_info[3];
-  unsigned long long T = 0ull;
+  unsigned long long T = 0ull, mask = ~0ull;
   int keq = 0;
-  if (!use_sel) topk_threshold(kw, M, nsel, sh, &T, &keq);
+  if (!use_sel) topk_threshold(kw, M, nsel, sh, &T, &keq, &mask);
   // compact the selected labels in label order
   int carry = 0, carry_eq = 0;
   for (int r = 0; r < M; r += nthr) {
     const int i = r + tid;
     const unsigned long long key = i < M ? kw[i] : 0ull;
-    const bool eq = !use_sel && i < M && key == T;
+    const bool eq = !use_sel && i < M && key != 0ull && (key & mask) == T;
     int tot_eq;
     const int before_eq = carry_eq + topk_round_scan(eq, sh, &tot_eq);
-    const bool take = i < M && (use_sel ? sel_flag[i] != 0 : (key > T || (eq && before_eq < keq)));
+    const bool take =
+        i < M && (use_sel ? sel_flag[i] != 0 : key != 0ull && ((key & mask) > T || (eq && before_eq < keq)));
     int tot;
     const int pos = carry + topk_round_scan(take, sh, &tot);
     if (take) {
@@ -184,8 +185,38 @@ cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const 
   while (n2 < Ms) n2 <<= 1;
   size_t smem = (size_t)std::max(Ms, 1) * sizeof(unsigned long long) + (size_t)n2 * (sizeof(double) + sizeof(int));
   ensure_max_smem(k_extract, 8192 * 20);
-  pdl_launch(k_extract, 1, kTopkThreads, smem, s, acc_lab, M, Mp, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap,
+  pdl_launch(k_extract, 1, topk_block(Ms), smem, s, acc_lab, M, Mp, W, Wp, count, p_d, reinterpret_cast<EstOut*>(est), cap,
              summary, count_out, sel_info, sel_flag);
+  return cudaGetLastError();
+}
+
+// One CTA: the step's host-visible results into pinned host memory (StepOutArgs; UVA
+// maps cudaMallocHost memory, so the host pointers are device pointers).  Stores only;
+// the host reads them after the stream synchronisation that follows.
+__global__ void __launch_bounds__(256) k_step_out(const StepOutArgs a) {
+  pdl_wait();
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < a.n_rslots; i += nthr) a.h_rslots[i] = a.rslots[i];
+  if (tid < 2) a.h_bad[tid] = a.bad[tid];
+  if (a.sel_info && tid < 4) a.h_sel[tid] = a.sel_info[tid];
+  if (tid < 8) a.h_summ[tid] = a.summ[tid];
+  // the estimates: 6 words each, as many as the extraction wrote (<= est_cap)
+  const int n = a.est_count ? min(max(*a.est_count, 0), a.est_cap) : 0;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(a.est);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(a.h_est);
+  for (int i = tid; i < 6 * n; i += nthr) dst[i] = src[i];
+  if (a.ds) {
+    const uint32_t* d0 = reinterpret_cast<const uint32_t*>(a.ds);
+    uint32_t* d1 = reinterpret_cast<uint32_t*>(a.h_ds);
+    for (int i = tid; i < (int)(sizeof(DevStep) / 4); i += nthr) d1[i] = d0[i];
+  }
+  __syncthreads();  // every thread has read bad before it is cleared
+  if (tid < 4) a.bad[tid] = 0;
+}
+
+cudaError_t launch_step_out(const StepOutArgs& a, cudaStream_t s) {
+  static_assert(sizeof(EstOut) == 24, "estimate layout");
+  pdl_launch(k_step_out, 1, 256, 0, s, a);
   return cudaGetLastError();
 }
 

@@ -81,6 +81,9 @@ cudaError_t launch_scan_chunks(const double* blk, int nb, double* loc, double* c
 // kMP particles per thread of the resampling kernel (the per-thread scans and bounds
 // are amortised over them).
 constexpr int kMP = 8, kMT = kBlockW / kMP;
+// small populations (fewer than kGatherSmall blocks): kGatherR x kMT threads per block
+// place the offspring (latency: more gathers in flight per SM)
+constexpr int kGatherR = 4, kGatherSmall = 4 * 148;
 
 // zero mass: particle g (of N updated) gets the offspring [ceil(g n_out / N), ...), i.e.
 // offspring j copies particle floor(j N / n_out), with weight 0
@@ -95,7 +98,7 @@ __device__ __forceinline__ int64_t n_spread(int64_t g, int64_t n_out, int64_t N)
 // (20 B) per particle, writes state + w + ancestor (24 B) per offspring; no marks, no
 // memsets, no max-scan.
 template <bool P2P>
-__global__ void __launch_bounds__(kMT) k_resample_gather(const ResampleGatherArgs g, const PeerOut po) {
+__global__ void __launch_bounds__(kMT * kGatherR) k_resample_gather(const ResampleGatherArgs g, const PeerOut po) {
   pdl_wait();
   ResampleArgs a = g.r;
   float w_off = g.w_off;
@@ -111,41 +114,13 @@ __global__ void __launch_bounds__(kMT) k_resample_gather(const ResampleGatherArg
   __shared__ double wsum[kMT / 32];
   __shared__ int wmax[kMT / 32];
   __shared__ int hb[kBlockW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the first kMT threads own kMP particles each (bounds); all blockDim.x threads (kMT, or
+  // kGatherR kMT for small populations: more offspring in flight) place offspring
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  const bool owner = tid < kMT;  // warp-uniform
   const int64_t b = blockIdx.x;
   const int64_t base = b * kBlockW;
   const int64_t nb = (a.n_local + kBlockW - 1) / kBlockW;
-  double w4[kMP];
-  if (base + kMP * tid + kMP - 1 < a.n_local) {
-#pragma unroll
-    for (int v = 0; v < kMP / 4; ++v) {
-      const float4 q = *reinterpret_cast<const float4*>(a.w + base + kMP * tid + 4 * v);
-      w4[4 * v + 0] = (double)q.x;
-      w4[4 * v + 1] = (double)q.y;
-      w4[4 * v + 2] = (double)q.z;
-      w4[4 * v + 3] = (double)q.w;
-    }
-  } else {
-#pragma unroll
-    for (int m = 0; m < kMP; ++m) {
-      const int64_t i = base + kMP * tid + m;
-      w4[m] = i < a.n_local ? (double)a.w[i] : 0.0;
-    }
-  }
-  double tsum = 0.0;
-#pragma unroll
-  for (int m = 0; m < kMP; ++m) tsum += w4[m];
-  double incl = tsum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  double wpre = 0.0;
-  for (int k = 0; k < warp; ++k) wpre += wsum[k];
-  const double excl = wpre + (incl - tsum);
   // block bounds from off(b) = coff[b / kResScanChunk] + loc[b] (every reader forms the same bits)
   auto off = [&](int64_t bb) { return g.coff[bb / kResScanChunk] + a.blk_off[bb]; };
   const double Eb = a.O_r + (a.zero_mass ? 0.0 : off(b));
@@ -155,41 +130,79 @@ __global__ void __launch_bounds__(kMT) k_resample_gather(const ResampleGatherArg
   const int64_t nEb1 = (b == nb - 1) ? a.hi
                        : (a.zero_mass ? n_spread(gb + kBlockW, a.n_out, a.n_upd)
                                       : n_of(a.O_r + off(b + 1), a.scale, a.U, a.lo, a.hi));
-  double L = excl;
-  int run = 0;
-  int h[kMP];
+  double w4[kMP];
+  double tsum = 0.0, incl = 0.0;
+  if (owner) {
+    if (base + kMP * tid + kMP - 1 < a.n_local) {
 #pragma unroll
-  for (int m = 0; m < kMP; ++m) {
-    const int k = kMP * tid + m;
-    const int64_t i = base + k;
-    L += w4[m];
-    int64_t hi;
-    if (i >= a.n_local - 1 || k == kBlockW - 1) hi = nEb1;
-    else if (a.zero_mass) hi = min(max(n_spread(a.g0 + i + 1, a.n_out, a.n_upd), nEb), nEb1);
-    else hi = n_of(Eb + L, a.scale, a.U, nEb, nEb1);
-    run = max(run, (int)(hi - nEb));
-    h[m] = run;
-  }
-  int incl_m = run;
+      for (int v = 0; v < kMP / 4; ++v) {
+        const float4 q = *reinterpret_cast<const float4*>(a.w + base + kMP * tid + 4 * v);
+        w4[4 * v + 0] = (double)q.x;
+        w4[4 * v + 1] = (double)q.y;
+        w4[4 * v + 2] = (double)q.z;
+        w4[4 * v + 3] = (double)q.w;
+      }
+    } else {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl_m, o);
-    if (lane >= o) incl_m = max(incl_m, v);
+      for (int m = 0; m < kMP; ++m) {
+        const int64_t i = base + kMP * tid + m;
+        w4[m] = i < a.n_local ? (double)a.w[i] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kMP; ++m) tsum += w4[m];
+    incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
   }
-  if (lane == 31) wmax[warp] = incl_m;
   __syncthreads();
-  int carry = 0;
-  for (int k = 0; k < warp; ++k) carry = max(carry, wmax[k]);
-  const int prev = __shfl_up_sync(0xffffffffu, incl_m, 1);
-  if (lane > 0) carry = max(carry, prev);
+  int h[kMP];
+  int incl_m = 0;
+  if (owner) {
+    double wpre = 0.0;
+    for (int k = 0; k < warp; ++k) wpre += wsum[k];
+    const double excl = wpre + (incl - tsum);
+    double L = excl;
+    int run = 0;
 #pragma unroll
-  for (int m = 0; m < kMP; ++m) hb[kMP * tid + m] = max(h[m], carry);
+    for (int m = 0; m < kMP; ++m) {
+      const int k = kMP * tid + m;
+      const int64_t i = base + k;
+      L += w4[m];
+      int64_t hi;
+      if (i >= a.n_local - 1 || k == kBlockW - 1) hi = nEb1;
+      else if (a.zero_mass) hi = min(max(n_spread(a.g0 + i + 1, a.n_out, a.n_upd), nEb), nEb1);
+      else hi = n_of(Eb + L, a.scale, a.U, nEb, nEb1);
+      run = max(run, (int)(hi - nEb));
+      h[m] = run;
+    }
+    incl_m = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl_m, o);
+      if (lane >= o) incl_m = max(incl_m, v);
+    }
+    if (lane == 31) wmax[warp] = incl_m;
+  }
+  __syncthreads();
+  if (owner) {
+    int carry = 0;
+    for (int k = 0; k < warp; ++k) carry = max(carry, wmax[k]);
+    const int prev = __shfl_up_sync(0xffffffffu, incl_m, 1);
+    if (lane > 0) carry = max(carry, prev);
+#pragma unroll
+    for (int m = 0; m < kMP; ++m) hb[kMP * tid + m] = max(h[m], carry);
+  }
   __syncthreads();
   // offspring [0, end) of this block: produced indices pbase + k
   const int end = (int)(nEb1 - nEb);
   const int64_t pbase = nEb - a.lo;
   int q = 0;
-  for (int k = tid; k < end; k += kMT) {
+  for (int k = tid; k < end; k += nthr) {
     int pos = 0;  // number of particles whose upper bound is <= k: the ancestor
 #pragma unroll
     for (int step = kBlockW / 2; step > 0; step >>= 1)
@@ -238,7 +251,7 @@ __global__ void k_resample_setup(const SetupArgs a, DevStep* ds) {
       clamped = 1;
     }
   }
-  const U4 o = philox_at(a.seed, 0, (uint32_t)ds->k, 3u);
+  const U4 o = philox_at(a.seed, 0, (uint32_t)(a.k > 0 ? a.k : ds->k), 3u);
   ds->n_out = n_out;
   ds->count_clamped = clamped;
   ds->U = u52(o.x, o.y);
@@ -256,10 +269,11 @@ cudaError_t launch_resample_setup(const SetupArgs& a, DevStep* ds, cudaStream_t 
 cudaError_t launch_resample_gather(const ResampleGatherArgs& a, const PeerOut* po, cudaStream_t s) {
   if (a.r.n_local <= 0) return cudaSuccess;
   const unsigned nb = (unsigned)((a.r.n_local + kBlockW - 1) / kBlockW);
+  const int nt = nb < (unsigned)kGatherSmall ? kMT * kGatherR : kMT;
   if (po)
-    pdl_launch(k_resample_gather<true>, nb, kMT, 0, s, a, *po);
+    pdl_launch(k_resample_gather<true>, nb, nt, 0, s, a, *po);
   else
-    pdl_launch(k_resample_gather<false>, nb, kMT, 0, s, a, PeerOut{});
+    pdl_launch(k_resample_gather<false>, nb, nt, 0, s, a, PeerOut{});
   return cudaGetLastError();
 }
 

@@ -88,17 +88,17 @@ __device__ __forceinline__ void select_body(const double* __restrict__ C_lab, co
   __syncthreads();
   const int nsel = snsel;
   if (nsel <= 0) return;  // uniform over the CTA
-  unsigned long long T;
+  unsigned long long T, mask;
   int keq;
-  topk_threshold(kw, M, nsel, sh, &T, &keq);
+  topk_threshold(kw, M, nsel, sh, &T, &keq, &mask);
   int carry = 0;
   for (int r = 0; r < M; r += nthr) {
     const int i = r + tid;
     const unsigned long long key = i < M ? kw[i] : 0ull;
-    const bool eq = i < M && key == T;
+    const bool eq = i < M && key != 0ull && (key & mask) == T;
     int tot;
     const int before = carry + topk_round_scan(eq, sh, &tot);
-    if (i < M && (key > T || (eq && before < keq))) sel_flag[i] = 1;
+    if (i < M && key != 0ull && ((key & mask) > T || (eq && before < keq))) sel_flag[i] = 1;
     carry += tot;
   }
 }
@@ -116,7 +116,7 @@ cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const
                           int32_t* sel_flag, double* info, cudaStream_t s) {
   size_t smem = (size_t)std::max(M, 1) * sizeof(unsigned long long);
   ensure_max_smem(k_select, 8192 * 8);
-  pdl_launch(k_select, 1, kTopkThreads, smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info);
+  pdl_launch(k_select, 1, topk_block(M), smem, s, C_lab, D_lab, M, W_pred, p_d, sel_flag, info);
   return cudaGetLastError();
 }
 
@@ -283,12 +283,14 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
 __global__ void __launch_bounds__(kTopkThreads) k_build_slots(const float* __restrict__ z, const int* Mp, int M_arg,
                                                               int model, int identity, int slots_pad,
                                                               int32_t* slot_label, float sx, float sy, SlotConsts sc,
-                                                              int* bad) {
+                                                              int* bad, float* zcopy) {
   pdl_wait();
   __shared__ int wsum[32];
   __shared__ int base_s;
   const int M = Mp ? *Mp : M_arg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  if (zcopy)  // later kernels read Z from zcopy; this one reads the source
+    for (int i = tid; i < 2 * M; i += nthr) zcopy[i] = z[i];
   const float hp = 1.57079632679489662f;
   if (identity || model != kRangeBearing) {
     for (int s = tid; s < slots_pad; s += nthr) slot_label[s] = s < M ? s : -1;
@@ -374,10 +376,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_build_slots(const float* __res
 
 cudaError_t launch_build_slots(const float* z, const int* Mp, int M, int model, int identity, int slots_pad,
                                int32_t* slot_label, float sensor_x, float sensor_y, SlotConsts sc, int* bad,
-                               cudaStream_t s) {
+                               cudaStream_t s, float* zcopy) {
   if (slots_pad <= 0) return cudaSuccess;
-  pdl_launch(k_build_slots, 1, kTopkThreads, 0, s, z, Mp, M, model, identity, slots_pad, slot_label, sensor_x,
-             sensor_y, sc, bad);
+  pdl_launch(k_build_slots, 1, topk_block(Mp ? slots_pad : M), 0, s, z, Mp, M, model, identity, slots_pad, slot_label,
+             sensor_x, sensor_y, sc, bad, zcopy);
   return cudaGetLastError();
 }
 
@@ -404,7 +406,7 @@ cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M,
                                 float sensor_y, SlotConsts sc, cudaStream_t s, const int* Mp, int M_alloc) {
   size_t smem = (size_t)std::max(Mp ? M_alloc : M, 1) * sizeof(unsigned long long);
   ensure_max_smem(k_select_slots, 8192 * 8);
-  pdl_launch(k_select_slots, 1, kTopkThreads, smem, s, C_lab, D_lab, M, Mp, W_pred, p_d, sel_flag, info, z, model, zl,
+  pdl_launch(k_select_slots, 1, topk_block(std::max(Mp ? M_alloc : M, slots_pad / 4)), smem, s, C_lab, D_lab, M, Mp, W_pred, p_d, sel_flag, info, z, model, zl,
              wz, layout, slots_pad, slot_label, js, sensor_x, sensor_y, sc);
   return cudaGetLastError();
 }

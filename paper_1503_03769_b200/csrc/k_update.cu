@@ -15,6 +15,8 @@
 // transposed butterfly and across warps through shared memory, giving one
 // fp32 partial per (particle, z-block).  Cross-CTA sums are fp64 in fixed order.
 #include "phd_internal.h"
+
+#include <atomic>
 #include "pair_math.cuh"
 #include "bulk.cuh"
 
@@ -153,7 +155,7 @@ __device__ __forceinline__ void residual(const float* rec, const float4& P, cons
 #ifndef PHD_PASS1_MINB8
 #define PHD_PASS1_MINB8 2
 #endif
-template <int MODEL, int PASS, int ZL>
+template <int MODEL, int PASS, int ZL, int TILE>
 __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
                                   ZL == 8 ? (kMaxWarpsZ > 8 ? 1 : (PASS == 1 ? PHD_PASS1_MINB8 : PHD_PASS_MINB8)) : 3)
     k_pass(const PassArgs a) {
@@ -161,14 +163,16 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
   using L = GRec<MODEL>;
   constexpr int NQ = PASS == 1 ? 1 : 4;  // pass 2: S'x, Svx, S'y, Svy (dW = C/D from pass 1)
   constexpr int NP = ZL / 2;
-  constexpr uint32_t kTileBytes = sizeof(float) * kTileP * L::WIDTH;
+  constexpr int tile = TILE;  // particles per smem tile: kTileP, or kTileSmall (plan_gp)
+  const uint32_t kTileBytes = sizeof(float) * tile * L::WIDTH;
+  const int chunk = tile < kFlushP ? tile : kFlushP;
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t mbar[kPassStages];
   const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, wz = nthr >> 5;
-  float* recs = smem;                                            // [kPassStages][kTileP][WIDTH]
-  float* psum = recs + kPassStages * kTileP * L::WIDTH;           // [2][wz][kTileP] (pass 2)
+  float* recs = smem;                                            // [kPassStages][tile][WIDTH]
+  float* psum = recs + kPassStages * tile * L::WIDTH;             // [2][wz][tile] (pass 2)
   // fp64 accumulators per lane slot in shared memory, [NQ*ZL][nthr] (conflict-free)
-  double* out64 = reinterpret_cast<double*>(psum + (PASS == 2 ? 2 * wz * kTileP : 0));
+  double* out64 = reinterpret_cast<double*>(psum + (PASS == 2 ? 2 * wz * tile : 0));
 
   const int zb = blockIdx.y;
   const int slot0 = (zb * wz + warp) * (32 * ZL) + lane * ZL;
@@ -200,12 +204,12 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
   #pragma unroll
     for (int q = 0; q < NQ * ZL; ++q) out64[q * nthr + tid] = 0.0;
 
-    const int64_t ntiles = (a.n + kTileP - 1) / kTileP;
+    const int64_t ntiles = (a.n + tile - 1) / tile;
     const int64_t t_begin = (int64_t)blockIdx.x * a.tiles_per_cta;
     const int64_t t_end = min(t_begin + a.tiles_per_cta, ntiles);
 
     // record tiles stream into shared memory by bulk copies (one thread issues them), a
-    // tile of kTileP records per stage; the records of padding slots past n are zero with
+    // tile of `tile` records per stage; the records of padding slots past n are zero with
     // log2(p_D c w) = -inf, so every term of theirs is exactly 0
     if (tid == 0) {
   #pragma unroll
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
       for (int s = 0; s < kPassStages; ++s)
         if (t_begin + s < t_end) {
           mbar_arrive_expect_tx(&mbar[s], kTileBytes);
-          bulk_g2s(recs + s * kTileP * L::WIDTH, a.rec + (t_begin + s) * kTileP * L::WIDTH, kTileBytes, &mbar[s]);
+          bulk_g2s(recs + s * tile * L::WIDTH, a.rec + (t_begin + s) * tile * L::WIDTH, kTileBytes, &mbar[s]);
         }
     }
 
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
       const int buf = it & 1;                   // psum double buffer
       const int stage = it % kPassStages;
       mbar_wait(&mbar[stage], (uint32_t)((it / kPassStages) & 1));
-      const float* rb = recs + stage * kTileP * L::WIDTH;
+      const float* rb = recs + stage * tile * L::WIDTH;
       // per-slot sums of <= kFlushP particles in fp32 -> fp64; pass 2 only for the js
       // slot pairs that carry state sums (the F2F conversions share the XU pipe with EX2)
       auto flush64 = [&]() {
@@ -245,9 +249,9 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
       // pass 2: state sums only in the first JS slot pairs of each lane, where the
       // index set I lives (uniform over the warp; one instance of the loop per JS)
   #pragma unroll 1
-      for (int c0 = 0; c0 < kTileP; c0 += kFlushP) {
+      for (int c0 = 0; c0 < tile; c0 += chunk) {
   #pragma unroll 1
-      for (int p0 = c0; p0 < c0 + kFlushP; p0 += 8) {
+      for (int p0 = c0; p0 < c0 + chunk; p0 += 8) {
         float pe[8];
   #pragma unroll(PASS == 1 ? kPPUnroll1 : kPPUnroll2)
         for (int pp = 0; pp < 8; ++pp) {
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
         }
         if (PASS == 2) {
           float s = transpose_reduce8(pe, lane);
-          if ((lane & 3) == 0) psum[(buf * wz + warp) * kTileP + p0 + (lane >> 2)] = s;
+          if ((lane & 3) == 0) psum[(buf * wz + warp) * tile + p0 + (lane >> 2)] = s;
         }
       }
       flush64();
@@ -318,17 +322,17 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
       if (tid == 0 && t + kPassStages < t_end) {
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&mbar[stage], kTileBytes);
-        bulk_g2s(recs + stage * kTileP * L::WIDTH, a.rec + (t + kPassStages) * kTileP * L::WIDTH, kTileBytes,
+        bulk_g2s(recs + stage * tile * L::WIDTH, a.rec + (t + kPassStages) * tile * L::WIDTH, kTileBytes,
                  &mbar[stage]);
       }
 
       if (PASS == 2) {
         // per-particle partial over this CTA's slots: fixed-order sum over warps
-        for (int p = tid; p < kTileP; p += nthr) {
-          int64_t i = t * kTileP + p;
+        for (int p = tid; p < tile; p += nthr) {
+          int64_t i = t * tile + p;
           if (i < a.n) {
             float s = 0.0f;
-            for (int w2 = 0; w2 < wz; ++w2) s += psum[(buf * wz + w2) * kTileP + p];
+            for (int w2 = 0; w2 < wz; ++w2) s += psum[(buf * wz + w2) * tile + p];
             a.P[(int64_t)zb * a.P_stride + i] = s;
           }
         }
@@ -349,25 +353,33 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
 }
 
 template <int MODEL, int PASS, int ZL>
-static size_t pass_smem(int wz) {
+static size_t pass_smem(int wz, int tile) {
   using L = GRec<MODEL>;
-  size_t b = sizeof(float) * kPassStages * kTileP * L::WIDTH;
-  if (PASS == 2) b += sizeof(float) * 2 * wz * kTileP;
+  size_t b = sizeof(float) * kPassStages * tile * L::WIDTH;
+  if (PASS == 2) b += sizeof(float) * 2 * wz * tile;
   b += sizeof(double) * (PASS == 1 ? 1 : 4) * ZL * wz * 32;
   return b;
 }
 
-template <int MODEL, int PASS, int ZL>
+template <int MODEL, int PASS, int ZL, int TILE>
 static void set_attr() {
-  ensure_max_smem(k_pass<MODEL, PASS, ZL>, pass_smem<MODEL, PASS, ZL>(max_warps_z(ZL)));
+  ensure_max_smem(k_pass<MODEL, PASS, ZL, TILE>, pass_smem<MODEL, PASS, ZL>(max_warps_z(ZL), TILE));
+}
+
+// the tile size is a template parameter (a runtime tile costs 4.5% in cfg 5's pass 2)
+template <int MODEL, int PASS, int ZL, int TILE>
+static cudaError_t launch_tile(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+  set_attr<MODEL, PASS, ZL, TILE>();
+  dim3 grid((unsigned)gp, (unsigned)zb);
+  pdl_launch(k_pass<MODEL, PASS, ZL, TILE>, grid, wz * 32, pass_smem<MODEL, PASS, ZL>(wz, TILE), s, a);
+  return cudaGetLastError();
 }
 
 template <int MODEL, int PASS, int ZL>
 static cudaError_t launch_one(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
-  set_attr<MODEL, PASS, ZL>();
-  dim3 grid((unsigned)gp, (unsigned)zb);
-  pdl_launch(k_pass<MODEL, PASS, ZL>, grid, wz * 32, pass_smem<MODEL, PASS, ZL>(wz), s, a);
-  return cudaGetLastError();
+  if (a.tile == kTileSmall) return launch_tile<MODEL, PASS, ZL, kTileSmall>(a, gp, zb, wz, s);
+  if (a.tile != kTileP) return cudaErrorInvalidValue;
+  return launch_tile<MODEL, PASS, ZL, kTileP>(a, gp, zb, wz, s);
 }
 
 template <int MODEL, int ZL>
@@ -441,9 +453,10 @@ cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, 
 
 template <int MODEL, int PASS, int ZL>
 static int occ_one(int wz) {
-  set_attr<MODEL, PASS, ZL>();
+  set_attr<MODEL, PASS, ZL, kTileP>();
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<MODEL, PASS, ZL>, wz * 32, pass_smem<MODEL, PASS, ZL>(wz));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<MODEL, PASS, ZL, kTileP>, wz * 32,
+                                                pass_smem<MODEL, PASS, ZL>(wz, kTileP));
   return n;
 }
 
@@ -454,8 +467,21 @@ static int occ_z(int model, int pass, int wz) {
   return pass == 1 ? occ_one<kRangeBearing, 1, ZL>(wz) : occ_one<kRangeBearing, 2, ZL>(wz);
 }
 
+// cached per (device, model, pass, zl, wz): asked once, not every update (a runtime call
+// per query costs host time on the small configs' critical path)
 int pass_occupancy(int model, int pass, int wz, int zl) {
-  return zl == 8 ? occ_z<8>(model, pass, wz) : occ_z<4>(model, pass, wz);
+  static std::atomic<int> cache[16][3][2][2][kMaxWarpsZ + 1];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool cacheable = dev >= 0 && dev < 16 && model >= 0 && model < 3 && (pass == 1 || pass == 2) &&
+                         wz >= 0 && wz <= kMaxWarpsZ;
+  if (cacheable) {
+    const int v = cache[dev][model][pass - 1][zl == 8][wz].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+  }
+  const int v = zl == 8 ? occ_z<8>(model, pass, wz) : occ_z<4>(model, pass, wz);
+  if (cacheable && v > 0) cache[dev][model][pass - 1][zl == 8][wz].store(v, std::memory_order_relaxed);
+  return v;
 }
 
 // C_slot[s] = sum over particle-CTAs (fixed order) of the pass-1 partials (fp64),
@@ -473,8 +499,18 @@ __global__ void k_reduce_C(const double* __restrict__ Cpart, int gp, int slots_p
   int s = s0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= s1) return;
   double c = 0.0;
-#pragma unroll 4
-  for (int b = lane; b < gp; b += 32) c += Cpart[(int64_t)b * slots_pad + s];
+  // batches of 8 predicated loads in flight per lane (the partials were just written:
+  // L2-latency bound); the sum keeps the order b = lane, lane + 32, ... (+0 is exact)
+  for (int b0 = lane; b0 < gp; b0 += 32 * 8) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int b = b0 + 32 * r;
+      v[r] = b < gp ? Cpart[(int64_t)b * slots_pad + s] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) c += v[r];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) {
@@ -571,6 +607,11 @@ cudaError_t launch_finalize(const float* w, const float* P, int64_t P_stride, in
   return cudaGetLastError();
 }
 
+#ifndef PHD_RACC_UNROLL
+#define PHD_RACC_UNROLL 4
+#endif
+constexpr int kRaccUnroll = PHD_RACC_UNROLL;
+
 // STPHD accumulators in label order (Eqs 16, 18):
 //   dW = C / D  (Eq 16 summed over i is exactly C_p/(kappa + C_p), the north_star identity),
 //   Sx = A0 / D + cx dW,  Svx = A1 / D,  Sy = A2 / D + cy dW,  Svy = A3 / D
@@ -584,7 +625,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
                              const float* __restrict__ s3, int model, const double* __restrict__ blk_w,
                              const double* __restrict__ blk_wp, int nb, double* acc_lab, double* rank_slots,
                              int rank, int world, int lead, const int32_t* __restrict__ sel_flag,
-                             int sums_scaled) {
+                             int sums_scaled, double n_local) {
   pdl_wait();
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double sa[256], sb[256];
@@ -620,6 +661,7 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
     if (threadIdx.x == 0) {
       rank_slots[rank] = sa[0];
       rank_slots[world + rank] = sb[0];
+      rank_slots[2 * world + rank] = n_local;  // N_r (the all-reduce sums N)
     }
     return;
   }
@@ -633,11 +675,21 @@ __global__ void k_reduce_acc(const double* __restrict__ Apart, int gp, int slots
   // state sums outside the index set I were not accumulated: their partials are not read
   const bool sums = sel_flag == nullptr || sel_flag[lab] != 0;
   double A[4] = {0, 0, 0, 0};
-#pragma unroll 2
-  for (int b = sums ? lane : gp; b < gp; b += 32) {
-    const double* p = Apart + (int64_t)b * 4 * slots_pad + s;
+  // batches of kRaccUnroll x 4 predicated loads in flight per lane (L2-latency bound: the
+  // partials were just written by pass 2); the sums keep the order b = lane, lane + 32, ...
+  for (int b0 = sums ? lane : gp; b0 < gp; b0 += 32 * kRaccUnroll) {
+    double v[kRaccUnroll][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) A[q] += p[(int64_t)q * slots_pad];
+    for (int r = 0; r < kRaccUnroll; ++r) {
+      const int b = b0 + 32 * r;
+      const double* p = Apart + (int64_t)b * 4 * slots_pad + s;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[r][q] = b < gp ? p[(int64_t)q * slots_pad] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < kRaccUnroll; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) A[q] += v[r][q];
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q)
@@ -676,10 +728,11 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1,
                               const float* s2, const float* s3, int model, const double* blk_w, const double* blk_wp,
                               int nb, double* acc_lab, double* rank_slots, int rank, int world, int lead,
-                              const int32_t* sel_flag, cudaStream_t s, int sums_scaled) {
+                              const int32_t* sel_flag, cudaStream_t s, int sums_scaled, double n_local) {
   int blocks = (n_slots + 7) / 8 + 1;  // 8 slots (warps) per block + the rank-mass block
   pdl_launch(k_reduce_acc, blocks, 256, 0, s, Apart, gp, slots_pad, n_slots, slot_label, C_lab, D_lab, s0, s1, s2, s3, model,
-                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead, sel_flag, sums_scaled);
+                                      blk_w, blk_wp, nb, acc_lab, rank_slots, rank, world, lead, sel_flag, sums_scaled,
+             n_local);
   return cudaGetLastError();
 }
 

@@ -203,7 +203,9 @@ struct phd_ctx {
   int64_t N = 0;          // global particles of the predicted/updated array
   int64_t n_local = 0, g0 = 0;
   int64_t n_surv_local = 0;
-  int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zl = 4, zb = 0, gp = 0, M_z = -1;
+  int M = 0, n_slots = 0, slots_pad = 0, wz = 2, zl = 4, zb = 0, gp = 0, M_z = -1, tile = kTileP;
+  bool bad_clean = false;  // the non-finite counters were cleared by the last k_step_out
+  int est_eager = 0;       // estimates k_step_out stores (one-sync step)
   double* C_slot = nullptr;
   int32_t* sel_flag = nullptr;   // k_select: label in the estimated index set I
   double* sel_info = nullptr;    // (W_id, LT, n_eligible, n_sel, ..)
@@ -254,6 +256,9 @@ struct phd_ctx {
   std::vector<GraphEntry> graphs;
   int32_t* h_stepin = nullptr;             // pinned: k, M, M_prev of the next replay
   DevStep* h_stepout = nullptr;            // pinned: the replay's resampling scalars
+  double* hd_meta = nullptr;               // device aliases of h_meta, h_est, h_stepout
+  phd_estimate* hd_est = nullptr;
+  DevStep* hd_stepout = nullptr;
   int64_t graph_captures = 0, graph_replays = 0;
   // timing
   bool timing = false;
@@ -611,6 +616,11 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   CUB(cudaMallocHost(&c->h_z, sizeof(float) * 2 * (p->max_meas + 1)));
   CUB(cudaMallocHost(&c->h_stepin, sizeof(int32_t) * 4));
   CUB(cudaMallocHost(&c->h_stepout, sizeof(DevStep)));
+  // device aliases of the pinned result buffers k_step_out stores into (UVA: the same
+  // addresses on this platform; asked for, not assumed)
+  CUB(cudaHostGetDevicePointer((void**)&c->hd_meta, c->h_meta, 0));
+  CUB(cudaHostGetDevicePointer((void**)&c->hd_est, c->h_est, 0));
+  CUB(cudaHostGetDevicePointer((void**)&c->hd_stepout, c->h_stepout, 0));
   for (int i = 0; i < 16; ++i) CUB(cudaEventCreate(&c->ev[i]));
   CUB(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
   CUB(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
@@ -1111,12 +1121,23 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
 
 static phd_status update_finish(phd_ctx* c);
 
-// particle-CTA count of the dense passes: one wave of resident CTAs over the z-blocks
+// particle-CTA count and record-tile size of the dense passes: one wave of resident CTAs
+// over the z-blocks; small populations (fewer than two CTAs' worth of kTileP tiles per
+// SM) take kTileSmall tiles so that they still fill the SMs (measured: cfg 2, 8 tiles of
+// 256, passes 37 -> 21 us with 64; cfg 3 keeps 256; PHD_TILE=64|256 forces a size)
 static int plan_gp(phd_ctx* c, int64_t n) {
-  const int64_t tiles = ceil_div(n, kTileP);
   int occ = std::min(pass_occupancy(c->model, 1, c->wz, c->zl), pass_occupancy(c->model, 2, c->wz, c->zl));
   occ = std::max(1, occ);
   int64_t want = std::max<int64_t>(1, (int64_t)occ * c->sms / std::max(1, c->zb));
+  int tile = kTileP;
+  const char* e = getenv("PHD_TILE");
+  if (e && *e) {
+    if (atoi(e) == kTileSmall) tile = kTileSmall;
+  } else if (ceil_div(n, kTileP) * std::max(1, c->zb) < 2 * (int64_t)c->sms) {
+    tile = kTileSmall;
+  }
+  c->tile = tile;
+  const int64_t tiles = ceil_div(n, tile);
   int64_t cap_gp = std::max<int64_t>(1, c->L.part_cap / c->slots_pad);
   int gp = (int)std::min<int64_t>(std::min(want, cap_gp), tiles);
   int64_t tpc = ceil_div(tiles, gp);
@@ -1141,6 +1162,19 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   if (M > 0 && !z) return fail(c, PHD_EINVAL, "z is NULL");
   timing_record(c, 2);
   c->M = M;
+  // gate = 1 skips the gated path for small updates (< 2^29 pairs, where the cell
+  // sort and candidate lists cost more than the dense passes: measured at cfg 3,
+  // 6.8e7 pairs, 0.28 ms dense vs 0.50 ms gated).  N is global in exact mode, so
+  // every rank takes the same branch; DCP groups always plan (collectively).
+  const bool small = c->p.gate == 1 && !c->dcp && (double)c->N * (double)M < 536870912.0;
+  // the candidate offsets are an int32 scan: at most M candidates per tile, so a
+  // capacity whose tiles x M could exceed INT32_MAX runs dense (same on every rank)
+  const bool fits32 = (double)c->L.g_ntiles * (double)M <= (double)INT32_MAX;
+  const bool try_gate = c->p.gate != 0 && M > 0 && !small && fits32;
+  // one-sync step with a device-resident Z and no gate plan (which reads zlab): the slot
+  // layout kernel reads Z where it is and leaves the copy in zlab (one launch, no copy)
+  const float* z_slots = c->zlab;
+  float* z_copy = nullptr;
   if (M > 0 && c->capturing) {
     // graph replay: Z_k staged by the host in the pinned h_z (after predict read Z_{k-1})
     CU(cudaMemcpyAsync(c->zlab, c->h_z, sizeof(float) * 2 * c->p.max_meas, cudaMemcpyHostToDevice, c->st));
@@ -1148,7 +1182,10 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     cudaPointerAttributes pa{};
     bool dev = cudaPointerGetAttributes(&pa, z) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
     cudaGetLastError();
-    if (dev) {  // device-resident Z stays on the device (the slot layout is built there)
+    if (dev && c->dev_scalars && !try_gate) {
+      z_slots = z;
+      z_copy = c->zlab;
+    } else if (dev) {  // device-resident Z stays on the device (the slot layout is built there)
       CU(cudaMemcpyAsync(c->zlab, z, sizeof(float) * 2 * M, cudaMemcpyDeviceToDevice, c->st));
     } else {
       memcpy(c->h_z, z, sizeof(float) * 2 * M);
@@ -1158,17 +1195,11 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   c->M_z = M;
   const int64_t n = c->n_local;
   bool gated = false;
-  // non-finite counters (k_zconst: C/D; the gated sort: NaN particles), before any of them runs
-  CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
-  // gate = 1 skips the gated path for small updates (< 2^29 pairs, where the cell
-  // sort and candidate lists cost more than the dense passes: measured at cfg 3,
-  // 6.8e7 pairs, 0.28 ms dense vs 0.50 ms gated).  N is global in exact mode, so
-  // every rank takes the same branch; DCP groups always plan (collectively).
-  const bool small = c->p.gate == 1 && !c->dcp && (double)c->N * (double)M < 536870912.0;
-  // the candidate offsets are an int32 scan: at most M candidates per tile, so a
-  // capacity whose tiles x M could exceed INT32_MAX runs dense (same on every rank)
-  const bool fits32 = (double)c->L.g_ntiles * (double)M <= (double)INT32_MAX;
-  if (c->p.gate != 0 && M > 0 && !small && fits32) {
+  // non-finite counters (k_zconst: C/D; the gated sort: NaN particles), before any of them
+  // runs; a one-sync step finds them cleared by the previous step's k_step_out
+  if (!(c->dev_scalars && !c->capturing && c->bad_clean)) CU(cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->st));
+  c->bad_clean = false;
+  if (try_gate) {
     phd_status st = gate_plan(c, M, n, &gated);
     if (st != PHD_OK) return st;
   }
@@ -1179,18 +1210,18 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     phd_status st = build_slots(c, M);
     if (st != PHD_OK) return st;
   }
-  const int64_t tiles = ceil_div(n, kTileP);
   if (M > 0) {  // slot -> label map and per-slot constants, on the device
     SlotConsts sc{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
-    KL(launch_build_slots(c->zlab, c->capturing ? &c->dstep->M : nullptr, M, c->model, gated ? 1 : 0, c->slots_pad,
-                          c->slot_label,
-                          (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->bad, c->st));
+    KL(launch_build_slots(z_slots, c->capturing ? &c->dstep->M : nullptr, M, c->model, gated ? 1 : 0, c->slots_pad,
+                          c->slot_label, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->bad, c->st,
+                          z_copy));
   }
   const int gp = M > 0 && n > 0 && !gated ? plan_gp(c, n) : 0;
   c->gp = gp;
   PassArgs pa{};
   pa.n = n;
-  pa.tiles_per_cta = gp > 0 ? ceil_div(tiles, gp) : 0;
+  pa.tile = gp > 0 ? c->tile : kTileP;
+  pa.tiles_per_cta = gp > 0 ? ceil_div(ceil_div(n, pa.tile), gp) : 0;
   pa.x = c->A[0];
   pa.vx = c->A[1];
   pa.y = c->A[2];
@@ -1303,20 +1334,20 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   KL(launch_reduce_acc(gated ? c->gA : c->Apart, gated ? 1 : gp, c->slots_pad, M > 0 ? c->slots_pad : 0, c->slot_label, c->C, c->D, c->s[0],
                        c->s[1], c->s[2], c->s[3], c->model, c->blk_w, c->blk_wp, nbw, c->acc, rank_slots, c->rank,
                        c->world, c->dcp || c->rank == 0 ? 1 : 0, c->select ? c->sel_flag : nullptr, c->st,
-                       pass2_sums_scaled() ? 1 : 0));
-  // rank slots [W_r | W_pred_r | N_r] (3 per rank); N_r written from the host
-  c->h_meta[3 * c->world + 16] = (double)n;
-  CU(cudaMemcpyAsync(rank_slots + 2 * c->world + c->rank, c->h_meta + 3 * c->world + 16, sizeof(double),
-                     cudaMemcpyHostToDevice, c->st));
+                       pass2_sums_scaled() ? 1 : 0, (double)n));
+  // rank slots [W_r | W_pred_r | N_r] (3 per rank), written by k_reduce_acc's last block
   if (c->world > 1) {
     if (c->dcp)  // groups keep their own accumulators; only the per-group masses are shared
       COMM(c->comm->allreduce_f64(rank_slots, (size_t)(3 * c->world), c->st));
     else
       COMM(c->comm->allreduce_f64(c->rslots, (size_t)(c->acc - c->rslots) + 5 * (size_t)M, c->st));
   }
-  CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 3 * c->world, cudaMemcpyDeviceToHost, c->st));
-  CU(cudaMemcpyAsync(c->h_meta + 3 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
-  if (c->select) CU(cudaMemcpyAsync(c->h_meta + 3 * c->world + 32, c->sel_info, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
+  if (!c->dev_scalars) {  // one-sync / graph step: k_step_out stores them at the end of the step
+    CU(cudaMemcpyAsync(c->h_meta, rank_slots, sizeof(double) * 3 * c->world, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(c->h_meta + 3 * c->world, c->bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
+    if (c->select)
+      CU(cudaMemcpyAsync(c->h_meta + 3 * c->world + 32, c->sel_info, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
+  }
   timing_record(c, 7);
   if (c->defer_update_sync) {  // phd_step: finished by phd_extract after its one synchronisation
     c->update_pending = true;
@@ -1486,7 +1517,7 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     KL(launch_extract(c->acc, c->M, rank_slots, rank_slots + c->world, c->world, c->p.p_d, c->est + 1, capd, c->summ,
                       &c->est[0].label, c->select ? c->sel_info : nullptr, c->select ? c->sel_flag : nullptr,
                       es, c->capturing ? &c->dstep->M : nullptr, c->p.max_meas));
-    CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, es));
+    if (!c->dev_scalars) CU(cudaMemcpyAsync(smh, c->summ, sizeof(double) * 8, cudaMemcpyDeviceToHost, es));
     // the estimate count is min(LT, eligible, cap) <= min(LT, cap): copy that many with the
     // summary, so the extraction costs one synchronisation
     // (inside phd_step LT is not on the host yet: copy up to kEstEager estimates, the
@@ -1494,12 +1525,13 @@ phd_status phd_extract(phd_ctx* c, phd_estimate* out, int32_t cap, int32_t* n_ou
     const int64_t ncopy = (!out && !c->dev_scalars) ? 0
                           : c->update_pending ? std::min<int64_t>(kEstEager, capd)
                                               : std::min<int64_t>(std::max<int64_t>(c->LT, 0), capd);
-    if (ncopy > 0)
-      CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * ncopy, cudaMemcpyDeviceToHost, es));
-    if (c->dev_scalars) {  // one-sync step: finished by step_finish after the step's synchronisation
+    if (c->dev_scalars) {  // one-sync step: k_step_out stores summary + estimates; step_finish
+      c->est_eager = (int)ncopy;
       CU(cudaEventRecord(c->join_ev, c->st2));
       return PHD_OK;
     }
+    if (ncopy > 0)
+      CU(cudaMemcpyAsync(c->h_est, c->est + 1, sizeof(phd_estimate) * ncopy, cudaMemcpyDeviceToHost, es));
     CU(cudaStreamSynchronize(c->st));
     if (c->update_pending) {
       phd_status st = update_finish(c);
@@ -1614,6 +1646,7 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     sa.R = c->p.particles_per_target;
     sa.lim = c->p.capacity - c->p.births_per_step;
     sa.seed = c->p.seed;
+    sa.k = c->capturing ? 0 : k;  // graph replays: k from the staged step block
     KL(launch_resample_setup(sa, c->dstep, c->st));
     const int64_t n = c->n_local;
     KL(launch_scan_chunks(c->blk_w, (int)ceil_div(n, kBlockW), c->blk_off, c->ctot, c->coff, c->scan_counter, c->st));
@@ -1625,8 +1658,26 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     ra.n_upd = c->N;
     ra.ds = c->dstep;
     KL(launch_resample_gather(rg_args(c, ra, 0.0f), nullptr, c->st));
-    CU(cudaMemcpyAsync(c->h_stepout, c->dstep, sizeof(DevStep), cudaMemcpyDeviceToHost, c->st));
     if (c->rank == 0) CU(cudaStreamWaitEvent(c->st, c->join_ev, 0));  // the extraction on st2
+    // everything the host reads after the step's synchronisation, by one kernel
+    StepOutArgs so{};
+    so.rslots = c->rslots;
+    so.n_rslots = 3 * c->world;
+    so.h_rslots = c->hd_meta;
+    so.bad = c->bad;
+    so.h_bad = reinterpret_cast<int32_t*>(c->hd_meta + 3 * c->world);
+    so.sel_info = c->select ? c->sel_info : nullptr;
+    so.h_sel = c->hd_meta + 3 * c->world + 32;
+    so.summ = c->summ;
+    so.h_summ = c->hd_meta + 3 * c->world + 4;
+    so.est = c->est + 1;
+    so.est_count = c->rank == 0 ? &c->est[0].label : nullptr;
+    so.h_est = c->hd_est;
+    so.est_cap = c->est_eager;
+    so.ds = c->dstep;
+    so.h_ds = c->hd_stepout;
+    KL(launch_step_out(so, c->st));
+    c->bad_clean = true;
     return PHD_OK;
   }
   timing_record(c, 10);
@@ -1890,7 +1941,7 @@ static phd_status step_graph(phd_ctx* c, int32_t k, const float* z, int32_t M, p
   phd_status st = build_slots(c, M);
   if (st != PHD_OK) return st;
   const int gp = plan_gp(c, N);
-  const int64_t key[8] = {c->n_out, (int64_t)(uintptr_t)c->A[0], c->zl, c->wz, c->zb, c->slots_pad, gp,
+  const int64_t key[8] = {c->n_out, (int64_t)(uintptr_t)c->A[0], c->zl | ((int64_t)c->tile << 8), c->wz, c->zb, c->slots_pad, gp,
                           std::min(cap, c->p.max_meas) > 0 ? 1 : 0};
   // stage this step's inputs: Z_k, (k, M, M_{k-1}), this rank's particle count
   cudaPointerAttributes pa{};
@@ -1966,8 +2017,7 @@ static phd_status step_onesync(phd_ctx* c, int32_t k, const float* z, int32_t M,
   c->h_stepin[0] = k;
   c->h_stepin[1] = M;
   c->h_stepin[2] = std::max(c->M_z, 0);
-  CU(cudaMemcpyAsync(c->dstep, c->h_stepin, sizeof(int32_t) * 3, cudaMemcpyHostToDevice, c->st));
-  c->dev_scalars = true;
+  c->dev_scalars = true;  // (k, M, M_prev) reach the kernels as arguments: no staged step block
   c->defer_update_sync = true;
   phd_status st = phd_predict(c, k, nullptr, 0);
   if (st == PHD_OK) st = phd_update(c, z, M);

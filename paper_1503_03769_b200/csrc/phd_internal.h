@@ -31,10 +31,20 @@ namespace phd {
 // and its memory is visible -- so the semantics are those of plain stream order,
 // but the launch and block scheduling of a kernel overlap the tail of the one
 // before it (the step is a chain of ~20-45 kernels, many of them short).
+// Right after the wait each kernel signals griddepcontrol.launch_dependents, so the next
+// kernel of the chain is launched (its CTAs parked at their own wait) while this one
+// runs: one kernel of lookahead.  A dependent grid launches only once every CTA of this
+// one has started and signalled, so parked CTAs never hold back this grid's own.
 // PHD_PDL=0 in the environment launches without the attribute.
+#ifndef PHD_PDL_EARLY
+#define PHD_PDL_EARLY 0
+#endif
 __device__ __forceinline__ void pdl_wait() {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if PHD_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
 #endif
 }
 bool pdl_enabled();
@@ -78,6 +88,7 @@ constexpr int kMinWarpsZ = 2;                   // >= kTileP threads: one partic
 #define PHD_TILE_P 256
 #endif
 constexpr int kTileP = PHD_TILE_P;              // particles per smem tile
+constexpr int kTileSmall = 64;                 // small populations (plan_gp)
 constexpr int kFlushTiles = 16;                 // fp32 mid-level -> fp64 every 16 tiles
 constexpr int kBlockW = 1024;                   // particles per finalize / scan block
 constexpr int kBlockOff = 1024;                 // offspring per gather block
@@ -99,6 +110,7 @@ struct SlotConsts {
 struct PassArgs {
   int64_t n;                 // local particles
   int64_t tiles_per_cta;
+  int tile;                  // particles per record tile: kTileP or kTileSmall (plan_gp)
   const float* x;
   const float* vx;
   const float* y;
@@ -211,9 +223,11 @@ cudaError_t launch_birth_is(const BirthISArgs& a, cudaStream_t s);
 cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, float sy, float* rb,
                            int64_t stride, cudaStream_t s);
 // pass-1 slot layout + per-slot constants on the device (k_build_slots, k_select.cu)
+// zcopy != nullptr: also copies Z (read from z) into zcopy (the device-resident Z of the
+// one-sync step: no separate device-to-device copy)
 cudaError_t launch_build_slots(const float* z, const int* Mp, int M, int model, int identity, int slots_pad,
                                int32_t* slot_label, float sensor_x, float sensor_y, SlotConsts sc, int* bad,
-                               cudaStream_t s);
+                               cudaStream_t s, float* zcopy = nullptr);
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
 // the dense pass 2 folds 1/D into its terms: its state-sum partials already carry 1/D
 bool pass2_sums_scaled();
@@ -264,7 +278,7 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
                               const double* C_lab, const double* D_lab, const float* s0, const float* s1, const float* s2,
                               const float* s3, int model, const double* blk_w, const double* blk_wp, int nb,
                               double* acc_lab, double* rank_slots, int rank, int world, int lead,
-                              const int32_t* sel_flag, cudaStream_t s, int sums_scaled = 0);
+                              const int32_t* sel_flag, cudaStream_t s, int sums_scaled, double n_local);
 // W = sum_{r < count} W[r], W_pred = sum Wp[r]; writes the estimates to est[0..)
 // and their count to *count_out (the header entry of the gather block).
 cudaError_t launch_extract(const double* acc_lab, int M, const double* W, const double* Wp, int count, double p_d,
@@ -301,8 +315,31 @@ struct SetupArgs {
   int fixed;                 // count mode fixed
   int64_t fixed_count, R, lim;  // N_out (fixed), particles per target, capacity - J (adaptive)
   uint64_t seed;
+  int32_t k;                 // the step (> 0), or 0: ds->k (graph replays)
 };
 cudaError_t launch_resample_setup(const SetupArgs& a, DevStep* ds, cudaStream_t s);
+
+// End of a one-sync / graph step (world 1): every result the host reads after the step's
+// one synchronisation, stored by one kernel into pinned host memory (mapped, UVA) instead
+// of one copy per buffer; the non-finite counters are cleared for the next step.
+struct StepOutArgs {
+  const double* rslots;                 // rank slots [3 world] -> h_rslots
+  int n_rslots;
+  double* h_rslots;
+  int* bad;                             // non-finite counters [4]: [0..1] -> h_bad, then zeroed
+  int32_t* h_bad;
+  const double* sel_info;               // [4] -> h_sel (nullptr: none)
+  double* h_sel;
+  const double* summ;                   // extraction summary [8] -> h_summ
+  double* h_summ;
+  const void* est;                      // estimates (24 B each), their count at *est_count
+  const int32_t* est_count;
+  void* h_est;
+  int est_cap;                          // at most this many copied
+  const DevStep* ds;                    // -> *h_ds (nullptr: none)
+  DevStep* h_ds;
+};
+cudaError_t launch_step_out(const StepOutArgs& a, cudaStream_t s);
 
 struct PeerOut {
   float* dst[kMaxPeers][5];   // owner q's next-step arrays x, vx, y, vy, w (peer pointers)

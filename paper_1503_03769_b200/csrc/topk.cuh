@@ -2,15 +2,31 @@
 // S8: order (dW desc, label asc), only dW > 0 eligible).  One CTA of 1024
 // threads, M <= 8192 keys in shared memory.  Keys are the fp64 bits of dW >= 0
 // (monotone in dW); 0 marks an ineligible label.  A most-significant-digit
-// radix select (8 passes of 8 bits) finds the K-th largest key T and how many
+// radix select (up to 8 passes of 8 bits) finds the K-th largest key T and how many
 // keys equal to T are taken (the lowest labels first), replacing a full bitonic
-// sort of all M labels.
+// sort of all M labels.  It stops early once the digit bucket holding the K-th key
+// holds exactly the keys still to take: then T is that bucket's prefix, compared
+// under the returned mask, and every nonzero key matching it is taken.
 #pragma once
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace phd {
 
 constexpr int kTopkThreads = 1024;
+
+// Block size of the one-CTA label kernels for M labels: one label per thread up to
+// kTopkThreads, at least 128 threads (fewer warps: cheaper barriers for small M).
+// PHD_TOPK_THREADS forces a size (A/B runs).
+inline int topk_block(int M) {
+  static const int forced = [] {
+    const char* e = getenv("PHD_TOPK_THREADS");
+    return e && *e ? atoi(e) : 0;
+  }();
+  if (forced >= 32 && forced <= kTopkThreads && forced % 32 == 0) return forced;
+  int t = (M + 127) / 128 * 128;
+  return t < 128 ? 128 : (t > kTopkThreads ? kTopkThreads : t);
+}
 
 struct TopkShared {
   int hist[256];
@@ -18,16 +34,19 @@ struct TopkShared {
   unsigned long long prefix;
   int k;
   int carry;
+  int done;
 };
 
-// T = K-th largest nonzero key of kw[0..M), keq = number of keys == T among the
-// K taken (all keys > T are taken).  Requires 1 <= K <= #nonzero keys.
+// T = K-th largest nonzero key of kw[0..M) under *mask_out (the top bits examined),
+// keq = number of nonzero keys with (key & mask) == T among the K taken (every nonzero
+// key with (key & mask) > T is taken).  Requires 1 <= K <= #nonzero keys.
 __device__ inline void topk_threshold(const unsigned long long* kw, int M, int K, TopkShared& sh,
-                                      unsigned long long* T, int* keq) {
+                                      unsigned long long* T, int* keq, unsigned long long* mask_out) {
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
     sh.prefix = 0ull;
     sh.k = K;
+    sh.done = 0;
   }
   unsigned long long mask = 0ull;
   for (int shift = 56; shift >= 0; shift -= 8) {
@@ -64,6 +83,7 @@ __device__ inline void topk_threshold(const unsigned long long* kw, int M, int K
           if (cum + c[j] >= k) {
             sh.prefix = prefix | ((unsigned long long)(255 - 8 * lane - j) << shift);
             sh.k = k - cum;
+            sh.done = cum + c[j] == k;  // the bucket holds exactly the keys still to take
             break;
           }
           cum += c[j];
@@ -72,9 +92,11 @@ __device__ inline void topk_threshold(const unsigned long long* kw, int M, int K
     }
     mask |= 255ull << shift;
     __syncthreads();
+    if (sh.done) break;  // uniform: read after the barrier
   }
   *T = sh.prefix;
   *keq = sh.k;
+  *mask_out = mask;
   __syncthreads();
 }
 

@@ -141,6 +141,18 @@ def test_update_parity(phd, orc, mname, n, M):
 
 
 @pytest.mark.parametrize("mname", ["position", "range_bearing"])
+@pytest.mark.parametrize("tile", ["64", "256"])
+def test_update_parity_record_tiles(phd, orc, mname, tile, monkeypatch):
+    """Every record-tile size of the dense passes (plan_gp shrinks tiles for small
+    populations; PHD_TILE forces one) on a ragged population spanning many tiles."""
+    monkeypatch.setenv("PHD_TILE", tile)
+    m = MODELS[mname]
+    f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 64 * 83 + 29, 300, seed=7)
+    _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
+    f.close()
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
 @pytest.mark.parametrize("M", [3200, 3600, 4090, 4096])
 def test_update_parity_large_m_layouts(phd, orc, mname, M):
     """max_meas = 4096 with M where the slot layout picks 256-slot z-blocks (4 slots per
