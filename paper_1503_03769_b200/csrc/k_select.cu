@@ -123,18 +123,29 @@ cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const
 // Pass-2 slot layout (one CTA).  Sequence = [selected labels | unselected labels],
 // each part grouped by bearing class (range-bearing) and padded to even counts so
 // that every f32x2 slot pair is class-homogeneous; labels ascending inside.  The
-// sequence fills first the "state-sum" slots -- the first 2 js slots of every lane,
-// js = ceil(#selected / (2 * lanes)) -- then the remaining slots, so that every
-// warp carries the same share of state-sum work.  *js_out = js.
-__device__ __forceinline__ int seq_slot(int p, int n_s, int lanes, int zl, int js) {
-  if (js < 0) return p;  // whole-z-block layout: the sequence in slot order
+// sequence fills first the "state-sum" slots -- the first 2 jl slots of every lane and
+// two more on every lane of the first n_hi warps, just enough for the selected labels
+// (a lane-uniform count wasted up to a pair per lane: cfg 4, 1000 of 3100 labels
+// selected, summed on 50 % of the slot pairs instead of 31 %) -- then the remaining slots.
+// *js_out = jl | (n_hi << 8).
+// Sequence position p -> slot.  The state-sum region: lanes of the first n_hi warps hold
+// 2 (jl + 1) sequence slots each, the other lanes 2 jl (lane-major inside a lane); then the
+// rest fills the remaining zl - 2 js(lane) slots of every lane in lane order.  jl < 0:
+// whole-z-block layout (the sequence in slot order).
+__device__ __forceinline__ int seq_slot(int p, int lanes, int zl, int jl, int n_hi) {
+  if (jl < 0) return p;
+  const int jh = jl + 1, lh = 32 * n_hi;  // lanes with jh pairs
+  const int s_hi = 2 * jh * lh, n_s = s_hi + 2 * jl * (lanes - lh);
   if (p < n_s) {
-    int l = p / (2 * js);
-    return l * zl + p % (2 * js);
+    if (p < s_hi) return (p / (2 * jh)) * zl + p % (2 * jh);
+    const int q = p - s_hi;
+    return (lh + q / (2 * jl)) * zl + q % (2 * jl);
   }
-  int q = p - n_s, rest = zl - 2 * js;
-  int l = q / rest;
-  return l * zl + 2 * js + q % rest;
+  int q = p - n_s;
+  const int rh = zl - 2 * jh, rl = zl - 2 * jl;
+  if (rh > 0 && q < rh * lh) return (q / rh) * zl + 2 * jh + q % rh;
+  q -= rh * lh;
+  return (lh + q / rl) * zl + 2 * jl + q % rl;
 }
 
 __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const int32_t* sel_flag, int M, int model,
@@ -147,12 +158,13 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
   constexpr int NC = 6;
   __shared__ int wsum[32][NC];
   __shared__ int cat_start[NC + 1];
-  __shared__ int s_js;
+  __shared__ int s_js, s_nhi;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nw = nthr >> 5;
   const int per = (M + nthr - 1) / nthr;
   const float hp = 1.57079632679489662f;
   const int lanes = slots_pad / zl;
   const bool rb = model == kRangeBearing;
+
   for (int s = tid; s < slots_pad; s += nthr) slot_label[s] = -1;
   auto cat_of = [&](int l) {
     int cls = 0;
@@ -212,23 +224,27 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
       cat_start[NC] = base;
       // state-sum layout: js slot pairs on every lane, or whole z-blocks (CTA-uniform)
       // when that needs fewer state-sum slots: *js_out = kJsZBlock | zb_sum
+      // per lane: jl slot pairs, one more on the lanes of the first n_hi warps (warp-
+      // uniform), just enough for the n_sel selected slots (js_layout)
       const int n_sel = cat_start[3];
-      int js = (n_sel + 2 * lanes - 1) / (2 * lanes);
-      js = min(max(js, 0), zl / 2);
+      int sum_slots;
+      const int32_t enc = js_layout(n_sel, lanes, zl, true, &sum_slots);
+      const int jl = enc & 0xFF, n_hi = (enc >> 8) & 0xFF;
       const int spz = wz * 32 * zl;
       const int zb_sum = (n_sel + spz - 1) / spz;
-      if (layout == 2 || (layout == 0 && zb_sum * spz < 2 * js * lanes)) {
+      if (layout == 2 || (layout == 0 && zb_sum * spz < sum_slots)) {
         *js_out = kJsZBlock | zb_sum;
         s_js = -1;
+        s_nhi = 0;
       } else {
-        *js_out = js;
-        s_js = js;
+        *js_out = jl | (n_hi << 8);
+        s_js = jl;
+        s_nhi = n_hi;
       }
     }
   }
   __syncthreads();
-  const int js = s_js;
-  const int n_s = js < 0 ? 0 : 2 * js * lanes;
+  const int js = s_js, n_hi = s_nhi;
   int pos[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) pos[c] = cat_start[c] + wsum[warp][c] + excl[c];
@@ -240,7 +256,7 @@ __device__ __forceinline__ void slots2_body(const float* __restrict__ z, const i
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
       if (c == cc) p = pos[cc]++;
-    slot_label[seq_slot(p, n_s, lanes, zl, js)] = l;
+    slot_label[seq_slot(p, lanes, zl, js, n_hi)] = l;
   }
   __syncthreads();
   // per-slot constants of the new layout (as k_build_slots) and d = 1/D (as k_zconst):

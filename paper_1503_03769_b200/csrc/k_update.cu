@@ -155,7 +155,7 @@ __device__ __forceinline__ void residual(const float* rec, const float4& P, cons
 #ifndef PHD_PASS1_MINB8
 #define PHD_PASS1_MINB8 2
 #endif
-template <int MODEL, int PASS, int ZL, int TILE>
+template <int MODEL, int PASS, int ZL, int TILE, bool SPLIT>
 __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
                                   ZL == 8 ? (kMaxWarpsZ > 8 ? 1 : (PASS == 1 ? PHD_PASS1_MINB8 : PHD_PASS_MINB8)) : 3)
     k_pass(const PassArgs a) {
@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(max_warps_z(ZL) * 32,
   if (PASS == 2) {
     const int v = a.js == nullptr ? NP : *a.js;
     // kJsZBlock | b: all slot pairs of the first b z-blocks (CTA-uniform), none elsewhere
-    js = (v & kJsZBlock) ? (zb < (v & (kJsZBlock - 1)) ? NP : 0) : min(v, NP);
+    // SPLIT (pass 2 of a per-warp layout, js_layout): the count of this warp
+    js = (v & kJsZBlock) ? (zb < (v & (kJsZBlock - 1)) ? NP : 0)
+                         : (SPLIT ? min(js_of_warp(v, zb * wz + warp), NP) : min(v, NP));
   }
   // one instance of the whole sweep per JS (pass 2: state sums for the first JS slot pairs
   // of every lane, where the index set I lives), so that each instance holds only the
@@ -361,25 +363,31 @@ static size_t pass_smem(int wz, int tile) {
   return b;
 }
 
-template <int MODEL, int PASS, int ZL, int TILE>
+template <int MODEL, int PASS, int ZL, int TILE, bool SPLIT>
 static void set_attr() {
-  ensure_max_smem(k_pass<MODEL, PASS, ZL, TILE>, pass_smem<MODEL, PASS, ZL>(max_warps_z(ZL), TILE));
+  ensure_max_smem(k_pass<MODEL, PASS, ZL, TILE, SPLIT>, pass_smem<MODEL, PASS, ZL>(max_warps_z(ZL), TILE));
 }
 
 // the tile size is a template parameter (a runtime tile costs 4.5% in cfg 5's pass 2)
-template <int MODEL, int PASS, int ZL, int TILE>
+template <int MODEL, int PASS, int ZL, int TILE, bool SPLIT>
 static cudaError_t launch_tile(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
-  set_attr<MODEL, PASS, ZL, TILE>();
+  set_attr<MODEL, PASS, ZL, TILE, SPLIT>();
   dim3 grid((unsigned)gp, (unsigned)zb);
-  pdl_launch(k_pass<MODEL, PASS, ZL, TILE>, grid, wz * 32, pass_smem<MODEL, PASS, ZL>(wz, TILE), s, a);
+  pdl_launch(k_pass<MODEL, PASS, ZL, TILE, SPLIT>, grid, wz * 32, pass_smem<MODEL, PASS, ZL>(wz, TILE), s, a);
   return cudaGetLastError();
+}
+
+template <int MODEL, int PASS, int ZL, int TILE>
+static cudaError_t launch_split(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
+  if (PASS == 2 && a.js_split) return launch_tile<MODEL, PASS, ZL, TILE, PASS == 2>(a, gp, zb, wz, s);
+  return launch_tile<MODEL, PASS, ZL, TILE, false>(a, gp, zb, wz, s);
 }
 
 template <int MODEL, int PASS, int ZL>
 static cudaError_t launch_one(const PassArgs& a, int gp, int zb, int wz, cudaStream_t s) {
-  if (a.tile == kTileSmall) return launch_tile<MODEL, PASS, ZL, kTileSmall>(a, gp, zb, wz, s);
+  if (a.tile == kTileSmall) return launch_split<MODEL, PASS, ZL, kTileSmall>(a, gp, zb, wz, s);
   if (a.tile != kTileP) return cudaErrorInvalidValue;
-  return launch_tile<MODEL, PASS, ZL, kTileP>(a, gp, zb, wz, s);
+  return launch_split<MODEL, PASS, ZL, kTileP>(a, gp, zb, wz, s);
 }
 
 template <int MODEL, int ZL>
@@ -453,9 +461,9 @@ cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, 
 
 template <int MODEL, int PASS, int ZL>
 static int occ_one(int wz) {
-  set_attr<MODEL, PASS, ZL, kTileP>();
+  set_attr<MODEL, PASS, ZL, kTileP, false>();
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<MODEL, PASS, ZL, kTileP>, wz * 32,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<MODEL, PASS, ZL, kTileP, false>, wz * 32,
                                                 pass_smem<MODEL, PASS, ZL>(wz, kTileP));
   return n;
 }

@@ -1309,6 +1309,17 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     if (c->select) {
       // index set I from dW = C/D and the mass identity; pass-2 slot layout with I first
       SlotConsts sc2{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
+      // pass 2's SPLIT instance when the per-warp state-sum layout is expected, from the
+      // previous step's LT (a guess for speed only: the layout is the select kernel's, from
+      // this step's data, and either instance computes its bits -- js_layout)
+      int ss_uniform, ss_split;
+      const int lanes = c->slots_pad / c->zl;
+      const int n_est = (int)std::min<int64_t>(c->LT > 0 ? c->LT : M / 4, M);
+      js_layout(n_est, lanes, c->zl, false, &ss_uniform);
+      js_layout(n_est, lanes, c->zl, true, &ss_split);
+      pa.js_split = ss_split < ss_uniform ? 1 : 0;
+      const char* jse = getenv("PHD_JS_SPLIT");  // tests: force either instance
+      if (jse && (jse[0] == '0' || jse[0] == '1')) pa.js_split = jse[0] - '0';
       KL(launch_select_slots(c->C, c->D, M, c->C_slot + c->slots_pad, c->p.p_d, c->sel_flag, c->sel_info, c->zlab,
                              c->model, c->zl, c->wz, sum_layout(), c->slots_pad, c->slot_label, c->s_lim,
                              (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc2, c->st,

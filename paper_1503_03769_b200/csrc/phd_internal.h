@@ -111,6 +111,7 @@ struct PassArgs {
   int64_t n;                 // local particles
   int64_t tiles_per_cta;
   int tile;                  // particles per record tile: kTileP or kTileSmall (plan_gp)
+  int js_split;              // pass 2: the per-warp state-sum layout may be used (js_layout)
   const float* x;
   const float* vx;
   const float* y;
@@ -353,10 +354,33 @@ cudaError_t launch_block_sums(const float* w, int64_t n, double* blk, cudaStream
 cudaError_t launch_select(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                           int32_t* sel_flag, double* info, cudaStream_t s);
 // k_select + the pass-2 slot layout with its per-slot constants (as k_build_slots) and 1/D
-// *js = j (0..ZL/2): the first j slot pairs of every lane carry the state sums, or
+// *js = j | (h << 8): the first j + 1 slot pairs of every lane of the first h warps (global
+// warp index, z-block major) and the first j of every other lane carry the state sums
+// (j in 0..ZL/2; warp-uniform, so each warp runs the sweep instance of its own count), or
 // kJsZBlock | b: every slot of the first b z-blocks does (layout 0: whichever needs fewer
 // sum slots; 1 / 2 force the per-lane / whole-z-block layout, for tests: PHD_SUM_LAYOUT)
 constexpr int32_t kJsZBlock = 0x10000;
+// slot pairs per lane with state sums, for global warp gw, from the per-lane encoding above
+__host__ __device__ inline int js_of_warp(int32_t v, int gw) { return (v & 0xFF) + (gw < ((v >> 8) & 0xFF) ? 1 : 0); }
+// The per-lane layout for n_sel selected slots over `lanes` lanes of zl slots: jl pairs
+// per lane, one more on the lanes of the first n_hi warps -- split only where it saves at
+// least a quarter of the lane-uniform layout's sum slots, else lane-uniform.  Returns the
+// encoding jl | (n_hi << 8) and the state-sum slots.  The layout depends only on this
+// step's data (a resumed run is bitwise the same); which pass-2 instance runs it is a
+// host guess (the SPLIT instance costs ~1 % where nothing is split, cfg 5): the non-SPLIT
+// instance reads a split encoding as "every slot pair" -- a superset, the same bits.
+__host__ __device__ inline int32_t js_layout(int n_sel, int lanes, int zl, bool allow_split, int* sum_slots) {
+  int jl = n_sel / (2 * lanes);
+  if (jl > zl / 2) jl = zl / 2;
+  const int rem = n_sel - 2 * jl * lanes > 0 ? n_sel - 2 * jl * lanes : 0;
+  int n_hi = jl < zl / 2 ? (rem + 63) / 64 : 0;
+  if (n_hi > 0 && (!allow_split || 4 * (2 * jl * lanes + 64 * n_hi) > 3 * (2 * (jl + 1) * lanes))) {
+    jl += 1;  // lane-uniform
+    n_hi = 0;
+  }
+  *sum_slots = 2 * jl * lanes + 64 * n_hi;
+  return jl | (n_hi << 8);
+}
 cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M, const double* W_pred, double p_d,
                                 int32_t* sel_flag, double* info, const float* z, int model, int zl, int wz,
                                 int layout, int slots_pad, int32_t* slot_label, int32_t* js, float sensor_x,

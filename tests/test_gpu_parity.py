@@ -551,6 +551,29 @@ def test_index_set_state_sums(phd, orc, mname, layout, M, monkeypatch):
     assert abs(s2["W"] - rhs) <= 2e-6 * rhs
 
 
+@pytest.mark.parametrize("mname", ["position", "range_bearing"])
+@pytest.mark.parametrize("M,clutter", [(700, 5.0), (2992, 5.0), (3100, 2000.0)])
+def test_pass2_instances_same_bits(phd, mname, M, clutter, monkeypatch):
+    """Pass 2's SPLIT instance (per-warp state-sum counts) and the plain one (which reads a
+    split layout as "every slot pair") are chosen by a host guess from the previous LT; the
+    slot layout is the select kernel's, from this step's data.  Either instance must give
+    the same bits (js_layout), so a resumed run does not depend on that guess."""
+    m = replace(MODELS[mname], clutter_rate=clutter, stphd_all=0)
+    z = _meas(m, M, 5)
+    soa, w = _cloud(m, 12001, z, 5)
+    res = []
+    for forced in ("0", "1"):
+        monkeypatch.setenv("PHD_JS_SPLIT", forced)
+        f = phd.Filter(m)
+        f.set_particles(soa, w, soa.shape[1], stage=phd.STAGE_PREDICTED)
+        f.update(z)
+        acc = f.accumulators(len(z))
+        _, wn, _ = f.get_particles()
+        res.append((acc, wn))
+        f.close()
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
 def test_edge_counts_and_flags(phd, orc):
     """M = 1; M = max_meas = 8192 (largest sort / slot layout); LT above the eligible labels
     (lt_clamped); adaptive N_out clamped to capacity - J (count_clamped)."""
