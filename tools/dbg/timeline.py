@@ -11,6 +11,9 @@ from torch.profiler import profile, ProfilerActivity
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 cfg = scenario.get(name)
 cfg = replace(cfg, scenario=replace(cfg.scenario, steps=40))
+if os.environ.get("GATE"):  # GATE=1: the gated update
+    cfg = replace(cfg, model=replace(cfg.model, gate=int(os.environ["GATE"])))
+NPROF = int(os.environ.get("NPROF", "4"))
 truth = scenario.simulate_truth(cfg)
 Z = scenario.measurements(cfg, truth)
 Zd = [torch.from_numpy(z).cuda() for z in Z]
@@ -18,11 +21,12 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 f = phd.Filter(cfg.model, stream=stream.cuda_stream)
 f.init_population(**scenario.init_args(cfg, truth))
-for k in range(1, 21):
+for k in range(1, 9 if cfg.model.fixed_count > 1000000 else 21):
     f.step_raw(k, Zd[k - 1].data_ptr(), len(Z[k - 1]))
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    for k in range(21, 25):
+    k0 = 9 if cfg.model.fixed_count > 1000000 else 21
+    for k in range(k0, k0 + NPROF):
         f.step_raw(k, Zd[k - 1].data_ptr(), len(Z[k - 1]))
     torch.cuda.synchronize()
 path = "/tmp/tl_%s.json" % name
@@ -40,5 +44,11 @@ for e in gpu:
 cpu = [e for e in ev if e.get("ph") == "X" and e.get("cat") == "cuda_runtime"]
 from collections import Counter
 c = Counter(e["name"] for e in cpu)
-print("runtime calls per 4 steps:", dict(c))
+print("runtime calls per %d steps:" % NPROF, dict(c))
+busy = sum(e["dur"] for e in gpu)
+span = gpu[-1]["ts"] + gpu[-1]["dur"] - gpu[0]["ts"]
+print("gpu ops %d, busy %.1f us, span %.1f us (%.1f us per step)" % (len(gpu), busy, span, span / NPROF))
+big = sorted(gpu, key=lambda e: -e["dur"])[:12]
+for e in big:
+    print("  %8.1f us  %s" % (e["dur"], e["name"][:80]))
 f.close()
