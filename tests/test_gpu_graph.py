@@ -90,3 +90,40 @@ def test_graph_step_zero_mass_and_stphd_all(phd, monkeypatch):
             assert f.graph_stats()[1] == 1
             assert s["zero_mass"] == ref[0]["zero_mass"] == 1 and np.array_equal(a, ref[1])
         f.close()
+
+
+def test_onesync_more_estimates_than_eager_copy(phd, monkeypatch):
+    """LT above the 256 estimates k_step_out stores with the step's results: the rest
+    are copied after the synchronisation; bitwise the classic step."""
+    base = scenario.get("cfg3")
+    cfg = replace(base, scenario=replace(base.scenario, n_targets=420, steps=3))
+    ref, _ = _run(phd, cfg, 3, False, monkeypatch, onesync=False)
+    one, _ = _run(phd, cfg, 3, False, monkeypatch, onesync=True)
+    assert max(s["n_est"] for s, *_ in ref) > 256
+    for (s0, e0, a0, p0, w0, m0), (s1, e1, a1, p1, w1, m1) in zip(ref, one):
+        assert s0 == s1 and np.array_equal(e0["labels"], e1["labels"]) and np.array_equal(e0["states"], e1["states"])
+        assert np.array_equal(e0["mass"], e1["mass"]) and np.array_equal(a0, a1) and np.array_equal(w0, w1)
+
+
+@pytest.mark.parametrize("onesync", [False, True])
+def test_nan_measurement_reported_then_cleared(phd, monkeypatch, onesync):
+    """A NaN measurement makes C non-finite: the step reports PHD_EMODEL (the one-sync
+    step through k_step_out's flags).  The counters start from zero again for the next
+    filter step (k_step_out clears them; the classic update clears them first)."""
+    monkeypatch.setenv("PHD_ONESYNC", "1" if onesync else "0")
+    cfg = scenario.get("cfg3")
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    f = phd.Filter(cfg.model)
+    f.init_population(**scenario.init_args(cfg, truth))
+    f.step(1, Z[0])
+    zbad = Z[1].copy()
+    zbad[3, 0] = np.nan
+    with pytest.raises(RuntimeError, match="non-finite"):
+        f.step(2, zbad)
+    f.close()
+    g = phd.Filter(cfg.model)  # a fresh filter on the same device: no stale flag
+    g.init_population(**scenario.init_args(cfg, truth))
+    g.step(1, Z[0])
+    g.step(2, Z[1])
+    g.close()
