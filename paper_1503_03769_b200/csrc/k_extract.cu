@@ -220,4 +220,7 @@ cudaError_t launch_step_out(const StepOutArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+
+void preload_extract() { touch_kernels(k_extract, k_step_out); }
+
 }  // namespace phd

@@ -1246,4 +1246,14 @@ cudaError_t launch_gate_reduce(int pass, const int32_t* mstart, const int32_t* m
   return cudaGetLastError();
 }
 
+
+void preload_gate() {
+  touch_kernels(k_scan_sum, k_scan_top, k_scan_apply, k_ms_hist<KeyCell>, k_ms_hist<KeyArr>, k_ms_hist<KeyZ>,
+                k_ms_scatter<KeyArr>, k_ms_scatter<KeyZ>, k_psort_pad, k_psort_scatter<kPosIso>,
+                k_psort_scatter<kRangeBearing>, k_gate_count, k_gate_fill, k_gate_count_labels, k_mstart_from_hist,
+                k_zero_i32, k_gate_reduce<1>, k_gate_reduce<2>, k_zbin_finish);
+  touch_kernels(k_gpass<kPosIso, 1, 2>, k_gpass<kPosIso, 2, PHD_GATE_NPAIR_POS>, k_gpass<kPosAniso, 1, 2>,
+                k_gpass<kPosAniso, 2, PHD_GATE_NPAIR_POS>, k_gpass<kRangeBearing, 1, 2>, k_gpass<kRangeBearing, 2, 2>);
+}
+
 }  // namespace phd

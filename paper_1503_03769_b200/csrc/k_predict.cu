@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <set>
 #include "philox.cuh"
 
 namespace phd {
@@ -27,6 +28,22 @@ cudaError_t ensure_max_smem_impl(const void* func, int bytes) {
   e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) have = bytes;
   return e;
+}
+
+void preload_kernels() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert(dev).second) return;
+  preload_predict();
+  preload_update();
+  preload_select();
+  preload_extract();
+  preload_resample();
+  preload_gate();
+  cudaGetLastError();  // attribute queries never leave an error behind
 }
 
 bool pdl_enabled() {
@@ -445,6 +462,12 @@ cudaError_t launch_sum_ranks(const double* const* srcs, int world, double* dst, 
   for (int r = 0; r < world; ++r) rp.p[r] = srcs[r];
   pdl_launch(k_sum_ranks, (unsigned)((n + 255) / 256), 256, 0, s, rp, world, dst, n);
   return cudaGetLastError();
+}
+
+
+void preload_predict() {
+  touch_kernels(k_predict<false>, k_predict<true>, k_birth_is, k_rb_repr, k_init_population, k_init_weights,
+                k_philox_kat, k_fill, k_sum_ranks);
 }
 
 }  // namespace phd

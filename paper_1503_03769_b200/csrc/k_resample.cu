@@ -8,6 +8,8 @@
 #include "phd_internal.h"
 #include "philox.cuh"
 
+#include <algorithm>
+
 namespace phd {
 
 __device__ __forceinline__ int64_t n_of(double B, double scale, double U, int64_t lo, int64_t hi) {
@@ -17,13 +19,49 @@ __device__ __forceinline__ int64_t n_of(double B, double scale, double U, int64_
   return n;
 }
 
+// Graph replay (world 1): this step's resampling scalars from the update's results, in
+// the host's arithmetic (phd_resample_exchange / next_count): n_out (fixed, or
+// max(LT, 1) R clamped to capacity - J), U = u52(Philox(0, k, 3, 0)), W = W_0 (the rank's
+// updated mass), scale = n_out / W, w_off = W / n_out; zero mass when !(W > 0).
+__device__ __forceinline__ void resample_setup_body(const SetupArgs& a, DevStep* ds) {
+  int64_t n_out = a.fixed_count;
+  int clamped = 0;
+  const double W = a.rslots[0];
+  if (!a.fixed) {
+    int64_t LT = a.sel_info ? (int64_t)a.sel_info[1] : (int64_t)floor(W + 0.5);
+    if (LT < 0) LT = 0;
+    n_out = (LT > 1 ? LT : 1) * a.R;
+    if (n_out > a.lim) {
+      n_out = a.lim;
+      clamped = 1;
+    }
+  }
+  const U4 o = philox_at(a.seed, 0, (uint32_t)(a.k > 0 ? a.k : ds->k), 3u);
+  ds->n_out = n_out;
+  ds->count_clamped = clamped;
+  ds->U = u52(o.x, o.y);
+  ds->W = W;
+  ds->zero_mass = !(W > 0.0);
+  ds->scale = W > 0.0 ? (double)n_out / W : 0.0;
+  ds->w_off = n_out > 0 ? (float)(W / (double)n_out) : 0.0f;
+}
+
+__global__ void k_resample_setup(const SetupArgs a, DevStep* ds) {
+  pdl_wait();
+  if (threadIdx.x == 0 && blockIdx.x == 0) resample_setup_body(a, ds);
+}
+
 // Multi-CTA exclusive scan of the block masses, deterministic: CTA c scans its chunk of
 // kResScanChunk (warp shuffles, then the warp totals: a fixed tree), writes the local
 // exclusive prefixes and its chunk total; the last CTA to finish (atomic ticket) adds the
 // chunk totals in order.  Readers form off(b) = coff[b / kResScanChunk] + loc[b].
+// ds != nullptr (one-sync / graph step): block 0 also computes the step's resampling
+// scalars (resample_setup_body; one launch fewer).
 __global__ void __launch_bounds__(1024) k_scan_chunks(const double* __restrict__ blk, int nb, double* loc,
-                                                      double* ctot, double* coff, unsigned* counter) {
+                                                      double* ctot, double* coff, unsigned* counter,
+                                                      const SetupArgs sa, DevStep* ds) {
   pdl_wait();
+  if (ds != nullptr && blockIdx.x == 0 && threadIdx.x == 0) resample_setup_body(sa, ds);
   __shared__ double ws[33];
   __shared__ bool last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -71,10 +109,11 @@ __global__ void __launch_bounds__(1024) k_scan_chunks(const double* __restrict__
 }
 
 cudaError_t launch_scan_chunks(const double* blk, int nb, double* loc, double* ctot, double* coff, unsigned* counter,
-                               cudaStream_t s) {
-  if (nb <= 0) return cudaSuccess;
-  pdl_launch(k_scan_chunks, (unsigned)((nb + kResScanChunk - 1) / kResScanChunk), kResScanChunk, 0, s, blk, nb, loc, ctot, coff,
-             counter);
+                               cudaStream_t s, const SetupArgs* sa, DevStep* ds) {
+  if (nb <= 0 && ds == nullptr) return cudaSuccess;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ((int64_t)nb + kResScanChunk - 1) / kResScanChunk);
+  pdl_launch(k_scan_chunks, grid, kResScanChunk, 0, s, blk, std::max(nb, 0), loc, ctot, coff, counter,
+             sa ? *sa : SetupArgs{}, ds);
   return cudaGetLastError();
 }
 
@@ -262,35 +301,6 @@ __global__ void __launch_bounds__(kMT * kGatherR) k_resample_gather(const Resamp
   if (P2P) __threadfence_system();
 }
 
-// Graph replay (world 1): this step's resampling scalars from the update's results, in
-// the host's arithmetic (phd_resample_exchange / next_count): n_out (fixed, or
-// max(LT, 1) R clamped to capacity - J), U = u52(Philox(0, k, 3, 0)), W = W_0 (the rank's
-// updated mass), scale = n_out / W, w_off = W / n_out; zero mass when !(W > 0).
-__global__ void k_resample_setup(const SetupArgs a, DevStep* ds) {
-  pdl_wait();
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int64_t n_out = a.fixed_count;
-  int clamped = 0;
-  const double W = a.rslots[0];
-  if (!a.fixed) {
-    int64_t LT = a.sel_info ? (int64_t)a.sel_info[1] : (int64_t)floor(W + 0.5);
-    if (LT < 0) LT = 0;
-    n_out = (LT > 1 ? LT : 1) * a.R;
-    if (n_out > a.lim) {
-      n_out = a.lim;
-      clamped = 1;
-    }
-  }
-  const U4 o = philox_at(a.seed, 0, (uint32_t)(a.k > 0 ? a.k : ds->k), 3u);
-  ds->n_out = n_out;
-  ds->count_clamped = clamped;
-  ds->U = u52(o.x, o.y);
-  ds->W = W;
-  ds->zero_mass = !(W > 0.0);
-  ds->scale = W > 0.0 ? (double)n_out / W : 0.0;
-  ds->w_off = n_out > 0 ? (float)(W / (double)n_out) : 0.0f;
-}
-
 cudaError_t launch_resample_setup(const SetupArgs& a, DevStep* ds, cudaStream_t s) {
   pdl_launch(k_resample_setup, 1, 32, 0, s, a, ds);
   return cudaGetLastError();
@@ -356,6 +366,12 @@ cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, i
   }
   pdl_launch(k_ring_unpack, (unsigned)((L + 255) / 256), 256, 0, s, a, b, narr, L, n, v);
   return cudaGetLastError();
+}
+
+
+void preload_resample() {
+  touch_kernels(k_resample_setup, k_scan_chunks, k_resample_gather<false>, k_resample_gather<true>, k_ring_pack,
+                k_ring_unpack);
 }
 
 }  // namespace phd

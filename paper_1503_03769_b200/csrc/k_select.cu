@@ -427,4 +427,7 @@ cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M,
   return cudaGetLastError();
 }
 
+
+void preload_select() { touch_kernels(k_block_sum, k_select, k_select_slots, k_build_slots); }
+
 }  // namespace phd

@@ -744,4 +744,21 @@ cudaError_t launch_reduce_acc(const double* Apart, int gp, int slots_pad, int n_
   return cudaGetLastError();
 }
 
+
+template <int MODEL>
+static void preload_model() {
+  touch_kernels(k_pass<MODEL, 1, 4, kTileP, false>, k_pass<MODEL, 1, 4, kTileSmall, false>,
+                k_pass<MODEL, 1, 8, kTileP, false>, k_pass<MODEL, 1, 8, kTileSmall, false>,
+                k_pass<MODEL, 2, 4, kTileP, false>, k_pass<MODEL, 2, 4, kTileSmall, false>,
+                k_pass<MODEL, 2, 8, kTileP, false>, k_pass<MODEL, 2, 8, kTileSmall, false>,
+                k_pass<MODEL, 2, 4, kTileP, true>, k_pass<MODEL, 2, 4, kTileSmall, true>,
+                k_pass<MODEL, 2, 8, kTileP, true>, k_pass<MODEL, 2, 8, kTileSmall, true>);
+}
+void preload_update() {
+  preload_model<kPosIso>();
+  preload_model<kPosAniso>();
+  preload_model<kRangeBearing>();
+  touch_kernels(k_records<kPosIso>, k_records<kRangeBearing>, k_reduce_C, k_zconst, k_finalize, k_reduce_acc);
+}
+
 }  // namespace phd

@@ -520,6 +520,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   } while (0)
   CUB(cudaSetDevice(device));
   CUB(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+  preload_kernels();  // no lazy kernel loading inside a step (first use of a variant)
   if (stream) {
     c->st = (cudaStream_t)stream;
   } else {
@@ -1658,9 +1659,9 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
     sa.lim = c->p.capacity - c->p.births_per_step;
     sa.seed = c->p.seed;
     sa.k = c->capturing ? 0 : k;  // graph replays: k from the staged step block
-    KL(launch_resample_setup(sa, c->dstep, c->st));
     const int64_t n = c->n_local;
-    KL(launch_scan_chunks(c->blk_w, (int)ceil_div(n, kBlockW), c->blk_off, c->ctot, c->coff, c->scan_counter, c->st));
+    KL(launch_scan_chunks(c->blk_w, (int)ceil_div(n, kBlockW), c->blk_off, c->ctot, c->coff, c->scan_counter, c->st,
+                          &sa, c->dstep));
     ResampleArgs ra{};
     ra.n_local = n;
     ra.g0 = 0;

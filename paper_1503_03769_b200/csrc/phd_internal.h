@@ -49,6 +49,25 @@ __device__ __forceinline__ void pdl_wait() {
 }
 bool pdl_enabled();
 
+// CUDA loads kernels lazily (CUDA_MODULE_LOADING=LAZY, the default): the first launch of
+// each one pays for loading it, ~0.1 ms, inside whichever step first needs that variant
+// (a tile size, a pass-2 instance, ...).  Each kernel file's preload_*() asks for the
+// attributes of all its kernels, which loads them; phd_create calls preload_kernels()
+// once per device.
+template <typename... K>
+inline void touch_kernels(K... k) {
+  cudaFuncAttributes a;
+  int dummy[] = {0, ((void)cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k)), 0)...};
+  (void)dummy;
+}
+void preload_update();
+void preload_select();
+void preload_extract();
+void preload_resample();
+void preload_predict();
+void preload_gate();
+void preload_kernels();  // all of the above, once per device (thread-safe)
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute: set it
 // once per (kernel, device) -- and again if a launch needs more -- so that one
 // process driving several GPUs can launch the >48 KB kernels on every device.
@@ -303,13 +322,7 @@ struct ResampleGatherArgs {
   float *ox, *ovx, *oy, *ovy, *ow;  // local outputs at the produced index (p2p == 0)
   int32_t* anc;              // [produced]: global ancestor
 };
-// exclusive fp64 scan of nb block masses: loc[b] (within its chunk of kResScanChunk), coff[c]
-// (chunk prefix; coff[nchunks] = total); deterministic, one launch (last CTA combines)
-cudaError_t launch_scan_chunks(const double* blk, int nb, double* loc, double* ctot, double* coff, unsigned* counter,
-                               cudaStream_t s);
-struct PeerOut;
-cudaError_t launch_resample_gather(const ResampleGatherArgs& a, const PeerOut* po, cudaStream_t s);
-// graph replay (world 1): n_out, U, W, scale, w_off, zero_mass of this step into ds
+// one-sync / graph step (world 1): n_out, U, W, scale, w_off, zero_mass of this step into ds
 struct SetupArgs {
   const double* rslots;      // rank slots [W_r | ...] (C2 buffer)
   const double* sel_info;    // (W by the mass identity, LT, ...) of k_select_slots
@@ -319,6 +332,13 @@ struct SetupArgs {
   int32_t k;                 // the step (> 0), or 0: ds->k (graph replays)
 };
 cudaError_t launch_resample_setup(const SetupArgs& a, DevStep* ds, cudaStream_t s);
+// exclusive fp64 scan of nb block masses: loc[b] (within its chunk of kResScanChunk), coff[c]
+// (chunk prefix; coff[nchunks] = total); deterministic, one launch (last CTA combines).
+// ds != nullptr: the same launch computes the step's resampling scalars (SetupArgs) into ds.
+cudaError_t launch_scan_chunks(const double* blk, int nb, double* loc, double* ctot, double* coff, unsigned* counter,
+                               cudaStream_t s, const SetupArgs* sa = nullptr, DevStep* ds = nullptr);
+struct PeerOut;
+cudaError_t launch_resample_gather(const ResampleGatherArgs& a, const PeerOut* po, cudaStream_t s);
 
 // End of a one-sync / graph step (world 1): every result the host reads after the step's
 // one synchronisation, stored by one kernel into pinned host memory (mapped, UVA) instead
