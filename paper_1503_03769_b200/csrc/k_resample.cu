@@ -46,11 +46,6 @@ __device__ __forceinline__ void resample_setup_body(const SetupArgs& a, DevStep*
   ds->w_off = n_out > 0 ? (float)(W / (double)n_out) : 0.0f;
 }
 
-__global__ void k_resample_setup(const SetupArgs a, DevStep* ds) {
-  pdl_wait();
-  if (threadIdx.x == 0 && blockIdx.x == 0) resample_setup_body(a, ds);
-}
-
 // Multi-CTA exclusive scan of the block masses, deterministic: CTA c scans its chunk of
 // kResScanChunk (warp shuffles, then the warp totals: a fixed tree), writes the local
 // exclusive prefixes and its chunk total; the last CTA to finish (atomic ticket) adds the
@@ -301,10 +296,6 @@ __global__ void __launch_bounds__(kMT * kGatherR) k_resample_gather(const Resamp
   if (P2P) __threadfence_system();
 }
 
-cudaError_t launch_resample_setup(const SetupArgs& a, DevStep* ds, cudaStream_t s) {
-  pdl_launch(k_resample_setup, 1, 32, 0, s, a, ds);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_resample_gather(const ResampleGatherArgs& a, const PeerOut* po, cudaStream_t s) {
   if (a.r.n_local <= 0) return cudaSuccess;
@@ -370,7 +361,7 @@ cudaError_t launch_ring_unpack(float* const* src, float* const* dst, int narr, i
 
 
 void preload_resample() {
-  touch_kernels(k_resample_setup, k_scan_chunks, k_resample_gather<false>, k_resample_gather<true>, k_ring_pack,
+  touch_kernels(k_scan_chunks, k_resample_gather<false>, k_resample_gather<true>, k_ring_pack,
                 k_ring_unpack);
 }
 

@@ -8,8 +8,9 @@
 //             k_select_slots -> k_pass<2> -> k_finalize -> k_reduce_acc -> [C2 all-reduce]
 //             -> D2H of the rank masses and flags (gated: k_gate.cu kernels instead)
 //   extract   k_extract on rank 0 (the central unit) + D2H of the estimates
-//   resample  k_scan_chunks -> k_resample_gather (one rank inside phd_step: k_resample_setup
-//             first, the extraction on a second stream, one host synchronisation per step)
+//   resample  k_scan_chunks -> k_resample_gather (one rank inside phd_step: k_scan_chunks also
+//             computes the resampling scalars; the extraction on a second stream, one host
+//             synchronisation per step)
 //   exchange  world 1: buffer swap; world > 1: k_resample_gather<true> into the owners'
 //             arrays over the peer-memory window + one barrier, or grouped ncclSend/ncclRecv (C3)
 #include <algorithm>
@@ -1648,7 +1649,7 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
   if (c->stage != kUpdated) return fail(c, PHD_ESTATE, "phd_resample_exchange needs an updated population");
   if (c->dev_scalars) {
     // one-sync / graph step (world 1, exact): n_out, U, W, zero mass of this step are
-    // computed on the device from the update's results (k_resample_setup), read back after
+    // computed on the device from the update's results (resample_setup_body in k_scan_chunks), read back after
     // the step's synchronisation
     SetupArgs sa{};
     sa.rslots = c->rslots;
@@ -1866,7 +1867,7 @@ phd_status phd_resample_exchange(phd_ctx* c, int32_t k) {
 // (predict, the dense update, extraction, resampling) -- one launch and one host
 // synchronisation instead of ~15 launches.  The per-step scalars (k, M, M_{k-1}) are
 // staged in pinned memory and copied by the graph's first node; the resampling
-// count, offset and mass are computed on the device (k_resample_setup); graphs are
+// count, offset and mass are computed on the device (resample_setup_body in k_scan_chunks); graphs are
 // cached per launch shape (particle count, slot layout, particle buffer), so a
 // configuration replays a handful of graphs.
 static bool graph_eligible(const phd_ctx* c, int M) {
@@ -2022,13 +2023,10 @@ static phd_status step_graph(phd_ctx* c, int32_t k, const float* z, int32_t M, p
 }
 
 // One-sync step (world 1, exact mode): the resampling count / offset / mass are computed
-// on the device (k_resample_setup), so predict -> update -> [extraction on st2 |
+// on the device (resample_setup_body in k_scan_chunks), so predict -> update -> [extraction on st2 |
 // resampling] run without the host in between and the step synchronises once, at its end.
 static phd_status step_onesync(phd_ctx* c, int32_t k, const float* z, int32_t M, phd_estimate* out, int32_t cap,
                                int32_t* n_out, phd_summary* s) {
-  c->h_stepin[0] = k;
-  c->h_stepin[1] = M;
-  c->h_stepin[2] = std::max(c->M_z, 0);
   c->dev_scalars = true;  // (k, M, M_prev) reach the kernels as arguments: no staged step block
   c->defer_update_sync = true;
   phd_status st = phd_predict(c, k, nullptr, 0);

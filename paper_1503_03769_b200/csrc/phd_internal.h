@@ -152,8 +152,8 @@ struct PassArgs {
 };
 
 // Per-step scalars of a CUDA-graph replay of phd_step (world 1, DESIGN.md §4 "graph
-// step"): the host stages k, M, M_prev (copied by the graph's first node); the
-// resampling setup kernel (k_resample_setup) fills the rest from the update's results.
+// step"): the host stages k, M, M_prev (copied by the graph's first node); block 0 of
+// k_scan_chunks (resample_setup_body) fills the rest from the update's results.
 // Kernels read them when handed a DevStep pointer, their by-value arguments otherwise.
 struct DevStep {
   int32_t k, M, M_prev, zero_mass;
@@ -331,7 +331,6 @@ struct SetupArgs {
   uint64_t seed;
   int32_t k;                 // the step (> 0), or 0: ds->k (graph replays)
 };
-cudaError_t launch_resample_setup(const SetupArgs& a, DevStep* ds, cudaStream_t s);
 // exclusive fp64 scan of nb block masses: loc[b] (within its chunk of kResScanChunk), coff[c]
 // (chunk prefix; coff[nchunks] = total); deterministic, one launch (last CTA combines).
 // ds != nullptr: the same launch computes the step's resampling scalars (SetupArgs) into ds.
