@@ -294,7 +294,11 @@ def run_ours(args):
         obj = [phd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    stream = torch.cuda.current_stream(dev)
+    # the filter's stream: a torch stream made current, so the CUDA events and the L2 flush
+    # are ordered with the filter's kernels (handle 0, the legacy stream, would make the
+    # library create a stream of its own)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ws_bytes = phd.workspace_size(m, world)
     workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)  # device memory from torch
     f = phd.Filter(m, rank=rank, world=world, nccl_id=nid, device=local, stream=stream.cuda_stream,
