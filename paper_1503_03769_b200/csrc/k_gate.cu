@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
         q[r][1] = make_float4(__ldg(src.c[4] + i), __ldg(src.c[5] + i), __ldg(src.c[6] + i), __ldg(src.c[7] + i));
       }
       q[r][N4 - 2] = make_float4(__ldg(src.x + i), __ldg(src.y + i), __ldg(src.vx + i), __ldg(src.vy + i));
-      q[r][N4 - 1] = make_float4(log2f(__ldg(src.w + i) * wscale), 0.0f, 0.0f, 0.0f);  // the dense TileLoader's expression
+      q[r][N4 - 1] = make_float4(log2f(__ldg(src.w + i) * wscale), 0.0f, 0.0f, 0.0f);  // the dense records' expression (k_records)
       lwm = fmaxf(lwm, q[r][N4 - 1].x);  // clamped duplicates of the last item do not change the max
       // a NaN particle makes every dense term NaN (C, D non-finite -> PHD_EMODEL); the
       // gated path might not evaluate it, so it is flagged here (one atomic per warp at the end)

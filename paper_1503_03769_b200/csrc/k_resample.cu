@@ -125,7 +125,7 @@ __device__ __forceinline__ int64_t n_spread(int64_t g, int64_t n_out, int64_t N)
   return (g * n_out + N - 1) / N;
 }
 // Systematic resampling and the offspring gather in one pass: per block
-// of kBlockW particles the bounds of k_resample_mark (same fp64 formula and pinning),
+// of kBlockW particles the offspring bounds n(B_i) (the fp64 formula and pinning above),
 // all kBlockW upper bounds in shared memory; then every offspring k of the block finds
 // its particle by binary search over those bounds (balanced whatever the weights) and
 // copies its state (coalesced writes at consecutive produced indices).  Reads w + state
