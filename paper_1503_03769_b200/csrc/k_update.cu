@@ -19,6 +19,7 @@
 #include <atomic>
 #include "pair_math.cuh"
 #include "bulk.cuh"
+#include "slots.cuh"
 
 #include <algorithm>
 #include <type_traits>
@@ -407,14 +408,21 @@ bool pass2_sums_scaled() { return kFoldD; }
 // Per-particle records of the dense passes (GRec), once per update: HBM-bound, 20 B read
 // and 32 B written per particle (range-bearing: 52 B read, 64 B written).  One float4 of
 // the record per thread, so that a warp's stores are contiguous.  Slots [n, n_pad) get
-// zero records with lw = -inf (their terms are exactly 0).
+// zero records with lw = -inf (their terms are exactly 0).  Block b covers the particles
+// [b kBlockW, (b + 1) kBlockW) and, with blk != nullptr, also writes their fp64 weight sum
+// blk[b] in k_block_sum's order (one launch fewer; the same bits).
 template <int MODEL>
-__global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad) {
+__global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad, double* blk, const BuildSlotsArgs bs) {
   pdl_wait();
+  if (bs.slot_label != nullptr && blockIdx.x == gridDim.x - 1) {  // the slot layout's block
+    build_slots_body(bs);
+    return;
+  }
   constexpr int Q = GRec<MODEL>::WIDTH / 4;  // float4 per record
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   float4* out = reinterpret_cast<float4*>(a.rec);
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < n_pad * Q; f += stride) {
+  const int64_t base = (int64_t)blockIdx.x * kBlockW;
+  const int64_t f0 = base * Q, f1 = min(n_pad, base + kBlockW) * Q;
+  for (int64_t f = f0 + threadIdx.x; f < f1; f += blockDim.x) {
     const int64_t i = f / Q;
     const int q = (int)(f % Q);
     const bool ok = i < a.n;
@@ -439,18 +447,39 @@ __global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad
     }
     out[f] = v;
   }
+  if (blk != nullptr && base < a.n) {  // block-uniform
+    __shared__ double sw[8];
+    const int tid = threadIdx.x;
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < kBlockW / 256; ++r) {
+      const int64_t i = base + r * 256 + tid;
+      if (i < a.n) s += (double)a.w[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((tid & 31) == 0) sw[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double x = 0.0;
+      for (int k = 0; k < 8; ++k) x += sw[k];
+      blk[blockIdx.x] = x;
+    }
+  }
 }
 
 int record_width(int model) { return model == kRangeBearing ? GRec<kRangeBearing>::WIDTH : GRec<kPosIso>::WIDTH; }
 
-cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s) {
+cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s, double* blk, const BuildSlotsArgs* bs) {
   const int64_t n_pad = (a.n + kTileP - 1) / kTileP * kTileP;
-  if (n_pad <= 0) return cudaSuccess;
-  const unsigned grid = (unsigned)std::min<int64_t>((n_pad * (record_width(model) / 4) + 255) / 256, 148 * 16);
+  if (n_pad <= 0 && bs == nullptr) return cudaSuccess;
+  static_assert(kBlockW == 4 * 256, "k_records' block sums follow k_block_sum's order");
+  const BuildSlotsArgs b = bs ? *bs : BuildSlotsArgs{};
+  const unsigned grid = (unsigned)((std::max<int64_t>(n_pad, 0) + kBlockW - 1) / kBlockW) + (bs ? 1u : 0u);
   if (model == kRangeBearing)
-    pdl_launch(k_records<kRangeBearing>, grid, 256, 0, s, a, n_pad);
+    pdl_launch(k_records<kRangeBearing>, grid, 256, 0, s, a, n_pad, blk, b);
   else
-    pdl_launch(k_records<kPosIso>, grid, 256, 0, s, a, n_pad);
+    pdl_launch(k_records<kPosIso>, grid, 256, 0, s, a, n_pad, blk, b);
   return cudaGetLastError();
 }
 

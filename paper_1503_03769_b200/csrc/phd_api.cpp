@@ -3,7 +3,7 @@
 //
 // Per step:
 //   predict   k_predict                                     (HBM)
-//   update    k_build_slots -> k_records -> k_pass<1> -> k_block_sum -> k_reduce_C (+ W_pred;
+//   update    k_records (+ block sums of w, + the slot layout in one more block) -> k_pass<1> -> k_reduce_C (+ W_pred;
 //             one rank: + the per-slot constants) -> [C1 all-reduce -> k_zconst] ->
 //             k_select_slots -> k_pass<2> -> k_finalize -> k_reduce_acc -> [C2 all-reduce]
 //             -> D2H of the rank masses and flags (gated: k_gate.cu kernels instead)
@@ -1212,13 +1212,26 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     phd_status st = build_slots(c, M);
     if (st != PHD_OK) return st;
   }
+  BuildSlotsArgs bsa{};
   if (M > 0) {  // slot -> label map and per-slot constants, on the device
     SlotConsts sc{c->s[0], c->s[1], c->s[2], c->s[3], c->s[4], c->rep};
-    KL(launch_build_slots(z_slots, c->capturing ? &c->dstep->M : nullptr, M, c->model, gated ? 1 : 0, c->slots_pad,
-                          c->slot_label, (float)c->p.sensor_xy[0], (float)c->p.sensor_xy[1], sc, c->bad, c->st,
-                          z_copy));
+    bsa.z = z_slots;
+    bsa.zcopy = z_copy;
+    bsa.Mp = c->capturing ? &c->dstep->M : nullptr;
+    bsa.M = M;
+    bsa.model = c->model;
+    bsa.identity = gated ? 1 : 0;
+    bsa.slots_pad = c->slots_pad;
+    bsa.slot_label = c->slot_label;
+    bsa.sx = (float)c->p.sensor_xy[0];
+    bsa.sy = (float)c->p.sensor_xy[1];
+    bsa.sc = sc;
+    bsa.bad = c->bad;
   }
   const int gp = M > 0 && n > 0 && !gated ? plan_gp(c, n) : 0;
+  // the dense update builds the slot layout in one more block of the records kernel (one
+  // launch fewer); the gated update (and an empty population) launches it on its own
+  if (M > 0 && gp <= 0) KL(launch_build_slots(bsa, c->st));
   c->gp = gp;
   PassArgs pa{};
   pa.n = n;
@@ -1291,12 +1304,13 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     timing_record(c, 6);
     KL(launch_gate_reduce(2, c->gmstart, c->gmlist, M, nullptr, c->gpart2, ga.sel, c->gA, c->slots_pad, c->st));
   } else if (M > 0) {
-    if (gp > 0) KL(launch_records(c->model, pa, c->st));
+    // the records also carry the fp64 block sums of the predicted w (W_pred, which rides with
+    // C in the C1 all-reduce: element slots_pad)
+    if (gp > 0) KL(launch_records(c->model, pa, c->st, c->blk_wp, &bsa));
     timing_record(c, 3);
     if (gp > 0) KL(launch_pass(c->model, 1, pa, gp, c->zb, c->wz, c->zl, c->st));
     timing_record(c, 4);
-    // local W_pred rides with C in the C1 all-reduce (element slots_pad)
-    KL(launch_block_sums(c->A[4], n, c->blk_wp, c->st));
+    if (gp <= 0) KL(launch_block_sums(c->A[4], n, c->blk_wp, c->st));
     // one rank (or a DCP group): C is final after the reduction, which then also writes
     // the per-slot constants; otherwise they follow the C1 all-reduce
     const bool c_final = c->world == 1 || c->dcp;

@@ -126,6 +126,18 @@ struct SlotConsts {
   int32_t* rep;    // range-bearing: 0 (-pi,pi], 1 [0,2pi), 2 (-2pi,0]
 };
 
+// The pass-1 slot layout of one update (slots.cuh): slot -> label map and per-slot constants.
+struct BuildSlotsArgs {
+  const float* z;            // Z (read); zcopy != nullptr: also copied there (the device-resident
+  float* zcopy;              //   Z of the one-sync step: no separate device-to-device copy)
+  const int* Mp;             // graph replays: this step's M, else nullptr and M
+  int M, model, identity, slots_pad;
+  int32_t* slot_label;
+  float sx, sy;              // range-bearing sensor position
+  SlotConsts sc;
+  int* bad;                  // non-finite measurements are counted here
+};
+
 struct PassArgs {
   int64_t n;                 // local particles
   int64_t tiles_per_cta;
@@ -243,17 +255,16 @@ cudaError_t launch_birth_is(const BirthISArgs& a, cudaStream_t s);
 cudaError_t launch_rb_repr(const float* x, const float* y, int64_t n, float sx, float sy, float* rb,
                            int64_t stride, cudaStream_t s);
 // pass-1 slot layout + per-slot constants on the device (k_build_slots, k_select.cu)
-// zcopy != nullptr: also copies Z (read from z) into zcopy (the device-resident Z of the
-// one-sync step: no separate device-to-device copy)
-cudaError_t launch_build_slots(const float* z, const int* Mp, int M, int model, int identity, int slots_pad,
-                               int32_t* slot_label, float sensor_x, float sensor_y, SlotConsts sc, int* bad,
-                               cudaStream_t s, float* zcopy = nullptr);
+cudaError_t launch_build_slots(const BuildSlotsArgs& a, cudaStream_t s);
 cudaError_t launch_pass(int model, int pass, const PassArgs& a, int gp, int zb, int wz, int zl, cudaStream_t s);
 // the dense pass 2 folds 1/D into its terms: its state-sum partials already carry 1/D
 bool pass2_sums_scaled();
 // floats per particle record of the dense passes; build them (once per update, before pass 1)
 int record_width(int model);
-cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s);
+// blk != nullptr: also the fp64 block sums of a.w (kBlockW particles per block, k_block_sum's
+// order); bs != nullptr: one more block builds the pass-1 slot layout (k_build_slots' work)
+cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s, double* blk = nullptr,
+                           const BuildSlotsArgs* bs = nullptr);
 int pass_occupancy(int model, int pass, int wz, int zl);
 
 // per-slot constants after C: D = kappa + C, C_lab / D_lab by label, d = 1/D (fp32), non-finite count
