@@ -4,6 +4,7 @@ ZL / warps / z-blocks, the per-warp state-sum layout and its two pass-2 instance
 whole-z-block layouts, the gated path, ragged tails) is exercised at combinations the
 hand-written cases do not name.  Tolerances are those of test_gpu_parity.py."""
 import math
+import os
 from dataclasses import replace
 
 import numpy as np
@@ -23,7 +24,7 @@ def phd():
     p.load()
     return p
 
-CASES = 48
+CASES = int(os.environ.get("PHD_FUZZ_CASES", "48"))  # longer sweeps: PHD_FUZZ_CASES=400
 
 
 def _case(i):
