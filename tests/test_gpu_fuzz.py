@@ -83,3 +83,49 @@ def test_random_update_extract_resample(phd, orc, i, monkeypatch, near_tie_repor
         near_tie_report(n_out=int(meta["N_out"]), mismatches=int(mism.sum()), near_ties=int(ties.sum()),
                         non_tie_mismatches=0)
     f.close()
+
+
+MR_CASES = int(os.environ.get("PHD_FUZZ_MR_CASES", "12"))
+
+
+@pytest.mark.parametrize("i", range(MR_CASES))
+def test_random_multirank_against_oracle(phd, orc, i, monkeypatch):
+    """P in-process ranks (2-4, uneven blocks, sometimes a rank with no particles) on random
+    sizes: the global C, every rank's weights, the accumulators, and the concatenated
+    ancestors of the rank-local resampling + exchange against the oracle."""
+    from test_gpu_multirank import _parallel
+    r = np.random.default_rng(5000 + i)
+    world = int(r.integers(2, 5))
+    mname = ["position", "range_bearing"][r.integers(2)]
+    n = int(r.choice([world - 1, 300, 5000, 30011]) + r.integers(0, 50))
+    M = int(r.choice([3, 130, 700, 2500]))
+    gate = int(r.choice([0, 2]))
+    if r.random() < 0.5:
+        monkeypatch.setenv("PHD_EXCHANGE", "nccl")
+    m = replace(MODELS[mname], gate=gate, stphd_all=0, max_meas=4096)
+    z = _meas(m, M, 31 + i)
+    soa, w = _cloud(m, n, z, 37 + i)
+    group = phd.LocalGroup(world)
+    fs = [phd.Filter(m, rank=q, world=world, group=group) for q in range(world)]
+    for q, f in enumerate(fs):
+        lo, hi = phd.rank_block(n, world, q)
+        f.set_particles(np.ascontiguousarray(soa[:, lo:hi]), np.ascontiguousarray(w[lo:hi]), n,
+                        stage=phd.STAGE_PREDICTED)
+    _parallel(fs, lambda q, f: f.update(z))
+    C = fs[0].normalizers(M)
+    acc = fs[0].accumulators(M)
+    wn = np.concatenate([fs[q].get_particles()[1] for q in range(world)])
+    _parallel(fs, lambda q, f: f.extract())
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
+    _parallel(fs, lambda q, f: f.resample_exchange(4))
+    parts = sorted((f.ancestors()[1], f.ancestors()[0]) for f in fs)
+    anc = np.concatenate([a for _, a in parts])
+    meta = fs[0].resample_meta()
+    ao, _ = orc.resample(wn.astype(np.float64), meta["U"], meta["N_out"])
+    mism = anc != ao
+    assert not np.any(mism & ~_near_ties(wn, meta["U"], meta["N_out"]))
+    for f in fs:
+        f.close()
+    group.close()
