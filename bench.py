@@ -444,45 +444,62 @@ def run_ours(args):
                          "oracle are checked element-wise in tests/test_gpu_parity.py::test_full_size_sampled"}
 
     # ---- gated update (NEXT-2): same workload, same steps, gate = 1 ----
-    gated = None
+    # exact gating (every skipped term underflows to 0), then with gate_floor F = log2(kappa) - 60
+    # (skipped terms < 2^F: every C(z) within N 2^F <= 2^-36 kappa of the exact one at N <= 2^24)
+    gated = gated_floor = None
     if not args.no_gated_leg and args.gate == 0:
-        f.close()
-        del workspace
-        mg = _replace(m, gate=1)
-        if world > 1:  # an NCCL unique id bootstraps one communicator: a fresh one for this filter
-            obj = [phd.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nid = obj[0]
-        workspace = torch.empty(phd.workspace_size(mg, world), dtype=torch.uint8, device=dev)
-        f = phd.Filter(mg, rank=rank, world=world, nccl_id=nid, device=local, stream=stream.cuda_stream,
-                       workspace=workspace)
-        reset()
-        run_steps(1, args.warmup, Zd, False)
-        g_st = []
-        pairs_g, ms_g = timed_steps(Zd, args.warmup + 1, lambda: g_st.append(f.gate_stats()))
-        g_ms = {"pass1": [], "pass2": [], "update": []}
+        def gated_leg(mg, note):
+            nonlocal f, workspace, nid
+            f.close()
+            workspace = None  # released before the next filter's workspace
+            if world > 1:  # an NCCL unique id bootstraps one communicator: a fresh one for this filter
+                obj = [phd.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                nid = obj[0]
+            workspace = torch.empty(phd.workspace_size(mg, world), dtype=torch.uint8, device=dev)
+            f = phd.Filter(mg, rank=rank, world=world, nccl_id=nid, device=local, stream=stream.cuda_stream,
+                           workspace=workspace)
+            reset()
+            run_steps(1, args.warmup, Zd, False)
+            g_st = []
+            pairs_g, ms_g = timed_steps(Zd, args.warmup + 1, lambda: g_st.append(f.gate_stats()))
+            g_ms = {"pass1": [], "pass2": [], "update": []}
 
-        def collect_g():
-            t = f.timing()
-            for key in g_ms:
-                g_ms[key].append(t[key])
+            def collect_g():
+                t = f.timing()
+                for key in g_ms:
+                    g_ms[key].append(t[key])
 
-        reset()
-        run_steps(1, args.warmup, Zd, False)
-        f.set_timing(True)
-        timed_steps(Zd, args.warmup + 1, collect_g)
-        f.set_timing(False)
-        ev = sum(s_["pairs"] for s_ in g_st)
-        gated = {"ms_per_step": ms_g / args.steps,
-                 "effective_pairs_per_s": pairs_g / (ms_g * 1e-3),
-                 "evaluated_pairs_per_step": ev / max(1, len(g_st)),
-                 "evaluated_fraction": ev / max(1, pairs_g // max(1, world)),
-                 "steps_gated": sum(s_["used"] for s_ in g_st),
-                 "kernel_ms": {k_: statistics.mean(v_) for k_, v_ in g_ms.items()},
-                 "pass_roofline": None,
-                 "note": "gate = 1: only (tile, measurement) pairs whose largest exponent is >= -130 are "
-                         "evaluated (every skipped term is exactly 0 in fp32 ftz); effective = N*M / step time, "
-                         "not a pairs/s roofline claim"}
+            reset()
+            run_steps(1, args.warmup, Zd, False)
+            f.set_timing(True)
+            timed_steps(Zd, args.warmup + 1, collect_g)
+            f.set_timing(False)
+            ev = sum(s_["pairs"] for s_ in g_st)
+            return {"ms_per_step": ms_g / args.steps,
+                    "effective_pairs_per_s": pairs_g / (ms_g * 1e-3),
+                    "evaluated_pairs_per_step": ev / max(1, len(g_st)),
+                    "evaluated_fraction": ev / max(1, pairs_g // max(1, world)),
+                    "steps_gated": sum(s_["used"] for s_ in g_st),
+                    "kernel_ms": {k_: statistics.mean(v_) for k_, v_ in g_ms.items()},
+                    "pass_roofline": None,
+                    "note": note}
+
+        gated = gated_leg(_replace(m, gate=1),
+                          "gate = 1: only (tile, measurement) pairs whose largest exponent is >= -130 are "
+                          "evaluated (every skipped term is exactly 0 in fp32 ftz); effective = N*M / step time, "
+                          "not a pairs/s roofline claim")
+        V = (m.region[1] - m.region[0]) * (m.region[3] - m.region[2])
+        kap = m.clutter_rate / V if V > 0 else 0.0
+        if kap > 0:
+            F = max(-126, min(-20, int(math.floor(math.log2(kap))) - 60))
+            gated_floor = gated_leg(_replace(m, gate=1, gate_floor=F),
+                                    "gate = 1, gate_floor = %d = floor(log2 kappa) - 60: pairs whose largest "
+                                    "term is below 2^%d are skipped too, so every C(z) is within N 2^%d "
+                                    "(<= 2^-36 kappa) of the exact gating (parity: test_gate_floor_parity)"
+                                    % (F, F, F))
+            gated_floor["gate_floor"] = F
+            gated_floor["C_abs_bound"] = float(n0 + J) * 2.0 ** F
 
     # per-rank stage times (max / mean over ranks): passes, resampling, exchange incl. its
     # barrier, and the share of particles each rank updated (load balance)
@@ -505,18 +522,20 @@ def run_ours(args):
     value = pairs / (ms * 1e-3)
     value_e = pairs_e / (ms_e * 1e-3)
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    if gated is not None and gated["evaluated_pairs_per_step"] > 0:
+    for gl in (gated, gated_floor):
+        if gl is None or gl["evaluated_pairs_per_step"] <= 0:
+            continue
         # evaluated pairs per gated pass against the same EX2-bound pair roofline as the dense passes
-        evp = gated["evaluated_pairs_per_step"]
-        r1 = evp / (gated["kernel_ms"]["pass1"] * 1e-3)
-        r2 = evp / (gated["kernel_ms"]["pass2"] * 1e-3)
+        evp = gl["evaluated_pairs_per_step"]
+        r1 = evp / (gl["kernel_ms"]["pass1"] * 1e-3)
+        r2 = evp / (gl["kernel_ms"]["pass2"] * 1e-3)
         pk = roofline_pairs_per_s(m.meas, "pass1", n_sm, SM_MAX_MHZ)
-        gated["pass_roofline"] = {"unit": "Gpair/s (evaluated)", "peak": pk / 1e9,
-                                  "pass1": r1 / 1e9, "pass1_frac": r1 / pk,
-                                  "pass2": r2 / 1e9, "pass2_frac_of_ex2_bound": r2 / pk,
-                                  "basis": "1 MUFU.EX2 per evaluated pair per pass, 16/clk/SM x %d SMs x %.0f MHz; "
-                                           "pass 2 also carries the state sums of the index set"
-                                           % (n_sm, SM_MAX_MHZ)}
+        gl["pass_roofline"] = {"unit": "Gpair/s (evaluated)", "peak": pk / 1e9,
+                               "pass1": r1 / 1e9, "pass1_frac": r1 / pk,
+                               "pass2": r2 / 1e9, "pass2_frac_of_ex2_bound": r2 / pk,
+                               "basis": "1 MUFU.EX2 per evaluated pair per pass, 16/clk/SM x %d SMs x %.0f MHz; "
+                                        "pass 2 also carries the state sums of the index set"
+                                        % (n_sm, SM_MAX_MHZ)}
     mhz = (clk or {}).get("sm_mhz") or SM_MAX_MHZ
     p2 = statistics.mean(pass_ms["pass2"])
     p1 = statistics.mean(pass_ms["pass1"])
@@ -632,6 +651,7 @@ def run_ours(args):
                           "note": "Table 1 (PAPER.md:497-513), context only: not this metric or workload"},
         "hbm_kernels": hbm,
         "gated": gated,
+        "gated_floor": gated_floor,
         "per_rank": per_rank,
         "graph_steps": graph_info,
         "near_ties": near,

@@ -116,7 +116,16 @@ typedef struct {
                                     gamma N(x; birth_mean, Q) / (J p_k(x|Z_{k-1})), p_k the
                                     stratified proposal mixture; needs
                                     birth_sigma_v > 0 and birth_std > 0 */
-  int32_t reserved1;          /* must be 0 */
+  int32_t gate_floor;         /* gated update only.  0: exact gating -- a (tile, measurement) pair
+                                 is skipped only when every term of it underflows to exactly 0
+                                 in the dense kernels (largest possible exponent < -130).
+                                 F in [-126, -20]: a pair is skipped when its largest possible
+                                 term p_D g w is below 2^F; each C(z) then differs from the dense
+                                 one by less than N_global 2^F (absolute; the weights and sums by
+                                 correspondingly less), which the caller sizes against its
+                                 tolerance (DESIGN.md §5 "Gated update": bench's floor
+                                 log2(kappa) - 60 keeps every C within 2^-36 kappa at N <= 2^24).
+                                 Other values: PHD_EINVAL. */
   double birth_mean[4];       /* x-bar (x, vx, y, vy) of birth_model 1 */
   double birth_std[4];        /* sqrt(diag Q) of birth_model 1, >= 0 */
   int32_t stphd_all;          /* 0: pass 2 accumulates the STPHD state sums S_l only for the

@@ -35,7 +35,7 @@ class Params(ctypes.Structure):
                 ("fixed_count", ctypes.c_int64), ("count_mode", ctypes.c_int32), ("max_meas", ctypes.c_int32),
                 ("capacity", ctypes.c_int64), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32),
                 ("reserved0", ctypes.c_int32), ("exchange_count", ctypes.c_int64), ("birth_model", ctypes.c_int32),
-                ("reserved1", ctypes.c_int32), ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4),
+                ("gate_floor", ctypes.c_int32), ("birth_mean", ctypes.c_double * 4), ("birth_std", ctypes.c_double * 4),
                 ("stphd_all", ctypes.c_int32), ("gate", ctypes.c_int32), ("proposal_scale", ctypes.c_double)]
 
 
@@ -196,7 +196,7 @@ def params_from(model):
     p.reserved0 = 0
     p.exchange_count = int(getattr(model, "exchange_count", 0))
     p.birth_model = int(getattr(model, "birth_model", 0))
-    p.reserved1 = 0
+    p.gate_floor = int(getattr(model, "gate_floor", 0))
     for i in range(4):
         p.birth_mean[i] = float(getattr(model, "birth_mean", (0.0, 0.0, 0.0, 0.0))[i])
         p.birth_std[i] = float(getattr(model, "birth_std", (0.0, 0.0, 0.0, 0.0))[i])

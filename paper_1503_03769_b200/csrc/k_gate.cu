@@ -560,7 +560,7 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
     e1 = fmaxf(e1, __shfl_xor_sync(0xffffffffu, e1, o));
     lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
   }
-  const float budget = lm - kGateLog2Min;  // e_max >= -130  <=>  alpha0 dx^2 + alpha1 dy^2 <= budget
+  const float budget = lm - g.floor;  // e_max >= floor  <=>  alpha0 dx^2 + alpha1 dy^2 <= budget
   int total = 0;
   if (!(budget > 0.0f && isfinite(b0) && isfinite(e0) && isfinite(b1) && isfinite(e1))) return 0;
   const float R0 = sqrtf(budget / -na0) * 1.0001f + 1e-3f;
@@ -600,7 +600,7 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
   auto passes = [&](float2 zz) {
     const float dx = dist_iv(zz.x, b0, b1);
     const float dy = g.wrap1 ? dist_arc(zz.y, e0, e1) : dist_iv(zz.y, e0, e1);
-    return fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm)) >= kGateLog2Min;
+    return fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm)) >= g.floor;
   };
   constexpr int kStash = 4;
   int j0n, j1n;

@@ -349,7 +349,8 @@ phd_status validate(const phd_params* p, int world, phd_ctx* c) {
       return fail(c, PHD_EINVAL, "birth_model 2 needs a range region with rmin >= 0");
   }
   if (!(p->proposal_scale >= 0 && p->proposal_scale <= 1e3)) return fail(c, PHD_EINVAL, "proposal_scale outside [0, 1e3]");
-  if (p->reserved1 != 0) return fail(c, PHD_EINVAL, "reserved fields must be 0");
+  if (p->gate_floor != 0 && (p->gate_floor < -126 || p->gate_floor > -20))
+    return fail(c, PHD_EINVAL, "gate_floor %d: 0 (exact) or in [-126, -20]", p->gate_floor);
   if (p->gate < 0 || p->gate > 2) return fail(c, PHD_EINVAL, "gate must be 0, 1 or 2");
   if (p->stphd_all != 0 && p->stphd_all != 1) return fail(c, PHD_EINVAL, "stphd_all must be 0 or 1");
   for (int i = 0; i < 4; ++i)
@@ -604,12 +605,14 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
       c->ggrid.lo1 = (float)-kPi;
       c->ggrid.inv_h1 = (float)(kGateG / (2.0 * kPi));
       c->ggrid.wrap1 = 1;
+      c->ggrid.floor = p->gate_floor != 0 ? (float)p->gate_floor : kGateLog2Min;
     } else {
       c->ggrid.lo0 = (float)p->region[0];
       c->ggrid.inv_h0 = (float)(kGateG / (p->region[1] - p->region[0]));
       c->ggrid.lo1 = (float)p->region[2];
       c->ggrid.inv_h1 = (float)(kGateG / (p->region[3] - p->region[2]));
       c->ggrid.wrap1 = 0;
+      c->ggrid.floor = p->gate_floor != 0 ? (float)p->gate_floor : kGateLog2Min;
     }
   }
   CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (48 + 4 * world)));

@@ -473,6 +473,7 @@ struct GateGrid {
   float lo0, lo1;                     // grid origin (x, y) or (r, -pi)
   float inv_h0, inv_h1;               // cells per unit
   int wrap1;                          // axis 1 is an angle (range-bearing): cells wrap mod kGateG
+  float floor;                        // log2 of the skipped terms' bound: kGateLog2Min (exact) or gate_floor
 };
 
 // Sorted copy of the particle block (n_pad = ntiles * kGateTP records of n4 float4):

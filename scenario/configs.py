@@ -46,6 +46,7 @@ class Model:
     stphd_all: int = 0             # 1: STPHD state sums for every measurement (not only the index set)
     proposal_scale: float = 1.0    # Eq 5 proposal: CV transition with noise std s sigma_a (1: prior)
     gate: int = 0                  # update: 0 dense, 1 gated (auto fallback), 2 gated when it fits
+    gate_floor: int = 0            # gated: 0 exact (skip only exact zeros), else skip terms < 2^gate_floor
 
 
 @dataclass(frozen=True)

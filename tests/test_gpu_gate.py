@@ -74,6 +74,42 @@ def test_gated_equals_dense(phd, orc, mname, stphd_all):
     assert g["summ"]["LT"] == d["summ"]["LT"]
 
 
+def _floor_for(orc, m, N):
+    """The bench's gate_floor: log2(kappa) - 60, so N 2^F <= 2^-36 kappa for N <= 2^24."""
+    return int(math.floor(math.log2(orc.kappa(m)))) - 60
+
+
+@pytest.mark.parametrize("mname", ["position", "range_bearing", "aniso"])
+@pytest.mark.parametrize("n,M", [(20011, 600), (9000, 1100), (64 * 150 + 5, 130)])
+def test_gate_floor_parity(phd, orc, mname, n, M):
+    """gate_floor F: pairs whose largest possible term is below 2^F are skipped.  Against the
+    oracle with the dense tolerances, and against the exact gating within the stated bound:
+    every C(z) within N 2^F (absolute) of the exact one, the weights within that relative
+    effect; fewer pairs evaluated."""
+    base = replace(MODELS[mname], gate=2)
+    F = _floor_for(orc, base, n)
+    m = replace(base, gate_floor=F)
+    z = _meas(m, M, n + M + 1)
+    soa, w = _cloud(m, n, z, n + M + 1)
+    g = _run(phd, m, soa, w, z)
+    e = _run(phd, base, soa, w, z)
+    assert g["gate"]["used"] == 1 and g["gate"]["pairs"] <= e["gate"]["pairs"]
+    Co = orc.normalizers(m, soa, w, z)
+    wo, acco = orc.update(m, soa, w, z, Co)
+    _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
+    assert np.all(np.abs(g["C"] - e["C"]) <= n * 2.0 ** F + 2e-6 * e["C"])
+    kap = orc.kappa(m)
+    # a skipped pair moved w' by < 2^F / kappa (its term over D >= kappa), M of them at most
+    assert np.all(np.abs(g["wn"] - e["wn"]) <= 2e-6 * e["wn"] + M * 2.0 ** F / kap)
+    assert list(g["est"]["labels"]) == list(e["est"]["labels"])
+
+
+def test_gate_floor_validation(phd):
+    for bad in (-10, -127, 5):
+        with pytest.raises(phd.PhdError, match="PHD_EINVAL"):
+            phd.Filter(replace(MODELS["position"], gate=1, gate_floor=bad))
+
+
 def test_gated_degenerate_inputs(phd, orc):
     """Ragged and degenerate tiles: one particle, zero-weight tiles, a point cloud
     (every pair a candidate), M = 1, M = 0 (no candidates), measurements outside
