@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gate", type=int, default=0, choices=[0, 1, 2],
                     help="update algorithm of the main line: 0 dense (the pairs/s roofline line), 1/2 gated")
+    ap.add_argument("--gate-floor", type=int, default=0,
+                    help="gate_floor of the main line's gated update (0: exact gating; DESIGN.md §5)")
     ap.add_argument("--no-gated-leg", action="store_true",
                     help="skip the extra gated-update measurement reported under \"gated\"")
     ap.add_argument("--cpu-sample", type=int, default=65536, help="particles in the oracle's bounded sample")
@@ -278,7 +280,8 @@ def run_ours(args):
     steps = args.warmup + args.steps
     cfg = scenario_for(args.config, 2 * steps + 1)
     from dataclasses import replace as _replace
-    cfg = _replace(cfg, model=_replace(cfg.model, mode=1 if args.mode == "dcp" else 0, gate=args.gate))
+    cfg = _replace(cfg, model=_replace(cfg.model, mode=1 if args.mode == "dcp" else 0, gate=args.gate,
+                                           gate_floor=args.gate_floor))
     m = cfg.model
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)

@@ -402,7 +402,7 @@ __device__ __forceinline__ void st_v8(float4* dst, float4 a, float4 b) {
 template <int MODEL>
 __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int32_t* __restrict__ keys, int64_t n,
                                                        int64_t per_blk, int nblk, const int32_t* __restrict__ hs,
-                                                       float wscale, GateSorted so) {
+                                                       float wscale, GateSorted so, double* blk_wp) {
   pdl_wait();
   constexpr bool RB = MODEL == kRangeBearing;
   constexpr int N4 = RB ? 4 : 2;
@@ -445,9 +445,11 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   // 3. rank and write the records (and the max of lw, for the tile kernels' fast path)
   const unsigned lt = (1u << lane) - 1u;
   float lwm = -INFINITY;
+  double wsum = 0.0;  // predicted w of this lane's items (W_pred block sum below)
   bool nanp = false;  // clamped duplicates of the last item repeat a real item: no false flag
   for (int64_t b0 = w0; b0 < w1; b0 += 32 * ROWS) {
     float4 q[ROWS][N4];
+    float wr[ROWS];
     int kr[ROWS];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
@@ -458,7 +460,8 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
         q[r][1] = make_float4(__ldg(src.c[4] + i), __ldg(src.c[5] + i), __ldg(src.c[6] + i), __ldg(src.c[7] + i));
       }
       q[r][N4 - 2] = make_float4(__ldg(src.x + i), __ldg(src.y + i), __ldg(src.vx + i), __ldg(src.vy + i));
-      q[r][N4 - 1] = make_float4(log2f(__ldg(src.w + i) * wscale), 0.0f, 0.0f, 0.0f);  // the dense records' expression (k_records)
+      wr[r] = __ldg(src.w + i);
+      q[r][N4 - 1] = make_float4(log2f(wr[r] * wscale), 0.0f, 0.0f, 0.0f);  // the dense records' expression (k_records)
       lwm = fmaxf(lwm, q[r][N4 - 1].x);  // clamped duplicates of the last item do not change the max
       // a NaN particle makes every dense term NaN (C, D non-finite -> PHD_EMODEL); the
       // gated path might not evaluate it, so it is flagged here (one atomic per warp at the end)
@@ -469,6 +472,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
     for (int r = 0; r < ROWS; ++r) {
       const int64_t i = b0 + r * 32 + lane;
       const bool ok = i < w1;
+      if (ok) wsum += (double)wr[r];  // this lane's items in order
       const int d = ok ? kr[r] : 0;
       // the one-digit fast path pays for clustered cells (position sensor: 0.322 -> 0.295 ms at
       // cfg 5); range-bearing rows in (r, theta) cells are less uniform (cfg 4: +2 %)
@@ -491,6 +495,18 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   for (int o = 16; o > 0; o >>= 1) lwm = fmaxf(lwm, __shfl_xor_sync(0xffffffffu, lwm, o));
   if (lane == 0 && w0 < w1) atomicMax(so.lw_max, f2ord(lwm));
   if (__any_sync(0xffffffffu, nanp) && lane == 0) atomicAdd(so.bad, 1);
+  if (blk_wp != nullptr) {  // fixed order: lanes' sums by xor tree, the warps in order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    __shared__ double wpart[kMsWarps];
+    if (lane == 0) wpart[warp] = wsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < kMsWarps; ++k) t += wpart[k];
+      blk_wp[blockIdx.x] = t;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1102,7 +1118,9 @@ cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64
 
 cudaError_t gate_sort_particles(int model, const float* const* A, const float* rb, int64_t rb_stride, int64_t n,
                                 int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
-                                int32_t* keys, const GateSorted& so, cudaStream_t s, int64_t* launches) {
+                                int32_t* keys, const GateSorted& so, cudaStream_t s, int64_t* launches, double* blk_wp,
+                                int* nblk_out) {
+  *nblk_out = 0;
   const bool rbm = model == kRangeBearing;
   // always launched: it also resets the lw max
   pdl_launch(k_psort_pad, (unsigned)std::max<int64_t>(1, (n_pad - n + 255) / 256), 256, 0, s, n, n_pad, so);
@@ -1118,6 +1136,7 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
   src.w = A[4];
   const int64_t per_blk = sort_block(n);
   const int nblk = (int)((n + per_blk - 1) / per_blk);
+  *nblk_out = nblk;
   const size_t smem = sizeof(uint32_t) * (size_t)kMsWarps * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins;
   ensure_max_smem(k_psort_scatter<kRangeBearing>, smem);
   ensure_max_smem(k_psort_scatter<kPosIso>, smem);
@@ -1126,9 +1145,10 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
   cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
   if (rbm)
-    pdl_launch(k_psort_scatter<kRangeBearing>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so);
+    pdl_launch(k_psort_scatter<kRangeBearing>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so,
+               blk_wp);
   else
-    pdl_launch(k_psort_scatter<kPosIso>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so);
+    pdl_launch(k_psort_scatter<kPosIso>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so, blk_wp);
   ++*launches;
   return cudaGetLastError();
 }

@@ -243,6 +243,7 @@ struct phd_ctx {
   double *gpart1 = nullptr, *gA = nullptr;
   bool gated = false;            // the last update ran the gated path
   int64_t g_entries = 0, g_tiles = 0;
+  int g_nwb = 0;  // predicted-w block sums written by the particle sort (gated W_pred)
   // CUDA-graph steps (world 1, dense): phd_step replays a captured graph per launch shape
   bool capturing = false;                  // the step's calls are being stream-captured
   bool dev_scalars = false;                // one-sync step: resampling scalars on the device,
@@ -1093,7 +1094,7 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   c->gso.n = n;
   c->gso.bad = c->bad;
   CU(gate_sort_particles(c->model, A, c->rb, c->L.cap_l, n, npad, c->wscale, c->ggrid, c->ghist, c->gscan,
-                         c->gkeys, c->gso, c->st, &c->launches));
+                         c->gkeys, c->gso, c->st, &c->launches, c->blk_wp, &c->g_nwb));
   CU(gate_zbin(c->zlab, M, c->ggrid, c->ghist, c->gscan, c->gzstart, c->gzitems, c->gzz, c->st, &c->launches));
   int64_t tot = 0;
   if (ntiles > 0) {
@@ -1287,11 +1288,11 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
     timing_record(c, 3);
     if (ntiles > 0) KL(launch_gpass(1, ga, c->st));
     timing_record(c, 4);
-    KL(launch_block_sums(c->A[4], n, c->blk_wp, c->st));
+    // W_pred's block sums: written by the particle sort (c->g_nwb blocks of its own)
     const bool c_final = c->world == 1 || c->dcp;  // else the constants follow the C1 all-reduce
     const ZConstArgs zc{c->slot_label, c->kappa, c->s[4], c->C, c->D, c->bad};
     KL(launch_gate_reduce(1, c->gmstart, c->gmlist, M, c->gpart1, nullptr, nullptr, c->C_slot, c->slots_pad, c->st,
-                          c->blk_wp, (int)ceil_div(n, kBlockW), c->C_slot + c->slots_pad, c_final ? &zc : nullptr,
+                          c->blk_wp, c->g_nwb, c->C_slot + c->slots_pad, c_final ? &zc : nullptr,
                           c->bad));
     if (!c_final) {
       COMM(c->comm->allreduce_f64(c->C_slot, (size_t)c->slots_pad + 1, c->st));

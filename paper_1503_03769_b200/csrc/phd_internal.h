@@ -506,12 +506,14 @@ struct GateArgs {
   int M;                              // measurements (bounds checks of the debug build)
 };
 
-// key + stable counting sort of the local particles; writes the sorted copy.
+// key + stable counting sort of the local particles; writes the sorted copy, and the fp64
+// sums of the predicted w per sort block into blk_wp[0 .. *nblk_out) (fixed order: the
+// W_pred that rides with C in the C1 all-reduce; the gated update needs no k_block_sum).
 // Launch count added to *launches.
 cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/, const float* rb, int64_t rb_stride,
                                 int64_t n, int64_t n_pad, float wscale, const GateGrid& grid, int32_t* hist,
                                 int32_t* scan_tmp, int32_t* keys /*[n] scratch*/, const GateSorted& so, cudaStream_t s,
-                                int64_t* launches);
+                                int64_t* launches, double* blk_wp, int* nblk_out);
 // measurements -> grid cells (one CTA): zcell_start[kGateBins + 1], items stable by label
 cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
                       int32_t* zcell_start, int32_t* zcell_items, float2* zcell_z, cudaStream_t s, int64_t* launches);
