@@ -17,5 +17,14 @@ done
 python tools/dbg/timeline.py cfg2 > gpurun_out/tl_cfg2.txt 2>&1; echo tl=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --no-cpu-baseline --no-gated-leg > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_gate.csv python bench.py --gate 1 --no-gated-leg --no-cpu-baseline > gpurun_out/ncu_gate.log 2>&1; echo ncu2=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_gate_floor.csv python bench.py --gate 1 --gate-floor -71 --no-gated-leg --no-cpu-baseline > gpurun_out/ncu_gate_floor.log 2>&1; echo ncu3=$?
 CFGS="cfg5 cfg4" bash tools/gpu_ncu_passes.sh
 bash tools/gpu_ncu_hbm.sh
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_gpass --launch-skip 4 -c 2 -f -o gpurun_out/gpass_full python bench.py --gate 1 --no-gated-leg --no-cpu-baseline --steps 1 --warmup 3 > gpurun_out/ncu_gpass.log 2>&1; echo ncu_gpass=$?
+# summarise the ncu reports on the box (the .ncu-rep files exceed gpurun's 64 MiB pull limit)
+python tools/ncu_summary.py full gpurun_out/pass_full_cfg5.ncu-rep gpurun_out/sum_passes_cfg5.json "ncu --set full --clock-control none, bench.py --config cfg5 --steps 1 --warmup 3: k_pass 1 and 2 of the 4th step" > /dev/null
+python tools/ncu_summary.py full gpurun_out/pass_full_cfg4.ncu-rep gpurun_out/sum_passes_cfg4.json "ncu --set full --clock-control none, bench.py --config cfg4 --steps 1 --warmup 3: k_pass 1 and 2 of the 4th step" > /dev/null
+python tools/ncu_summary.py full gpurun_out/hbm_full.ncu-rep gpurun_out/sum_hbm.json "ncu --set full --clock-control none, bench.py (cfg5) --steps 1 --warmup 3: k_predict, k_records, k_scan_chunks, k_resample_gather" > /dev/null
+python tools/ncu_summary.py full gpurun_out/gpass_full.ncu-rep gpurun_out/sum_gpass.json "ncu --set full --clock-control none, bench.py --gate 1 (cfg5) --steps 1 --warmup 3: k_gpass 1 and 2" > /dev/null
+rm -f gpurun_out/*.ncu-rep
+du -sh gpurun_out
