@@ -405,6 +405,11 @@ static cudaError_t launch_z(int model, int pass, const PassArgs& a, int gp, int 
 
 bool pass2_sums_scaled() { return kFoldD; }
 
+#ifndef PHD_REC_THREADS
+#define PHD_REC_THREADS 1024
+#endif
+constexpr int kRecThreads = PHD_REC_THREADS;  // >= 256 (the block sums' threads)
+
 // Per-particle records of the dense passes (GRec), once per update: HBM-bound, 20 B read
 // and 32 B written per particle (range-bearing: 52 B read, 64 B written).  One float4 of
 // the record per thread, so that a warp's stores are contiguous.  Slots [n, n_pad) get
@@ -412,7 +417,8 @@ bool pass2_sums_scaled() { return kFoldD; }
 // [b kBlockW, (b + 1) kBlockW) and, with blk != nullptr, also writes their fp64 weight sum
 // blk[b] in k_block_sum's order (one launch fewer; the same bits).
 template <int MODEL>
-__global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad, double* blk, const BuildSlotsArgs bs) {
+__global__ void __launch_bounds__(kRecThreads) k_records(const PassArgs a, int64_t n_pad, double* blk,
+                                                         const BuildSlotsArgs bs) {
   pdl_wait();
   if (bs.slot_label != nullptr && blockIdx.x == gridDim.x - 1) {  // the slot layout's block
     build_slots_body(bs);
@@ -447,18 +453,20 @@ __global__ void __launch_bounds__(256) k_records(const PassArgs a, int64_t n_pad
     }
     out[f] = v;
   }
-  if (blk != nullptr && base < a.n) {  // block-uniform
+  if (blk != nullptr && base < a.n) {  // block-uniform; the first 256 threads, k_block_sum's order
     __shared__ double sw[8];
     const int tid = threadIdx.x;
     double s = 0.0;
+    if (tid < 256) {
 #pragma unroll
-    for (int r = 0; r < kBlockW / 256; ++r) {
-      const int64_t i = base + r * 256 + tid;
-      if (i < a.n) s += (double)a.w[i];
+      for (int r = 0; r < kBlockW / 256; ++r) {
+        const int64_t i = base + r * 256 + tid;
+        if (i < a.n) s += (double)a.w[i];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((tid & 31) == 0) sw[tid >> 5] = s;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((tid & 31) == 0) sw[tid >> 5] = s;
     __syncthreads();
     if (tid == 0) {
       double x = 0.0;
@@ -477,9 +485,9 @@ cudaError_t launch_records(int model, const PassArgs& a, cudaStream_t s, double*
   const BuildSlotsArgs b = bs ? *bs : BuildSlotsArgs{};
   const unsigned grid = (unsigned)((std::max<int64_t>(n_pad, 0) + kBlockW - 1) / kBlockW) + (bs ? 1u : 0u);
   if (model == kRangeBearing)
-    pdl_launch(k_records<kRangeBearing>, grid, 256, 0, s, a, n_pad, blk, b);
+    pdl_launch(k_records<kRangeBearing>, grid, kRecThreads, 0, s, a, n_pad, blk, b);
   else
-    pdl_launch(k_records<kPosIso>, grid, 256, 0, s, a, n_pad, blk, b);
+    pdl_launch(k_records<kPosIso>, grid, kRecThreads, 0, s, a, n_pad, blk, b);
   return cudaGetLastError();
 }
 
