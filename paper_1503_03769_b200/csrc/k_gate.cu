@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   constexpr bool RB = MODEL == kRangeBearing;
   constexpr int N4 = RB ? 4 : 2;
   constexpr int ROWS = RB ? 2 : 4;
-  constexpr int nbins = kGateBins, nw = kGateBins / 2;
+  constexpr int nw = kGateBins / 2;
   extern __shared__ uint32_t sm[];
   uint32_t* wh = sm;
   int* base = reinterpret_cast<int*>(sm + kMsWarps * nw);
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
       __syncwarp();
       if (ok) {
         if (lane == __ffs(peers) - 1) atomicAdd(&my[d >> 1], (uint32_t)__popc(peers) << (16 * (d & 1)));
-        PHD_DCHECK(pos >= 0 && pos < n && d >= 0 && d < nbins);
+        PHD_DCHECK(pos >= 0 && pos < n && d >= 0 && d < kGateBins);
         float4* dst = so.rec + (int64_t)pos * N4;
 #pragma unroll
         for (int k = 0; k < N4; k += 2) st_v8(dst + k, q[r][k], q[r][k + 1]);
