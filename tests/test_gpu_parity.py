@@ -628,3 +628,47 @@ def test_range_bearing_seam_exact_pi(phd, orc):
     f, z, soa, w, C, acc, wn, est, summ, Co, wo, acco = _update_case(phd, orc, m, 6000, len(z), 2, z=z)
     _check_update(orc, m, C, acc, wn, w, Co, wo, acco)
     f.close()
+
+
+@pytest.mark.parametrize("gate", [0, 2])
+def test_max_size_2pow26(phd, orc, gate, near_tie_report):
+    """4x cfg 5 (2^26 particles, M = 4096: 2.7e11 pairs per pass, > 2^32 pair and byte
+    offsets): the 64-bit indexing of every stage at a size beyond the BASELINE configs,
+    dense and gated -- sampled normalisers and weights against the oracle, the mass
+    identity, and every ancestor of the 67 M offspring."""
+    base = scenario.get("cfg5")
+    J = base.model.births_per_step
+    m = replace(base.model, fixed_count=(1 << 26) - J, capacity=1 << 26, gate=gate)
+    cfg = replace(base, model=m, scenario=replace(base.scenario, steps=2))
+    truth = scenario.simulate_truth(cfg)
+    Z = scenario.measurements(cfg, truth)
+    f = phd.Filter(m)
+    f.init_population(**scenario.init_args(cfg, truth))
+    f.predict(1)
+    ps, pw, _ = f.get_particles()
+    N = ps.shape[1]
+    assert N == 1 << 26
+    f.update(Z[0])
+    M = len(Z[0])
+    C = f.normalizers(M)
+    _, wn, _ = f.get_particles()
+    est, summ = f.extract()
+    if gate:
+        assert f.gate_stats()["used"] == 1
+    kap = orc.kappa(m)
+    rng = np.random.default_rng(3)
+    for p in rng.choice(M, 2, replace=False):
+        Co = orc.normalizers(m, ps, pw, Z[0][p:p + 1])[0]
+        assert abs(C[p] - Co) <= 1e-5 * Co + 1e-9 * kap
+    idx = np.concatenate([rng.choice(N, 64, replace=False), np.argsort(wn)[-64:], np.arange(N - 64, N)])
+    wo, _ = orc.update(m, ps[:, idx], pw[idx], Z[0], C)
+    assert np.all(np.abs(wn[idx] - wo) <= 1e-4 * wo + 1e-7 * pw[idx])
+    rhs = (1 - m.p_d) * summ["W_pred"] + math.fsum(C / (kap + C))
+    assert abs(summ["W"] - rhs) <= 1e-5 * rhs
+    del ps
+    f.resample_exchange(1)
+    anc, _ = f.ancestors()
+    meta = f.resample_meta()
+    assert len(anc) == m.fixed_count and np.all(np.diff(anc) >= 0)
+    check_ancestors(orc, anc, wn, meta["U"], meta["N_out"], near_tie_report, n=N, gate=gate)
+    f.close()
