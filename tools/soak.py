@@ -1,5 +1,6 @@
-"""Soak run: many full steps of every config through the public API, dense and
-gated, checking status, finite masses and the mass identity each step.
+"""Soak run: many full steps of every config through the public API (t = 0 population on
+the device), dense, gated and gated with a gate_floor, checking status and finite masses
+each step.
 
     python tools/soak.py [--steps 100]
 """
@@ -23,14 +24,16 @@ def main():
     import scenario
     for cname in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
         cfg = scenario.get(cname)
-        steps = min(args.steps, 100 if cname in ("cfg1", "cfg2") else 30)
+        steps = min(args.steps, args.steps if cname in ("cfg1", "cfg2", "cfg3") else max(10, args.steps // 4))
         cfg = replace(cfg, scenario=replace(cfg.scenario, steps=max(cfg.scenario.steps, steps)))
         truth = scenario.simulate_truth(cfg)
         Z = scenario.measurements(cfg, truth)
-        soa, w = scenario.initial_population(cfg, truth)
-        for gate in (0, 2):
-            f = phd.Filter(replace(cfg.model, gate=gate))
-            f.set_particles(soa, w, soa.shape[1])
+        ia = scenario.init_args(cfg, truth)
+        V = (cfg.model.region[1] - cfg.model.region[0]) * (cfg.model.region[3] - cfg.model.region[2])
+        F = max(-126, min(-20, int(math.floor(math.log2(cfg.model.clutter_rate / V))) - 60))
+        for gate, floor in ((0, 0), (2, 0), (2, F)):
+            f = phd.Filter(replace(cfg.model, gate=gate, gate_floor=floor))
+            f.init_population(**ia)
             t0 = time.perf_counter()
             gated = 0
             lts = []
@@ -41,8 +44,8 @@ def main():
                 lts.append(s["LT"])
             dt = time.perf_counter() - t0
             f.close()
-            print("%s gate=%d steps=%d gated=%d wall %.2f s  LT last 5 %s" % (cname, gate, steps, gated, dt, lts[-5:]),
-                  flush=True)
+            print("%s gate=%d floor=%d steps=%d gated=%d wall %.2f s  LT last 5 %s"
+                  % (cname, gate, floor, steps, gated, dt, lts[-5:]), flush=True)
     print("soak done")
 
 
