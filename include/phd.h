@@ -138,9 +138,10 @@ typedef struct {
                                     cell (a sorted copy; the filter's particle order and hence
                                     resampling are unchanged), tiles of 512 paired only with the
                                     measurements whose largest possible exponent over the tile is
-                                    >= -130, i.e. every skipped term underflows to exactly 0 in
-                                    the dense kernels (same non-zero terms, fp64 sums in another
-                                    fixed order).  Runs dense for an update whose candidate
+                                    >= -130, i.e. every skipped pass-1 term underflows to exactly
+                                    0 in the dense kernels (same non-zero terms, fp64 sums in
+                                    another fixed order); a skipped pass-2 term u/(kappa + C) is
+                                    below 2^-130/kappa, far below fp32 resolution of any weight.  Runs dense for an update whose candidate
                                     pairs exceed half of N x M or the workspace, or with
                                     N x M < 2^29 in exact mode (the sort would dominate);
                                  2: gated whenever the candidate lists fit the workspace. */
