@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
   __shared__ int zr[kGateChunk + 2];         // bearing representation   (range-bearing)
   __shared__ float2 zc[kGateChunk + 2];      // -(Cartesian centre)      (range-bearing, pass 2)
   __shared__ int zi[kGateChunk + 2];         // chunk-local entry index  (pass 2: selected first)
-  __shared__ int wcnt[WARPS + 1];
+  __shared__ unsigned gmask[kGateChunk / 32];  // pass 2: "in I" ballot per 32 candidates
   __shared__ float wpart[PASS == 1 ? WARPS : 1][PASS == 1 ? kGateChunk : 1];   // pass 1: per-warp sums
   __shared__ float4 wq[PASS == 2 ? WARPS : 1][PASS == 2 ? kGateChunk + 2 : 1];     // pass 2: per-warp state sums
 
@@ -832,90 +832,50 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
         }
       }
     } else {
-      // stable partition: labels in I first (their state sums are reduced), then the rest
-      int base_sel = 0;
-      for (int k0 = 0; k0 < cl; k0 += THREADS) {
-        const int k = k0 + tid;
-        int l = -1, fl = 0;
-        if (k < cl) {
-          l = g.cand[e0 + cb + k];
-          fl = g.sel == nullptr ? 1 : (g.sel[l] != 0);
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, fl);
-        if (lane == 0) wcnt[warp] = __popc(bal);
-        __syncthreads();
-        if (tid == 0) {
-          int sacc = 0;
-          for (int w = 0; w < WARPS; ++w) {
-            const int c = wcnt[w];
-            wcnt[w] = sacc;
-            sacc += c;
-          }
-          wcnt[WARPS] = sacc;
-        }
-        __syncthreads();
-        if (k < cl && fl) {
-          const int pos = base_sel + wcnt[warp] + __popc(bal & ((1u << lane) - 1u));
-          PHD_DCHECK(pos < kGateChunk + 2);
-          zi[pos] = k;
-        }
-        base_sel += wcnt[WARPS];
-        __syncthreads();
-      }
-      nsel = base_sel;
-      base_sel_unpadded = base_sel;
-      // an odd selected count is padded with one sentinel candidate (every term
-      // exactly 0, zi = -1: never written), so the selected loop runs in pairs
-      const int nsel2 = (nsel + 1) & ~1;
-      if (tid == 0 && nsel2 > nsel) zi[nsel] = -1;
-      // second sweep: the unselected after the selected, in order
-      int base_un = nsel2;
-      for (int k0 = 0; k0 < cl; k0 += THREADS) {
-        const int k = k0 + tid;
+      // stable partition: labels in I first (their state sums are reduced), then the
+      // rest.  One sweep of ballots (candidate k = tid + THREADS i lies in 32-group
+      // k >> 5, owned by one warp), one barrier, then every candidate's position from the
+      // group masks: selected ones at their rank among the selected, the others after
+      // the (pair-padded) selected block at their rank among the unselected.
+      for (int k = tid; k < ((cl + 31) & ~31); k += THREADS) {
         int fl = 0;
         if (k < cl) {
           const int l = g.cand[e0 + cb + k];
-          fl = (g.sel == nullptr ? 1 : (g.sel[l] != 0)) ? 0 : 1;
+          fl = g.sel == nullptr ? 1 : (g.sel[l] != 0);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, fl);
-        if (lane == 0) wcnt[warp] = __popc(bal);
-        __syncthreads();
-        if (tid == 0) {
-          int sacc = 0;
-          for (int w = 0; w < WARPS; ++w) {
-            const int c = wcnt[w];
-            wcnt[w] = sacc;
-            sacc += c;
-          }
-          wcnt[WARPS] = sacc;
-        }
-        __syncthreads();
-        if (k < cl && fl) {
-          PHD_DCHECK(base_un + wcnt[warp] + __popc(bal & ((1u << lane) - 1u)) < kGateChunk + 2);
-          zi[base_un + wcnt[warp] + __popc(bal & ((1u << lane) - 1u))] = k;
-        }
-        base_un += wcnt[WARPS];
-        __syncthreads();
+        if (lane == 0) gmask[k >> 5] = bal;
       }
-      for (int pos = tid; pos < cl + (nsel2 - nsel); pos += THREADS) {
-        const int ki = zi[pos];
-        if (ki < 0) {  // sentinel
-          zn[pos] = f2(-1e30f, -1e30f);
-          zd[pos] = FOLD ? INFINITY : 0.0f;
-          if (RB) {
-            zr[pos] = 0;
-            zc[pos] = f2(0.0f, 0.0f);
-          }
-          continue;
-        }
-        PHD_DCHECK(pos < kGateChunk + 2 && ki < cl && e0 + cb + ki < g.E);
-        const int l = g.cand[e0 + cb + ki];
+      __syncthreads();
+      const int ng = (cl + 31) >> 5;
+      for (int q = 0; q < ng; ++q) nsel += __popc(gmask[q]);
+      base_sel_unpadded = nsel;
+      const int nsel2 = (nsel + 1) & ~1;
+      for (int k = tid; k < cl; k += THREADS) {
+        const int grp = k >> 5;
+        const unsigned m = gmask[grp];
+        int before = __popc(m & ((1u << (k & 31)) - 1u));
+        for (int q = 0; q < grp; ++q) before += __popc(gmask[q]);
+        const bool s = (m >> (k & 31)) & 1u;
+        const int pos = s ? before : nsel2 + (k - before);
+        PHD_DCHECK(pos < kGateChunk + 2);
+        const int l = g.cand[e0 + cb + k];
         PHD_DCHECK(l >= 0 && l < g.M);
+        zi[pos] = k;
         zn[pos] = f2(g.sc.s0[l], g.sc.s1[l]);
         zd[pos] = FOLD ? log2f(g.sc.d[l]) / g.na0 : g.sc.d[l];  // fold: d = 0 -> +inf
         if (RB) {
           zr[pos] = g.sc.rep[l];
           zc[pos] = f2(g.sc.s2[l], g.sc.s3[l]);
+        }
+      }
+      if (tid == 0 && nsel2 > nsel) {  // sentinel: every term exactly 0, zi = -1 (never written)
+        zi[nsel] = -1;
+        zn[nsel] = f2(-1e30f, -1e30f);
+        zd[nsel] = FOLD ? INFINITY : 0.0f;
+        if (RB) {
+          zr[nsel] = 0;
+          zc[nsel] = f2(0.0f, 0.0f);
         }
       }
       nsel = nsel2;
