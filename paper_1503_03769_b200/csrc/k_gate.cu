@@ -14,7 +14,7 @@
 //      (the filter's own particle order, which defines resampling, is untouched).
 //      NaN particles are counted here (the dense C would be NaN).
 //   2. gate_zbin: measurements binned into the same cells (the same counting sort).
-//   3. k_gate_count / k_gate_fill (tile_enum): per tile of kGateTP sorted particles,
+//   3. k_gate_count / k_gate_fill (tile_enum): per tile of gate_tp sorted particles,
 //      the bounding box and max log2(p_D c w); a measurement is a candidate of the
 //      tile iff
 //         e_max = -alpha0 dx^2 - alpha1 dy^2 + max_i log2(p_D c w_i) >= -130
@@ -526,6 +526,7 @@ struct RecView {
   int stride;
   int64_t n;             // particles (records [n, n_pad) are padding)
   const int* lw_max;     // ordered-int encoding of max lw over all particles (k_psort_scatter)
+  int tp;                // particles per tile (gate_tp)
 };
 
 
@@ -533,15 +534,16 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
                                          const int32_t* __restrict__ zcell_start, const int32_t* __restrict__ zcell_items,
                                          const float2* __restrict__ zcell_z, int32_t* dst, int cap) {
   const int lane = threadIdx.x & 31;
-  const int64_t p0 = (int64_t)t * kGateTP;
+  const int tp = rv.tp;
+  const int64_t p0 = (int64_t)t * tp;
   float b0 = INFINITY, b1 = -INFINITY, e0 = INFINITY, e1 = -INFINITY, lm = -INFINITY;
   // Fast path: a full tile whose first and last particles share an interior cell holds
   // only particles of that cell (the tiles are in cell-key order), so the cell's box
   // (a little widened against the fp32 rounding of the cell index) and the global
   // max of log2(p_D c w) bound the tile conservatively: never fewer candidates.
   bool fast = false;
-  if (p0 + kGateTP <= rv.n) {
-    const int64_t oa = p0 * rv.stride, ob = (p0 + kGateTP - 1) * rv.stride;
+  if (p0 + tp <= rv.n) {
+    const int64_t oa = p0 * rv.stride, ob = (p0 + tp - 1) * rv.stride;
     const int ax = cell_raw(__ldg(rv.c0 + oa), g.lo0, g.inv_h0), ay = cell_raw(__ldg(rv.c1 + oa), g.lo1, g.inv_h1);
     const int bx = cell_raw(__ldg(rv.c0 + ob), g.lo0, g.inv_h0), by = cell_raw(__ldg(rv.c1 + ob), g.lo1, g.inv_h1);
     if (ax == bx && ay == by && ax > 0 && ax < kGateG - 1 && ay > 0 && ay < kGateG - 1) {
@@ -554,7 +556,7 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
       lm = ord2f(__ldg(rv.lw_max));
     }
   }
-  for (int j = lane; j < (fast ? 0 : kGateTP); j += 32) {
+  for (int j = lane; j < (fast ? 0 : tp); j += 32) {
     const int64_t o = (p0 + j) * rv.stride;
     const float l = __ldg(rv.lw + o);
     const float v0 = __ldg(rv.c0 + o), v1 = __ldg(rv.c1 + o);
@@ -715,8 +717,8 @@ __global__ void k_zero_i32(int32_t* a, int64_t n) {
 }
 
 // ---------------------------------------------------------------------------
-// The gated passes.  Tile t = sorted particles [t*512, t*512 + 512); a CTA of
-// kGateTP / (2 NPAIR) threads, thread tid holds 2 NPAIR particles as NPAIR f32x2 pairs
+// The gated passes.  Tile t = sorted particles [t*TP, t*TP + TP); a CTA of
+// TP / (2 NPAIR) threads, thread tid holds 2 NPAIR particles as NPAIR f32x2 pairs
 // h = 0, 1: (tid + 256 h, tid + 128 + 256 h).  Per candidate the thread sums
 // its four terms before the cross-lane reduction.
 
@@ -727,12 +729,17 @@ struct GPair {
   float2 VX, VY;
 };
 
-template <int MODEL, int PASS, int NPAIR>
-__global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing && PASS == 2) ? 5 : 8)
+#ifndef PHD_GPASS2_MINB
+#define PHD_GPASS2_MINB 8
+#endif
+// (resident CTAs per SM scale with 512 / TP: the same threads per SM for both tile sizes)
+template <int MODEL, int PASS, int NPAIR, int TP = gate_tp(MODEL)>
+__global__ void __launch_bounds__(TP / (2 * NPAIR),
+                                  ((MODEL == kRangeBearing && PASS == 2) ? 5 : (PASS == 2 ? PHD_GPASS2_MINB : 8)) * 512 / TP)
     k_gpass(const GateArgs g) {
   pdl_wait();
   constexpr bool RB = MODEL == kRangeBearing;
-  constexpr int THREADS = kGateTP / (2 * NPAIR);  // particle pairs (tid + 2 THREADS h, + THREADS) per thread
+  constexpr int THREADS = TP / (2 * NPAIR);  // particle pairs (tid + 2 THREADS h, + THREADS) per thread
   constexpr int WARPS = THREADS / 32;
   // + 2: pass 2 pads an odd selected count with one sentinel candidate
   __shared__ float2 zn[kGateChunk + 2];      // (-z0, -z1)
@@ -751,7 +758,7 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
   constexpr int N4 = RB ? 4 : 2;
 #pragma unroll
   for (int h = 0; h < NPAIR; ++h) {
-    const int64_t pa = (int64_t)t * kGateTP + 2 * THREADS * h + tid, pb = pa + THREADS;
+    const int64_t pa = (int64_t)t * TP + 2 * THREADS * h + tid, pb = pa + THREADS;
     const float4* ra = g.so.rec + pa * N4;
     const float4* rbp = g.so.rec + pb * N4;
     P[h].LW = f2(__ldg(ra + N4 - 1).x, __ldg(rbp + N4 - 1).x);
@@ -983,8 +990,8 @@ __global__ void __launch_bounds__(kGateTP / (2 * NPAIR), (MODEL == kRangeBearing
   if (PASS == 2) {
 #pragma unroll
     for (int h = 0; h < NPAIR; ++h) {
-      const int64_t pa = (int64_t)t * kGateTP + 2 * THREADS * h + tid;
-      PHD_DCHECK(pa + THREADS < (int64_t)g.ntiles * kGateTP);
+      const int64_t pa = (int64_t)t * TP + 2 * THREADS * h + tid;
+      PHD_DCHECK(pa + THREADS < (int64_t)g.ntiles * TP);
       g.Ps[pa] = pacc[h].x;
       g.Ps[pa + THREADS] = pacc[h].y;
     }
@@ -1148,7 +1155,7 @@ cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, fl
   if (ntiles <= 0) return cudaSuccess;
   const bool rbm = model == kRangeBearing;
   const float* f = reinterpret_cast<const float*>(so.rec);
-  RecView rv{f, f + (rbm ? 2 : 1), f + 4 * (so.n4 - 1), 4 * so.n4, so.n, so.lw_max};
+  RecView rv{f, f + (rbm ? 2 : 1), f + 4 * (so.n4 - 1), 4 * so.n4, so.n, so.lw_max, gate_tp(model)};
   const unsigned blocks = (unsigned)((ntiles + 7) / 8);
   if (fill)
     pdl_launch(k_gate_fill, blocks, 256, 0, s, rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tstart, cbuf,
@@ -1197,9 +1204,9 @@ static cudaError_t gpass_m(int pass, const GateArgs& g, cudaStream_t s) {
   // 0.42 -> 0.44 ms, so pass 1 keeps 4)
   constexpr int NP2 = MODEL == kRangeBearing ? 2 : PHD_GATE_NPAIR_POS;
   if (pass == 1)
-    pdl_launch(k_gpass<MODEL, 1, 2>, g.ntiles, kGateTP / 4, 0, s, g);
+    pdl_launch(k_gpass<MODEL, 1, 2>, g.ntiles, gate_tp(MODEL) / 4, 0, s, g);
   else
-    pdl_launch(k_gpass<MODEL, 2, NP2>, g.ntiles, kGateTP / (2 * NP2), 0, s, g);
+    pdl_launch(k_gpass<MODEL, 2, NP2>, g.ntiles, gate_tp(MODEL) / (2 * NP2), 0, s, g);
   return cudaGetLastError();
 }
 

@@ -121,7 +121,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   // gated update buffers (DESIGN.md §5 "Gated update"); 256-byte stubs when gate == 0
   const bool gt = p->gate != 0;
   L.g_npad = align_up((size_t)L.cap_l, kGateTP);
-  L.g_ntiles = (int)(L.g_npad / kGateTP);
+  L.g_ntiles = (int)(L.g_npad / kGateTPMin);  // the most tiles of either tile size
   L.g_ecap = std::max<int64_t>((int64_t)1 << 20, (int64_t)L.g_ntiles * std::min(p->max_meas, 256));
   L.g_hist = std::max<int64_t>((int64_t)kGateBins * sort_blocks_max(L.cap_l),
                                (int64_t)kSortMaxBins * sort_blocks_max(L.g_ecap)) + 1;
@@ -1088,8 +1088,9 @@ static void gate_slots(phd_ctx* c, int M) {
 // (collectively for world > 1: every rank must use the same slot layout).
 static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   *use = false;
-  const int64_t npad = ceil_div(n, kGateTP) * kGateTP;
-  const int ntiles = (int)(npad / kGateTP);
+  const int tp = gate_tp(c->model);
+  const int64_t npad = ceil_div(n, tp) * tp;
+  const int ntiles = (int)(npad / tp);
   const float* A[5] = {c->A[0], c->A[1], c->A[2], c->A[3], c->A[4]};
   c->gso.n = n;
   c->gso.bad = c->bad;
@@ -1110,7 +1111,7 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
   c->g_tiles = ntiles;
   const bool fits = tot <= c->L.g_ecap;
   // gate = 1 runs dense when the candidates are most of the pairs
-  const bool pays = (double)tot * kGateTP <= 0.5 * (double)n * (double)M;
+  const bool pays = (double)tot * tp <= 0.5 * (double)n * (double)M;
   double veto = (fits && (c->p.gate == 2 || pays)) ? 0.0 : 1.0;
   if (c->world > 1) {
     double* d = c->C_slot;  // scratch: rewritten by the update
@@ -2110,7 +2111,7 @@ phd_status phd_get_gate_stats(phd_ctx* c, int64_t* out) {
   if (!c || !out) return PHD_EINVAL;
   out[0] = c->gated ? 1 : 0;
   out[1] = c->g_entries;
-  out[2] = c->g_entries * kGateTP;
+  out[2] = c->g_entries * gate_tp(c->model);
   out[3] = c->g_tiles;
   return PHD_OK;
 }

@@ -419,7 +419,7 @@ cudaError_t launch_select_slots(const double* C_lab, const double* D_lab, int M,
 // ---- gated update (k_gate.cu, DESIGN.md §5 "Gated update") ------------------
 // Particles are ordered by a Morton cell key in measurement space (stable
 // counting sort; the filter's own particle order is untouched, the passes read
-// a sorted copy), cut into tiles of kGateTP, and every tile is paired only with
+// a sorted copy), cut into tiles of gate_tp(model), and every tile is paired only with
 // the measurements whose largest possible exponent over the tile's bounding box,
 //   e_max = -alpha0 dx^2 - alpha1 dy^2 + max_i log2(p_D c w_i),
 // is >= kGateLog2Min: every skipped pair has e < -130, so its fp32 term
@@ -465,7 +465,14 @@ inline int64_t sort_block(int64_t n) {
 // upper bound of the block count for n <= cap items (hist / scan buffers)
 inline int64_t sort_blocks_max(int64_t cap) { return (cap + sort_block(cap) - 1) / sort_block(cap) + kSortBlocks + 1; }
 constexpr int kSortMaxBins = 4096;    // bins per counting-sort pass (12-bit digits)
-constexpr int kGateTP = 512;          // particles per tile (256 threads x 2, f32x2)
+// particles per gated tile: 1024 for the position sensor (a cfg 5 tile lies inside one
+// 31 m cell either way, so half the tiles and entries for the same candidates), 512 for
+// range-bearing ((r, theta) tiles span more cells); kGateTP bounds both (allocation)
+#ifndef PHD_GATE_TP_POS
+#define PHD_GATE_TP_POS 1024
+#endif
+constexpr int kGateTP = 1024, kGateTPMin = 512;
+__host__ __device__ constexpr int gate_tp(int model) { return model == kRangeBearing ? 512 : PHD_GATE_TP_POS; }
 constexpr int kGateChunk = 256;       // candidates staged in shared memory at a time
 constexpr float kGateLog2Min = -130.0f;
 
@@ -476,7 +483,7 @@ struct GateGrid {
   float floor;                        // log2 of the skipped terms' bound: kGateLog2Min (exact) or gate_floor
 };
 
-// Sorted copy of the particle block (n_pad = ntiles * kGateTP records of n4 float4):
+// Sorted copy of the particle block (n_pad = ntiles * gate_tp records of n4 float4):
 //   position      (x, y, vx, vy), (lw, 0, 0, 0)
 //   range-bearing (r_hi, r_lo, thA hi, thA lo), (thB hi, thB lo, thC hi, thC lo), (x, y, vx, vy), (lw, 0, 0, 0)
 // with lw = log2(p_D c w) (-inf for w = 0 and padding).
