@@ -683,16 +683,20 @@ __global__ void __launch_bounds__(256) k_gate_fill(const RecView rv, int ntiles,
                                                    GateGrid g, const int32_t* __restrict__ zcell_start,
                                                    const int32_t* __restrict__ zcell_items,
                                                    const float2* __restrict__ zcell_z, const int32_t* __restrict__ tstart,
-                                                   const int32_t* __restrict__ cbuf, int32_t* cand) {
+                                                   const int32_t* __restrict__ cbuf, int32_t* cand, int64_t ecap) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
   const int e0 = tstart[t], K = tstart[t + 1] - e0;
+  // launched before the host has checked the total against the workspace: entries past
+  // ecap are not written (the update then runs dense and ignores cand)
+  const int64_t room = ecap - (int64_t)e0;
+  const int Kw = room <= 0 ? 0 : (room < (int64_t)K ? (int)room : K);
   if (K <= kGateKBuf) {
-    for (int j = lane; j < K; j += 32) cand[e0 + j] = cbuf[(int64_t)t * kGateKBuf + j];
-  } else {
-    tile_enum(t, rv, na0, na1, g, zcell_start, zcell_items, zcell_z, cand + e0, 0x7fffffff);
+    for (int j = lane; j < Kw; j += 32) cand[e0 + j] = cbuf[(int64_t)t * kGateKBuf + j];
+  } else if (Kw > 0) {
+    tile_enum(t, rv, na0, na1, g, zcell_start, zcell_items, zcell_z, cand + e0, Kw);
   }
 }
 
@@ -1151,7 +1155,7 @@ cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* hist
 
 cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1, const GateGrid& grid,
                        const int32_t* zcell_start, const int32_t* zcell_items, const float2* zcell_z, int32_t* tcount,
-                       const int32_t* tstart, int32_t* cbuf, int32_t* cand, cudaStream_t s) {
+                       const int32_t* tstart, int32_t* cbuf, int32_t* cand, cudaStream_t s, int64_t ecap) {
   if (ntiles <= 0) return cudaSuccess;
   const bool rbm = model == kRangeBearing;
   const float* f = reinterpret_cast<const float*>(so.rec);
@@ -1159,7 +1163,7 @@ cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, fl
   const unsigned blocks = (unsigned)((ntiles + 7) / 8);
   if (fill)
     pdl_launch(k_gate_fill, blocks, 256, 0, s, rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tstart, cbuf,
-                                       cand);
+               cand, ecap);
   else
     pdl_launch(k_gate_count, blocks, 256, 0, s, rv, ntiles, na0, na1, grid, zcell_start, zcell_items, zcell_z, tcount, cbuf);
   return cudaGetLastError();

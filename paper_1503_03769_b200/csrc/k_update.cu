@@ -24,6 +24,10 @@
 #include <algorithm>
 #include <type_traits>
 
+#ifndef PHD_FIN_STAGE
+#define PHD_FIN_STAGE 1
+#endif
+
 #ifndef PHD_PP_UNROLL1
 #define PHD_PP_UNROLL1 8
 #endif
@@ -605,8 +609,29 @@ __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, c
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * kBlockW;
   double a = 0.0, b = 0.0;
+  constexpr int R = kBlockW / 256;
+  if (PHD_FIN_STAGE && inv != nullptr && base + kBlockW <= n) {
+    // gated update, full block: the R index loads, then the R gathers of P through inv, in
+    // flight together (the gather is the latency chain of this kernel)
+    float wi[R], s[R];
+    int32_t j[R];
 #pragma unroll
-  for (int r = 0; r < kBlockW / 256; ++r) {
+    for (int r = 0; r < R; ++r) {
+      j[r] = inv[base + r * 256 + tid];
+      wi[r] = w[base + r * 256 + tid];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = zb > 0 ? P[j[r]] : 0.0f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float wn = wi[r] * nu + s[r];
+      w_out[base + r * 256 + tid] = wn;
+      a += (double)wn;
+      b += (double)wi[r];
+    }
+  } else {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
     int64_t i = base + r * 256 + tid;
     if (i < n) {
       float wi = w[i];
@@ -621,6 +646,7 @@ __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ w, c
       a += (double)wn;
       b += (double)wi;
     }
+  }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

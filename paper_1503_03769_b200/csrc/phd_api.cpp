@@ -250,6 +250,7 @@ struct phd_ctx {
                                            // extraction on st2 overlapping the resampling
   cudaStream_t st2 = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t ev_plan = nullptr;  // the gate plan's candidate total has reached the host
   bool graph_off = false;                  // disabled (PHD_GRAPH=0, or a capture failed)
   struct GraphEntry {
     int64_t key[8];
@@ -631,6 +632,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
   CUB(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
   CUB(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
   CUB(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+  CUB(cudaEventCreateWithFlags(&c->ev_plan, cudaEventDisableTiming));
   // derived model constants (fp32 for the pair kernels, fp64 for kappa)
   double s0 = p->sigma_z[0], s1 = p->sigma_z[1];
   bool rbm = p->meas == PHD_MEAS_RANGE_BEARING;
@@ -708,6 +710,7 @@ void phd_destroy(phd_ctx* c) {
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
+  if (c->ev_plan) cudaEventDestroy(c->ev_plan);
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->h_meta) cudaFreeHost(c->h_meta);
@@ -1104,7 +1107,12 @@ static phd_status gate_plan(phd_ctx* c, int M, int64_t n, bool* use) {
     CU(gate_scan(c->gtstart, ntiles, c->gscan, c->st, &c->launches));
     int32_t* h = reinterpret_cast<int32_t*>(c->h_meta + 3 * c->world + 40);
     CU(cudaMemcpyAsync(h, c->gtstart + ntiles, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
-    CU(cudaStreamSynchronize(c->st));
+    CU(cudaEventRecord(c->ev_plan, c->st));
+    // the candidate fill runs while the host waits for the total (bounded by the workspace;
+    // unused if the update then runs dense)
+    KL(gate_tiles(1, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->gzz, nullptr,
+                  c->gtstart, c->gcbuf, c->gcand, c->st, c->L.g_ecap));
+    CU(cudaEventSynchronize(c->ev_plan));
     tot = *h;
   }
   c->g_entries = tot;
@@ -1264,10 +1272,7 @@ phd_status phd_update(phd_ctx* c, const float* z, int32_t M) {
   pa.js = nullptr;
   if (M > 0 && gated) {
     // candidate lists, entries grouped by label, then the two gated passes
-    const int ntiles = (int)c->g_tiles;
-    if (ntiles > 0)
-      KL(gate_tiles(1, c->model, c->gso, ntiles, c->na0, c->na1, c->ggrid, c->gzstart, c->gzitems, c->gzz, nullptr,
-                    c->gtstart, c->gcbuf, c->gcand, c->st));
+    const int ntiles = (int)c->g_tiles;  // (the candidate fill ran in gate_plan)
     CU(gate_sort_entries(c->gcand, c->g_entries, M, c->gk, c->gv, c->gmlist, c->ghist, c->gscan, c->gmstart, c->st,
                          &c->launches));
     GateArgs ga{};

@@ -530,7 +530,7 @@ constexpr int kGateKBufH = 1024;
 cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1,
                        const GateGrid& grid, const int32_t* zcell_start, const int32_t* zcell_items,
                        const float2* zcell_z, int32_t* tcount, const int32_t* tstart, int32_t* cbuf, int32_t* cand,
-                       cudaStream_t s);
+                       cudaStream_t s, int64_t ecap = 0);  // fill: entries [0, ecap) of cand are written
 // exclusive scan of n int32 (in place); out[n] = total.  tmp >= ceil(n / 4096) + 1 ints.
 cudaError_t gate_scan(int32_t* a, int64_t n, int32_t* tmp, cudaStream_t s, int64_t* launches);
 // stable sort of the E candidate entries by label: mlist = entry indices grouped by
