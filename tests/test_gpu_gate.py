@@ -171,6 +171,31 @@ def test_gated_tile_overflow(phd, orc):
     _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
 
 
+def test_gated_workspace_overflow_runs_dense(phd, orc):
+    """More candidate entries than the workspace holds (every tile of a 400 k particle
+    cloud in an 80 m square sees all 3000 measurements: 1.2 M entries against 2^20): the
+    candidate fill, launched before the host reads the total, writes only what fits, and
+    the update runs dense with the oracle's results (sampled: C of a few measurements over all particles,
+    weights of a particle sample, the mass identity)."""
+    m = replace(POS, gate=2, max_meas=4096, capacity=1 << 19)
+    rng = np.random.default_rng(29)
+    z = rng.uniform(-40.0, 40.0, (3000, 2)).astype(np.float32)
+    soa, w = _cloud(m, 400000, z, 29)
+    soa[0] = np.clip(soa[0], -40.0, 40.0)
+    soa[2] = np.clip(soa[2], -40.0, 40.0)
+    g = _run(phd, m, soa, w, z)
+    assert g["gate"]["used"] == 0
+    kap = orc.kappa(m)
+    for p in rng.choice(len(z), 3, replace=False):
+        Co = orc.normalizers(m, soa, w, z[p:p + 1])[0]
+        assert abs(g["C"][p] - Co) <= 1e-5 * Co + 1e-9 * kap
+    idx = rng.choice(soa.shape[1], 48, replace=False)
+    wo, _ = orc.update(m, soa[:, idx], w[idx], z, g["C"])
+    assert np.all(np.abs(g["wn"][idx] - wo) <= 1e-4 * wo + 1e-7 * w[idx])
+    rhs = (1 - m.p_d) * math.fsum(w.astype(np.float64)) + math.fsum(g["C"] / (kap + g["C"]))
+    assert abs(g["summ"]["W"] - rhs) <= 2e-6 * rhs
+
+
 def test_gated_auto_falls_back(phd, orc):
     """gate = 1 runs dense when the candidates are most of N x M (a point cloud) or the
     update is small (< 2^29 pairs, as here)."""
