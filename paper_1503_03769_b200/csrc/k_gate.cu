@@ -399,8 +399,15 @@ __device__ __forceinline__ void st_v8(float4* dst, float4 a, float4 b) {
                : "memory");
 }
 
-template <int MODEL>
-__global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int32_t* __restrict__ keys, int64_t n,
+// ps_warps(MODEL) warps per CTA, their 16-bit sub-histograms (8 KB each) + 16 KB of bases in
+// shared memory.  Position: 16 (one CTA per SM, 144 KB; cfg 5 ranking 345 -> 325 us, gated
+// step 2.03 -> 2.00 ms); range-bearing keeps 8 (cfg 4 +1 % with 16); 12 and 24 were slower.
+#ifndef PHD_PSORT_WARPS
+#define PHD_PSORT_WARPS 16
+#endif
+__host__ __device__ constexpr int ps_warps(int model) { return model == kRangeBearing ? 8 : PHD_PSORT_WARPS; }
+template <int MODEL, int kPsWarps = ps_warps(MODEL)>
+__global__ void __launch_bounds__(kPsWarps * 32) k_psort_scatter(GatherSrc src, const int32_t* __restrict__ keys, int64_t n,
                                                        int64_t per_blk, int nblk, const int32_t* __restrict__ hs,
                                                        float wscale, GateSorted so, double* blk_wp) {
   pdl_wait();
@@ -410,14 +417,14 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   constexpr int nw = kGateBins / 2;
   extern __shared__ uint32_t sm[];
   uint32_t* wh = sm;
-  int* base = reinterpret_cast<int*>(sm + kMsWarps * nw);
+  int* base = reinterpret_cast<int*>(sm + kPsWarps * nw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = tid; j < kMsWarps * nw; j += blockDim.x) wh[j] = 0u;
+  for (int j = tid; j < kPsWarps * nw; j += blockDim.x) wh[j] = 0u;
   __syncthreads();
   const int64_t i0 = (int64_t)blockIdx.x * per_blk;
   const int64_t i1 = min(n, i0 + per_blk);
-  const int64_t pw = per_blk / kMsWarps;
-  const int64_t w0 = min(i1, i0 + warp * pw), w1 = min(i1, w0 + pw);
+  const int64_t pw = per_blk / kPsWarps;  // the last warp also takes the remainder
+  const int64_t w0 = min(i1, i0 + warp * pw), w1 = warp == kPsWarps - 1 ? i1 : min(i1, w0 + pw);
   uint32_t* my = wh + warp * nw;
   // 1. per-warp sub-histograms
   for (int64_t b0 = w0; b0 < w1; b0 += 32 * kMsRows) {
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   for (int j = tid; j < nw; j += blockDim.x) {
     uint32_t run = 0u;
 #pragma unroll
-    for (int w = 0; w < kMsWarps; ++w) {
+    for (int w = 0; w < kPsWarps; ++w) {
       const uint32_t c = wh[w * nw + j];
       wh[w * nw + j] = run;
       run += c;
@@ -498,12 +505,12 @@ __global__ void __launch_bounds__(256) k_psort_scatter(GatherSrc src, const int3
   if (blk_wp != nullptr) {  // fixed order: lanes' sums by xor tree, the warps in order
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-    __shared__ double wpart[kMsWarps];
+    __shared__ double wpart[kPsWarps];
     if (lane == 0) wpart[warp] = wsum;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int k = 0; k < kMsWarps; ++k) t += wpart[k];
+      for (int k = 0; k < kPsWarps; ++k) t += wpart[k];
       blk_wp[blockIdx.x] = t;
     }
   }
@@ -1108,18 +1115,22 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
   const int64_t per_blk = sort_block(n);
   const int nblk = (int)((n + per_blk - 1) / per_blk);
   *nblk_out = nblk;
-  const size_t smem = sizeof(uint32_t) * (size_t)kMsWarps * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins;
-  ensure_max_smem(k_psort_scatter<kRangeBearing>, smem);
-  ensure_max_smem(k_psort_scatter<kPosIso>, smem);
+  const int psw = ps_warps(rbm ? kRangeBearing : kPosIso);
+  const size_t smem = sizeof(uint32_t) * (size_t)psw * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins;
+  ensure_max_smem(k_psort_scatter<kRangeBearing>,
+                  sizeof(uint32_t) * (size_t)ps_warps(kRangeBearing) * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins);
+  ensure_max_smem(k_psort_scatter<kPosIso>,
+                  sizeof(uint32_t) * (size_t)ps_warps(kPosIso) * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins);
   pdl_launch(k_ms_hist<KeyCell>, nblk, 256, 0, s, kf, n, per_blk, kGateBins, nblk, hist, keys);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
   if (rbm)
-    pdl_launch(k_psort_scatter<kRangeBearing>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so,
-               blk_wp);
+    pdl_launch(k_psort_scatter<kRangeBearing>, nblk, psw * 32, smem, s, src, keys, n, per_blk, nblk, hist, wscale,
+               so, blk_wp);
   else
-    pdl_launch(k_psort_scatter<kPosIso>, nblk, 256, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so, blk_wp);
+    pdl_launch(k_psort_scatter<kPosIso>, nblk, psw * 32, smem, s, src, keys, n, per_blk, nblk, hist, wscale, so,
+               blk_wp);
   ++*launches;
   return cudaGetLastError();
 }
