@@ -31,6 +31,8 @@
 //   6. k_gpass<2>: weights (sum_z u d_z per particle, complete inside the CTA)
 //      and the centred STPHD state sums for candidates in the index set I.
 #include "phd_internal.h"
+
+#include <type_traits>
 #include "pair_math.cuh"
 
 #include <algorithm>
@@ -901,10 +903,17 @@ __global__ void __launch_bounds__(TP / (2 * NPAIR),
     __syncthreads();
 
     if (PASS == 1) {
-      for (int k8 = 0; k8 < cl8; k8 += 8) {
+      // groups of 8 candidates per transposed reduction; the last, partial group skips the
+      // padding candidates' terms (exactly 0) instead of evaluating them (CTA-uniform branch)
+      auto group8 = [&](int k8, auto tail_tag) {
+        constexpr bool TAIL = decltype(tail_tag)::value;
         float v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
+          if (TAIL && k8 + j >= cl) {
+            v[j] = 0.0f;
+            continue;
+          }
           float2 d0, d1;
           float2 u = __fadd2_rn(term(k8 + j, 0, d0, d1), term(k8 + j, 1, d0, d1));
           if (NPAIR == 4) u = __fadd2_rn(u, __fadd2_rn(term(k8 + j, 2, d0, d1), term(k8 + j, 3, d0, d1)));
@@ -915,7 +924,10 @@ __global__ void __launch_bounds__(TP / (2 * NPAIR),
           PHD_DCHECK(k8 + (lane >> 2) < kGateChunk);
           wpart[warp][k8 + (lane >> 2)] = r;
         }
-      }
+      };
+      const int cfull = cl & ~7;
+      for (int k8 = 0; k8 < cfull; k8 += 8) group8(k8, std::false_type{});
+      if (cfull < cl) group8(cfull, std::true_type{});
       __syncthreads();
       for (int k = tid; k < cl; k += THREADS) {
         double sum = 0.0;
@@ -925,13 +937,17 @@ __global__ void __launch_bounds__(TP / (2 * NPAIR),
         g.part1[e0 + cb + k] = sum;
       }
     } else {
-      // selected candidates, two at a time: weights + the four centred state sums
-      for (int k = 0; k < nsel; k += 2) {
+      // selected candidates, two at a time: weights + the four centred state sums; an odd
+      // count's last pair skips its sentinel's terms (exactly 0) instead of evaluating them
+      auto pair2 = [&](int k, auto tail_tag) {
+        constexpr bool TAIL = decltype(tail_tag)::value;
         float v[8];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int kk = k + hh;
-          {
+          if (TAIL && hh == 1) {
+            v[4] = v[5] = v[6] = v[7] = 0.0f;
+          } else {
             float2 a0 = f2(0.0f, 0.0f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
             for (int h = 0; h < NPAIR; ++h) {
@@ -966,7 +982,10 @@ __global__ void __launch_bounds__(TP / (2 * NPAIR),
           PHD_DCHECK(k + (q >> 2) < kGateChunk + 2);
           reinterpret_cast<float*>(&wq[warp][k + (q >> 2)])[q & 3] = r;
         }
-      }
+      };
+      const int npf = base_sel_unpadded & ~1;  // full pairs of selected candidates
+      for (int k = 0; k < npf; k += 2) pair2(k, std::false_type{});
+      if (nsel > npf) pair2(npf, std::true_type{});
       // the rest: weights only
       const int kend = cl + (nsel - base_sel_unpadded);
 #pragma unroll 2
