@@ -47,6 +47,9 @@ def test_gated_update_parity(phd, orc, mname, n, M):
     soa, w = _cloud(m, n, z, n + M)
     g = _run(phd, m, soa, w, z)
     assert g["gate"]["used"] == 1
+    # tiles of gate_tp particles: 1024 for the position sensors, 512 for range-bearing
+    tp = 512 if m.meas == RANGE_BEARING else 1024
+    assert g["gate"]["tiles"] == -(-n // tp) and g["gate"]["pairs"] == g["gate"]["entries"] * tp
     Co = orc.normalizers(m, soa, w, z)
     wo, acco = orc.update(m, soa, w, z, Co)
     _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
