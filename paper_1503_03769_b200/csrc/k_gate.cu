@@ -1227,6 +1227,9 @@ cudaError_t gate_sort_entries(const int32_t* cand, int64_t E, int M, int32_t* kb
   return csort_pass(kbuf, vbuf, E, 12, 1 << (bits - 12), hist, scan_tmp, nullptr, mlist, s, launches);
 }
 
+#ifndef PHD_GATE_NPAIR1_POS
+#define PHD_GATE_NPAIR1_POS 2
+#endif
 #ifndef PHD_GATE_NPAIR_POS
 #define PHD_GATE_NPAIR_POS 4
 #endif
@@ -1237,8 +1240,9 @@ static cudaError_t gpass_m(int pass, const GateArgs& g, cudaStream_t s) {
   // (measured at cfg 5: pass 2 0.73 -> 0.64 ms with 8 particles per thread, pass 1
   // 0.42 -> 0.44 ms, so pass 1 keeps 4)
   constexpr int NP2 = MODEL == kRangeBearing ? 2 : PHD_GATE_NPAIR_POS;
+  constexpr int NP1 = MODEL == kRangeBearing ? 2 : PHD_GATE_NPAIR1_POS;
   if (pass == 1)
-    pdl_launch(k_gpass<MODEL, 1, 2>, g.ntiles, gate_tp(MODEL) / 4, 0, s, g);
+    pdl_launch(k_gpass<MODEL, 1, NP1>, g.ntiles, gate_tp(MODEL) / (2 * NP1), 0, s, g);
   else
     pdl_launch(k_gpass<MODEL, 2, NP2>, g.ntiles, gate_tp(MODEL) / (2 * NP2), 0, s, g);
   return cudaGetLastError();
@@ -1273,7 +1277,7 @@ void preload_gate() {
                 k_ms_scatter<KeyArr>, k_ms_scatter<KeyZ>, k_psort_pad, k_psort_scatter<kPosIso>,
                 k_psort_scatter<kRangeBearing>, k_gate_count, k_gate_fill, k_gate_count_labels, k_mstart_from_hist,
                 k_zero_i32, k_gate_reduce<1>, k_gate_reduce<2>, k_zbin_finish);
-  touch_kernels(k_gpass<kPosIso, 1, 2>, k_gpass<kPosIso, 2, PHD_GATE_NPAIR_POS>, k_gpass<kPosAniso, 1, 2>,
+  touch_kernels(k_gpass<kPosIso, 1, PHD_GATE_NPAIR1_POS>, k_gpass<kPosIso, 2, PHD_GATE_NPAIR_POS>, k_gpass<kPosAniso, 1, PHD_GATE_NPAIR1_POS>,
                 k_gpass<kPosAniso, 2, PHD_GATE_NPAIR_POS>, k_gpass<kRangeBearing, 1, 2>, k_gpass<kRangeBearing, 2, 2>);
 }
 
