@@ -1,6 +1,7 @@
 """Dense update throughput against the particle count on one GPU (cfg 5's model and
 measurement sets, N = 2^18 .. 2^27, M = 4096): step ms and update pairs/s, back-to-back
-steps, CUDA events on the filter stream.  usage: python tools/dbg/n_sweep.py > out.json"""
+steps, CUDA events on the filter stream.  GATE=1: the gated update (pairs/s is then the
+"effective" N*M per second).  usage: [GATE=1] python tools/dbg/n_sweep.py > out.json"""
 import os, sys, json
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import torch
@@ -14,7 +15,7 @@ torch.cuda.set_stream(stream)
 rows = []
 for lg in range(18, 28):
     N = 1 << lg
-    m = replace(base.model, fixed_count=N - J, capacity=N)
+    m = replace(base.model, fixed_count=N - J, capacity=N, gate=int(os.environ.get("GATE", "0")))
     cfg = replace(base, model=m, scenario=replace(base.scenario, steps=8))
     truth = scenario.simulate_truth(cfg)
     Z = scenario.measurements(cfg, truth)
@@ -36,4 +37,5 @@ for lg in range(18, 28):
     rows.append({"N": N, "M": len(Z[0]), "step_ms": ms, "pairs_per_s": pairs / 4 / (ms * 1e-3)})
     f.close()
     print(json.dumps(rows[-1]), file=sys.stderr)
-print(json.dumps({"what": "dense step, cfg 5 model, N = 2^18..2^27, back to back, 1 GPU", "rows": rows}, indent=1))
+what = "gated (gate = 1) step" if os.environ.get("GATE", "0") != "0" else "dense step"
+print(json.dumps({"what": what + ", cfg 5 model, N = 2^18..2^27, back to back, 1 GPU", "rows": rows}, indent=1))
