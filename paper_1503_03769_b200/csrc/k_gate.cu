@@ -522,9 +522,8 @@ __global__ void __launch_bounds__(kPsWarps * 32) k_psort_scatter(GatherSrc src, 
 // per tile (one warp): bounding box in measurement space, max log2(p_D c w),
 // then the candidates: cells of the window in rounds of 32 (lane = cell),
 // measurements of a cell in item order, written in (round, lane, item) order
-// -- deterministic.  The count pass also keeps the first kGateKBuf candidates
+// -- deterministic.  The count pass also keeps the first kbuf (gate_kbuf) candidates
 // of every tile, so the fill pass copies them instead of enumerating again.
-constexpr int kGateKBuf = kGateKBufH;
 
 // the tile kernels' view of the sorted records: c0, c1 (measurement-space
 // coordinates) and lw of record p at [p * stride]
@@ -673,7 +672,7 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
   return total;
 }
 
-// count pass: tcount[t] and the first kGateKBuf candidates in cbuf[t][.]
+// count pass: tcount[t] and the first kbuf candidates in cbuf[t][.]
 __global__ void __launch_bounds__(256) k_gate_count(const RecView rv, int ntiles, float na0, float na1,
                                                     GateGrid g, const int32_t* __restrict__ zcell_start,
                                                     const int32_t* __restrict__ zcell_items,
@@ -682,12 +681,12 @@ __global__ void __launch_bounds__(256) k_gate_count(const RecView rv, int ntiles
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
   const int total = tile_enum(t, rv, na0, na1, g, zcell_start, zcell_items, zcell_z,
-                              cbuf + (int64_t)t * kGateKBuf, kGateKBuf);
+                              cbuf + (int64_t)t * g.kbuf, g.kbuf);
   if ((threadIdx.x & 31) == 0) tcount[t] = total;
 }
 
 // fill pass: copy the buffered candidates to cand[tstart[t]..]; tiles with more
-// than kGateKBuf candidates enumerate again
+// than kbuf candidates enumerate again
 __global__ void __launch_bounds__(256) k_gate_fill(const RecView rv, int ntiles, float na0, float na1,
                                                    GateGrid g, const int32_t* __restrict__ zcell_start,
                                                    const int32_t* __restrict__ zcell_items,
@@ -702,8 +701,8 @@ __global__ void __launch_bounds__(256) k_gate_fill(const RecView rv, int ntiles,
   // ecap are not written (the update then runs dense and ignores cand)
   const int64_t room = ecap - (int64_t)e0;
   const int Kw = room <= 0 ? 0 : (room < (int64_t)K ? (int)room : K);
-  if (K <= kGateKBuf) {
-    for (int j = lane; j < Kw; j += 32) cand[e0 + j] = cbuf[(int64_t)t * kGateKBuf + j];
+  if (K <= g.kbuf) {
+    for (int j = lane; j < Kw; j += 32) cand[e0 + j] = cbuf[(int64_t)t * g.kbuf + j];
   } else if (Kw > 0) {
     tile_enum(t, rv, na0, na1, g, zcell_start, zcell_items, zcell_z, cand + e0, Kw);
   }

@@ -145,7 +145,7 @@ Layout make_layout(const phd_params* p, int world, int sms) {
   L.o_gzstart = gtake(sizeof(int32_t) * (kGateBins + 1));
   L.o_gzitems = gtake(sizeof(int32_t) * ((size_t)p->max_meas + 1));
   L.o_gzz = gtake(sizeof(float) * 2 * ((size_t)p->max_meas + 1));
-  L.o_gcbuf = gtake(sizeof(int32_t) * (size_t)L.g_ntiles * kGateKBufH);
+  L.o_gcbuf = gtake(sizeof(int32_t) * (size_t)L.g_ntiles * gate_kbuf(p->max_meas));
   L.o_gA = gtake(sizeof(double) * 4 * (size_t)L.slots_max);
   L.o_glwmax = gtake(sizeof(int) * 4);
   L.total = off;
@@ -608,6 +608,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
       c->ggrid.inv_h1 = (float)(kGateG / (2.0 * kPi));
       c->ggrid.wrap1 = 1;
       c->ggrid.floor = p->gate_floor != 0 ? (float)p->gate_floor : kGateLog2Min;
+      c->ggrid.kbuf = gate_kbuf(p->max_meas);
     } else {
       c->ggrid.lo0 = (float)p->region[0];
       c->ggrid.inv_h0 = (float)(kGateG / (p->region[1] - p->region[0]));
@@ -615,6 +616,7 @@ static phd_status create_impl(const phd_params* p, int32_t rank, int32_t world, 
       c->ggrid.inv_h1 = (float)(kGateG / (p->region[3] - p->region[2]));
       c->ggrid.wrap1 = 0;
       c->ggrid.floor = p->gate_floor != 0 ? (float)p->gate_floor : kGateLog2Min;
+      c->ggrid.kbuf = gate_kbuf(p->max_meas);
     }
   }
   CUB(cudaMallocHost(&c->h_meta, sizeof(double) * (48 + 4 * world)));

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <utility>
+#include <algorithm>
 #include <stdint.h>
 
 namespace phd {
@@ -481,6 +482,7 @@ struct GateGrid {
   float inv_h0, inv_h1;               // cells per unit
   int wrap1;                          // axis 1 is an angle (range-bearing): cells wrap mod kGateG
   float floor;                        // log2 of the skipped terms' bound: kGateLog2Min (exact) or gate_floor
+  int kbuf;                           // candidates the count pass buffers per tile (gate_kbuf)
 };
 
 // Sorted copy of the particle block (n_pad = ntiles * gate_tp records of n4 float4):
@@ -525,8 +527,11 @@ cudaError_t gate_sort_particles(int model, const float* const* A /*x,vx,y,vy,w*/
 cudaError_t gate_zbin(const float* z, int M, const GateGrid& grid, int32_t* hist, int32_t* scan_tmp,
                       int32_t* zcell_start, int32_t* zcell_items, float2* zcell_z, cudaStream_t s, int64_t* launches);
 // per-tile bounding boxes + candidate counts (fill = 0) or labels (fill = 1)
-// (fill = 0 also buffers the first kGateKBuf candidates per tile in cbuf [ntiles][kGateKBuf])
-constexpr int kGateKBufH = 1024;
+// (fill = 0 also buffers the first kbuf candidates per tile in cbuf [ntiles][kbuf]).  kbuf covers
+// max_meas (a tile has at most M candidates) up to 4096, so the fill pass is a copy and never
+// enumerates a window again (the long windows of tiles spanning a Morton jump set its duration)
+constexpr int kGateKBufMax = 4096;
+inline int gate_kbuf(int max_meas) { return std::min(kGateKBufMax, std::max(32, (max_meas + 31) & ~31)); }
 cudaError_t gate_tiles(int fill, int model, const GateSorted& so, int ntiles, float na0, float na1,
                        const GateGrid& grid, const int32_t* zcell_start, const int32_t* zcell_items,
                        const float2* zcell_z, int32_t* tcount, const int32_t* tstart, int32_t* cbuf, int32_t* cand,

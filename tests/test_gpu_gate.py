@@ -158,17 +158,18 @@ def test_gated_many_measurements(phd, orc, mname):
 
 
 def test_gated_tile_overflow(phd, orc):
-    """Tiles with more candidates than the count pass buffers (1024): the fill pass
-    enumerates their windows again; crowded cells (> 4 measurements) take the long
-    per-cell loop.  3000 measurements and the particles inside a 250 m square."""
-    m = replace(POS, gate=2, max_meas=4096)
+    """Tiles with more candidates than the count pass buffers (gate_kbuf: max_meas up to
+    4096): the fill pass enumerates their windows again; crowded cells (> 4 measurements)
+    take the long per-cell loop.  5000 measurements (max_meas 8192) and the particles inside
+    an 80 m square, so every tile has all 5000 candidates."""
+    m = replace(POS, gate=2, max_meas=8192)
     rng = np.random.default_rng(23)
-    z = rng.uniform(-125.0, 125.0, (3000, 2)).astype(np.float32)
+    z = rng.uniform(-40.0, 40.0, (5000, 2)).astype(np.float32)
     soa, w = _cloud(m, 6000, z, 23)
-    soa[0] = np.clip(soa[0], -125.0, 125.0)
-    soa[2] = np.clip(soa[2], -125.0, 125.0)
+    soa[0] = np.clip(soa[0], -40.0, 40.0)
+    soa[2] = np.clip(soa[2], -40.0, 40.0)
     g = _run(phd, m, soa, w, z)
-    assert g["gate"]["used"] == 1 and g["gate"]["entries"] > 1024 * g["gate"]["tiles"] // 2
+    assert g["gate"]["used"] == 1 and g["gate"]["entries"] == 5000 * g["gate"]["tiles"]
     Co = orc.normalizers(m, soa, w, z)
     wo, acco = orc.update(m, soa, w, z, Co)
     _check_update(orc, m, g["C"], g["acc"], g["wn"], w, Co, wo, acco)
