@@ -538,6 +538,13 @@ struct RecView {
 };
 
 
+// window enumeration switches to a scan of all M binned measurements when the window has more
+// than M / kGateDirectRatio cells (0 = never, A/B builds)
+#ifndef PHD_GATE_DIRECT
+#define PHD_GATE_DIRECT 1
+#endif
+constexpr int kGateDirectRatio = 8;
+
 __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, float na1, const GateGrid& g,
                                          const int32_t* __restrict__ zcell_start, const int32_t* __restrict__ zcell_items,
                                          const float2* __restrict__ zcell_z, int32_t* dst, int cap) {
@@ -628,6 +635,30 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
     const float dy = g.wrap1 ? dist_arc(zz.y, e0, e1) : dist_iv(zz.y, e0, e1);
     return fmaf(na0, dx * dx, fmaf(na1, dy * dy, lm)) >= g.floor;
   };
+  // long windows (tiles spanning a Morton jump cover a large part of the grid): scan every
+  // binned measurement in cell order instead, four rounds of 32 with their loads in flight
+  // (no dependent cell-range loads); the same test, so the same candidate set
+  const int Mz = __ldg(zcell_start + kGateBins);
+  if (PHD_GATE_DIRECT && nc * kGateDirectRatio > Mz) {
+    for (int r0 = 0; r0 < Mz; r0 += 128) {
+      float2 zz[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = r0 + 32 * u + lane;
+        zz[u] = j < Mz ? zcell_z[j] : make_float2(INFINITY, INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = r0 + 32 * u + lane;
+        const bool ok = j < Mz && passes(zz[u]);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        const int w = total + __popc(bal & ((1u << lane) - 1u));
+        if (ok && dst != nullptr && w < cap) dst[w] = zcell_items[j];
+        total += __popc(bal);
+      }
+    }
+    return total;
+  }
   constexpr int kStash = 4;
   int j0n, j1n;
   cell_range(lane, j0n, j1n);
