@@ -15,3 +15,4 @@ GATE=1 NPROF=2 python tools/dbg/timeline.py cfg5 > gpurun_out/tl_gate_cfg5.txt 2
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_gpass|k_psort_scatter" --launch-skip 6 -c 3 -f -o gpurun_out/gpass_full python bench.py --gate 1 --no-gated-leg --no-cpu-baseline --steps 1 --warmup 3 > gpurun_out/ncu_gpass.log 2>&1; echo ncu_gpass=$?
 python tools/ncu_summary.py full gpurun_out/gpass_full.ncu-rep gpurun_out/sum_gpass.json "ncu --set full --clock-control none, bench.py --gate 1 (cfg5) --steps 1 --warmup 3: k_psort_scatter, k_gpass 1 and 2" > /dev/null
 rm -f gpurun_out/*.ncu-rep
+GATE=1 python tools/dbg/n_sweep.py > gpurun_out/n_sweep_gated.json 2> gpurun_out/n_sweep_gated.err; echo nsweep=$?
