@@ -11,6 +11,9 @@ from torch.profiler import profile, ProfilerActivity
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 cfg = scenario.get(name)
 cfg = replace(cfg, scenario=replace(cfg.scenario, steps=40))
+if os.environ.get("NPART"):  # NPART=n: the config's model at n particles (capacity n + births)
+    n_ = int(os.environ["NPART"])
+    cfg = scenario.scaled(cfg, n_out=n_ - cfg.model.births_per_step, capacity=n_)
 if os.environ.get("GATE"):  # GATE=1: the gated update
     cfg = replace(cfg, model=replace(cfg.model, gate=int(os.environ["GATE"])))
 NPROF = int(os.environ.get("NPROF", "4"))
