@@ -543,7 +543,10 @@ struct RecView {
 #ifndef PHD_GATE_DIRECT
 #define PHD_GATE_DIRECT 1
 #endif
-constexpr int kGateDirectRatio = 8;
+#ifndef PHD_GATE_DIRECT_RATIO
+#define PHD_GATE_DIRECT_RATIO 8
+#endif
+constexpr int kGateDirectRatio = PHD_GATE_DIRECT_RATIO;
 
 __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, float na1, const GateGrid& g,
                                          const int32_t* __restrict__ zcell_start, const int32_t* __restrict__ zcell_items,
