@@ -256,7 +256,7 @@ struct KeyZ {  // measurement l = (z[2l], z[2l+1]) -> its cell
 };
 
 template <class KF>
-__global__ void __launch_bounds__(256) k_ms_hist(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk, int32_t* hist,
+__global__ void __launch_bounds__(1024) k_ms_hist(KF kf, int64_t n, int64_t per_blk, int nbins, int nblk, int32_t* hist,
                                                  int32_t* keys_out = nullptr) {
   pdl_wait();
   __shared__ int h[kSortMaxBins];
@@ -1173,7 +1173,11 @@ cudaError_t gate_sort_particles(int model, const float* const* A, const float* r
                   sizeof(uint32_t) * (size_t)ps_warps(kRangeBearing) * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins);
   ensure_max_smem(k_psort_scatter<kPosIso>,
                   sizeof(uint32_t) * (size_t)ps_warps(kPosIso) * (kGateBins / 2) + sizeof(int) * (size_t)kGateBins);
-  pdl_launch(k_ms_hist<KeyCell>, nblk, 256, 0, s, kf, n, per_blk, kGateBins, nblk, hist, keys);
+#ifndef PHD_CELL_HIST_THREADS
+#define PHD_CELL_HIST_THREADS 1024
+#endif
+  // 1024 threads per 64 K-particle block: the cell histogram is latency-bound on its loads
+  pdl_launch(k_ms_hist<KeyCell>, nblk, PHD_CELL_HIST_THREADS, 0, s, kf, n, per_blk, kGateBins, nblk, hist, keys);
   ++*launches;
   cudaError_t e = gate_scan(hist, (int64_t)kGateBins * nblk, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
