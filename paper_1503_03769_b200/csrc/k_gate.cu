@@ -543,6 +543,10 @@ struct RecView {
 #ifndef PHD_GATE_DIRECT
 #define PHD_GATE_DIRECT 1
 #endif
+#ifndef PHD_BOX_UNROLL
+#define PHD_BOX_UNROLL 8
+#endif
+constexpr int kBoxUnroll = PHD_BOX_UNROLL;
 #ifndef PHD_GATE_DIRECT_RATIO
 #define PHD_GATE_DIRECT_RATIO 8
 #endif
@@ -574,7 +578,8 @@ __device__ __forceinline__ int tile_enum(int t, const RecView& rv, float na0, fl
       lm = ord2f(__ldg(rv.lw_max));
     }
   }
-  for (int j = lane; j < (fast ? 0 : tp); j += 32) {
+#pragma unroll kBoxUnroll
+  for (int j = lane; j < (fast ? 0 : tp); j += 32) {  // (the box loads of several rows in flight)
     const int64_t o = (p0 + j) * rv.stride;
     const float l = __ldg(rv.lw + o);
     const float v0 = __ldg(rv.c0 + o), v1 = __ldg(rv.c1 + o);
